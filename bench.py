@@ -1,0 +1,331 @@
+#!/usr/bin/env python
+"""bench.py: exact 1-NN queries/sec of the iSAX path on BASELINE.json's workloads.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 3] [--impl isax|reference]
+
+What one step is: one batch of Q queries answered end to end by
+the query path a6-a10 (query PAA/SAX/LUT, window BSF, full LB scan plus compaction, refine,
+finalise) on an index built before the timed region. The build (a1-a5) is timed on its own
+and reported under "build". At N=1 the workload is config 3 (100M x 256, the metric's
+config). `value` is queries/s over all ranks. For N>1 every rank holds a replica of the
+index and answers its own query batch, with no data-path collective (weak scaling;
+DESIGN.md "Multi-GPU").
+
+Extra keys: roofline (the dominant kernel, lbscan, timed live with CUDA events on its
+stream), cpu_baseline (the oracle on this host's cores, on a bounded sample), e2e (the same
+metric through isax_nn1 with host buffers, copies included), gpu_launches and clocks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "exact 1-NN queries/sec on 100M×256 fp32 series; scan/refine HBM GB/s vs peak"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=3, help="BASELINE.json config 1..5 (3 = the metric's)")
+    ap.add_argument("--impl", default="isax", choices=["isax", "reference"])
+    ap.add_argument("--queries", type=int, default=0, help="override Q per step")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="budget of the oracle cpu_baseline sample")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--stats-out", default="")
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------------------------ clocks
+REASONS = ["gpu_idle", "applications_clocks_setting", "sw_power_cap", "hw_slowdown", "sync_boost",
+           "sw_thermal_slowdown", "hw_thermal_slowdown", "hw_power_brake_slowdown"]
+
+
+class ClockSampler:
+    """nvidia-smi sampling of SM clock and throttle reasons during the timed region."""
+
+    def __init__(self, dev: int):
+        self.dev = dev
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        q = "clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active"
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.dev), f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                                          "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, mx, reasons = [], [], set()
+        for r in self.rows:
+            p = [x.strip() for x in r.split(",")]
+            if len(p) < 4:
+                continue
+            try:
+                sm.append(float(p[0]))
+                mx.append(float(p[1]))
+                mask = int(p[3], 16)
+            except ValueError:
+                continue
+            for b, name in enumerate(REASONS):
+                if mask & (1 << b) and name != "gpu_idle":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+# ------------------------------------------------------------------------------------ oracle
+def cpu_baseline(wl, q_dev, budget_s: float, rank: int):
+    """The oracle (C7 brute force, oracle/oracle.c, OpenMP on all host cores) on a bounded sample.
+
+    Sample: the first S dataset series (streamed from the device generator in 1M-series chunks,
+    copied to host; copies excluded from the timing) against the first 4 queries. S grows
+    chunk by chunk until the oracle has spent ~budget_s seconds. queries/s for the whole
+    workload = 4 / (t * N / S).
+    """
+    import torch
+
+    import datagen
+    from oracle import clib
+
+    qh = q_dev[:4].cpu().numpy()
+    qy, _, _, _, _ = clib.summarise(qh, want_paa=False)
+    sc = clib.NN1Scan(qy, K=32)
+    chunk = 1 << 20
+    buf = torch.empty((chunk, wl.n), dtype=torch.float32, device="cuda")
+    host = torch.empty((chunk, wl.n), dtype=torch.float32, pin_memory=True)
+    t_or, S = 0.0, 0
+    while S < wl.N and t_or < budget_s:
+        c = min(chunk, wl.N - S)
+        datagen.series(wl, S, c, out=buf[:c])
+        host[:c].copy_(buf[:c])
+        t0 = time.perf_counter()
+        sc.feed(S, host[:c].numpy())
+        t_or += time.perf_counter() - t0
+        S += c
+    qps = 4.0 / (t_or * wl.N / S)
+    return {"value": qps, "unit": "queries/s", "cores": clib.num_threads(), "kind": "oracle",
+            "sample": f"brute-force exact 1-NN (oracle C7) of 4 queries over the first {S} of {wl.N} series "
+                      f"({t_or:.2f} s); scaled to the full collection"}
+
+
+# ------------------------------------------------------------------------------------ main
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    import torch
+
+    import datagen
+
+    wl = datagen.WORKLOADS[args.config]
+    if args.impl == "reference":
+        return run_reference(args, wl, world, rank, local)
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2009_01614_b200 import isax
+
+    Q = args.queries or wl.Q
+    if world > 1:  # every rank answers its own queries (different seed)
+        import dataclasses
+
+        wlq = dataclasses.replace(wl, q_seed=wl.q_seed + 7919 * rank)
+    else:
+        wlq = wl
+    # ---- build (a1-a5), timed on its own
+    free, _ = torch.cuda.mem_get_info()
+    raw_bytes = wl.N * wl.n * 4
+    t0 = time.perf_counter()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if 2 * raw_bytes + (8 << 30) < free:
+        x = datagen.series(wl, 0, wl.N)
+        torch.cuda.synchronize()
+        ev0.record()
+        ix = isax.Index.build(x)
+        ev1.record()
+        torch.cuda.synchronize()
+        build_mode = "device-resident input"
+        del x
+        torch.cuda.empty_cache()
+    else:
+        fptr, ctx = datagen.fill_callback(wl)
+        ev0.record()
+        ix = isax.Index.build_stream(wl.N, wl.n, fptr, ctx)
+        ev1.record()
+        torch.cuda.synchronize()
+        build_mode = "streamed input (generator fill callback, 2 passes; generation time included)"
+    build_s = ev0.elapsed_time(ev1) / 1e3
+    q, src = datagen.queries(wlq, Q)
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    # ---- warmup
+    for _ in range(max(args.warmup, 0)):
+        ids, dist_ = ix.nn1(q)
+    torch.cuda.synchronize()
+    # ---- timed: K steps on the device
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clk = ClockSampler(local)
+    clk.start()
+    time.sleep(0.3)
+    lb_ms, rf_ms, cand, refined, launches, rounds = [], [], [], [], 0, []
+    e_start, e_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e_start.record(stream)
+    for _ in range(args.steps):
+        ids, dist_ = ix.nn1(q)
+        st = ix.stats()
+        lb_ms.append(st["ms_first_batch"]["lbscan"])
+        rf_ms.append(st["ms_first_batch"]["refine"])
+        cand.append(sum(st["candidates"]))
+        refined.append(sum(st["refined"]))
+        rounds.append(max(st["rounds"]))
+        launches += st.get("launches", 0)
+    e_end.record(stream)
+    torch.cuda.synchronize()
+    clocks = clk.stop()
+    ms = e_start.elapsed_time(e_end)
+    if dist:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        dist.barrier()
+    total_q = Q * args.steps * world
+    value = total_q / (ms / 1e3)
+    # ---- e2e through isax_nn1 with host (pinned) buffers, copies inside the timed region
+    qh = torch.empty((Q, wl.n), dtype=torch.float32, pin_memory=True)
+    qh.copy_(q)
+    oid = torch.empty(Q, dtype=torch.int64, pin_memory=True)
+    odist = torch.empty(Q, dtype=torch.float32, pin_memory=True)
+    ix.nn1_host(qh.numpy(), oid.numpy(), odist.numpy())
+    if dist:
+        dist.barrier()
+    e2e_steps = max(1, min(args.steps, 10))
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        ix.nn1_host(qh.numpy(), oid.numpy(), odist.numpy())
+    e2e_s = time.perf_counter() - t0
+    if dist:
+        t = torch.tensor([e2e_s], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    assert (oid.numpy() == ids.cpu().numpy()).all(), "host and device paths disagree"
+    # ---- roofline: lbscan (dominant kernel), bytes it must read per launch
+    hbm, peak_src = peaks()
+    G = 4
+    groups = math.ceil(min(Q, 128) / G)
+    lb_launch_ms = statistics.mean(lb_ms)
+    cand_mean = statistics.mean(cand)
+    alg_bytes = 16.0 * wl.N * groups + 4.0 * cand_mean
+    achieved = alg_bytes / (lb_launch_ms / 1e3) / 1e9
+    roofline = {"kernel": "lbscan_kernel<4>", "bound": "hbm", "achieved": round(achieved, 1), "peak": hbm,
+                "unit": "GB/s", "frac": round(achieved / hbm, 4), "traffic": None,
+                "peak_source": peak_src,
+                "bytes_per_launch": alg_bytes,
+                "bytes_rule": f"16 B per summary x N x ceil(Q/G) query groups (G={G} queries share one pass) + 4 B per candidate",
+                "launch_ms": round(lb_launch_ms, 4), "refine_ms": round(statistics.mean(rf_ms), 4),
+                "lookups_per_s": 16.0 * wl.N * min(Q, 128) / (lb_launch_ms / 1e3)}
+    out = {
+        "metric": METRIC, "value": round(value, 2), "unit": "queries/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": wl.name, "N": wl.N, "n": wl.n, "w": 16, "card": 256, "queries_per_step": Q,
+                   "queries": f"{min(Q, wl.q_walks)} random walks + {max(0, Q - wl.q_walks)} noisy copies (sigma {wl.sigma})",
+                   "parallelism": f"replicas x{world} (each rank: own query batch)",
+                   "l2": "inputs larger than L2 (SAX array 16N B, stored rows 4nN B)" if wl.N * 16 > 126e6
+                   else "working set fits in L2 (small config)",
+                   "source": wl.cite},
+        "roofline": roofline,
+        "e2e": {"value": round(Q * e2e_steps * world / e2e_s, 2), "unit": "queries/s",
+                "h2d_bytes_per_step": Q * wl.n * 4, "d2h_bytes_per_step": Q * 12,
+                "how": "isax_nn1 on pinned host buffers, wall clock, copies inside"},
+        "gpu_launches": launches,
+        "clocks": clocks,
+        "build": {"seconds": round(build_s, 3), "mode": build_mode, "N": wl.N, "n": wl.n,
+                  "input_GBps": round(raw_bytes / build_s / 1e9, 1), "index_device_bytes": ix.device_bytes},
+        "stats": {"candidates_per_query": cand_mean / Q, "refined_per_query": statistics.mean(refined) / Q,
+                  "rounds_max": max(rounds)},
+    }
+    if rank == 0 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(wl, q, args.cpu_seconds, rank)
+    if args.stats_out and rank == 0:
+        with open(args.stats_out, "w") as f:
+            json.dump(ix.stats(), f)
+    ix.close()
+    if rank == 0:
+        print(json.dumps(out))
+    if dist:
+        dist.destroy_process_group()
+
+
+def run_reference(args, wl, world, rank, local):
+    """--impl reference: the oracle (no reference implementation exists), timed on host cores."""
+    if rank != 0:
+        return
+    import torch
+
+    import datagen
+
+    torch.cuda.set_device(local)
+    q, _ = datagen.queries(wl, args.queries or wl.Q)
+    per_step = max(2.0, 60.0 / max(1, args.steps + args.warmup))
+    for _ in range(args.warmup):
+        cpu_baseline(wl, q, min(per_step, 2.0), rank)
+    vals, last = [], None
+    for _ in range(args.steps):
+        last = cpu_baseline(wl, q, per_step, rank)
+        vals.append(last["value"])
+    v = statistics.mean(vals)
+    out = {"impl": "reference", "metric": METRIC, "value": v, "unit": "queries/s", "n_gpus": world,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * 4 / v, "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": {"workload": wl.name, "N": wl.N, "n": wl.n, "w": 16, "card": 256},
+           "cpu_baseline": {"kind": "oracle", "cores": last["cores"], "sample": last["sample"], "value": v,
+                            "unit": "queries/s"},
+           "e2e": {"value": v, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,127 @@
+/* isax.h: C-ABI of libisax.so, exact 1-NN Euclidean search over iSAX-summarised data series
+ * on one B200 (sm_100a).
+ *
+ * Method: ParIS / ParIS+ / MESSI, "Data Series Indexing Gone Parallel" (arXiv 2009.01614).
+ * Citations: P:n = PAPER.md line n; S:n = SPEC.md line n; R<k> = the reading recorded in
+ * DESIGN.md "Readings".
+ *
+ * Conventions (all entry points)
+ *  - Series are row-major fp32 [count][n]. Sizes are element counts.
+ *  - Pointers may be host (pageable or pinned) or device, unless a function says otherwise.
+ *    The kind is detected with cudaPointerGetAttributes.
+ *  - Inputs are borrowed for the duration of the call only. They are never modified or
+ *    retained.
+ *  - Return: ISAX_OK (0) or a negative ISAX_E_* code. On error, out-parameters are left
+ *    untouched and isax_last_error() returns a thread-local message.
+ *  - One index may be used by one host thread at a time; calls on the same index are
+ *    serialised by an internal mutex. Separate indices are independent.
+ *  - v1 supports w = 16, card = 256, n a multiple of 64 in [64, 1024], N < 2^32 - 1.
+ *    Other valid arguments return ISAX_E_UNSUPPORTED.
+ */
+#ifndef ISAX_H
+#define ISAX_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+    ISAX_OK = 0,
+    ISAX_E_INVAL = -1,       /* bad argument: NULL pointer, n % w != 0, card not a power of 2 */
+    ISAX_E_EMPTY = -2,       /* N == 0: an empty collection has no answer */
+    ISAX_E_UNSUPPORTED = -3, /* valid by the method, outside what v1 implements */
+    ISAX_E_NOMEM = -4,       /* a device or pinned allocation failed */
+    ISAX_E_CUDA = -5,        /* a CUDA runtime error; the message names it */
+    ISAX_E_NONFINITE = -6,   /* NaN or Inf in a series or a query */
+    ISAX_E_CALLBACK = -7     /* a fill callback returned non-zero */
+};
+
+/* Tunables. Pass NULL for the defaults. */
+typedef struct isax_opts {
+    uint32_t window_L;   /* leaf-sized window of the approximate answer (R5). Default 1024. */
+    int32_t slack_log2;  /* prune/abandon slack delta = 2^slack_log2 (R8). Default -12. */
+    uint32_t batch_Q;    /* queries processed per device batch. Default 128. */
+    uint32_t cand_cap;   /* candidate-list capacity per query per round. Default 1<<20. Overflow runs more rounds. */
+    uint32_t flags;      /* reserved, must be 0 */
+} isax_opts;
+
+typedef struct isax_index isax_index; /* opaque; owns all of its device memory */
+
+/* Fill callback for isax_build_stream. It writes `count` raw series (ids first_id ..
+ * first_id+count-1) into the DEVICE buffer dev_dst, [count][n] fp32, on cuda_stream (a
+ * cudaStream_t). It must return 0 on success. It is called twice per chunk, in id order
+ * (pass 1 summarises, pass 2 scatters), so it must produce the same bytes both times. */
+typedef int (*isax_fill_fn)(void *ctx, uint64_t first_id, uint64_t count, float *dev_dst, void *cuda_stream);
+
+/* Build an index over N raw series (north_star (a); P:289-336 MESSI stages 1-2, done as a
+ * summarise + sort instead of a pointer tree).
+ *  series : [N][n] fp32 raw values, host or device.
+ *  w      : PAA segments; must divide n. v1: 16.
+ *  card   : symbols per segment, a power of 2 in [2, 256]. v1: 256 (8 bits).
+ *  opts   : NULL for defaults.
+ *  out    : receives the index; free it with isax_free.
+ * Each series is z-normalised (R2), summarised by PAA then SAX (R3, R4), and keyed by its
+ * plane-interleaved iSAX word (R6). The z-normalised rows are stored on the device in
+ * ascending (key, id) order: the SAX-sorted, leaf-contiguous layout.
+ * Errors: E_EMPTY if N == 0; E_INVAL; E_UNSUPPORTED; E_NONFINITE; E_NOMEM; E_CUDA. */
+int isax_build(const float *series, uint64_t N, uint32_t n, uint32_t w, uint32_t card,
+               const isax_opts *opts, isax_index **out);
+
+/* Same as isax_build, but the raw series come from `fill`, `chunk` series at a time (0 = a
+ * default). This is for collections whose raw copy cannot sit next to the index in HBM:
+ * BASELINE.json configs 3 and 4, 102.4 GB each. */
+int isax_build_stream(uint64_t N, uint32_t n, uint32_t w, uint32_t card, isax_fill_fn fill, void *ctx,
+                      uint64_t chunk, const isax_opts *opts, isax_index **out);
+
+/* Exact 1-NN of Q raw queries (north_star (b)).
+ *  queries  : [Q][n] fp32 raw; each is z-normalised by the build's rule.
+ *  out_id   : [Q] int64, the original 0-based id of the nearest series. Ties go to the lowest id.
+ *  out_dist : [Q] fp32, sqrt of the squared Euclidean distance between the z-normalised
+ *             query and that series.
+ * Any pointer kinds. Synchronous: it returns when the outputs are written. Q == 0 is a no-op.
+ * The answers do not depend on Q, batching or stream. */
+int isax_nn1(const isax_index *ix, const float *queries, uint32_t Q, int64_t *out_id, float *out_dist);
+
+/* Same as isax_nn1 with DEVICE pointers, enqueued on cuda_stream (a cudaStream_t; NULL =
+ * the legacy default stream). It synchronises the stream once per batch of opts.batch_Q
+ * queries, to read the candidate-overflow flags. */
+int isax_nn1_async(const isax_index *ix, const float *d_queries, uint32_t Q, int64_t *d_out_id,
+                   float *d_out_dist, void *cuda_stream);
+
+/* Copy index contents to caller buffers (any pointer kinds, NULL = skip):
+ *  sax_by_id [count][w] u8: the iSAX words of ids first_id .. first_id+count-1.
+ *  perm      [N] u32: perm[pos] = id of the series stored at sorted position pos.
+ *  stored    [count][n] fp32: the z-normalised rows at sorted positions first_id .. +count-1.
+ * Errors: E_INVAL if first_id + count > N. */
+int isax_export(const isax_index *ix, uint64_t first_id, uint64_t count, uint8_t *sax_by_id, uint32_t *perm,
+                float *stored);
+
+/* Debug / parity entry: the query-side summaries and bounds the path uses.
+ *  q_paa  [Q][w] fp64 (NULL = skip), q_sax [Q][w] u8 (NULL = skip),
+ *  lut    [Q][w][card] fp32 (NULL = skip): (n/w) * mindist^2 per segment and symbol, rounded down,
+ *  lb2    [Q][count] fp32 (NULL = skip): LB^2 of sorted positions first_pos .. +count-1
+ *         (S:117-125), accumulated as the scan kernel does.
+ *  win    [Q][2] u32 (NULL = skip): the approximate-answer window [start, end) (R5).
+ * Any pointer kinds. */
+int isax_query_debug(const isax_index *ix, const float *queries, uint32_t Q, double *q_paa, uint8_t *q_sax,
+                     float *lut, uint64_t first_pos, uint64_t count, float *lb2, uint32_t *win);
+
+/* Counters of the last isax_nn1 / isax_nn1_async call, as a JSON object written to buf.
+ * It holds per-query window, candidates, refined, abandoned and rounds, plus per-stage
+ * device milliseconds. Returns the length needed (excluding NUL); truncates if cap is too small. */
+int isax_stats(const isax_index *ix, char *buf, size_t cap);
+
+/* Index geometry: any out pointer may be NULL. device_bytes = bytes the index holds on the device. */
+int isax_info(const isax_index *ix, uint64_t *N, uint32_t *n, uint32_t *w, uint32_t *card, uint64_t *device_bytes);
+
+void isax_free(isax_index *ix);      /* NULL-safe */
+const char *isax_last_error(void);   /* thread-local message of the last failing call on this thread */
+const char *isax_version(void);      /* "isax-b200 <semver> sm_100a" */
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ISAX_H */

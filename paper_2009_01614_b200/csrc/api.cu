@@ -1,0 +1,578 @@
+// api.cu: the C-ABI entry points of libisax.so (include/isax.h).
+//
+// This is host orchestration only: argument checks, pointer-kind detection, device memory,
+// the build's two passes, and the query batches and rounds. Every step of the method runs in
+// the kernels of summarise.cu, sort.cu, permute.cu, query.cu, lbscan.cu and refine.cu. There
+// is no CPU fallback: without a usable CUDA device every call returns ISAX_E_CUDA.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "isax_internal.cuh"
+
+namespace isax {
+
+static thread_local std::string g_err;
+
+int set_error(int code, const std::string &msg) {
+    g_err = msg;
+    return code;
+}
+
+int cuda_error(cudaError_t e, const char *what) {
+    std::string m = std::string(what) + ": " + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) + ")";
+    if (e == cudaErrorMemoryAllocation) return set_error(ISAX_E_NOMEM, m);
+    return set_error(ISAX_E_CUDA, m);
+}
+
+static bool is_device_ptr(const void *p) {
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+static isax_opts default_opts(const isax_opts *o) {
+    isax_opts r{1024, -12, 128, 1u << 20, 0};
+    if (o) {
+        if (o->window_L) r.window_L = o->window_L;
+        if (o->slack_log2) r.slack_log2 = o->slack_log2;
+        if (o->batch_Q) r.batch_Q = o->batch_Q;
+        if (o->cand_cap) r.cand_cap = o->cand_cap;
+        r.flags = o->flags;
+    }
+    return r;
+}
+
+static int check_geometry(uint64_t N, uint32_t n, uint32_t w, uint32_t card, const isax_opts &o) {
+    if (w == 0 || n == 0) return set_error(ISAX_E_INVAL, "n and w must be positive");
+    if (n % w) return set_error(ISAX_E_INVAL, "w must divide n (S:71)");
+    if (card < 2 || card > 256 || (card & (card - 1))) return set_error(ISAX_E_INVAL, "card must be a power of two in [2, 256]");
+    if (N == 0) return set_error(ISAX_E_EMPTY, "empty collection (N == 0)");
+    if (w != 16 || card != 256) return set_error(ISAX_E_UNSUPPORTED, "v1 supports w=16, card=256 only");
+    if (n % 64 || n > 1024) return set_error(ISAX_E_UNSUPPORTED, "v1 supports n a multiple of 64 in [64, 1024]");
+    if (N >= 0xffffffffull) return set_error(ISAX_E_UNSUPPORTED, "v1 supports N < 2^32 - 1");
+    if (o.window_L == 0 || o.window_L > 4096) return set_error(ISAX_E_INVAL, "window_L must be in [1, 4096]");
+    if (o.slack_log2 > -8 || o.slack_log2 < -20) return set_error(ISAX_E_INVAL, "slack_log2 must be in [-20, -8]");
+    if (o.batch_Q > 1024) return set_error(ISAX_E_INVAL, "batch_Q must be <= 1024");
+    if (o.flags) return set_error(ISAX_E_INVAL, "flags must be 0");
+    return ISAX_OK;
+}
+
+template <class T>
+static cudaError_t dmalloc(T **p, size_t count, size_t *acc) {
+    cudaError_t e = cudaMalloc((void **)p, std::max<size_t>(count, 1) * sizeof(T));
+    if (e == cudaSuccess && acc) *acc += std::max<size_t>(count, 1) * sizeof(T);
+    return e;
+}
+
+static void free_scratch(isax_index *ix) {
+    QueryScratch &q = ix->qs;
+    cudaFree(q.qy); cudaFree(q.qpaa); cudaFree(q.qsax); cudaFree(q.lut); cudaFree(q.win); cudaFree(q.bsf);
+    cudaFree(q.cand); cudaFree(q.cand_cnt); cudaFree(q.near); cudaFree(q.near_cnt); cudaFree(q.qmap); cudaFree(q.qrange);
+    cudaFree(q.counters);
+    if (q.h_cnt) cudaFreeHost(q.h_cnt);
+    q = QueryScratch{};
+}
+
+static int alloc_scratch(isax_index *ix) {
+    QueryScratch &q = ix->qs;
+    if (q.cap_Q) return ISAX_OK;
+    const uint32_t Q = ix->opts.batch_Q;
+    const uint32_t cap = ix->opts.cand_cap;
+    size_t acc = 0;
+    cudaError_t e = cudaSuccess;
+#define A(ptr, cnt) \
+    if (e == cudaSuccess) e = dmalloc(&q.ptr, (size_t)(cnt), &acc)
+    A(qy, (size_t)Q * ix->n);
+    A(qpaa, (size_t)Q * W);
+    A(qsax, (size_t)Q * W);
+    A(lut, (size_t)Q * W * CARD);
+    A(win, (size_t)Q * 2);
+    A(bsf, Q);
+    A(cand, (size_t)Q * cap);
+    A(cand_cnt, Q);
+    A(near, (size_t)Q * NEAR_K);
+    A(near_cnt, Q);
+    A(qmap, Q);
+    A(qrange, (size_t)Q * 2);
+    A(counters, (size_t)Q * 4);
+#undef A
+    if (e == cudaSuccess) e = cudaMallocHost(&q.h_cnt, sizeof(uint32_t) * (size_t)Q * 8);
+    if (e != cudaSuccess) {
+        free_scratch(ix);
+        return cuda_error(e, "allocating query scratch");
+    }
+    q.cap_Q = Q;
+    q.cand_cap = cap;
+    ix->device_bytes += acc;
+    return ISAX_OK;
+}
+
+// ------------------------------------------------------------------------------------ build
+struct Source {  // where pass 1 / pass 2 read raw rows from
+    const float *dev = nullptr;  // whole collection resident on the device
+    const float *host = nullptr; // whole collection in host memory (chunked H2D)
+    isax_fill_fn fill = nullptr; // user producer (chunked)
+    void *ctx = nullptr;
+};
+
+static int build_impl(const Source &src, uint64_t N, uint32_t n, uint32_t w, uint32_t card, uint64_t chunk,
+                      const isax_opts *opts, isax_index **out) {
+    if (!out) return set_error(ISAX_E_INVAL, "out is NULL");
+    isax_opts o = default_opts(opts);
+    int rc = check_geometry(N, n, w, card, o);
+    if (rc) return rc;
+    int dev = 0;
+    ISAX_CUDA(cudaGetDevice(&dev));
+    cudaStream_t s;
+    ISAX_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    isax_index *ix = new isax_index();
+    ix->N = N; ix->n = n; ix->w = w; ix->card = card; ix->opts = o; ix->device = dev;
+    uint8_t *sax_by_id = nullptr;
+    uint4 *keys = nullptr;
+    double2 *musig = nullptr;
+    uint32_t *ids = nullptr, *bad = nullptr, *inv = nullptr;
+    float *stage = nullptr;
+    uint32_t h_bad = 0;
+    const bool chunked = src.dev == nullptr;
+    if (chunk == 0) chunk = std::max<uint64_t>(1, (1ull << 30) / ((uint64_t)n * 4));  // ~1 GB per chunk
+    chunk = std::min(chunk, N);
+    cudaError_t e = cudaSuccess;
+    auto fail = [&](int code) {
+        cudaStreamSynchronize(s);
+        cudaFree(sax_by_id); cudaFree(keys); cudaFree(musig); cudaFree(ids); cudaFree(bad); cudaFree(inv);
+        cudaFree(stage);
+        cudaFree(ix->stored); cudaFree(ix->sax); cudaFree(ix->perm);
+        delete ix;
+        cudaStreamDestroy(s);
+        return code;
+    };
+#define TRY(call)                                                \
+    do {                                                         \
+        e = (call);                                              \
+        if (e != cudaSuccess) return fail(cuda_error(e, #call)); \
+    } while (0)
+    TRY(dmalloc(&sax_by_id, N * W, nullptr));
+    TRY(dmalloc(&keys, N, nullptr));
+    TRY(dmalloc(&musig, N, nullptr));
+    TRY(dmalloc(&ids, N, nullptr));
+    TRY(dmalloc(&ix->perm, N, &ix->device_bytes));
+    TRY(dmalloc(&bad, 1, nullptr));
+    TRY(cudaMemsetAsync(bad, 0, sizeof(uint32_t), s));
+    if (chunked) TRY(dmalloc(&stage, chunk * n, nullptr));
+    // pass 1: summarise
+    auto produce = [&](uint64_t id0, uint64_t cnt) -> int {
+        if (src.host) {
+            e = cudaMemcpyAsync(stage, src.host + id0 * n, cnt * n * sizeof(float), cudaMemcpyHostToDevice, s);
+            if (e != cudaSuccess) return cuda_error(e, "H2D chunk");
+            return ISAX_OK;
+        }
+        if (src.fill(src.ctx, id0, cnt, stage, (void *)s) != 0)
+            return set_error(ISAX_E_CALLBACK, "fill callback returned non-zero");
+        return ISAX_OK;
+    };
+    if (!chunked) {
+        launch_summarise(src.dev, N, n, 0, sax_by_id, keys, musig, bad, s);
+    } else {
+        for (uint64_t id0 = 0; id0 < N; id0 += chunk) {
+            const uint64_t cnt = std::min(chunk, N - id0);
+            if ((rc = produce(id0, cnt))) return fail(rc);
+            launch_summarise(stage, cnt, n, id0, sax_by_id, keys, musig, bad, s);
+        }
+    }
+    TRY(cudaGetLastError());
+    TRY(cudaMemcpyAsync(&h_bad, bad, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    TRY(cudaStreamSynchronize(s));
+    if (h_bad) return fail(set_error(ISAX_E_NONFINITE, "a series holds NaN or Inf"));
+    // canonical order (R6)
+    if ((rc = radix_sort_keys(keys, ids, N, ix->perm, s))) return fail(rc);
+    cudaFree(keys);
+    keys = nullptr;
+    cudaFree(ids);
+    ids = nullptr;
+    TRY(dmalloc(&ix->sax, N * W, &ix->device_bytes));
+    launch_gather_sax(sax_by_id, ix->perm, N, ix->sax, s);
+    TRY(cudaStreamSynchronize(s));
+    cudaFree(sax_by_id);
+    sax_by_id = nullptr;
+    // pass 2: store the z-normalised rows in sorted order
+    TRY(dmalloc(&ix->stored, N * n, &ix->device_bytes));
+    if (!chunked) {
+        launch_gather_rows(src.dev, musig, ix->perm, N, n, ix->stored, s);
+    } else {
+        TRY(dmalloc(&inv, N, nullptr));
+        launch_invert_perm(ix->perm, N, inv, s);
+        for (uint64_t id0 = 0; id0 < N; id0 += chunk) {
+            const uint64_t cnt = std::min(chunk, N - id0);
+            if ((rc = produce(id0, cnt))) return fail(rc);
+            launch_scatter_rows(stage, cnt, id0, musig, inv, n, ix->stored, s);
+        }
+    }
+    TRY(cudaGetLastError());
+    TRY(cudaStreamSynchronize(s));
+    cudaFree(musig); cudaFree(inv); cudaFree(stage); cudaFree(bad);
+    for (auto &ev : ix->ev) TRY(cudaEventCreate(&ev));
+#undef TRY
+    cudaStreamDestroy(s);
+    *out = ix;
+    return ISAX_OK;
+}
+
+// ------------------------------------------------------------------------------------ query
+static int nn1_device(isax_index *ix, const float *d_q, uint32_t Q, int64_t *d_id, float *d_dist, cudaStream_t s) {
+    int rc = alloc_scratch(ix);
+    if (rc) return rc;
+    QueryScratch &qs = ix->qs;
+    const float delta = std::ldexp(1.0f, ix->opts.slack_log2);
+    ix->st_win.assign(2 * (size_t)Q, 0);
+    ix->st_cand.assign(Q, 0);
+    ix->st_refined.assign(Q, 0);
+    ix->st_abandoned.assign(Q, 0);
+    ix->st_rounds.assign(Q, 0);
+    ix->st_near.assign(Q, 0);
+    ix->st_ms = StageTimes{};
+    ix->st_launches = 0;
+    // a device flag for non-finite queries
+    uint32_t *flag = nullptr;
+    ISAX_CUDA(cudaMalloc(&flag, sizeof(uint32_t)));
+    ISAX_CUDA(cudaMemsetAsync(flag, 0, sizeof(uint32_t), s));
+    std::vector<uint32_t> hmap(qs.cap_Q);
+    int result = ISAX_OK;
+    for (uint32_t b0 = 0; b0 < Q && result == ISAX_OK; b0 += qs.cap_Q) {
+        const uint32_t B = std::min(qs.cap_Q, Q - b0);
+        const bool timed = b0 == 0;
+        if (timed) cudaEventRecord(ix->ev[0], s);
+        launch_qprep(ix, d_q + (uint64_t)b0 * ix->n, B, s, flag);
+        ix->st_launches += 2;
+        if (timed) cudaEventRecord(ix->ev[1], s);
+        launch_window(ix, B, nullptr, delta, s);
+        if (timed) cudaEventRecord(ix->ev[2], s);
+        // Rounds (R10). Round 0 scans every position for every query. A query whose candidate
+        // list overflowed in range [a, b) gets that range split into pieces that fit, and the
+        // pieces are scanned in later rounds with the tighter BSF. A query whose near list
+        // overflowed keeps its BSF, empties the near list, re-refines its window and rescans
+        // everything, so the near ties of the final BSF are all collected.
+        std::vector<std::vector<std::pair<uint32_t, uint32_t>>> pending(B);
+        std::vector<uint32_t> hrange(2 * (size_t)B);
+        std::vector<uint32_t> cur_lo(B), cur_hi(B);
+        for (uint32_t i = 0; i < B; i++) pending[i].push_back({0u, (uint32_t)ix->N});
+        std::vector<uint32_t> rewin;
+        for (uint32_t round = 0;; round++) {
+            uint32_t nact = 0, lo = 0xffffffffu, hi = 0;
+            for (uint32_t i = 0; i < B; i++) {
+                if (pending[i].empty()) continue;
+                auto r = pending[i].back();
+                pending[i].pop_back();
+                cur_lo[i] = r.first;
+                cur_hi[i] = r.second;
+                hmap[nact] = i;
+                hrange[2 * nact] = r.first;
+                hrange[2 * nact + 1] = r.second;
+                lo = std::min(lo, r.first);
+                hi = std::max(hi, r.second);
+                nact++;
+            }
+            if (!nact) break;
+            if (round > 0) {
+                ISAX_CUDA(cudaMemsetAsync(qs.cand_cnt, 0, B * sizeof(uint32_t), s));
+                if (!rewin.empty()) {
+                    for (uint32_t i : rewin) ISAX_CUDA(cudaMemsetAsync(qs.near_cnt + i, 0, sizeof(uint32_t), s));
+                    ISAX_CUDA(cudaMemcpyAsync(qs.qmap, rewin.data(), rewin.size() * sizeof(uint32_t),
+                                              cudaMemcpyHostToDevice, s));
+                    launch_window(ix, (uint32_t)rewin.size(), qs.qmap, delta, s);
+                    ix->st_launches += 1;
+                    rewin.clear();
+                }
+            }
+            ISAX_CUDA(cudaMemcpyAsync(qs.qmap, hmap.data(), nact * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+            ISAX_CUDA(cudaMemcpyAsync(qs.qrange, hrange.data(), 2 * nact * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+            launch_lbscan(ix, nact, qs.qmap, qs.qrange, lo, hi, delta, s);
+            if (timed && round == 0) cudaEventRecord(ix->ev[3], s);
+            launch_refine(ix, B, delta, s);
+            ix->st_launches += 2;
+            if (timed && round == 0) cudaEventRecord(ix->ev[4], s);
+            ISAX_CUDA(cudaGetLastError());
+            ISAX_CUDA(cudaMemcpyAsync(qs.h_cnt, qs.cand_cnt, B * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+            ISAX_CUDA(cudaMemcpyAsync(qs.h_cnt + qs.cap_Q, qs.near_cnt, B * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+            ISAX_CUDA(cudaMemcpyAsync(qs.h_cnt + 2 * qs.cap_Q, flag, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+            ISAX_CUDA(cudaStreamSynchronize(s));
+            if (qs.h_cnt[2 * qs.cap_Q]) {
+                result = set_error(ISAX_E_NONFINITE, "a query holds NaN or Inf");
+                break;
+            }
+            for (uint32_t k = 0; k < nact; k++) {
+                const uint32_t i = hmap[k];
+                const uint32_t cnt = qs.h_cnt[i];
+                ix->st_cand[b0 + i] += std::min(cnt, qs.cand_cap);
+                ix->st_rounds[b0 + i] = round + 1;
+                if (qs.h_cnt[qs.cap_Q + i] > (uint32_t)NEAR_K) {
+                    pending[i].clear();
+                    pending[i].push_back({0u, (uint32_t)ix->N});
+                    rewin.push_back(i);
+                } else if (cnt > qs.cand_cap) {
+                    const uint64_t a = cur_lo[i], b = cur_hi[i];
+                    const uint64_t pieces = std::min<uint64_t>(b - a, 2 * ((uint64_t)cnt + qs.cand_cap - 1) / qs.cand_cap);
+                    for (uint64_t p = pieces; p-- > 0;)  // pushed in reverse: scanned in ascending order
+                        pending[i].push_back({(uint32_t)(a + (b - a) * p / pieces), (uint32_t)(a + (b - a) * (p + 1) / pieces)});
+                }
+            }
+            if (round > 100000) {
+                result = set_error(ISAX_E_CUDA, "candidate rounds did not converge");
+                break;
+            }
+        }
+        if (result) break;
+        launch_finalize(ix, B, delta, d_id + b0, d_dist + b0, s);
+        ix->st_launches += 1;
+        if (timed) cudaEventRecord(ix->ev[5], s);
+        ISAX_CUDA(cudaGetLastError());
+        // stats
+        std::vector<uint32_t> tmp((size_t)B * 4);
+        ISAX_CUDA(cudaMemcpyAsync(tmp.data(), qs.counters, tmp.size() * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+        std::vector<uint32_t> tw((size_t)B * 2);
+        ISAX_CUDA(cudaMemcpyAsync(tw.data(), qs.win, tw.size() * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+        ISAX_CUDA(cudaStreamSynchronize(s));
+        for (uint32_t i = 0; i < B; i++) {
+            ix->st_refined[b0 + i] = tmp[4 * i];
+            ix->st_abandoned[b0 + i] = tmp[4 * i + 1];
+            ix->st_near[b0 + i] = qs.h_cnt[qs.cap_Q + i];
+            ix->st_win[2 * (b0 + i)] = tw[2 * i];
+            ix->st_win[2 * (b0 + i) + 1] = tw[2 * i + 1];
+        }
+        if (timed) {
+            cudaEventElapsedTime(&ix->st_ms.qprep, ix->ev[0], ix->ev[1]);
+            cudaEventElapsedTime(&ix->st_ms.window, ix->ev[1], ix->ev[2]);
+            cudaEventElapsedTime(&ix->st_ms.lbscan, ix->ev[2], ix->ev[3]);
+            cudaEventElapsedTime(&ix->st_ms.refine, ix->ev[3], ix->ev[4]);
+            float tot = 0;
+            cudaEventElapsedTime(&tot, ix->ev[0], ix->ev[5]);
+            ix->st_ms.finalize = tot;  // whole first batch
+        }
+    }
+    cudaFree(flag);
+    return result;
+}
+
+}  // namespace isax
+
+using namespace isax;
+
+extern "C" {
+
+int isax_build(const float *series, uint64_t N, uint32_t n, uint32_t w, uint32_t card, const isax_opts *opts,
+               isax_index **out) {
+    if (!series && N) return set_error(ISAX_E_INVAL, "series is NULL");
+    Source src;
+    if (N && is_device_ptr(series)) {
+        if (reinterpret_cast<uintptr_t>(series) % 16) return set_error(ISAX_E_INVAL, "device series must be 16-byte aligned");
+        src.dev = series;
+    } else {
+        src.host = series;
+    }
+    return build_impl(src, N, n, w, card, 0, opts, out);
+}
+
+int isax_build_stream(uint64_t N, uint32_t n, uint32_t w, uint32_t card, isax_fill_fn fill, void *ctx, uint64_t chunk,
+                      const isax_opts *opts, isax_index **out) {
+    if (!fill) return set_error(ISAX_E_INVAL, "fill is NULL");
+    Source src;
+    src.fill = fill;
+    src.ctx = ctx;
+    return build_impl(src, N, n, w, card, chunk, opts, out);
+}
+
+int isax_nn1_async(const isax_index *cix, const float *d_queries, uint32_t Q, int64_t *d_out_id, float *d_out_dist,
+                   void *cuda_stream) {
+    if (!cix) return set_error(ISAX_E_INVAL, "index is NULL");
+    if (Q == 0) return ISAX_OK;
+    if (!d_queries || !d_out_id || !d_out_dist) return set_error(ISAX_E_INVAL, "NULL pointer");
+    isax_index *ix = const_cast<isax_index *>(cix);
+    std::lock_guard<std::mutex> lk(ix->mu);
+    return nn1_device(ix, d_queries, Q, d_out_id, d_out_dist, (cudaStream_t)cuda_stream);
+}
+
+int isax_nn1(const isax_index *cix, const float *queries, uint32_t Q, int64_t *out_id, float *out_dist) {
+    if (!cix) return set_error(ISAX_E_INVAL, "index is NULL");
+    if (Q == 0) return ISAX_OK;
+    if (!queries || !out_id || !out_dist) return set_error(ISAX_E_INVAL, "NULL pointer");
+    isax_index *ix = const_cast<isax_index *>(cix);
+    std::lock_guard<std::mutex> lk(ix->mu);
+    cudaStream_t s;
+    ISAX_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    const size_t qbytes = (size_t)Q * ix->n * sizeof(float);
+    const bool qdev = is_device_ptr(queries), idev = is_device_ptr(out_id), ddev = is_device_ptr(out_dist);
+    float *dq = nullptr;
+    int64_t *did = nullptr;
+    float *dd = nullptr;
+    int rc = ISAX_OK;
+    cudaError_t e = cudaSuccess;
+    if (!qdev) {
+        e = cudaMalloc(&dq, qbytes);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(dq, queries, qbytes, cudaMemcpyHostToDevice, s);
+    }
+    if (e == cudaSuccess && !idev) e = cudaMalloc(&did, Q * sizeof(int64_t));
+    if (e == cudaSuccess && !ddev) e = cudaMalloc(&dd, Q * sizeof(float));
+    if (e != cudaSuccess) rc = cuda_error(e, "isax_nn1 staging");
+    if (!rc)
+        rc = nn1_device(ix, qdev ? queries : dq, Q, idev ? out_id : did, ddev ? out_dist : dd, s);
+    if (!rc && !idev) e = cudaMemcpyAsync(out_id, did, Q * sizeof(int64_t), cudaMemcpyDeviceToHost, s);
+    if (!rc && e == cudaSuccess && !ddev) e = cudaMemcpyAsync(out_dist, dd, Q * sizeof(float), cudaMemcpyDeviceToHost, s);
+    if (!rc && e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (!rc && e != cudaSuccess) rc = cuda_error(e, "isax_nn1 copy-out");
+    cudaStreamSynchronize(s);
+    cudaFree(dq); cudaFree(did); cudaFree(dd);
+    cudaStreamDestroy(s);
+    return rc;
+}
+
+int isax_export(const isax_index *ix, uint64_t first_id, uint64_t count, uint8_t *sax_by_id, uint32_t *perm,
+                float *stored) {
+    if (!ix) return set_error(ISAX_E_INVAL, "index is NULL");
+    if (first_id > ix->N || count > ix->N - first_id) return set_error(ISAX_E_INVAL, "range out of bounds");
+    cudaStream_t s;
+    ISAX_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    int rc = ISAX_OK;
+    cudaError_t e = cudaSuccess;
+    if (perm) e = cudaMemcpyAsync(perm, ix->perm, ix->N * sizeof(uint32_t), cudaMemcpyDefault, s);
+    if (e == cudaSuccess && stored && count)
+        e = cudaMemcpyAsync(stored, ix->stored + first_id * ix->n, count * ix->n * sizeof(float), cudaMemcpyDefault, s);
+    if (e == cudaSuccess && sax_by_id && count) {
+        uint32_t *inv = nullptr;
+        uint8_t *tmp = nullptr;
+        e = cudaMalloc(&inv, ix->N * sizeof(uint32_t));
+        if (e == cudaSuccess) e = cudaMalloc(&tmp, count * W);
+        if (e == cudaSuccess) {
+            launch_invert_perm(ix->perm, ix->N, inv, s);
+            launch_export_sax(ix->sax, inv, first_id, count, tmp, s);
+            e = cudaMemcpyAsync(sax_by_id, tmp, count * W, cudaMemcpyDefault, s);
+        }
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        cudaFree(inv);
+        cudaFree(tmp);
+    }
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) rc = cuda_error(e, "isax_export");
+    cudaStreamDestroy(s);
+    return rc;
+}
+
+int isax_query_debug(const isax_index *cix, const float *queries, uint32_t Q, double *q_paa, uint8_t *q_sax, float *lut,
+                     uint64_t first_pos, uint64_t count, float *lb2, uint32_t *win) {
+    if (!cix) return set_error(ISAX_E_INVAL, "index is NULL");
+    if (!queries && Q) return set_error(ISAX_E_INVAL, "queries is NULL");
+    if (lb2 && (first_pos > cix->N || count > cix->N - first_pos)) return set_error(ISAX_E_INVAL, "range out of bounds");
+    isax_index *ix = const_cast<isax_index *>(cix);
+    std::lock_guard<std::mutex> lk(ix->mu);
+    int rc = alloc_scratch(ix);
+    if (rc) return rc;
+    if (Q > ix->qs.cap_Q) return set_error(ISAX_E_INVAL, "Q exceeds batch_Q");
+    if (Q == 0) return ISAX_OK;
+    cudaStream_t s;
+    ISAX_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    const size_t qbytes = (size_t)Q * ix->n * sizeof(float);
+    float *dq = nullptr, *dlb = nullptr;
+    uint32_t *flag = nullptr;
+    cudaError_t e = cudaMalloc(&dq, qbytes);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(dq, queries, qbytes, cudaMemcpyDefault, s);
+    if (e == cudaSuccess) e = cudaMalloc(&flag, sizeof(uint32_t));
+    if (e == cudaSuccess) e = cudaMemsetAsync(flag, 0, sizeof(uint32_t), s);
+    if (e == cudaSuccess) {
+        launch_qprep(ix, dq, Q, s, flag);
+        e = cudaGetLastError();
+    }
+    const QueryScratch &qs = ix->qs;
+    if (e == cudaSuccess && q_paa) e = cudaMemcpyAsync(q_paa, qs.qpaa, (size_t)Q * W * sizeof(double), cudaMemcpyDefault, s);
+    if (e == cudaSuccess && q_sax) e = cudaMemcpyAsync(q_sax, qs.qsax, (size_t)Q * W, cudaMemcpyDefault, s);
+    if (e == cudaSuccess && lut) e = cudaMemcpyAsync(lut, qs.lut, (size_t)Q * W * CARD * sizeof(float), cudaMemcpyDefault, s);
+    if (e == cudaSuccess && win) e = cudaMemcpyAsync(win, qs.win, (size_t)Q * 2 * sizeof(uint32_t), cudaMemcpyDefault, s);
+    if (e == cudaSuccess && lb2 && count) {
+        e = cudaMalloc(&dlb, (size_t)Q * count * sizeof(float));
+        if (e == cudaSuccess) {
+            launch_lb_dump(ix, Q, first_pos, count, dlb, s);
+            e = cudaMemcpyAsync(lb2, dlb, (size_t)Q * count * sizeof(float), cudaMemcpyDefault, s);
+        }
+    }
+    uint32_t h_flag = 0;
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&h_flag, flag, sizeof(uint32_t), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    rc = e == cudaSuccess ? ISAX_OK : cuda_error(e, "isax_query_debug");
+    if (!rc && h_flag) rc = set_error(ISAX_E_NONFINITE, "a query holds NaN or Inf");
+    cudaStreamSynchronize(s);
+    cudaFree(dq); cudaFree(dlb); cudaFree(flag);
+    cudaStreamDestroy(s);
+    return rc;
+}
+
+int isax_stats(const isax_index *cix, char *buf, size_t cap) {
+    if (!cix) return set_error(ISAX_E_INVAL, "index is NULL");
+    isax_index *ix = const_cast<isax_index *>(cix);
+    std::lock_guard<std::mutex> lk(ix->mu);
+    std::string j = "{";
+    char tmp[256];
+    snprintf(tmp, sizeof tmp,
+             "\"N\":%llu,\"n\":%u,\"window_L\":%u,\"slack_log2\":%d,\"batch_Q\":%u,\"cand_cap\":%u,"
+             "\"ms_first_batch\":{\"qprep\":%.4f,\"window\":%.4f,\"lbscan\":%.4f,\"refine\":%.4f,\"total\":%.4f},",
+             (unsigned long long)ix->N, ix->n, ix->opts.window_L, ix->opts.slack_log2, ix->opts.batch_Q,
+             ix->opts.cand_cap, ix->st_ms.qprep, ix->st_ms.window, ix->st_ms.lbscan, ix->st_ms.refine,
+             ix->st_ms.finalize);
+    j += tmp;
+    auto arr = [&](const char *name, const std::vector<uint32_t> &v, bool last) {
+        j += "\"";
+        j += name;
+        j += "\":[";
+        for (size_t i = 0; i < v.size(); i++) {
+            if (i) j += ",";
+            j += std::to_string(v[i]);
+        }
+        j += last ? "]" : "],";
+    };
+    arr("window", ix->st_win, false);
+    arr("candidates", ix->st_cand, false);
+    arr("refined", ix->st_refined, false);
+    arr("abandoned", ix->st_abandoned, false);
+    arr("rounds", ix->st_rounds, false);
+    arr("near", ix->st_near, false);
+    j += "\"launches\":" + std::to_string(ix->st_launches);
+    j += "}";
+    if (buf && cap) {
+        size_t k = std::min(cap - 1, j.size());
+        memcpy(buf, j.data(), k);
+        buf[k] = 0;
+    }
+    return (int)j.size();
+}
+
+int isax_info(const isax_index *ix, uint64_t *N, uint32_t *n, uint32_t *w, uint32_t *card, uint64_t *device_bytes) {
+    if (!ix) return set_error(ISAX_E_INVAL, "index is NULL");
+    if (N) *N = ix->N;
+    if (n) *n = ix->n;
+    if (w) *w = ix->w;
+    if (card) *card = ix->card;
+    if (device_bytes) *device_bytes = ix->device_bytes;
+    return ISAX_OK;
+}
+
+void isax_free(isax_index *ix) {
+    if (!ix) return;
+    {
+        std::lock_guard<std::mutex> lk(ix->mu);
+        cudaFree(ix->stored);
+        cudaFree(ix->sax);
+        cudaFree(ix->perm);
+        free_scratch(ix);
+        for (auto &ev : ix->ev)
+            if (ev) cudaEventDestroy(ev);
+    }
+    delete ix;
+}
+
+const char *isax_last_error(void) { return g_err.c_str(); }
+
+const char *isax_version(void) { return "isax-b200 0.1.0 sm_100a"; }
+
+}  // extern "C"

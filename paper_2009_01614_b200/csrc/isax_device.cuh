@@ -1,0 +1,62 @@
+// isax_device.cuh: device helpers shared by the libisax kernels (iSAX symbol, key, compare).
+#pragma once
+#include "isax_internal.cuh"
+
+namespace isax {
+
+__host__ __device__ __forceinline__ uint64_t umin64(uint64_t a, uint64_t b) { return a < b ? a : b; }
+
+// Number of beta_k <= m over the 255 breakpoints in `beta` (the tie goes up: S:90, R4).
+__device__ __forceinline__ uint32_t sax_symbol(const double *beta, double m) {
+    uint32_t c = 0;
+#pragma unroll
+    for (uint32_t step = 128; step >= 1; step >>= 1)
+        if (beta[c + step - 1] <= m) c += step;
+    return c;
+}
+
+// Plane-major bit interleave (R6): key bit (127 - 16p - s) = bit (7 - p) of symbol s.
+// key.w holds planes 0,1 (most significant), key.x holds planes 6,7.
+__device__ __forceinline__ uint4 isax_key(const uint32_t sym[W]) {
+    uint32_t plane[8];
+#pragma unroll
+    for (int p = 0; p < 8; p++) {
+        uint32_t v = 0;
+#pragma unroll
+        for (int s = 0; s < W; s++) v |= ((sym[s] >> (7 - p)) & 1u) << (15 - s);
+        plane[p] = v;
+    }
+    return make_uint4((plane[6] << 16) | plane[7], (plane[4] << 16) | plane[5], (plane[2] << 16) | plane[3],
+                      (plane[0] << 16) | plane[1]);
+}
+
+__device__ __forceinline__ uint4 word_key(uint4 wv) {
+    uint32_t sym[W];
+    const uint32_t v[4] = {wv.x, wv.y, wv.z, wv.w};
+#pragma unroll
+    for (int s = 0; s < W; s++) sym[s] = (v[s >> 2] >> (8 * (s & 3))) & 0xFFu;
+    return isax_key(sym);
+}
+
+__device__ __forceinline__ bool key_less(uint4 a, uint4 b) {
+    if (a.w != b.w) return a.w < b.w;
+    if (a.z != b.z) return a.z < b.z;
+    if (a.y != b.y) return a.y < b.y;
+    return a.x < b.x;
+}
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+__device__ __forceinline__ double warp_sum_d(double v) {
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+__device__ __forceinline__ float bsf_d2(unsigned long long p) { return __uint_as_float((uint32_t)(p >> 32)); }
+
+}  // namespace isax

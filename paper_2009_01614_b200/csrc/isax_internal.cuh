@@ -1,0 +1,134 @@
+// isax_internal.cuh: shared declarations of the libisax.so translation units (not part of the ABI).
+//
+// Data layout in HBM, per index:
+//   stored [N][n] fp32  z-normalised rows, in ascending (key, id) order (sorted position = pos)
+//   sax    [N][16] u8   iSAX word of the row at pos (16 B per series, one uint4 load)
+//   perm   [N] u32      perm[pos] = original id
+// The 16 breakpoints' worth of state a query needs (LUT) is built per query batch.
+#pragma once
+#include <cstdint>
+#include <cstddef>
+#include <mutex>
+#include <string>
+#include <vector>
+#include <cuda_runtime.h>
+
+#include "../../include/isax.h"
+
+namespace isax {
+
+constexpr int W = 16;        // segments ("w is fixed to 16")
+constexpr int CARD = 256;    // symbols per segment (8 bits)
+constexpr int NEAR_K = 256;  // near-tie list capacity per query (R9)
+
+// Packed BSF: high 32 bits = fp32 bits of d^2 (non-negative, so the bit order is the
+// numeric order), low 32 bits = original id. atomicMin on the packed word is the
+// lexicographic min of (d^2, id) (ties to the lowest id per north_star).
+__host__ __device__ inline unsigned long long pack_bsf(float d2, uint32_t id) {
+#ifdef __CUDA_ARCH__
+    return ((unsigned long long)__float_as_uint(d2) << 32) | id;
+#else
+    uint32_t b;
+    memcpy(&b, &d2, 4);
+    return ((unsigned long long)b << 32) | id;
+#endif
+}
+
+struct NearEntry {  // a completed refinement within (1+delta) of the BSF at that moment (R9)
+    uint32_t id;
+    uint32_t pos;
+    float d2;
+    uint32_t pad;
+};
+
+// Per-batch scratch owned by the index (sized for opts.batch_Q queries).
+struct QueryScratch {
+    uint32_t cap_Q = 0;
+    uint32_t cand_cap = 0;
+    float *qy = nullptr;            // [Q][n] z-normalised queries
+    double *qpaa = nullptr;         // [Q][16]
+    uint8_t *qsax = nullptr;        // [Q][16]
+    float *lut = nullptr;           // [Q][16][256] fp32, rounded down
+    uint32_t *win = nullptr;        // [Q][2] window [start, end)
+    unsigned long long *bsf = nullptr;  // [Q] packed
+    uint32_t *cand = nullptr;       // [Q][cand_cap] sorted positions
+    uint32_t *cand_cnt = nullptr;   // [Q] (may exceed cand_cap: overflow)
+    NearEntry *near = nullptr;      // [Q][NEAR_K]
+    uint32_t *near_cnt = nullptr;   // [Q]
+    uint32_t *qmap = nullptr;       // [Q] active slot -> batch slot, for re-scan rounds
+    uint32_t *qrange = nullptr;     // [Q][2] sorted-position range [r0, r1) of each active slot
+    uint32_t *counters = nullptr;   // [Q][4]: refined, abandoned, rounds, near_overflow
+    uint32_t *h_cnt = nullptr;      // pinned host mirror of cand_cnt + near_cnt + counters
+};
+
+struct StageTimes {
+    float qprep = 0, window = 0, lbscan = 0, refine = 0, finalize = 0;
+};
+
+}  // namespace isax
+
+struct isax_index {
+    uint64_t N = 0;
+    uint32_t n = 0, w = 0, card = 0;
+    isax_opts opts{};
+    int device = 0;
+    float *stored = nullptr;
+    uint8_t *sax = nullptr;
+    uint32_t *perm = nullptr;
+    size_t device_bytes = 0;
+    isax::QueryScratch qs;
+    std::mutex mu;
+    // last-call statistics (host copies)
+    std::vector<uint32_t> st_win, st_cand, st_refined, st_abandoned, st_rounds, st_near;
+    isax::StageTimes st_ms;
+    uint64_t st_launches = 0;  // kernels launched by the last nn1 call
+    cudaEvent_t ev[8] = {};
+};
+
+namespace isax {
+
+// ---- error plumbing (api.cu) ----
+int set_error(int code, const std::string &msg);
+int cuda_error(cudaError_t e, const char *what);
+
+#define ISAX_CUDA(call)                                            \
+    do {                                                           \
+        cudaError_t _e = (call);                                   \
+        if (_e != cudaSuccess) return ::isax::cuda_error(_e, #call); \
+    } while (0)
+
+// ---- kernels' host launchers ----
+// summarise.cu
+// Pass 1 of the build over rows [0, count) of x (raw, device). Writes, for id = id0 + r:
+// sax_by_id[id], key[id] (uint4, 128-bit interleaved), musig[id] (mu, sigma as double2),
+// and sets *bad if a row holds NaN/Inf.
+void launch_summarise(const float *x, uint64_t count, uint32_t n, uint64_t id0, uint8_t *sax_by_id,
+                      uint4 *key, double2 *musig, uint32_t *bad, cudaStream_t s);
+// sort.cu: stable LSD radix sort of (key, id) ascending. The input ids are iota. On return
+// perm (= ids_out) holds ids in ascending (key, id) order. Scratch is allocated internally.
+int radix_sort_keys(uint4 *keys, uint32_t *ids, uint64_t N, uint32_t *perm_out, cudaStream_t s);
+// permute.cu
+void launch_gather_rows(const float *x, const double2 *musig, const uint32_t *perm, uint64_t N, uint32_t n,
+                        float *stored, cudaStream_t s);
+void launch_scatter_rows(const float *x, uint64_t count, uint64_t id0, const double2 *musig, const uint32_t *inv,
+                         uint32_t n, float *stored, cudaStream_t s);
+void launch_gather_sax(const uint8_t *sax_by_id, const uint32_t *perm, uint64_t N, uint8_t *sax, cudaStream_t s);
+void launch_invert_perm(const uint32_t *perm, uint64_t N, uint32_t *inv, cudaStream_t s);
+void launch_export_sax(const uint8_t *sax, const uint32_t *inv, uint64_t first_id, uint64_t count, uint8_t *out,
+                       cudaStream_t s);
+// query.cu
+void launch_qprep(const isax_index *ix, const float *queries, uint32_t Q, cudaStream_t s, uint32_t *bad);
+void launch_window(const isax_index *ix, uint32_t Q, const uint32_t *qmap, float delta, cudaStream_t s);
+void launch_lb_dump(const isax_index *ix, uint32_t Q, uint64_t first_pos, uint64_t count, float *out,
+                    cudaStream_t s);
+// lbscan.cu
+// Scan sorted positions [lo, hi) for the nq queries qmap[0..nq), each restricted to its own
+// position range qrange[2i], qrange[2i+1] (overflow rounds split a query's range).
+void launch_lbscan(const isax_index *ix, uint32_t nq, const uint32_t *qmap, const uint32_t *qrange, uint32_t lo,
+                   uint32_t hi, float delta, cudaStream_t s);
+// refine.cu
+void launch_refine(const isax_index *ix, uint32_t Q, float delta, cudaStream_t s);
+void launch_finalize(const isax_index *ix, uint32_t Q, float delta, int64_t *out_id, float *out_dist,
+                     cudaStream_t s);
+
+}  // namespace isax

@@ -1,0 +1,247 @@
+// query.cu: query preparation (north_star (b) "the query's PAA") and the approximate answer
+// (north_star (b) "an initial best-so-far from the leaf matching the query's iSAX word").
+//
+//  qprep_kernel  one CTA per query: z-norm (R2, same fp64 order as the build), PAA, SAX, key,
+//                the per-segment mindist LUT, and the window position. It also resets the
+//                per-query counters and the packed BSF.
+//                LUT[s][c] = (n/w) * max(0, beta_c - m_s, m_s - beta_{c+1})^2 in fp64, rounded
+//                DOWN to fp32 (R7), so an fp32 sum of LUT entries never
+//                overestimates the fp64 bound by more than its own summation error.
+//                locate: the first sorted position whose key is >= the query key. One warp
+//                runs a 32-ary search: each step probes 32 positions, so ~6 dependent loads
+//                at N = 1e8 (R5).
+//  window_kernel one CTA per query refines the L sorted rows around that position. P:271-272:
+//                "the real distance between the query and the best candidate series, which is
+//                in the leaf with the smallest lower bound distance"; P:341-345 for MESSI.
+//                The CTA reduces the window minimum first, then appends only the near ties
+//                (R9), so the near list does not fill with the whole window.
+#include "isax_device.cuh"
+
+namespace isax {
+
+#include "breakpoints.inc"
+
+__constant__ double c_beta_q[ISAX_NBETA] = ISAX_BETA_INIT;
+
+__global__ void __launch_bounds__(256) qprep_kernel(const float *__restrict__ queries, uint32_t n,
+                                                    const uint4 *__restrict__ sax, uint64_t N, uint32_t L,
+                                                    float *__restrict__ qy, double *__restrict__ qpaa,
+                                                    uint8_t *__restrict__ qsax, float *__restrict__ lut,
+                                                    uint32_t *__restrict__ win, unsigned long long *__restrict__ bsf,
+                                                    uint32_t *__restrict__ cand_cnt, uint32_t *__restrict__ near_cnt,
+                                                    uint32_t *__restrict__ counters, uint32_t *__restrict__ bad) {
+    __shared__ float row[1024];
+    __shared__ double beta[ISAX_NBETA];
+    __shared__ double m[W];
+    __shared__ uint32_t sym[W];
+    __shared__ double stats[2];
+    const uint32_t q = blockIdx.x, t = threadIdx.x;
+    for (uint32_t i = t; i < n; i += blockDim.x) row[i] = queries[(uint64_t)q * n + i];
+    for (uint32_t k = t; k < ISAX_NBETA; k += blockDim.x) beta[k] = c_beta_q[k];
+    __syncthreads();
+    if (t == 0) {  // C1, strictly left to right (R3): one thread, the same operations as summarise.cu
+        double s = 0.0;
+        bool finite = true;
+        for (uint32_t i = 0; i < n; i++) {
+            finite &= isfinite(row[i]);
+            s = __dadd_rn(s, (double)row[i]);
+        }
+        const double mu = __ddiv_rn(s, (double)n);
+        double s2 = 0.0;
+        for (uint32_t i = 0; i < n; i++) {
+            double d = __dsub_rn((double)row[i], mu);
+            s2 = __dadd_rn(s2, __dmul_rn(d, d));
+        }
+        stats[0] = mu;
+        stats[1] = __dsqrt_rn(__ddiv_rn(s2, (double)n));
+        if (!finite) atomicOr(bad, 1u);
+        // reset the per-query state of this batch slot
+        cand_cnt[q] = 0;
+        near_cnt[q] = 0;
+        counters[4 * q + 0] = counters[4 * q + 1] = counters[4 * q + 2] = counters[4 * q + 3] = 0;
+        bsf[q] = ~0ull;
+    }
+    __syncthreads();
+    const double mu = stats[0], sd = stats[1];
+    const bool flat = sd < 1e-12;
+    for (uint32_t i = t; i < n; i += blockDim.x) {
+        const float y = flat ? 0.0f : __double2float_rn(__ddiv_rn(__dsub_rn((double)row[i], mu), sd));
+        row[i] = y;
+        qy[(uint64_t)q * n + i] = y;
+    }
+    __syncthreads();
+    const uint32_t seg = n / W;
+    if (t < W) {  // C2 + C4
+        double acc = 0.0;
+        for (uint32_t j = 0; j < seg; j++) acc = __dadd_rn(acc, (double)row[t * seg + j]);
+        const double mm = __ddiv_rn(acc, (double)seg);
+        m[t] = mm;
+        sym[t] = sax_symbol(beta, mm);
+        qpaa[q * W + t] = mm;
+        qsax[q * W + t] = (uint8_t)sym[t];
+    }
+    __syncthreads();
+    // LUT (R7): the fp64 mindist per (segment, symbol), scaled by n/w, rounded down to fp32
+    const double segd = (double)seg;
+    for (uint32_t e = t; e < W * CARD; e += blockDim.x) {
+        const uint32_t s = e >> 8, c = e & 255u;
+        const double mm = m[s];
+        double d = 0.0;
+        if (c > 0 && mm < beta[c - 1]) d = __dsub_rn(beta[c - 1], mm);
+        else if (c < CARD - 1 && mm > beta[c]) d = __dsub_rn(mm, beta[c]);
+        lut[((uint64_t)q * W + s) * CARD + c] = __double2float_rd(__dmul_rn(segd, __dmul_rn(d, d)));
+    }
+    if (t < 32) {  // locate: first pos with key(pos) >= key(q), 32-ary search by warp 0
+        uint32_t sy[W];
+#pragma unroll
+        for (int s = 0; s < W; s++) sy[s] = sym[s];
+        const uint4 kq = isax_key(sy);
+        uint64_t lo = 0, hi = N;
+        while (hi - lo > 32) {
+            const uint64_t span = hi - lo;
+            const uint64_t p = lo + (span * (t + 1)) / 33;
+            const bool less = key_less(word_key(__ldg(sax + p)), kq);
+            const uint32_t bal = __ballot_sync(0xffffffffu, less);
+            const uint32_t c = __popc(bal);  // probes are increasing, so `less` is a prefix
+            const uint64_t p_last = __shfl_sync(0xffffffffu, p, (c == 0 ? 0 : c - 1));
+            const uint64_t p_next = __shfl_sync(0xffffffffu, p, (c == 32 ? 31 : c));
+            if (c == 0) hi = p_next;
+            else {
+                lo = p_last + 1;
+                if (c < 32) hi = p_next;
+            }
+        }
+        const bool less = (lo + t < hi) && key_less(word_key(__ldg(sax + lo + t)), kq);
+        const uint64_t pos = lo + __popc(__ballot_sync(0xffffffffu, less));
+        if (t == 0) {
+            uint64_t start = 0, end = N;
+            if (N > L) {
+                const int64_t s0 = (int64_t)pos - (int64_t)(L / 2);
+                const int64_t smax = (int64_t)(N - L);
+                start = (uint64_t)(s0 < 0 ? 0 : (s0 > smax ? smax : s0));
+                end = start + L;
+            }
+            win[2 * q] = (uint32_t)start;
+            win[2 * q + 1] = (uint32_t)end;
+        }
+    }
+}
+
+void launch_qprep(const isax_index *ix, const float *queries, uint32_t Q, cudaStream_t s, uint32_t *bad) {
+    const QueryScratch &qs = ix->qs;
+    qprep_kernel<<<Q, 256, 0, s>>>(queries, ix->n, reinterpret_cast<const uint4 *>(ix->sax), ix->N,
+                                   ix->opts.window_L, qs.qy, qs.qpaa, qs.qsax, qs.lut, qs.win, qs.bsf, qs.cand_cnt,
+                                   qs.near_cnt, qs.counters, bad);
+}
+
+// ------------------------------------------------------------------------------------ window
+// d^2 of one row by one warp: lane holds elements [k*128 + 4*lane, +4) for k < NS.
+template <int NS>
+__device__ __forceinline__ float row_d2(const float *__restrict__ row, const float4 (&qv)[NS], uint32_t n,
+                                        uint32_t lane) {
+    float acc = 0.f;
+#pragma unroll
+    for (int k = 0; k < NS; k++) {
+        const uint32_t i = k * 128 + 4 * lane;
+        if (i < n) {
+            const float4 v = __ldcs(reinterpret_cast<const float4 *>(row + i));
+            float d;
+            d = v.x - qv[k].x; acc = fmaf(d, d, acc);
+            d = v.y - qv[k].y; acc = fmaf(d, d, acc);
+            d = v.z - qv[k].z; acc = fmaf(d, d, acc);
+            d = v.w - qv[k].w; acc = fmaf(d, d, acc);
+        }
+    }
+    return warp_sum(acc);
+}
+
+constexpr uint32_t WIN_MAX = 4096;
+
+template <int NS>
+__global__ void __launch_bounds__(256) window_kernel(const float *__restrict__ stored, const uint32_t *__restrict__ perm,
+                                                     uint32_t n, const float *__restrict__ qy,
+                                                     const uint32_t *__restrict__ win, const uint32_t *__restrict__ qmap,
+                                                     unsigned long long *__restrict__ bsf, NearEntry *__restrict__ near,
+                                                     uint32_t *__restrict__ near_cnt, uint32_t *__restrict__ counters,
+                                                     float onepd) {
+    __shared__ float d2s[WIN_MAX];
+    __shared__ unsigned long long smin;
+    __shared__ unsigned long long cur;
+    const uint32_t q = qmap ? qmap[blockIdx.x] : blockIdx.x;
+    const uint32_t t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const uint32_t ws = win[2 * q], we = win[2 * q + 1], L = we - ws;
+    float4 qv[NS];
+#pragma unroll
+    for (int k = 0; k < NS; k++) {
+        const uint32_t i = k * 128 + 4 * lane;
+        qv[k] = i < n ? *reinterpret_cast<const float4 *>(qy + (uint64_t)q * n + i) : make_float4(0, 0, 0, 0);
+    }
+    if (t == 0) smin = ~0ull;
+    __syncthreads();
+    unsigned long long mine = ~0ull;
+    for (uint32_t r = warp; r < L; r += 8) {
+        const float d2 = row_d2<NS>(stored + (uint64_t)(ws + r) * n, qv, n, lane);
+        if (lane == 0) {
+            d2s[r] = d2;
+            const unsigned long long p = pack_bsf(d2, perm[ws + r]);
+            mine = p < mine ? p : mine;
+        }
+    }
+    if (lane == 0) atomicMin(&smin, mine);
+    __syncthreads();
+    if (t == 0) {
+        atomicMin(&bsf[q], smin);
+        cur = atomicAdd(&bsf[q], 0ull);
+        atomicAdd(&counters[4 * q + 0], L);
+    }
+    __syncthreads();
+    const float lim = bsf_d2(cur) * onepd;
+    for (uint32_t r = t; r < L; r += blockDim.x) {
+        if (d2s[r] <= lim) {
+            const uint32_t k = atomicAdd(&near_cnt[q], 1u);
+            if (k < NEAR_K) near[(uint64_t)q * NEAR_K + k] = NearEntry{perm[ws + r], ws + r, d2s[r], 0};
+        }
+    }
+}
+
+void launch_window(const isax_index *ix, uint32_t Q, const uint32_t *qmap, float delta, cudaStream_t s) {
+    const QueryScratch &qs = ix->qs;
+    const float onepd = 1.0f + delta;
+    const uint32_t ns = (ix->n + 127) / 128;
+#define WIN_CASE(K)                                                                                          \
+    case K:                                                                                                  \
+        window_kernel<K><<<Q, 256, 0, s>>>(ix->stored, ix->perm, ix->n, qs.qy, qs.win, qmap, qs.bsf, qs.near, \
+                                           qs.near_cnt, qs.counters, onepd);                                 \
+        break;
+    switch (ns) {
+        WIN_CASE(1) WIN_CASE(2) WIN_CASE(3) WIN_CASE(4) WIN_CASE(5) WIN_CASE(6) WIN_CASE(7) WIN_CASE(8)
+    }
+#undef WIN_CASE
+}
+
+// ------------------------------------------------------------------------------------ LB dump
+// Debug / parity: LB^2 of a range of sorted positions, accumulated exactly as lbscan does it
+// (fp32, segments 0..15 left to right).
+__global__ void lb_dump_kernel(const uint4 *__restrict__ sax, const float *__restrict__ lut, uint32_t Q,
+                               uint64_t first, uint64_t count, float *__restrict__ out) {
+    const uint32_t q = blockIdx.y;
+    const float *L = lut + (uint64_t)q * W * CARD;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint4 wv = sax[first + i];
+        const uint32_t v[4] = {wv.x, wv.y, wv.z, wv.w};
+        float lb = 0.f;
+#pragma unroll
+        for (int s = 0; s < W; s++) lb += L[s * CARD + ((v[s >> 2] >> (8 * (s & 3))) & 0xFFu)];
+        out[(uint64_t)q * count + i] = lb;
+    }
+}
+
+void launch_lb_dump(const isax_index *ix, uint32_t Q, uint64_t first_pos, uint64_t count, float *out,
+                    cudaStream_t s) {
+    if (!count || !Q) return;
+    const dim3 grid((unsigned)umin64((count + 255) / 256, 1184), Q);
+    lb_dump_kernel<<<grid, 256, 0, s>>>(reinterpret_cast<const uint4 *>(ix->sax), ix->qs.lut, Q, first_pos, count,
+                                        out);
+}
+
+}  // namespace isax

@@ -1,0 +1,177 @@
+// refine.cu: early-abandoning real distances over the candidate lists, then the exact finalise.
+//
+// "a number of real distance calculation workers consume [the candidate list] in
+// parallel and compute the real distances". P:357: "we may find a series with a smaller
+// distance to the query, in which case we update the BSF". north_star (b): "refinement with
+// early-abandoning squared Euclidean distance and an atomically shrinking BSF".
+//
+// refine_kernel: one warp per candidate. Candidates from every query of the batch are one
+//   flat index space (a prefix over the per-query counts, in shared memory), so a single
+//   launch reaches steady state. For each candidate:
+//   - it reads the current BSF of its query (relaxed: a stale value is only looser);
+//   - it streams the row in 512-byte steps (float4 per lane);
+//   - after each step but the last, it abandons iff the partial sum > bsf * (1 + delta) (R8);
+//   - on completion it does atomicMin on the packed (d^2, id) word, and appends (id, pos, d^2)
+//     to the near list if d^2 <= bsf * (1 + delta) (R9).
+// finalize_kernel: one warp per query. Near-list entries within (1 + delta) of the final BSF
+//   are recomputed in fp64, in one fixed order for every row. The answer is the
+//   lexicographic min of (d^2_fp64, id) (lowest id on ties; north_star). dist = fp32(sqrt(d^2)).
+#include "isax_device.cuh"
+
+namespace isax {
+
+constexpr int RF_THREADS = 256;
+constexpr int RF_MAXQ = 1024;
+
+template <int NS>
+__global__ void __launch_bounds__(RF_THREADS) refine_kernel(const float *__restrict__ stored,
+                                                           const uint32_t *__restrict__ perm, uint32_t n,
+                                                           const float *__restrict__ qy, uint32_t Q,
+                                                           const uint32_t *__restrict__ cand,
+                                                           const uint32_t *__restrict__ cand_cnt, uint32_t cap,
+                                                           unsigned long long *__restrict__ bsf,
+                                                           NearEntry *__restrict__ near, uint32_t *__restrict__ near_cnt,
+                                                           uint32_t *__restrict__ counters, float onepd) {
+    __shared__ uint32_t pre[RF_MAXQ + 1];
+    const uint32_t t = threadIdx.x, lane = t & 31;
+    if (t == 0) {
+        uint32_t run = 0;
+        for (uint32_t q = 0; q < Q; q++) {
+            pre[q] = run;
+            run += min(cand_cnt[q], cap);
+        }
+        pre[Q] = run;
+    }
+    __syncthreads();
+    const uint32_t total = pre[Q];
+    const uint32_t nwarps = gridDim.x * (RF_THREADS / 32);
+    uint32_t cur_q = 0xffffffffu;
+    float4 qv[NS];
+    uint32_t done = 0, abandoned = 0;
+    for (uint32_t f = blockIdx.x * (RF_THREADS / 32) + (t >> 5); f < total; f += nwarps) {
+        uint32_t lo = 0, hi = Q;  // last q with pre[q] <= f
+        while (hi - lo > 1) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (pre[mid] <= f) lo = mid;
+            else hi = mid;
+        }
+        const uint32_t q = lo;
+        if (q != cur_q) {
+            if (cur_q != 0xffffffffu && lane == 0) {
+                atomicAdd(&counters[4 * cur_q + 0], done);
+                atomicAdd(&counters[4 * cur_q + 1], abandoned);
+            }
+            done = abandoned = 0;
+            cur_q = q;
+#pragma unroll
+            for (int k = 0; k < NS; k++) {
+                const uint32_t i = k * 128 + 4 * lane;
+                qv[k] = i < n ? *reinterpret_cast<const float4 *>(qy + (uint64_t)q * n + i) : make_float4(0, 0, 0, 0);
+            }
+        }
+        const uint32_t pos = cand[(uint64_t)q * cap + (f - pre[q])];
+        const float *row = stored + (uint64_t)pos * n;
+        const float lim = bsf_d2(*((volatile unsigned long long *)&bsf[q])) * onepd;
+        float acc = 0.f;
+        bool ab = false;
+#pragma unroll
+        for (int k = 0; k < NS; k++) {
+            const uint32_t i = k * 128 + 4 * lane;
+            if (i < n) {
+                const float4 v = __ldcs(reinterpret_cast<const float4 *>(row + i));
+                float d;
+                d = v.x - qv[k].x; acc = fmaf(d, d, acc);
+                d = v.y - qv[k].y; acc = fmaf(d, d, acc);
+                d = v.z - qv[k].z; acc = fmaf(d, d, acc);
+                d = v.w - qv[k].w; acc = fmaf(d, d, acc);
+            }
+            if (k + 1 < NS && (k + 1) * 128 < n) {
+                if (warp_sum(acc) > lim) {  // early abandon (R8)
+                    ab = true;
+                    break;
+                }
+            }
+        }
+        if (ab) {
+            abandoned++;
+            continue;
+        }
+        const float d2 = warp_sum(acc);
+        done++;
+        if (lane == 0 && d2 <= lim) {
+            const uint32_t id = perm[pos];
+            atomicMin(&bsf[q], pack_bsf(d2, id));
+            const uint32_t k = atomicAdd(&near_cnt[q], 1u);
+            if (k < NEAR_K) near[(uint64_t)q * NEAR_K + k] = NearEntry{id, pos, d2, 0};
+        }
+    }
+    if (cur_q != 0xffffffffu && lane == 0) {
+        atomicAdd(&counters[4 * cur_q + 0], done);
+        atomicAdd(&counters[4 * cur_q + 1], abandoned);
+    }
+}
+
+void launch_refine(const isax_index *ix, uint32_t Q, float delta, cudaStream_t s) {
+    const QueryScratch &qs = ix->qs;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const unsigned grid = sms * 8;
+    const float onepd = 1.0f + delta;
+    const uint32_t ns = (ix->n + 127) / 128;
+#define RF_CASE(K)                                                                                              \
+    case K:                                                                                                     \
+        refine_kernel<K><<<grid, RF_THREADS, 0, s>>>(ix->stored, ix->perm, ix->n, qs.qy, Q, qs.cand, qs.cand_cnt, \
+                                                     qs.cand_cap, qs.bsf, qs.near, qs.near_cnt, qs.counters, onepd); \
+        break;
+    switch (ns) {
+        RF_CASE(1) RF_CASE(2) RF_CASE(3) RF_CASE(4) RF_CASE(5) RF_CASE(6) RF_CASE(7) RF_CASE(8)
+    }
+#undef RF_CASE
+}
+
+// ------------------------------------------------------------------------------------ finalize
+__global__ void __launch_bounds__(32) finalize_kernel(const float *__restrict__ stored, uint32_t n,
+                                                      const float *__restrict__ qy,
+                                                      const unsigned long long *__restrict__ bsf,
+                                                      const NearEntry *__restrict__ near,
+                                                      const uint32_t *__restrict__ near_cnt, float onepd,
+                                                      int64_t *__restrict__ out_id, float *__restrict__ out_dist) {
+    const uint32_t q = blockIdx.x, lane = threadIdx.x;
+    const unsigned long long fin = bsf[q];
+    const float lim = bsf_d2(fin) * onepd;
+    const uint32_t cnt = min(near_cnt[q], (uint32_t)NEAR_K);
+    double best = __longlong_as_double(0x7ff0000000000000ll);  // +inf
+    uint32_t best_id = (uint32_t)(fin & 0xffffffffu);
+    bool have = false;
+    for (uint32_t k = 0; k < cnt; k++) {
+        const NearEntry e = near[(uint64_t)q * NEAR_K + k];
+        if (!(e.d2 <= lim)) continue;
+        const float *row = stored + (uint64_t)e.pos * n;
+        const float *qr = qy + (uint64_t)q * n;
+        double acc = 0.0;
+        for (uint32_t i = lane; i < n; i += 32) {
+            const double d = __dsub_rn((double)qr[i], (double)row[i]);
+            acc = __dadd_rn(acc, __dmul_rn(d, d));
+        }
+        acc = warp_sum_d(acc);
+        if (!have || acc < best || (acc == best && e.id < best_id)) {
+            best = acc;
+            best_id = e.id;
+            have = true;
+        }
+    }
+    if (lane == 0) {
+        out_id[q] = (int64_t)best_id;
+        out_dist[q] = have ? __double2float_rn(sqrt(best)) : sqrtf(bsf_d2(fin));
+    }
+}
+
+void launch_finalize(const isax_index *ix, uint32_t Q, float delta, int64_t *out_id, float *out_dist,
+                     cudaStream_t s) {
+    const QueryScratch &qs = ix->qs;
+    finalize_kernel<<<Q, 32, 0, s>>>(ix->stored, ix->n, qs.qy, qs.bsf, qs.near, qs.near_cnt, 1.0f + delta, out_id,
+                                     out_dist);
+}
+
+}  // namespace isax

@@ -1,0 +1,111 @@
+// summarise.cu: build pass 1, z-norm -> PAA -> SAX -> 128-bit key, one series per thread.
+//
+// Method: P:168 (PAA, iSAX symbols); P:213-222 / P:293-296 (bulk summarisation by the index
+// workers); P:216-217 (root subtree = the first bit of each segment). Readings R2-R4 and R6
+// (DESIGN.md).
+//
+// Precision (R3): mu, sigma and each PAA mean are fp64 sums taken strictly left to right over
+// the points of one series, with no FMA contraction (explicit __d*_rn intrinsics). That is the
+// plain definition, so the words match the oracle bit for bit, independent of launch shape.
+// The order of a sum is per series, so each thread owns one series, and a warp stages its 32
+// rows in shared memory with coalesced 512-byte loads. The stride is padded to n+1 words, so
+// the per-thread sequential reads are bank-conflict free (bank = (lane + i) mod 32).
+//
+// Roofline: 4n bytes read + 16 (word) + 16 (key) + 16 (mu, sigma) bytes written per series;
+// ~4n fp64 ops. HBM-bound at n=256 if fp64 latency chains are hidden by enough warps (6 per SM).
+#include "isax_device.cuh"
+
+namespace isax {
+
+#include "breakpoints.inc"
+
+__constant__ double c_beta[ISAX_NBETA] = ISAX_BETA_INIT;
+
+__global__ void __launch_bounds__(32) summarise_kernel(const float *__restrict__ x, uint64_t count, uint32_t n,
+                                                         uint64_t id0, uint8_t *__restrict__ sax_by_id,
+                                                         uint4 *__restrict__ key, double2 *__restrict__ musig,
+                                                         uint32_t *__restrict__ bad) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    double *beta = reinterpret_cast<double *>(smem_raw);
+    float *rows = reinterpret_cast<float *>(smem_raw + ISAX_NBETA * sizeof(double) + 8);
+    const uint32_t lane = threadIdx.x;
+    const uint32_t stride = n + 1;
+    for (uint32_t k = lane; k < ISAX_NBETA; k += 32) beta[k] = c_beta[k];
+    const uint32_t seg = n / W;
+    const uint64_t ngroups = (count + 31) / 32;
+    for (uint64_t g = blockIdx.x; g < ngroups; g += gridDim.x) {
+        const uint64_t r0 = g * 32;
+        const uint32_t nrows = (uint32_t)umin64(32, count - r0);
+        __syncwarp();
+        // stage: each instruction reads 512 contiguous bytes of one row
+        for (uint32_t r = 0; r < nrows; r++) {
+            const float4 *src = reinterpret_cast<const float4 *>(x + (r0 + r) * n);
+#pragma unroll 4
+            for (uint32_t i = lane; i < n / 4; i += 32) {
+                float4 v = __ldcs(src + i);
+                float *d = rows + r * stride + 4 * i;
+                d[0] = v.x; d[1] = v.y; d[2] = v.z; d[3] = v.w;
+            }
+        }
+        __syncwarp();
+        if (lane < nrows) {
+            float *row = rows + lane * stride;
+            // C1: mu and sigma, left to right (R2, R3)
+            double s = 0.0;
+            bool finite = true;
+            for (uint32_t i = 0; i < n; i++) {
+                float v = row[i];
+                finite &= isfinite(v);
+                s = __dadd_rn(s, (double)v);
+            }
+            const double mu = __ddiv_rn(s, (double)n);
+            double s2 = 0.0;
+            for (uint32_t i = 0; i < n; i++) {
+                double t = __dsub_rn((double)row[i], mu);
+                s2 = __dadd_rn(s2, __dmul_rn(t, t));
+            }
+            const double sd = __dsqrt_rn(__ddiv_rn(s2, (double)n));
+            const bool flat = sd < 1e-12;
+            for (uint32_t i = 0; i < n; i++)
+                row[i] = flat ? 0.0f : __double2float_rn(__ddiv_rn(__dsub_rn((double)row[i], mu), sd));
+            // C2 + C4: PAA means (left to right per segment) and symbols
+            uint32_t sym[W];
+#pragma unroll
+            for (int sg = 0; sg < W; sg++) {
+                double acc = 0.0;
+                for (uint32_t j = 0; j < seg; j++) acc = __dadd_rn(acc, (double)row[sg * seg + j]);
+                sym[sg] = sax_symbol(beta, __ddiv_rn(acc, (double)seg));
+            }
+            const uint64_t id = id0 + r0 + lane;
+            uint4 wv;
+            wv.x = sym[0] | (sym[1] << 8) | (sym[2] << 16) | (sym[3] << 24);
+            wv.y = sym[4] | (sym[5] << 8) | (sym[6] << 16) | (sym[7] << 24);
+            wv.z = sym[8] | (sym[9] << 8) | (sym[10] << 16) | (sym[11] << 24);
+            wv.w = sym[12] | (sym[13] << 8) | (sym[14] << 16) | (sym[15] << 24);
+            reinterpret_cast<uint4 *>(sax_by_id)[id] = wv;
+            key[id] = isax_key(sym);
+            musig[id] = make_double2(mu, sd);
+            if (!finite) atomicOr(bad, 1u);
+        }
+    }
+}
+
+void launch_summarise(const float *x, uint64_t count, uint32_t n, uint64_t id0, uint8_t *sax_by_id, uint4 *key,
+                      double2 *musig, uint32_t *bad, cudaStream_t s) {
+    if (count == 0) return;
+    const size_t smem = ISAX_NBETA * sizeof(double) + 8 + 32 * (size_t)(n + 1) * sizeof(float);
+    static size_t configured = 0;
+    if (smem > configured) {
+        cudaFuncSetAttribute(summarise_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        configured = smem;
+    }
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int per_sm = (int)std::max<size_t>(1, std::min<size_t>(16, (227 * 1024) / (smem + 1024)));
+    const uint64_t groups = (count + 31) / 32;
+    const uint64_t grid = umin64(groups, (uint64_t)sms * per_sm);
+    summarise_kernel<<<(unsigned)grid, 32, smem, s>>>(x, count, n, id0, sax_by_id, key, musig, bad);
+}
+
+}  // namespace isax

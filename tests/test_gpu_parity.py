@@ -1,0 +1,182 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the oracle on the same seeded bytes.
+
+Bars:
+* iSAX words, the permutation and the stored z-normalised rows: bit-exact.
+* query PAA and word: bit-exact; LB^2: within the fp32 summation bound of the fp64 oracle.
+* NN ids: exact (ties to the lowest id); distances within 1e-5 relative (north_star).
+Sizes span many tiles and a ragged tail; edge cases cover N = 1, N < window, duplicates,
+constant series, exact-copy queries, overflow rounds and batch splitting.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import datagen  # noqa: E402
+from oracle import clib, ref  # noqa: E402
+from paper_2009_01614_b200 import isax  # noqa: E402
+from tests.gpu_util import assert_nn_parity, oracle_nn1, small_workload  # noqa: E402
+
+
+def _build(x, **opts):
+    return isax.Index.build(x, **opts)
+
+
+@pytest.mark.parametrize("N,n,kind", [(100_000, 256, "walk"), (12_345, 128, "walk"), (4_099, 64, "sines"), (1, 256, "walk")])
+def test_summaries_perm_and_rows_bit_exact(N, n, kind):
+    wl = small_workload(N, n, kind)
+    x = datagen.series(wl, 0, N)
+    xh = x.cpu().numpy()
+    with _build(x) as ix:
+        ex = ix.export(0, N, sax=True, perm=True, stored=True)
+    y, mu, sd, m, word = clib.summarise(xh)
+    np.testing.assert_array_equal(ex["sax"], word)  # C4 words, by id
+    perm = ref.canonical_order(word)  # C5
+    np.testing.assert_array_equal(ex["perm"].astype(np.int64), perm)
+    np.testing.assert_array_equal(ex["stored"], y[perm])  # C1 rows, in sorted order
+
+
+@pytest.mark.parametrize("N,n", [(100_000, 256), (9_999, 128)])
+def test_query_summary_lb_and_window(N, n):
+    wl = small_workload(N, n, Q=16)
+    x = datagen.series(wl, 0, N)
+    q, _ = datagen.queries(wl)
+    xh, qh = x.cpu().numpy(), q.cpu().numpy()
+    with _build(x) as ix:
+        ex = ix.export(0, N, sax=True, perm=True)
+        dbg = ix.query_debug(qh, 0, N)
+    _, _, _, qm, qw = clib.summarise(qh)
+    np.testing.assert_array_equal(dbg["q_paa"], qm)
+    np.testing.assert_array_equal(dbg["q_sax"], qw)
+    words_sorted = ex["sax"][ex["perm"]]
+    hi, lo = ref.isax_keys(words_sorted)
+    qhi, qlo = ref.isax_keys(qw)
+    for i in range(len(qh)):
+        lb_or = ref.lb2(qm[i], words_sorted, n)  # C6, fp64
+        lb_gpu = dbg["lb2"][i].astype(np.float64)
+        # fp32 sum of 16 rounded-down terms: never above the fp64 bound beyond summation error
+        assert np.all(lb_gpu <= lb_or * (1 + 2e-6) + 1e-30)
+        assert np.all(lb_gpu >= lb_or * (1 - 1e-5) - 1e-6)
+        pos = ref.lower_bound_pos(hi, lo, qhi[i], qlo[i])
+        assert tuple(dbg["win"][i]) == ref.window(pos, N, 1024)
+
+
+@pytest.mark.parametrize("N,n,kind,q_noisy", [(100_000, 256, "walk", 0), (100_000, 256, "walk", 8),
+                                              (20_000, 256, "sines", 16), (7_777, 128, "walk", 4)])
+def test_nn1_matches_oracle(N, n, kind, q_noisy):
+    wl = small_workload(N, n, kind, Q=16, q_noisy=q_noisy, sigma=0.1)
+    x = datagen.series(wl, 0, N)
+    q, src = datagen.queries(wl)
+    xh, qh = x.cpu().numpy(), q.cpu().numpy()
+    ids_or, dist_or, _ = oracle_nn1(xh, qh)
+    with _build(x) as ix:
+        ids, dist = ix.nn1(q)  # device path (isax_nn1_async)
+        st = ix.stats()
+        ids_h, dist_h = ix.nn1(qh)  # host path (isax_nn1)
+    assert_nn_parity(ids.cpu().numpy(), dist.cpu().numpy(), ids_or, dist_or)
+    np.testing.assert_array_equal(ids_h.numpy(), ids.cpu().numpy())
+    np.testing.assert_array_equal(dist_h.numpy(), dist.cpu().numpy())
+    for j in range(len(qh)):
+        w0, w1 = st["window"][2 * j], st["window"][2 * j + 1]
+        assert st["candidates"][j] + (w1 - w0) <= N
+        assert st["refined"][j] + st["abandoned"][j] >= (w1 - w0)
+
+
+def test_ties_duplicates_constants_and_exact_copies():
+    N, n = 5_000, 256
+    wl = small_workload(N, n, Q=8)
+    x = datagen.series(wl, 0, N).clone()
+    x[4000] = x[17]  # exact duplicate: the tie must resolve to id 17
+    x[4001] = x[17] * 3.0 + 2.0  # same shape after z-norm (up to rounding)
+    x[10] = 1.5  # constant series -> all-zero row
+    x[4002] = -7.0
+    q, _ = datagen.queries(wl)
+    q = q.clone()
+    q[0] = x[4000]
+    q[1] = x[10] + 1.0  # constant query -> the all-zero row; ties between ids 10 and 4002 -> 10
+    q[2] = x[123]
+    xh, qh = x.cpu().numpy(), q.cpu().numpy()
+    ids_or, dist_or, _ = oracle_nn1(xh, qh)
+    with _build(x) as ix:
+        ids, dist = ix.nn1(q)
+    ids, dist = ids.cpu().numpy(), dist.cpu().numpy()
+    assert_nn_parity(ids, dist, ids_or, dist_or)
+    assert ids[0] == 17 and dist[0] == 0.0
+    assert ids[1] == 10 and dist[1] == 0.0
+    assert ids[2] == 123 and dist[2] == 0.0
+
+
+@pytest.mark.parametrize("opts", [dict(window_L=1), dict(window_L=4096), dict(cand_cap=7), dict(batch_Q=3),
+                                  dict(slack_log2=-20)])
+def test_options_do_not_change_answers(opts):
+    N, n = 30_000, 256
+    wl = small_workload(N, n, Q=12, q_noisy=4)
+    x = datagen.series(wl, 0, N)
+    q, _ = datagen.queries(wl)
+    ids_or, dist_or, _ = oracle_nn1(x.cpu().numpy(), q.cpu().numpy())
+    with _build(x, **opts) as ix:
+        ids, dist = ix.nn1(q)
+        st = ix.stats()
+    assert_nn_parity(ids.cpu().numpy(), dist.cpu().numpy(), ids_or, dist_or)
+    if "cand_cap" in opts:
+        assert max(st["rounds"]) >= 2  # overflow rounds were exercised
+
+
+def test_tiny_collections():
+    for N in (1, 2, 3, 31, 33, 1023, 1025):
+        wl = small_workload(N, 64, Q=5, seed=N)
+        x = datagen.series(wl, 0, N)
+        q, _ = datagen.queries(wl)
+        ids_or, dist_or, _ = oracle_nn1(x.cpu().numpy(), q.cpu().numpy())
+        with _build(x) as ix:
+            ids, dist = ix.nn1(q)
+        assert_nn_parity(ids.cpu().numpy(), dist.cpu().numpy(), ids_or, dist_or)
+
+
+def test_streamed_build_equals_device_build():
+    N, n = 50_000, 256
+    wl = small_workload(N, n)
+    x = datagen.series(wl, 0, N)
+    fptr, ctx = datagen.fill_callback(wl)
+    with _build(x) as a, isax.Index.build_stream(N, n, fptr, ctx, chunk=7_000) as b:
+        ea = a.export(0, N, sax=True, perm=True, stored=True)
+        eb = b.export(0, N, sax=True, perm=True, stored=True)
+    for k in ea:
+        np.testing.assert_array_equal(ea[k], eb[k])
+    with isax.Index.build(x.cpu().numpy()) as c:  # host pointer -> chunked H2D path
+        ec = c.export(0, N, sax=True, perm=True, stored=True)
+    for k in ea:
+        np.testing.assert_array_equal(ea[k], ec[k])
+
+
+def test_errors():
+    x = torch.zeros((10, 256), device="cuda")
+    with pytest.raises(isax.IsaxError) as e:
+        isax.Index.build(x[:0])
+    assert e.value.name == "ISAX_E_EMPTY"
+    with pytest.raises(isax.IsaxError) as e:
+        isax.Index.build(torch.zeros((10, 250), device="cuda"))
+    assert e.value.name == "ISAX_E_INVAL"
+    with pytest.raises(isax.IsaxError) as e:
+        isax.Index.build(x, card=3)
+    assert e.value.name == "ISAX_E_INVAL"
+    with pytest.raises(isax.IsaxError) as e:
+        isax.Index.build(x, w=8)
+    assert e.value.name == "ISAX_E_UNSUPPORTED"
+    bad = torch.randn((100, 256), device="cuda")
+    bad[37, 5] = float("nan")
+    with pytest.raises(isax.IsaxError) as e:
+        isax.Index.build(bad)
+    assert e.value.name == "ISAX_E_NONFINITE"
+    with isax.Index.build(torch.randn((100, 256), device="cuda").cumsum(1)) as ix:
+        q = torch.randn((3, 256), device="cuda")
+        q[1, 0] = float("inf")
+        with pytest.raises(isax.IsaxError) as e:
+            ix.nn1(q)
+        assert e.value.name == "ISAX_E_NONFINITE"
+        ids, dist = ix.nn1(torch.zeros((0, 256), device="cuda"))
+        assert ids.numel() == 0
