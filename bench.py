@@ -210,7 +210,7 @@ def main():
     clk = ClockSampler(local)
     clk.start()
     time.sleep(0.3)
-    lb_ms, rf_ms, cand, refined, launches, rounds = [], [], [], [], 0, []
+    lb_ms, rf_ms, cand, refined, launches, rounds, scan_b = [], [], [], [], 0, [], []
     e_start, e_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e_start.record(stream)
     for _ in range(args.steps):
@@ -222,6 +222,7 @@ def main():
         refined.append(sum(st["refined"]))
         rounds.append(max(st["rounds"]))
         launches += st.get("launches", 0)
+        scan_b.append(st["scan_bytes_first_launch"])
     e_end.record(stream)
     torch.cuda.synchronize()
     clocks = clk.stop()
@@ -253,17 +254,16 @@ def main():
     assert (oid.numpy() == ids.cpu().numpy()).all(), "host and device paths disagree"
     # ---- roofline: lbscan (dominant kernel), bytes it must read per launch
     hbm, peak_src = peaks()
-    G = 4
-    groups = math.ceil(min(Q, 128) / G)
     lb_launch_ms = statistics.mean(lb_ms)
     cand_mean = statistics.mean(cand)
-    alg_bytes = 16.0 * wl.N * groups + 4.0 * cand_mean
+    alg_bytes = statistics.mean(scan_b) + 4.0 * cand_mean
     achieved = alg_bytes / (lb_launch_ms / 1e3) / 1e9
-    roofline = {"kernel": "lbscan_kernel<4>", "bound": "hbm", "achieved": round(achieved, 1), "peak": hbm,
+    roofline = {"kernel": "leafscan_kernel<8>", "bound": "hbm", "achieved": round(achieved, 1), "peak": hbm,
                 "unit": "GB/s", "frac": round(achieved / hbm, 4), "traffic": None,
                 "peak_source": peak_src,
                 "bytes_per_launch": alg_bytes,
-                "bytes_rule": f"16 B per summary x N x ceil(Q/G) query groups (G={G} queries share one pass) + 4 B per candidate",
+                "bytes_rule": "32 B node summary per leaf per group of 8 queries + 1 KB of words per surviving leaf "
+                              "(read once per group) + 4 B per candidate written; counted by the kernel",
                 "launch_ms": round(lb_launch_ms, 4), "refine_ms": round(statistics.mean(rf_ms), 4),
                 "lookups_per_s": 16.0 * wl.N * min(Q, 128) / (lb_launch_ms / 1e3)}
     out = {

@@ -45,8 +45,13 @@ typedef struct isax_opts {
     int32_t slack_log2;  /* prune/abandon slack delta = 2^slack_log2 (R8). Default -12. */
     uint32_t batch_Q;    /* queries processed per device batch. Default 128. */
     uint32_t cand_cap;   /* candidate-list capacity per query per round. Default 1<<20. Overflow runs more rounds. */
-    uint32_t flags;      /* reserved, must be 0 */
+    uint32_t flags;      /* ISAX_FLAG_* bits; 0 = defaults */
 } isax_opts;
+
+/* opts.flags: scan every summary with no leaf pruning (the ParIS flat scan) instead
+ * of the default leaf-pruned scan (MESSI's node pruning). The answers are identical;
+ * this exists for A/B measurement. */
+#define ISAX_FLAG_FLAT_SCAN 1u
 
 typedef struct isax_index isax_index; /* opaque; owns all of its device memory */
 

@@ -59,7 +59,7 @@ static int check_geometry(uint64_t N, uint32_t n, uint32_t w, uint32_t card, con
     if (o.window_L == 0 || o.window_L > 4096) return set_error(ISAX_E_INVAL, "window_L must be in [1, 4096]");
     if (o.slack_log2 > -8 || o.slack_log2 < -20) return set_error(ISAX_E_INVAL, "slack_log2 must be in [-20, -8]");
     if (o.batch_Q > 1024) return set_error(ISAX_E_INVAL, "batch_Q must be <= 1024");
-    if (o.flags) return set_error(ISAX_E_INVAL, "flags must be 0");
+    if (o.flags & ~ISAX_FLAG_FLAT_SCAN) return set_error(ISAX_E_INVAL, "unknown flags");
     return ISAX_OK;
 }
 
@@ -74,7 +74,7 @@ static void free_scratch(isax_index *ix) {
     QueryScratch &q = ix->qs;
     cudaFree(q.qy); cudaFree(q.qpaa); cudaFree(q.qsax); cudaFree(q.lut); cudaFree(q.win); cudaFree(q.bsf);
     cudaFree(q.cand); cudaFree(q.cand_cnt); cudaFree(q.near); cudaFree(q.near_cnt); cudaFree(q.qmap); cudaFree(q.qrange);
-    cudaFree(q.counters);
+    cudaFree(q.counters); cudaFree(q.counters_leaf); cudaFree(q.leaf_loads);
     if (q.h_cnt) cudaFreeHost(q.h_cnt);
     q = QueryScratch{};
 }
@@ -101,6 +101,8 @@ static int alloc_scratch(isax_index *ix) {
     A(qmap, Q);
     A(qrange, (size_t)Q * 2);
     A(counters, (size_t)Q * 4);
+    A(counters_leaf, Q);
+    A(leaf_loads, 1);
 #undef A
     if (e == cudaSuccess) e = cudaMallocHost(&q.h_cnt, sizeof(uint32_t) * (size_t)Q * 8);
     if (e != cudaSuccess) {
@@ -147,7 +149,7 @@ static int build_impl(const Source &src, uint64_t N, uint32_t n, uint32_t w, uin
         cudaStreamSynchronize(s);
         cudaFree(sax_by_id); cudaFree(keys); cudaFree(musig); cudaFree(ids); cudaFree(bad); cudaFree(inv);
         cudaFree(stage);
-        cudaFree(ix->stored); cudaFree(ix->sax); cudaFree(ix->perm);
+        cudaFree(ix->stored); cudaFree(ix->sax); cudaFree(ix->perm); cudaFree(ix->lmeta);
         delete ix;
         cudaStreamDestroy(s);
         return code;
@@ -197,6 +199,8 @@ static int build_impl(const Source &src, uint64_t N, uint32_t n, uint32_t w, uin
     ids = nullptr;
     TRY(dmalloc(&ix->sax, N * W, &ix->device_bytes));
     launch_gather_sax(sax_by_id, ix->perm, N, ix->sax, s);
+    TRY(dmalloc(&ix->lmeta, ((N + 63) / 64) * 32, &ix->device_bytes));
+    launch_leaf_meta(ix->sax, N, ix->lmeta, s);
     TRY(cudaStreamSynchronize(s));
     cudaFree(sax_by_id);
     sax_by_id = nullptr;
@@ -235,8 +239,12 @@ static int nn1_device(isax_index *ix, const float *d_q, uint32_t Q, int64_t *d_i
     ix->st_abandoned.assign(Q, 0);
     ix->st_rounds.assign(Q, 0);
     ix->st_near.assign(Q, 0);
+    ix->st_leaves.assign(Q, 0);
+    ix->st_bsf0.assign(Q, 0.f);
     ix->st_ms = StageTimes{};
     ix->st_launches = 0;
+    ix->st_scan_bytes = ix->st_scan_bytes_first = 0;
+    ISAX_CUDA(cudaMemsetAsync(qs.leaf_loads, 0, sizeof(unsigned long long), s));
     // a device flag for non-finite queries
     uint32_t *flag = nullptr;
     ISAX_CUDA(cudaMalloc(&flag, sizeof(uint32_t)));
@@ -248,9 +256,12 @@ static int nn1_device(isax_index *ix, const float *d_q, uint32_t Q, int64_t *d_i
         const bool timed = b0 == 0;
         if (timed) cudaEventRecord(ix->ev[0], s);
         launch_qprep(ix, d_q + (uint64_t)b0 * ix->n, B, s, flag);
+        ISAX_CUDA(cudaMemsetAsync(qs.counters_leaf, 0, B * sizeof(uint32_t), s));
         ix->st_launches += 2;
         if (timed) cudaEventRecord(ix->ev[1], s);
         launch_window(ix, B, nullptr, delta, s);
+        std::vector<unsigned long long> bsf_pk(B);
+        ISAX_CUDA(cudaMemcpyAsync(bsf_pk.data(), qs.bsf, B * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
         if (timed) cudaEventRecord(ix->ev[2], s);
         // Rounds (R10). Round 0 scans every position for every query. A query whose candidate
         // list overflowed in range [a, b) gets that range split into pieces that fit, and the
@@ -291,7 +302,7 @@ static int nn1_device(isax_index *ix, const float *d_q, uint32_t Q, int64_t *d_i
             }
             ISAX_CUDA(cudaMemcpyAsync(qs.qmap, hmap.data(), nact * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
             ISAX_CUDA(cudaMemcpyAsync(qs.qrange, hrange.data(), 2 * nact * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
-            launch_lbscan(ix, nact, qs.qmap, qs.qrange, lo, hi, delta, s);
+            ix->st_scan_bytes += launch_lbscan(ix, nact, qs.qmap, qs.qrange, lo, hi, delta, s);
             if (timed && round == 0) cudaEventRecord(ix->ev[3], s);
             launch_refine(ix, B, delta, s);
             ix->st_launches += 2;
@@ -301,6 +312,11 @@ static int nn1_device(isax_index *ix, const float *d_q, uint32_t Q, int64_t *d_i
             ISAX_CUDA(cudaMemcpyAsync(qs.h_cnt + qs.cap_Q, qs.near_cnt, B * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
             ISAX_CUDA(cudaMemcpyAsync(qs.h_cnt + 2 * qs.cap_Q, flag, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
             ISAX_CUDA(cudaStreamSynchronize(s));
+            if (b0 == 0 && round == 0) {
+                unsigned long long ll = 0;
+                ISAX_CUDA(cudaMemcpy(&ll, qs.leaf_loads, sizeof ll, cudaMemcpyDeviceToHost));
+                ix->st_scan_bytes_first = ix->st_scan_bytes + 1024ull * ll;
+            }
             if (qs.h_cnt[2 * qs.cap_Q]) {
                 result = set_error(ISAX_E_NONFINITE, "a query holds NaN or Inf");
                 break;
@@ -336,11 +352,16 @@ static int nn1_device(isax_index *ix, const float *d_q, uint32_t Q, int64_t *d_i
         ISAX_CUDA(cudaMemcpyAsync(tmp.data(), qs.counters, tmp.size() * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
         std::vector<uint32_t> tw((size_t)B * 2);
         ISAX_CUDA(cudaMemcpyAsync(tw.data(), qs.win, tw.size() * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+        std::vector<uint32_t> tl(B);
+        ISAX_CUDA(cudaMemcpyAsync(tl.data(), qs.counters_leaf, B * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
         ISAX_CUDA(cudaStreamSynchronize(s));
         for (uint32_t i = 0; i < B; i++) {
             ix->st_refined[b0 + i] = tmp[4 * i];
             ix->st_abandoned[b0 + i] = tmp[4 * i + 1];
             ix->st_near[b0 + i] = qs.h_cnt[qs.cap_Q + i];
+            ix->st_leaves[b0 + i] = tl[i];
+            const uint32_t hi32 = (uint32_t)(bsf_pk[i] >> 32);
+            memcpy(&ix->st_bsf0[b0 + i], &hi32, 4);
             ix->st_win[2 * (b0 + i)] = tw[2 * i];
             ix->st_win[2 * (b0 + i) + 1] = tw[2 * i + 1];
         }
@@ -537,7 +558,17 @@ int isax_stats(const isax_index *cix, char *buf, size_t cap) {
     arr("abandoned", ix->st_abandoned, false);
     arr("rounds", ix->st_rounds, false);
     arr("near", ix->st_near, false);
+    arr("leaves_alive", ix->st_leaves, false);
+    j += "\"bsf0_d2\":[";
+    for (size_t i = 0; i < ix->st_bsf0.size(); i++) {
+        char b[32];
+        snprintf(b, sizeof b, "%s%.9g", i ? "," : "", ix->st_bsf0[i]);
+        j += b;
+    }
+    j += "],";
     j += "\"launches\":" + std::to_string(ix->st_launches);
+    j += ",\"scan_bytes\":" + std::to_string(ix->st_scan_bytes);
+    j += ",\"scan_bytes_first_launch\":" + std::to_string(ix->st_scan_bytes_first);
     j += "}";
     if (buf && cap) {
         size_t k = std::min(cap - 1, j.size());
@@ -564,6 +595,7 @@ void isax_free(isax_index *ix) {
         cudaFree(ix->stored);
         cudaFree(ix->sax);
         cudaFree(ix->perm);
+        cudaFree(ix->lmeta);
         free_scratch(ix);
         for (auto &ev : ix->ev)
             if (ev) cudaEventDestroy(ev);

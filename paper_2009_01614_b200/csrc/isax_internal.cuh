@@ -58,6 +58,8 @@ struct QueryScratch {
     uint32_t *qmap = nullptr;       // [Q] active slot -> batch slot, for re-scan rounds
     uint32_t *qrange = nullptr;     // [Q][2] sorted-position range [r0, r1) of each active slot
     uint32_t *counters = nullptr;   // [Q][4]: refined, abandoned, rounds, near_overflow
+    uint32_t *counters_leaf = nullptr;  // [Q]: (leaf, query) pairs that survived the node bound
+    unsigned long long *leaf_loads = nullptr;  // leaves whose 64 words the scan read (all launches of a call)
     uint32_t *h_cnt = nullptr;      // pinned host mirror of cand_cnt + near_cnt + counters
 };
 
@@ -75,13 +77,16 @@ struct isax_index {
     float *stored = nullptr;
     uint8_t *sax = nullptr;
     uint32_t *perm = nullptr;
+    uint8_t *lmeta = nullptr;  // [ceil(N/64)][32]: per-leaf min (16 B) and max (16 B) symbols
     size_t device_bytes = 0;
     isax::QueryScratch qs;
     std::mutex mu;
     // last-call statistics (host copies)
-    std::vector<uint32_t> st_win, st_cand, st_refined, st_abandoned, st_rounds, st_near;
+    std::vector<uint32_t> st_win, st_cand, st_refined, st_abandoned, st_rounds, st_near, st_leaves;
+    std::vector<float> st_bsf0;
     isax::StageTimes st_ms;
     uint64_t st_launches = 0;  // kernels launched by the last nn1 call
+    uint64_t st_scan_bytes = 0, st_scan_bytes_first = 0;  // summary bytes the scan read (all / first launch)
     cudaEvent_t ev[8] = {};
 };
 
@@ -124,8 +129,11 @@ void launch_lb_dump(const isax_index *ix, uint32_t Q, uint64_t first_pos, uint64
 // lbscan.cu
 // Scan sorted positions [lo, hi) for the nq queries qmap[0..nq), each restricted to its own
 // position range qrange[2i], qrange[2i+1] (overflow rounds split a query's range).
-void launch_lbscan(const isax_index *ix, uint32_t nq, const uint32_t *qmap, const uint32_t *qrange, uint32_t lo,
-                   uint32_t hi, float delta, cudaStream_t s);
+void launch_leaf_meta(const uint8_t *sax, uint64_t N, uint8_t *lmeta, cudaStream_t s);
+// Returns the bytes of summaries it reads that the host can count (node summaries or flat
+// words); the leaf scan adds 1 KB per leaf load to qs.leaf_loads on the device.
+uint64_t launch_lbscan(const isax_index *ix, uint32_t nq, const uint32_t *qmap, const uint32_t *qrange, uint32_t lo,
+                       uint32_t hi, float delta, cudaStream_t s);
 // refine.cu
 void launch_refine(const isax_index *ix, uint32_t Q, float delta, cudaStream_t s);
 void launch_finalize(const isax_index *ix, uint32_t Q, float delta, int64_t *out_id, float *out_dist,

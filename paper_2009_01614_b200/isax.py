@@ -76,8 +76,11 @@ def _ptr(a):
     return ctypes.c_void_p(a.data_ptr())
 
 
-def _opts(window_L=0, slack_log2=0, batch_Q=0, cand_cap=0):
-    return Opts(window_L, slack_log2, batch_Q, cand_cap, 0)
+FLAG_FLAT_SCAN = 1  # include/isax.h ISAX_FLAG_FLAT_SCAN
+
+
+def _opts(window_L=0, slack_log2=0, batch_Q=0, cand_cap=0, flags=0):
+    return Opts(window_L, slack_log2, batch_Q, cand_cap, flags)
 
 
 class Index:

@@ -86,6 +86,44 @@ def test_nn1_matches_oracle(N, n, kind, q_noisy):
         assert st["refined"][j] + st["abandoned"][j] >= (w1 - w0)
 
 
+@pytest.mark.parametrize("N,n,kind", [(200_000, 256, "walk"), (50_001, 128, "walk"), (30_000, 256, "sines")])
+def test_candidate_set_is_exactly_the_lb_filter(N, n, kind):
+    """The leaf-pruned scan keeps exactly {pos outside the window : LB^2(pos) <= bsf0^2 (1 + delta)}.
+
+    It is compared with the per-position LB^2 from isax_query_debug (the same fp32 order) and
+    with the flat scan (ISAX_FLAG_FLAT_SCAN). The fp64 oracle LB brackets the count.
+    """
+    wl = small_workload(N, n, kind, Q=12, q_noisy=4 if kind == "walk" else 12, sigma=0.1)
+    x = datagen.series(wl, 0, N)
+    q, _ = datagen.queries(wl)
+    qh = q.cpu().numpy()
+    with _build(x) as ix, _build(x, flags=1) as flat:
+        ids, dist = ix.nn1(q)
+        st = ix.stats()
+        ids_f, dist_f = flat.nn1(q)
+        st_f = flat.stats()
+        dbg = ix.query_debug(qh, 0, N)
+        ex = ix.export(0, N, sax=True, perm=True)
+    np.testing.assert_array_equal(ids.cpu().numpy(), ids_f.cpu().numpy())
+    np.testing.assert_array_equal(dist.cpu().numpy(), dist_f.cpu().numpy())
+    assert st["candidates"] == st_f["candidates"]
+    onepd = np.float32(1 + 2.0**-12)
+    _, _, _, qm, _ = clib.summarise(qh)
+    words_sorted = ex["sax"][ex["perm"]]
+    for i in range(len(qh)):
+        assert st["rounds"][i] == 1
+        T = np.float32(st["bsf0_d2"][i]) * onepd
+        w0, w1 = st["window"][2 * i], st["window"][2 * i + 1]
+        keep = dbg["lb2"][i] <= T
+        keep[w0:w1] = False
+        assert st["candidates"][i] == int(keep.sum())
+        lb_or = ref.lb2(qm[i], words_sorted, n)
+        lb_or[w0:w1] = np.inf
+        assert (lb_or <= T * (1 - 1e-5)).sum() <= st["candidates"][i] <= (lb_or <= T * (1 + 1e-5)).sum()
+        assert st["leaves_alive"][i] <= (N + 63) // 64
+    assert st_f["leaves_alive"] == [0] * len(qh)
+
+
 def test_ties_duplicates_constants_and_exact_copies():
     N, n = 5_000, 256
     wl = small_workload(N, n, Q=8)
