@@ -74,7 +74,7 @@ static void free_scratch(isax_index *ix) {
     QueryScratch &q = ix->qs;
     cudaFree(q.qy); cudaFree(q.qpaa); cudaFree(q.qsax); cudaFree(q.lut); cudaFree(q.win); cudaFree(q.bsf);
     cudaFree(q.cand); cudaFree(q.cand_cnt); cudaFree(q.near); cudaFree(q.near_cnt); cudaFree(q.qmap); cudaFree(q.qrange);
-    cudaFree(q.counters); cudaFree(q.counters_leaf); cudaFree(q.leaf_loads);
+    cudaFree(q.counters); cudaFree(q.counters_leaf); cudaFree(q.leaf_loads); cudaFree(q.task_ctr);
     if (q.h_cnt) cudaFreeHost(q.h_cnt);
     q = QueryScratch{};
 }
@@ -103,6 +103,7 @@ static int alloc_scratch(isax_index *ix) {
     A(counters, (size_t)Q * 4);
     A(counters_leaf, Q);
     A(leaf_loads, 1);
+    A(task_ctr, 1);
 #undef A
     if (e == cudaSuccess) e = cudaMallocHost(&q.h_cnt, sizeof(uint32_t) * (size_t)Q * 8);
     if (e != cudaSuccess) {

@@ -60,6 +60,7 @@ struct QueryScratch {
     uint32_t *counters = nullptr;   // [Q][4]: refined, abandoned, rounds, near_overflow
     uint32_t *counters_leaf = nullptr;  // [Q]: (leaf, query) pairs that survived the node bound
     unsigned long long *leaf_loads = nullptr;  // leaves whose 64 words the scan read (all launches of a call)
+    uint32_t *task_ctr = nullptr;              // work counter of the persistent leaf scan
     uint32_t *h_cnt = nullptr;      // pinned host mirror of cand_cnt + near_cnt + counters
 };
 

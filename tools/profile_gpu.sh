@@ -7,6 +7,6 @@ $CMD > gpurun_out/${tag}_plain.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none -c 5000 --csv --log-file gpurun_out/${tag}_launches.csv $CMD > gpurun_out/${tag}_ncu_launches.log 2>&1
 echo "launches rc=$?"
 $CMD > gpurun_out/${tag}_plain2.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:$kre -s 1 -c 1 -o gpurun_out/${tag}_prof $CMD > gpurun_out/${tag}_ncu_full.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:$kre -s 0 -c 1 -o gpurun_out/${tag}_prof $CMD > gpurun_out/${tag}_ncu_full.log 2>&1
 echo "full rc=$?"
 tail -3 gpurun_out/${tag}_ncu_full.log
