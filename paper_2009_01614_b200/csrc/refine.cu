@@ -111,13 +111,199 @@ __global__ void __launch_bounds__(RF_THREADS) refine_kernel(const float *__restr
     }
 }
 
+// Quarter-warp variant for n <= 256 (the paper's lengths, 128 and 256). Eight lanes own one
+// candidate, so a warp has four rows in flight and each lane streams NH float4 per half-row
+// (512 B per quarter per half at n = 256). The abandon check after the first half reduces over
+// the 8 lanes only (3 xor shuffles). Same arithmetic contract as refine_kernel: fp32 partial
+// sums, abandon iff partial > bsf (1 + delta), packed atomicMin, near list.
+// exclusive prefix of min(cand_cnt[q], cap) over q < Q into pre[0..Q], by the whole CTA
+__device__ __forceinline__ void cand_prefix(const uint32_t *__restrict__ cand_cnt, uint32_t Q, uint32_t cap,
+                                            uint32_t *pre) {
+    __shared__ uint32_t wsum[RF_THREADS / 32];
+    const uint32_t t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    uint32_t carry = 0;
+    for (uint32_t b = 0; b < Q; b += RF_THREADS) {
+        const uint32_t q = b + t;
+        const uint32_t v = q < Q ? min(cand_cnt[q], cap) : 0;
+        uint32_t inc = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t u = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= (uint32_t)o) inc += u;
+        }
+        if (lane == 31) wsum[warp] = inc;
+        __syncthreads();
+        uint32_t wpre = 0, tot = 0;
+        for (uint32_t w = 0; w < RF_THREADS / 32; w++) {
+            if (w < warp) wpre += wsum[w];
+            tot += wsum[w];
+        }
+        if (q < Q) pre[q] = carry + wpre + inc - v;
+        carry += tot;
+        __syncthreads();
+    }
+    if (t == 0) pre[Q] = carry;
+    __syncthreads();
+}
+
+// Quarter-warp variant for n <= 256 (the paper's lengths, 128 and 256). Eight lanes own a
+// candidate and keep two candidates in flight: both first halves are loaded before either is
+// reduced, which gives each lane 2 NH float4 outstanding. At n = 256 that is 1 KB per quarter
+// and 4 KB per warp. The abandon check after the first half reduces over the quarter's 8 lanes
+// (3 xor shuffles). The query row is read through the read-only path (L1-resident).
+// The BSF threshold is refreshed from L2 every RF_REFRESH candidates; a stale value is only
+// looser. Same arithmetic contract as refine_kernel.
+constexpr uint32_t RF_REFRESH = 4;
+
+template <int NH>
+__global__ void __launch_bounds__(RF_THREADS) refine_q_kernel(const float *__restrict__ stored,
+                                                             const uint32_t *__restrict__ perm, uint32_t n,
+                                                             const float *__restrict__ qy, uint32_t Q,
+                                                             const uint32_t *__restrict__ cand,
+                                                             const uint32_t *__restrict__ cand_cnt, uint32_t cap,
+                                                             unsigned long long *__restrict__ bsf,
+                                                             NearEntry *__restrict__ near,
+                                                             uint32_t *__restrict__ near_cnt,
+                                                             uint32_t *__restrict__ counters, float onepd) {
+    __shared__ uint32_t pre[RF_MAXQ + 1];
+    const uint32_t t = threadIdx.x, lane = t & 31, ql = lane & 7;
+    const uint32_t qmask = 0xFFu << (lane & 24);
+    cand_prefix(cand_cnt, Q, cap, pre);
+    const uint32_t total = pre[Q];
+    const uint32_t nquart = gridDim.x * (RF_THREADS / 8);
+    auto locate = [&](uint32_t f) {  // last q with pre[q] <= f
+        uint32_t lo = 0, hi = Q;
+        while (hi - lo > 1) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (pre[mid] <= f) lo = mid;
+            else hi = mid;
+        }
+        return lo;
+    };
+    uint32_t cur_q = 0xffffffffu, done = 0, abandoned = 0, since = 0;
+    float lim_c = 0.f;
+    // each quarter owns a contiguous range of the flat candidate index: consecutive candidates
+    // share a query (its counters are flushed only when the query changes) and sit close together
+    // in the sorted order
+    const uint32_t per = (total + nquart - 1) / nquart;
+    const uint32_t qi = (blockIdx.x * RF_THREADS + t) >> 3;
+    const uint32_t fbeg = min(qi * per, total), fend = min(fbeg + per, total);
+    for (uint32_t f0 = fbeg; f0 < fend; f0 += 2) {
+        uint32_t qv[2], pv[2];
+        bool live[2];
+#pragma unroll
+        for (int c = 0; c < 2; c++) {
+            const uint32_t f = f0 + c;
+            live[c] = f < fend;
+            qv[c] = live[c] ? locate(f) : 0;
+            pv[c] = live[c] ? cand[(uint64_t)qv[c] * cap + (f - pre[qv[c]])] : 0;
+        }
+        float4 v[2][NH];
+#pragma unroll
+        for (int c = 0; c < 2; c++)
+#pragma unroll
+            for (int k = 0; k < NH; k++)
+                v[c][k] = live[c] ? __ldcs(reinterpret_cast<const float4 *>(stored + (uint64_t)pv[c] * n) + k * 8 + ql)
+                                  : make_float4(0, 0, 0, 0);
+#pragma unroll
+        for (int c = 0; c < 2; c++) {
+            if (!live[c]) continue;
+            const uint32_t q = qv[c], pos = pv[c];
+            if (q != cur_q) {
+                if (cur_q != 0xffffffffu && ql == 0) {
+                    atomicAdd(&counters[4 * cur_q + 0], done);
+                    atomicAdd(&counters[4 * cur_q + 1], abandoned);
+                }
+                done = abandoned = 0;
+                cur_q = q;
+                since = RF_REFRESH;
+            }
+            if (since++ >= RF_REFRESH) {
+                lim_c = bsf_d2(*((volatile unsigned long long *)&bsf[q])) * onepd;
+                since = 1;
+            }
+            const float lim = lim_c;
+            const float4 *qr = reinterpret_cast<const float4 *>(qy + (uint64_t)q * n);
+            float acc = 0.f;
+#pragma unroll
+            for (int k = 0; k < NH; k++) {
+                const float4 w = __ldg(qr + k * 8 + ql);
+                float d;
+                d = v[c][k].x - w.x; acc = fmaf(d, d, acc);
+                d = v[c][k].y - w.y; acc = fmaf(d, d, acc);
+                d = v[c][k].z - w.z; acc = fmaf(d, d, acc);
+                d = v[c][k].w - w.w; acc = fmaf(d, d, acc);
+            }
+            float part = acc;
+            part += __shfl_xor_sync(qmask, part, 1);
+            part += __shfl_xor_sync(qmask, part, 2);
+            part += __shfl_xor_sync(qmask, part, 4);
+            if (part > lim) {  // early abandon after half the row (R8)
+                abandoned++;
+                continue;
+            }
+            const float4 *row = reinterpret_cast<const float4 *>(stored + (uint64_t)pos * n);
+            float4 u[NH];
+#pragma unroll
+            for (int k = 0; k < NH; k++) u[k] = __ldcs(row + 8 * NH + k * 8 + ql);
+#pragma unroll
+            for (int k = 0; k < NH; k++) {
+                const float4 w = __ldg(qr + 8 * NH + k * 8 + ql);
+                float d;
+                d = u[k].x - w.x; acc = fmaf(d, d, acc);
+                d = u[k].y - w.y; acc = fmaf(d, d, acc);
+                d = u[k].z - w.z; acc = fmaf(d, d, acc);
+                d = u[k].w - w.w; acc = fmaf(d, d, acc);
+            }
+            acc += __shfl_xor_sync(qmask, acc, 1);
+            acc += __shfl_xor_sync(qmask, acc, 2);
+            acc += __shfl_xor_sync(qmask, acc, 4);
+            done++;
+            if (acc <= lim) {
+                // re-read the current BSF before claiming a near slot (the cached one may be stale)
+                const float cur = bsf_d2(*((volatile unsigned long long *)&bsf[q])) * onepd;
+                lim_c = cur;
+                if (ql == 0 && acc <= cur) {
+                    const uint32_t id = perm[pos];
+                    atomicMin(&bsf[q], pack_bsf(acc, id));
+                    const uint32_t k = atomicAdd(&near_cnt[q], 1u);
+                    if (k < NEAR_K) near[(uint64_t)q * NEAR_K + k] = NearEntry{id, pos, acc, 0};
+                }
+            }
+        }
+    }
+    if (cur_q != 0xffffffffu && ql == 0) {
+        atomicAdd(&counters[4 * cur_q + 0], done);
+        atomicAdd(&counters[4 * cur_q + 1], abandoned);
+    }
+}
+
 void launch_refine(const isax_index *ix, uint32_t Q, float delta, cudaStream_t s) {
     const QueryScratch &qs = ix->qs;
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const unsigned grid = sms * 8;
     const float onepd = 1.0f + delta;
+    if (ix->n <= 256) {
+        int per_sm = 1;
+        const uint32_t nh = ix->n / 64;
+        if (nh == 4) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, refine_q_kernel<4>, RF_THREADS, 0);
+        else if (nh == 2) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, refine_q_kernel<2>, RF_THREADS, 0);
+        else per_sm = 4;
+        const unsigned grid = sms * std::max(1, per_sm);  // exactly one full wave
+        switch (nh) {
+#define RQ_CASE(K)                                                                                                  \
+    case K:                                                                                                         \
+        refine_q_kernel<K><<<grid, RF_THREADS, 0, s>>>(ix->stored, ix->perm, ix->n, qs.qy, Q, qs.cand, qs.cand_cnt, \
+                                                       qs.cand_cap, qs.bsf, qs.near, qs.near_cnt, qs.counters,      \
+                                                       onepd);                                                      \
+        break;
+            RQ_CASE(1) RQ_CASE(2) RQ_CASE(3) RQ_CASE(4)
+#undef RQ_CASE
+        }
+        return;
+    }
+    const unsigned grid = sms * 8;
     const uint32_t ns = (ix->n + 127) / 128;
 #define RF_CASE(K)                                                                                              \
     case K:                                                                                                     \
