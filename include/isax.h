@@ -46,7 +46,13 @@ typedef struct isax_opts {
     uint32_t batch_Q;    /* queries processed per device batch. Default 128. */
     uint32_t cand_cap;   /* candidate-list capacity per query per round. Default 1<<20. Overflow runs more rounds. */
     uint32_t flags;      /* ISAX_FLAG_* bits; 0 = defaults */
+    uint32_t probe_bits; /* multi-probe approximate answer (R5): refine extra windows at the 2^probe_bits - 1 keys
+                            obtained by flipping the most fragile plane-0/1 key bits. 0 = default 4; max 5;
+                            ISAX_PROBES_NONE = main window only. */
+    uint32_t probe_L;    /* rows per probe window. 0 = default 256. */
 } isax_opts;
+
+#define ISAX_PROBES_NONE 0xFFFFFFFFu
 
 /* opts.flags: scan every summary with no leaf pruning (the ParIS flat scan) instead
  * of the default leaf-pruned scan (MESSI's node pruning). The answers are identical;

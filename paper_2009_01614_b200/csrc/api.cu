@@ -8,6 +8,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <limits>
 #include <string>
 
 #include "isax_internal.cuh"
@@ -37,8 +38,10 @@ static bool is_device_ptr(const void *p) {
 }
 
 static isax_opts default_opts(const isax_opts *o) {
-    isax_opts r{1024, -12, 128, 1u << 20, 0};
+    isax_opts r{1024, -12, 128, 1u << 20, 0, 4, 256};
     if (o) {
+        if (o->probe_bits) r.probe_bits = o->probe_bits;
+        if (o->probe_L) r.probe_L = o->probe_L;
         if (o->window_L) r.window_L = o->window_L;
         if (o->slack_log2) r.slack_log2 = o->slack_log2;
         if (o->batch_Q) r.batch_Q = o->batch_Q;
@@ -60,6 +63,8 @@ static int check_geometry(uint64_t N, uint32_t n, uint32_t w, uint32_t card, con
     if (o.slack_log2 > -8 || o.slack_log2 < -20) return set_error(ISAX_E_INVAL, "slack_log2 must be in [-20, -8]");
     if (o.batch_Q > 1024) return set_error(ISAX_E_INVAL, "batch_Q must be <= 1024");
     if (o.flags & ~ISAX_FLAG_FLAT_SCAN) return set_error(ISAX_E_INVAL, "unknown flags");
+    if (o.probe_bits != ISAX_PROBES_NONE && o.probe_bits > 5) return set_error(ISAX_E_INVAL, "probe_bits must be <= 5");
+    if (o.probe_L == 0 || o.probe_L > 1024) return set_error(ISAX_E_INVAL, "probe_L must be in [1, 1024]");
     return ISAX_OK;
 }
 
@@ -72,8 +77,8 @@ static cudaError_t dmalloc(T **p, size_t count, size_t *acc) {
 
 static void free_scratch(isax_index *ix) {
     QueryScratch &q = ix->qs;
-    cudaFree(q.qy); cudaFree(q.qpaa); cudaFree(q.qsax); cudaFree(q.lut); cudaFree(q.win); cudaFree(q.bsf);
-    cudaFree(q.cand); cudaFree(q.cand_cnt); cudaFree(q.near); cudaFree(q.near_cnt); cudaFree(q.qmap); cudaFree(q.qrange);
+    cudaFree(q.qy); cudaFree(q.qpaa); cudaFree(q.qsax); cudaFree(q.lut); cudaFree(q.win); cudaFree(q.pwin); cudaFree(q.bsf);
+    cudaFree(q.cand); cudaFree(q.cand_cnt); cudaFree(q.near); cudaFree(q.near_cnt); cudaFree(q.qmap); cudaFree(q.qband); cudaFree(q.cand_hist);
     cudaFree(q.counters); cudaFree(q.counters_leaf); cudaFree(q.leaf_loads); cudaFree(q.task_ctr);
     if (q.h_cnt) cudaFreeHost(q.h_cnt);
     q = QueryScratch{};
@@ -93,13 +98,15 @@ static int alloc_scratch(isax_index *ix) {
     A(qsax, (size_t)Q * W);
     A(lut, (size_t)Q * W * CARD);
     A(win, (size_t)Q * 2);
+    A(pwin, (size_t)Q * (MAX_PROBES - 1));
     A(bsf, Q);
     A(cand, (size_t)Q * cap);
     A(cand_cnt, Q);
     A(near, (size_t)Q * NEAR_K);
     A(near_cnt, Q);
     A(qmap, Q);
-    A(qrange, (size_t)Q * 2);
+    A(qband, Q);
+    A(cand_hist, (size_t)Q * HIST_BINS);
     A(counters, (size_t)Q * 4);
     A(counters_leaf, Q);
     A(leaf_loads, 1);
@@ -229,6 +236,13 @@ static int build_impl(const Source &src, uint64_t N, uint32_t n, uint32_t w, uin
 }
 
 // ------------------------------------------------------------------------------------ query
+static float bsf_d2_host(unsigned long long p) {
+    const uint32_t hi = (uint32_t)(p >> 32);
+    float f;
+    memcpy(&f, &hi, 4);
+    return f;
+}
+
 static int nn1_device(isax_index *ix, const float *d_q, uint32_t Q, int64_t *d_id, float *d_dist, cudaStream_t s) {
     int rc = alloc_scratch(ix);
     if (rc) return rc;
@@ -264,32 +278,42 @@ static int nn1_device(isax_index *ix, const float *d_q, uint32_t Q, int64_t *d_i
         std::vector<unsigned long long> bsf_pk(B);
         ISAX_CUDA(cudaMemcpyAsync(bsf_pk.data(), qs.bsf, B * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
         if (timed) cudaEventRecord(ix->ev[2], s);
-        // Rounds (R10). Round 0 scans every position for every query. A query whose candidate
-        // list overflowed in range [a, b) gets that range split into pieces that fit, and the
-        // pieces are scanned in later rounds with the tighter BSF. A query whose near list
-        // overflowed keeps its BSF, empties the near list, re-refines its window and rescans
-        // everything, so the near ties of the final BSF are all collected.
-        std::vector<std::vector<std::pair<uint32_t, uint32_t>>> pending(B);
-        std::vector<uint32_t> hrange(2 * (size_t)B);
-        std::vector<uint32_t> cur_lo(B), cur_hi(B);
-        for (uint32_t i = 0; i < B; i++) pending[i].push_back({0u, (uint32_t)ix->N});
+        // Rounds (R10). Round 0 scans the band (-1, +inf) for every query, i.e. everything
+        // under the window BSF. If a query's candidate list overflows, its band is shrunk to the
+        // largest prefix of its LB histogram that fits, so the smallest bounds are refined first
+        // and the BSF tightens (MESSI's priority-queue order). When a shrunk band
+        // completes, the next band starts where it ended. It is skipped when the BSF has
+        // dropped below it. If a query's near list overflowed, its BSF is kept, the list is
+        // emptied, the window is re-refined and everything is rescanned, so every near tie of
+        // the final BSF is collected.
+        const float onepd = 1.0f + delta;
+        const float INF = std::numeric_limits<float>::infinity();
+        std::vector<float2> band(B, make_float2(-1.0f, INF));
+        std::vector<char> pending(B, 1);
+        std::vector<float> bsf_h(B);
+        std::vector<float2> hband(B);
+        std::vector<uint32_t> hist((size_t)B * HIST_BINS);
+        std::vector<unsigned long long> bsf_now(B);
         std::vector<uint32_t> rewin;
+        bool first = true;
         for (uint32_t round = 0;; round++) {
-            uint32_t nact = 0, lo = 0xffffffffu, hi = 0;
+            if (first) {  // the window result (bsf_pk was copied right after the window kernel)
+                ISAX_CUDA(cudaStreamSynchronize(s));
+                for (uint32_t i = 0; i < B; i++) bsf_h[i] = bsf_d2_host(bsf_pk[i]);
+                first = false;
+            }
+            uint32_t nact = 0;
+            std::vector<float> tused(B, -1.0f);
             for (uint32_t i = 0; i < B; i++) {
-                if (pending[i].empty()) continue;
-                auto r = pending[i].back();
-                pending[i].pop_back();
-                cur_lo[i] = r.first;
-                cur_hi[i] = r.second;
+                if (!pending[i]) continue;
+                pending[i] = 0;
                 hmap[nact] = i;
-                hrange[2 * nact] = r.first;
-                hrange[2 * nact + 1] = r.second;
-                lo = std::min(lo, r.first);
-                hi = std::max(hi, r.second);
+                hband[nact] = band[i];
+                tused[i] = std::fmin(bsf_h[i] * onepd, band[i].y);
                 nact++;
             }
             if (!nact) break;
+            ISAX_CUDA(cudaMemsetAsync(qs.cand_hist, 0, (size_t)B * HIST_BINS * sizeof(uint32_t), s));
             if (round > 0) {
                 ISAX_CUDA(cudaMemsetAsync(qs.cand_cnt, 0, B * sizeof(uint32_t), s));
                 if (!rewin.empty()) {
@@ -302,8 +326,8 @@ static int nn1_device(isax_index *ix, const float *d_q, uint32_t Q, int64_t *d_i
                 }
             }
             ISAX_CUDA(cudaMemcpyAsync(qs.qmap, hmap.data(), nact * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
-            ISAX_CUDA(cudaMemcpyAsync(qs.qrange, hrange.data(), 2 * nact * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
-            ix->st_scan_bytes += launch_lbscan(ix, nact, qs.qmap, qs.qrange, lo, hi, delta, s);
+            ISAX_CUDA(cudaMemcpyAsync(qs.qband, hband.data(), nact * sizeof(float2), cudaMemcpyHostToDevice, s));
+            ix->st_scan_bytes += launch_lbscan(ix, nact, qs.qmap, qs.qband, delta, s);
             if (timed && round == 0) cudaEventRecord(ix->ev[3], s);
             launch_refine(ix, B, delta, s);
             ix->st_launches += 2;
@@ -312,6 +336,7 @@ static int nn1_device(isax_index *ix, const float *d_q, uint32_t Q, int64_t *d_i
             ISAX_CUDA(cudaMemcpyAsync(qs.h_cnt, qs.cand_cnt, B * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
             ISAX_CUDA(cudaMemcpyAsync(qs.h_cnt + qs.cap_Q, qs.near_cnt, B * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
             ISAX_CUDA(cudaMemcpyAsync(qs.h_cnt + 2 * qs.cap_Q, flag, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+            ISAX_CUDA(cudaMemcpyAsync(bsf_now.data(), qs.bsf, B * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
             ISAX_CUDA(cudaStreamSynchronize(s));
             if (b0 == 0 && round == 0) {
                 unsigned long long ll = 0;
@@ -322,20 +347,36 @@ static int nn1_device(isax_index *ix, const float *d_q, uint32_t Q, int64_t *d_i
                 result = set_error(ISAX_E_NONFINITE, "a query holds NaN or Inf");
                 break;
             }
+            bool any_ovf = false;
+            for (uint32_t k = 0; k < nact; k++) any_ovf |= qs.h_cnt[hmap[k]] > qs.cand_cap;
+            if (any_ovf)
+                ISAX_CUDA(cudaMemcpy(hist.data(), qs.cand_hist, hist.size() * sizeof(uint32_t), cudaMemcpyDeviceToHost));
             for (uint32_t k = 0; k < nact; k++) {
                 const uint32_t i = hmap[k];
                 const uint32_t cnt = qs.h_cnt[i];
+                bsf_h[i] = bsf_d2_host(bsf_now[i]);
                 ix->st_cand[b0 + i] += std::min(cnt, qs.cand_cap);
                 ix->st_rounds[b0 + i] = round + 1;
-                if (qs.h_cnt[qs.cap_Q + i] > (uint32_t)NEAR_K) {
-                    pending[i].clear();
-                    pending[i].push_back({0u, (uint32_t)ix->N});
+                if (qs.h_cnt[qs.cap_Q + i] > (uint32_t)NEAR_K) {  // near overflow: start over, BSF kept
+                    band[i] = make_float2(-1.0f, INF);
+                    pending[i] = 1;
                     rewin.push_back(i);
-                } else if (cnt > qs.cand_cap) {
-                    const uint64_t a = cur_lo[i], b = cur_hi[i];
-                    const uint64_t pieces = std::min<uint64_t>(b - a, 2 * ((uint64_t)cnt + qs.cand_cap - 1) / qs.cand_cap);
-                    for (uint64_t p = pieces; p-- > 0;)  // pushed in reverse: scanned in ascending order
-                        pending[i].push_back({(uint32_t)(a + (b - a) * p / pieces), (uint32_t)(a + (b - a) * (p + 1) / pieces)});
+                } else if (cnt > qs.cand_cap) {  // shrink the band to the histogram prefix that fits
+                    const float lo0 = std::fmax(band[i].x, 0.0f), span = tused[i] - lo0;
+                    uint64_t cum = 0;
+                    int kk = -1;
+                    for (uint32_t bb = 0; bb < HIST_BINS; bb++) {
+                        cum += hist[(size_t)i * HIST_BINS + bb];
+                        if (cum > (uint64_t)qs.cand_cap * 9 / 10) break;
+                        kk = (int)bb;
+                    }
+                    band[i].y = lo0 + span * (float)(kk + 1) / (float)HIST_BINS;
+                    if (kk < 0) band[i].y = lo0 + span / (float)HIST_BINS;
+                    pending[i] = 1;
+                } else if (tused[i] == band[i].y && bsf_h[i] * onepd > band[i].y) {
+                    // the band was capped below the BSF: continue with the next band
+                    band[i] = make_float2(band[i].y, INF);
+                    pending[i] = 1;
                 }
             }
             if (round > 100000) {

@@ -20,6 +20,8 @@ namespace isax {
 constexpr int W = 16;        // segments ("w is fixed to 16")
 constexpr int CARD = 256;    // symbols per segment (8 bits)
 constexpr int NEAR_K = 256;  // near-tie list capacity per query (R9)
+constexpr uint32_t MAX_PROBES = 32;  // 2^probe_bits windows per query, probe_bits <= 5
+constexpr uint32_t HIST_BINS = 64;   // per-query histogram of kept LB^2 inside its band (R10)
 
 // Packed BSF: high 32 bits = fp32 bits of d^2 (non-negative, so the bit order is the
 // numeric order), low 32 bits = original id. atomicMin on the packed word is the
@@ -50,13 +52,15 @@ struct QueryScratch {
     uint8_t *qsax = nullptr;        // [Q][16]
     float *lut = nullptr;           // [Q][16][256] fp32, rounded down
     uint32_t *win = nullptr;        // [Q][2] window [start, end)
+    uint32_t *pwin = nullptr;       // [Q][MAX_PROBES-1] probe window starts (probe_L rows each)
     unsigned long long *bsf = nullptr;  // [Q] packed
     uint32_t *cand = nullptr;       // [Q][cand_cap] sorted positions
     uint32_t *cand_cnt = nullptr;   // [Q] (may exceed cand_cap: overflow)
     NearEntry *near = nullptr;      // [Q][NEAR_K]
     uint32_t *near_cnt = nullptr;   // [Q]
     uint32_t *qmap = nullptr;       // [Q] active slot -> batch slot, for re-scan rounds
-    uint32_t *qrange = nullptr;     // [Q][2] sorted-position range [r0, r1) of each active slot
+    float2 *qband = nullptr;        // [Q] LB band (lo, hi] of each active slot (R10)
+    uint32_t *cand_hist = nullptr;  // [Q][HIST_BINS] histogram of kept LB^2 in the band
     uint32_t *counters = nullptr;   // [Q][4]: refined, abandoned, rounds, near_overflow
     uint32_t *counters_leaf = nullptr;  // [Q]: (leaf, query) pairs that survived the node bound
     unsigned long long *leaf_loads = nullptr;  // leaves whose 64 words the scan read (all launches of a call)
@@ -124,17 +128,17 @@ void launch_export_sax(const uint8_t *sax, const uint32_t *inv, uint64_t first_i
                        cudaStream_t s);
 // query.cu
 void launch_qprep(const isax_index *ix, const float *queries, uint32_t Q, cudaStream_t s, uint32_t *bad);
+uint32_t probe_bits(const isax_index *ix);
 void launch_window(const isax_index *ix, uint32_t Q, const uint32_t *qmap, float delta, cudaStream_t s);
 void launch_lb_dump(const isax_index *ix, uint32_t Q, uint64_t first_pos, uint64_t count, float *out,
                     cudaStream_t s);
 // lbscan.cu
-// Scan sorted positions [lo, hi) for the nq queries qmap[0..nq), each restricted to its own
-// position range qrange[2i], qrange[2i+1] (overflow rounds split a query's range).
 void launch_leaf_meta(const uint8_t *sax, uint64_t N, uint8_t *lmeta, cudaStream_t s);
-// Returns the bytes of summaries it reads that the host can count (node summaries or flat
-// words); the leaf scan adds 1 KB per leaf load to qs.leaf_loads on the device.
-uint64_t launch_lbscan(const isax_index *ix, uint32_t nq, const uint32_t *qmap, const uint32_t *qrange, uint32_t lo,
-                       uint32_t hi, float delta, cudaStream_t s);
+// Scan all sorted positions for the nq queries qmap[0..nq), keeping band[i].x < LB^2 <= min(band[i].y,
+// bsf^2 (1+delta)) for slot i. Returns the summary bytes it reads that the host can count (node
+// summaries or flat words); the leaf scan adds its 1 KB leaf loads to qs.leaf_loads on the device.
+uint64_t launch_lbscan(const isax_index *ix, uint32_t nq, const uint32_t *qmap, const float2 *band, float delta,
+                       cudaStream_t s);
 // refine.cu
 void launch_refine(const isax_index *ix, uint32_t Q, float delta, cudaStream_t s);
 void launch_finalize(const isax_index *ix, uint32_t Q, float delta, int64_t *out_id, float *out_dist,

@@ -6,17 +6,17 @@
 // series that are not pruned, are stored in a candidate list". north_star (b): "a full scan of
 // mindist_PAA_iSAX lower bounds over all summaries, compaction of the unpruned candidates".
 //
-// v1 design:
-//  - Each CTA serves a group of G queries. Their fp32 LUTs (16 x 256 x 4 B = 16 KB each) sit
-//    in shared memory, so one pass over the SAX array serves G queries: HBM traffic is
-//    16 B x N per G queries.
-//  - Each thread streams 16-byte words with ld.global.nc.L1::no_allocate (no reuse), U words
-//    in flight per thread.
-//  - LB^2 = sum over segments 0..15, left to right in fp32 (the same order as
-//    isax_query_debug). A position is kept iff LB^2 <= T = bsf^2 * (1 + delta) and it lies
-//    outside the window (R8).
-//  - Compaction: __ballot_sync, then one atomicAdd per warp per query with survivors, then
-//    each kept lane writes its position at base + popc(ballot & lanemask_lt).
+// Keep rule, per query slot (R8, R10): a position p outside the window is a candidate iff
+//     band_lo < LB^2(p) <= T,   T = min(band_hi, bsf^2 (1 + delta))
+// LB^2 is the fp32 sum of LUT[s][sym_s] over s = 0..15, left to right, the same order as
+// isax_query_debug. Round 0 uses band (-1, +inf). When a query's list overflows, the host
+// shrinks band_hi with the per-query LB histogram, so the smallest bounds are refined first
+// (MESSI's priority-queue order, done in LB bands). The next band then starts
+// where the previous one ended.
+//
+// Two kernels:
+//  - lbscan_kernel (ISAX_FLAG_FLAT_SCAN): the ParIS flat scan of every 16-byte word.
+//  - leafscan_kernel (default): MESSI-style node pruning on the sorted array (R11).
 #include "isax_device.cuh"
 
 namespace isax {
@@ -29,6 +29,38 @@ __device__ __forceinline__ uint4 ld_stream(const uint4 *p) {
     return r;
 }
 
+__device__ __forceinline__ uint32_t byte_of(const uint32_t (&v)[4], int s) { return (v[s >> 2] >> (8 * (s & 3))) & 0xFFu; }
+
+// the fp32 LB^2 of one word against one LUT, segments 0..15 left to right
+__device__ __forceinline__ float word_lb(const float *L, const uint4 &wv) {
+    const uint32_t v[4] = {wv.x, wv.y, wv.z, wv.w};
+    float lb = 0.f;
+#pragma unroll
+    for (int s = 0; s < W; s++) lb += L[s * CARD + byte_of(v, s)];
+    return lb;
+}
+
+// histogram bin of a kept bound inside its band (for the host's band shrinking)
+__device__ __forceinline__ uint32_t hist_bin(float lb, float lo, float hi) {
+    const float l0 = fmaxf(lo, 0.f);
+    const float span = hi - l0;
+    const float x = span > 0.f ? __fdividef(lb - l0, span) : 0.f;
+    return min((uint32_t)(fmaxf(x, 0.f) * (float)HIST_BINS), HIST_BINS - 1);
+}
+
+struct __align__(16) QConst {  // per query slot, read with one 16-byte shared load
+    float lo, T;               // band (lo, T]: T = min(band_hi, bsf^2 (1 + delta))
+    uint32_t ws, we;           // window [ws, we): already refined, never a candidate
+};
+
+__device__ __forceinline__ QConst load_qconst(uint32_t qi, bool valid, const unsigned long long *bsf,
+                                              const float2 *band, uint32_t slot, const uint32_t *win, float onepd) {
+    const float2 b = valid ? band[slot] : make_float2(0.f, -1.f);
+    const float tq = valid ? fminf(bsf_d2(bsf[qi]) * onepd, b.y) : -1.0f;  // an invalid slot keeps nothing
+    return QConst{b.x, tq, win[2 * qi], win[2 * qi + 1]};
+}
+
+// ------------------------------------------------------------------------------------ flat scan
 constexpr int LB_THREADS = 256;
 constexpr int LB_U = 4;
 
@@ -36,15 +68,15 @@ template <int G>
 __global__ void __launch_bounds__(LB_THREADS) lbscan_kernel(const uint4 *__restrict__ sax, uint32_t N,
                                                             const float *__restrict__ lut_all,
                                                             const uint32_t *__restrict__ qmap,
-                                                            const uint32_t *__restrict__ qrange, uint32_t nq,
-                                                            uint32_t scan_lo, uint32_t scan_hi,
+                                                            const float2 *__restrict__ band, uint32_t nq,
                                                             const unsigned long long *__restrict__ bsf,
                                                             const uint32_t *__restrict__ win, float onepd,
                                                             uint32_t *__restrict__ cand,
-                                                            uint32_t *__restrict__ cand_cnt, uint32_t cap) {
+                                                            uint32_t *__restrict__ cand_cnt, uint32_t cap,
+                                                            uint32_t *__restrict__ hist) {
     extern __shared__ __align__(16) float slut[];  // [G][16][256]
-    __shared__ float T[G];
-    __shared__ uint32_t ws[G], we[G], r0[G], r1[G], qid[G];
+    __shared__ QConst qc[G];
+    __shared__ uint32_t qid[G];
     const uint32_t t = threadIdx.x, lane = t & 31;
     const uint32_t g0 = blockIdx.y * G;
     for (uint32_t e = t; e < G * W * CARD; e += LB_THREADS) {
@@ -54,44 +86,38 @@ __global__ void __launch_bounds__(LB_THREADS) lbscan_kernel(const uint4 *__restr
     }
     if (t < G) {
         const bool valid = g0 + t < nq;
-        const uint32_t qi = valid ? qmap[g0 + t] : 0;
+        const uint32_t qi = valid ? qmap[g0 + t] : qmap[g0];
         qid[t] = qi;
-        T[t] = valid ? bsf_d2(bsf[qi]) * onepd : -1.0f;  // an invalid slot keeps nothing
-        ws[t] = win[2 * qi];
-        we[t] = win[2 * qi + 1];
-        r0[t] = valid ? qrange[2 * (g0 + t)] : 0;
-        r1[t] = valid ? qrange[2 * (g0 + t) + 1] : 0;
+        qc[t] = load_qconst(qi, valid, bsf, band, g0 + t, win, onepd);
     }
     __syncthreads();
     const uint32_t lt = (1u << lane) - 1u;
     const uint64_t step = (uint64_t)gridDim.x * LB_THREADS * LB_U;
-    for (uint64_t base = scan_lo + (uint64_t)blockIdx.x * LB_THREADS * LB_U; base < scan_hi; base += step) {
+    for (uint64_t base = (uint64_t)blockIdx.x * LB_THREADS * LB_U; base < N; base += step) {
         uint4 wv[LB_U];
 #pragma unroll
         for (int u = 0; u < LB_U; u++) {
             const uint64_t pos = base + u * LB_THREADS + t;
-            wv[u] = pos < scan_hi ? ld_stream(sax + pos) : make_uint4(0, 0, 0, 0);
+            wv[u] = pos < N ? ld_stream(sax + pos) : make_uint4(0, 0, 0, 0);
         }
 #pragma unroll
         for (int u = 0; u < LB_U; u++) {
             const uint32_t pos = (uint32_t)(base + u * LB_THREADS + t);
-            const bool inr = base + u * LB_THREADS + t < scan_hi;
-            const uint32_t v[4] = {wv[u].x, wv[u].y, wv[u].z, wv[u].w};
+            const bool inr = base + u * LB_THREADS + t < N;
 #pragma unroll
             for (int g = 0; g < G; g++) {
-                const float *L = slut + g * W * CARD;
-                float lb = 0.f;
-#pragma unroll
-                for (int s = 0; s < W; s++) lb += L[s * CARD + ((v[s >> 2] >> (8 * (s & 3))) & 0xFFu)];
-                const bool keep = inr && lb <= T[g] && (pos < ws[g] || pos >= we[g]) && pos >= r0[g] && pos < r1[g];
+                const QConst k = qc[g];
+                const float lb = word_lb(slut + g * W * CARD, wv[u]);
+                const bool keep = inr && lb > k.lo && lb <= k.T && (pos < k.ws || pos >= k.we);
                 const uint32_t bal = __ballot_sync(0xffffffffu, keep);
                 if (bal) {
                     uint32_t off = 0;
                     if (lane == 0) off = atomicAdd(&cand_cnt[qid[g]], (uint32_t)__popc(bal));
                     off = __shfl_sync(0xffffffffu, off, 0);
                     if (keep) {
-                        const uint32_t k = off + __popc(bal & lt);
-                        if (k < cap) cand[(uint64_t)qid[g] * cap + k] = pos;
+                        const uint32_t kk = off + __popc(bal & lt);
+                        if (kk < cap) cand[(uint64_t)qid[g] * cap + kk] = pos;
+                        atomicAdd(&hist[qid[g] * HIST_BINS + hist_bin(lb, k.lo, k.T)], 1u);
                     }
                 }
             }
@@ -100,8 +126,8 @@ __global__ void __launch_bounds__(LB_THREADS) lbscan_kernel(const uint4 *__restr
 }
 
 template <int G>
-static void launch_g(const isax_index *ix, uint32_t nq, const uint32_t *qmap, const uint32_t *qrange, uint32_t lo,
-                     uint32_t hi, float onepd, cudaStream_t s) {
+static void launch_g(const isax_index *ix, uint32_t nq, const uint32_t *qmap, const float2 *band, float onepd,
+                     cudaStream_t s) {
     const size_t smem = (size_t)G * W * CARD * sizeof(float);
     static bool configured = false;
     if (!configured) {
@@ -113,44 +139,40 @@ static void launch_g(const isax_index *ix, uint32_t nq, const uint32_t *qmap, co
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const uint32_t groups = (nq + G - 1) / G;
     const int per_sm = std::max(1, (int)((227 * 1024) / (smem + 2048)));
-    const uint64_t tiles = ((uint64_t)(hi - lo) + LB_THREADS * LB_U - 1) / (LB_THREADS * LB_U);
+    const uint64_t tiles = (ix->N + LB_THREADS * LB_U - 1) / (LB_THREADS * LB_U);
     uint64_t gx = ((uint64_t)sms * per_sm + groups - 1) / groups;
     gx = std::max<uint64_t>(1, umin64(gx, tiles));
-    const dim3 grid((unsigned)gx, groups);
     const QueryScratch &qs = ix->qs;
-    lbscan_kernel<G><<<grid, LB_THREADS, smem, s>>>(reinterpret_cast<const uint4 *>(ix->sax), (uint32_t)ix->N, qs.lut,
-                                                   qmap, qrange, nq, lo, hi, qs.bsf, qs.win, onepd, qs.cand,
-                                                   qs.cand_cnt, qs.cand_cap);
+    lbscan_kernel<G><<<dim3((unsigned)gx, groups), LB_THREADS, smem, s>>>(
+        reinterpret_cast<const uint4 *>(ix->sax), (uint32_t)ix->N, qs.lut, qmap, band, nq, qs.bsf, qs.win, onepd,
+        qs.cand, qs.cand_cnt, qs.cand_cap, qs.cand_hist);
 }
 
 // ------------------------------------------------------------------------------------ leaf scan
-// v2, the default: the MESSI idea on the sorted array. P:346-349: "the index workers traverse
-// the index subtrees ... using BSF to decide which subtrees will be pruned"; leaves that
-// survive are examined "by first computing lower bound distances using the iSAX summaries".
+// The default scan: MESSI's node pruning on the sorted array (R11). P:346-349: "the index
+// workers traverse the index subtrees ... using BSF to decide which subtrees will be pruned";
+// leaves that survive are examined "by first computing lower bound distances using the
+// iSAX summaries".
 //
-// A leaf is LEAF consecutive sorted positions. Its node summary (build: leaf_meta_kernel) is the
-// per-segment [min, max] symbol. The node's region on segment s is [beta_min, beta_{max+1}), and
-// its MINDIST term is min over c in [min, max] of LUT[s][c]. LUT[s][.] is V-shaped around the
-// query's own symbol q_s (zero there, growing away from it), so that minimum is
-// LUT[s][clamp(q_s, min, max)]: one lookup per segment per leaf.
-//   node LB^2 <= LB^2 of every member (termwise <=, and fp32 addition is monotone)
-// A leaf is pruned iff node LB^2 > T (1 + 2^-19). The extra 2^-19 covers the different fp32
-// summation order of the warp reduction (16 terms: < 2^-20 relative). Members of surviving
-// leaves get the exact per-series test of v1, so the candidate set is exactly v1's.
+// A leaf is LEAF consecutive sorted positions. Its node summary (leaf_meta_kernel) is the
+// per-segment [min, max] symbol. The node's region on segment s is [beta_min, beta_{max+1}).
+// Its MINDIST term is the minimum of LUT[s][c] over c in [min, max]. LUT[s][.] is V-shaped
+// around the query's own symbol q_s, so that minimum is LUT[s][clamp(q_s, min, max)].
+// The node bound is summed over s = 0..15 left to right in fp32, exactly like the per-series
+// bound. Every term is <= the member's term, and fp32 addition is monotone, so node LB^2 <=
+// member LB^2 holds exactly. A leaf is pruned iff node LB^2 > T. The candidate set is
+// therefore exactly the flat scan's (tests/test_gpu_parity.py).
 //
-// Work unit: one warp, two leaves. Lane = (leaf half, segment). The node LB needs 1 lookup +
-// 4 xor-shuffle adds per leaf per query. A leaf's 64 words (1 KB) are read only if some query
-// of the CTA's group keeps it.
+// Persistent CTAs (one per SM, 1024 threads) pull (query group, chunk of `chunk` leaves) tasks
+// from an atomic counter. LUTs of the group's G <= 8 queries sit in shared memory. Per chunk:
+//  A. lane = leaf: node bounds for all G queries; surviving leaves and their query masks go to
+//     a shared worklist;
+//  B. warps stream the worklist with two leaves' 1 KB of words in flight and run the
+//     per-series test for each query that kept the leaf. Candidates are buffered in shared
+//     memory per query slot and flushed once per group (one global atomic per slot).
 constexpr uint32_t LEAF = 64;
-
-constexpr int LF_THREADS = 1024;  // one CTA per SM; all 32 warps share the group's LUTs
-
-struct __align__(16) QConst {  // per query slot, read with one 16-byte shared load
-    float T, Tb;               // T = bsf^2 (1 + delta); Tb = T (1 + 2^-19) for the node bound
-    uint32_t ws, we;           // window [ws, we): already refined, never a candidate
-};
-
-constexpr uint32_t CHUNK = 8192;  // leaves per phase-A/phase-B round of a CTA
+constexpr int LF_THREADS = 1024;
+constexpr uint32_t CHUNK = 8192;  // max leaves per phase-A/phase-B round of a CTA
 constexpr uint32_t CBUF = 1024;   // shared candidate buffer per query slot
 
 // append `keep` lanes' positions for query slot g: shared buffer first, global list if it is full
@@ -181,48 +203,41 @@ __device__ __forceinline__ void emit(bool keep, uint32_t pos, uint32_t g, uint32
     }
 }
 
-__device__ __forceinline__ uint32_t byte_of(const uint32_t (&v)[4], int s) { return (v[s >> 2] >> (8 * (s & 3))) & 0xFFu; }
-
-// The kernel runs two phases per chunk of CHUNK leaves:
-//  A. lane = leaf: node LB^2 = sum_s LUT[s][clamp(q_s, min_s, max_s)], summed over s = 0..15
-//     left to right, exactly like the per-series LB. Every term is <= the member's term and
-//     fp32 addition is monotone, so node LB^2 <= member LB^2 holds exactly. Surviving leaves
-//     and their query masks go to a shared worklist.
-//  B. warps stream the worklist with two leaves' 1 KB of words in flight, and run the
-//     per-series test for each query that kept the leaf. Candidates are buffered in shared
-//     memory per query slot and flushed once per CTA (one global atomic per slot).
 template <int G>
 __global__ void __launch_bounds__(LF_THREADS, 1) leafscan_kernel(
     const uint4 *__restrict__ sax, const uint8_t *__restrict__ lmeta, uint32_t N, const float *__restrict__ lut_all,
-    const uint8_t *__restrict__ qsax_all, const uint32_t *__restrict__ qmap, const uint32_t *__restrict__ qrange,
-    uint32_t nq, uint32_t leaf_lo, uint32_t leaf_hi, uint32_t chunk, const unsigned long long *__restrict__ bsf,
+    const uint8_t *__restrict__ qsax_all, const uint32_t *__restrict__ qmap, const float2 *__restrict__ band,
+    uint32_t nq, uint32_t nleaf, uint32_t chunk, const unsigned long long *__restrict__ bsf,
     const uint32_t *__restrict__ win, float onepd, uint32_t *__restrict__ cand, uint32_t *__restrict__ cand_cnt,
-    uint32_t cap, uint32_t *__restrict__ leaves_alive, unsigned long long *__restrict__ leaf_loads,
-    uint32_t *__restrict__ task_ctr) {
+    uint32_t cap, uint32_t *__restrict__ hist, uint32_t *__restrict__ leaves_alive,
+    unsigned long long *__restrict__ leaf_loads, uint32_t *__restrict__ task_ctr) {
     extern __shared__ __align__(16) float slut[];  // [G][16][256] LUTs, [G][CBUF] candidates, [CHUNK] worklist
     uint32_t *cbuf = reinterpret_cast<uint32_t *>(slut + G * W * CARD);
     uint32_t *worklist = cbuf + G * CBUF;  // (leaf offset in chunk) | (query mask << 16)
     __shared__ QConst qc[G];
     __shared__ uint4 qsym[G];
-    __shared__ uint32_t r0[G], r1[G], qid[G], cb_cnt[G], alive_cnt[G], fbase[G];
+    __shared__ uint32_t qid[G], cb_cnt[G], alive_cnt[G], fbase[G];
+    __shared__ uint32_t shist[G][HIST_BINS];
     __shared__ uint32_t wl_cnt, s_task;
-    __shared__ int restricted;
     const uint32_t t = threadIdx.x, lane = t & 31, warp = t >> 5;
     constexpr uint32_t NW = LF_THREADS / 32;
     const uint32_t lt = (1u << lane) - 1u;
-    const uint32_t nchunks = (leaf_hi - leaf_lo + chunk - 1) / chunk;
+    const uint32_t nchunks = (nleaf + chunk - 1) / chunk;
     const uint32_t ngroups = (nq + G - 1) / G;
     const uint32_t ntasks = nchunks * ngroups;
     const uint4 *meta4 = reinterpret_cast<const uint4 *>(lmeta);
     uint32_t loads = 0;
     uint32_t g0 = 0xffffffffu;  // first query slot of the group whose LUTs are loaded
-    bool restr = false;
-    // empty the shared candidate buffers of the loaded group into the global lists
+    // empty the shared candidate buffers and histograms of the loaded group into global memory
     auto flush = [&]() {
         if (t < G) {
             const uint32_t c = min(cb_cnt[t], CBUF);
             fbase[t] = (c && g0 + t < nq) ? atomicAdd(&cand_cnt[qid[t]], c) : 0;
             if (alive_cnt[t] && g0 + t < nq) atomicAdd(&leaves_alive[qid[t]], alive_cnt[t]);
+        }
+        for (uint32_t e = t; e < G * HIST_BINS; e += LF_THREADS) {
+            const uint32_t g = e / HIST_BINS, b = e % HIST_BINS;
+            if (g0 + g < nq && shist[g][b]) atomicAdd(&hist[qid[g] * HIST_BINS + b], shist[g][b]);
         }
         __syncthreads();
         for (uint32_t g = 0; g < G; g++) {
@@ -236,14 +251,13 @@ __global__ void __launch_bounds__(LF_THREADS, 1) leafscan_kernel(
         __syncthreads();
     };
     if (t == 0) wl_cnt = 0;
-    // persistent CTA: tasks (group, chunk) in group-major order from an atomic counter
     for (;;) {
         if (t == 0) s_task = atomicAdd(task_ctr, 1u);
         __syncthreads();
         const uint32_t task = s_task;
         if (task >= ntasks) break;
         const uint32_t grp = task / nchunks, ch = task % nchunks;
-        if (grp * G != g0) {
+        if (grp * G != g0) {  // new query group: load its LUTs and constants
             if (g0 != 0xffffffffu) flush();
             g0 = grp * G;
             for (uint32_t e = t; e < G * W * CARD; e += LF_THREADS) {
@@ -251,8 +265,7 @@ __global__ void __launch_bounds__(LF_THREADS, 1) leafscan_kernel(
                 const uint32_t qi = g0 + g < nq ? qmap[g0 + g] : qmap[g0];
                 slut[e] = lut_all[(uint64_t)qi * W * CARD + (e % (W * CARD))];
             }
-            if (t == 0) restricted = 0;
-            __syncthreads();
+            for (uint32_t e = t; e < G * HIST_BINS; e += LF_THREADS) shist[e / HIST_BINS][e % HIST_BINS] = 0;
             if (t < G) {
                 const bool valid = g0 + t < nq;
                 const uint32_t qi = valid ? qmap[g0 + t] : qmap[g0];
@@ -260,18 +273,12 @@ __global__ void __launch_bounds__(LF_THREADS, 1) leafscan_kernel(
                 cb_cnt[t] = 0;
                 alive_cnt[t] = 0;
                 qsym[t] = reinterpret_cast<const uint4 *>(qsax_all)[qi];
-                const float tq = valid ? bsf_d2(bsf[qi]) * onepd : -1.0f;  // an invalid slot keeps nothing
-                qc[t] = QConst{tq, tq, win[2 * qi], win[2 * qi + 1]};
-                r0[t] = valid ? qrange[2 * (g0 + t)] : 0;
-                r1[t] = valid ? qrange[2 * (g0 + t) + 1] : 0;
-                if (valid && (r0[t] > leaf_lo * LEAF || r1[t] < min(leaf_hi * LEAF, N))) atomicOr(&restricted, 1);
+                qc[t] = load_qconst(qi, valid, bsf, band, g0 + t, win, onepd);
             }
             __syncthreads();
-            restr = restricted != 0;
         }
-        {
-        const uint32_t c0 = leaf_lo + ch * chunk;
-        const uint32_t c1 = min(c0 + chunk, leaf_hi);
+        const uint32_t c0 = ch * chunk;
+        const uint32_t c1 = min(c0 + chunk, nleaf);
         // ---- phase A: lane = leaf; warp w takes leaves c0 + 32 w + lane, then + 32 NW, ...
         uint32_t leaf = c0 + warp * 32 + lane;
         uint4 mn_n = make_uint4(0, 0, 0, 0), mx_n = make_uint4(~0u, ~0u, ~0u, ~0u);
@@ -283,7 +290,7 @@ __global__ void __launch_bounds__(LF_THREADS, 1) leafscan_kernel(
             const uint32_t mn[4] = {mn_n.x, mn_n.y, mn_n.z, mn_n.w};
             const uint32_t mx[4] = {mx_n.x, mx_n.y, mx_n.z, mx_n.w};
             const uint32_t nxt = leaf + 32 * NW;
-            if (nxt < c1) {
+            if (nxt < c1) {  // software pipeline: the next node summary is in flight
                 mn_n = __ldg(meta4 + 2 * (uint64_t)nxt);
                 mx_n = __ldg(meta4 + 2 * (uint64_t)nxt + 1);
             }
@@ -302,12 +309,6 @@ __global__ void __launch_bounds__(LF_THREADS, 1) leafscan_kernel(
                 if (lb <= qc[g].T) alive |= 1u << g;
             }
             if (leaf >= c1) alive = 0;
-            if (restr && alive) {  // overflow rounds: the leaf must meet this slot's position range
-                const uint32_t p0 = leaf * LEAF, p1 = min(p0 + LEAF, N);
-#pragma unroll
-                for (int g = 0; g < G; g++)
-                    if (!(p0 < r1[g] && p1 > r0[g])) alive &= ~(1u << g);
-            }
             const uint32_t bal = __ballot_sync(0xffffffffu, alive != 0);
             if (bal) {
                 uint32_t off = 0;
@@ -347,12 +348,9 @@ __global__ void __launch_bounds__(LF_THREADS, 1) leafscan_kernel(
 #pragma unroll
                     for (int u = 0; u < 2; u++) {
                         const uint32_t pos = base + u * 32 + lane;
-                        const uint32_t v[4] = {wv[k][u].x, wv[k][u].y, wv[k][u].z, wv[k][u].w};
-                        float lb = 0.f;
-#pragma unroll
-                        for (int s2 = 0; s2 < W; s2++) lb += L[s2 * CARD + byte_of(v, s2)];
-                        bool keep = pos < N && lb <= kq.T && (pos < kq.ws || pos >= kq.we);
-                        if (restr) keep = keep && pos >= r0[g] && pos < r1[g];
+                        const float lb = word_lb(L, wv[k][u]);
+                        const bool keep = pos < N && lb > kq.lo && lb <= kq.T && (pos < kq.ws || pos >= kq.we);
+                        if (keep) atomicAdd(&shist[g][hist_bin(lb, kq.lo, kq.T)], 1u);
                         emit(keep, pos, g, qid[g], lane, lt, cbuf, cb_cnt, cand, cand_cnt, cap);
                     }
                 }
@@ -360,15 +358,14 @@ __global__ void __launch_bounds__(LF_THREADS, 1) leafscan_kernel(
         }
         __syncthreads();
         if (t == 0) wl_cnt = 0;
-        }
     }
     if (g0 != 0xffffffffu) flush();
     if (lane == 0 && loads) atomicAdd(leaf_loads, (unsigned long long)loads);
 }
 
 template <int G>
-static void launch_leaf(const isax_index *ix, uint32_t nq, const uint32_t *qmap, const uint32_t *qrange, uint32_t lo,
-                        uint32_t hi, float onepd, cudaStream_t s) {
+static void launch_leaf(const isax_index *ix, uint32_t nq, const uint32_t *qmap, const float2 *band, float onepd,
+                        cudaStream_t s) {
     const size_t smem = (size_t)G * W * CARD * sizeof(float) + (size_t)G * CBUF * sizeof(uint32_t) + CHUNK * 4;
     static bool configured = false;
     if (!configured) {
@@ -379,8 +376,7 @@ static void launch_leaf(const isax_index *ix, uint32_t nq, const uint32_t *qmap,
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const uint32_t groups = (nq + G - 1) / G;
-    const uint32_t leaf_lo = lo / LEAF, leaf_hi = (hi + LEAF - 1) / LEAF;
-    const uint32_t nleaf = leaf_hi - leaf_lo;
+    const uint32_t nleaf = (uint32_t)((ix->N + LEAF - 1) / LEAF);
     // chunk: as large as possible (fewer phase barriers) while leaving >= 8 tasks per SM for balance
     uint32_t chunk = CHUNK;
     while (chunk > 512 && (uint64_t)groups * ((nleaf + chunk - 1) / chunk) < 8ull * sms) chunk >>= 1;
@@ -389,29 +385,29 @@ static void launch_leaf(const isax_index *ix, uint32_t nq, const uint32_t *qmap,
     const QueryScratch &qs = ix->qs;
     cudaMemsetAsync(qs.task_ctr, 0, sizeof(uint32_t), s);
     leafscan_kernel<G><<<grid, LF_THREADS, smem, s>>>(
-        reinterpret_cast<const uint4 *>(ix->sax), ix->lmeta, (uint32_t)ix->N, qs.lut, qs.qsax, qmap, qrange, nq,
-        leaf_lo, leaf_hi, chunk, qs.bsf, qs.win, onepd, qs.cand, qs.cand_cnt, qs.cand_cap, qs.counters_leaf,
-        qs.leaf_loads, qs.task_ctr);
+        reinterpret_cast<const uint4 *>(ix->sax), ix->lmeta, (uint32_t)ix->N, qs.lut, qs.qsax, qmap, band, nq, nleaf,
+        chunk, qs.bsf, qs.win, onepd, qs.cand, qs.cand_cnt, qs.cand_cap, qs.cand_hist, qs.counters_leaf, qs.leaf_loads,
+        qs.task_ctr);
 }
 
-uint64_t launch_lbscan(const isax_index *ix, uint32_t nq, const uint32_t *qmap, const uint32_t *qrange, uint32_t lo,
-                       uint32_t hi, float delta, cudaStream_t s) {
-    if (!nq || hi <= lo) return 0;
+uint64_t launch_lbscan(const isax_index *ix, uint32_t nq, const uint32_t *qmap, const float2 *band, float delta,
+                       cudaStream_t s) {
+    if (!nq) return 0;
     const float onepd = 1.0f + delta;
-    if (ix->opts.flags & ISAX_FLAG_FLAT_SCAN) {  // ParIS flat scan (v1), kept for A/B measurement
+    if (ix->opts.flags & ISAX_FLAG_FLAT_SCAN) {  // ParIS flat scan, kept for A/B measurement
         const uint32_t G = nq >= 4 ? 4 : nq;
-        if (G == 4) launch_g<4>(ix, nq, qmap, qrange, lo, hi, onepd, s);
-        else if (G == 3) launch_g<3>(ix, nq, qmap, qrange, lo, hi, onepd, s);
-        else if (G == 2) launch_g<2>(ix, nq, qmap, qrange, lo, hi, onepd, s);
-        else launch_g<1>(ix, nq, qmap, qrange, lo, hi, onepd, s);
-        return 16ull * (hi - lo) * ((nq + G - 1) / G);  // words read
+        if (G == 4) launch_g<4>(ix, nq, qmap, band, onepd, s);
+        else if (G == 3) launch_g<3>(ix, nq, qmap, band, onepd, s);
+        else if (G == 2) launch_g<2>(ix, nq, qmap, band, onepd, s);
+        else launch_g<1>(ix, nq, qmap, band, onepd, s);
+        return 16ull * ix->N * ((nq + G - 1) / G);  // words read
     }
     const uint32_t G = nq >= 8 ? 8 : nq >= 4 ? 4 : nq >= 2 ? 2 : 1;
-    if (G == 8) launch_leaf<8>(ix, nq, qmap, qrange, lo, hi, onepd, s);
-    else if (G == 4) launch_leaf<4>(ix, nq, qmap, qrange, lo, hi, onepd, s);
-    else if (G == 2) launch_leaf<2>(ix, nq, qmap, qrange, lo, hi, onepd, s);
-    else launch_leaf<1>(ix, nq, qmap, qrange, lo, hi, onepd, s);
-    const uint64_t leaves = (hi + LEAF - 1) / LEAF - lo / LEAF;
+    if (G == 8) launch_leaf<8>(ix, nq, qmap, band, onepd, s);
+    else if (G == 4) launch_leaf<4>(ix, nq, qmap, band, onepd, s);
+    else if (G == 2) launch_leaf<2>(ix, nq, qmap, band, onepd, s);
+    else launch_leaf<1>(ix, nq, qmap, band, onepd, s);
+    const uint64_t leaves = (ix->N + LEAF - 1) / LEAF;
     return 32ull * leaves * ((nq + G - 1) / G);  // node summaries read; leaf words are counted on the device
 }
 

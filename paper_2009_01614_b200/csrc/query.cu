@@ -25,6 +25,7 @@ __constant__ double c_beta_q[ISAX_NBETA] = ISAX_BETA_INIT;
 
 __global__ void __launch_bounds__(256) qprep_kernel(const float *__restrict__ queries, uint32_t n,
                                                     const uint4 *__restrict__ sax, uint64_t N, uint32_t L,
+                                                    uint32_t P, uint32_t Lp, uint32_t *__restrict__ pwin,
                                                     float *__restrict__ qy, double *__restrict__ qpaa,
                                                     uint8_t *__restrict__ qsax, float *__restrict__ lut,
                                                     uint32_t *__restrict__ win, unsigned long long *__restrict__ bsf,
@@ -91,15 +92,45 @@ __global__ void __launch_bounds__(256) qprep_kernel(const float *__restrict__ qu
         else if (c < CARD - 1 && mm > beta[c]) d = __dsub_rn(mm, beta[c]);
         lut[((uint64_t)q * W + s) * CARD + c] = __double2float_rd(__dmul_rn(segd, __dmul_rn(d, d)));
     }
-    if (t < 32) {  // locate: first pos with key(pos) >= key(q), 32-ary search by warp 0
+    // Multi-probe approximate answer (R5). Besides the query's own key, probe the keys obtained
+    // by moving the symbols of the P most fragile key bits across their nearest region
+    // boundary. The candidates are the plane-0/1 bits whose segment mean lies closest to the
+    // breakpoint that flips them. A near-duplicate whose noise flipped an early key bit lands
+    // far from its source in the sorted order; one of the probes lands next to it.
+    __shared__ uint32_t sel_s[8], sel_c[8];
+    if (t < 32 && P > 0) {
+        const uint32_t pl = t >> 4, sg = t & 15;
+        const uint32_t c = sym[sg], step = 128u >> pl;
+        const uint32_t lo_c = (c / step) * step, hi_c = lo_c + step;
+        const double mm = m[sg];
+        const double dlo = lo_c > 0 ? mm - beta[lo_c - 1] : 1e300;
+        const double dhi = hi_c < CARD ? beta[hi_c - 1] - mm : 1e300;
+        const uint32_t target = dlo < dhi ? lo_c - 1 : hi_c;
+        const float mg = (float)fmin(dlo, dhi);
+        uint32_t key = (__float_as_uint(fmaxf(mg, 0.f)) & ~31u) | t;
+        for (uint32_t k = 0; k < P; k++) {
+            const uint32_t mn = __reduce_min_sync(0xffffffffu, key);
+            if (key == mn) {
+                sel_s[k] = sg;
+                sel_c[k] = target;
+                key = 0xffffffffu;
+            }
+        }
+    }
+    __syncthreads();
+    const uint32_t NP = 1u << P;
+    const uint32_t warp = t >> 5, lane = t & 31;
+    for (uint32_t j = warp; j < NP; j += blockDim.x / 32) {  // locate each probe key, one warp per probe
         uint32_t sy[W];
 #pragma unroll
-        for (int s = 0; s < W; s++) sy[s] = sym[s];
+        for (int s2 = 0; s2 < W; s2++) sy[s2] = sym[s2];
+        for (uint32_t b = 0; b < P; b++)
+            if ((j >> b) & 1u) sy[sel_s[b]] = sel_c[b];
         const uint4 kq = isax_key(sy);
         uint64_t lo = 0, hi = N;
         while (hi - lo > 32) {
             const uint64_t span = hi - lo;
-            const uint64_t p = lo + (span * (t + 1)) / 33;
+            const uint64_t p = lo + (span * (lane + 1)) / 33;
             const bool less = key_less(word_key(__ldg(sax + p)), kq);
             const uint32_t bal = __ballot_sync(0xffffffffu, less);
             const uint32_t c = __popc(bal);  // probes are increasing, so `less` is a prefix
@@ -111,18 +142,22 @@ __global__ void __launch_bounds__(256) qprep_kernel(const float *__restrict__ qu
                 if (c < 32) hi = p_next;
             }
         }
-        const bool less = (lo + t < hi) && key_less(word_key(__ldg(sax + lo + t)), kq);
+        const bool less = (lo + lane < hi) && key_less(word_key(__ldg(sax + lo + lane)), kq);
         const uint64_t pos = lo + __popc(__ballot_sync(0xffffffffu, less));
-        if (t == 0) {
-            uint64_t start = 0, end = N;
-            if (N > L) {
-                const int64_t s0 = (int64_t)pos - (int64_t)(L / 2);
-                const int64_t smax = (int64_t)(N - L);
+        if (lane == 0) {
+            const uint32_t len = j == 0 ? L : Lp;
+            uint64_t start = 0;
+            if (N > len) {
+                const int64_t s0 = (int64_t)pos - (int64_t)(len / 2);
+                const int64_t smax = (int64_t)(N - len);
                 start = (uint64_t)(s0 < 0 ? 0 : (s0 > smax ? smax : s0));
-                end = start + L;
             }
-            win[2 * q] = (uint32_t)start;
-            win[2 * q + 1] = (uint32_t)end;
+            if (j == 0) {
+                win[2 * q] = (uint32_t)start;
+                win[2 * q + 1] = (uint32_t)(start + (N > len ? len : N));
+            } else {
+                pwin[q * (MAX_PROBES - 1) + j - 1] = (uint32_t)start;
+            }
         }
     }
 }
@@ -130,7 +165,7 @@ __global__ void __launch_bounds__(256) qprep_kernel(const float *__restrict__ qu
 void launch_qprep(const isax_index *ix, const float *queries, uint32_t Q, cudaStream_t s, uint32_t *bad) {
     const QueryScratch &qs = ix->qs;
     qprep_kernel<<<Q, 256, 0, s>>>(queries, ix->n, reinterpret_cast<const uint4 *>(ix->sax), ix->N,
-                                   ix->opts.window_L, qs.qy, qs.qpaa, qs.qsax, qs.lut, qs.win, qs.bsf, qs.cand_cnt,
+                                   ix->opts.window_L, probe_bits(ix), ix->opts.probe_L, qs.pwin, qs.qy, qs.qpaa, qs.qsax, qs.lut, qs.win, qs.bsf, qs.cand_cnt,
                                    qs.near_cnt, qs.counters, bad);
 }
 
@@ -155,21 +190,27 @@ __device__ __forceinline__ float row_d2(const float *__restrict__ row, const flo
     return warp_sum(acc);
 }
 
-constexpr uint32_t WIN_MAX = 4096;
-
 template <int NS>
 __global__ void __launch_bounds__(256) window_kernel(const float *__restrict__ stored, const uint32_t *__restrict__ perm,
-                                                     uint32_t n, const float *__restrict__ qy,
-                                                     const uint32_t *__restrict__ win, const uint32_t *__restrict__ qmap,
+                                                     uint32_t n, uint64_t N, const float *__restrict__ qy,
+                                                     const uint32_t *__restrict__ win, const uint32_t *__restrict__ pwin,
+                                                     uint32_t nprobe, uint32_t Lp, const uint32_t *__restrict__ qmap,
                                                      unsigned long long *__restrict__ bsf, NearEntry *__restrict__ near,
                                                      uint32_t *__restrict__ near_cnt, uint32_t *__restrict__ counters,
                                                      float onepd) {
-    __shared__ float d2s[WIN_MAX];
+    extern __shared__ float d2s[];  // one d^2 per refined row
     __shared__ unsigned long long smin;
     __shared__ unsigned long long cur;
     const uint32_t q = qmap ? qmap[blockIdx.x] : blockIdx.x;
     const uint32_t t = threadIdx.x, lane = t & 31, warp = t >> 5;
     const uint32_t ws = win[2 * q], we = win[2 * q + 1], L = we - ws;
+    const uint32_t lp = (uint32_t)(N < Lp ? N : Lp);
+    const uint32_t rows = L + nprobe * lp;
+    auto row_pos = [&](uint32_t r) -> uint32_t {
+        if (r < L) return ws + r;
+        r -= L;
+        return pwin[q * (MAX_PROBES - 1) + r / lp] + r % lp;
+    };
     float4 qv[NS];
 #pragma unroll
     for (int k = 0; k < NS; k++) {
@@ -179,11 +220,12 @@ __global__ void __launch_bounds__(256) window_kernel(const float *__restrict__ s
     if (t == 0) smin = ~0ull;
     __syncthreads();
     unsigned long long mine = ~0ull;
-    for (uint32_t r = warp; r < L; r += 8) {
-        const float d2 = row_d2<NS>(stored + (uint64_t)(ws + r) * n, qv, n, lane);
+    for (uint32_t r = warp; r < rows; r += 8) {
+        const uint32_t pos = row_pos(r);
+        const float d2 = row_d2<NS>(stored + (uint64_t)pos * n, qv, n, lane);
         if (lane == 0) {
             d2s[r] = d2;
-            const unsigned long long p = pack_bsf(d2, perm[ws + r]);
+            const unsigned long long p = pack_bsf(d2, perm[pos]);
             mine = p < mine ? p : mine;
         }
     }
@@ -192,26 +234,38 @@ __global__ void __launch_bounds__(256) window_kernel(const float *__restrict__ s
     if (t == 0) {
         atomicMin(&bsf[q], smin);
         cur = atomicAdd(&bsf[q], 0ull);
-        atomicAdd(&counters[4 * q + 0], L);
+        atomicAdd(&counters[4 * q + 0], rows);
     }
     __syncthreads();
     const float lim = bsf_d2(cur) * onepd;
-    for (uint32_t r = t; r < L; r += blockDim.x) {
+    for (uint32_t r = t; r < rows; r += blockDim.x) {
         if (d2s[r] <= lim) {
+            const uint32_t pos = row_pos(r);
             const uint32_t k = atomicAdd(&near_cnt[q], 1u);
-            if (k < NEAR_K) near[(uint64_t)q * NEAR_K + k] = NearEntry{perm[ws + r], ws + r, d2s[r], 0};
+            if (k < NEAR_K) near[(uint64_t)q * NEAR_K + k] = NearEntry{perm[pos], pos, d2s[r], 0};
         }
     }
+}
+
+uint32_t probe_bits(const isax_index *ix) {
+    return ix->opts.probe_bits == ISAX_PROBES_NONE ? 0u : ix->opts.probe_bits;
 }
 
 void launch_window(const isax_index *ix, uint32_t Q, const uint32_t *qmap, float delta, cudaStream_t s) {
     const QueryScratch &qs = ix->qs;
     const float onepd = 1.0f + delta;
     const uint32_t ns = (ix->n + 127) / 128;
+    const uint32_t nprobe = (1u << probe_bits(ix)) - 1;
+    const uint32_t lp = (uint32_t)(ix->N < ix->opts.probe_L ? ix->N : ix->opts.probe_L);
+    const uint32_t L = (uint32_t)(ix->N < ix->opts.window_L ? ix->N : ix->opts.window_L);
+    const size_t smem = sizeof(float) * ((size_t)L + (size_t)nprobe * lp);
 #define WIN_CASE(K)                                                                                          \
     case K:                                                                                                  \
-        window_kernel<K><<<Q, 256, 0, s>>>(ix->stored, ix->perm, ix->n, qs.qy, qs.win, qmap, qs.bsf, qs.near, \
-                                           qs.near_cnt, qs.counters, onepd);                                 \
+        if (smem > 48 * 1024)                                                                                \
+            cudaFuncSetAttribute(window_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);  \
+        window_kernel<K><<<Q, 256, smem, s>>>(ix->stored, ix->perm, ix->n, ix->N, qs.qy, qs.win, qs.pwin,    \
+                                              nprobe, ix->opts.probe_L, qmap, qs.bsf, qs.near, qs.near_cnt,   \
+                                              qs.counters, onepd);                                           \
         break;
     switch (ns) {
         WIN_CASE(1) WIN_CASE(2) WIN_CASE(3) WIN_CASE(4) WIN_CASE(5) WIN_CASE(6) WIN_CASE(7) WIN_CASE(8)

@@ -149,7 +149,8 @@ def test_ties_duplicates_constants_and_exact_copies():
 
 
 @pytest.mark.parametrize("opts", [dict(window_L=1), dict(window_L=4096), dict(cand_cap=7), dict(batch_Q=3),
-                                  dict(slack_log2=-20)])
+                                  dict(slack_log2=-20), dict(probe_bits=0xFFFFFFFF), dict(probe_bits=5, probe_L=1),
+                                  dict(probe_bits=2, probe_L=1024)])
 def test_options_do_not_change_answers(opts):
     N, n = 30_000, 256
     wl = small_workload(N, n, Q=12, q_noisy=4)
