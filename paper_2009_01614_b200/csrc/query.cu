@@ -190,6 +190,13 @@ __device__ __forceinline__ float row_d2(const float *__restrict__ row, const flo
     return warp_sum(acc);
 }
 
+// The rows of one query (main window, then probe windows) are split over several CTAs of
+// WIN_ROWS rows each, so a batch keeps every SM busy. Each warp refines two rows at a time, with
+// 2 KB of loads in flight. Each CTA folds its minimum into the global packed BSF. It then appends
+// the rows within (1 + delta) of the BSF it reads back. That BSF can only be >= the final one, so
+// the near list is a superset of the final near ties (R9).
+constexpr uint32_t WIN_ROWS = 512;
+
 template <int NS>
 __global__ void __launch_bounds__(256) window_kernel(const float *__restrict__ stored, const uint32_t *__restrict__ perm,
                                                      uint32_t n, uint64_t N, const float *__restrict__ qy,
@@ -198,14 +205,17 @@ __global__ void __launch_bounds__(256) window_kernel(const float *__restrict__ s
                                                      unsigned long long *__restrict__ bsf, NearEntry *__restrict__ near,
                                                      uint32_t *__restrict__ near_cnt, uint32_t *__restrict__ counters,
                                                      float onepd) {
-    extern __shared__ float d2s[];  // one d^2 per refined row
+    __shared__ float d2s[WIN_ROWS];
     __shared__ unsigned long long smin;
     __shared__ unsigned long long cur;
-    const uint32_t q = qmap ? qmap[blockIdx.x] : blockIdx.x;
+    const uint32_t q = qmap ? qmap[blockIdx.y] : blockIdx.y;
     const uint32_t t = threadIdx.x, lane = t & 31, warp = t >> 5;
     const uint32_t ws = win[2 * q], we = win[2 * q + 1], L = we - ws;
     const uint32_t lp = (uint32_t)(N < Lp ? N : Lp);
     const uint32_t rows = L + nprobe * lp;
+    const uint32_t r0 = blockIdx.x * WIN_ROWS;
+    if (r0 >= rows) return;
+    const uint32_t r1 = min(rows, r0 + WIN_ROWS);
     auto row_pos = [&](uint32_t r) -> uint32_t {
         if (r < L) return ws + r;
         r -= L;
@@ -220,13 +230,39 @@ __global__ void __launch_bounds__(256) window_kernel(const float *__restrict__ s
     if (t == 0) smin = ~0ull;
     __syncthreads();
     unsigned long long mine = ~0ull;
-    for (uint32_t r = warp; r < rows; r += 8) {
-        const uint32_t pos = row_pos(r);
-        const float d2 = row_d2<NS>(stored + (uint64_t)pos * n, qv, n, lane);
+    for (uint32_t r = r0 + warp * 2; r < r1; r += 16) {
+        const bool two = r + 1 < r1;
+        const uint32_t pa = row_pos(r), pb = two ? row_pos(r + 1) : pa;
+        const float *ra = stored + (uint64_t)pa * n, *rb = stored + (uint64_t)pb * n;
+        float aa = 0.f, ab = 0.f;
+#pragma unroll
+        for (int k = 0; k < NS; k++) {
+            const uint32_t i = k * 128 + 4 * lane;
+            if (i < n) {
+                const float4 va = __ldcs(reinterpret_cast<const float4 *>(ra + i));
+                const float4 vb = __ldcs(reinterpret_cast<const float4 *>(rb + i));
+                float d;
+                d = va.x - qv[k].x; aa = fmaf(d, d, aa);
+                d = va.y - qv[k].y; aa = fmaf(d, d, aa);
+                d = va.z - qv[k].z; aa = fmaf(d, d, aa);
+                d = va.w - qv[k].w; aa = fmaf(d, d, aa);
+                d = vb.x - qv[k].x; ab = fmaf(d, d, ab);
+                d = vb.y - qv[k].y; ab = fmaf(d, d, ab);
+                d = vb.z - qv[k].z; ab = fmaf(d, d, ab);
+                d = vb.w - qv[k].w; ab = fmaf(d, d, ab);
+            }
+        }
+        aa = warp_sum(aa);
+        ab = warp_sum(ab);
         if (lane == 0) {
-            d2s[r] = d2;
-            const unsigned long long p = pack_bsf(d2, perm[pos]);
+            d2s[r - r0] = aa;
+            const unsigned long long p = pack_bsf(aa, perm[pa]);
             mine = p < mine ? p : mine;
+            if (two) {
+                d2s[r + 1 - r0] = ab;
+                const unsigned long long pq = pack_bsf(ab, perm[pb]);
+                mine = pq < mine ? pq : mine;
+            }
         }
     }
     if (lane == 0) atomicMin(&smin, mine);
@@ -234,15 +270,15 @@ __global__ void __launch_bounds__(256) window_kernel(const float *__restrict__ s
     if (t == 0) {
         atomicMin(&bsf[q], smin);
         cur = atomicAdd(&bsf[q], 0ull);
-        atomicAdd(&counters[4 * q + 0], rows);
+        atomicAdd(&counters[4 * q + 0], r1 - r0);
     }
     __syncthreads();
     const float lim = bsf_d2(cur) * onepd;
-    for (uint32_t r = t; r < rows; r += blockDim.x) {
-        if (d2s[r] <= lim) {
+    for (uint32_t r = r0 + t; r < r1; r += blockDim.x) {
+        if (d2s[r - r0] <= lim) {
             const uint32_t pos = row_pos(r);
             const uint32_t k = atomicAdd(&near_cnt[q], 1u);
-            if (k < NEAR_K) near[(uint64_t)q * NEAR_K + k] = NearEntry{perm[pos], pos, d2s[r], 0};
+            if (k < NEAR_K) near[(uint64_t)q * NEAR_K + k] = NearEntry{perm[pos], pos, d2s[r - r0], 0};
         }
     }
 }
@@ -258,12 +294,11 @@ void launch_window(const isax_index *ix, uint32_t Q, const uint32_t *qmap, float
     const uint32_t nprobe = (1u << probe_bits(ix)) - 1;
     const uint32_t lp = (uint32_t)(ix->N < ix->opts.probe_L ? ix->N : ix->opts.probe_L);
     const uint32_t L = (uint32_t)(ix->N < ix->opts.window_L ? ix->N : ix->opts.window_L);
-    const size_t smem = sizeof(float) * ((size_t)L + (size_t)nprobe * lp);
+    const uint32_t rows = L + nprobe * lp;
+    const dim3 grid((rows + WIN_ROWS - 1) / WIN_ROWS, Q);
 #define WIN_CASE(K)                                                                                          \
     case K:                                                                                                  \
-        if (smem > 48 * 1024)                                                                                \
-            cudaFuncSetAttribute(window_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);  \
-        window_kernel<K><<<Q, 256, smem, s>>>(ix->stored, ix->perm, ix->n, ix->N, qs.qy, qs.win, qs.pwin,    \
+        window_kernel<K><<<grid, 256, 0, s>>>(ix->stored, ix->perm, ix->n, ix->N, qs.qy, qs.win, qs.pwin,    \
                                               nprobe, ix->opts.probe_L, qmap, qs.bsf, qs.near, qs.near_cnt,   \
                                               qs.counters, onepd);                                           \
         break;
