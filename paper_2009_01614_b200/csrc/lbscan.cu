@@ -340,9 +340,11 @@ __global__ void __launch_bounds__(LF_THREADS, 1) leafscan_kernel(
                 const uint32_t base = (c0 + (ent[k] & 0xFFFFu)) * LEAF;
                 loads++;
                 if (lane < G && ((am >> lane) & 1u)) atomicAdd(&alive_cnt[lane], 1u);
-#pragma unroll
-                for (int g = 0; g < G; g++) {
-                    if (!((am >> g) & 1u)) continue;
+                // rolled loop over the queries that kept the leaf: unrolling it over G made the
+                // kernel ~120 KB of SASS, and instruction-cache misses became the top stall
+#pragma unroll 1
+                for (uint32_t mm = am; mm; mm &= mm - 1) {
+                    const uint32_t g = __ffs(mm) - 1;
                     const QConst kq = qc[g];
                     const float *L = slut + g * W * CARD;
 #pragma unroll
