@@ -166,17 +166,13 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2009_01614_b200 import isax
 
-    Q = args.queries or wl.Q
-    if world > 1:  # every rank answers its own queries (different seed)
-        import dataclasses
+    from paper_2009_01614_b200 import dist as pdist
 
-        wlq = dataclasses.replace(wl, q_seed=wl.q_seed + 7919 * rank)
-    else:
-        wlq = wl
+    Q = args.queries or wl.Q
+    wlq = pdist.rank_workload(wl, rank)  # replicas: every rank answers its own queries
     # ---- build (a1-a5), timed on its own
     free, _ = torch.cuda.mem_get_info()
     raw_bytes = wl.N * wl.n * 4
-    t0 = time.perf_counter()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if 2 * raw_bytes + (8 << 30) < free:
         x = datagen.series(wl, 0, wl.N)
@@ -203,14 +199,13 @@ def main():
     for _ in range(max(args.warmup, 0)):
         ids, dist_ = ix.nn1(q)
     torch.cuda.synchronize()
-    # ---- timed: K steps on the device
+    # ---- timed: K steps on the device, bracketed by barrier + synchronize
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
     clk = ClockSampler(local)
     clk.start()
     time.sleep(0.3)
-    lb_ms, rf_ms, cand, refined, launches, rounds, scan_b = [], [], [], [], 0, [], []
     e_start, e_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e_start.record(stream)
     for _ in range(args.steps):
@@ -218,26 +213,28 @@ def main():
     e_end.record(stream)
     torch.cuda.synchronize()
     clocks = clk.stop()
-    ms = e_start.elapsed_time(e_end)
-    # per-kernel times and counters: a separate pass of the same steps (stats() is host work,
-    # kept out of the timed region)
+    if dist:
+        dist.barrier()
+    ms = pdist.max_over_ranks(e_start.elapsed_time(e_end), device="cuda")
+    value = pdist.aggregate_qps(Q, args.steps, world, ms)
+    # ---- per-kernel times and counters: a separate pass of the same steps (stats() is host
+    # work, kept out of the timed region). The library times its first batch with CUDA events
+    # on the stream its kernels run on.
+    keys = ["lbscan", "refine", "window", "qprep"]
+    kms = {k: [] for k in keys}
+    cand, refined, rounds, scan_b, ref_b, pairs, launches = [], [], [], [], [], [], 0
     for _ in range(args.steps):
         ids, dist_ = ix.nn1(q)
         st = ix.stats()
-        lb_ms.append(st["ms_first_batch"]["lbscan"])
-        rf_ms.append(st["ms_first_batch"]["refine"])
+        for k in keys:
+            kms[k].append(st["ms_first_batch"][k])
         cand.append(sum(st["candidates"]))
         refined.append(sum(st["refined"]))
         rounds.append(max(st["rounds"]))
         launches += st.get("launches", 0)
         scan_b.append(st["scan_bytes_first_launch"])
-    if dist:
-        t = torch.tensor([ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-        dist.barrier()
-    total_q = Q * args.steps * world
-    value = total_q / (ms / 1e3)
+        ref_b.append(st["refine_bytes_first_launch"])
+        pairs.append(st["leaf_pairs_first_launch"])
     # ---- e2e through isax_nn1 with host (pinned) buffers, copies inside the timed region
     qh = torch.empty((Q, wl.n), dtype=torch.float32, pin_memory=True)
     qh.copy_(q)
@@ -250,26 +247,45 @@ def main():
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
         ix.nn1_host(qh.numpy(), oid.numpy(), odist.numpy())
-    e2e_s = time.perf_counter() - t0
-    if dist:
-        t = torch.tensor([e2e_s], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item())
+    e2e_s = pdist.max_over_ranks(time.perf_counter() - t0, device="cuda")
     assert (oid.numpy() == ids.cpu().numpy()).all(), "host and device paths disagree"
-    # ---- roofline: lbscan (dominant kernel), bytes it must read per launch
+    # ---- roofline of the dominant kernel (leafscan) and of the HBM-bound kernels
     hbm, peak_src = peaks()
-    lb_launch_ms = statistics.mean(lb_ms)
-    cand_mean = statistics.mean(cand)
-    alg_bytes = statistics.mean(scan_b) + 4.0 * cand_mean
-    achieved = alg_bytes / (lb_launch_ms / 1e3) / 1e9
-    roofline = {"kernel": "leafscan_kernel<8>", "bound": "hbm", "achieved": round(achieved, 1), "peak": hbm,
-                "unit": "GB/s", "frac": round(achieved / hbm, 4), "traffic": None,
-                "peak_source": peak_src,
-                "bytes_per_launch": alg_bytes,
-                "bytes_rule": "32 B node summary per leaf per group of 8 queries + 1 KB of words per surviving leaf "
-                              "(read once per group) + 4 B per candidate written; counted by the kernel",
-                "launch_ms": round(lb_launch_ms, 4), "refine_ms": round(statistics.mean(rf_ms), 4),
-                "lookups_per_s": 16.0 * wl.N * min(Q, 128) / (lb_launch_ms / 1e3)}
+    sm_mhz = clocks.get("sm_mhz") or 1965.0
+    lb_ms = statistics.mean(kms["lbscan"])
+    rf_ms = statistics.mean(kms["refine"])
+    nq1 = min(Q, 128)
+    leaves = (wl.N + 63) // 64
+    # algorithmic LUT lookups of the first scan launch: 16 per leaf per query (node bounds) plus
+    # 16 per member of every (leaf, query) pair that survived (per-series bounds)
+    lookups = 16.0 * leaves * nq1 + 16.0 * 64 * statistics.mean(pairs)
+    lk_peak = 148 * 32 * sm_mhz * 1e6  # one conflict-free 32-lane LDS wavefront per clock per SM
+    lk_rate = lookups / (lb_ms / 1e3)
+    scan_bytes = statistics.mean(scan_b) + 4.0 * statistics.mean(cand) * nq1 / Q
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            tr = json.load(f).get(wl.name, {})
+        traffic = tr.get("leafscan_dram_bytes")
+    except Exception:
+        pass
+    roofline = {"kernel": "leafscan_kernel<8>", "bound": "alu", "achieved": round(lk_rate / 1e12, 4),
+                "peak": round(lk_peak / 1e12, 4), "unit": "T LUT lookups/s", "frac": round(lk_rate / lk_peak, 4),
+                "traffic": traffic,
+                "peak_rule": "148 SMs x 32 lanes x SM clock (one conflict-free shared-memory wavefront per clock per SM); "
+                             "DESIGN.md sec. 6",
+                "lookups_per_launch": lookups, "launch_ms": round(lb_ms, 4),
+                "hbm_view": {"bytes_per_launch": scan_bytes, "achieved": round(scan_bytes / (lb_ms / 1e3) / 1e9, 1),
+                             "peak": hbm, "unit": "GB/s", "frac": round(scan_bytes / (lb_ms / 1e3) / 1e9 / hbm, 4),
+                             "peak_source": peak_src}}
+    rbytes = statistics.mean(ref_b)
+    kernels = {
+        "refine_q_kernel": {"bound": "hbm", "bytes_per_launch": rbytes, "launch_ms": round(rf_ms, 4),
+                            "achieved": round(rbytes / (rf_ms / 1e3) / 1e9, 1), "peak": hbm, "unit": "GB/s",
+                            "frac": round(rbytes / (rf_ms / 1e3) / 1e9 / hbm, 4),
+                            "bytes_rule": "2n B per half row read (n float32 per row), counted by the kernel"},
+        "ms_first_batch": {k: round(statistics.mean(v), 4) for k, v in kms.items()},
+    }
     out = {
         "metric": METRIC, "value": round(value, 2), "unit": "queries/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4), "higher_is_better": True,
@@ -281,6 +297,7 @@ def main():
                    else "working set fits in L2 (small config)",
                    "source": wl.cite},
         "roofline": roofline,
+        "kernels": kernels,
         "e2e": {"value": round(Q * e2e_steps * world / e2e_s, 2), "unit": "queries/s",
                 "h2d_bytes_per_step": Q * wl.n * 4, "d2h_bytes_per_step": Q * 12,
                 "how": "isax_nn1 on pinned host buffers, wall clock, copies inside"},
@@ -288,7 +305,7 @@ def main():
         "clocks": clocks,
         "build": {"seconds": round(build_s, 3), "mode": build_mode, "N": wl.N, "n": wl.n,
                   "input_GBps": round(raw_bytes / build_s / 1e9, 1), "index_device_bytes": ix.device_bytes},
-        "stats": {"candidates_per_query": cand_mean / Q, "refined_per_query": statistics.mean(refined) / Q,
+        "stats": {"candidates_per_query": statistics.mean(cand) / Q, "refined_per_query": statistics.mean(refined) / Q,
                   "rounds_max": max(rounds)},
     }
     if rank == 0 and not args.no_cpu_baseline:
@@ -300,6 +317,7 @@ def main():
     if rank == 0:
         print(json.dumps(out))
     if dist:
+        dist.barrier()
         dist.destroy_process_group()
 
 

@@ -79,7 +79,7 @@ static void free_scratch(isax_index *ix) {
     QueryScratch &q = ix->qs;
     cudaFree(q.qy); cudaFree(q.qpaa); cudaFree(q.qsax); cudaFree(q.lut); cudaFree(q.win); cudaFree(q.pwin); cudaFree(q.bsf);
     cudaFree(q.cand); cudaFree(q.cand_cnt); cudaFree(q.near); cudaFree(q.near_cnt); cudaFree(q.qmap); cudaFree(q.qband); cudaFree(q.cand_hist);
-    cudaFree(q.counters); cudaFree(q.counters_leaf); cudaFree(q.leaf_loads); cudaFree(q.task_ctr);
+    cudaFree(q.counters); cudaFree(q.counters_leaf); cudaFree(q.leaf_loads); cudaFree(q.task_ctr); cudaFree(q.refine_bytes);
     if (q.h_cnt) cudaFreeHost(q.h_cnt);
     q = QueryScratch{};
 }
@@ -111,6 +111,7 @@ static int alloc_scratch(isax_index *ix) {
     A(counters_leaf, Q);
     A(leaf_loads, 1);
     A(task_ctr, 1);
+    A(refine_bytes, 1);
 #undef A
     if (e == cudaSuccess) e = cudaMallocHost(&q.h_cnt, sizeof(uint32_t) * (size_t)Q * 8);
     if (e != cudaSuccess) {
@@ -260,6 +261,8 @@ static int nn1_device(isax_index *ix, const float *d_q, uint32_t Q, int64_t *d_i
     ix->st_launches = 0;
     ix->st_scan_bytes = ix->st_scan_bytes_first = 0;
     ISAX_CUDA(cudaMemsetAsync(qs.leaf_loads, 0, sizeof(unsigned long long), s));
+    ISAX_CUDA(cudaMemsetAsync(qs.refine_bytes, 0, sizeof(unsigned long long), s));
+    ix->st_refine_bytes_first = 0;
     // a device flag for non-finite queries
     uint32_t *flag = nullptr;
     ISAX_CUDA(cudaMalloc(&flag, sizeof(uint32_t)));
@@ -342,6 +345,13 @@ static int nn1_device(isax_index *ix, const float *d_q, uint32_t Q, int64_t *d_i
                 unsigned long long ll = 0;
                 ISAX_CUDA(cudaMemcpy(&ll, qs.leaf_loads, sizeof ll, cudaMemcpyDeviceToHost));
                 ix->st_scan_bytes_first = ix->st_scan_bytes + 1024ull * ll;
+                ISAX_CUDA(cudaMemcpy(&ll, qs.refine_bytes, sizeof ll, cudaMemcpyDeviceToHost));
+                ix->st_refine_bytes_first = ll;
+                std::vector<uint32_t> la(B);
+                ISAX_CUDA(cudaMemcpy(la.data(), qs.counters_leaf, B * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+                ix->st_leaf_pairs_first = 0;
+                for (uint32_t v : la) ix->st_leaf_pairs_first += v;
+                ix->st_scan_q_first = nact;
             }
             if (qs.h_cnt[2 * qs.cap_Q]) {
                 result = set_error(ISAX_E_NONFINITE, "a query holds NaN or Inf");
@@ -611,6 +621,10 @@ int isax_stats(const isax_index *cix, char *buf, size_t cap) {
     j += "\"launches\":" + std::to_string(ix->st_launches);
     j += ",\"scan_bytes\":" + std::to_string(ix->st_scan_bytes);
     j += ",\"scan_bytes_first_launch\":" + std::to_string(ix->st_scan_bytes_first);
+    j += ",\"refine_bytes_first_launch\":" + std::to_string(ix->st_refine_bytes_first);
+    j += ",\"leaf_pairs_first_launch\":" + std::to_string(ix->st_leaf_pairs_first);
+    j += ",\"scan_queries_first_launch\":" + std::to_string(ix->st_scan_q_first);
+    j += ",\"leaves\":" + std::to_string((ix->N + 63) / 64);
     j += "}";
     if (buf && cap) {
         size_t k = std::min(cap - 1, j.size());

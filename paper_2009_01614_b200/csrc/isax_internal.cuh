@@ -65,6 +65,7 @@ struct QueryScratch {
     uint32_t *counters_leaf = nullptr;  // [Q]: (leaf, query) pairs that survived the node bound
     unsigned long long *leaf_loads = nullptr;  // leaves whose 64 words the scan read (all launches of a call)
     uint32_t *task_ctr = nullptr;              // work counter of the persistent leaf scan
+    unsigned long long *refine_bytes = nullptr;  // bytes of rows the refine kernel read (all launches of a call)
     uint32_t *h_cnt = nullptr;      // pinned host mirror of cand_cnt + near_cnt + counters
 };
 
@@ -92,6 +93,8 @@ struct isax_index {
     isax::StageTimes st_ms;
     uint64_t st_launches = 0;  // kernels launched by the last nn1 call
     uint64_t st_scan_bytes = 0, st_scan_bytes_first = 0;  // summary bytes the scan read (all / first launch)
+    uint64_t st_refine_bytes_first = 0;                    // row bytes the first refine launch read
+    uint64_t st_leaf_pairs_first = 0, st_scan_q_first = 0; // (leaf, query) pairs kept / queries of the first scan
     cudaEvent_t ev[8] = {};
 };
 

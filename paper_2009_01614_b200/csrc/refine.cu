@@ -164,9 +164,11 @@ __global__ void __launch_bounds__(RF_THREADS) refine_q_kernel(const float *__res
                                                              unsigned long long *__restrict__ bsf,
                                                              NearEntry *__restrict__ near,
                                                              uint32_t *__restrict__ near_cnt,
-                                                             uint32_t *__restrict__ counters, float onepd) {
+                                                             uint32_t *__restrict__ counters, float onepd,
+                                                             unsigned long long *__restrict__ refine_bytes) {
     __shared__ uint32_t pre[RF_MAXQ + 1];
     const uint32_t t = threadIdx.x, lane = t & 31, ql = lane & 7;
+    unsigned long long rows_read = 0;  // half rows read by this quarter
     const uint32_t qmask = 0xFFu << (lane & 24);
     cand_prefix(cand_cnt, Q, cap, pre);
     const uint32_t total = pre[Q];
@@ -214,6 +216,7 @@ __global__ void __launch_bounds__(RF_THREADS) refine_q_kernel(const float *__res
                     atomicAdd(&counters[4 * cur_q + 0], done);
                     atomicAdd(&counters[4 * cur_q + 1], abandoned);
                 }
+                rows_read += 2 * done + abandoned;
                 done = abandoned = 0;
                 cur_q = q;
                 since = RF_REFRESH;
@@ -276,6 +279,8 @@ __global__ void __launch_bounds__(RF_THREADS) refine_q_kernel(const float *__res
         atomicAdd(&counters[4 * cur_q + 0], done);
         atomicAdd(&counters[4 * cur_q + 1], abandoned);
     }
+    rows_read += 2 * done + abandoned;
+    if (ql == 0 && rows_read) atomicAdd(refine_bytes, rows_read * 2ull * n);
 }
 
 void launch_refine(const isax_index *ix, uint32_t Q, float delta, cudaStream_t s) {
@@ -296,7 +301,7 @@ void launch_refine(const isax_index *ix, uint32_t Q, float delta, cudaStream_t s
     case K:                                                                                                         \
         refine_q_kernel<K><<<grid, RF_THREADS, 0, s>>>(ix->stored, ix->perm, ix->n, qs.qy, Q, qs.cand, qs.cand_cnt, \
                                                        qs.cand_cap, qs.bsf, qs.near, qs.near_cnt, qs.counters,      \
-                                                       onepd);                                                      \
+                                                       onepd, qs.refine_bytes);                                     \
         break;
             RQ_CASE(1) RQ_CASE(2) RQ_CASE(3) RQ_CASE(4)
 #undef RQ_CASE
