@@ -31,6 +31,21 @@ __device__ __forceinline__ uint4 ld_stream(const uint4 *p) {
 
 __device__ __forceinline__ uint32_t byte_of(const uint32_t (&v)[4], int s) { return (v[s >> 2] >> (8 * (s & 3))) & 0xFFu; }
 
+// packed 16-bit lane min / max (native on sm_90+; the byte-lane __vminu4 is emulated)
+__device__ __forceinline__ uint32_t max_u16x2(uint32_t a, uint32_t b) {
+    uint32_t d;
+    asm("max.u16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+    return d;
+}
+__device__ __forceinline__ uint32_t min_u16x2(uint32_t a, uint32_t b) {
+    uint32_t d;
+    asm("min.u16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+    return d;
+}
+// bytes (b0, b1, b2, b3) of w -> u16x2 (b0, b1) and (b2, b3)
+__device__ __forceinline__ uint32_t lo_u16x2(uint32_t w) { return __byte_perm(w, 0u, 0x4140); }
+__device__ __forceinline__ uint32_t hi_u16x2(uint32_t w) { return __byte_perm(w, 0u, 0x4342); }
+
 // the fp32 LB^2 of one word against one LUT, segments 0..15 left to right
 __device__ __forceinline__ float word_lb(const float *L, const uint4 &wv) {
     const uint32_t v[4] = {wv.x, wv.y, wv.z, wv.w};
@@ -215,7 +230,7 @@ __global__ void __launch_bounds__(LF_THREADS, 1) leafscan_kernel(
     uint32_t *cbuf = reinterpret_cast<uint32_t *>(slut + G * W * CARD);
     uint32_t *worklist = cbuf + G * CBUF;  // (leaf offset in chunk) | (query mask << 16)
     __shared__ QConst qc[G];
-    __shared__ uint4 qsym[G];
+    __shared__ uint4 qsym[G][2];  // the query's 16 symbols as 8 u16x2 pairs
     __shared__ uint32_t qid[G], cb_cnt[G], alive_cnt[G], fbase[G];
     __shared__ uint32_t shist[G][HIST_BINS];
     __shared__ uint32_t wl_cnt, s_task;
@@ -272,7 +287,9 @@ __global__ void __launch_bounds__(LF_THREADS, 1) leafscan_kernel(
                 qid[t] = qi;
                 cb_cnt[t] = 0;
                 alive_cnt[t] = 0;
-                qsym[t] = reinterpret_cast<const uint4 *>(qsax_all)[qi];
+                const uint4 w = reinterpret_cast<const uint4 *>(qsax_all)[qi];
+                qsym[t][0] = make_uint4(lo_u16x2(w.x), hi_u16x2(w.x), lo_u16x2(w.y), hi_u16x2(w.y));
+                qsym[t][1] = make_uint4(lo_u16x2(w.z), hi_u16x2(w.z), lo_u16x2(w.w), hi_u16x2(w.w));
                 qc[t] = load_qconst(qi, valid, bsf, band, g0 + t, win, onepd);
             }
             __syncthreads();
@@ -287,8 +304,11 @@ __global__ void __launch_bounds__(LF_THREADS, 1) leafscan_kernel(
             mx_n = __ldg(meta4 + 2 * (uint64_t)leaf + 1);
         }
         for (; leaf - lane < c1; leaf += 32 * NW) {
-            const uint32_t mn[4] = {mn_n.x, mn_n.y, mn_n.z, mn_n.w};
-            const uint32_t mx[4] = {mx_n.x, mx_n.y, mx_n.z, mx_n.w};
+            // the leaf's per-segment [min, max] as u16x2 pairs (segments 2j, 2j+1)
+            const uint32_t mn[8] = {lo_u16x2(mn_n.x), hi_u16x2(mn_n.x), lo_u16x2(mn_n.y), hi_u16x2(mn_n.y),
+                                    lo_u16x2(mn_n.z), hi_u16x2(mn_n.z), lo_u16x2(mn_n.w), hi_u16x2(mn_n.w)};
+            const uint32_t mx[8] = {lo_u16x2(mx_n.x), hi_u16x2(mx_n.x), lo_u16x2(mx_n.y), hi_u16x2(mx_n.y),
+                                    lo_u16x2(mx_n.z), hi_u16x2(mx_n.z), lo_u16x2(mx_n.w), hi_u16x2(mx_n.w)};
             const uint32_t nxt = leaf + 32 * NW;
             if (nxt < c1) {  // software pipeline: the next node summary is in flight
                 mn_n = __ldg(meta4 + 2 * (uint64_t)nxt);
@@ -297,15 +317,15 @@ __global__ void __launch_bounds__(LF_THREADS, 1) leafscan_kernel(
             uint32_t alive = 0;
 #pragma unroll
             for (int g = 0; g < G; g++) {
-                const uint4 q4 = qsym[g];
-                const uint32_t qv[4] = {q4.x, q4.y, q4.z, q4.w};
-                uint32_t cl[4];
+                const uint4 qa = qsym[g][0], qb = qsym[g][1];
+                const uint32_t qv[8] = {qa.x, qa.y, qa.z, qa.w, qb.x, qb.y, qb.z, qb.w};
+                uint32_t cl[8];
 #pragma unroll
-                for (int k = 0; k < 4; k++) cl[k] = __vminu4(__vmaxu4(qv[k], mn[k]), mx[k]);
+                for (int k = 0; k < 8; k++) cl[k] = min_u16x2(max_u16x2(qv[k], mn[k]), mx[k]);
                 const float *L = slut + g * W * CARD;
                 float lb = 0.f;
 #pragma unroll
-                for (int s2 = 0; s2 < W; s2++) lb += L[s2 * CARD + byte_of(cl, s2)];
+                for (int s2 = 0; s2 < W; s2++) lb += L[s2 * CARD + ((cl[s2 >> 1] >> (16 * (s2 & 1))) & 0xFFFFu)];
                 if (lb <= qc[g].T) alive |= 1u << g;
             }
             if (leaf >= c1) alive = 0;

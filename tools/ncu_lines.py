@@ -26,8 +26,12 @@ for r in csv.reader(io.StringIO(raw)):
         continue
     if hdr is None or len(r) <= ai or not r[0].isdigit():
         continue
+    try:
+        v = float(r[ai] or 0)
+    except ValueError:  # a source line whose quotes broke the CSV
+        continue
     key = (cur_file, int(r[0]), r[1].strip()[:100])
-    agg[key] = agg.get(key, 0.0) + float(r[ai] or 0)
+    agg[key] = agg.get(key, 0.0) + v
 tot = sum(agg.values()) or 1
 for (f, ln, src), v in sorted(agg.items(), key=lambda kv: -kv[1])[:top]:
     print(f"{100 * v / tot:5.1f}%  {f}:{ln}  {src}")
