@@ -59,4 +59,21 @@ __device__ __forceinline__ double warp_sum_d(double v) {
 
 __device__ __forceinline__ float bsf_d2(unsigned long long p) { return __uint_as_float((uint32_t)(p >> 32)); }
 
+// y = fp32_rne(fl64((x - mu) / sd)), the stored value of R2/R3, without a full fp64 division per
+// element. q = (x - mu) * rcp, with rcp = fl64(1/sd), is within 2.5 fp64 ulps of the correctly
+// rounded quotient Q. If rounding q +- 8 ulp steps (>= 4 ulps even across a binade) to fp32 gives
+// one value, rounding Q gives it too
+// (Q lies between them and rounding is monotone). Otherwise, about once in 1e8 elements, the true
+// division decides. The result equals the definition bit for bit.
+__device__ __forceinline__ float znorm_value(float x, double mu, double sd, double rcp) {
+    const double t = __dsub_rn((double)x, mu);
+    const double q = __dmul_rn(t, rcp);
+    if (q == 0.0) return __double2float_rn(__ddiv_rn(t, sd));
+    const long long b = __double_as_longlong(q);
+    const float y1 = __double2float_rn(__longlong_as_double(b + 8));
+    const float y2 = __double2float_rn(__longlong_as_double(b - 8));
+    if (y1 == y2) return y1;
+    return __double2float_rn(__ddiv_rn(t, sd));
+}
+
 }  // namespace isax

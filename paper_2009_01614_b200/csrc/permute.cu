@@ -11,21 +11,22 @@
 
 namespace isax {
 
-__device__ __forceinline__ float zval(float x, double mu, double sd, bool flat) {
-    return flat ? 0.0f : __double2float_rn(__ddiv_rn(__dsub_rn((double)x, mu), sd));
+__device__ __forceinline__ float zval(float x, double mu, double sd, bool flat, double rcp) {
+    return flat ? 0.0f : znorm_value(x, mu, sd, rcp);
 }
 
 __device__ __forceinline__ void norm_row(const float *__restrict__ src, float *__restrict__ dst, double2 ms,
                                          uint32_t n, uint32_t lane) {
     const bool flat = ms.y < 1e-12;
+    const double rcp = __drcp_rn(ms.y);
     const float4 *s4 = reinterpret_cast<const float4 *>(src);
     float4 *d4 = reinterpret_cast<float4 *>(dst);
     for (uint32_t i = lane; i < n / 4; i += 32) {
         float4 v = __ldcs(s4 + i);
-        v.x = zval(v.x, ms.x, ms.y, flat);
-        v.y = zval(v.y, ms.x, ms.y, flat);
-        v.z = zval(v.z, ms.x, ms.y, flat);
-        v.w = zval(v.w, ms.x, ms.y, flat);
+        v.x = zval(v.x, ms.x, ms.y, flat, rcp);
+        v.y = zval(v.y, ms.x, ms.y, flat, rcp);
+        v.z = zval(v.z, ms.x, ms.y, flat, rcp);
+        v.w = zval(v.w, ms.x, ms.y, flat, rcp);
         d4[i] = v;
     }
 }

@@ -43,37 +43,67 @@ __global__ void __launch_bounds__(RS_THREADS) rs_hist(const uint4 *__restrict__ 
     hist[(uint64_t)threadIdx.x * gridDim.x + blockIdx.x] = h[threadIdx.x];
 }
 
-// Exclusive scan in place over `len` u32 with one block of 1024 threads.
-__global__ void __launch_bounds__(1024) rs_scan(uint32_t *__restrict__ a, uint64_t len) {
-    __shared__ uint32_t part[1024];
-    const uint64_t per = (len + 1023) / 1024;
-    const uint64_t s0 = threadIdx.x * per, s1 = umin64(len, s0 + per);
-    uint32_t sum = 0;
-    for (uint64_t i = s0; i < s1; i++) sum += a[i];
-    part[threadIdx.x] = sum;
-    __syncthreads();
-    for (int off = 1; off < 1024; off <<= 1) {
-        uint32_t v = threadIdx.x >= (unsigned)off ? part[threadIdx.x - off] : 0;
-        __syncthreads();
-        part[threadIdx.x] += v;
-        __syncthreads();
+// Per-digit exclusive scan over the blocks: CTA d scans hist[d][0..nb) in place and writes the
+// digit total. The scatter adds the exclusive prefix of the totals (its own 256-entry scan).
+constexpr int SC_THREADS = 1024;
+
+__device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t *tot) {
+    __shared__ uint32_t ws[32];
+    const uint32_t t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    uint32_t inc = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t u = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= (uint32_t)o) inc += u;
     }
-    uint32_t run = part[threadIdx.x] - sum;  // exclusive
-    for (uint64_t i = s0; i < s1; i++) {
-        uint32_t v = a[i];
-        a[i] = run;
+    if (lane == 31) ws[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+        const uint32_t nw = blockDim.x / 32;
+        uint32_t x = lane < nw ? ws[lane] : 0, xi = x;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t u = __shfl_up_sync(0xffffffffu, xi, o);
+            if (lane >= (uint32_t)o) xi += u;
+        }
+        if (lane < nw) ws[lane] = xi - x;
+        if (lane == nw - 1 && tot) *tot = xi;
+    }
+    __syncthreads();
+    const uint32_t r = ws[warp] + inc - v;
+    __syncthreads();
+    return r;
+}
+
+__global__ void __launch_bounds__(SC_THREADS) rs_scan_digits(uint32_t *__restrict__ hist, uint32_t nb,
+                                                             uint32_t *__restrict__ dtotal) {
+    __shared__ uint32_t total;
+    const uint32_t d = blockIdx.x;
+    uint32_t *h = hist + (uint64_t)d * nb;
+    const uint32_t per = (nb + SC_THREADS - 1) / SC_THREADS;
+    const uint32_t s0 = threadIdx.x * per, s1 = min(nb, s0 + per);
+    uint32_t sum = 0;
+    for (uint32_t i = s0; i < s1; i++) sum += h[i];
+    uint32_t run = block_exclusive_scan(sum, &total);
+    for (uint32_t i = s0; i < s1; i++) {
+        const uint32_t v = h[i];
+        h[i] = run;
         run += v;
     }
+    __syncthreads();
+    if (threadIdx.x == 0) dtotal[d] = total;
 }
 
 __global__ void __launch_bounds__(RS_THREADS) rs_scatter(const uint4 *__restrict__ kin, const uint32_t *__restrict__ vin,
                                                          uint4 *__restrict__ kout, uint32_t *__restrict__ vout,
                                                          uint64_t N, uint64_t per_block, int pass,
-                                                         const uint32_t *__restrict__ offs) {
+                                                         const uint32_t *__restrict__ offs,
+                                                         const uint32_t *__restrict__ dtotal) {
     __shared__ uint32_t base[256];
     __shared__ uint32_t wcnt[RS_WARPS][256];
     const uint32_t t = threadIdx.x, lane = t & 31, warp = t >> 5;
-    base[t] = offs[(uint64_t)t * gridDim.x + blockIdx.x];
+    const uint32_t doff = block_exclusive_scan(dtotal[t], nullptr);  // start of digit t's output
+    base[t] = doff + offs[(uint64_t)t * gridDim.x + blockIdx.x];
 #pragma unroll
     for (int w = 0; w < RS_WARPS; w++) wcnt[w][t] = 0;
     __syncthreads();
@@ -132,7 +162,7 @@ int radix_sort_keys(uint4 *keys, uint32_t *ids, uint64_t N, uint32_t *perm_out, 
     uint4 *k2 = nullptr;
     uint32_t *hist = nullptr;
     ISAX_CUDA(cudaMalloc(&k2, N * sizeof(uint4)));
-    cudaError_t e = cudaMalloc(&hist, nb * 256 * sizeof(uint32_t));
+    cudaError_t e = cudaMalloc(&hist, (nb * 256 + 256) * sizeof(uint32_t));
     if (e != cudaSuccess) {
         cudaFree(k2);
         return cuda_error(e, "cudaMalloc(sort hist)");
@@ -141,8 +171,8 @@ int radix_sort_keys(uint4 *keys, uint32_t *ids, uint64_t N, uint32_t *perm_out, 
     uint32_t *va = ids, *vb = perm_out;
     for (int pass = 0; pass < 16; pass++) {
         rs_hist<<<(unsigned)nb, RS_THREADS, 0, s>>>(ka, N, per_block, pass, hist);
-        rs_scan<<<1, 1024, 0, s>>>(hist, nb * 256);
-        rs_scatter<<<(unsigned)nb, RS_THREADS, 0, s>>>(ka, va, kb, vb, N, per_block, pass, hist);
+        rs_scan_digits<<<256, SC_THREADS, 0, s>>>(hist, (uint32_t)nb, hist + nb * 256);
+        rs_scatter<<<(unsigned)nb, RS_THREADS, 0, s>>>(ka, va, kb, vb, N, per_block, pass, hist, hist + nb * 256);
         std::swap(ka, kb);
         std::swap(va, vb);
     }

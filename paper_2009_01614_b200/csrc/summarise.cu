@@ -21,61 +21,101 @@ namespace isax {
 
 __constant__ double c_beta[ISAX_NBETA] = ISAX_BETA_INIT;
 
-__global__ void __launch_bounds__(32) summarise_kernel(const float *__restrict__ x, uint64_t count, uint32_t n,
+// NT = n when the kernel is specialised for it (index math by a constant), 0 = generic n.
+template <uint32_t NT>
+__global__ void __launch_bounds__(32) summarise_kernel(const float *__restrict__ x, uint64_t count, uint32_t n_rt,
                                                          uint64_t id0, uint8_t *__restrict__ sax_by_id,
                                                          uint4 *__restrict__ key, double2 *__restrict__ musig,
                                                          uint32_t *__restrict__ bad) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     double *beta = reinterpret_cast<double *>(smem_raw);
-    float *rows = reinterpret_cast<float *>(smem_raw + ISAX_NBETA * sizeof(double) + 8);
+    double2 *ms = reinterpret_cast<double2 *>(smem_raw + ISAX_NBETA * sizeof(double) + 8);  // [32] (mu, sigma)
+    float *rows = reinterpret_cast<float *>(ms + 32);
+    const uint32_t n = NT ? NT : n_rt;
     const uint32_t lane = threadIdx.x;
-    const uint32_t stride = n + 1;
+    const uint32_t stride = n + 1;  // bank = (lane + i) mod 32 for the per-thread sequential reads
     for (uint32_t k = lane; k < ISAX_NBETA; k += 32) beta[k] = c_beta[k];
     const uint32_t seg = n / W;
+    const uint32_t per_row = n / 4;
     const uint64_t ngroups = (count + 31) / 32;
     for (uint64_t g = blockIdx.x; g < ngroups; g += gridDim.x) {
         const uint64_t r0 = g * 32;
         const uint32_t nrows = (uint32_t)umin64(32, count - r0);
         __syncwarp();
-        // stage: each instruction reads 512 contiguous bytes of one row
-        for (uint32_t r = 0; r < nrows; r++) {
-            const float4 *src = reinterpret_cast<const float4 *>(x + (r0 + r) * n);
-#pragma unroll 4
-            for (uint32_t i = lane; i < n / 4; i += 32) {
-                float4 v = __ldcs(src + i);
-                float *d = rows + r * stride + 4 * i;
-                d[0] = v.x; d[1] = v.y; d[2] = v.z; d[3] = v.w;
+        // stage the 32 rows (contiguous in memory): lane l moves float4 e = l, l+32, ... of the
+        // tile, 16 loads in flight per lane before the shared stores (each warp instruction reads
+        // 512 contiguous bytes)
+        {
+            const uint32_t total = nrows * per_row;
+            const float4 *src = reinterpret_cast<const float4 *>(x + r0 * n);
+            constexpr uint32_t B = 16;
+            for (uint32_t e0 = 0; e0 < total; e0 += 32 * B) {
+                float4 v[B];
+#pragma unroll
+                for (uint32_t k = 0; k < B; k++) {
+                    const uint32_t e = e0 + k * 32 + lane;
+                    if (e < total) v[k] = __ldcs(src + e);
+                }
+#pragma unroll
+                for (uint32_t k = 0; k < B; k++) {
+                    const uint32_t e = e0 + k * 32 + lane;
+                    if (e < total) {
+                        float *d = rows + (e / per_row) * stride + 4 * (e % per_row);
+                        d[0] = v[k].x; d[1] = v[k].y; d[2] = v[k].z; d[3] = v[k].w;
+                    }
+                }
             }
         }
         __syncwarp();
+        bool finite = true;
         if (lane < nrows) {
-            float *row = rows + lane * stride;
-            // C1: mu and sigma, left to right (R2, R3)
+            const float *row = rows + lane * stride;
+            // C1: mu and sigma, left to right (R2, R3). These two chains are the only sequential
+            // parts; the loops are unrolled so the shared loads run ahead of the add chain.
             double s = 0.0;
-            bool finite = true;
+#pragma unroll 16
             for (uint32_t i = 0; i < n; i++) {
-                float v = row[i];
+                const float v = row[i];
                 finite &= isfinite(v);
                 s = __dadd_rn(s, (double)v);
             }
             const double mu = __ddiv_rn(s, (double)n);
             double s2 = 0.0;
+#pragma unroll 16
             for (uint32_t i = 0; i < n; i++) {
-                double t = __dsub_rn((double)row[i], mu);
+                const double t = __dsub_rn((double)row[i], mu);
                 s2 = __dadd_rn(s2, __dmul_rn(t, t));
             }
-            const double sd = __dsqrt_rn(__ddiv_rn(s2, (double)n));
-            const bool flat = sd < 1e-12;
-            for (uint32_t i = 0; i < n; i++)
-                row[i] = flat ? 0.0f : __double2float_rn(__ddiv_rn(__dsub_rn((double)row[i], mu), sd));
-            // C2 + C4: PAA means (left to right per segment) and symbols
+            ms[lane] = make_double2(mu, __dsqrt_rn(__ddiv_rn(s2, (double)n)));
+        }
+        __syncwarp();
+        // y = fp32((x - mu) / sigma) for the whole tile, warp-cooperatively: the divisions are
+        // independent, so all 32 lanes stream them with full ILP; y overwrites x in place
+        double rcp = 0.0;
+        if (lane < nrows) rcp = __drcp_rn(ms[lane].y);
+        for (uint32_t r = 0; r < nrows; r++) {
+            const double2 m = ms[r];
+            const double rr = __shfl_sync(0xffffffffu, rcp, r);
+            float *p = rows + r * stride;
+#pragma unroll 4
+            for (uint32_t c = lane; c < n; c += 32)
+                p[c] = m.y < 1e-12 ? 0.0f : znorm_value(p[c], m.x, m.y, rr);
+        }
+        __syncwarp();
+        if (lane < nrows) {
+            const float *row = rows + lane * stride;
+            // C2: the 16 segment sums, left to right within each segment, interleaved across segments
+            double acc[W];
+#pragma unroll
+            for (int sg = 0; sg < W; sg++) acc[sg] = 0.0;
+            for (uint32_t j = 0; j < seg; j++) {
+#pragma unroll
+                for (int sg = 0; sg < W; sg++) acc[sg] = __dadd_rn(acc[sg], (double)row[sg * seg + j]);
+            }
+            // C4: symbols, 16 independent binary searches
             uint32_t sym[W];
 #pragma unroll
-            for (int sg = 0; sg < W; sg++) {
-                double acc = 0.0;
-                for (uint32_t j = 0; j < seg; j++) acc = __dadd_rn(acc, (double)row[sg * seg + j]);
-                sym[sg] = sax_symbol(beta, __ddiv_rn(acc, (double)seg));
-            }
+            for (int sg = 0; sg < W; sg++) sym[sg] = sax_symbol(beta, __ddiv_rn(acc[sg], (double)seg));
             const uint64_t id = id0 + r0 + lane;
             uint4 wv;
             wv.x = sym[0] | (sym[1] << 8) | (sym[2] << 16) | (sym[3] << 24);
@@ -84,28 +124,36 @@ __global__ void __launch_bounds__(32) summarise_kernel(const float *__restrict__
             wv.w = sym[12] | (sym[13] << 8) | (sym[14] << 16) | (sym[15] << 24);
             reinterpret_cast<uint4 *>(sax_by_id)[id] = wv;
             key[id] = isax_key(sym);
-            musig[id] = make_double2(mu, sd);
+            musig[id] = ms[lane];
             if (!finite) atomicOr(bad, 1u);
         }
     }
 }
 
-void launch_summarise(const float *x, uint64_t count, uint32_t n, uint64_t id0, uint8_t *sax_by_id, uint4 *key,
-                      double2 *musig, uint32_t *bad, cudaStream_t s) {
-    if (count == 0) return;
-    const size_t smem = ISAX_NBETA * sizeof(double) + 8 + 32 * (size_t)(n + 1) * sizeof(float);
+template <uint32_t NT>
+static void launch_summarise_t(const float *x, uint64_t count, uint32_t n, uint64_t id0, uint8_t *sax_by_id,
+                               uint4 *key, double2 *musig, uint32_t *bad, cudaStream_t s) {
+    const size_t smem = ISAX_NBETA * sizeof(double) + 8 + 32 * sizeof(double2) + 32 * (size_t)(n + 1) * sizeof(float);
     static size_t configured = 0;
     if (smem > configured) {
-        cudaFuncSetAttribute(summarise_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(summarise_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         configured = smem;
     }
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int per_sm = (int)std::max<size_t>(1, std::min<size_t>(16, (227 * 1024) / (smem + 1024)));
+    const int per_sm = (int)std::max<size_t>(1, std::min<size_t>(32, (227 * 1024) / (smem + 1024)));
     const uint64_t groups = (count + 31) / 32;
     const uint64_t grid = umin64(groups, (uint64_t)sms * per_sm);
-    summarise_kernel<<<(unsigned)grid, 32, smem, s>>>(x, count, n, id0, sax_by_id, key, musig, bad);
+    summarise_kernel<NT><<<(unsigned)grid, 32, smem, s>>>(x, count, n, id0, sax_by_id, key, musig, bad);
+}
+
+void launch_summarise(const float *x, uint64_t count, uint32_t n, uint64_t id0, uint8_t *sax_by_id, uint4 *key,
+                      double2 *musig, uint32_t *bad, cudaStream_t s) {
+    if (count == 0) return;
+    if (n == 256) launch_summarise_t<256>(x, count, n, id0, sax_by_id, key, musig, bad, s);
+    else if (n == 128) launch_summarise_t<128>(x, count, n, id0, sax_by_id, key, musig, bad, s);
+    else launch_summarise_t<0>(x, count, n, id0, sax_by_id, key, musig, bad, s);
 }
 
 }  // namespace isax
