@@ -257,6 +257,7 @@ static int nn1_device(isax_index *ix, const float *d_q, uint32_t Q, int64_t *d_i
     ix->st_near.assign(Q, 0);
     ix->st_leaves.assign(Q, 0);
     ix->st_bsf0.assign(Q, 0.f);
+    ix->st_bsf_final.assign(Q, 0.f);
     ix->st_ms = StageTimes{};
     ix->st_launches = 0;
     ix->st_scan_bytes = ix->st_scan_bytes_first = 0;
@@ -365,6 +366,7 @@ static int nn1_device(isax_index *ix, const float *d_q, uint32_t Q, int64_t *d_i
                 const uint32_t i = hmap[k];
                 const uint32_t cnt = qs.h_cnt[i];
                 bsf_h[i] = bsf_d2_host(bsf_now[i]);
+                ix->st_bsf_final[b0 + i] = bsf_h[i];
                 ix->st_cand[b0 + i] += std::min(cnt, qs.cand_cap);
                 ix->st_rounds[b0 + i] = round + 1;
                 if (qs.h_cnt[qs.cap_Q + i] > (uint32_t)NEAR_K) {  // near overflow: start over, BSF kept
@@ -611,6 +613,13 @@ int isax_stats(const isax_index *cix, char *buf, size_t cap) {
     arr("rounds", ix->st_rounds, false);
     arr("near", ix->st_near, false);
     arr("leaves_alive", ix->st_leaves, false);
+    j += "\"bsf_final_d2\":[";
+    for (size_t i = 0; i < ix->st_bsf_final.size(); i++) {
+        char b[32];
+        snprintf(b, sizeof b, "%s%.9g", i ? "," : "", ix->st_bsf_final[i]);
+        j += b;
+    }
+    j += "],";
     j += "\"bsf0_d2\":[";
     for (size_t i = 0; i < ix->st_bsf0.size(); i++) {
         char b[32];

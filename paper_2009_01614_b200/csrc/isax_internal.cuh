@@ -89,7 +89,7 @@ struct isax_index {
     std::mutex mu;
     // last-call statistics (host copies)
     std::vector<uint32_t> st_win, st_cand, st_refined, st_abandoned, st_rounds, st_near, st_leaves;
-    std::vector<float> st_bsf0;
+    std::vector<float> st_bsf0, st_bsf_final;
     isax::StageTimes st_ms;
     uint64_t st_launches = 0;  // kernels launched by the last nn1 call
     uint64_t st_scan_bytes = 0, st_scan_bytes_first = 0;  // summary bytes the scan read (all / first launch)

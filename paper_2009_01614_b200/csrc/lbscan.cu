@@ -55,6 +55,22 @@ __device__ __forceinline__ float word_lb(const float *L, const uint4 &wv) {
     return lb;
 }
 
+// sum of the u8 LUT entries of one word. ub is the shared address of the query's [16][256] u8
+// table (256-aligned, < 2^24): PRMT merges symbol byte s into the low byte of ub, and the segment
+// offset s * 256 becomes the load's immediate.
+__device__ __forceinline__ uint32_t ld_sh_u8(uint32_t addr) {
+    uint32_t r;
+    asm volatile("ld.shared.u8 %0, [%1];" : "=r"(r) : "r"(addr));
+    return r;
+}
+__device__ __forceinline__ uint32_t word_e8(uint32_t ub, const uint4 &wv) {
+    const uint32_t v[4] = {wv.x, wv.y, wv.z, wv.w};
+    uint32_t es = 0;
+#pragma unroll
+    for (int s = 0; s < W; s++) es += ld_sh_u8(__byte_perm(v[s >> 2], ub, 0x7650u | (uint32_t)(s & 3)) + s * CARD);
+    return es;
+}
+
 // histogram bin of a kept bound inside its band (for the host's band shrinking)
 __device__ __forceinline__ uint32_t hist_bin(float lb, float lo, float hi) {
     const float l0 = fmaxf(lo, 0.f);
@@ -188,7 +204,7 @@ static void launch_g(const isax_index *ix, uint32_t nq, const uint32_t *qmap, co
 constexpr uint32_t LEAF = 64;
 constexpr int LF_THREADS = 1024;
 constexpr uint32_t CHUNK = 8192;  // max leaves per phase-A/phase-B round of a CTA
-constexpr uint32_t CBUF = 1024;   // shared candidate buffer per query slot
+constexpr uint32_t CBUF = 512;    // shared candidate buffer per query slot
 
 // append `keep` lanes' positions for query slot g: shared buffer first, global list if it is full
 __device__ __forceinline__ void emit(bool keep, uint32_t pos, uint32_t g, uint32_t q, uint32_t lane, uint32_t lt,
@@ -226,8 +242,14 @@ __global__ void __launch_bounds__(LF_THREADS, 1) leafscan_kernel(
     const uint32_t *__restrict__ win, float onepd, uint32_t *__restrict__ cand, uint32_t *__restrict__ cand_cnt,
     uint32_t cap, uint32_t *__restrict__ hist, uint32_t *__restrict__ leaves_alive,
     unsigned long long *__restrict__ leaf_loads, uint32_t *__restrict__ task_ctr) {
-    extern __shared__ __align__(16) float slut[];  // [G][16][256] LUTs, [G][CBUF] candidates, [CHUNK] worklist
-    uint32_t *cbuf = reinterpret_cast<uint32_t *>(slut + G * W * CARD);
+    // shared: [G][16][256] fp32 LUTs | [G][16][256] u8 LUTs | [G][CBUF] candidates | [CHUNK] worklist
+    // (the dynamic region follows the static variables, so the u8 tables are aligned by hand: the
+    // PRMT address trick needs a 256-aligned base)
+    extern __shared__ __align__(16) float slut[];
+    const uint32_t raw8 = (uint32_t)__cvta_generic_to_shared(slut + G * W * CARD);
+    const uint32_t lut8_sh = (raw8 + 255u) & ~255u;
+    uint8_t *lut8 = reinterpret_cast<uint8_t *>(slut + G * W * CARD) + (lut8_sh - raw8);
+    uint32_t *cbuf = reinterpret_cast<uint32_t *>(lut8 + G * W * CARD);
     uint32_t *worklist = cbuf + G * CBUF;  // (leaf offset in chunk) | (query mask << 16)
     __shared__ QConst qc[G];
     __shared__ uint4 qsym[G][2];  // the query's 16 symbols as 8 u16x2 pairs
@@ -291,6 +313,18 @@ __global__ void __launch_bounds__(LF_THREADS, 1) leafscan_kernel(
                 qsym[t][0] = make_uint4(lo_u16x2(w.x), hi_u16x2(w.x), lo_u16x2(w.y), hi_u16x2(w.y));
                 qsym[t][1] = make_uint4(lo_u16x2(w.z), hi_u16x2(w.z), lo_u16x2(w.w), hi_u16x2(w.w));
                 qc[t] = load_qconst(qi, valid, bsf, band, g0 + t, win, onepd);
+            }
+            __syncthreads();
+            // u8 LUT (R12): e = floor(LUT * 254 / T), rounded down at every step and clamped at 255,
+            // so sum_s e <= LB^2 * 254 / T; "sum e > 254" implies LB^2 > T and prunes a member exactly
+            for (uint32_t e = t; e < G * W * CARD; e += LF_THREADS) {
+                const float T = qc[e / (W * CARD)].T;
+                uint32_t v = 255;
+                if (T > 0.f) {
+                    const float x = __fmul_rd(slut[e], __fdiv_rd(254.0f, T));
+                    v = x >= 255.f ? 255u : (uint32_t)x;
+                }
+                lut8[e] = (uint8_t)v;
             }
             __syncthreads();
         }
@@ -365,13 +399,17 @@ __global__ void __launch_bounds__(LF_THREADS, 1) leafscan_kernel(
 #pragma unroll 1
                 for (uint32_t mm = am; mm; mm &= mm - 1) {
                     const uint32_t g = __ffs(mm) - 1;
-                    const QConst kq = qc[g];
-                    const float *L = slut + g * W * CARD;
+                    const uint32_t ub = lut8_sh + g * W * CARD;  // this query's u8 LUT (256-aligned)
 #pragma unroll
                     for (int u = 0; u < 2; u++) {
                         const uint32_t pos = base + u * 32 + lane;
-                        const float lb = word_lb(L, wv[k][u]);
-                        const bool keep = pos < N && lb > kq.lo && lb <= kq.T && (pos < kq.ws || pos >= kq.we);
+                        // integer filter: 3 instructions per lookup (PRMT address, LDS.U8, IADD)
+                        const bool maybe = pos < N && word_e8(ub, wv[k][u]) <= 254u;
+                        if (!__any_sync(0xffffffffu, maybe)) continue;
+                        // rare: the exact fp32 test, the same rule as the flat scan
+                        const QConst kq = qc[g];
+                        const float lb = maybe ? word_lb(slut + g * W * CARD, wv[k][u]) : 0.f;
+                        const bool keep = maybe && lb > kq.lo && lb <= kq.T && (pos < kq.ws || pos >= kq.we);
                         if (keep) atomicAdd(&shist[g][hist_bin(lb, kq.lo, kq.T)], 1u);
                         emit(keep, pos, g, qid[g], lane, lt, cbuf, cb_cnt, cand, cand_cnt, cap);
                     }
@@ -388,7 +426,7 @@ __global__ void __launch_bounds__(LF_THREADS, 1) leafscan_kernel(
 template <int G>
 static void launch_leaf(const isax_index *ix, uint32_t nq, const uint32_t *qmap, const float2 *band, float onepd,
                         cudaStream_t s) {
-    const size_t smem = (size_t)G * W * CARD * sizeof(float) + (size_t)G * CBUF * sizeof(uint32_t) + CHUNK * 4;
+    const size_t smem = (size_t)G * W * CARD * (sizeof(float) + 1) + 256 + (size_t)G * CBUF * sizeof(uint32_t) + CHUNK * 4;
     static bool configured = false;
     if (!configured) {
         cudaFuncSetAttribute(leafscan_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
