@@ -245,10 +245,10 @@ __global__ void __launch_bounds__(LF_THREADS, 1) leafscan_kernel(
     // shared: [G][16][256] fp32 LUTs | [G][16][256] u8 LUTs | [G][CBUF] candidates | [CHUNK] worklist
     // (the dynamic region follows the static variables, so the u8 tables are aligned by hand: the
     // PRMT address trick needs a 256-aligned base)
-    extern __shared__ __align__(16) float slut[];
-    const uint32_t raw8 = (uint32_t)__cvta_generic_to_shared(slut + G * W * CARD);
+    extern __shared__ __align__(16) uint8_t smem_dyn[];
+    const uint32_t raw8 = (uint32_t)__cvta_generic_to_shared(smem_dyn);
     const uint32_t lut8_sh = (raw8 + 255u) & ~255u;
-    uint8_t *lut8 = reinterpret_cast<uint8_t *>(slut + G * W * CARD) + (lut8_sh - raw8);
+    uint8_t *lut8 = smem_dyn + (lut8_sh - raw8);
     uint32_t *cbuf = reinterpret_cast<uint32_t *>(lut8 + G * W * CARD);
     uint32_t *worklist = cbuf + G * CBUF;  // (leaf offset in chunk) | (query mask << 16)
     __shared__ QConst qc[G];
@@ -297,11 +297,6 @@ __global__ void __launch_bounds__(LF_THREADS, 1) leafscan_kernel(
         if (grp * G != g0) {  // new query group: load its LUTs and constants
             if (g0 != 0xffffffffu) flush();
             g0 = grp * G;
-            for (uint32_t e = t; e < G * W * CARD; e += LF_THREADS) {
-                const uint32_t g = e / (W * CARD);
-                const uint32_t qi = g0 + g < nq ? qmap[g0 + g] : qmap[g0];
-                slut[e] = lut_all[(uint64_t)qi * W * CARD + (e % (W * CARD))];
-            }
             for (uint32_t e = t; e < G * HIST_BINS; e += LF_THREADS) shist[e / HIST_BINS][e % HIST_BINS] = 0;
             if (t < G) {
                 const bool valid = g0 + t < nq;
@@ -318,10 +313,12 @@ __global__ void __launch_bounds__(LF_THREADS, 1) leafscan_kernel(
             // u8 LUT (R12): e = floor(LUT * 254 / T), rounded down at every step and clamped at 255,
             // so sum_s e <= LB^2 * 254 / T; "sum e > 254" implies LB^2 > T and prunes a member exactly
             for (uint32_t e = t; e < G * W * CARD; e += LF_THREADS) {
-                const float T = qc[e / (W * CARD)].T;
+                const uint32_t g = e / (W * CARD);
+                const float T = qc[g].T;
                 uint32_t v = 255;
                 if (T > 0.f) {
-                    const float x = __fmul_rd(slut[e], __fdiv_rd(254.0f, T));
+                    const float lv = __ldg(lut_all + (uint64_t)qid[g] * W * CARD + (e % (W * CARD)));
+                    const float x = __fmul_rd(lv, __fdiv_rd(254.0f, T));
                     v = x >= 255.f ? 255u : (uint32_t)x;
                 }
                 lut8[e] = (uint8_t)v;
@@ -356,11 +353,17 @@ __global__ void __launch_bounds__(LF_THREADS, 1) leafscan_kernel(
                 uint32_t cl[8];
 #pragma unroll
                 for (int k = 0; k < 8; k++) cl[k] = min_u16x2(max_u16x2(qv[k], mn[k]), mx[k]);
-                const float *L = slut + g * W * CARD;
-                float lb = 0.f;
+                {
+                    // u8 node bound: sum of floor(LUT * 254 / T) terms. A pruned node (sum > 254)
+                    // has every member's u8 sum > 254 too (floor is monotone), and the u8 member test
+                    // is a superset of the exact one, so no candidate is lost.
+                    const uint32_t ub = lut8_sh + g * W * CARD;
+                    uint32_t es = 0;
 #pragma unroll
-                for (int s2 = 0; s2 < W; s2++) lb += L[s2 * CARD + ((cl[s2 >> 1] >> (16 * (s2 & 1))) & 0xFFFFu)];
-                if (lb <= qc[g].T) alive |= 1u << g;
+                    for (int s2 = 0; s2 < W; s2++)
+                        es += ld_sh_u8(__byte_perm(cl[s2 >> 1], ub, 0x7650u | (uint32_t)(2 * (s2 & 1))) + s2 * CARD);
+                    if (es <= 254u) alive |= 1u << g;
+                }
             }
             if (leaf >= c1) alive = 0;
             const uint32_t bal = __ballot_sync(0xffffffffu, alive != 0);
@@ -408,7 +411,7 @@ __global__ void __launch_bounds__(LF_THREADS, 1) leafscan_kernel(
                         if (!__any_sync(0xffffffffu, maybe)) continue;
                         // rare: the exact fp32 test, the same rule as the flat scan
                         const QConst kq = qc[g];
-                        const float lb = maybe ? word_lb(slut + g * W * CARD, wv[k][u]) : 0.f;
+                        const float lb = maybe ? word_lb(lut_all + (uint64_t)qid[g] * W * CARD, wv[k][u]) : 0.f;
                         const bool keep = maybe && lb > kq.lo && lb <= kq.T && (pos < kq.ws || pos >= kq.we);
                         if (keep) atomicAdd(&shist[g][hist_bin(lb, kq.lo, kq.T)], 1u);
                         emit(keep, pos, g, qid[g], lane, lt, cbuf, cb_cnt, cand, cand_cnt, cap);
@@ -426,7 +429,7 @@ __global__ void __launch_bounds__(LF_THREADS, 1) leafscan_kernel(
 template <int G>
 static void launch_leaf(const isax_index *ix, uint32_t nq, const uint32_t *qmap, const float2 *band, float onepd,
                         cudaStream_t s) {
-    const size_t smem = (size_t)G * W * CARD * (sizeof(float) + 1) + 256 + (size_t)G * CBUF * sizeof(uint32_t) + CHUNK * 4;
+    const size_t smem = (size_t)G * W * CARD + 256 + (size_t)G * CBUF * sizeof(uint32_t) + CHUNK * 4;
     static bool configured = false;
     if (!configured) {
         cudaFuncSetAttribute(leafscan_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -462,8 +465,9 @@ uint64_t launch_lbscan(const isax_index *ix, uint32_t nq, const uint32_t *qmap, 
         else launch_g<1>(ix, nq, qmap, band, onepd, s);
         return 16ull * ix->N * ((nq + G - 1) / G);  // words read
     }
-    const uint32_t G = nq >= 8 ? 8 : nq >= 4 ? 4 : nq >= 2 ? 2 : 1;
-    if (G == 8) launch_leaf<8>(ix, nq, qmap, band, onepd, s);
+    const uint32_t G = nq >= 16 ? 16 : nq >= 8 ? 8 : nq >= 4 ? 4 : nq >= 2 ? 2 : 1;
+    if (G == 16) launch_leaf<16>(ix, nq, qmap, band, onepd, s);
+    else if (G == 8) launch_leaf<8>(ix, nq, qmap, band, onepd, s);
     else if (G == 4) launch_leaf<4>(ix, nq, qmap, band, onepd, s);
     else if (G == 2) launch_leaf<2>(ix, nq, qmap, band, onepd, s);
     else launch_leaf<1>(ix, nq, qmap, band, onepd, s);
