@@ -158,7 +158,7 @@ static int build_impl(const Source &src, uint64_t N, uint32_t n, uint32_t w, uin
         cudaStreamSynchronize(s);
         cudaFree(sax_by_id); cudaFree(keys); cudaFree(musig); cudaFree(ids); cudaFree(bad); cudaFree(inv);
         cudaFree(stage);
-        cudaFree(ix->stored); cudaFree(ix->sax); cudaFree(ix->perm); cudaFree(ix->lmeta);
+        cudaFree(ix->stored); cudaFree(ix->sax); cudaFree(ix->perm); cudaFree(ix->lmeta); cudaFree(ix->smeta);
         delete ix;
         cudaStreamDestroy(s);
         return code;
@@ -209,7 +209,8 @@ static int build_impl(const Source &src, uint64_t N, uint32_t n, uint32_t w, uin
     TRY(dmalloc(&ix->sax, N * W, &ix->device_bytes));
     launch_gather_sax(sax_by_id, ix->perm, N, ix->sax, s);
     TRY(dmalloc(&ix->lmeta, ((N + 63) / 64) * 32, &ix->device_bytes));
-    launch_leaf_meta(ix->sax, N, ix->lmeta, s);
+    TRY(dmalloc(&ix->smeta, ((N + 1023) / 1024) * 32, &ix->device_bytes));
+    launch_leaf_meta(ix->sax, N, ix->lmeta, ix->smeta, s);
     TRY(cudaStreamSynchronize(s));
     cudaFree(sax_by_id);
     sax_by_id = nullptr;
@@ -661,6 +662,7 @@ void isax_free(isax_index *ix) {
         cudaFree(ix->sax);
         cudaFree(ix->perm);
         cudaFree(ix->lmeta);
+        cudaFree(ix->smeta);
         free_scratch(ix);
         for (auto &ev : ix->ev)
             if (ev) cudaEventDestroy(ev);

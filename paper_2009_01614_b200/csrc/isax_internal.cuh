@@ -84,6 +84,7 @@ struct isax_index {
     uint8_t *sax = nullptr;
     uint32_t *perm = nullptr;
     uint8_t *lmeta = nullptr;  // [ceil(N/64)][32]: per-leaf min (16 B) and max (16 B) symbols
+    uint8_t *smeta = nullptr;  // [ceil(N/1024)][32]: per-super-node (16 leaves) min and max symbols
     size_t device_bytes = 0;
     isax::QueryScratch qs;
     std::mutex mu;
@@ -136,7 +137,7 @@ void launch_window(const isax_index *ix, uint32_t Q, const uint32_t *qmap, float
 void launch_lb_dump(const isax_index *ix, uint32_t Q, uint64_t first_pos, uint64_t count, float *out,
                     cudaStream_t s);
 // lbscan.cu
-void launch_leaf_meta(const uint8_t *sax, uint64_t N, uint8_t *lmeta, cudaStream_t s);
+void launch_leaf_meta(const uint8_t *sax, uint64_t N, uint8_t *lmeta, uint8_t *smeta, cudaStream_t s);
 // Scan all sorted positions for the nq queries qmap[0..nq), keeping band[i].x < LB^2 <= min(band[i].y,
 // bsf^2 (1+delta)) for slot i. Returns the summary bytes it reads that the host can count (node
 // summaries or flat words); the leaf scan adds its 1 KB leaf loads to qs.leaf_loads on the device.

@@ -202,6 +202,7 @@ static void launch_g(const isax_index *ix, uint32_t nq, const uint32_t *qmap, co
 //     per-series test for each query that kept the leaf. Candidates are buffered in shared
 //     memory per query slot and flushed once per group (one global atomic per slot).
 constexpr uint32_t LEAF = 64;
+constexpr uint32_t SUPER = 16;  // leaves per super-node
 constexpr int LF_THREADS = 1024;
 constexpr uint32_t CHUNK = 8192;  // max leaves per phase-A/phase-B round of a CTA
 constexpr uint32_t CBUF = 512;    // shared candidate buffer per query slot
@@ -236,9 +237,9 @@ __device__ __forceinline__ void emit(bool keep, uint32_t pos, uint32_t g, uint32
 
 template <int G>
 __global__ void __launch_bounds__(LF_THREADS, 1) leafscan_kernel(
-    const uint4 *__restrict__ sax, const uint8_t *__restrict__ lmeta, uint32_t N, const float *__restrict__ lut_all,
-    const uint8_t *__restrict__ qsax_all, const uint32_t *__restrict__ qmap, const float2 *__restrict__ band,
-    uint32_t nq, uint32_t nleaf, uint32_t chunk, const unsigned long long *__restrict__ bsf,
+    const uint4 *__restrict__ sax, const uint8_t *__restrict__ lmeta, const uint8_t *__restrict__ smeta, uint32_t N,
+    const float *__restrict__ lut_all, const uint8_t *__restrict__ qsax_all, const uint32_t *__restrict__ qmap,
+    const float2 *__restrict__ band, uint32_t nq, uint32_t nleaf, uint32_t chunk, const unsigned long long *__restrict__ bsf,
     const uint32_t *__restrict__ win, float onepd, uint32_t *__restrict__ cand, uint32_t *__restrict__ cand_cnt,
     uint32_t cap, uint32_t *__restrict__ hist, uint32_t *__restrict__ leaves_alive,
     unsigned long long *__restrict__ leaf_loads, uint32_t *__restrict__ task_ctr) {
@@ -263,6 +264,8 @@ __global__ void __launch_bounds__(LF_THREADS, 1) leafscan_kernel(
     const uint32_t ngroups = (nq + G - 1) / G;
     const uint32_t ntasks = nchunks * ngroups;
     const uint4 *meta4 = reinterpret_cast<const uint4 *>(lmeta);
+    const uint4 *smeta4 = reinterpret_cast<const uint4 *>(smeta);
+    const uint32_t nsuper = (nleaf + SUPER - 1) / SUPER;
     uint32_t loads = 0;
     uint32_t g0 = 0xffffffffu;  // first query slot of the group whose LUTs are loaded
     // empty the shared candidate buffers and histograms of the loaded group into global memory
@@ -328,13 +331,55 @@ __global__ void __launch_bounds__(LF_THREADS, 1) leafscan_kernel(
         const uint32_t c0 = ch * chunk;
         const uint32_t c1 = min(c0 + chunk, nleaf);
         // ---- phase A: lane = leaf; warp w takes leaves c0 + 32 w + lane, then + 32 NW, ...
+        // A warp-iteration covers 32 consecutive leaves = two super-nodes of 16 leaves (chunk
+        // starts are multiples of 32). Lane (h = lane / 16, gq = lane % 16) first bounds super-node
+        // h for query gq (R11: one more level of the tree). A leaf bound is computed only for the
+        // queries whose super-node survived.
         uint32_t leaf = c0 + warp * 32 + lane;
+        const uint32_t gq = lane & 15;
         uint4 mn_n = make_uint4(0, 0, 0, 0), mx_n = make_uint4(~0u, ~0u, ~0u, ~0u);
+        uint4 smn_n = mn_n, smx_n = mx_n;
         if (leaf < c1) {
             mn_n = __ldg(meta4 + 2 * (uint64_t)leaf);
             mx_n = __ldg(meta4 + 2 * (uint64_t)leaf + 1);
         }
+        {
+            const uint32_t sup = (leaf - lane) / 16 + (lane >> 4);
+            if (sup < nsuper) {
+                smn_n = __ldg(smeta4 + 2 * (uint64_t)sup);
+                smx_n = __ldg(smeta4 + 2 * (uint64_t)sup + 1);
+            }
+        }
         for (; leaf - lane < c1; leaf += 32 * NW) {
+            uint32_t smask_mine, smask_any;
+            {
+                const uint32_t smn[8] = {lo_u16x2(smn_n.x), hi_u16x2(smn_n.x), lo_u16x2(smn_n.y), hi_u16x2(smn_n.y),
+                                         lo_u16x2(smn_n.z), hi_u16x2(smn_n.z), lo_u16x2(smn_n.w), hi_u16x2(smn_n.w)};
+                const uint32_t smx[8] = {lo_u16x2(smx_n.x), hi_u16x2(smx_n.x), lo_u16x2(smx_n.y), hi_u16x2(smx_n.y),
+                                         lo_u16x2(smx_n.z), hi_u16x2(smx_n.z), lo_u16x2(smx_n.w), hi_u16x2(smx_n.w)};
+                const uint32_t sup_n = (leaf + 32 * NW - lane) / 16 + (lane >> 4);
+                if (leaf + 32 * NW - lane < c1 && sup_n < nsuper) {  // prefetch the next super-nodes
+                    smn_n = __ldg(smeta4 + 2 * (uint64_t)sup_n);
+                    smx_n = __ldg(smeta4 + 2 * (uint64_t)sup_n + 1);
+                }
+                bool salive = false;
+                if (gq < G) {
+                    const uint4 qa = qsym[gq][0], qb = qsym[gq][1];
+                    const uint32_t qv[8] = {qa.x, qa.y, qa.z, qa.w, qb.x, qb.y, qb.z, qb.w};
+                    const uint32_t ub = lut8_sh + gq * W * CARD;
+                    uint32_t es = 0;
+#pragma unroll
+                    for (int k = 0; k < 8; k++) {
+                        const uint32_t c2 = min_u16x2(max_u16x2(qv[k], smn[k]), smx[k]);
+                        es += ld_sh_u8(__byte_perm(c2, ub, 0x7650u) + (2 * k) * CARD);
+                        es += ld_sh_u8(__byte_perm(c2, ub, 0x7652u) + (2 * k + 1) * CARD);
+                    }
+                    salive = es <= 254u;
+                }
+                const uint32_t sb = __ballot_sync(0xffffffffu, salive);
+                smask_mine = lane < 16 ? (sb & 0xFFFFu) : (sb >> 16);
+                smask_any = (sb & 0xFFFFu) | (sb >> 16);
+            }
             // the leaf's per-segment [min, max] as u16x2 pairs (segments 2j, 2j+1)
             const uint32_t mn[8] = {lo_u16x2(mn_n.x), hi_u16x2(mn_n.x), lo_u16x2(mn_n.y), hi_u16x2(mn_n.y),
                                     lo_u16x2(mn_n.z), hi_u16x2(mn_n.z), lo_u16x2(mn_n.w), hi_u16x2(mn_n.w)};
@@ -348,6 +393,7 @@ __global__ void __launch_bounds__(LF_THREADS, 1) leafscan_kernel(
             uint32_t alive = 0;
 #pragma unroll
             for (int g = 0; g < G; g++) {
+                if (!((smask_any >> g) & 1u)) continue;  // both super-nodes pruned for query g
                 const uint4 qa = qsym[g][0], qb = qsym[g][1];
                 const uint32_t qv[8] = {qa.x, qa.y, qa.z, qa.w, qb.x, qb.y, qb.z, qb.w};
                 uint32_t cl[8];
@@ -365,6 +411,7 @@ __global__ void __launch_bounds__(LF_THREADS, 1) leafscan_kernel(
                     if (es <= 254u) alive |= 1u << g;
                 }
             }
+            alive &= smask_mine;
             if (leaf >= c1) alive = 0;
             const uint32_t bal = __ballot_sync(0xffffffffu, alive != 0);
             if (bal) {
@@ -448,7 +495,8 @@ static void launch_leaf(const isax_index *ix, uint32_t nq, const uint32_t *qmap,
     const QueryScratch &qs = ix->qs;
     cudaMemsetAsync(qs.task_ctr, 0, sizeof(uint32_t), s);
     leafscan_kernel<G><<<grid, LF_THREADS, smem, s>>>(
-        reinterpret_cast<const uint4 *>(ix->sax), ix->lmeta, (uint32_t)ix->N, qs.lut, qs.qsax, qmap, band, nq, nleaf,
+        reinterpret_cast<const uint4 *>(ix->sax), ix->lmeta, ix->smeta, (uint32_t)ix->N, qs.lut, qs.qsax, qmap, band, nq,
+        nleaf,
         chunk, qs.bsf, qs.win, onepd, qs.cand, qs.cand_cnt, qs.cand_cap, qs.cand_hist, qs.counters_leaf, qs.leaf_loads,
         qs.task_ctr);
 }
@@ -497,10 +545,33 @@ __global__ void leaf_meta_kernel(const uint4 *__restrict__ sax, uint64_t N, uint
     }
 }
 
-void launch_leaf_meta(const uint8_t *sax, uint64_t N, uint8_t *lmeta, cudaStream_t s) {
+// Build: per super-node of SUPER leaves, the per-segment min / max over its leaves' summaries.
+__global__ void super_meta_kernel(const uint4 *__restrict__ lmeta, uint64_t nleaf, uint4 *__restrict__ smeta) {
+    const uint64_t ns = (nleaf + SUPER - 1) / SUPER;
+    for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < ns; j += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t mn[4] = {~0u, ~0u, ~0u, ~0u}, mx[4] = {0, 0, 0, 0};
+        const uint64_t l1 = umin64(nleaf, (j + 1) * SUPER);
+        for (uint64_t l = j * SUPER; l < l1; l++) {
+            const uint4 a = __ldg(lmeta + 2 * l), b = __ldg(lmeta + 2 * l + 1);
+            const uint32_t va[4] = {a.x, a.y, a.z, a.w}, vb[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+            for (int k = 0; k < 4; k++) {
+                mn[k] = __vminu4(mn[k], va[k]);
+                mx[k] = __vmaxu4(mx[k], vb[k]);
+            }
+        }
+        smeta[2 * j] = make_uint4(mn[0], mn[1], mn[2], mn[3]);
+        smeta[2 * j + 1] = make_uint4(mx[0], mx[1], mx[2], mx[3]);
+    }
+}
+
+void launch_leaf_meta(const uint8_t *sax, uint64_t N, uint8_t *lmeta, uint8_t *smeta, cudaStream_t s) {
     const uint64_t nleaf = (N + LEAF - 1) / LEAF;
     const unsigned grid = (unsigned)std::max<uint64_t>(1, umin64((nleaf + 255) / 256, 148 * 16));
     leaf_meta_kernel<<<grid, 256, 0, s>>>(reinterpret_cast<const uint4 *>(sax), N, lmeta);
+    const uint64_t ns = (nleaf + SUPER - 1) / SUPER;
+    super_meta_kernel<<<(unsigned)std::max<uint64_t>(1, umin64((ns + 255) / 256, 148 * 16)), 256, 0, s>>>(
+        reinterpret_cast<const uint4 *>(lmeta), nleaf, reinterpret_cast<uint4 *>(smeta));
 }
 
 }  // namespace isax
