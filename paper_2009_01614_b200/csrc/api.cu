@@ -80,7 +80,8 @@ static void free_scratch(isax_index *ix) {
     cudaFree(q.qy); cudaFree(q.qpaa); cudaFree(q.qsax); cudaFree(q.lut); cudaFree(q.win); cudaFree(q.pwin); cudaFree(q.bsf);
     cudaFree(q.cand); cudaFree(q.cand_cnt); cudaFree(q.near); cudaFree(q.near_cnt); cudaFree(q.qmap); cudaFree(q.qband); cudaFree(q.cand_hist);
     cudaFree(q.counters); cudaFree(q.counters_leaf); cudaFree(q.leaf_loads); cudaFree(q.task_ctr); cudaFree(q.refine_bytes);
-    if (q.h_cnt) cudaFreeHost(q.h_cnt);
+    cudaFree(q.flag); cudaFree(q.qmap2);
+    if (q.h_mirror) cudaFreeHost(q.h_mirror);
     q = QueryScratch{};
 }
 
@@ -113,7 +114,10 @@ static int alloc_scratch(isax_index *ix) {
     A(task_ctr, 1);
     A(refine_bytes, 1);
 #undef A
-    if (e == cudaSuccess) e = cudaMallocHost(&q.h_cnt, sizeof(uint32_t) * (size_t)Q * 8);
+    A(flag, 1);
+    A(qmap2, Q);
+    if (e == cudaSuccess) e = cudaMallocHost(&q.h_mirror, HostMirror::bytes(Q));
+    if (e == cudaSuccess) q.hm.carve(q.h_mirror, Q);
     if (e != cudaSuccess) {
         free_scratch(ix);
         return cuda_error(e, "allocating query scratch");
@@ -249,7 +253,10 @@ static int nn1_device(isax_index *ix, const float *d_q, uint32_t Q, int64_t *d_i
     int rc = alloc_scratch(ix);
     if (rc) return rc;
     QueryScratch &qs = ix->qs;
+    HostMirror &hm = qs.hm;
     const float delta = std::ldexp(1.0f, ix->opts.slack_log2);
+    const float onepd = 1.0f + delta;
+    const float INF = std::numeric_limits<float>::infinity();
     ix->st_win.assign(2 * (size_t)Q, 0);
     ix->st_cand.assign(Q, 0);
     ix->st_refined.assign(Q, 0);
@@ -262,26 +269,21 @@ static int nn1_device(isax_index *ix, const float *d_q, uint32_t Q, int64_t *d_i
     ix->st_ms = StageTimes{};
     ix->st_launches = 0;
     ix->st_scan_bytes = ix->st_scan_bytes_first = 0;
+    ix->st_refine_bytes_first = 0;
     ISAX_CUDA(cudaMemsetAsync(qs.leaf_loads, 0, sizeof(unsigned long long), s));
     ISAX_CUDA(cudaMemsetAsync(qs.refine_bytes, 0, sizeof(unsigned long long), s));
-    ix->st_refine_bytes_first = 0;
-    // a device flag for non-finite queries
-    uint32_t *flag = nullptr;
-    ISAX_CUDA(cudaMalloc(&flag, sizeof(uint32_t)));
-    ISAX_CUDA(cudaMemsetAsync(flag, 0, sizeof(uint32_t), s));
-    std::vector<uint32_t> hmap(qs.cap_Q);
+    ISAX_CUDA(cudaMemsetAsync(qs.flag, 0, sizeof(uint32_t), s));
     int result = ISAX_OK;
     for (uint32_t b0 = 0; b0 < Q && result == ISAX_OK; b0 += qs.cap_Q) {
         const uint32_t B = std::min(qs.cap_Q, Q - b0);
         const bool timed = b0 == 0;
         if (timed) cudaEventRecord(ix->ev[0], s);
-        launch_qprep(ix, d_q + (uint64_t)b0 * ix->n, B, s, flag);
+        launch_qprep(ix, d_q + (uint64_t)b0 * ix->n, B, s, qs.flag);
         ISAX_CUDA(cudaMemsetAsync(qs.counters_leaf, 0, B * sizeof(uint32_t), s));
         ix->st_launches += 2;
         if (timed) cudaEventRecord(ix->ev[1], s);
         launch_window(ix, B, nullptr, delta, s);
-        std::vector<unsigned long long> bsf_pk(B);
-        ISAX_CUDA(cudaMemcpyAsync(bsf_pk.data(), qs.bsf, B * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+        ISAX_CUDA(cudaMemcpyAsync(hm.bsf0, qs.bsf, B * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
         if (timed) cudaEventRecord(ix->ev[2], s);
         // Rounds (R10). Round 0 scans the band (-1, +inf) for every query, i.e. everything
         // under the window BSF. If a query's candidate list overflows, its band is shrunk to the
@@ -291,30 +293,21 @@ static int nn1_device(isax_index *ix, const float *d_q, uint32_t Q, int64_t *d_i
         // dropped below it. If a query's near list overflowed, its BSF is kept, the list is
         // emptied, the window is re-refined and everything is rescanned, so every near tie of
         // the final BSF is collected.
-        const float onepd = 1.0f + delta;
-        const float INF = std::numeric_limits<float>::infinity();
+        // Every round ends with one host synchronisation. The finalise kernel and all counter
+        // copies are enqueued before it; they are redone only if another round follows.
         std::vector<float2> band(B, make_float2(-1.0f, INF));
         std::vector<char> pending(B, 1);
-        std::vector<float> bsf_h(B);
-        std::vector<float2> hband(B);
+        std::vector<float> bsf_h(B, INF), tused(B, -1.0f);
         std::vector<uint32_t> hist((size_t)B * HIST_BINS);
-        std::vector<unsigned long long> bsf_now(B);
         std::vector<uint32_t> rewin;
-        bool first = true;
         for (uint32_t round = 0;; round++) {
-            if (first) {  // the window result (bsf_pk was copied right after the window kernel)
-                ISAX_CUDA(cudaStreamSynchronize(s));
-                for (uint32_t i = 0; i < B; i++) bsf_h[i] = bsf_d2_host(bsf_pk[i]);
-                first = false;
-            }
             uint32_t nact = 0;
-            std::vector<float> tused(B, -1.0f);
             for (uint32_t i = 0; i < B; i++) {
                 if (!pending[i]) continue;
                 pending[i] = 0;
-                hmap[nact] = i;
-                hband[nact] = band[i];
-                tused[i] = std::fmin(bsf_h[i] * onepd, band[i].y);
+                hm.qmap[nact] = i;
+                hm.band[nact] = band[i];
+                tused[i] = std::fmin(bsf_h[i] * onepd, band[i].y);  // round 0: set after the sync
                 nact++;
             }
             if (!nact) break;
@@ -323,54 +316,62 @@ static int nn1_device(isax_index *ix, const float *d_q, uint32_t Q, int64_t *d_i
                 ISAX_CUDA(cudaMemsetAsync(qs.cand_cnt, 0, B * sizeof(uint32_t), s));
                 if (!rewin.empty()) {
                     for (uint32_t i : rewin) ISAX_CUDA(cudaMemsetAsync(qs.near_cnt + i, 0, sizeof(uint32_t), s));
-                    ISAX_CUDA(cudaMemcpyAsync(qs.qmap, rewin.data(), rewin.size() * sizeof(uint32_t),
+                    memcpy(hm.rewin, rewin.data(), rewin.size() * sizeof(uint32_t));
+                    ISAX_CUDA(cudaMemcpyAsync(qs.qmap2, hm.rewin, rewin.size() * sizeof(uint32_t),
                                               cudaMemcpyHostToDevice, s));
-                    launch_window(ix, (uint32_t)rewin.size(), qs.qmap, delta, s);
+                    launch_window(ix, (uint32_t)rewin.size(), qs.qmap2, delta, s);
                     ix->st_launches += 1;
                     rewin.clear();
                 }
             }
-            ISAX_CUDA(cudaMemcpyAsync(qs.qmap, hmap.data(), nact * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
-            ISAX_CUDA(cudaMemcpyAsync(qs.qband, hband.data(), nact * sizeof(float2), cudaMemcpyHostToDevice, s));
+            ISAX_CUDA(cudaMemcpyAsync(qs.qmap, hm.qmap, nact * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+            ISAX_CUDA(cudaMemcpyAsync(qs.qband, hm.band, nact * sizeof(float2), cudaMemcpyHostToDevice, s));
             ix->st_scan_bytes += launch_lbscan(ix, nact, qs.qmap, qs.qband, delta, s);
             if (timed && round == 0) cudaEventRecord(ix->ev[3], s);
             launch_refine(ix, B, delta, s);
-            ix->st_launches += 2;
             if (timed && round == 0) cudaEventRecord(ix->ev[4], s);
+            launch_finalize(ix, B, delta, d_id + b0, d_dist + b0, s);  // speculative: redone after another round
+            ix->st_launches += 3;
+            if (timed && round == 0) cudaEventRecord(ix->ev[5], s);
             ISAX_CUDA(cudaGetLastError());
-            ISAX_CUDA(cudaMemcpyAsync(qs.h_cnt, qs.cand_cnt, B * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
-            ISAX_CUDA(cudaMemcpyAsync(qs.h_cnt + qs.cap_Q, qs.near_cnt, B * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
-            ISAX_CUDA(cudaMemcpyAsync(qs.h_cnt + 2 * qs.cap_Q, flag, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
-            ISAX_CUDA(cudaMemcpyAsync(bsf_now.data(), qs.bsf, B * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+            ISAX_CUDA(cudaMemcpyAsync(hm.cand_cnt, qs.cand_cnt, B * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+            ISAX_CUDA(cudaMemcpyAsync(hm.near_cnt, qs.near_cnt, B * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+            ISAX_CUDA(cudaMemcpyAsync(hm.flag, qs.flag, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+            ISAX_CUDA(cudaMemcpyAsync(hm.bsf, qs.bsf, B * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+            ISAX_CUDA(cudaMemcpyAsync(hm.counters, qs.counters, (size_t)B * 4 * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+            ISAX_CUDA(cudaMemcpyAsync(hm.win, qs.win, (size_t)B * 2 * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+            ISAX_CUDA(cudaMemcpyAsync(hm.leaves, qs.counters_leaf, B * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+            ISAX_CUDA(cudaMemcpyAsync(hm.leaf_loads, qs.leaf_loads, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+            ISAX_CUDA(cudaMemcpyAsync(hm.refine_bytes, qs.refine_bytes, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
             ISAX_CUDA(cudaStreamSynchronize(s));
-            if (b0 == 0 && round == 0) {
-                unsigned long long ll = 0;
-                ISAX_CUDA(cudaMemcpy(&ll, qs.leaf_loads, sizeof ll, cudaMemcpyDeviceToHost));
-                ix->st_scan_bytes_first = ix->st_scan_bytes + 1024ull * ll;
-                ISAX_CUDA(cudaMemcpy(&ll, qs.refine_bytes, sizeof ll, cudaMemcpyDeviceToHost));
-                ix->st_refine_bytes_first = ll;
-                std::vector<uint32_t> la(B);
-                ISAX_CUDA(cudaMemcpy(la.data(), qs.counters_leaf, B * sizeof(uint32_t), cudaMemcpyDeviceToHost));
-                ix->st_leaf_pairs_first = 0;
-                for (uint32_t v : la) ix->st_leaf_pairs_first += v;
-                ix->st_scan_q_first = nact;
-            }
-            if (qs.h_cnt[2 * qs.cap_Q]) {
+            if (*hm.flag) {
                 result = set_error(ISAX_E_NONFINITE, "a query holds NaN or Inf");
                 break;
             }
+            if (round == 0) {  // the window BSF: the threshold round 0 used
+                for (uint32_t i = 0; i < B; i++) {
+                    bsf_h[i] = bsf_d2_host(hm.bsf0[i]);
+                    tused[i] = bsf_h[i] * onepd;
+                }
+                if (b0 == 0) {
+                    ix->st_scan_bytes_first = ix->st_scan_bytes + 1024ull * *hm.leaf_loads;
+                    ix->st_refine_bytes_first = *hm.refine_bytes;
+                    ix->st_leaf_pairs_first = 0;
+                    for (uint32_t i = 0; i < B; i++) ix->st_leaf_pairs_first += hm.leaves[i];
+                    ix->st_scan_q_first = nact;
+                }
+            }
             bool any_ovf = false;
-            for (uint32_t k = 0; k < nact; k++) any_ovf |= qs.h_cnt[hmap[k]] > qs.cand_cap;
+            for (uint32_t k = 0; k < nact; k++) any_ovf |= hm.cand_cnt[hm.qmap[k]] > qs.cand_cap;
             if (any_ovf)
                 ISAX_CUDA(cudaMemcpy(hist.data(), qs.cand_hist, hist.size() * sizeof(uint32_t), cudaMemcpyDeviceToHost));
             for (uint32_t k = 0; k < nact; k++) {
-                const uint32_t i = hmap[k];
-                const uint32_t cnt = qs.h_cnt[i];
-                bsf_h[i] = bsf_d2_host(bsf_now[i]);
-                ix->st_bsf_final[b0 + i] = bsf_h[i];
+                const uint32_t i = hm.qmap[k];
+                const uint32_t cnt = hm.cand_cnt[i];
+                bsf_h[i] = bsf_d2_host(hm.bsf[i]);
                 ix->st_cand[b0 + i] += std::min(cnt, qs.cand_cap);
                 ix->st_rounds[b0 + i] = round + 1;
-                if (qs.h_cnt[qs.cap_Q + i] > (uint32_t)NEAR_K) {  // near overflow: start over, BSF kept
+                if (hm.near_cnt[i] > (uint32_t)NEAR_K) {  // near overflow: start over, BSF kept
                     band[i] = make_float2(-1.0f, INF);
                     pending[i] = 1;
                     rewin.push_back(i);
@@ -398,27 +399,15 @@ static int nn1_device(isax_index *ix, const float *d_q, uint32_t Q, int64_t *d_i
             }
         }
         if (result) break;
-        launch_finalize(ix, B, delta, d_id + b0, d_dist + b0, s);
-        ix->st_launches += 1;
-        if (timed) cudaEventRecord(ix->ev[5], s);
-        ISAX_CUDA(cudaGetLastError());
-        // stats
-        std::vector<uint32_t> tmp((size_t)B * 4);
-        ISAX_CUDA(cudaMemcpyAsync(tmp.data(), qs.counters, tmp.size() * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
-        std::vector<uint32_t> tw((size_t)B * 2);
-        ISAX_CUDA(cudaMemcpyAsync(tw.data(), qs.win, tw.size() * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
-        std::vector<uint32_t> tl(B);
-        ISAX_CUDA(cudaMemcpyAsync(tl.data(), qs.counters_leaf, B * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
-        ISAX_CUDA(cudaStreamSynchronize(s));
         for (uint32_t i = 0; i < B; i++) {
-            ix->st_refined[b0 + i] = tmp[4 * i];
-            ix->st_abandoned[b0 + i] = tmp[4 * i + 1];
-            ix->st_near[b0 + i] = qs.h_cnt[qs.cap_Q + i];
-            ix->st_leaves[b0 + i] = tl[i];
-            const uint32_t hi32 = (uint32_t)(bsf_pk[i] >> 32);
-            memcpy(&ix->st_bsf0[b0 + i], &hi32, 4);
-            ix->st_win[2 * (b0 + i)] = tw[2 * i];
-            ix->st_win[2 * (b0 + i) + 1] = tw[2 * i + 1];
+            ix->st_refined[b0 + i] = hm.counters[4 * i];
+            ix->st_abandoned[b0 + i] = hm.counters[4 * i + 1];
+            ix->st_near[b0 + i] = hm.near_cnt[i];
+            ix->st_leaves[b0 + i] = hm.leaves[i];
+            ix->st_bsf0[b0 + i] = bsf_d2_host(hm.bsf0[i]);
+            ix->st_bsf_final[b0 + i] = bsf_d2_host(hm.bsf[i]);
+            ix->st_win[2 * (b0 + i)] = hm.win[2 * i];
+            ix->st_win[2 * (b0 + i) + 1] = hm.win[2 * i + 1];
         }
         if (timed) {
             cudaEventElapsedTime(&ix->st_ms.qprep, ix->ev[0], ix->ev[1]);
@@ -427,10 +416,9 @@ static int nn1_device(isax_index *ix, const float *d_q, uint32_t Q, int64_t *d_i
             cudaEventElapsedTime(&ix->st_ms.refine, ix->ev[3], ix->ev[4]);
             float tot = 0;
             cudaEventElapsedTime(&tot, ix->ev[0], ix->ev[5]);
-            ix->st_ms.finalize = tot;  // whole first batch
+            ix->st_ms.finalize = tot;  // whole first round of the first batch
         }
     }
-    cudaFree(flag);
     return result;
 }
 

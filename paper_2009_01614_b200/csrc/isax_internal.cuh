@@ -43,6 +43,31 @@ struct NearEntry {  // a completed refinement within (1+delta) of the BSF at tha
     uint32_t pad;
 };
 
+// Pinned host mirror of the per-batch counters (one async copy each per round, one sync).
+struct HostMirror {
+    uint32_t *cand_cnt, *near_cnt, *flag, *counters, *win, *leaves, *qmap, *rewin;
+    unsigned long long *bsf, *bsf0, *leaf_loads, *refine_bytes;
+    float2 *band;
+    static size_t bytes(uint32_t Q) { return (size_t)Q * (8 * 4 + 4 * 4 + 2 * 4 + 8 * 2 + 8) + 256; }
+    void carve(void *base, uint32_t Q) {
+        unsigned char *p = static_cast<unsigned char *>(base);
+        auto take = [&](size_t n) { unsigned char *r = p; p += (n + 15) & ~size_t(15); return r; };
+        bsf = reinterpret_cast<unsigned long long *>(take(8ull * Q));
+        bsf0 = reinterpret_cast<unsigned long long *>(take(8ull * Q));
+        leaf_loads = reinterpret_cast<unsigned long long *>(take(8));
+        refine_bytes = reinterpret_cast<unsigned long long *>(take(8));
+        band = reinterpret_cast<float2 *>(take(8ull * Q));
+        cand_cnt = reinterpret_cast<uint32_t *>(take(4ull * Q));
+        near_cnt = reinterpret_cast<uint32_t *>(take(4ull * Q));
+        flag = reinterpret_cast<uint32_t *>(take(4));
+        counters = reinterpret_cast<uint32_t *>(take(16ull * Q));
+        win = reinterpret_cast<uint32_t *>(take(8ull * Q));
+        leaves = reinterpret_cast<uint32_t *>(take(4ull * Q));
+        qmap = reinterpret_cast<uint32_t *>(take(4ull * Q));
+        rewin = reinterpret_cast<uint32_t *>(take(4ull * Q));
+    }
+};
+
 // Per-batch scratch owned by the index (sized for opts.batch_Q queries).
 struct QueryScratch {
     uint32_t cap_Q = 0;
@@ -66,7 +91,10 @@ struct QueryScratch {
     unsigned long long *leaf_loads = nullptr;  // leaves whose 64 words the scan read (all launches of a call)
     uint32_t *task_ctr = nullptr;              // work counter of the persistent leaf scan
     unsigned long long *refine_bytes = nullptr;  // bytes of rows the refine kernel read (all launches of a call)
-    uint32_t *h_cnt = nullptr;      // pinned host mirror of cand_cnt + near_cnt + counters
+    uint32_t *flag = nullptr;       // non-finite query flag
+    uint32_t *qmap2 = nullptr;      // [Q] slots whose window is re-refined
+    void *h_mirror = nullptr;       // pinned host memory of hm
+    HostMirror hm{};
 };
 
 struct StageTimes {

@@ -256,6 +256,7 @@ __global__ void __launch_bounds__(LF_THREADS, 1) leafscan_kernel(
     __shared__ uint4 qsym[G][2];  // the query's 16 symbols as 8 u16x2 pairs
     __shared__ uint32_t qid[G], cb_cnt[G], alive_cnt[G], fbase[G];
     __shared__ uint32_t shist[G][HIST_BINS];
+    __shared__ float qscale[G];
     __shared__ uint32_t wl_cnt, s_task;
     const uint32_t t = threadIdx.x, lane = t & 31, warp = t >> 5;
     constexpr uint32_t NW = LF_THREADS / 32;
@@ -311,17 +312,18 @@ __global__ void __launch_bounds__(LF_THREADS, 1) leafscan_kernel(
                 qsym[t][0] = make_uint4(lo_u16x2(w.x), hi_u16x2(w.x), lo_u16x2(w.y), hi_u16x2(w.y));
                 qsym[t][1] = make_uint4(lo_u16x2(w.z), hi_u16x2(w.z), lo_u16x2(w.w), hi_u16x2(w.w));
                 qc[t] = load_qconst(qi, valid, bsf, band, g0 + t, win, onepd);
+                qscale[t] = qc[t].T > 0.f ? __fdiv_rd(254.0f, qc[t].T) : 0.f;  // 254 / T, rounded down
             }
             __syncthreads();
             // u8 LUT (R12): e = floor(LUT * 254 / T), rounded down at every step and clamped at 255,
             // so sum_s e <= LB^2 * 254 / T; "sum e > 254" implies LB^2 > T and prunes a member exactly
             for (uint32_t e = t; e < G * W * CARD; e += LF_THREADS) {
                 const uint32_t g = e / (W * CARD);
-                const float T = qc[g].T;
+                const float sc = qscale[g];
                 uint32_t v = 255;
-                if (T > 0.f) {
+                if (sc > 0.f) {
                     const float lv = __ldg(lut_all + (uint64_t)qid[g] * W * CARD + (e % (W * CARD)));
-                    const float x = __fmul_rd(lv, __fdiv_rd(254.0f, T));
+                    const float x = __fmul_rd(lv, sc);
                     v = x >= 255.f ? 255u : (uint32_t)x;
                 }
                 lut8[e] = (uint8_t)v;
