@@ -113,9 +113,9 @@ static int alloc_scratch(isax_index *ix) {
     A(leaf_loads, 1);
     A(task_ctr, 1);
     A(refine_bytes, 1);
-#undef A
     A(flag, 1);
     A(qmap2, Q);
+#undef A
     if (e == cudaSuccess) e = cudaMallocHost(&q.h_mirror, HostMirror::bytes(Q));
     if (e == cudaSuccess) q.hm.carve(q.h_mirror, Q);
     if (e != cudaSuccess) {

@@ -17,6 +17,7 @@
 // Two kernels:
 //  - lbscan_kernel (ISAX_FLAG_FLAT_SCAN): the ParIS flat scan of every 16-byte word.
 //  - leafscan_kernel (default): MESSI-style node pruning on the sorted array (R11).
+#include <cstdlib>
 #include "isax_device.cuh"
 
 namespace isax {
@@ -70,6 +71,15 @@ __device__ __forceinline__ uint32_t word_e8(uint32_t ub, const uint4 &wv) {
     for (int s = 0; s < W; s++) es += ld_sh_u8(__byte_perm(v[s >> 2], ub, 0x7650u | (uint32_t)(s & 3)) + s * CARD);
     return es;
 }
+
+// 16-byte global -> shared asynchronous copy (LDGSTS); zero-fills the destination when !valid
+__device__ __forceinline__ void cp_async16(void *dst_smem, const void *src, bool valid) {
+    const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst_smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(valid ? 16 : 0) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
 // histogram bin of a kept bound inside its band (for the host's band shrinking)
 __device__ __forceinline__ uint32_t hist_bin(float lb, float lo, float hi) {
@@ -242,7 +252,7 @@ __global__ void __launch_bounds__(LF_THREADS, 1) leafscan_kernel(
     const float2 *__restrict__ band, uint32_t nq, uint32_t nleaf, uint32_t chunk, const unsigned long long *__restrict__ bsf,
     const uint32_t *__restrict__ win, float onepd, uint32_t *__restrict__ cand, uint32_t *__restrict__ cand_cnt,
     uint32_t cap, uint32_t *__restrict__ hist, uint32_t *__restrict__ leaves_alive,
-    unsigned long long *__restrict__ leaf_loads, uint32_t *__restrict__ task_ctr) {
+    unsigned long long *__restrict__ leaf_loads, uint32_t *__restrict__ task_ctr, int dbg_mode) {
     // shared: [G][16][256] fp32 LUTs | [G][16][256] u8 LUTs | [G][CBUF] candidates | [CHUNK] worklist
     // (the dynamic region follows the static variables, so the u8 tables are aligned by hand: the
     // PRMT address trick needs a 256-aligned base)
@@ -252,6 +262,7 @@ __global__ void __launch_bounds__(LF_THREADS, 1) leafscan_kernel(
     uint8_t *lut8 = smem_dyn + (lut8_sh - raw8);
     uint32_t *cbuf = reinterpret_cast<uint32_t *>(lut8 + G * W * CARD);
     uint32_t *worklist = cbuf + G * CBUF;  // (leaf offset in chunk) | (query mask << 16)
+    uint4 *stage = reinterpret_cast<uint4 *>(worklist + CHUNK);  // [NW][2][LEAF] phase-B word staging
     __shared__ QConst qc[G];
     __shared__ uint4 qsym[G][2];  // the query's 16 symbols as 8 u16x2 pairs
     __shared__ uint32_t qid[G], cb_cnt[G], alive_cnt[G], fbase[G];
@@ -424,49 +435,63 @@ __global__ void __launch_bounds__(LF_THREADS, 1) leafscan_kernel(
             }
         }
         __syncthreads();
-        // ---- phase B: the members of surviving leaves; two leaves' words in flight per warp
-        const uint32_t nwl = wl_cnt;
-        for (uint32_t e = warp * 2; e < nwl; e += 2 * NW) {
-            uint32_t ent[2];
-            uint4 wv[2][2];
+        // ---- phase B: the members of surviving leaves. Each warp takes entries warp, warp + NW,
+        // ... and double-buffers their 1 KB of words in its own shared staging slots with
+        // cp.async: the next leaf is in flight while the current one is tested (no registers
+        // held across the global latency).
+        const uint32_t nwl = dbg_mode == 1 ? 0u : wl_cnt;
+        uint4 *slot = stage + warp * 2 * LEAF;  // [2][LEAF] words
+        auto prefetch = [&](uint32_t e, uint32_t buf) {
+            const uint32_t base = (c0 + (worklist[e] & 0xFFFFu)) * LEAF;
 #pragma unroll
-            for (int k = 0; k < 2; k++) {
-                ent[k] = e + k < nwl ? worklist[e + k] : 0;
-                const uint32_t base = (c0 + (ent[k] & 0xFFFFu)) * LEAF;
+            for (int u = 0; u < 2; u++) {
+                const uint32_t pos = base + u * 32 + lane;
+                cp_async16(slot + buf * LEAF + u * 32 + lane, sax + (pos < N ? pos : 0), pos < N);
+            }
+            cp_async_commit();
+        };
+        if (warp < nwl) prefetch(warp, 0);
+        uint32_t buf = 0;
+        for (uint32_t e = warp; e < nwl; e += NW, buf ^= 1u) {
+            const bool more = e + NW < nwl;
+            if (more) prefetch(e + NW, buf ^ 1u);
+            if (more) cp_async_wait<1>();
+            else cp_async_wait<0>();
+            __syncwarp();
+            const uint32_t ent = worklist[e];
+            const uint32_t am = ent >> 16;
+            const uint32_t base = (c0 + (ent & 0xFFFFu)) * LEAF;
+            uint4 wv[2];
+#pragma unroll
+            for (int u = 0; u < 2; u++) wv[u] = slot[buf * LEAF + u * 32 + lane];
+            loads++;
+            if (lane < G && ((am >> lane) & 1u)) atomicAdd(&alive_cnt[lane], 1u);
+            // rolled loop over the queries that kept the leaf: unrolling it over G made the
+            // kernel ~120 KB of SASS, and instruction-cache misses became the top stall
+#pragma unroll 1
+            for (uint32_t mm = am; mm; mm &= mm - 1) {
+                const uint32_t g = __ffs(mm) - 1;
+                const uint32_t ub = lut8_sh + g * W * CARD;  // this query's u8 LUT (256-aligned)
+                // integer filter of both half-leaves: 3 instructions per lookup (PRMT address,
+                // LDS.U8, IADD), 32 independent shared loads, one warp vote
+                const uint32_t p0 = base + lane, p1 = base + 32 + lane;
+                const uint32_t e0 = word_e8(ub, wv[0]), e1 = word_e8(ub, wv[1]);
+                const bool m0 = p0 < N && e0 <= 254u, m1 = p1 < N && e1 <= 254u;
+                if (!__any_sync(0xffffffffu, m0 || m1)) continue;
+                // rare: the exact fp32 test, the same rule as the flat scan
+                const QConst kq = qc[g];
+                const float *Lg = lut_all + (uint64_t)qid[g] * W * CARD;
 #pragma unroll
                 for (int u = 0; u < 2; u++) {
-                    const uint32_t pos = base + u * 32 + lane;
-                    wv[k][u] = (e + k < nwl && pos < N) ? ld_stream(sax + pos) : make_uint4(0, 0, 0, 0);
+                    const bool maybe = u ? m1 : m0;
+                    const uint32_t pos = u ? p1 : p0;
+                    const float lb = maybe ? word_lb(Lg, wv[u]) : 0.f;
+                    const bool keep = maybe && lb > kq.lo && lb <= kq.T && (pos < kq.ws || pos >= kq.we);
+                    if (keep) atomicAdd(&shist[g][hist_bin(lb, kq.lo, kq.T)], 1u);
+                    emit(keep, pos, g, qid[g], lane, lt, cbuf, cb_cnt, cand, cand_cnt, cap);
                 }
             }
-#pragma unroll
-            for (int k = 0; k < 2; k++) {
-                if (e + k >= nwl) break;
-                const uint32_t am = ent[k] >> 16;
-                const uint32_t base = (c0 + (ent[k] & 0xFFFFu)) * LEAF;
-                loads++;
-                if (lane < G && ((am >> lane) & 1u)) atomicAdd(&alive_cnt[lane], 1u);
-                // rolled loop over the queries that kept the leaf: unrolling it over G made the
-                // kernel ~120 KB of SASS, and instruction-cache misses became the top stall
-#pragma unroll 1
-                for (uint32_t mm = am; mm; mm &= mm - 1) {
-                    const uint32_t g = __ffs(mm) - 1;
-                    const uint32_t ub = lut8_sh + g * W * CARD;  // this query's u8 LUT (256-aligned)
-#pragma unroll
-                    for (int u = 0; u < 2; u++) {
-                        const uint32_t pos = base + u * 32 + lane;
-                        // integer filter: 3 instructions per lookup (PRMT address, LDS.U8, IADD)
-                        const bool maybe = pos < N && word_e8(ub, wv[k][u]) <= 254u;
-                        if (!__any_sync(0xffffffffu, maybe)) continue;
-                        // rare: the exact fp32 test, the same rule as the flat scan
-                        const QConst kq = qc[g];
-                        const float lb = maybe ? word_lb(lut_all + (uint64_t)qid[g] * W * CARD, wv[k][u]) : 0.f;
-                        const bool keep = maybe && lb > kq.lo && lb <= kq.T && (pos < kq.ws || pos >= kq.we);
-                        if (keep) atomicAdd(&shist[g][hist_bin(lb, kq.lo, kq.T)], 1u);
-                        emit(keep, pos, g, qid[g], lane, lt, cbuf, cb_cnt, cand, cand_cnt, cap);
-                    }
-                }
-            }
+            __syncwarp();  // the slot is rewritten by the prefetch two entries ahead
         }
         __syncthreads();
         if (t == 0) wl_cnt = 0;
@@ -478,7 +503,8 @@ __global__ void __launch_bounds__(LF_THREADS, 1) leafscan_kernel(
 template <int G>
 static void launch_leaf(const isax_index *ix, uint32_t nq, const uint32_t *qmap, const float2 *band, float onepd,
                         cudaStream_t s) {
-    const size_t smem = (size_t)G * W * CARD + 256 + (size_t)G * CBUF * sizeof(uint32_t) + CHUNK * 4;
+    const size_t smem = (size_t)G * W * CARD + 256 + (size_t)G * CBUF * sizeof(uint32_t) + CHUNK * 4 +
+                        (size_t)(LF_THREADS / 32) * 2 * LEAF * sizeof(uint4);
     static bool configured = false;
     if (!configured) {
         cudaFuncSetAttribute(leafscan_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -500,7 +526,7 @@ static void launch_leaf(const isax_index *ix, uint32_t nq, const uint32_t *qmap,
         reinterpret_cast<const uint4 *>(ix->sax), ix->lmeta, ix->smeta, (uint32_t)ix->N, qs.lut, qs.qsax, qmap, band, nq,
         nleaf,
         chunk, qs.bsf, qs.win, onepd, qs.cand, qs.cand_cnt, qs.cand_cap, qs.cand_hist, qs.counters_leaf, qs.leaf_loads,
-        qs.task_ctr);
+        qs.task_ctr, getenv("ISAX_DBG_SCAN") ? atoi(getenv("ISAX_DBG_SCAN")) : 0);
 }
 
 uint64_t launch_lbscan(const isax_index *ix, uint32_t nq, const uint32_t *qmap, const float2 *band, float delta,
