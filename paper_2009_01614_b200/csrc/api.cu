@@ -466,31 +466,34 @@ int isax_nn1(const isax_index *cix, const float *queries, uint32_t Q, int64_t *o
     if (!queries || !out_id || !out_dist) return set_error(ISAX_E_INVAL, "NULL pointer");
     isax_index *ix = const_cast<isax_index *>(cix);
     std::lock_guard<std::mutex> lk(ix->mu);
-    cudaStream_t s;
-    ISAX_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    // the index keeps one stream and staging buffers for host pointers (grown on demand)
+    if (!ix->io_stream) ISAX_CUDA(cudaStreamCreateWithFlags(&ix->io_stream, cudaStreamNonBlocking));
+    cudaStream_t s = ix->io_stream;
     const size_t qbytes = (size_t)Q * ix->n * sizeof(float);
     const bool qdev = is_device_ptr(queries), idev = is_device_ptr(out_id), ddev = is_device_ptr(out_dist);
-    float *dq = nullptr;
-    int64_t *did = nullptr;
-    float *dd = nullptr;
-    int rc = ISAX_OK;
-    cudaError_t e = cudaSuccess;
-    if (!qdev) {
-        e = cudaMalloc(&dq, qbytes);
-        if (e == cudaSuccess) e = cudaMemcpyAsync(dq, queries, qbytes, cudaMemcpyHostToDevice, s);
+    if (Q > ix->io_cap) {
+        cudaFree(ix->io_q);
+        cudaFree(ix->io_id);
+        cudaFree(ix->io_dist);
+        ix->io_q = nullptr;
+        ix->io_id = nullptr;
+        ix->io_dist = nullptr;
+        ix->io_cap = 0;
+        cudaError_t e = cudaMalloc(&ix->io_q, qbytes);
+        if (e == cudaSuccess) e = cudaMalloc(&ix->io_id, Q * sizeof(int64_t));
+        if (e == cudaSuccess) e = cudaMalloc(&ix->io_dist, Q * sizeof(float));
+        if (e != cudaSuccess) return cuda_error(e, "isax_nn1 staging");
+        ix->io_cap = Q;
     }
-    if (e == cudaSuccess && !idev) e = cudaMalloc(&did, Q * sizeof(int64_t));
-    if (e == cudaSuccess && !ddev) e = cudaMalloc(&dd, Q * sizeof(float));
-    if (e != cudaSuccess) rc = cuda_error(e, "isax_nn1 staging");
-    if (!rc)
-        rc = nn1_device(ix, qdev ? queries : dq, Q, idev ? out_id : did, ddev ? out_dist : dd, s);
-    if (!rc && !idev) e = cudaMemcpyAsync(out_id, did, Q * sizeof(int64_t), cudaMemcpyDeviceToHost, s);
-    if (!rc && e == cudaSuccess && !ddev) e = cudaMemcpyAsync(out_dist, dd, Q * sizeof(float), cudaMemcpyDeviceToHost, s);
+    cudaError_t e = cudaSuccess;
+    if (!qdev) e = cudaMemcpyAsync(ix->io_q, queries, qbytes, cudaMemcpyHostToDevice, s);
+    if (e != cudaSuccess) return cuda_error(e, "isax_nn1 H2D");
+    int rc = nn1_device(ix, qdev ? queries : ix->io_q, Q, idev ? out_id : ix->io_id, ddev ? out_dist : ix->io_dist, s);
+    if (!rc && !idev) e = cudaMemcpyAsync(out_id, ix->io_id, Q * sizeof(int64_t), cudaMemcpyDeviceToHost, s);
+    if (!rc && e == cudaSuccess && !ddev) e = cudaMemcpyAsync(out_dist, ix->io_dist, Q * sizeof(float), cudaMemcpyDeviceToHost, s);
     if (!rc && e == cudaSuccess) e = cudaStreamSynchronize(s);
     if (!rc && e != cudaSuccess) rc = cuda_error(e, "isax_nn1 copy-out");
-    cudaStreamSynchronize(s);
-    cudaFree(dq); cudaFree(did); cudaFree(dd);
-    cudaStreamDestroy(s);
+    if (rc) cudaStreamSynchronize(s);
     return rc;
 }
 
@@ -654,6 +657,10 @@ void isax_free(isax_index *ix) {
         free_scratch(ix);
         for (auto &ev : ix->ev)
             if (ev) cudaEventDestroy(ev);
+        cudaFree(ix->io_q);
+        cudaFree(ix->io_id);
+        cudaFree(ix->io_dist);
+        if (ix->io_stream) cudaStreamDestroy(ix->io_stream);
     }
     delete ix;
 }

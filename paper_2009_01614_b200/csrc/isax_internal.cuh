@@ -125,6 +125,12 @@ struct isax_index {
     uint64_t st_refine_bytes_first = 0;                    // row bytes the first refine launch read
     uint64_t st_leaf_pairs_first = 0, st_scan_q_first = 0; // (leaf, query) pairs kept / queries of the first scan
     cudaEvent_t ev[8] = {};
+    // isax_nn1 (host pointers): one stream and device staging, grown on demand
+    cudaStream_t io_stream = nullptr;
+    float *io_q = nullptr;
+    int64_t *io_id = nullptr;
+    float *io_dist = nullptr;
+    uint32_t io_cap = 0;
 };
 
 namespace isax {
