@@ -17,7 +17,6 @@
 // Two kernels:
 //  - lbscan_kernel (ISAX_FLAG_FLAT_SCAN): the ParIS flat scan of every 16-byte word.
 //  - leafscan_kernel (default): MESSI-style node pruning on the sorted array (R11).
-#include <cstdlib>
 #include "isax_device.cuh"
 
 namespace isax {
@@ -252,7 +251,7 @@ __global__ void __launch_bounds__(LF_THREADS, 1) leafscan_kernel(
     const float2 *__restrict__ band, uint32_t nq, uint32_t nleaf, uint32_t chunk, const unsigned long long *__restrict__ bsf,
     const uint32_t *__restrict__ win, float onepd, uint32_t *__restrict__ cand, uint32_t *__restrict__ cand_cnt,
     uint32_t cap, uint32_t *__restrict__ hist, uint32_t *__restrict__ leaves_alive,
-    unsigned long long *__restrict__ leaf_loads, uint32_t *__restrict__ task_ctr, int dbg_mode) {
+    unsigned long long *__restrict__ leaf_loads, uint32_t *__restrict__ task_ctr) {
     // shared: [G][16][256] fp32 LUTs | [G][16][256] u8 LUTs | [G][CBUF] candidates | [CHUNK] worklist
     // (the dynamic region follows the static variables, so the u8 tables are aligned by hand: the
     // PRMT address trick needs a 256-aligned base)
@@ -439,7 +438,7 @@ __global__ void __launch_bounds__(LF_THREADS, 1) leafscan_kernel(
         // ... and double-buffers their 1 KB of words in its own shared staging slots with
         // cp.async: the next leaf is in flight while the current one is tested (no registers
         // held across the global latency).
-        const uint32_t nwl = dbg_mode == 1 ? 0u : wl_cnt;
+        const uint32_t nwl = wl_cnt;
         uint4 *slot = stage + warp * 2 * LEAF;  // [2][LEAF] words
         auto prefetch = [&](uint32_t e, uint32_t buf) {
             const uint32_t base = (c0 + (worklist[e] & 0xFFFFu)) * LEAF;
@@ -526,7 +525,7 @@ static void launch_leaf(const isax_index *ix, uint32_t nq, const uint32_t *qmap,
         reinterpret_cast<const uint4 *>(ix->sax), ix->lmeta, ix->smeta, (uint32_t)ix->N, qs.lut, qs.qsax, qmap, band, nq,
         nleaf,
         chunk, qs.bsf, qs.win, onepd, qs.cand, qs.cand_cnt, qs.cand_cap, qs.cand_hist, qs.counters_leaf, qs.leaf_loads,
-        qs.task_ctr, getenv("ISAX_DBG_SCAN") ? atoi(getenv("ISAX_DBG_SCAN")) : 0);
+        qs.task_ctr);
 }
 
 uint64_t launch_lbscan(const isax_index *ix, uint32_t nq, const uint32_t *qmap, const float2 *band, float delta,
