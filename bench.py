@@ -255,10 +255,13 @@ def main():
     lb_ms = statistics.mean(kms["lbscan"])
     rf_ms = statistics.mean(kms["refine"])
     nq1 = min(Q, 128)
-    leaves = (wl.N + 63) // 64
-    # algorithmic LUT lookups of the first scan launch: 16 per leaf per query (node bounds) plus
-    # 16 per member of every (leaf, query) pair that survived (per-series bounds)
-    lookups = 16.0 * leaves * nq1 + 16.0 * 64 * statistics.mean(pairs)
+    leaf_size, super_size = st.get("leaf_size", 64), st.get("super_size", 1024)
+    supers = (wl.N + super_size - 1) // super_size
+    # algorithmic LUT lookups of the first scan launch: 16 per super-node per query (root-level
+    # node bounds) plus 16 per member of every (leaf, query) pair that survived (per-series
+    # bounds). Leaf-level bounds (16 per leaf of a surviving super-node) are not counted, so this
+    # understates the work done.
+    lookups = 16.0 * supers * nq1 + 16.0 * leaf_size * statistics.mean(pairs)
     lk_peak = 148 * 32 * sm_mhz * 1e6  # one conflict-free 32-lane LDS wavefront per clock per SM
     lk_rate = lookups / (lb_ms / 1e3)
     scan_bytes = statistics.mean(scan_b) + 4.0 * statistics.mean(cand) * nq1 / Q
@@ -269,7 +272,7 @@ def main():
         traffic = tr.get("leafscan_dram_bytes")
     except Exception:
         pass
-    roofline = {"kernel": "leafscan_kernel<8>", "bound": "alu", "achieved": round(lk_rate / 1e12, 4),
+    roofline = {"kernel": "leafscan_kernel<16>", "bound": "alu", "achieved": round(lk_rate / 1e12, 4),
                 "peak": round(lk_peak / 1e12, 4), "unit": "T LUT lookups/s", "frac": round(lk_rate / lk_peak, 4),
                 "traffic": traffic,
                 "peak_rule": "148 SMs x 32 lanes x SM clock (one conflict-free shared-memory wavefront per clock per SM); "

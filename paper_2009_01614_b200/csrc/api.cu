@@ -77,9 +77,9 @@ static cudaError_t dmalloc(T **p, size_t count, size_t *acc) {
 
 static void free_scratch(isax_index *ix) {
     QueryScratch &q = ix->qs;
-    cudaFree(q.qy); cudaFree(q.qpaa); cudaFree(q.qsax); cudaFree(q.lut); cudaFree(q.win); cudaFree(q.pwin); cudaFree(q.bsf);
+    cudaFree(q.qy); cudaFree(q.qpaa); cudaFree(q.qsax); cudaFree(q.lut); cudaFree(q.lut8); cudaFree(q.qconst); cudaFree(q.win); cudaFree(q.pwin); cudaFree(q.bsf);
     cudaFree(q.cand); cudaFree(q.cand_cnt); cudaFree(q.near); cudaFree(q.near_cnt); cudaFree(q.qmap); cudaFree(q.qband); cudaFree(q.cand_hist);
-    cudaFree(q.counters); cudaFree(q.counters_leaf); cudaFree(q.leaf_loads); cudaFree(q.task_ctr); cudaFree(q.refine_bytes);
+    cudaFree(q.counters); cudaFree(q.counters_leaf); cudaFree(q.scan_bytes_dev); cudaFree(q.task_ctr); cudaFree(q.refine_bytes);
     cudaFree(q.flag); cudaFree(q.qmap2);
     if (q.h_mirror) cudaFreeHost(q.h_mirror);
     q = QueryScratch{};
@@ -98,6 +98,8 @@ static int alloc_scratch(isax_index *ix) {
     A(qpaa, (size_t)Q * W);
     A(qsax, (size_t)Q * W);
     A(lut, (size_t)Q * W * CARD);
+    A(lut8, (size_t)Q * W * CARD);
+    A(qconst, Q);
     A(win, (size_t)Q * 2);
     A(pwin, (size_t)Q * (MAX_PROBES - 1));
     A(bsf, Q);
@@ -110,7 +112,7 @@ static int alloc_scratch(isax_index *ix) {
     A(cand_hist, (size_t)Q * HIST_BINS);
     A(counters, (size_t)Q * 4);
     A(counters_leaf, Q);
-    A(leaf_loads, 1);
+    A(scan_bytes_dev, 1);
     A(task_ctr, 1);
     A(refine_bytes, 1);
     A(flag, 1);
@@ -212,8 +214,8 @@ static int build_impl(const Source &src, uint64_t N, uint32_t n, uint32_t w, uin
     ids = nullptr;
     TRY(dmalloc(&ix->sax, N * W, &ix->device_bytes));
     launch_gather_sax(sax_by_id, ix->perm, N, ix->sax, s);
-    TRY(dmalloc(&ix->lmeta, ((N + 63) / 64) * 32, &ix->device_bytes));
-    TRY(dmalloc(&ix->smeta, ((N + 1023) / 1024) * 32, &ix->device_bytes));
+    TRY(dmalloc(&ix->lmeta, ((N + LEAF_SIZE - 1) / LEAF_SIZE) * 32, &ix->device_bytes));
+    TRY(dmalloc(&ix->smeta, ((N + SUPER_SIZE - 1) / SUPER_SIZE) * 32, &ix->device_bytes));
     launch_leaf_meta(ix->sax, N, ix->lmeta, ix->smeta, s);
     TRY(cudaStreamSynchronize(s));
     cudaFree(sax_by_id);
@@ -270,7 +272,7 @@ static int nn1_device(isax_index *ix, const float *d_q, uint32_t Q, int64_t *d_i
     ix->st_launches = 0;
     ix->st_scan_bytes = ix->st_scan_bytes_first = 0;
     ix->st_refine_bytes_first = 0;
-    ISAX_CUDA(cudaMemsetAsync(qs.leaf_loads, 0, sizeof(unsigned long long), s));
+    ISAX_CUDA(cudaMemsetAsync(qs.scan_bytes_dev, 0, sizeof(unsigned long long), s));
     ISAX_CUDA(cudaMemsetAsync(qs.refine_bytes, 0, sizeof(unsigned long long), s));
     ISAX_CUDA(cudaMemsetAsync(qs.flag, 0, sizeof(uint32_t), s));
     int result = ISAX_OK;
@@ -331,7 +333,7 @@ static int nn1_device(isax_index *ix, const float *d_q, uint32_t Q, int64_t *d_i
             launch_refine(ix, B, delta, s);
             if (timed && round == 0) cudaEventRecord(ix->ev[4], s);
             launch_finalize(ix, B, delta, d_id + b0, d_dist + b0, s);  // speculative: redone after another round
-            ix->st_launches += 3;
+            ix->st_launches += (ix->opts.flags & ISAX_FLAG_FLAT_SCAN) ? 3 : 4;  // the leaf scan adds scanprep_kernel
             if (timed && round == 0) cudaEventRecord(ix->ev[5], s);
             ISAX_CUDA(cudaGetLastError());
             ISAX_CUDA(cudaMemcpyAsync(hm.cand_cnt, qs.cand_cnt, B * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
@@ -341,7 +343,7 @@ static int nn1_device(isax_index *ix, const float *d_q, uint32_t Q, int64_t *d_i
             ISAX_CUDA(cudaMemcpyAsync(hm.counters, qs.counters, (size_t)B * 4 * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
             ISAX_CUDA(cudaMemcpyAsync(hm.win, qs.win, (size_t)B * 2 * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
             ISAX_CUDA(cudaMemcpyAsync(hm.leaves, qs.counters_leaf, B * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
-            ISAX_CUDA(cudaMemcpyAsync(hm.leaf_loads, qs.leaf_loads, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+            ISAX_CUDA(cudaMemcpyAsync(hm.scan_bytes_dev, qs.scan_bytes_dev, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
             ISAX_CUDA(cudaMemcpyAsync(hm.refine_bytes, qs.refine_bytes, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
             ISAX_CUDA(cudaStreamSynchronize(s));
             if (*hm.flag) {
@@ -354,7 +356,7 @@ static int nn1_device(isax_index *ix, const float *d_q, uint32_t Q, int64_t *d_i
                     tused[i] = bsf_h[i] * onepd;
                 }
                 if (b0 == 0) {
-                    ix->st_scan_bytes_first = ix->st_scan_bytes + 1024ull * *hm.leaf_loads;
+                    ix->st_scan_bytes_first = ix->st_scan_bytes + *hm.scan_bytes_dev;
                     ix->st_refine_bytes_first = *hm.refine_bytes;
                     ix->st_leaf_pairs_first = 0;
                     for (uint32_t i = 0; i < B; i++) ix->st_leaf_pairs_first += hm.leaves[i];
@@ -625,7 +627,9 @@ int isax_stats(const isax_index *cix, char *buf, size_t cap) {
     j += ",\"refine_bytes_first_launch\":" + std::to_string(ix->st_refine_bytes_first);
     j += ",\"leaf_pairs_first_launch\":" + std::to_string(ix->st_leaf_pairs_first);
     j += ",\"scan_queries_first_launch\":" + std::to_string(ix->st_scan_q_first);
-    j += ",\"leaves\":" + std::to_string((ix->N + 63) / 64);
+    j += ",\"leaves\":" + std::to_string((ix->N + LEAF_SIZE - 1) / LEAF_SIZE);
+    j += ",\"leaf_size\":" + std::to_string(LEAF_SIZE);
+    j += ",\"super_size\":" + std::to_string(SUPER_SIZE);
     j += "}";
     if (buf && cap) {
         size_t k = std::min(cap - 1, j.size());

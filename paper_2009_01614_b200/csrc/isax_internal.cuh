@@ -22,6 +22,8 @@ constexpr int CARD = 256;    // symbols per segment (8 bits)
 constexpr int NEAR_K = 256;  // near-tie list capacity per query (R9)
 constexpr uint32_t MAX_PROBES = 32;  // 2^probe_bits windows per query, probe_bits <= 5
 constexpr uint32_t HIST_BINS = 64;   // per-query histogram of kept LB^2 inside its band (R10)
+constexpr uint32_t LEAF_SIZE = 32;    // sorted positions per leaf node (R11)
+constexpr uint32_t SUPER_SIZE = 1024; // sorted positions per super-node (R11)
 
 // Packed BSF: high 32 bits = fp32 bits of d^2 (non-negative, so the bit order is the
 // numeric order), low 32 bits = original id. atomicMin on the packed word is the
@@ -46,7 +48,7 @@ struct NearEntry {  // a completed refinement within (1+delta) of the BSF at tha
 // Pinned host mirror of the per-batch counters (one async copy each per round, one sync).
 struct HostMirror {
     uint32_t *cand_cnt, *near_cnt, *flag, *counters, *win, *leaves, *qmap, *rewin;
-    unsigned long long *bsf, *bsf0, *leaf_loads, *refine_bytes;
+    unsigned long long *bsf, *bsf0, *scan_bytes_dev, *refine_bytes;
     float2 *band;
     static size_t bytes(uint32_t Q) { return (size_t)Q * (8 * 4 + 4 * 4 + 2 * 4 + 8 * 2 + 8) + 256; }
     void carve(void *base, uint32_t Q) {
@@ -54,7 +56,7 @@ struct HostMirror {
         auto take = [&](size_t n) { unsigned char *r = p; p += (n + 15) & ~size_t(15); return r; };
         bsf = reinterpret_cast<unsigned long long *>(take(8ull * Q));
         bsf0 = reinterpret_cast<unsigned long long *>(take(8ull * Q));
-        leaf_loads = reinterpret_cast<unsigned long long *>(take(8));
+        scan_bytes_dev = reinterpret_cast<unsigned long long *>(take(8));
         refine_bytes = reinterpret_cast<unsigned long long *>(take(8));
         band = reinterpret_cast<float2 *>(take(8ull * Q));
         cand_cnt = reinterpret_cast<uint32_t *>(take(4ull * Q));
@@ -76,6 +78,8 @@ struct QueryScratch {
     double *qpaa = nullptr;         // [Q][16]
     uint8_t *qsax = nullptr;        // [Q][16]
     float *lut = nullptr;           // [Q][16][256] fp32, rounded down
+    uint8_t *lut8 = nullptr;        // [Q][16][256] u8 scan table of each active slot (R11b)
+    uint4 *qconst = nullptr;        // [Q] scan constants of each active slot (band lo, T, window)
     uint32_t *win = nullptr;        // [Q][2] window [start, end)
     uint32_t *pwin = nullptr;       // [Q][MAX_PROBES-1] probe window starts (probe_L rows each)
     unsigned long long *bsf = nullptr;  // [Q] packed
@@ -88,7 +92,7 @@ struct QueryScratch {
     uint32_t *cand_hist = nullptr;  // [Q][HIST_BINS] histogram of kept LB^2 in the band
     uint32_t *counters = nullptr;   // [Q][4]: refined, abandoned, rounds, near_overflow
     uint32_t *counters_leaf = nullptr;  // [Q]: (leaf, query) pairs that survived the node bound
-    unsigned long long *leaf_loads = nullptr;  // leaves whose 64 words the scan read (all launches of a call)
+    unsigned long long *scan_bytes_dev = nullptr;  // leaf words and leaf summaries the leaf scan read, bytes (all launches of a call)
     uint32_t *task_ctr = nullptr;              // work counter of the persistent leaf scan
     unsigned long long *refine_bytes = nullptr;  // bytes of rows the refine kernel read (all launches of a call)
     uint32_t *flag = nullptr;       // non-finite query flag
@@ -111,8 +115,8 @@ struct isax_index {
     float *stored = nullptr;
     uint8_t *sax = nullptr;
     uint32_t *perm = nullptr;
-    uint8_t *lmeta = nullptr;  // [ceil(N/64)][32]: per-leaf min (16 B) and max (16 B) symbols
-    uint8_t *smeta = nullptr;  // [ceil(N/1024)][32]: per-super-node (16 leaves) min and max symbols
+    uint8_t *lmeta = nullptr;  // [ceil(N/LEAF_SIZE)][32]: per-leaf min (16 B) and max (16 B) symbols
+    uint8_t *smeta = nullptr;  // [ceil(N/SUPER_SIZE)][32]: per-super-node min and max symbols
     size_t device_bytes = 0;
     isax::QueryScratch qs;
     std::mutex mu;
@@ -174,7 +178,7 @@ void launch_lb_dump(const isax_index *ix, uint32_t Q, uint64_t first_pos, uint64
 void launch_leaf_meta(const uint8_t *sax, uint64_t N, uint8_t *lmeta, uint8_t *smeta, cudaStream_t s);
 // Scan all sorted positions for the nq queries qmap[0..nq), keeping band[i].x < LB^2 <= min(band[i].y,
 // bsf^2 (1+delta)) for slot i. Returns the summary bytes it reads that the host can count (node
-// summaries or flat words); the leaf scan adds its 1 KB leaf loads to qs.leaf_loads on the device.
+// summaries or flat words); the leaf scan adds its leaf-word and leaf-summary bytes to qs.scan_bytes_dev on the device.
 uint64_t launch_lbscan(const isax_index *ix, uint32_t nq, const uint32_t *qmap, const float2 *band, float delta,
                        cudaStream_t s);
 // refine.cu

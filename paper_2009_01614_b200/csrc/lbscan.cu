@@ -194,24 +194,35 @@ static void launch_g(const isax_index *ix, uint32_t nq, const uint32_t *qmap, co
 // leaves that survive are examined "by first computing lower bound distances using the
 // iSAX summaries".
 //
-// A leaf is LEAF consecutive sorted positions. Its node summary (leaf_meta_kernel) is the
-// per-segment [min, max] symbol. The node's region on segment s is [beta_min, beta_{max+1}).
-// Its MINDIST term is the minimum of LUT[s][c] over c in [min, max]. LUT[s][.] is V-shaped
-// around the query's own symbol q_s, so that minimum is LUT[s][clamp(q_s, min, max)].
-// The node bound is summed over s = 0..15 left to right in fp32, exactly like the per-series
-// bound. Every term is <= the member's term, and fp32 addition is monotone, so node LB^2 <=
-// member LB^2 holds exactly. A leaf is pruned iff node LB^2 > T. The candidate set is
-// therefore exactly the flat scan's (tests/test_gpu_parity.py).
+// Two node levels: a leaf is LEAF consecutive sorted positions, a super-node SUPER leaves. A
+// node's summary (leaf_meta_kernel, super_meta_kernel) is the per-segment [min, max] symbol. The
+// node's region on segment s is [beta_min, beta_{max+1}). Its MINDIST term is the minimum of
+// LUT[s][c] over c in [min, max]. LUT[s][.] is V-shaped around the query's own symbol q_s, so that
+// minimum is LUT[s][clamp(q_s, min, max)]. Every node term is <= the term of each member (and of
+// each child node), so a pruned node holds no candidate.
+//
+// The tests use the u8 tables of scanprep_kernel (R11b): e = floor(LUT * 254 / T), rounded down at
+// every step and clamped at 255, so sum_s e <= LB^2 * 254 / T and "sum e > 254" implies LB^2 > T.
+// floor is monotone, so a node pruned this way has every member pruned too. Members that pass the
+// u8 test get the exact fp32 rule of the flat scan, so the candidate set is exactly the flat scan's
+// (tests/test_gpu_parity.py).
 //
 // Persistent CTAs (one per SM, 1024 threads) pull (query group, chunk of `chunk` leaves) tasks
-// from an atomic counter. LUTs of the group's G <= 8 queries sit in shared memory. Per chunk:
-//  A. lane = leaf: node bounds for all G queries; surviving leaves and their query masks go to
-//     a shared worklist;
-//  B. warps stream the worklist with two leaves' 1 KB of words in flight and run the
-//     per-series test for each query that kept the leaf. Candidates are buffered in shared
-//     memory per query slot and flushed once per group (one global atomic per slot).
-constexpr uint32_t LEAF = 64;
-constexpr uint32_t SUPER = 16;  // leaves per super-node
+// from an atomic counter. The u8 tables of the group's G <= 16 queries sit in shared memory.
+// Per chunk:
+//  A. warp iteration = one super-node, lane = one of its 32 leaves. Lanes (query gq, segment half)
+//     bound the super-node for all G queries; a leaf bound is computed only for the queries whose
+//     super-node survived, and leaf summaries are read only for super-nodes that survived. The next
+//     iteration's super test and leaf-summary loads are issued before this iteration's leaf tests.
+//     Surviving leaves and their query masks go to a shared worklist.
+//  B. each warp takes two worklist entries at a time (lane = member of each leaf) and
+//     double-buffers their words with cp.async. For every query of either mask it runs the u8
+//     member test (two independent chains when both leaves kept the query), one warp vote, and
+//     the exact fp32 test for the rare survivors. Candidates are buffered in shared memory per
+//     query slot and flushed once per group (one global atomic per slot).
+constexpr uint32_t LEAF = LEAF_SIZE;
+constexpr uint32_t SUPER = SUPER_SIZE / LEAF_SIZE;  // leaves per super-node
+static_assert(LEAF == 32 && SUPER == 32, "phase A maps a super-node to a warp iteration and a leaf to a lane");
 constexpr int LF_THREADS = 1024;
 constexpr uint32_t CHUNK = 8192;  // max leaves per phase-A/phase-B round of a CTA
 constexpr uint32_t CBUF = 512;    // shared candidate buffer per query slot
@@ -244,15 +255,44 @@ __device__ __forceinline__ void emit(bool keep, uint32_t pos, uint32_t g, uint32
     }
 }
 
+// u8 table entry (R11b): floor(v * sc) with sc = 254 / T rounded down, clamped at 255. v = 0 maps
+// to 0, so T = 0 (an exact duplicate in the window) keeps exactly the members with LB^2 = 0.
+__device__ __forceinline__ uint32_t q8(float v, float sc) {
+    if (!(v > 0.f)) return 0u;
+    const float x = __fmul_rd(v, sc);
+    return x >= 255.f ? 255u : (uint32_t)x;
+}
+
+// Per active slot of a scan launch: its constants (band lo, T, window) and its u8 table, once,
+// instead of in every CTA that takes one of its tasks. One CTA per slot.
+__global__ void __launch_bounds__(256) scanprep_kernel(const float *__restrict__ lut_all, const uint32_t *__restrict__ qmap,
+                                                       const float2 *__restrict__ band,
+                                                       const unsigned long long *__restrict__ bsf,
+                                                       const uint32_t *__restrict__ win, float onepd,
+                                                       uint8_t *__restrict__ lut8, uint4 *__restrict__ qconst) {
+    const uint32_t i = blockIdx.x;
+    const uint32_t qi = qmap[i];
+    const QConst k = load_qconst(qi, true, bsf, band, i, win, onepd);
+    if (threadIdx.x == 0) qconst[i] = make_uint4(__float_as_uint(k.lo), __float_as_uint(k.T), k.ws, k.we);
+    const bool none = !(k.T >= 0.f);  // an empty band keeps nothing
+    const float sc = none ? 0.f : __fdiv_rd(254.0f, k.T);  // T = 0 -> +inf
+    const float4 *L = reinterpret_cast<const float4 *>(lut_all + (uint64_t)qi * W * CARD);
+    uint32_t *o = reinterpret_cast<uint32_t *>(lut8 + (uint64_t)i * W * CARD);
+    for (uint32_t e = threadIdx.x; e < W * CARD / 4; e += blockDim.x) {
+        const float4 v = __ldg(L + e);
+        o[e] = none ? 0xFFFFFFFFu : (q8(v.x, sc) | q8(v.y, sc) << 8 | q8(v.z, sc) << 16 | q8(v.w, sc) << 24);
+    }
+}
+
 template <int G>
 __global__ void __launch_bounds__(LF_THREADS, 1) leafscan_kernel(
     const uint4 *__restrict__ sax, const uint8_t *__restrict__ lmeta, const uint8_t *__restrict__ smeta, uint32_t N,
-    const float *__restrict__ lut_all, const uint8_t *__restrict__ qsax_all, const uint32_t *__restrict__ qmap,
-    const float2 *__restrict__ band, uint32_t nq, uint32_t nleaf, uint32_t chunk, const unsigned long long *__restrict__ bsf,
-    const uint32_t *__restrict__ win, float onepd, uint32_t *__restrict__ cand, uint32_t *__restrict__ cand_cnt,
-    uint32_t cap, uint32_t *__restrict__ hist, uint32_t *__restrict__ leaves_alive,
-    unsigned long long *__restrict__ leaf_loads, uint32_t *__restrict__ task_ctr) {
-    // shared: [G][16][256] fp32 LUTs | [G][16][256] u8 LUTs | [G][CBUF] candidates | [CHUNK] worklist
+    const float *__restrict__ lut_all, const uint8_t *__restrict__ lut8_all, const uint4 *__restrict__ qconst_all,
+    const uint8_t *__restrict__ qsax_all, const uint32_t *__restrict__ qmap, uint32_t nq, uint32_t nleaf,
+    uint32_t chunk, uint32_t *__restrict__ cand, uint32_t *__restrict__ cand_cnt, uint32_t cap,
+    uint32_t *__restrict__ hist, uint32_t *__restrict__ leaves_alive, unsigned long long *__restrict__ scan_bytes_dev,
+    uint32_t *__restrict__ task_ctr) {
+    // shared: [G][16][256] u8 tables | [G][CBUF] candidates | [CHUNK] worklist | [NW][2][2 LEAF] words
     // (the dynamic region follows the static variables, so the u8 tables are aligned by hand: the
     // PRMT address trick needs a 256-aligned base)
     extern __shared__ __align__(16) uint8_t smem_dyn[];
@@ -261,15 +301,15 @@ __global__ void __launch_bounds__(LF_THREADS, 1) leafscan_kernel(
     uint8_t *lut8 = smem_dyn + (lut8_sh - raw8);
     uint32_t *cbuf = reinterpret_cast<uint32_t *>(lut8 + G * W * CARD);
     uint32_t *worklist = cbuf + G * CBUF;  // (leaf offset in chunk) | (query mask << 16)
-    uint4 *stage = reinterpret_cast<uint4 *>(worklist + CHUNK);  // [NW][2][LEAF] phase-B word staging
+    uint4 *stage = reinterpret_cast<uint4 *>(worklist + CHUNK);
     __shared__ QConst qc[G];
     __shared__ uint4 qsym[G][2];  // the query's 16 symbols as 8 u16x2 pairs
     __shared__ uint32_t qid[G], cb_cnt[G], alive_cnt[G], fbase[G];
     __shared__ uint32_t shist[G][HIST_BINS];
-    __shared__ float qscale[G];
     __shared__ uint32_t wl_cnt, s_task;
     const uint32_t t = threadIdx.x, lane = t & 31, warp = t >> 5;
     constexpr uint32_t NW = LF_THREADS / 32;
+    constexpr uint32_t FULL = 0xffffffffu;
     const uint32_t lt = (1u << lane) - 1u;
     const uint32_t nchunks = (nleaf + chunk - 1) / chunk;
     const uint32_t ngroups = (nq + G - 1) / G;
@@ -277,10 +317,14 @@ __global__ void __launch_bounds__(LF_THREADS, 1) leafscan_kernel(
     const uint4 *meta4 = reinterpret_cast<const uint4 *>(lmeta);
     const uint4 *smeta4 = reinterpret_cast<const uint4 *>(smeta);
     const uint32_t nsuper = (nleaf + SUPER - 1) / SUPER;
-    uint32_t loads = 0;
-    uint32_t g0 = 0xffffffffu;  // first query slot of the group whose LUTs are loaded
+    unsigned long long bytes = 0;  // leaf words and leaf summaries this thread's warp read (lane 0)
+    uint32_t my_alive = 0;         // lane g < G: loaded (leaf, query g) pairs of this warp
+    uint32_t g0 = 0xffffffffu;     // first query slot of the group whose tables are loaded
     // empty the shared candidate buffers and histograms of the loaded group into global memory
     auto flush = [&]() {
+        if (lane < G && my_alive) atomicAdd(&alive_cnt[lane], my_alive);
+        my_alive = 0;
+        __syncthreads();
         if (t < G) {
             const uint32_t c = min(cb_cnt[t], CBUF);
             fbase[t] = (c && g0 + t < nq) ? atomicAdd(&cand_cnt[qid[t]], c) : 0;
@@ -308,202 +352,209 @@ __global__ void __launch_bounds__(LF_THREADS, 1) leafscan_kernel(
         const uint32_t task = s_task;
         if (task >= ntasks) break;
         const uint32_t grp = task / nchunks, ch = task % nchunks;
-        if (grp * G != g0) {  // new query group: load its LUTs and constants
+        if (grp * G != g0) {  // new query group: load its tables and constants
             if (g0 != 0xffffffffu) flush();
             g0 = grp * G;
             for (uint32_t e = t; e < G * HIST_BINS; e += LF_THREADS) shist[e / HIST_BINS][e % HIST_BINS] = 0;
             if (t < G) {
                 const bool valid = g0 + t < nq;
-                const uint32_t qi = valid ? qmap[g0 + t] : qmap[g0];
+                const uint32_t slot = valid ? g0 + t : g0;
+                const uint32_t qi = qmap[slot];
                 qid[t] = qi;
                 cb_cnt[t] = 0;
                 alive_cnt[t] = 0;
                 const uint4 w = reinterpret_cast<const uint4 *>(qsax_all)[qi];
                 qsym[t][0] = make_uint4(lo_u16x2(w.x), hi_u16x2(w.x), lo_u16x2(w.y), hi_u16x2(w.y));
                 qsym[t][1] = make_uint4(lo_u16x2(w.z), hi_u16x2(w.z), lo_u16x2(w.w), hi_u16x2(w.w));
-                qc[t] = load_qconst(qi, valid, bsf, band, g0 + t, win, onepd);
-                qscale[t] = qc[t].T > 0.f ? __fdiv_rd(254.0f, qc[t].T) : 0.f;  // 254 / T, rounded down
+                const uint4 k = qconst_all[slot];
+                qc[t] = valid ? QConst{__uint_as_float(k.x), __uint_as_float(k.y), k.z, k.w} : QConst{0.f, -1.f, 0u, 0u};
             }
-            __syncthreads();
-            // u8 LUT (R12): e = floor(LUT * 254 / T), rounded down at every step and clamped at 255,
-            // so sum_s e <= LB^2 * 254 / T; "sum e > 254" implies LB^2 > T and prunes a member exactly
-            for (uint32_t e = t; e < G * W * CARD; e += LF_THREADS) {
-                const uint32_t g = e / (W * CARD);
-                const float sc = qscale[g];
-                uint32_t v = 255;
-                if (sc > 0.f) {
-                    const float lv = __ldg(lut_all + (uint64_t)qid[g] * W * CARD + (e % (W * CARD)));
-                    const float x = __fmul_rd(lv, sc);
-                    v = x >= 255.f ? 255u : (uint32_t)x;
-                }
-                lut8[e] = (uint8_t)v;
-            }
-            __syncthreads();
-        }
-        const uint32_t c0 = ch * chunk;
-        const uint32_t c1 = min(c0 + chunk, nleaf);
-        // ---- phase A: lane = leaf; warp w takes leaves c0 + 32 w + lane, then + 32 NW, ...
-        // A warp-iteration covers 32 consecutive leaves = two super-nodes of 16 leaves (chunk
-        // starts are multiples of 32). Lane (h = lane / 16, gq = lane % 16) first bounds super-node
-        // h for query gq (R11: one more level of the tree). A leaf bound is computed only for the
-        // queries whose super-node survived.
-        uint32_t leaf = c0 + warp * 32 + lane;
-        const uint32_t gq = lane & 15;
-        uint4 mn_n = make_uint4(0, 0, 0, 0), mx_n = make_uint4(~0u, ~0u, ~0u, ~0u);
-        uint4 smn_n = mn_n, smx_n = mx_n;
-        if (leaf < c1) {
-            mn_n = __ldg(meta4 + 2 * (uint64_t)leaf);
-            mx_n = __ldg(meta4 + 2 * (uint64_t)leaf + 1);
-        }
-        {
-            const uint32_t sup = (leaf - lane) / 16 + (lane >> 4);
-            if (sup < nsuper) {
-                smn_n = __ldg(smeta4 + 2 * (uint64_t)sup);
-                smx_n = __ldg(smeta4 + 2 * (uint64_t)sup + 1);
-            }
-        }
-        for (; leaf - lane < c1; leaf += 32 * NW) {
-            uint32_t smask_mine, smask_any;
+            // the group's u8 tables; a padding slot gets all-255 entries (it prunes everything)
             {
-                const uint32_t smn[8] = {lo_u16x2(smn_n.x), hi_u16x2(smn_n.x), lo_u16x2(smn_n.y), hi_u16x2(smn_n.y),
-                                         lo_u16x2(smn_n.z), hi_u16x2(smn_n.z), lo_u16x2(smn_n.w), hi_u16x2(smn_n.w)};
-                const uint32_t smx[8] = {lo_u16x2(smx_n.x), hi_u16x2(smx_n.x), lo_u16x2(smx_n.y), hi_u16x2(smx_n.y),
-                                         lo_u16x2(smx_n.z), hi_u16x2(smx_n.z), lo_u16x2(smx_n.w), hi_u16x2(smx_n.w)};
-                const uint32_t sup_n = (leaf + 32 * NW - lane) / 16 + (lane >> 4);
-                if (leaf + 32 * NW - lane < c1 && sup_n < nsuper) {  // prefetch the next super-nodes
-                    smn_n = __ldg(smeta4 + 2 * (uint64_t)sup_n);
-                    smx_n = __ldg(smeta4 + 2 * (uint64_t)sup_n + 1);
-                }
-                bool salive = false;
-                if (gq < G) {
-                    const uint4 qa = qsym[gq][0], qb = qsym[gq][1];
-                    const uint32_t qv[8] = {qa.x, qa.y, qa.z, qa.w, qb.x, qb.y, qb.z, qb.w};
-                    const uint32_t ub = lut8_sh + gq * W * CARD;
-                    uint32_t es = 0;
+                const uint4 *src = reinterpret_cast<const uint4 *>(lut8_all + (uint64_t)g0 * W * CARD);
+                uint4 *dst = reinterpret_cast<uint4 *>(lut8);
+                constexpr uint32_t PER = W * CARD / 16;
+                for (uint32_t e = t; e < G * PER; e += LF_THREADS)
+                    dst[e] = g0 + e / PER < nq ? __ldg(src + e) : make_uint4(FULL, FULL, FULL, FULL);
+            }
+            __syncthreads();
+        }
+        const uint32_t c0 = ch * chunk;  // a multiple of SUPER
+        const uint32_t c1 = min(c0 + chunk, nleaf);
+        // ---- phase A. Warp iteration j covers super-node sn = c0 / SUPER + warp + NW j.
+        const uint32_t sfirst = c0 / SUPER + warp, send = (c1 + SUPER - 1) / SUPER;
+        // lane j holds the summary of this warp's j-th super-node (<= 8 per chunk)
+        uint4 pmn = make_uint4(0, 0, 0, 0), pmx = pmn;
+        {
+            const uint32_t sj = sfirst + NW * lane;
+            if (sj < send && sj < nsuper) {
+                pmn = __ldg(smeta4 + 2 * (uint64_t)sj);
+                pmx = __ldg(smeta4 + 2 * (uint64_t)sj + 1);
+            }
+        }
+        // super test of the warp's j-th super-node: lane (gq, hs) sums segments 8 hs .. 8 hs + 7 for
+        // query gq, the two halves are combined with one shuffle. Returns the mask of queries kept.
+        const uint32_t gq = lane & 15u, hs = lane >> 4;
+        const uint32_t ubq = lut8_sh + (gq < G ? gq : 0u) * W * CARD + hs * 8u * CARD;
+        auto super_mask = [&](uint32_t j) -> uint32_t {
+            // (the source lane evaluates the shuffled operand, so all four words are moved and
+            // the half is selected after the shuffle)
+            const uint32_t nx = __shfl_sync(FULL, pmn.x, j), ny = __shfl_sync(FULL, pmn.y, j);
+            const uint32_t nz = __shfl_sync(FULL, pmn.z, j), nw = __shfl_sync(FULL, pmn.w, j);
+            const uint32_t xx = __shfl_sync(FULL, pmx.x, j), xy = __shfl_sync(FULL, pmx.y, j);
+            const uint32_t xz = __shfl_sync(FULL, pmx.z, j), xw = __shfl_sync(FULL, pmx.w, j);
+            const uint32_t a0 = hs ? nz : nx, a1 = hs ? nw : ny, b0 = hs ? xz : xx, b1 = hs ? xw : xy;
+            const uint4 qh = qsym[gq < G ? gq : 0u][hs];
+            const uint32_t qv[4] = {qh.x, qh.y, qh.z, qh.w};
+            const uint32_t smn[4] = {lo_u16x2(a0), hi_u16x2(a0), lo_u16x2(a1), hi_u16x2(a1)};
+            const uint32_t smx[4] = {lo_u16x2(b0), hi_u16x2(b0), lo_u16x2(b1), hi_u16x2(b1)};
+            uint32_t es = 0;
 #pragma unroll
-                    for (int k = 0; k < 8; k++) {
-                        const uint32_t c2 = min_u16x2(max_u16x2(qv[k], smn[k]), smx[k]);
-                        es += ld_sh_u8(__byte_perm(c2, ub, 0x7650u) + (2 * k) * CARD);
-                        es += ld_sh_u8(__byte_perm(c2, ub, 0x7652u) + (2 * k + 1) * CARD);
-                    }
-                    salive = es <= 254u;
+            for (int k = 0; k < 4; k++) {
+                const uint32_t c2 = min_u16x2(max_u16x2(qv[k], smn[k]), smx[k]);
+                es += ld_sh_u8(__byte_perm(c2, ubq, 0x7650u) + (2 * k) * CARD);
+                es += ld_sh_u8(__byte_perm(c2, ubq, 0x7652u) + (2 * k + 1) * CARD);
+            }
+            es += __shfl_xor_sync(FULL, es, 16);
+            return __ballot_sync(FULL, gq < G && es <= 254u) & 0xFFFFu;
+        };
+        // software pipeline: the super test and leaf-summary loads of iteration j + 1 are issued
+        // before the leaf tests of iteration j
+        uint32_t smask = 0;
+        uint4 mn_n = make_uint4(0, 0, 0, 0), mx_n = mn_n;
+        if (sfirst < send) {
+            smask = super_mask(0);
+            const uint32_t leaf = sfirst * SUPER + lane;
+            if (smask && leaf < c1) {
+                mn_n = __ldg(meta4 + 2 * (uint64_t)leaf);
+                mx_n = __ldg(meta4 + 2 * (uint64_t)leaf + 1);
+            }
+        }
+        uint32_t j = 0;
+        for (uint32_t sn = sfirst; sn < send; sn += NW, j++) {
+            const uint32_t leaf = sn * SUPER + lane;
+            const uint32_t cur_mask = smask;
+            const uint4 mn4 = mn_n, mx4 = mx_n;
+            if (sn + NW < send) {
+                smask = super_mask(j + 1);
+                const uint32_t l2 = leaf + NW * SUPER;
+                if (smask && l2 < c1) {
+                    mn_n = __ldg(meta4 + 2 * (uint64_t)l2);
+                    mx_n = __ldg(meta4 + 2 * (uint64_t)l2 + 1);
                 }
-                const uint32_t sb = __ballot_sync(0xffffffffu, salive);
-                smask_mine = lane < 16 ? (sb & 0xFFFFu) : (sb >> 16);
-                smask_any = (sb & 0xFFFFu) | (sb >> 16);
             }
+            if (!cur_mask) continue;  // the whole super-node is pruned for every query
+            if (lane == 0) bytes += 32ull * SUPER;
             // the leaf's per-segment [min, max] as u16x2 pairs (segments 2j, 2j+1)
-            const uint32_t mn[8] = {lo_u16x2(mn_n.x), hi_u16x2(mn_n.x), lo_u16x2(mn_n.y), hi_u16x2(mn_n.y),
-                                    lo_u16x2(mn_n.z), hi_u16x2(mn_n.z), lo_u16x2(mn_n.w), hi_u16x2(mn_n.w)};
-            const uint32_t mx[8] = {lo_u16x2(mx_n.x), hi_u16x2(mx_n.x), lo_u16x2(mx_n.y), hi_u16x2(mx_n.y),
-                                    lo_u16x2(mx_n.z), hi_u16x2(mx_n.z), lo_u16x2(mx_n.w), hi_u16x2(mx_n.w)};
-            const uint32_t nxt = leaf + 32 * NW;
-            if (nxt < c1) {  // software pipeline: the next node summary is in flight
-                mn_n = __ldg(meta4 + 2 * (uint64_t)nxt);
-                mx_n = __ldg(meta4 + 2 * (uint64_t)nxt + 1);
-            }
+            const uint32_t mn[8] = {lo_u16x2(mn4.x), hi_u16x2(mn4.x), lo_u16x2(mn4.y), hi_u16x2(mn4.y),
+                                    lo_u16x2(mn4.z), hi_u16x2(mn4.z), lo_u16x2(mn4.w), hi_u16x2(mn4.w)};
+            const uint32_t mx[8] = {lo_u16x2(mx4.x), hi_u16x2(mx4.x), lo_u16x2(mx4.y), hi_u16x2(mx4.y),
+                                    lo_u16x2(mx4.z), hi_u16x2(mx4.z), lo_u16x2(mx4.w), hi_u16x2(mx4.w)};
             uint32_t alive = 0;
 #pragma unroll
             for (int g = 0; g < G; g++) {
-                if (!((smask_any >> g) & 1u)) continue;  // both super-nodes pruned for query g
+                if (!((cur_mask >> g) & 1u)) continue;
                 const uint4 qa = qsym[g][0], qb = qsym[g][1];
                 const uint32_t qv[8] = {qa.x, qa.y, qa.z, qa.w, qb.x, qb.y, qb.z, qb.w};
                 uint32_t cl[8];
 #pragma unroll
                 for (int k = 0; k < 8; k++) cl[k] = min_u16x2(max_u16x2(qv[k], mn[k]), mx[k]);
-                {
-                    // u8 node bound: sum of floor(LUT * 254 / T) terms. A pruned node (sum > 254)
-                    // has every member's u8 sum > 254 too (floor is monotone), and the u8 member test
-                    // is a superset of the exact one, so no candidate is lost.
-                    const uint32_t ub = lut8_sh + g * W * CARD;
-                    uint32_t es = 0;
+                const uint32_t ub = lut8_sh + g * W * CARD;
+                uint32_t es = 0;
 #pragma unroll
-                    for (int s2 = 0; s2 < W; s2++)
-                        es += ld_sh_u8(__byte_perm(cl[s2 >> 1], ub, 0x7650u | (uint32_t)(2 * (s2 & 1))) + s2 * CARD);
-                    if (es <= 254u) alive |= 1u << g;
-                }
+                for (int s2 = 0; s2 < W; s2++)
+                    es += ld_sh_u8(__byte_perm(cl[s2 >> 1], ub, 0x7650u | (uint32_t)(2 * (s2 & 1))) + s2 * CARD);
+                if (es <= 254u) alive |= 1u << g;
             }
-            alive &= smask_mine;
             if (leaf >= c1) alive = 0;
-            const uint32_t bal = __ballot_sync(0xffffffffu, alive != 0);
+            const uint32_t bal = __ballot_sync(FULL, alive != 0);
             if (bal) {
                 uint32_t off = 0;
                 if (lane == 0) off = atomicAdd(&wl_cnt, (uint32_t)__popc(bal));
-                off = __shfl_sync(0xffffffffu, off, 0);
+                off = __shfl_sync(FULL, off, 0);
                 if (alive) worklist[off + __popc(bal & lt)] = (leaf - c0) | (alive << 16);
             }
         }
         __syncthreads();
-        // ---- phase B: the members of surviving leaves. Each warp takes entries warp, warp + NW,
-        // ... and double-buffers their 1 KB of words in its own shared staging slots with
-        // cp.async: the next leaf is in flight while the current one is tested (no registers
-        // held across the global latency).
+        // ---- phase B: the members of surviving leaves, two worklist entries (A, B) per warp step.
+        // Each warp takes steps warp, warp + NW, ... and double-buffers their words in its own
+        // shared staging slots with cp.async: the next step is in flight while the current one is
+        // tested (no registers held across the global latency).
         const uint32_t nwl = wl_cnt;
-        uint4 *slot = stage + warp * 2 * LEAF;  // [2][LEAF] words
-        auto prefetch = [&](uint32_t e, uint32_t buf) {
-            const uint32_t base = (c0 + (worklist[e] & 0xFFFFu)) * LEAF;
+        const uint32_t nstep = (nwl + 1) / 2;
+        uint4 *slot = stage + warp * 4 * LEAF;  // [2 buffers][2 entries][LEAF] words
+        auto prefetch = [&](uint32_t p, uint32_t buf) {
 #pragma unroll
-            for (int u = 0; u < 2; u++) {
-                const uint32_t pos = base + u * 32 + lane;
-                cp_async16(slot + buf * LEAF + u * 32 + lane, sax + (pos < N ? pos : 0), pos < N);
+            for (uint32_t u = 0; u < 2; u++) {
+                const uint32_t e = 2 * p + u;
+                const uint32_t pos = e < nwl ? (c0 + (worklist[e] & 0xFFFFu)) * LEAF + lane : N;
+                cp_async16(slot + (2 * buf + u) * LEAF + lane, sax + (pos < N ? pos : 0), pos < N);
             }
             cp_async_commit();
         };
-        if (warp < nwl) prefetch(warp, 0);
+        if (warp < nstep) prefetch(warp, 0);
         uint32_t buf = 0;
-        for (uint32_t e = warp; e < nwl; e += NW, buf ^= 1u) {
-            const bool more = e + NW < nwl;
-            if (more) prefetch(e + NW, buf ^ 1u);
+        for (uint32_t p = warp; p < nstep; p += NW, buf ^= 1u) {
+            const bool more = p + NW < nstep;
+            if (more) prefetch(p + NW, buf ^ 1u);
             if (more) cp_async_wait<1>();
             else cp_async_wait<0>();
             __syncwarp();
-            const uint32_t ent = worklist[e];
-            const uint32_t am = ent >> 16;
-            const uint32_t base = (c0 + (ent & 0xFFFFu)) * LEAF;
-            uint4 wv[2];
-#pragma unroll
-            for (int u = 0; u < 2; u++) wv[u] = slot[buf * LEAF + u * 32 + lane];
-            loads++;
-            if (lane < G && ((am >> lane) & 1u)) atomicAdd(&alive_cnt[lane], 1u);
-            // rolled loop over the queries that kept the leaf: unrolling it over G made the
+            const bool hasB = 2 * p + 1 < nwl;
+            const uint32_t entA = worklist[2 * p], entB = hasB ? worklist[2 * p + 1] : 0u;
+            const uint32_t mA = entA >> 16, mB = entB >> 16;
+            const uint32_t pA = (c0 + (entA & 0xFFFFu)) * LEAF + lane;
+            const uint32_t pB = hasB ? (c0 + (entB & 0xFFFFu)) * LEAF + lane : N;
+            const uint4 wA = slot[(2 * buf) * LEAF + lane], wB = slot[(2 * buf + 1) * LEAF + lane];
+            if (lane == 0) bytes += (hasB ? 2ull : 1ull) * 16ull * LEAF;
+            if (lane < G) my_alive += ((mA >> lane) & 1u) + ((mB >> lane) & 1u);
+            // rolled loop over the queries that kept either leaf: unrolling it over G made the
             // kernel ~120 KB of SASS, and instruction-cache misses became the top stall
 #pragma unroll 1
-            for (uint32_t mm = am; mm; mm &= mm - 1) {
+            for (uint32_t mm = mA | mB; mm; mm &= mm - 1) {
                 const uint32_t g = __ffs(mm) - 1;
-                const uint32_t ub = lut8_sh + g * W * CARD;  // this query's u8 LUT (256-aligned)
-                // integer filter of both half-leaves: 3 instructions per lookup (PRMT address,
-                // LDS.U8, IADD), 32 independent shared loads, one warp vote
-                const uint32_t p0 = base + lane, p1 = base + 32 + lane;
-                const uint32_t e0 = word_e8(ub, wv[0]), e1 = word_e8(ub, wv[1]);
-                const bool m0 = p0 < N && e0 <= 254u, m1 = p1 < N && e1 <= 254u;
-                if (!__any_sync(0xffffffffu, m0 || m1)) continue;
+                const uint32_t ub = lut8_sh + g * W * CARD;  // this query's u8 table (256-aligned)
+                const bool inA = (mA >> g) & 1u, inB = (mB >> g) & 1u;
+                // integer member filter: 3 instructions per lookup (PRMT address, LDS.U8, IADD);
+                // two independent chains when both leaves kept the query
+                uint32_t eA = 255u, eB = 255u;
+                if (inA && inB) {
+                    eA = word_e8(ub, wA);
+                    eB = word_e8(ub, wB);
+                } else if (inA) {
+                    eA = word_e8(ub, wA);
+                } else {
+                    eB = word_e8(ub, wB);
+                }
+                const bool m0 = pA < N && eA <= 254u, m1 = pB < N && eB <= 254u;
+                if (!__any_sync(FULL, m0 || m1)) continue;
                 // rare: the exact fp32 test, the same rule as the flat scan
                 const QConst kq = qc[g];
                 const float *Lg = lut_all + (uint64_t)qid[g] * W * CARD;
 #pragma unroll
                 for (int u = 0; u < 2; u++) {
                     const bool maybe = u ? m1 : m0;
-                    const uint32_t pos = u ? p1 : p0;
-                    const float lb = maybe ? word_lb(Lg, wv[u]) : 0.f;
+                    const uint32_t pos = u ? pB : pA;
+                    const float lb = maybe ? word_lb(Lg, u ? wB : wA) : 0.f;
                     const bool keep = maybe && lb > kq.lo && lb <= kq.T && (pos < kq.ws || pos >= kq.we);
                     if (keep) atomicAdd(&shist[g][hist_bin(lb, kq.lo, kq.T)], 1u);
                     emit(keep, pos, g, qid[g], lane, lt, cbuf, cb_cnt, cand, cand_cnt, cap);
                 }
             }
-            __syncwarp();  // the slot is rewritten by the prefetch two entries ahead
+            __syncwarp();  // the slots are rewritten by the prefetch two steps ahead
         }
         __syncthreads();
         if (t == 0) wl_cnt = 0;
     }
     if (g0 != 0xffffffffu) flush();
-    if (lane == 0 && loads) atomicAdd(leaf_loads, (unsigned long long)loads);
+    if (lane == 0 && bytes) atomicAdd(scan_bytes_dev, bytes);
 }
 
 template <int G>
-static void launch_leaf(const isax_index *ix, uint32_t nq, const uint32_t *qmap, const float2 *band, float onepd,
-                        cudaStream_t s) {
+static void launch_leaf(const isax_index *ix, uint32_t nq, const uint32_t *qmap, cudaStream_t s) {
+    constexpr uint32_t NW = LF_THREADS / 32;
     const size_t smem = (size_t)G * W * CARD + 256 + (size_t)G * CBUF * sizeof(uint32_t) + CHUNK * 4 +
-                        (size_t)(LF_THREADS / 32) * 2 * LEAF * sizeof(uint4);
+                        (size_t)NW * 4 * LEAF * sizeof(uint4);
     static bool configured = false;
     if (!configured) {
         cudaFuncSetAttribute(leafscan_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -514,7 +565,8 @@ static void launch_leaf(const isax_index *ix, uint32_t nq, const uint32_t *qmap,
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const uint32_t groups = (nq + G - 1) / G;
     const uint32_t nleaf = (uint32_t)((ix->N + LEAF - 1) / LEAF);
-    // chunk: as large as possible (fewer phase barriers) while leaving >= 8 tasks per SM for balance
+    // chunk: as large as possible (fewer phase barriers) while leaving >= 8 tasks per SM for
+    // balance; a power of two >= 512, so a multiple of SUPER
     uint32_t chunk = CHUNK;
     while (chunk > 512 && (uint64_t)groups * ((nleaf + chunk - 1) / chunk) < 8ull * sms) chunk >>= 1;
     const uint64_t tasks = (uint64_t)groups * ((nleaf + chunk - 1) / chunk);
@@ -522,10 +574,9 @@ static void launch_leaf(const isax_index *ix, uint32_t nq, const uint32_t *qmap,
     const QueryScratch &qs = ix->qs;
     cudaMemsetAsync(qs.task_ctr, 0, sizeof(uint32_t), s);
     leafscan_kernel<G><<<grid, LF_THREADS, smem, s>>>(
-        reinterpret_cast<const uint4 *>(ix->sax), ix->lmeta, ix->smeta, (uint32_t)ix->N, qs.lut, qs.qsax, qmap, band, nq,
-        nleaf,
-        chunk, qs.bsf, qs.win, onepd, qs.cand, qs.cand_cnt, qs.cand_cap, qs.cand_hist, qs.counters_leaf, qs.leaf_loads,
-        qs.task_ctr);
+        reinterpret_cast<const uint4 *>(ix->sax), ix->lmeta, ix->smeta, (uint32_t)ix->N, qs.lut, qs.lut8, qs.qconst,
+        qs.qsax, qmap, nq, nleaf, chunk, qs.cand, qs.cand_cnt, qs.cand_cap, qs.cand_hist, qs.counters_leaf,
+        qs.scan_bytes_dev, qs.task_ctr);
 }
 
 uint64_t launch_lbscan(const isax_index *ix, uint32_t nq, const uint32_t *qmap, const float2 *band, float delta,
@@ -540,14 +591,16 @@ uint64_t launch_lbscan(const isax_index *ix, uint32_t nq, const uint32_t *qmap, 
         else launch_g<1>(ix, nq, qmap, band, onepd, s);
         return 16ull * ix->N * ((nq + G - 1) / G);  // words read
     }
+    const QueryScratch &qs = ix->qs;
+    scanprep_kernel<<<nq, 256, 0, s>>>(qs.lut, qmap, band, qs.bsf, qs.win, onepd, qs.lut8, qs.qconst);
     const uint32_t G = nq >= 16 ? 16 : nq >= 8 ? 8 : nq >= 4 ? 4 : nq >= 2 ? 2 : 1;
-    if (G == 16) launch_leaf<16>(ix, nq, qmap, band, onepd, s);
-    else if (G == 8) launch_leaf<8>(ix, nq, qmap, band, onepd, s);
-    else if (G == 4) launch_leaf<4>(ix, nq, qmap, band, onepd, s);
-    else if (G == 2) launch_leaf<2>(ix, nq, qmap, band, onepd, s);
-    else launch_leaf<1>(ix, nq, qmap, band, onepd, s);
-    const uint64_t leaves = (ix->N + LEAF - 1) / LEAF;
-    return 32ull * leaves * ((nq + G - 1) / G);  // node summaries read; leaf words are counted on the device
+    if (G == 16) launch_leaf<16>(ix, nq, qmap, s);
+    else if (G == 8) launch_leaf<8>(ix, nq, qmap, s);
+    else if (G == 4) launch_leaf<4>(ix, nq, qmap, s);
+    else if (G == 2) launch_leaf<2>(ix, nq, qmap, s);
+    else launch_leaf<1>(ix, nq, qmap, s);
+    const uint64_t nsuper = (ix->N + SUPER_SIZE - 1) / SUPER_SIZE;
+    return 32ull * nsuper * ((nq + G - 1) / G);  // super-node summaries; leaf summaries and words are counted on the device
 }
 
 // ------------------------------------------------------------------------------------ leaf meta

@@ -120,7 +120,7 @@ def test_candidate_set_is_exactly_the_lb_filter(N, n, kind):
         lb_or = ref.lb2(qm[i], words_sorted, n)
         lb_or[w0:w1] = np.inf
         assert (lb_or <= T * (1 - 1e-5)).sum() <= st["candidates"][i] <= (lb_or <= T * (1 + 1e-5)).sum()
-        assert st["leaves_alive"][i] <= (N + 63) // 64
+        assert st["leaves_alive"][i] <= (N + st["leaf_size"] - 1) // st["leaf_size"]
     assert st_f["leaves_alive"] == [0] * len(qh)
 
 
