@@ -164,7 +164,7 @@ static int build_impl(const Source &src, uint64_t N, uint32_t n, uint32_t w, uin
         cudaStreamSynchronize(s);
         cudaFree(sax_by_id); cudaFree(keys); cudaFree(musig); cudaFree(ids); cudaFree(bad); cudaFree(inv);
         cudaFree(stage);
-        cudaFree(ix->stored); cudaFree(ix->sax); cudaFree(ix->perm); cudaFree(ix->lmeta); cudaFree(ix->smeta);
+        cudaFree(ix->stored); cudaFree(ix->sax); cudaFree(ix->perm); cudaFree(ix->lmeta); cudaFree(ix->smeta); cudaFree(ix->hmeta);
         delete ix;
         cudaStreamDestroy(s);
         return code;
@@ -216,7 +216,8 @@ static int build_impl(const Source &src, uint64_t N, uint32_t n, uint32_t w, uin
     launch_gather_sax(sax_by_id, ix->perm, N, ix->sax, s);
     TRY(dmalloc(&ix->lmeta, ((N + LEAF_SIZE - 1) / LEAF_SIZE) * 32, &ix->device_bytes));
     TRY(dmalloc(&ix->smeta, ((N + SUPER_SIZE - 1) / SUPER_SIZE) * 32, &ix->device_bytes));
-    launch_leaf_meta(ix->sax, N, ix->lmeta, ix->smeta, s);
+    TRY(dmalloc(&ix->hmeta, ((N + HYPER_SIZE - 1) / HYPER_SIZE) * 32, &ix->device_bytes));
+    launch_leaf_meta(ix->sax, N, ix->lmeta, ix->smeta, ix->hmeta, s);
     TRY(cudaStreamSynchronize(s));
     cudaFree(sax_by_id);
     sax_by_id = nullptr;
@@ -630,6 +631,7 @@ int isax_stats(const isax_index *cix, char *buf, size_t cap) {
     j += ",\"leaves\":" + std::to_string((ix->N + LEAF_SIZE - 1) / LEAF_SIZE);
     j += ",\"leaf_size\":" + std::to_string(LEAF_SIZE);
     j += ",\"super_size\":" + std::to_string(SUPER_SIZE);
+    j += ",\"hyper_size\":" + std::to_string(HYPER_SIZE);
     j += "}";
     if (buf && cap) {
         size_t k = std::min(cap - 1, j.size());
@@ -658,6 +660,7 @@ void isax_free(isax_index *ix) {
         cudaFree(ix->perm);
         cudaFree(ix->lmeta);
         cudaFree(ix->smeta);
+        cudaFree(ix->hmeta);
         free_scratch(ix);
         for (auto &ev : ix->ev)
             if (ev) cudaEventDestroy(ev);

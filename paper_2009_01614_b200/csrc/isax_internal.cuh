@@ -24,6 +24,7 @@ constexpr uint32_t MAX_PROBES = 32;  // 2^probe_bits windows per query, probe_bi
 constexpr uint32_t HIST_BINS = 64;   // per-query histogram of kept LB^2 inside its band (R10)
 constexpr uint32_t LEAF_SIZE = 32;    // sorted positions per leaf node (R11)
 constexpr uint32_t SUPER_SIZE = 1024; // sorted positions per super-node (R11)
+constexpr uint32_t HYPER_SIZE = 32768; // sorted positions per hyper-node (R11)
 
 // Packed BSF: high 32 bits = fp32 bits of d^2 (non-negative, so the bit order is the
 // numeric order), low 32 bits = original id. atomicMin on the packed word is the
@@ -117,6 +118,7 @@ struct isax_index {
     uint32_t *perm = nullptr;
     uint8_t *lmeta = nullptr;  // [ceil(N/LEAF_SIZE)][32]: per-leaf min (16 B) and max (16 B) symbols
     uint8_t *smeta = nullptr;  // [ceil(N/SUPER_SIZE)][32]: per-super-node min and max symbols
+    uint8_t *hmeta = nullptr;  // [ceil(N/HYPER_SIZE)][32]: per-hyper-node min and max symbols
     size_t device_bytes = 0;
     isax::QueryScratch qs;
     std::mutex mu;
@@ -175,7 +177,7 @@ void launch_window(const isax_index *ix, uint32_t Q, const uint32_t *qmap, float
 void launch_lb_dump(const isax_index *ix, uint32_t Q, uint64_t first_pos, uint64_t count, float *out,
                     cudaStream_t s);
 // lbscan.cu
-void launch_leaf_meta(const uint8_t *sax, uint64_t N, uint8_t *lmeta, uint8_t *smeta, cudaStream_t s);
+void launch_leaf_meta(const uint8_t *sax, uint64_t N, uint8_t *lmeta, uint8_t *smeta, uint8_t *hmeta, cudaStream_t s);
 // Scan all sorted positions for the nq queries qmap[0..nq), keeping band[i].x < LB^2 <= min(band[i].y,
 // bsf^2 (1+delta)) for slot i. Returns the summary bytes it reads that the host can count (node
 // summaries or flat words); the leaf scan adds its leaf-word and leaf-summary bytes to qs.scan_bytes_dev on the device.

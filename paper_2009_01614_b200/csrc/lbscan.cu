@@ -71,6 +71,26 @@ __device__ __forceinline__ uint32_t word_e8(uint32_t ub, const uint4 &wv) {
     return es;
 }
 
+// u8 node bound (R11, R11b) of a node summary (per-segment min mn, max mx) against one query:
+// q holds the query's symbols as 8 u16x2 pairs; each term is the table entry at the clamped
+// symbol, clamp(q_s, mn_s, mx_s), done two segments at a time with u16x2 min / max.
+__device__ __forceinline__ uint32_t node_e8(uint32_t ub, const uint4 &qa, const uint4 &qb, const uint4 &mn4,
+                                           const uint4 &mx4) {
+    const uint32_t qv[8] = {qa.x, qa.y, qa.z, qa.w, qb.x, qb.y, qb.z, qb.w};
+    const uint32_t mn[8] = {lo_u16x2(mn4.x), hi_u16x2(mn4.x), lo_u16x2(mn4.y), hi_u16x2(mn4.y),
+                            lo_u16x2(mn4.z), hi_u16x2(mn4.z), lo_u16x2(mn4.w), hi_u16x2(mn4.w)};
+    const uint32_t mx[8] = {lo_u16x2(mx4.x), hi_u16x2(mx4.x), lo_u16x2(mx4.y), hi_u16x2(mx4.y),
+                            lo_u16x2(mx4.z), hi_u16x2(mx4.z), lo_u16x2(mx4.w), hi_u16x2(mx4.w)};
+    uint32_t es = 0;
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+        const uint32_t c2 = min_u16x2(max_u16x2(qv[k], mn[k]), mx[k]);
+        es += ld_sh_u8(__byte_perm(c2, ub, 0x7650u) + (2 * k) * CARD);
+        es += ld_sh_u8(__byte_perm(c2, ub, 0x7652u) + (2 * k + 1) * CARD);
+    }
+    return es;
+}
+
 // 16-byte global -> shared asynchronous copy (LDGSTS); zero-fills the destination when !valid
 __device__ __forceinline__ void cp_async16(void *dst_smem, const void *src, bool valid) {
     const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst_smem);
@@ -222,10 +242,15 @@ static void launch_g(const isax_index *ix, uint32_t nq, const uint32_t *qmap, co
 //     query slot and flushed once per group (one global atomic per slot).
 constexpr uint32_t LEAF = LEAF_SIZE;
 constexpr uint32_t SUPER = SUPER_SIZE / LEAF_SIZE;  // leaves per super-node
+constexpr uint32_t HYPER = HYPER_SIZE / SUPER_SIZE; // super-nodes per hyper-node
+static_assert(HYPER == 32, "phase A maps the super-nodes of a hyper-node to the lanes of a warp");
 static_assert(LEAF == 32 && SUPER == 32, "phase A maps a super-node to a warp iteration and a leaf to a lane");
 constexpr int LF_THREADS = 1024;
 constexpr uint32_t CHUNK = 8192;  // max leaves per phase-A/phase-B round of a CTA
 constexpr uint32_t CBUF = 512;    // shared candidate buffer per query slot
+// a u8 member sum <= E_SURE implies LB^2 <= T: sum_s LUT_s * sc < (sum e + 16) / (1 - 2^-23) and
+// sc >= (254 / T)(1 - 2^-23), so LB^2 < (237 + 16) / 254 * T * (1 + 2^-20) < T (R11b)
+constexpr uint32_t E_SURE = 237;
 
 // append `keep` lanes' positions for query slot g: shared buffer first, global list if it is full
 __device__ __forceinline__ void emit(bool keep, uint32_t pos, uint32_t g, uint32_t q, uint32_t lane, uint32_t lt,
@@ -286,8 +311,8 @@ __global__ void __launch_bounds__(256) scanprep_kernel(const float *__restrict__
 
 template <int G>
 __global__ void __launch_bounds__(LF_THREADS, 1) leafscan_kernel(
-    const uint4 *__restrict__ sax, const uint8_t *__restrict__ lmeta, const uint8_t *__restrict__ smeta, uint32_t N,
-    const float *__restrict__ lut_all, const uint8_t *__restrict__ lut8_all, const uint4 *__restrict__ qconst_all,
+    const uint4 *__restrict__ sax, const uint8_t *__restrict__ lmeta, const uint8_t *__restrict__ smeta,
+    const uint8_t *__restrict__ hmeta, uint32_t N, const float *__restrict__ lut_all, const uint8_t *__restrict__ lut8_all, const uint4 *__restrict__ qconst_all,
     const uint8_t *__restrict__ qsax_all, const uint32_t *__restrict__ qmap, uint32_t nq, uint32_t nleaf,
     uint32_t chunk, uint32_t *__restrict__ cand, uint32_t *__restrict__ cand_cnt, uint32_t cap,
     uint32_t *__restrict__ hist, uint32_t *__restrict__ leaves_alive, unsigned long long *__restrict__ scan_bytes_dev,
@@ -307,6 +332,8 @@ __global__ void __launch_bounds__(LF_THREADS, 1) leafscan_kernel(
     __shared__ uint32_t qid[G], cb_cnt[G], alive_cnt[G], fbase[G];
     __shared__ uint32_t shist[G][HIST_BINS];
     __shared__ uint32_t wl_cnt, s_task;
+    __shared__ uint32_t hmask[CHUNK / (SUPER * HYPER) + 1];  // query mask of each hyper-node of the chunk
+    __shared__ uint32_t smask_sh[CHUNK / SUPER];            // query mask of each super-node of the chunk
     const uint32_t t = threadIdx.x, lane = t & 31, warp = t >> 5;
     constexpr uint32_t NW = LF_THREADS / 32;
     constexpr uint32_t FULL = 0xffffffffu;
@@ -316,8 +343,8 @@ __global__ void __launch_bounds__(LF_THREADS, 1) leafscan_kernel(
     const uint32_t ntasks = nchunks * ngroups;
     const uint4 *meta4 = reinterpret_cast<const uint4 *>(lmeta);
     const uint4 *smeta4 = reinterpret_cast<const uint4 *>(smeta);
-    const uint32_t nsuper = (nleaf + SUPER - 1) / SUPER;
-    unsigned long long bytes = 0;  // leaf words and leaf summaries this thread's warp read (lane 0)
+    const uint4 *hmeta4 = reinterpret_cast<const uint4 *>(hmeta);
+    uint32_t bytes = 0;            // node summaries and words this thread read
     uint32_t my_alive = 0;         // lane g < G: loaded (leaf, query g) pairs of this warp
     uint32_t g0 = 0xffffffffu;     // first query slot of the group whose tables are loaded
     // empty the shared candidate buffers and histograms of the loaded group into global memory
@@ -381,90 +408,68 @@ __global__ void __launch_bounds__(LF_THREADS, 1) leafscan_kernel(
         }
         const uint32_t c0 = ch * chunk;  // a multiple of SUPER
         const uint32_t c1 = min(c0 + chunk, nleaf);
-        // ---- phase A. Warp iteration j covers super-node sn = c0 / SUPER + warp + NW j.
-        const uint32_t sfirst = c0 / SUPER + warp, send = (c1 + SUPER - 1) / SUPER;
-        // lane j holds the summary of this warp's j-th super-node (<= 8 per chunk)
-        uint4 pmn = make_uint4(0, 0, 0, 0), pmx = pmn;
-        {
-            const uint32_t sj = sfirst + NW * lane;
-            if (sj < send && sj < nsuper) {
-                pmn = __ldg(smeta4 + 2 * (uint64_t)sj);
-                pmx = __ldg(smeta4 + 2 * (uint64_t)sj + 1);
+        // ---- phase A: three node levels, top down.
+        const uint32_t s0 = c0 / SUPER, send = (c1 + SUPER - 1) / SUPER;  // the chunk's super-nodes
+        const uint32_t h0 = s0 / HYPER, nh = (send - 1) / HYPER - h0 + 1;  // its hyper-nodes (<= 8)
+        for (uint32_t e = t; e < send - s0; e += LF_THREADS) smask_sh[e] = 0;
+        if (t < nh) hmask[t] = 0;
+        __syncthreads();
+        // A0: thread = (hyper-node, query). A hyper-node may extend beyond the chunk (chunk of 512
+        // leaves): its bound is over a superset of the chunk's positions, still a lower bound.
+        if (t < nh * 16u) {
+            const uint32_t h = t >> 4, g = t & 15u;
+            if (g < G) {
+                const uint4 a = __ldg(hmeta4 + 2 * (uint64_t)(h0 + h)), b = __ldg(hmeta4 + 2 * (uint64_t)(h0 + h) + 1);
+                if (node_e8(lut8_sh + g * W * CARD, qsym[g][0], qsym[g][1], a, b) <= 254u) atomicOr(&hmask[h], 1u << g);
+                bytes += 32;
             }
         }
-        // super test of the warp's j-th super-node: lane (gq, hs) sums segments 8 hs .. 8 hs + 7 for
-        // query gq, the two halves are combined with one shuffle. Returns the mask of queries kept.
-        const uint32_t gq = lane & 15u, hs = lane >> 4;
-        const uint32_t ubq = lut8_sh + (gq < G ? gq : 0u) * W * CARD + hs * 8u * CARD;
-        auto super_mask = [&](uint32_t j) -> uint32_t {
-            // (the source lane evaluates the shuffled operand, so all four words are moved and
-            // the half is selected after the shuffle)
-            const uint32_t nx = __shfl_sync(FULL, pmn.x, j), ny = __shfl_sync(FULL, pmn.y, j);
-            const uint32_t nz = __shfl_sync(FULL, pmn.z, j), nw = __shfl_sync(FULL, pmn.w, j);
-            const uint32_t xx = __shfl_sync(FULL, pmx.x, j), xy = __shfl_sync(FULL, pmx.y, j);
-            const uint32_t xz = __shfl_sync(FULL, pmx.z, j), xw = __shfl_sync(FULL, pmx.w, j);
-            const uint32_t a0 = hs ? nz : nx, a1 = hs ? nw : ny, b0 = hs ? xz : xx, b1 = hs ? xw : xy;
-            const uint4 qh = qsym[gq < G ? gq : 0u][hs];
-            const uint32_t qv[4] = {qh.x, qh.y, qh.z, qh.w};
-            const uint32_t smn[4] = {lo_u16x2(a0), hi_u16x2(a0), lo_u16x2(a1), hi_u16x2(a1)};
-            const uint32_t smx[4] = {lo_u16x2(b0), hi_u16x2(b0), lo_u16x2(b1), hi_u16x2(b1)};
-            uint32_t es = 0;
-#pragma unroll
-            for (int k = 0; k < 4; k++) {
-                const uint32_t c2 = min_u16x2(max_u16x2(qv[k], smn[k]), smx[k]);
-                es += ld_sh_u8(__byte_perm(c2, ubq, 0x7650u) + (2 * k) * CARD);
-                es += ld_sh_u8(__byte_perm(c2, ubq, 0x7652u) + (2 * k + 1) * CARD);
+        __syncthreads();
+        // A1: for each (hyper-node, query) that survived, lane = one of its 32 super-nodes
+        for (uint32_t pr = warp; pr < nh * 16u; pr += NW) {
+            const uint32_t h = pr >> 4, g = pr & 15u;
+            if (!((hmask[h] >> g) & 1u)) continue;
+            const uint32_t sn = (h0 + h) * HYPER + lane;
+            if (sn >= s0 && sn < send) {
+                bytes += 32;
+                const uint4 a = __ldg(smeta4 + 2 * (uint64_t)sn), b = __ldg(smeta4 + 2 * (uint64_t)sn + 1);
+                if (node_e8(lut8_sh + g * W * CARD, qsym[g][0], qsym[g][1], a, b) <= 254u)
+                    atomicOr(&smask_sh[sn - s0], 1u << g);
             }
-            es += __shfl_xor_sync(FULL, es, 16);
-            return __ballot_sync(FULL, gq < G && es <= 254u) & 0xFFFFu;
-        };
-        // software pipeline: the super test and leaf-summary loads of iteration j + 1 are issued
-        // before the leaf tests of iteration j
-        uint32_t smask = 0;
+        }
+        __syncthreads();
+        // A2: warp iteration = one super-node (s0 + warp + NW j), lane = one of its 32 leaves, for
+        // the queries that kept the super-node. Leaf summaries are read only under surviving
+        // super-nodes, one iteration ahead.
+        uint32_t nmask = 0;
         uint4 mn_n = make_uint4(0, 0, 0, 0), mx_n = mn_n;
-        if (sfirst < send) {
-            smask = super_mask(0);
-            const uint32_t leaf = sfirst * SUPER + lane;
-            if (smask && leaf < c1) {
+        if (s0 + warp < send) {
+            nmask = smask_sh[warp];
+            const uint32_t leaf = (s0 + warp) * SUPER + lane;
+            if (nmask && leaf < c1) {
                 mn_n = __ldg(meta4 + 2 * (uint64_t)leaf);
                 mx_n = __ldg(meta4 + 2 * (uint64_t)leaf + 1);
             }
         }
-        uint32_t j = 0;
-        for (uint32_t sn = sfirst; sn < send; sn += NW, j++) {
+        for (uint32_t sn = s0 + warp; sn < send; sn += NW) {
             const uint32_t leaf = sn * SUPER + lane;
-            const uint32_t cur_mask = smask;
+            const uint32_t cur_mask = nmask;
             const uint4 mn4 = mn_n, mx4 = mx_n;
             if (sn + NW < send) {
-                smask = super_mask(j + 1);
+                nmask = smask_sh[sn + NW - s0];
                 const uint32_t l2 = leaf + NW * SUPER;
-                if (smask && l2 < c1) {
+                if (nmask && l2 < c1) {
                     mn_n = __ldg(meta4 + 2 * (uint64_t)l2);
                     mx_n = __ldg(meta4 + 2 * (uint64_t)l2 + 1);
                 }
             }
             if (!cur_mask) continue;  // the whole super-node is pruned for every query
-            if (lane == 0) bytes += 32ull * SUPER;
-            // the leaf's per-segment [min, max] as u16x2 pairs (segments 2j, 2j+1)
-            const uint32_t mn[8] = {lo_u16x2(mn4.x), hi_u16x2(mn4.x), lo_u16x2(mn4.y), hi_u16x2(mn4.y),
-                                    lo_u16x2(mn4.z), hi_u16x2(mn4.z), lo_u16x2(mn4.w), hi_u16x2(mn4.w)};
-            const uint32_t mx[8] = {lo_u16x2(mx4.x), hi_u16x2(mx4.x), lo_u16x2(mx4.y), hi_u16x2(mx4.y),
-                                    lo_u16x2(mx4.z), hi_u16x2(mx4.z), lo_u16x2(mx4.w), hi_u16x2(mx4.w)};
+            if (leaf < c1) bytes += 32;
             uint32_t alive = 0;
 #pragma unroll
             for (int g = 0; g < G; g++) {
                 if (!((cur_mask >> g) & 1u)) continue;
-                const uint4 qa = qsym[g][0], qb = qsym[g][1];
-                const uint32_t qv[8] = {qa.x, qa.y, qa.z, qa.w, qb.x, qb.y, qb.z, qb.w};
-                uint32_t cl[8];
-#pragma unroll
-                for (int k = 0; k < 8; k++) cl[k] = min_u16x2(max_u16x2(qv[k], mn[k]), mx[k]);
-                const uint32_t ub = lut8_sh + g * W * CARD;
-                uint32_t es = 0;
-#pragma unroll
-                for (int s2 = 0; s2 < W; s2++)
-                    es += ld_sh_u8(__byte_perm(cl[s2 >> 1], ub, 0x7650u | (uint32_t)(2 * (s2 & 1))) + s2 * CARD);
-                if (es <= 254u) alive |= 1u << g;
+                if (node_e8(lut8_sh + g * W * CARD, qsym[g][0], qsym[g][1], mn4, mx4) <= 254u) alive |= 1u << g;
             }
             if (leaf >= c1) alive = 0;
             const uint32_t bal = __ballot_sync(FULL, alive != 0);
@@ -506,7 +511,7 @@ __global__ void __launch_bounds__(LF_THREADS, 1) leafscan_kernel(
             const uint32_t pA = (c0 + (entA & 0xFFFFu)) * LEAF + lane;
             const uint32_t pB = hasB ? (c0 + (entB & 0xFFFFu)) * LEAF + lane : N;
             const uint4 wA = slot[(2 * buf) * LEAF + lane], wB = slot[(2 * buf + 1) * LEAF + lane];
-            if (lane == 0) bytes += (hasB ? 2ull : 1ull) * 16ull * LEAF;
+            bytes += (pA < N ? 16u : 0u) + (pB < N ? 16u : 0u);
             if (lane < G) my_alive += ((mA >> lane) & 1u) + ((mB >> lane) & 1u);
             // rolled loop over the queries that kept either leaf: unrolling it over G made the
             // kernel ~120 KB of SASS, and instruction-cache misses became the top stall
@@ -528,16 +533,25 @@ __global__ void __launch_bounds__(LF_THREADS, 1) leafscan_kernel(
                 }
                 const bool m0 = pA < N && eA <= 254u, m1 = pB < N && eB <= 254u;
                 if (!__any_sync(FULL, m0 || m1)) continue;
-                // rare: the exact fp32 test, the same rule as the flat scan
+                // The flat scan's rule is lo < LB^2 <= T on the exact fp32 bound. A u8 sum <= E_SURE
+                // already implies LB^2 <= T (R11b), and in the first band (lo < 0) lo < LB^2 always
+                // holds, so only the members with a u8 sum in (E_SURE, 254] (or any in later bands)
+                // need the exact bound. A sure member's histogram bin comes from its u8 sum, never
+                // above its exact bin (band shrinking, R10, stays an upper bound on the count).
                 const QConst kq = qc[g];
                 const float *Lg = lut_all + (uint64_t)qid[g] * W * CARD;
+                const bool band0 = kq.lo < 0.f;
 #pragma unroll
                 for (int u = 0; u < 2; u++) {
                     const bool maybe = u ? m1 : m0;
+                    const uint32_t e8 = u ? eB : eA;
                     const uint32_t pos = u ? pB : pA;
-                    const float lb = maybe ? word_lb(Lg, u ? wB : wA) : 0.f;
-                    const bool keep = maybe && lb > kq.lo && lb <= kq.T && (pos < kq.ws || pos >= kq.we);
-                    if (keep) atomicAdd(&shist[g][hist_bin(lb, kq.lo, kq.T)], 1u);
+                    const bool sure = maybe && band0 && e8 <= E_SURE;
+                    const bool check = maybe && !sure;
+                    const float lb = check ? word_lb(Lg, u ? wB : wA) : 0.f;
+                    const bool keep = (sure || (check && lb > kq.lo && lb <= kq.T)) && (pos < kq.ws || pos >= kq.we);
+                    if (keep)
+                        atomicAdd(&shist[g][sure ? min(e8 * HIST_BINS / 254u, HIST_BINS - 1) : hist_bin(lb, kq.lo, kq.T)], 1u);
                     emit(keep, pos, g, qid[g], lane, lt, cbuf, cb_cnt, cand, cand_cnt, cap);
                 }
             }
@@ -547,7 +561,8 @@ __global__ void __launch_bounds__(LF_THREADS, 1) leafscan_kernel(
         if (t == 0) wl_cnt = 0;
     }
     if (g0 != 0xffffffffu) flush();
-    if (lane == 0 && bytes) atomicAdd(scan_bytes_dev, bytes);
+    bytes = __reduce_add_sync(FULL, bytes);
+    if (lane == 0 && bytes) atomicAdd(scan_bytes_dev, (unsigned long long)bytes);
 }
 
 template <int G>
@@ -574,7 +589,7 @@ static void launch_leaf(const isax_index *ix, uint32_t nq, const uint32_t *qmap,
     const QueryScratch &qs = ix->qs;
     cudaMemsetAsync(qs.task_ctr, 0, sizeof(uint32_t), s);
     leafscan_kernel<G><<<grid, LF_THREADS, smem, s>>>(
-        reinterpret_cast<const uint4 *>(ix->sax), ix->lmeta, ix->smeta, (uint32_t)ix->N, qs.lut, qs.lut8, qs.qconst,
+        reinterpret_cast<const uint4 *>(ix->sax), ix->lmeta, ix->smeta, ix->hmeta, (uint32_t)ix->N, qs.lut, qs.lut8, qs.qconst,
         qs.qsax, qmap, nq, nleaf, chunk, qs.cand, qs.cand_cnt, qs.cand_cap, qs.cand_hist, qs.counters_leaf,
         qs.scan_bytes_dev, qs.task_ctr);
 }
@@ -599,8 +614,7 @@ uint64_t launch_lbscan(const isax_index *ix, uint32_t nq, const uint32_t *qmap, 
     else if (G == 4) launch_leaf<4>(ix, nq, qmap, s);
     else if (G == 2) launch_leaf<2>(ix, nq, qmap, s);
     else launch_leaf<1>(ix, nq, qmap, s);
-    const uint64_t nsuper = (ix->N + SUPER_SIZE - 1) / SUPER_SIZE;
-    return 32ull * nsuper * ((nq + G - 1) / G);  // super-node summaries; leaf summaries and words are counted on the device
+    return 0;  // the leaf scan counts the node summaries and words it reads on the device
 }
 
 // ------------------------------------------------------------------------------------ leaf meta
@@ -625,14 +639,16 @@ __global__ void leaf_meta_kernel(const uint4 *__restrict__ sax, uint64_t N, uint
     }
 }
 
-// Build: per super-node of SUPER leaves, the per-segment min / max over its leaves' summaries.
-__global__ void super_meta_kernel(const uint4 *__restrict__ lmeta, uint64_t nleaf, uint4 *__restrict__ smeta) {
-    const uint64_t ns = (nleaf + SUPER - 1) / SUPER;
-    for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < ns; j += (uint64_t)gridDim.x * blockDim.x) {
+// Build: per parent node of `factor` children, the per-segment min / max over its children's
+// summaries (super-nodes over leaves, hyper-nodes over super-nodes).
+__global__ void parent_meta_kernel(const uint4 *__restrict__ child, uint64_t nchild, uint32_t factor,
+                                   uint4 *__restrict__ parent) {
+    const uint64_t np = (nchild + factor - 1) / factor;
+    for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < np; j += (uint64_t)gridDim.x * blockDim.x) {
         uint32_t mn[4] = {~0u, ~0u, ~0u, ~0u}, mx[4] = {0, 0, 0, 0};
-        const uint64_t l1 = umin64(nleaf, (j + 1) * SUPER);
-        for (uint64_t l = j * SUPER; l < l1; l++) {
-            const uint4 a = __ldg(lmeta + 2 * l), b = __ldg(lmeta + 2 * l + 1);
+        const uint64_t l1 = umin64(nchild, (j + 1) * factor);
+        for (uint64_t l = j * factor; l < l1; l++) {
+            const uint4 a = __ldg(child + 2 * l), b = __ldg(child + 2 * l + 1);
             const uint32_t va[4] = {a.x, a.y, a.z, a.w}, vb[4] = {b.x, b.y, b.z, b.w};
 #pragma unroll
             for (int k = 0; k < 4; k++) {
@@ -640,18 +656,21 @@ __global__ void super_meta_kernel(const uint4 *__restrict__ lmeta, uint64_t nlea
                 mx[k] = __vmaxu4(mx[k], vb[k]);
             }
         }
-        smeta[2 * j] = make_uint4(mn[0], mn[1], mn[2], mn[3]);
-        smeta[2 * j + 1] = make_uint4(mx[0], mx[1], mx[2], mx[3]);
+        parent[2 * j] = make_uint4(mn[0], mn[1], mn[2], mn[3]);
+        parent[2 * j + 1] = make_uint4(mx[0], mx[1], mx[2], mx[3]);
     }
 }
 
-void launch_leaf_meta(const uint8_t *sax, uint64_t N, uint8_t *lmeta, uint8_t *smeta, cudaStream_t s) {
+void launch_leaf_meta(const uint8_t *sax, uint64_t N, uint8_t *lmeta, uint8_t *smeta, uint8_t *hmeta, cudaStream_t s) {
     const uint64_t nleaf = (N + LEAF - 1) / LEAF;
     const unsigned grid = (unsigned)std::max<uint64_t>(1, umin64((nleaf + 255) / 256, 148 * 16));
     leaf_meta_kernel<<<grid, 256, 0, s>>>(reinterpret_cast<const uint4 *>(sax), N, lmeta);
     const uint64_t ns = (nleaf + SUPER - 1) / SUPER;
-    super_meta_kernel<<<(unsigned)std::max<uint64_t>(1, umin64((ns + 255) / 256, 148 * 16)), 256, 0, s>>>(
-        reinterpret_cast<const uint4 *>(lmeta), nleaf, reinterpret_cast<uint4 *>(smeta));
+    parent_meta_kernel<<<(unsigned)std::max<uint64_t>(1, umin64((ns + 255) / 256, 148 * 16)), 256, 0, s>>>(
+        reinterpret_cast<const uint4 *>(lmeta), nleaf, SUPER, reinterpret_cast<uint4 *>(smeta));
+    const uint64_t nh = (ns + HYPER - 1) / HYPER;
+    parent_meta_kernel<<<(unsigned)std::max<uint64_t>(1, umin64((nh + 255) / 256, 148 * 16)), 256, 0, s>>>(
+        reinterpret_cast<const uint4 *>(smeta), ns, HYPER, reinterpret_cast<uint4 *>(hmeta));
 }
 
 }  // namespace isax
