@@ -222,7 +222,7 @@ def main():
     # on the stream its kernels run on.
     keys = ["lbscan", "refine", "window", "qprep"]
     kms = {k: [] for k in keys}
-    cand, refined, rounds, scan_b, ref_b, pairs, launches = [], [], [], [], [], [], 0
+    cand, refined, skipped, rounds, scan_b, ref_b, pairs, launches = [], [], [], [], [], [], [], 0
     for _ in range(args.steps):
         ids, dist_ = ix.nn1(q)
         st = ix.stats()
@@ -230,6 +230,7 @@ def main():
             kms[k].append(st["ms_first_batch"][k])
         cand.append(sum(st["candidates"]))
         refined.append(sum(st["refined"]))
+        skipped.append(sum(st.get("skipped", [0])))
         rounds.append(max(st["rounds"]))
         launches += st.get("launches", 0)
         scan_b.append(st["scan_bytes_first_launch"])
@@ -309,6 +310,7 @@ def main():
         "build": {"seconds": round(build_s, 3), "mode": build_mode, "N": wl.N, "n": wl.n,
                   "input_GBps": round(raw_bytes / build_s / 1e9, 1), "index_device_bytes": ix.device_bytes},
         "stats": {"candidates_per_query": statistics.mean(cand) / Q, "refined_per_query": statistics.mean(refined) / Q,
+                  "skipped_per_query": statistics.mean(skipped) / Q,
                   "rounds_max": max(rounds)},
     }
     if rank == 0 and not args.no_cpu_baseline:

@@ -78,7 +78,7 @@ static cudaError_t dmalloc(T **p, size_t count, size_t *acc) {
 static void free_scratch(isax_index *ix) {
     QueryScratch &q = ix->qs;
     cudaFree(q.qy); cudaFree(q.qpaa); cudaFree(q.qsax); cudaFree(q.lut); cudaFree(q.lut8); cudaFree(q.qconst); cudaFree(q.win); cudaFree(q.pwin); cudaFree(q.bsf);
-    cudaFree(q.cand); cudaFree(q.cand_cnt); cudaFree(q.near); cudaFree(q.near_cnt); cudaFree(q.qmap); cudaFree(q.qband); cudaFree(q.cand_hist);
+    cudaFree(q.cand); cudaFree(q.candq); cudaFree(q.qscale); cudaFree(q.cand_cnt); cudaFree(q.near); cudaFree(q.near_cnt); cudaFree(q.qmap); cudaFree(q.qband); cudaFree(q.cand_hist);
     cudaFree(q.counters); cudaFree(q.counters_leaf); cudaFree(q.scan_bytes_dev); cudaFree(q.task_ctr); cudaFree(q.refine_bytes);
     cudaFree(q.flag); cudaFree(q.qmap2);
     if (q.h_mirror) cudaFreeHost(q.h_mirror);
@@ -104,6 +104,8 @@ static int alloc_scratch(isax_index *ix) {
     A(pwin, (size_t)Q * (MAX_PROBES - 1));
     A(bsf, Q);
     A(cand, (size_t)Q * cap);
+    A(candq, (size_t)Q * cap);
+    A(qscale, Q);
     A(cand_cnt, Q);
     A(near, (size_t)Q * NEAR_K);
     A(near_cnt, Q);
@@ -264,6 +266,7 @@ static int nn1_device(isax_index *ix, const float *d_q, uint32_t Q, int64_t *d_i
     ix->st_cand.assign(Q, 0);
     ix->st_refined.assign(Q, 0);
     ix->st_abandoned.assign(Q, 0);
+    ix->st_skipped.assign(Q, 0);
     ix->st_rounds.assign(Q, 0);
     ix->st_near.assign(Q, 0);
     ix->st_leaves.assign(Q, 0);
@@ -405,6 +408,7 @@ static int nn1_device(isax_index *ix, const float *d_q, uint32_t Q, int64_t *d_i
         for (uint32_t i = 0; i < B; i++) {
             ix->st_refined[b0 + i] = hm.counters[4 * i];
             ix->st_abandoned[b0 + i] = hm.counters[4 * i + 1];
+            ix->st_skipped[b0 + i] = hm.counters[4 * i + 2];
             ix->st_near[b0 + i] = hm.near_cnt[i];
             ix->st_leaves[b0 + i] = hm.leaves[i];
             ix->st_bsf0[b0 + i] = bsf_d2_host(hm.bsf0[i]);
@@ -605,6 +609,7 @@ int isax_stats(const isax_index *cix, char *buf, size_t cap) {
     arr("candidates", ix->st_cand, false);
     arr("refined", ix->st_refined, false);
     arr("abandoned", ix->st_abandoned, false);
+    arr("skipped", ix->st_skipped, false);
     arr("rounds", ix->st_rounds, false);
     arr("near", ix->st_near, false);
     arr("leaves_alive", ix->st_leaves, false);

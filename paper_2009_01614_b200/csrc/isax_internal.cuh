@@ -85,13 +85,15 @@ struct QueryScratch {
     uint32_t *pwin = nullptr;       // [Q][MAX_PROBES-1] probe window starts (probe_L rows each)
     unsigned long long *bsf = nullptr;  // [Q] packed
     uint32_t *cand = nullptr;       // [Q][cand_cap] sorted positions
+    uint8_t *candq = nullptr;       // [Q][cand_cap] u8 bound b of each candidate: b / qscale <= LB^2
+    float *qscale = nullptr;        // [Q] 254 / T of the query's last scan, rounded down (R11b)
     uint32_t *cand_cnt = nullptr;   // [Q] (may exceed cand_cap: overflow)
     NearEntry *near = nullptr;      // [Q][NEAR_K]
     uint32_t *near_cnt = nullptr;   // [Q]
     uint32_t *qmap = nullptr;       // [Q] active slot -> batch slot, for re-scan rounds
     float2 *qband = nullptr;        // [Q] LB band (lo, hi] of each active slot (R10)
     uint32_t *cand_hist = nullptr;  // [Q][HIST_BINS] histogram of kept LB^2 in the band
-    uint32_t *counters = nullptr;   // [Q][4]: refined, abandoned, rounds, near_overflow
+    uint32_t *counters = nullptr;   // [Q][4]: refined, abandoned, skipped by the u8 bound, (unused)
     uint32_t *counters_leaf = nullptr;  // [Q]: (leaf, query) pairs that survived the node bound
     unsigned long long *scan_bytes_dev = nullptr;  // leaf words and leaf summaries the leaf scan read, bytes (all launches of a call)
     uint32_t *task_ctr = nullptr;              // work counter of the persistent leaf scan
@@ -123,7 +125,7 @@ struct isax_index {
     isax::QueryScratch qs;
     std::mutex mu;
     // last-call statistics (host copies)
-    std::vector<uint32_t> st_win, st_cand, st_refined, st_abandoned, st_rounds, st_near, st_leaves;
+    std::vector<uint32_t> st_win, st_cand, st_refined, st_abandoned, st_skipped, st_rounds, st_near, st_leaves;
     std::vector<float> st_bsf0, st_bsf_final;
     isax::StageTimes st_ms;
     uint64_t st_launches = 0;  // kernels launched by the last nn1 call

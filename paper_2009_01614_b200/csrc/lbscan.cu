@@ -132,6 +132,7 @@ __global__ void __launch_bounds__(LB_THREADS) lbscan_kernel(const uint4 *__restr
                                                             const unsigned long long *__restrict__ bsf,
                                                             const uint32_t *__restrict__ win, float onepd,
                                                             uint32_t *__restrict__ cand,
+                                                            uint8_t *__restrict__ candq,
                                                             uint32_t *__restrict__ cand_cnt, uint32_t cap,
                                                             uint32_t *__restrict__ hist) {
     extern __shared__ __align__(16) float slut[];  // [G][16][256]
@@ -176,7 +177,10 @@ __global__ void __launch_bounds__(LB_THREADS) lbscan_kernel(const uint4 *__restr
                     off = __shfl_sync(0xffffffffu, off, 0);
                     if (keep) {
                         const uint32_t kk = off + __popc(bal & lt);
-                        if (kk < cap) cand[(uint64_t)qid[g] * cap + kk] = pos;
+                        if (kk < cap) {
+                            cand[(uint64_t)qid[g] * cap + kk] = pos;
+                            candq[(uint64_t)qid[g] * cap + kk] = 0;  // no bound recorded: never skipped
+                        }
                         atomicAdd(&hist[qid[g] * HIST_BINS + hist_bin(lb, k.lo, k.T)], 1u);
                     }
                 }
@@ -205,7 +209,7 @@ static void launch_g(const isax_index *ix, uint32_t nq, const uint32_t *qmap, co
     const QueryScratch &qs = ix->qs;
     lbscan_kernel<G><<<dim3((unsigned)gx, groups), LB_THREADS, smem, s>>>(
         reinterpret_cast<const uint4 *>(ix->sax), (uint32_t)ix->N, qs.lut, qmap, band, nq, qs.bsf, qs.win, onepd,
-        qs.cand, qs.cand_cnt, qs.cand_cap, qs.cand_hist);
+        qs.cand, qs.candq, qs.cand_cnt, qs.cand_cap, qs.cand_hist);
 }
 
 // ------------------------------------------------------------------------------------ leaf scan
@@ -253,9 +257,10 @@ constexpr uint32_t CBUF = 512;    // shared candidate buffer per query slot
 constexpr uint32_t E_SURE = 237;
 
 // append `keep` lanes' positions for query slot g: shared buffer first, global list if it is full
-__device__ __forceinline__ void emit(bool keep, uint32_t pos, uint32_t g, uint32_t q, uint32_t lane, uint32_t lt,
-                                     uint32_t *cbuf, uint32_t *cb_cnt, uint32_t *cand, uint32_t *cand_cnt,
-                                     uint32_t cap) {
+// with its u8 bound b (b / sc <= LB^2, for the refine's skip test)
+__device__ __forceinline__ void emit(bool keep, uint32_t pos, uint32_t b, uint32_t g, uint32_t q, uint32_t lane,
+                                     uint32_t lt, uint32_t *cbuf, uint8_t *qbuf, uint32_t *cb_cnt, uint32_t *cand,
+                                     uint8_t *candq, uint32_t *cand_cnt, uint32_t cap) {
     const uint32_t bal = __ballot_sync(0xffffffffu, keep);
     if (!bal) return;
     const uint32_t c = __popc(bal);
@@ -264,19 +269,28 @@ __device__ __forceinline__ void emit(bool keep, uint32_t pos, uint32_t g, uint32
     off = __shfl_sync(0xffffffffu, off, 0);
     const uint32_t r = __popc(bal & lt);
     if (off + c <= CBUF) {
-        if (keep) cbuf[g * CBUF + off + r] = pos;
+        if (keep) {
+            cbuf[g * CBUF + off + r] = pos;
+            qbuf[g * CBUF + off + r] = (uint8_t)b;
+        }
         return;
     }
     // the buffer fills up: the slots below CBUF are still written (the flush copies exactly
     // min(count, CBUF) entries), the rest go straight to the global list
     const uint32_t room = off < CBUF ? CBUF - off : 0;
-    if (keep && r < room) cbuf[g * CBUF + off + r] = pos;
+    if (keep && r < room) {
+        cbuf[g * CBUF + off + r] = pos;
+        qbuf[g * CBUF + off + r] = (uint8_t)b;
+    }
     uint32_t goff = 0;
     if (lane == 0) goff = atomicAdd(&cand_cnt[q], c - room);
     goff = __shfl_sync(0xffffffffu, goff, 0);
     if (keep && r >= room) {
         const uint32_t k = goff + r - room;
-        if (k < cap) cand[(uint64_t)q * cap + k] = pos;
+        if (k < cap) {
+            cand[(uint64_t)q * cap + k] = pos;
+            candq[(uint64_t)q * cap + k] = (uint8_t)b;
+        }
     }
 }
 
@@ -294,13 +308,15 @@ __global__ void __launch_bounds__(256) scanprep_kernel(const float *__restrict__
                                                        const float2 *__restrict__ band,
                                                        const unsigned long long *__restrict__ bsf,
                                                        const uint32_t *__restrict__ win, float onepd,
-                                                       uint8_t *__restrict__ lut8, uint4 *__restrict__ qconst) {
+                                                       uint8_t *__restrict__ lut8, uint4 *__restrict__ qconst,
+                                                       float *__restrict__ qscale) {
     const uint32_t i = blockIdx.x;
     const uint32_t qi = qmap[i];
     const QConst k = load_qconst(qi, true, bsf, band, i, win, onepd);
     if (threadIdx.x == 0) qconst[i] = make_uint4(__float_as_uint(k.lo), __float_as_uint(k.T), k.ws, k.we);
     const bool none = !(k.T >= 0.f);  // an empty band keeps nothing
     const float sc = none ? 0.f : __fdiv_rd(254.0f, k.T);  // T = 0 -> +inf
+    if (threadIdx.x == 0) qscale[qi] = sc;
     const float4 *L = reinterpret_cast<const float4 *>(lut_all + (uint64_t)qi * W * CARD);
     uint32_t *o = reinterpret_cast<uint32_t *>(lut8 + (uint64_t)i * W * CARD);
     for (uint32_t e = threadIdx.x; e < W * CARD / 4; e += blockDim.x) {
@@ -314,7 +330,7 @@ __global__ void __launch_bounds__(LF_THREADS, 1) leafscan_kernel(
     const uint4 *__restrict__ sax, const uint8_t *__restrict__ lmeta, const uint8_t *__restrict__ smeta,
     const uint8_t *__restrict__ hmeta, uint32_t N, const float *__restrict__ lut_all, const uint8_t *__restrict__ lut8_all, const uint4 *__restrict__ qconst_all,
     const uint8_t *__restrict__ qsax_all, const uint32_t *__restrict__ qmap, uint32_t nq, uint32_t nleaf,
-    uint32_t chunk, uint32_t *__restrict__ cand, uint32_t *__restrict__ cand_cnt, uint32_t cap,
+    uint32_t chunk, uint32_t *__restrict__ cand, uint8_t *__restrict__ candq, uint32_t *__restrict__ cand_cnt, uint32_t cap,
     uint32_t *__restrict__ hist, uint32_t *__restrict__ leaves_alive, unsigned long long *__restrict__ scan_bytes_dev,
     uint32_t *__restrict__ task_ctr) {
     // shared: [G][16][256] u8 tables | [G][CBUF] candidates | [CHUNK] worklist | [NW][2][2 LEAF] words
@@ -327,9 +343,11 @@ __global__ void __launch_bounds__(LF_THREADS, 1) leafscan_kernel(
     uint32_t *cbuf = reinterpret_cast<uint32_t *>(lut8 + G * W * CARD);
     uint32_t *worklist = cbuf + G * CBUF;  // (leaf offset in chunk) | (query mask << 16)
     uint4 *stage = reinterpret_cast<uint4 *>(worklist + CHUNK);
+    uint8_t *qbuf = reinterpret_cast<uint8_t *>(stage + (LF_THREADS / 32) * 4 * LEAF);  // [G][CBUF] u8 bounds
     __shared__ QConst qc[G];
     __shared__ uint4 qsym[G][2];  // the query's 16 symbols as 8 u16x2 pairs
     __shared__ uint32_t qid[G], cb_cnt[G], alive_cnt[G], fbase[G];
+    __shared__ float qsc[G];  // 254 / T rounded down (the u8 table scale)
     __shared__ uint32_t shist[G][HIST_BINS];
     __shared__ uint32_t wl_cnt, s_task;
     __shared__ uint32_t hmask[CHUNK / (SUPER * HYPER) + 1];  // query mask of each hyper-node of the chunk
@@ -367,7 +385,10 @@ __global__ void __launch_bounds__(LF_THREADS, 1) leafscan_kernel(
             const uint32_t c = min(cb_cnt[g], CBUF);
             for (uint32_t i = t; i < c; i += LF_THREADS) {
                 const uint32_t k = fbase[g] + i;
-                if (k < cap) cand[(uint64_t)qid[g] * cap + k] = cbuf[g * CBUF + i];
+                if (k < cap) {
+                    cand[(uint64_t)qid[g] * cap + k] = cbuf[g * CBUF + i];
+                    candq[(uint64_t)qid[g] * cap + k] = qbuf[g * CBUF + i];
+                }
             }
         }
         __syncthreads();
@@ -395,6 +416,7 @@ __global__ void __launch_bounds__(LF_THREADS, 1) leafscan_kernel(
                 qsym[t][1] = make_uint4(lo_u16x2(w.z), hi_u16x2(w.z), lo_u16x2(w.w), hi_u16x2(w.w));
                 const uint4 k = qconst_all[slot];
                 qc[t] = valid ? QConst{__uint_as_float(k.x), __uint_as_float(k.y), k.z, k.w} : QConst{0.f, -1.f, 0u, 0u};
+                qsc[t] = valid && __uint_as_float(k.y) >= 0.f ? __fdiv_rd(254.0f, __uint_as_float(k.y)) : 0.f;  // as scanprep
             }
             // the group's u8 tables; a padding slot gets all-255 entries (it prunes everything)
             {
@@ -550,9 +572,15 @@ __global__ void __launch_bounds__(LF_THREADS, 1) leafscan_kernel(
                     const bool check = maybe && !sure;
                     const float lb = check ? word_lb(Lg, u ? wB : wA) : 0.f;
                     const bool keep = (sure || (check && lb > kq.lo && lb <= kq.T)) && (pos < kq.ws || pos >= kq.we);
+                    // the candidate's u8 bound for the refine's skip test: b <= LB^2 * sc
+                    uint32_t b = e8;
+                    if (check) {
+                        const float y = __fmul_rd(lb, qsc[g]);
+                        b = lb > 0.f ? (y >= 254.f ? 254u : (uint32_t)y) : 0u;
+                    }
                     if (keep)
                         atomicAdd(&shist[g][sure ? min(e8 * HIST_BINS / 254u, HIST_BINS - 1) : hist_bin(lb, kq.lo, kq.T)], 1u);
-                    emit(keep, pos, g, qid[g], lane, lt, cbuf, cb_cnt, cand, cand_cnt, cap);
+                    emit(keep, pos, b, g, qid[g], lane, lt, cbuf, qbuf, cb_cnt, cand, candq, cand_cnt, cap);
                 }
             }
             __syncwarp();  // the slots are rewritten by the prefetch two steps ahead
@@ -569,7 +597,7 @@ template <int G>
 static void launch_leaf(const isax_index *ix, uint32_t nq, const uint32_t *qmap, cudaStream_t s) {
     constexpr uint32_t NW = LF_THREADS / 32;
     const size_t smem = (size_t)G * W * CARD + 256 + (size_t)G * CBUF * sizeof(uint32_t) + CHUNK * 4 +
-                        (size_t)NW * 4 * LEAF * sizeof(uint4);
+                        (size_t)NW * 4 * LEAF * sizeof(uint4) + (size_t)G * CBUF;
     static bool configured = false;
     if (!configured) {
         cudaFuncSetAttribute(leafscan_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -590,7 +618,7 @@ static void launch_leaf(const isax_index *ix, uint32_t nq, const uint32_t *qmap,
     cudaMemsetAsync(qs.task_ctr, 0, sizeof(uint32_t), s);
     leafscan_kernel<G><<<grid, LF_THREADS, smem, s>>>(
         reinterpret_cast<const uint4 *>(ix->sax), ix->lmeta, ix->smeta, ix->hmeta, (uint32_t)ix->N, qs.lut, qs.lut8, qs.qconst,
-        qs.qsax, qmap, nq, nleaf, chunk, qs.cand, qs.cand_cnt, qs.cand_cap, qs.cand_hist, qs.counters_leaf,
+        qs.qsax, qmap, nq, nleaf, chunk, qs.cand, qs.candq, qs.cand_cnt, qs.cand_cap, qs.cand_hist, qs.counters_leaf,
         qs.scan_bytes_dev, qs.task_ctr);
 }
 
@@ -598,6 +626,8 @@ uint64_t launch_lbscan(const isax_index *ix, uint32_t nq, const uint32_t *qmap, 
                        cudaStream_t s) {
     if (!nq) return 0;
     const float onepd = 1.0f + delta;
+    const QueryScratch &qs = ix->qs;
+    scanprep_kernel<<<nq, 256, 0, s>>>(qs.lut, qmap, band, qs.bsf, qs.win, onepd, qs.lut8, qs.qconst, qs.qscale);
     if (ix->opts.flags & ISAX_FLAG_FLAT_SCAN) {  // ParIS flat scan, kept for A/B measurement
         const uint32_t G = nq >= 4 ? 4 : nq;
         if (G == 4) launch_g<4>(ix, nq, qmap, band, onepd, s);
@@ -606,8 +636,6 @@ uint64_t launch_lbscan(const isax_index *ix, uint32_t nq, const uint32_t *qmap, 
         else launch_g<1>(ix, nq, qmap, band, onepd, s);
         return 16ull * ix->N * ((nq + G - 1) / G);  // words read
     }
-    const QueryScratch &qs = ix->qs;
-    scanprep_kernel<<<nq, 256, 0, s>>>(qs.lut, qmap, band, qs.bsf, qs.win, onepd, qs.lut8, qs.qconst);
     const uint32_t G = nq >= 16 ? 16 : nq >= 8 ? 8 : nq >= 4 ? 4 : nq >= 2 ? 2 : 1;
     if (G == 16) launch_leaf<16>(ix, nq, qmap, s);
     else if (G == 8) launch_leaf<8>(ix, nq, qmap, s);

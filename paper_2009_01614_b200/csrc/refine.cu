@@ -111,11 +111,6 @@ __global__ void __launch_bounds__(RF_THREADS) refine_kernel(const float *__restr
     }
 }
 
-// Quarter-warp variant for n <= 256 (the paper's lengths, 128 and 256). Eight lanes own one
-// candidate, so a warp has four rows in flight and each lane streams NH float4 per half-row
-// (512 B per quarter per half at n = 256). The abandon check after the first half reduces over
-// the 8 lanes only (3 xor shuffles). Same arithmetic contract as refine_kernel: fp32 partial
-// sums, abandon iff partial > bsf (1 + delta), packed atomicMin, near list.
 // exclusive prefix of min(cand_cnt[q], cap) over q < Q into pre[0..Q], by the whole CTA
 __device__ __forceinline__ void cand_prefix(const uint32_t *__restrict__ cand_cnt, uint32_t Q, uint32_t cap,
                                             uint32_t *pre) {
@@ -160,6 +155,8 @@ __global__ void __launch_bounds__(RF_THREADS) refine_q_kernel(const float *__res
                                                              const uint32_t *__restrict__ perm, uint32_t n,
                                                              const float *__restrict__ qy, uint32_t Q,
                                                              const uint32_t *__restrict__ cand,
+                                                             const uint8_t *__restrict__ candq,
+                                                             const float *__restrict__ qscale,
                                                              const uint32_t *__restrict__ cand_cnt, uint32_t cap,
                                                              unsigned long long *__restrict__ bsf,
                                                              NearEntry *__restrict__ near,
@@ -299,7 +296,8 @@ void launch_refine(const isax_index *ix, uint32_t Q, float delta, cudaStream_t s
         switch (nh) {
 #define RQ_CASE(K)                                                                                                  \
     case K:                                                                                                         \
-        refine_q_kernel<K><<<grid, RF_THREADS, 0, s>>>(ix->stored, ix->perm, ix->n, qs.qy, Q, qs.cand, qs.cand_cnt, \
+        refine_q_kernel<K><<<grid, RF_THREADS, 0, s>>>(ix->stored, ix->perm, ix->n, qs.qy, Q, qs.cand, qs.candq,     \
+                                                       qs.qscale, qs.cand_cnt,                                      \
                                                        qs.cand_cap, qs.bsf, qs.near, qs.near_cnt, qs.counters,      \
                                                        onepd, qs.refine_bytes);                                     \
         break;
