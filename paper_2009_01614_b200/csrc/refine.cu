@@ -219,7 +219,11 @@ __global__ void __launch_bounds__(RF_THREADS) refine_q_kernel(const float *__res
                 since = RF_REFRESH;
             }
             if (since++ >= RF_REFRESH) {
-                lim_c = bsf_d2(*((volatile unsigned long long *)&bsf[q])) * onepd;
+                // read by the quarter's first lane and broadcast: the quarter's lanes must take the
+                // same abandon decision (their shuffles below assume it)
+                float l = 0.f;
+                if (ql == 0) l = bsf_d2(*((volatile unsigned long long *)&bsf[q])) * onepd;
+                lim_c = __shfl_sync(qmask, l, lane & 24);
                 since = 1;
             }
             const float lim = lim_c;
@@ -261,7 +265,9 @@ __global__ void __launch_bounds__(RF_THREADS) refine_q_kernel(const float *__res
             done++;
             if (acc <= lim) {
                 // re-read the current BSF before claiming a near slot (the cached one may be stale)
-                const float cur = bsf_d2(*((volatile unsigned long long *)&bsf[q])) * onepd;
+                float cur = 0.f;
+                if (ql == 0) cur = bsf_d2(*((volatile unsigned long long *)&bsf[q])) * onepd;
+                cur = __shfl_sync(qmask, cur, lane & 24);
                 lim_c = cur;
                 if (ql == 0 && acc <= cur) {
                     const uint32_t id = perm[pos];
