@@ -220,7 +220,7 @@ def main():
     # ---- per-kernel times and counters: a separate pass of the same steps (stats() is host
     # work, kept out of the timed region). The library times its first batch with CUDA events
     # on the stream its kernels run on.
-    keys = ["lbscan", "refine", "window", "qprep"]
+    keys = ["lbscan", "candcheck", "refine", "window", "qprep"]
     kms = {k: [] for k in keys}
     cand, refined, skipped, rounds, scan_b, ref_b, pairs, launches = [], [], [], [], [], [], [], 0
     for _ in range(args.steps):

@@ -78,7 +78,7 @@ static cudaError_t dmalloc(T **p, size_t count, size_t *acc) {
 static void free_scratch(isax_index *ix) {
     QueryScratch &q = ix->qs;
     cudaFree(q.qy); cudaFree(q.qpaa); cudaFree(q.qsax); cudaFree(q.lut); cudaFree(q.lut8); cudaFree(q.qconst); cudaFree(q.win); cudaFree(q.pwin); cudaFree(q.bsf);
-    cudaFree(q.cand); cudaFree(q.candq); cudaFree(q.qscale); cudaFree(q.cand_cnt); cudaFree(q.near); cudaFree(q.near_cnt); cudaFree(q.qmap); cudaFree(q.qband); cudaFree(q.cand_hist);
+    cudaFree(q.cand); cudaFree(q.candq); cudaFree(q.cand2); cudaFree(q.candq2); cudaFree(q.cand_cnt2); cudaFree(q.qscale); cudaFree(q.qT); cudaFree(q.cand_cnt); cudaFree(q.near); cudaFree(q.near_cnt); cudaFree(q.qmap); cudaFree(q.qband); cudaFree(q.cand_hist);
     cudaFree(q.counters); cudaFree(q.counters_leaf); cudaFree(q.scan_bytes_dev); cudaFree(q.task_ctr); cudaFree(q.refine_bytes);
     cudaFree(q.flag); cudaFree(q.qmap2);
     if (q.h_mirror) cudaFreeHost(q.h_mirror);
@@ -105,7 +105,11 @@ static int alloc_scratch(isax_index *ix) {
     A(bsf, Q);
     A(cand, (size_t)Q * cap);
     A(candq, (size_t)Q * cap);
+    A(cand2, (size_t)Q * cap);
+    A(candq2, (size_t)Q * cap);
+    A(cand_cnt2, Q);
     A(qscale, Q);
+    A(qT, Q);
     A(cand_cnt, Q);
     A(near, (size_t)Q * NEAR_K);
     A(near_cnt, Q);
@@ -333,14 +337,18 @@ static int nn1_device(isax_index *ix, const float *d_q, uint32_t Q, int64_t *d_i
             ISAX_CUDA(cudaMemcpyAsync(qs.qmap, hm.qmap, nact * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
             ISAX_CUDA(cudaMemcpyAsync(qs.qband, hm.band, nact * sizeof(float2), cudaMemcpyHostToDevice, s));
             ix->st_scan_bytes += launch_lbscan(ix, nact, qs.qmap, qs.qband, delta, s);
+            if (timed && round == 0) cudaEventRecord(ix->ev[6], s);
+            launch_candcheck(ix, B, s);
             if (timed && round == 0) cudaEventRecord(ix->ev[3], s);
             launch_refine(ix, B, delta, s);
             if (timed && round == 0) cudaEventRecord(ix->ev[4], s);
             launch_finalize(ix, B, delta, d_id + b0, d_dist + b0, s);  // speculative: redone after another round
-            ix->st_launches += (ix->opts.flags & ISAX_FLAG_FLAT_SCAN) ? 3 : 4;  // the leaf scan adds scanprep_kernel
+            // scanprep + scan, candcheck, refine, finalize
+            ix->st_launches += ((ix->opts.flags & ISAX_FLAG_FLAT_SCAN) ? 1 : 2) + 3;
             if (timed && round == 0) cudaEventRecord(ix->ev[5], s);
             ISAX_CUDA(cudaGetLastError());
             ISAX_CUDA(cudaMemcpyAsync(hm.cand_cnt, qs.cand_cnt, B * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+            ISAX_CUDA(cudaMemcpyAsync(hm.cand_cnt2, qs.cand_cnt2, B * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
             ISAX_CUDA(cudaMemcpyAsync(hm.near_cnt, qs.near_cnt, B * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
             ISAX_CUDA(cudaMemcpyAsync(hm.flag, qs.flag, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
             ISAX_CUDA(cudaMemcpyAsync(hm.bsf, qs.bsf, B * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
@@ -375,7 +383,7 @@ static int nn1_device(isax_index *ix, const float *d_q, uint32_t Q, int64_t *d_i
                 const uint32_t i = hm.qmap[k];
                 const uint32_t cnt = hm.cand_cnt[i];
                 bsf_h[i] = bsf_d2_host(hm.bsf[i]);
-                ix->st_cand[b0 + i] += std::min(cnt, qs.cand_cap);
+                ix->st_cand[b0 + i] += hm.cand_cnt2[i];  // after the exact rule (candcheck_kernel)
                 ix->st_rounds[b0 + i] = round + 1;
                 if (hm.near_cnt[i] > (uint32_t)NEAR_K) {  // near overflow: start over, BSF kept
                     band[i] = make_float2(-1.0f, INF);
@@ -419,7 +427,8 @@ static int nn1_device(isax_index *ix, const float *d_q, uint32_t Q, int64_t *d_i
         if (timed) {
             cudaEventElapsedTime(&ix->st_ms.qprep, ix->ev[0], ix->ev[1]);
             cudaEventElapsedTime(&ix->st_ms.window, ix->ev[1], ix->ev[2]);
-            cudaEventElapsedTime(&ix->st_ms.lbscan, ix->ev[2], ix->ev[3]);
+            cudaEventElapsedTime(&ix->st_ms.lbscan, ix->ev[2], ix->ev[6]);
+            cudaEventElapsedTime(&ix->st_ms.candcheck, ix->ev[6], ix->ev[3]);
             cudaEventElapsedTime(&ix->st_ms.refine, ix->ev[3], ix->ev[4]);
             float tot = 0;
             cudaEventElapsedTime(&tot, ix->ev[0], ix->ev[5]);
@@ -590,9 +599,9 @@ int isax_stats(const isax_index *cix, char *buf, size_t cap) {
     char tmp[256];
     snprintf(tmp, sizeof tmp,
              "\"N\":%llu,\"n\":%u,\"window_L\":%u,\"slack_log2\":%d,\"batch_Q\":%u,\"cand_cap\":%u,"
-             "\"ms_first_batch\":{\"qprep\":%.4f,\"window\":%.4f,\"lbscan\":%.4f,\"refine\":%.4f,\"total\":%.4f},",
+             "\"ms_first_batch\":{\"qprep\":%.4f,\"window\":%.4f,\"lbscan\":%.4f,\"candcheck\":%.4f,\"refine\":%.4f,\"total\":%.4f},",
              (unsigned long long)ix->N, ix->n, ix->opts.window_L, ix->opts.slack_log2, ix->opts.batch_Q,
-             ix->opts.cand_cap, ix->st_ms.qprep, ix->st_ms.window, ix->st_ms.lbscan, ix->st_ms.refine,
+             ix->opts.cand_cap, ix->st_ms.qprep, ix->st_ms.window, ix->st_ms.lbscan, ix->st_ms.candcheck, ix->st_ms.refine,
              ix->st_ms.finalize);
     j += tmp;
     auto arr = [&](const char *name, const std::vector<uint32_t> &v, bool last) {

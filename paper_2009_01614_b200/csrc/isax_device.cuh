@@ -76,4 +76,35 @@ __device__ __forceinline__ float znorm_value(float x, double mu, double sd, doub
     return __double2float_rn(__ddiv_rn(t, sd));
 }
 
+// exclusive prefix of min(cand_cnt[q], cap) over q < Q into pre[0..Q], by the whole CTA
+template <int NT>
+__device__ __forceinline__ void cand_prefix(const uint32_t *__restrict__ cand_cnt, uint32_t Q, uint32_t cap,
+                                            uint32_t *pre) {
+    __shared__ uint32_t wsum[NT / 32];
+    const uint32_t t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    uint32_t carry = 0;
+    for (uint32_t b = 0; b < Q; b += NT) {
+        const uint32_t q = b + t;
+        const uint32_t v = q < Q ? min(cand_cnt[q], cap) : 0;
+        uint32_t inc = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t u = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= (uint32_t)o) inc += u;
+        }
+        if (lane == 31) wsum[warp] = inc;
+        __syncthreads();
+        uint32_t wpre = 0, tot = 0;
+        for (uint32_t w = 0; w < NT / 32; w++) {
+            if (w < warp) wpre += wsum[w];
+            tot += wsum[w];
+        }
+        if (q < Q) pre[q] = carry + wpre + inc - v;
+        carry += tot;
+        __syncthreads();
+    }
+    if (t == 0) pre[Q] = carry;
+    __syncthreads();
+}
+
 }  // namespace isax

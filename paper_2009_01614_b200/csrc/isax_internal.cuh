@@ -25,6 +25,7 @@ constexpr uint32_t HIST_BINS = 64;   // per-query histogram of kept LB^2 inside 
 constexpr uint32_t LEAF_SIZE = 32;    // sorted positions per leaf node (R11)
 constexpr uint32_t SUPER_SIZE = 1024; // sorted positions per super-node (R11)
 constexpr uint32_t HYPER_SIZE = 32768; // sorted positions per hyper-node (R11)
+constexpr uint32_t B_UNCHECKED = 255;  // candq marker: the exact fp32 rule is still to be applied
 
 // Packed BSF: high 32 bits = fp32 bits of d^2 (non-negative, so the bit order is the
 // numeric order), low 32 bits = original id. atomicMin on the packed word is the
@@ -48,10 +49,10 @@ struct NearEntry {  // a completed refinement within (1+delta) of the BSF at tha
 
 // Pinned host mirror of the per-batch counters (one async copy each per round, one sync).
 struct HostMirror {
-    uint32_t *cand_cnt, *near_cnt, *flag, *counters, *win, *leaves, *qmap, *rewin;
+    uint32_t *cand_cnt, *cand_cnt2, *near_cnt, *flag, *counters, *win, *leaves, *qmap, *rewin;
     unsigned long long *bsf, *bsf0, *scan_bytes_dev, *refine_bytes;
     float2 *band;
-    static size_t bytes(uint32_t Q) { return (size_t)Q * (8 * 4 + 4 * 4 + 2 * 4 + 8 * 2 + 8) + 256; }
+    static size_t bytes(uint32_t Q) { return (size_t)Q * (8 * 4 + 4 * 4 + 2 * 4 + 8 * 2 + 12) + 512; }
     void carve(void *base, uint32_t Q) {
         unsigned char *p = static_cast<unsigned char *>(base);
         auto take = [&](size_t n) { unsigned char *r = p; p += (n + 15) & ~size_t(15); return r; };
@@ -61,6 +62,7 @@ struct HostMirror {
         refine_bytes = reinterpret_cast<unsigned long long *>(take(8));
         band = reinterpret_cast<float2 *>(take(8ull * Q));
         cand_cnt = reinterpret_cast<uint32_t *>(take(4ull * Q));
+        cand_cnt2 = reinterpret_cast<uint32_t *>(take(4ull * Q));
         near_cnt = reinterpret_cast<uint32_t *>(take(4ull * Q));
         flag = reinterpret_cast<uint32_t *>(take(4));
         counters = reinterpret_cast<uint32_t *>(take(16ull * Q));
@@ -85,8 +87,13 @@ struct QueryScratch {
     uint32_t *pwin = nullptr;       // [Q][MAX_PROBES-1] probe window starts (probe_L rows each)
     unsigned long long *bsf = nullptr;  // [Q] packed
     uint32_t *cand = nullptr;       // [Q][cand_cap] sorted positions
-    uint8_t *candq = nullptr;       // [Q][cand_cap] u8 bound b of each candidate: b / qscale <= LB^2
+    uint8_t *candq = nullptr;       // [Q][cand_cap] u8 bound b of each candidate: b / qscale <= LB^2,
+                                    // or B_UNCHECKED: kept on its u8 sum alone, exact rule pending
+    uint32_t *cand2 = nullptr;      // [Q][cand_cap] the candidates after candcheck_kernel (the refine's list)
+    uint8_t *candq2 = nullptr;      // [Q][cand_cap] their u8 bounds
+    uint32_t *cand_cnt2 = nullptr;  // [Q]
     float *qscale = nullptr;        // [Q] 254 / T of the query's last scan, rounded down (R11b)
+    float *qT = nullptr;            // [Q] T of the query's last scan
     uint32_t *cand_cnt = nullptr;   // [Q] (may exceed cand_cap: overflow)
     NearEntry *near = nullptr;      // [Q][NEAR_K]
     uint32_t *near_cnt = nullptr;   // [Q]
@@ -105,7 +112,7 @@ struct QueryScratch {
 };
 
 struct StageTimes {
-    float qprep = 0, window = 0, lbscan = 0, refine = 0, finalize = 0;
+    float qprep = 0, window = 0, lbscan = 0, candcheck = 0, refine = 0, finalize = 0;
 };
 
 }  // namespace isax
@@ -185,6 +192,9 @@ void launch_leaf_meta(const uint8_t *sax, uint64_t N, uint8_t *lmeta, uint8_t *s
 // summaries or flat words); the leaf scan adds its leaf-word and leaf-summary bytes to qs.scan_bytes_dev on the device.
 uint64_t launch_lbscan(const isax_index *ix, uint32_t nq, const uint32_t *qmap, const float2 *band, float delta,
                        cudaStream_t s);
+// lbscan.cu: the exact fp32 rule for the candidates the leaf scan kept on their u8 sum alone,
+// and compaction of every list into cand2 / cand_cnt2 (the refine's input)
+void launch_candcheck(const isax_index *ix, uint32_t Q, cudaStream_t s);
 // refine.cu
 void launch_refine(const isax_index *ix, uint32_t Q, float delta, cudaStream_t s);
 void launch_finalize(const isax_index *ix, uint32_t Q, float delta, int64_t *out_id, float *out_dist,

@@ -309,14 +309,17 @@ __global__ void __launch_bounds__(256) scanprep_kernel(const float *__restrict__
                                                        const unsigned long long *__restrict__ bsf,
                                                        const uint32_t *__restrict__ win, float onepd,
                                                        uint8_t *__restrict__ lut8, uint4 *__restrict__ qconst,
-                                                       float *__restrict__ qscale) {
+                                                       float *__restrict__ qscale, float *__restrict__ qT) {
     const uint32_t i = blockIdx.x;
     const uint32_t qi = qmap[i];
     const QConst k = load_qconst(qi, true, bsf, band, i, win, onepd);
     if (threadIdx.x == 0) qconst[i] = make_uint4(__float_as_uint(k.lo), __float_as_uint(k.T), k.ws, k.we);
     const bool none = !(k.T >= 0.f);  // an empty band keeps nothing
     const float sc = none ? 0.f : __fdiv_rd(254.0f, k.T);  // T = 0 -> +inf
-    if (threadIdx.x == 0) qscale[qi] = sc;
+    if (threadIdx.x == 0) {
+        qscale[qi] = sc;
+        qT[qi] = k.T;
+    }
     const float4 *L = reinterpret_cast<const float4 *>(lut_all + (uint64_t)qi * W * CARD);
     uint32_t *o = reinterpret_cast<uint32_t *>(lut8 + (uint64_t)i * W * CARD);
     for (uint32_t e = threadIdx.x; e < W * CARD / 4; e += blockDim.x) {
@@ -506,9 +509,11 @@ __global__ void __launch_bounds__(LF_THREADS, 1) leafscan_kernel(
         // ---- phase B: the members of surviving leaves, two worklist entries (A, B) per warp step.
         // Each warp takes steps warp, warp + NW, ... and double-buffers their words in its own
         // shared staging slots with cp.async: the next step is in flight while the current one is
-        // tested (no registers held across the global latency).
+        // tested (no registers held across the global latency). (A shared step counter for
+        // dynamic balance measured 3% slower.)
         const uint32_t nwl = wl_cnt;
         const uint32_t nstep = (nwl + 1) / 2;
+        if (t == 0) bytes += nwl * LEAF * 16u;  // the worklist leaves' words (a partial last leaf is counted whole)
         uint4 *slot = stage + warp * 4 * LEAF;  // [2 buffers][2 entries][LEAF] words
         auto prefetch = [&](uint32_t p, uint32_t buf) {
 #pragma unroll
@@ -533,7 +538,6 @@ __global__ void __launch_bounds__(LF_THREADS, 1) leafscan_kernel(
             const uint32_t pA = (c0 + (entA & 0xFFFFu)) * LEAF + lane;
             const uint32_t pB = hasB ? (c0 + (entB & 0xFFFFu)) * LEAF + lane : N;
             const uint4 wA = slot[(2 * buf) * LEAF + lane], wB = slot[(2 * buf + 1) * LEAF + lane];
-            bytes += (pA < N ? 16u : 0u) + (pB < N ? 16u : 0u);
             if (lane < G) my_alive += ((mA >> lane) & 1u) + ((mB >> lane) & 1u);
             // rolled loop over the queries that kept either leaf: unrolling it over G made the
             // kernel ~120 KB of SASS, and instruction-cache misses became the top stall
@@ -557,9 +561,11 @@ __global__ void __launch_bounds__(LF_THREADS, 1) leafscan_kernel(
                 if (!__any_sync(FULL, m0 || m1)) continue;
                 // The flat scan's rule is lo < LB^2 <= T on the exact fp32 bound. A u8 sum <= E_SURE
                 // already implies LB^2 <= T (R11b), and in the first band (lo < 0) lo < LB^2 always
-                // holds, so only the members with a u8 sum in (E_SURE, 254] (or any in later bands)
-                // need the exact bound. A sure member's histogram bin comes from its u8 sum, never
-                // above its exact bin (band shrinking, R10, stays an upper bound on the count).
+                // holds. In the first band, members with a u8 sum in (E_SURE, 254] are kept marked
+                // B_UNCHECKED and get the exact rule in candcheck_kernel, many at a time; in later
+                // bands every member gets it here. A first-band member's histogram bin comes from
+                // its u8 sum, never above its exact bin (band shrinking, R10, stays an upper bound
+                // on the count).
                 const QConst kq = qc[g];
                 const float *Lg = lut_all + (uint64_t)qid[g] * W * CARD;
                 const bool band0 = kq.lo < 0.f;
@@ -568,18 +574,18 @@ __global__ void __launch_bounds__(LF_THREADS, 1) leafscan_kernel(
                     const bool maybe = u ? m1 : m0;
                     const uint32_t e8 = u ? eB : eA;
                     const uint32_t pos = u ? pB : pA;
-                    const bool sure = maybe && band0 && e8 <= E_SURE;
-                    const bool check = maybe && !sure;
+                    const bool first = maybe && band0;
+                    const bool check = maybe && !band0;
                     const float lb = check ? word_lb(Lg, u ? wB : wA) : 0.f;
-                    const bool keep = (sure || (check && lb > kq.lo && lb <= kq.T)) && (pos < kq.ws || pos >= kq.we);
-                    // the candidate's u8 bound for the refine's skip test: b <= LB^2 * sc
-                    uint32_t b = e8;
+                    const bool keep = (first || (check && lb > kq.lo && lb <= kq.T)) && (pos < kq.ws || pos >= kq.we);
+                    // the candidate's u8 bound b <= LB^2 * sc (for the refine), or B_UNCHECKED
+                    uint32_t b = e8 <= E_SURE ? e8 : B_UNCHECKED;
                     if (check) {
                         const float y = __fmul_rd(lb, qsc[g]);
                         b = lb > 0.f ? (y >= 254.f ? 254u : (uint32_t)y) : 0u;
                     }
                     if (keep)
-                        atomicAdd(&shist[g][sure ? min(e8 * HIST_BINS / 254u, HIST_BINS - 1) : hist_bin(lb, kq.lo, kq.T)], 1u);
+                        atomicAdd(&shist[g][first ? min(e8 * HIST_BINS / 254u, HIST_BINS - 1) : hist_bin(lb, kq.lo, kq.T)], 1u);
                     emit(keep, pos, b, g, qid[g], lane, lt, cbuf, qbuf, cb_cnt, cand, candq, cand_cnt, cap);
                 }
             }
@@ -627,7 +633,7 @@ uint64_t launch_lbscan(const isax_index *ix, uint32_t nq, const uint32_t *qmap, 
     if (!nq) return 0;
     const float onepd = 1.0f + delta;
     const QueryScratch &qs = ix->qs;
-    scanprep_kernel<<<nq, 256, 0, s>>>(qs.lut, qmap, band, qs.bsf, qs.win, onepd, qs.lut8, qs.qconst, qs.qscale);
+    scanprep_kernel<<<nq, 256, 0, s>>>(qs.lut, qmap, band, qs.bsf, qs.win, onepd, qs.lut8, qs.qconst, qs.qscale, qs.qT);
     if (ix->opts.flags & ISAX_FLAG_FLAT_SCAN) {  // ParIS flat scan, kept for A/B measurement
         const uint32_t G = nq >= 4 ? 4 : nq;
         if (G == 4) launch_g<4>(ix, nq, qmap, band, onepd, s);
@@ -643,6 +649,137 @@ uint64_t launch_lbscan(const isax_index *ix, uint32_t nq, const uint32_t *qmap, 
     else if (G == 2) launch_leaf<2>(ix, nq, qmap, s);
     else launch_leaf<1>(ix, nq, qmap, s);
     return 0;  // the leaf scan counts the node summaries and words it reads on the device
+}
+
+// ------------------------------------------------------------------------------------ candcheck
+// The exact fp32 rule (LB^2 <= T, the flat scan's) for the candidates the leaf scan kept on their
+// u8 sum alone (candq == B_UNCHECKED), many at a time: a CTA takes a slice of the flat candidate
+// index (all queries' lists back to back), loads the fp32 LUT of each query it meets into shared
+// memory, and each thread tests one candidate (its word from the sorted SAX array, 16 shared
+// lookups summed left to right). Every list is compacted into cand2 (order is immaterial, R9);
+// the kept ones' u8 bound becomes floor(LB^2 * sc).
+constexpr int CK_THREADS = 256;
+
+__global__ void __launch_bounds__(CK_THREADS) candcheck_kernel(
+    const uint32_t *__restrict__ cand, const uint8_t *__restrict__ candq, const uint32_t *__restrict__ cand_cnt,
+    uint32_t Q, uint32_t cap, const uint4 *__restrict__ sax, const float *__restrict__ lut_all,
+    const float *__restrict__ qT, const float *__restrict__ qscale, uint32_t *__restrict__ cand2,
+    uint8_t *__restrict__ candq2, uint32_t *__restrict__ cand_cnt2) {
+    constexpr int U = 8;  // candidates per thread per iteration, all loads in flight together
+    __shared__ uint32_t pre[1025];
+    __shared__ __align__(16) float slut[W * CARD];
+    constexpr uint32_t FULL = 0xffffffffu;
+    const uint32_t t = threadIdx.x, lane = t & 31;
+    const uint32_t lt = (1u << lane) - 1u;
+    cand_prefix<CK_THREADS>(cand_cnt, Q, cap, pre);
+    const uint32_t total = pre[Q];
+    // one contiguous slice per CTA; the LUT of the slice's first query goes to shared memory
+    // (lanes of a later query read the global LUT)
+    const uint32_t per = (total + gridDim.x - 1) / gridDim.x;
+    const uint32_t f0 = min(blockIdx.x * per, total), f1 = min(f0 + per, total);
+    if (f0 >= f1) return;
+    uint32_t q0;
+    {
+        uint32_t lo = 0, hi = Q;
+        while (hi - lo > 1) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (pre[mid] <= f0) lo = mid;
+            else hi = mid;
+        }
+        q0 = lo;
+    }
+    {
+        const float4 *src = reinterpret_cast<const float4 *>(lut_all + (uint64_t)q0 * W * CARD);
+        float4 v[W * CARD / 4 / CK_THREADS];
+#pragma unroll
+        for (int k = 0; k < W * CARD / 4 / CK_THREADS; k++) v[k] = __ldg(src + k * CK_THREADS + t);
+#pragma unroll
+        for (int k = 0; k < W * CARD / 4 / CK_THREADS; k++) reinterpret_cast<float4 *>(slut)[k * CK_THREADS + t] = v[k];
+    }
+    __syncthreads();
+    uint32_t q = q0;  // a thread's query only moves forward
+    for (uint32_t fb = f0; fb < f1; fb += U * CK_THREADS) {
+        uint32_t qk[U], pos[U], b[U];
+        bool valid[U];
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const uint32_t f = fb + u * CK_THREADS + t;
+            valid[u] = f < f1;
+            if (valid[u])
+                while (pre[q + 1] <= f) q++;
+            qk[u] = q;
+            const uint64_t k = (uint64_t)q * cap + (f - pre[q]);
+            pos[u] = valid[u] ? cand[k] : 0u;
+            b[u] = valid[u] ? candq[k] : 0u;
+        }
+        uint4 wv[U];
+#pragma unroll
+        for (int u = 0; u < U; u++) wv[u] = valid[u] && b[u] == B_UNCHECKED ? __ldg(sax + pos[u]) : make_uint4(0, 0, 0, 0);
+        bool keep[U];
+        bool one_q = true;  // this lane's U candidates share one query
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            keep[u] = valid[u];
+            one_q &= !valid[u] || qk[u] == qk[0];
+            if (valid[u] && b[u] == B_UNCHECKED) {
+                const float *L = qk[u] == q0 ? slut : lut_all + (uint64_t)qk[u] * W * CARD;
+                const float lb = word_lb(L, wv[u]);
+                keep[u] = lb <= qT[qk[u]];  // first band: lo < 0 <= LB^2 always
+                const float y = __fmul_rd(lb, qscale[qk[u]]);
+                b[u] = lb > 0.f ? (y >= 254.f ? 254u : (uint32_t)y) : 0u;
+            }
+        }
+        // append to the query's compacted list: one global atomic per warp when the whole warp's
+        // candidates share a query (the common case), else one per (query, u) peer group
+        const uint32_t q_lane = qk[0];
+        const uint32_t q_w = __shfl_sync(FULL, q_lane, 0);  // (every lane shuffles: no short circuit)
+        if (__all_sync(FULL, one_q && q_lane == q_w)) {
+            uint32_t bal[U], cnt = 0;
+#pragma unroll
+            for (int u = 0; u < U; u++) {
+                bal[u] = __ballot_sync(FULL, keep[u]);
+                cnt += __popc(bal[u]);
+            }
+            uint32_t base = 0;
+            if (lane == 0 && cnt) base = atomicAdd(&cand_cnt2[q_lane], cnt);
+            base = __shfl_sync(FULL, base, 0);
+#pragma unroll
+            for (int u = 0; u < U; u++) {
+                if (keep[u]) {
+                    const uint64_t k2 = (uint64_t)q_lane * cap + base + __popc(bal[u] & lt);
+                    cand2[k2] = pos[u];
+                    candq2[k2] = (uint8_t)b[u];
+                }
+                base += __popc(bal[u]);
+            }
+        } else {
+#pragma unroll
+            for (int u = 0; u < U; u++) {
+                const uint32_t peers = __match_any_sync(FULL, keep[u] ? qk[u] : 0xffffffffu);
+                if (keep[u]) {
+                    const uint32_t leader = __ffs(peers) - 1;
+                    uint32_t base = 0;
+                    if (lane == leader) base = atomicAdd(&cand_cnt2[qk[u]], (uint32_t)__popc(peers));
+                    base = __shfl_sync(peers, base, leader);
+                    const uint64_t k2 = (uint64_t)qk[u] * cap + base + __popc(peers & lt);
+                    cand2[k2] = pos[u];
+                    candq2[k2] = (uint8_t)b[u];
+                }
+            }
+        }
+    }
+}
+
+void launch_candcheck(const isax_index *ix, uint32_t Q, cudaStream_t s) {
+    const QueryScratch &qs = ix->qs;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaMemsetAsync(qs.cand_cnt2, 0, Q * sizeof(uint32_t), s);
+    const unsigned grid = (unsigned)sms * 8;  // the total is only known on the device
+    candcheck_kernel<<<grid, CK_THREADS, 0, s>>>(qs.cand, qs.candq, qs.cand_cnt, Q, qs.cand_cap,
+                                                 reinterpret_cast<const uint4 *>(ix->sax), qs.lut, qs.qT, qs.qscale,
+                                                 qs.cand2, qs.candq2, qs.cand_cnt2);
 }
 
 // ------------------------------------------------------------------------------------ leaf meta

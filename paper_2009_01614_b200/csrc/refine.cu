@@ -111,36 +111,6 @@ __global__ void __launch_bounds__(RF_THREADS) refine_kernel(const float *__restr
     }
 }
 
-// exclusive prefix of min(cand_cnt[q], cap) over q < Q into pre[0..Q], by the whole CTA
-__device__ __forceinline__ void cand_prefix(const uint32_t *__restrict__ cand_cnt, uint32_t Q, uint32_t cap,
-                                            uint32_t *pre) {
-    __shared__ uint32_t wsum[RF_THREADS / 32];
-    const uint32_t t = threadIdx.x, lane = t & 31, warp = t >> 5;
-    uint32_t carry = 0;
-    for (uint32_t b = 0; b < Q; b += RF_THREADS) {
-        const uint32_t q = b + t;
-        const uint32_t v = q < Q ? min(cand_cnt[q], cap) : 0;
-        uint32_t inc = v;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t u = __shfl_up_sync(0xffffffffu, inc, o);
-            if (lane >= (uint32_t)o) inc += u;
-        }
-        if (lane == 31) wsum[warp] = inc;
-        __syncthreads();
-        uint32_t wpre = 0, tot = 0;
-        for (uint32_t w = 0; w < RF_THREADS / 32; w++) {
-            if (w < warp) wpre += wsum[w];
-            tot += wsum[w];
-        }
-        if (q < Q) pre[q] = carry + wpre + inc - v;
-        carry += tot;
-        __syncthreads();
-    }
-    if (t == 0) pre[Q] = carry;
-    __syncthreads();
-}
-
 // Quarter-warp variant for n <= 256 (the paper's lengths, 128 and 256). Eight lanes own a
 // candidate and keep two candidates in flight: both first halves are loaded before either is
 // reduced, which gives each lane 2 NH float4 outstanding. At n = 256 that is 1 KB per quarter
@@ -167,7 +137,7 @@ __global__ void __launch_bounds__(RF_THREADS) refine_q_kernel(const float *__res
     const uint32_t t = threadIdx.x, lane = t & 31, ql = lane & 7;
     unsigned long long rows_read = 0;  // half rows read by this quarter
     const uint32_t qmask = 0xFFu << (lane & 24);
-    cand_prefix(cand_cnt, Q, cap, pre);
+    cand_prefix<RF_THREADS>(cand_cnt, Q, cap, pre);
     const uint32_t total = pre[Q];
     const uint32_t nquart = gridDim.x * (RF_THREADS / 8);
     auto locate = [&](uint32_t f) {  // last q with pre[q] <= f
@@ -302,8 +272,8 @@ void launch_refine(const isax_index *ix, uint32_t Q, float delta, cudaStream_t s
         switch (nh) {
 #define RQ_CASE(K)                                                                                                  \
     case K:                                                                                                         \
-        refine_q_kernel<K><<<grid, RF_THREADS, 0, s>>>(ix->stored, ix->perm, ix->n, qs.qy, Q, qs.cand, qs.candq,     \
-                                                       qs.qscale, qs.cand_cnt,                                      \
+        refine_q_kernel<K><<<grid, RF_THREADS, 0, s>>>(ix->stored, ix->perm, ix->n, qs.qy, Q, qs.cand2, qs.candq2,   \
+                                                       qs.qscale, qs.cand_cnt2,                                      \
                                                        qs.cand_cap, qs.bsf, qs.near, qs.near_cnt, qs.counters,      \
                                                        onepd, qs.refine_bytes);                                     \
         break;
@@ -316,7 +286,7 @@ void launch_refine(const isax_index *ix, uint32_t Q, float delta, cudaStream_t s
     const uint32_t ns = (ix->n + 127) / 128;
 #define RF_CASE(K)                                                                                              \
     case K:                                                                                                     \
-        refine_kernel<K><<<grid, RF_THREADS, 0, s>>>(ix->stored, ix->perm, ix->n, qs.qy, Q, qs.cand, qs.cand_cnt, \
+        refine_kernel<K><<<grid, RF_THREADS, 0, s>>>(ix->stored, ix->perm, ix->n, qs.qy, Q, qs.cand2, qs.cand_cnt2, \
                                                      qs.cand_cap, qs.bsf, qs.near, qs.near_cnt, qs.counters, onepd); \
         break;
     switch (ns) {

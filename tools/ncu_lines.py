@@ -1,6 +1,8 @@
 """Warp-stall samples per CUDA source line (interleaved cuda,sass source page).
 
-python tools/ncu_lines.py <report.ncu-rep> [top]
+python tools/ncu_lines.py <report.ncu-rep> [top] [column]
+
+column: "stall" (default, warp-stall samples) or "inst" (warp instructions executed)
 """
 import csv
 import io
@@ -9,6 +11,8 @@ import sys
 
 rep = sys.argv[1]
 top = int(sys.argv[2]) if len(sys.argv) > 2 else 30
+col = sys.argv[3] if len(sys.argv) > 3 else "stall"
+col_name = {"stall": "Warp Stall Sampling (All Samples)", "inst": "Instructions Executed"}[col]
 raw = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
                      capture_output=True, text=True).stdout
 agg = {}
@@ -22,7 +26,7 @@ for r in csv.reader(io.StringIO(raw)):
         continue
     if r[0] == "Line No":
         hdr = r
-        ai = r.index("Warp Stall Sampling (All Samples)")
+        ai = r.index(col_name)
         continue
     if hdr is None or len(r) <= ai or not r[0].isdigit():
         continue
