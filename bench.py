@@ -44,6 +44,8 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="budget of the oracle cpu_baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--stats-out", default="")
+    ap.add_argument("--opt", action="append", default=[],
+                    help="index option key=value (isax_opts field, e.g. probe_L=128); default: the library's")
     return ap.parse_args()
 
 
@@ -169,6 +171,7 @@ def main():
     from paper_2009_01614_b200 import dist as pdist
 
     Q = args.queries or wl.Q
+    opts = {k: int(v) for k, v in (o.split("=", 1) for o in args.opt)}
     wlq = pdist.rank_workload(wl, rank)  # replicas: every rank answers its own queries
     # ---- build (a1-a5), timed on its own
     free, _ = torch.cuda.mem_get_info()
@@ -178,7 +181,7 @@ def main():
         x = datagen.series(wl, 0, wl.N)
         torch.cuda.synchronize()
         ev0.record()
-        ix = isax.Index.build(x)
+        ix = isax.Index.build(x, **opts)
         ev1.record()
         torch.cuda.synchronize()
         build_mode = "device-resident input"
@@ -187,7 +190,7 @@ def main():
     else:
         fptr, ctx = datagen.fill_callback(wl)
         ev0.record()
-        ix = isax.Index.build_stream(wl.N, wl.n, fptr, ctx)
+        ix = isax.Index.build_stream(wl.N, wl.n, fptr, ctx, **opts)
         ev1.record()
         torch.cuda.synchronize()
         build_mode = "streamed input (generator fill callback, 2 passes; generation time included)"
@@ -299,7 +302,7 @@ def main():
                    "parallelism": f"replicas x{world} (each rank: own query batch)",
                    "l2": "inputs larger than L2 (SAX array 16N B, stored rows 4nN B)" if wl.N * 16 > 126e6
                    else "working set fits in L2 (small config)",
-                   "source": wl.cite},
+                   "source": wl.cite, "index_opts": opts or "library defaults"},
         "roofline": roofline,
         "kernels": kernels,
         "e2e": {"value": round(Q * e2e_steps * world / e2e_s, 2), "unit": "queries/s",

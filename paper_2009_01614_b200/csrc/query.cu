@@ -229,42 +229,51 @@ __global__ void __launch_bounds__(256) window_kernel(const float *__restrict__ s
     }
     if (t == 0) smin = ~0ull;
     __syncthreads();
+    // four rows per warp step, all their loads in flight before any reduction; the warp's minimum
+    // is tracked as (d^2 bits, row) and its id is looked up once at the end (the answer itself
+    // comes from the near list, R9; the id in the BSF word is only a fallback)
+    constexpr int RW = 4;
     unsigned long long mine = ~0ull;
-    for (uint32_t r = r0 + warp * 2; r < r1; r += 16) {
-        const bool two = r + 1 < r1;
-        const uint32_t pa = row_pos(r), pb = two ? row_pos(r + 1) : pa;
-        const float *ra = stored + (uint64_t)pa * n, *rb = stored + (uint64_t)pb * n;
-        float aa = 0.f, ab = 0.f;
+    for (uint32_t r = r0 + warp * RW; r < r1; r += 8 * RW) {
+        const float *rp[RW];
+#pragma unroll
+        for (int j = 0; j < RW; j++) rp[j] = stored + (uint64_t)row_pos(r + j < r1 ? r + j : r) * n;
+        float4 v[RW][NS];
 #pragma unroll
         for (int k = 0; k < NS; k++) {
             const uint32_t i = k * 128 + 4 * lane;
-            if (i < n) {
-                const float4 va = __ldcs(reinterpret_cast<const float4 *>(ra + i));
-                const float4 vb = __ldcs(reinterpret_cast<const float4 *>(rb + i));
-                float d;
-                d = va.x - qv[k].x; aa = fmaf(d, d, aa);
-                d = va.y - qv[k].y; aa = fmaf(d, d, aa);
-                d = va.z - qv[k].z; aa = fmaf(d, d, aa);
-                d = va.w - qv[k].w; aa = fmaf(d, d, aa);
-                d = vb.x - qv[k].x; ab = fmaf(d, d, ab);
-                d = vb.y - qv[k].y; ab = fmaf(d, d, ab);
-                d = vb.z - qv[k].z; ab = fmaf(d, d, ab);
-                d = vb.w - qv[k].w; ab = fmaf(d, d, ab);
-            }
+#pragma unroll
+            for (int j = 0; j < RW; j++)
+                v[j][k] = i < n ? __ldcs(reinterpret_cast<const float4 *>(rp[j] + i)) : make_float4(0, 0, 0, 0);
         }
-        aa = warp_sum(aa);
-        ab = warp_sum(ab);
+        float a[RW];
+#pragma unroll
+        for (int j = 0; j < RW; j++) {
+            float s = 0.f;
+#pragma unroll
+            for (int k = 0; k < NS; k++) {
+                if (k * 128 + 4 * lane < n) {
+                    float d;
+                    d = v[j][k].x - qv[k].x; s = fmaf(d, d, s);
+                    d = v[j][k].y - qv[k].y; s = fmaf(d, d, s);
+                    d = v[j][k].z - qv[k].z; s = fmaf(d, d, s);
+                    d = v[j][k].w - qv[k].w; s = fmaf(d, d, s);
+                }
+            }
+            a[j] = warp_sum(s);
+        }
         if (lane == 0) {
-            d2s[r - r0] = aa;
-            const unsigned long long p = pack_bsf(aa, perm[pa]);
-            mine = p < mine ? p : mine;
-            if (two) {
-                d2s[r + 1 - r0] = ab;
-                const unsigned long long pq = pack_bsf(ab, perm[pb]);
-                mine = pq < mine ? pq : mine;
+#pragma unroll
+            for (int j = 0; j < RW; j++) {
+                if (r + j < r1) {
+                    d2s[r + j - r0] = a[j];
+                    const unsigned long long p = pack_bsf(a[j], r + j);
+                    mine = p < mine ? p : mine;
+                }
             }
         }
     }
+    if (lane == 0 && mine != ~0ull) mine = pack_bsf(bsf_d2(mine), perm[row_pos((uint32_t)mine)]);
     if (lane == 0) atomicMin(&smin, mine);
     __syncthreads();
     if (t == 0) {
