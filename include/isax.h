@@ -44,7 +44,8 @@ typedef struct isax_opts {
     uint32_t window_L;   /* leaf-sized window of the approximate answer (R5). Default 1024. */
     int32_t slack_log2;  /* prune/abandon slack delta = 2^slack_log2 (R8). Default -12. */
     uint32_t batch_Q;    /* queries processed per device batch. Default 128. */
-    uint32_t cand_cap;   /* candidate-list capacity per query per round. Default 1<<20. Overflow runs more rounds. */
+    uint32_t cand_cap;   /* candidate-list capacity per query per round. 0 = default: min(N, 2^23), halved while the
+                            query scratch (about 10 B x batch_Q x cand_cap) does not fit. Overflow runs more rounds. */
     uint32_t flags;      /* ISAX_FLAG_* bits; 0 = defaults */
     uint32_t probe_bits; /* multi-probe approximate answer (R5): refine extra windows at the 2^probe_bits - 1 keys
                             obtained by flipping the most fragile plane-0/1 key bits. 0 = default 4; max 5;

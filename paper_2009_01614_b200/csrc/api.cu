@@ -38,7 +38,7 @@ static bool is_device_ptr(const void *p) {
 }
 
 static isax_opts default_opts(const isax_opts *o) {
-    isax_opts r{1024, -12, 128, 1u << 20, 0, 4, 256};
+    isax_opts r{1024, -12, 128, 0, 0, 4, 256};  // cand_cap 0: chosen at the first query (alloc_scratch)
     if (o) {
         if (o->probe_bits) r.probe_bits = o->probe_bits;
         if (o->probe_L) r.probe_L = o->probe_L;
@@ -78,18 +78,32 @@ static cudaError_t dmalloc(T **p, size_t count, size_t *acc) {
 static void free_scratch(isax_index *ix) {
     QueryScratch &q = ix->qs;
     cudaFree(q.qy); cudaFree(q.qpaa); cudaFree(q.qsax); cudaFree(q.lut); cudaFree(q.lut8); cudaFree(q.qconst); cudaFree(q.win); cudaFree(q.pwin); cudaFree(q.bsf);
-    cudaFree(q.cand); cudaFree(q.candq); cudaFree(q.cand2); cudaFree(q.candq2); cudaFree(q.cand_cnt2); cudaFree(q.qscale); cudaFree(q.qT); cudaFree(q.cand_cnt); cudaFree(q.near); cudaFree(q.near_cnt); cudaFree(q.qmap); cudaFree(q.qband); cudaFree(q.cand_hist);
+    cudaFree(q.cand); cudaFree(q.candq); cudaFree(q.cand2); cudaFree(q.candq2); cudaFree(q.cand_cnt2); cudaFree(q.cnt_hi); cudaFree(q.cnt_f); cudaFree(q.qscale); cudaFree(q.qT); cudaFree(q.cand_cnt); cudaFree(q.near); cudaFree(q.near_cnt); cudaFree(q.qmap); cudaFree(q.qband); cudaFree(q.cand_hist);
     cudaFree(q.counters); cudaFree(q.counters_leaf); cudaFree(q.scan_bytes_dev); cudaFree(q.task_ctr); cudaFree(q.refine_bytes);
     cudaFree(q.flag); cudaFree(q.qmap2);
     if (q.h_mirror) cudaFreeHost(q.h_mirror);
     q = QueryScratch{};
 }
 
+// Candidate capacity per query: the caller's, or min(N, 2^23) (a query never has more than N
+// candidates), halved while the scratch does not fit in device memory (down to 2^16). A query that
+// overflows it runs more rounds (R10), each a rescan, so the default is generous: at 100 queries
+// over 200M series a few queries keep millions of candidates.
+static int alloc_scratch_cap(isax_index *ix, uint32_t cap);
 static int alloc_scratch(isax_index *ix) {
+    if (ix->qs.cap_Q) return ISAX_OK;
+    if (ix->opts.cand_cap) return alloc_scratch_cap(ix, ix->opts.cand_cap);
+    uint32_t cap = (uint32_t)std::min<uint64_t>(ix->N, 1ull << 23);
+    for (;;) {
+        const int rc = alloc_scratch_cap(ix, cap);
+        if (rc != ISAX_E_NOMEM || cap <= (1u << 16)) return rc;
+        cap = std::max(cap / 2, 1u << 16);
+    }
+}
+
+static int alloc_scratch_cap(isax_index *ix, uint32_t cap) {
     QueryScratch &q = ix->qs;
-    if (q.cap_Q) return ISAX_OK;
     const uint32_t Q = ix->opts.batch_Q;
-    const uint32_t cap = ix->opts.cand_cap;
     size_t acc = 0;
     cudaError_t e = cudaSuccess;
 #define A(ptr, cnt) \
@@ -108,6 +122,8 @@ static int alloc_scratch(isax_index *ix) {
     A(cand2, (size_t)Q * cap);
     A(candq2, (size_t)Q * cap);
     A(cand_cnt2, Q);
+    A(cnt_hi, Q);
+    A(cnt_f, Q);
     A(qscale, Q);
     A(qT, Q);
     A(cand_cnt, Q);
@@ -128,6 +144,8 @@ static int alloc_scratch(isax_index *ix) {
     if (e == cudaSuccess) q.hm.carve(q.h_mirror, Q);
     if (e != cudaSuccess) {
         free_scratch(ix);
+        cudaGetLastError();  // clear a sticky allocation error before a smaller retry
+        if (e == cudaErrorMemoryAllocation) return set_error(ISAX_E_NOMEM, "query scratch does not fit in device memory");
         return cuda_error(e, "allocating query scratch");
     }
     q.cap_Q = Q;
@@ -343,12 +361,13 @@ static int nn1_device(isax_index *ix, const float *d_q, uint32_t Q, int64_t *d_i
             launch_refine(ix, B, delta, s);
             if (timed && round == 0) cudaEventRecord(ix->ev[4], s);
             launch_finalize(ix, B, delta, d_id + b0, d_dist + b0, s);  // speculative: redone after another round
-            // scanprep + scan, candcheck, refine, finalize
-            ix->st_launches += ((ix->opts.flags & ISAX_FLAG_FLAT_SCAN) ? 1 : 2) + 3;
+            // scanprep + scan, candcheck, refine + filter + refine, finalize
+            ix->st_launches += ((ix->opts.flags & ISAX_FLAG_FLAT_SCAN) ? 1 : 2) + 5;
             if (timed && round == 0) cudaEventRecord(ix->ev[5], s);
             ISAX_CUDA(cudaGetLastError());
             ISAX_CUDA(cudaMemcpyAsync(hm.cand_cnt, qs.cand_cnt, B * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
             ISAX_CUDA(cudaMemcpyAsync(hm.cand_cnt2, qs.cand_cnt2, B * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+            ISAX_CUDA(cudaMemcpyAsync(hm.cnt_hi, qs.cnt_hi, B * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
             ISAX_CUDA(cudaMemcpyAsync(hm.near_cnt, qs.near_cnt, B * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
             ISAX_CUDA(cudaMemcpyAsync(hm.flag, qs.flag, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
             ISAX_CUDA(cudaMemcpyAsync(hm.bsf, qs.bsf, B * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
@@ -383,7 +402,7 @@ static int nn1_device(isax_index *ix, const float *d_q, uint32_t Q, int64_t *d_i
                 const uint32_t i = hm.qmap[k];
                 const uint32_t cnt = hm.cand_cnt[i];
                 bsf_h[i] = bsf_d2_host(hm.bsf[i]);
-                ix->st_cand[b0 + i] += hm.cand_cnt2[i];  // after the exact rule (candcheck_kernel)
+                ix->st_cand[b0 + i] += hm.cand_cnt2[i] + hm.cnt_hi[i];  // after the exact rule (candcheck_kernel)
                 ix->st_rounds[b0 + i] = round + 1;
                 if (hm.near_cnt[i] > (uint32_t)NEAR_K) {  // near overflow: start over, BSF kept
                     band[i] = make_float2(-1.0f, INF);
@@ -601,7 +620,7 @@ int isax_stats(const isax_index *cix, char *buf, size_t cap) {
              "\"N\":%llu,\"n\":%u,\"window_L\":%u,\"slack_log2\":%d,\"batch_Q\":%u,\"cand_cap\":%u,"
              "\"ms_first_batch\":{\"qprep\":%.4f,\"window\":%.4f,\"lbscan\":%.4f,\"candcheck\":%.4f,\"refine\":%.4f,\"total\":%.4f},",
              (unsigned long long)ix->N, ix->n, ix->opts.window_L, ix->opts.slack_log2, ix->opts.batch_Q,
-             ix->opts.cand_cap, ix->st_ms.qprep, ix->st_ms.window, ix->st_ms.lbscan, ix->st_ms.candcheck, ix->st_ms.refine,
+             ix->qs.cand_cap, ix->st_ms.qprep, ix->st_ms.window, ix->st_ms.lbscan, ix->st_ms.candcheck, ix->st_ms.refine,
              ix->st_ms.finalize);
     j += tmp;
     auto arr = [&](const char *name, const std::vector<uint32_t> &v, bool last) {

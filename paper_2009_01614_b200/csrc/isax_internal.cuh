@@ -49,10 +49,10 @@ struct NearEntry {  // a completed refinement within (1+delta) of the BSF at tha
 
 // Pinned host mirror of the per-batch counters (one async copy each per round, one sync).
 struct HostMirror {
-    uint32_t *cand_cnt, *cand_cnt2, *near_cnt, *flag, *counters, *win, *leaves, *qmap, *rewin;
+    uint32_t *cand_cnt, *cand_cnt2, *cnt_hi, *near_cnt, *flag, *counters, *win, *leaves, *qmap, *rewin;
     unsigned long long *bsf, *bsf0, *scan_bytes_dev, *refine_bytes;
     float2 *band;
-    static size_t bytes(uint32_t Q) { return (size_t)Q * (8 * 4 + 4 * 4 + 2 * 4 + 8 * 2 + 12) + 512; }
+    static size_t bytes(uint32_t Q) { return (size_t)Q * (8 * 4 + 4 * 4 + 2 * 4 + 8 * 2 + 16) + 512; }
     void carve(void *base, uint32_t Q) {
         unsigned char *p = static_cast<unsigned char *>(base);
         auto take = [&](size_t n) { unsigned char *r = p; p += (n + 15) & ~size_t(15); return r; };
@@ -63,6 +63,7 @@ struct HostMirror {
         band = reinterpret_cast<float2 *>(take(8ull * Q));
         cand_cnt = reinterpret_cast<uint32_t *>(take(4ull * Q));
         cand_cnt2 = reinterpret_cast<uint32_t *>(take(4ull * Q));
+        cnt_hi = reinterpret_cast<uint32_t *>(take(4ull * Q));
         near_cnt = reinterpret_cast<uint32_t *>(take(4ull * Q));
         flag = reinterpret_cast<uint32_t *>(take(4));
         counters = reinterpret_cast<uint32_t *>(take(16ull * Q));
@@ -91,7 +92,9 @@ struct QueryScratch {
                                     // or B_UNCHECKED: kept on its u8 sum alone, exact rule pending
     uint32_t *cand2 = nullptr;      // [Q][cand_cap] the candidates after candcheck_kernel (the refine's list)
     uint8_t *candq2 = nullptr;      // [Q][cand_cap] their u8 bounds
-    uint32_t *cand_cnt2 = nullptr;  // [Q]
+    uint32_t *cand_cnt2 = nullptr;  // [Q] first refine pass: cand2[q][0 .. cand_cnt2)
+    uint32_t *cnt_hi = nullptr;     // [Q] second pass before filtering: cand2[q][cap - cnt_hi .. cap)
+    uint32_t *cnt_f = nullptr;      // [Q] second pass after filtering: cand[q][0 .. cnt_f)
     float *qscale = nullptr;        // [Q] 254 / T of the query's last scan, rounded down (R11b)
     float *qT = nullptr;            // [Q] T of the query's last scan
     uint32_t *cand_cnt = nullptr;   // [Q] (may exceed cand_cap: overflow)

@@ -659,12 +659,16 @@ uint64_t launch_lbscan(const isax_index *ix, uint32_t nq, const uint32_t *qmap, 
 // lookups summed left to right). Every list is compacted into cand2 (order is immaterial, R9);
 // the kept ones' u8 bound becomes floor(LB^2 * sc).
 constexpr int CK_THREADS = 256;
+constexpr uint32_t B_SPLIT = 140;     // second refine pass: b > B_SPLIT, i.e. LB^2 above about 0.55 T
+constexpr uint32_t SPLIT_MIN = 4096;  // ... for queries with more candidates than this
+constexpr uint32_t SPLIT_TARGET = 65536;  // first-pass size a lowered split aims at
 
 __global__ void __launch_bounds__(CK_THREADS) candcheck_kernel(
     const uint32_t *__restrict__ cand, const uint8_t *__restrict__ candq, const uint32_t *__restrict__ cand_cnt,
     uint32_t Q, uint32_t cap, const uint4 *__restrict__ sax, const float *__restrict__ lut_all,
     const float *__restrict__ qT, const float *__restrict__ qscale, uint32_t *__restrict__ cand2,
-    uint8_t *__restrict__ candq2, uint32_t *__restrict__ cand_cnt2) {
+    uint8_t *__restrict__ candq2, uint32_t *__restrict__ cand_cnt2, uint32_t *__restrict__ cnt_hi,
+    const uint32_t *__restrict__ hist) {
     constexpr int U = 8;  // candidates per thread per iteration, all loads in flight together
     __shared__ uint32_t pre[1025];
     __shared__ __align__(16) float slut[W * CARD];
@@ -688,6 +692,23 @@ __global__ void __launch_bounds__(CK_THREADS) candcheck_kernel(
         }
         q0 = lo;
     }
+    // the split of q0's list between the two refine passes: B_SPLIT, lowered so that the first
+    // pass holds about SPLIT_TARGET candidates when the scan's histogram of LB^2 / T (R10; bins
+    // of width T / 64 = 254 / 64 u8 units) says the list is much longer
+    __shared__ uint32_t s_b1;
+    if (t < 32) {
+        const uint32_t c = hist[q0 * HIST_BINS + 2 * t] + hist[q0 * HIST_BINS + 2 * t + 1];
+        uint32_t inc = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t u = __shfl_up_sync(FULL, inc, o);
+            if (t >= (uint32_t)o) inc += u;
+        }
+        const uint32_t over = __ballot_sync(FULL, inc >= SPLIT_TARGET);
+        uint32_t b1 = B_SPLIT;
+        if (over) b1 = min(B_SPLIT, (2u * (__ffs(over) - 1) + 2u) * 254u / HIST_BINS);
+        if (t == 0) s_b1 = b1;
+    }
     {
         const float4 *src = reinterpret_cast<const float4 *>(lut_all + (uint64_t)q0 * W * CARD);
         float4 v[W * CARD / 4 / CK_THREADS];
@@ -697,6 +718,7 @@ __global__ void __launch_bounds__(CK_THREADS) candcheck_kernel(
         for (int k = 0; k < W * CARD / 4 / CK_THREADS; k++) reinterpret_cast<float4 *>(slut)[k * CK_THREADS + t] = v[k];
     }
     __syncthreads();
+    const uint32_t b1 = s_b1;
     uint32_t q = q0;  // a thread's query only moves forward
     for (uint32_t fb = f0; fb < f1; fb += U * CK_THREADS) {
         uint32_t qk[U], pos[U], b[U];
@@ -729,41 +751,52 @@ __global__ void __launch_bounds__(CK_THREADS) candcheck_kernel(
                 b[u] = lb > 0.f ? (y >= 254.f ? 254u : (uint32_t)y) : 0u;
             }
         }
-        // append to the query's compacted list: one global atomic per warp when the whole warp's
-        // candidates share a query (the common case), else one per (query, u) peer group
+        // Append to the query's lists in cand2: the first refine pass's from the front, and for a
+        // query with more than SPLIT_MIN candidates the ones with b > B_SPLIT (LB^2 above about
+        // 0.55 T) from the back, for the second pass (refine.cu). One global atomic per list per
+        // warp when the whole warp's candidates share a query (the common case), else one per
+        // (query, list, u) peer group.
+        bool hi[U];
+#pragma unroll
+        for (int u = 0; u < U; u++)
+            hi[u] = keep[u] && b[u] > (qk[u] == q0 ? b1 : B_SPLIT) && pre[qk[u] + 1] - pre[qk[u]] > SPLIT_MIN;
+        auto put = [&](uint32_t qq, uint32_t idx, bool h, uint32_t p, uint32_t bb) {
+            const uint64_t k2 = (uint64_t)qq * cap + (h ? cap - 1 - idx : idx);
+            cand2[k2] = p;
+            candq2[k2] = (uint8_t)bb;
+        };
         const uint32_t q_lane = qk[0];
         const uint32_t q_w = __shfl_sync(FULL, q_lane, 0);  // (every lane shuffles: no short circuit)
         if (__all_sync(FULL, one_q && q_lane == q_w)) {
-            uint32_t bal[U], cnt = 0;
+            uint32_t bl[U], bh[U], cl = 0, ch = 0;
 #pragma unroll
             for (int u = 0; u < U; u++) {
-                bal[u] = __ballot_sync(FULL, keep[u]);
-                cnt += __popc(bal[u]);
+                bl[u] = __ballot_sync(FULL, keep[u] && !hi[u]);
+                bh[u] = __ballot_sync(FULL, hi[u]);
+                cl += __popc(bl[u]);
+                ch += __popc(bh[u]);
             }
             uint32_t base = 0;
-            if (lane == 0 && cnt) base = atomicAdd(&cand_cnt2[q_lane], cnt);
-            base = __shfl_sync(FULL, base, 0);
+            if (lane == 0 && cl) base = atomicAdd(&cand_cnt2[q_lane], cl);
+            if (lane == 1 && ch) base = atomicAdd(&cnt_hi[q_lane], ch);
+            uint32_t basel = __shfl_sync(FULL, base, 0), baseh = __shfl_sync(FULL, base, 1);
 #pragma unroll
             for (int u = 0; u < U; u++) {
-                if (keep[u]) {
-                    const uint64_t k2 = (uint64_t)q_lane * cap + base + __popc(bal[u] & lt);
-                    cand2[k2] = pos[u];
-                    candq2[k2] = (uint8_t)b[u];
-                }
-                base += __popc(bal[u]);
+                if (keep[u] && !hi[u]) put(q_lane, basel + __popc(bl[u] & lt), false, pos[u], b[u]);
+                if (hi[u]) put(q_lane, baseh + __popc(bh[u] & lt), true, pos[u], b[u]);
+                basel += __popc(bl[u]);
+                baseh += __popc(bh[u]);
             }
         } else {
 #pragma unroll
             for (int u = 0; u < U; u++) {
-                const uint32_t peers = __match_any_sync(FULL, keep[u] ? qk[u] : 0xffffffffu);
+                const uint32_t peers = __match_any_sync(FULL, keep[u] ? 2 * qk[u] + (hi[u] ? 1u : 0u) : 0xffffffffu);
                 if (keep[u]) {
                     const uint32_t leader = __ffs(peers) - 1;
                     uint32_t base = 0;
-                    if (lane == leader) base = atomicAdd(&cand_cnt2[qk[u]], (uint32_t)__popc(peers));
+                    if (lane == leader) base = atomicAdd(hi[u] ? &cnt_hi[qk[u]] : &cand_cnt2[qk[u]], (uint32_t)__popc(peers));
                     base = __shfl_sync(peers, base, leader);
-                    const uint64_t k2 = (uint64_t)qk[u] * cap + base + __popc(peers & lt);
-                    cand2[k2] = pos[u];
-                    candq2[k2] = (uint8_t)b[u];
+                    put(qk[u], base + __popc(peers & lt), hi[u], pos[u], b[u]);
                 }
             }
         }
@@ -776,10 +809,11 @@ void launch_candcheck(const isax_index *ix, uint32_t Q, cudaStream_t s) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaMemsetAsync(qs.cand_cnt2, 0, Q * sizeof(uint32_t), s);
+    cudaMemsetAsync(qs.cnt_hi, 0, Q * sizeof(uint32_t), s);
     const unsigned grid = (unsigned)sms * 8;  // the total is only known on the device
     candcheck_kernel<<<grid, CK_THREADS, 0, s>>>(qs.cand, qs.candq, qs.cand_cnt, Q, qs.cand_cap,
                                                  reinterpret_cast<const uint4 *>(ix->sax), qs.lut, qs.qT, qs.qscale,
-                                                 qs.cand2, qs.candq2, qs.cand_cnt2);
+                                                 qs.cand2, qs.candq2, qs.cand_cnt2, qs.cnt_hi, qs.cand_hist);
 }
 
 // ------------------------------------------------------------------------------------ leaf meta

@@ -256,43 +256,99 @@ __global__ void __launch_bounds__(RF_THREADS) refine_q_kernel(const float *__res
     if (ql == 0 && rows_read) atomicAdd(refine_bytes, rows_read * 2ull * n);
 }
 
+// The second refine pass's list (MESSI's priority order, approximated by two bands):
+// candcheck_kernel puts a large query's candidates with b > B_SPLIT (LB^2 above about 0.55 T) at
+// the back of its cand2 region. After the first pass has tightened the BSF, filter_kernel keeps of
+// them only those that pass the skip test (R11b): b / sc <= LB^2, so b > lim * sc (rounded up)
+// means LB^2 > lim = bsf^2 (1 + delta), and the row can hold neither a new answer nor a near tie.
+// The survivors go to the front of the scan's own list (cand, free again) for the second pass.
+__global__ void __launch_bounds__(RF_THREADS) filter_kernel(const uint32_t *__restrict__ cand2,
+                                                           const uint8_t *__restrict__ candq2,
+                                                           const uint32_t *__restrict__ cnt_hi, uint32_t Q, uint32_t cap,
+                                                           const unsigned long long *__restrict__ bsf,
+                                                           const float *__restrict__ qscale, float onepd,
+                                                           uint32_t *__restrict__ out, uint32_t *__restrict__ cnt_f,
+                                                           uint32_t *__restrict__ counters) {
+    __shared__ uint32_t pre[RF_MAXQ + 1];
+    constexpr uint32_t FULL = 0xffffffffu;
+    const uint32_t t = threadIdx.x, lane = t & 31;
+    const uint32_t lt = (1u << lane) - 1u;
+    cand_prefix<RF_THREADS>(cnt_hi, Q, cap, pre);
+    const uint32_t total = pre[Q];
+    const uint32_t stride = gridDim.x * RF_THREADS;
+    for (uint32_t f0 = blockIdx.x * RF_THREADS + (t & ~31u); f0 < total; f0 += stride) {
+        const uint32_t f = f0 + lane;
+        const bool valid = f < total;
+        uint32_t q = 0, pos = 0;
+        bool live = false;
+        if (valid) {
+            uint32_t lo = 0, hi = Q;  // last q with pre[q] <= f
+            while (hi - lo > 1) {
+                const uint32_t mid = (lo + hi) >> 1;
+                if (pre[mid] <= f) lo = mid;
+                else hi = mid;
+            }
+            q = lo;
+            const uint64_t k = (uint64_t)q * cap + (cap - 1 - (f - pre[q]));
+            pos = cand2[k];
+            const uint32_t b = candq2[k];
+            live = !((float)b > __fmul_ru(bsf_d2(*((volatile const unsigned long long *)&bsf[q])) * onepd, qscale[q]));
+        }
+        const uint32_t peers = __match_any_sync(FULL, valid ? 2 * q + (live ? 1u : 0u) : 0xffffffffu);
+        if (valid) {
+            const uint32_t leader = __ffs(peers) - 1;
+            uint32_t base = 0;
+            if (lane == leader) base = atomicAdd(live ? &cnt_f[q] : &counters[4 * q + 2], (uint32_t)__popc(peers));
+            base = __shfl_sync(peers, base, leader);
+            if (live) out[(uint64_t)q * cap + base + __popc(peers & lt)] = pos;
+        }
+    }
+}
+
 void launch_refine(const isax_index *ix, uint32_t Q, float delta, cudaStream_t s) {
     const QueryScratch &qs = ix->qs;
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const float onepd = 1.0f + delta;
-    if (ix->n <= 256) {
-        int per_sm = 1;
-        const uint32_t nh = ix->n / 64;
-        if (nh == 4) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, refine_q_kernel<4>, RF_THREADS, 0);
-        else if (nh == 2) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, refine_q_kernel<2>, RF_THREADS, 0);
-        else per_sm = 4;
-        const unsigned grid = sms * std::max(1, per_sm);  // exactly one full wave
-        switch (nh) {
+    // pass 1: cand2[q][0 .. cand_cnt2); then the filtered second band into cand[q][0 .. cnt_f)
+    auto pass = [&](const uint32_t *list, const uint32_t *cnt) {
+        if (ix->n <= 256) {
+            int per_sm = 1;
+            const uint32_t nh = ix->n / 64;
+            if (nh == 4) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, refine_q_kernel<4>, RF_THREADS, 0);
+            else if (nh == 2) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, refine_q_kernel<2>, RF_THREADS, 0);
+            else per_sm = 4;
+            const unsigned grid = sms * std::max(1, per_sm);  // exactly one full wave
+            switch (nh) {
 #define RQ_CASE(K)                                                                                                  \
     case K:                                                                                                         \
-        refine_q_kernel<K><<<grid, RF_THREADS, 0, s>>>(ix->stored, ix->perm, ix->n, qs.qy, Q, qs.cand2, qs.candq2,   \
-                                                       qs.qscale, qs.cand_cnt2,                                      \
-                                                       qs.cand_cap, qs.bsf, qs.near, qs.near_cnt, qs.counters,      \
+        refine_q_kernel<K><<<grid, RF_THREADS, 0, s>>>(ix->stored, ix->perm, ix->n, qs.qy, Q, list, nullptr, nullptr, \
+                                                       cnt, qs.cand_cap, qs.bsf, qs.near, qs.near_cnt, qs.counters, \
                                                        onepd, qs.refine_bytes);                                     \
         break;
-            RQ_CASE(1) RQ_CASE(2) RQ_CASE(3) RQ_CASE(4)
+                RQ_CASE(1) RQ_CASE(2) RQ_CASE(3) RQ_CASE(4)
 #undef RQ_CASE
+            }
+            return;
         }
-        return;
-    }
-    const unsigned grid = sms * 8;
-    const uint32_t ns = (ix->n + 127) / 128;
+        const unsigned grid = sms * 8;
+        const uint32_t ns = (ix->n + 127) / 128;
 #define RF_CASE(K)                                                                                              \
     case K:                                                                                                     \
-        refine_kernel<K><<<grid, RF_THREADS, 0, s>>>(ix->stored, ix->perm, ix->n, qs.qy, Q, qs.cand2, qs.cand_cnt2, \
+        refine_kernel<K><<<grid, RF_THREADS, 0, s>>>(ix->stored, ix->perm, ix->n, qs.qy, Q, list, cnt,            \
                                                      qs.cand_cap, qs.bsf, qs.near, qs.near_cnt, qs.counters, onepd); \
         break;
-    switch (ns) {
-        RF_CASE(1) RF_CASE(2) RF_CASE(3) RF_CASE(4) RF_CASE(5) RF_CASE(6) RF_CASE(7) RF_CASE(8)
-    }
+        switch (ns) {
+            RF_CASE(1) RF_CASE(2) RF_CASE(3) RF_CASE(4) RF_CASE(5) RF_CASE(6) RF_CASE(7) RF_CASE(8)
+        }
 #undef RF_CASE
+    };
+    pass(qs.cand2, qs.cand_cnt2);
+    cudaMemsetAsync(qs.cnt_f, 0, Q * sizeof(uint32_t), s);
+    filter_kernel<<<sms * 4, RF_THREADS, 0, s>>>(qs.cand2, qs.candq2, qs.cnt_hi, Q, qs.cand_cap, qs.bsf, qs.qscale,
+                                                 onepd, qs.cand, qs.cnt_f, qs.counters);
+    pass(qs.cand, qs.cnt_f);
 }
 
 // ------------------------------------------------------------------------------------ finalize
