@@ -269,38 +269,84 @@ __global__ void __launch_bounds__(RF_THREADS) filter_kernel(const uint32_t *__re
                                                            const float *__restrict__ qscale, float onepd,
                                                            uint32_t *__restrict__ out, uint32_t *__restrict__ cnt_f,
                                                            uint32_t *__restrict__ counters) {
+    constexpr int U = 8;  // candidates per thread per iteration, loads in flight together
     __shared__ uint32_t pre[RF_MAXQ + 1];
     constexpr uint32_t FULL = 0xffffffffu;
     const uint32_t t = threadIdx.x, lane = t & 31;
     const uint32_t lt = (1u << lane) - 1u;
     cand_prefix<RF_THREADS>(cnt_hi, Q, cap, pre);
     const uint32_t total = pre[Q];
-    const uint32_t stride = gridDim.x * RF_THREADS;
-    for (uint32_t f0 = blockIdx.x * RF_THREADS + (t & ~31u); f0 < total; f0 += stride) {
-        const uint32_t f = f0 + lane;
-        const bool valid = f < total;
-        uint32_t q = 0, pos = 0;
-        bool live = false;
-        if (valid) {
-            uint32_t lo = 0, hi = Q;  // last q with pre[q] <= f
-            while (hi - lo > 1) {
-                const uint32_t mid = (lo + hi) >> 1;
-                if (pre[mid] <= f) lo = mid;
-                else hi = mid;
-            }
-            q = lo;
-            const uint64_t k = (uint64_t)q * cap + (cap - 1 - (f - pre[q]));
-            pos = cand2[k];
-            const uint32_t b = candq2[k];
-            live = !((float)b > __fmul_ru(bsf_d2(*((volatile const unsigned long long *)&bsf[q])) * onepd, qscale[q]));
+    // one contiguous slice per CTA (its queries change rarely)
+    const uint32_t per = (total + gridDim.x - 1) / gridDim.x;
+    const uint32_t f0 = min(blockIdx.x * per, total), f1 = min(f0 + per, total);
+    if (f0 >= f1) return;
+    uint32_t q = 0;
+    {
+        uint32_t lo = 0, hi = Q;
+        while (hi - lo > 1) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (pre[mid] <= f0) lo = mid;
+            else hi = mid;
         }
-        const uint32_t peers = __match_any_sync(FULL, valid ? 2 * q + (live ? 1u : 0u) : 0xffffffffu);
-        if (valid) {
-            const uint32_t leader = __ffs(peers) - 1;
+        q = lo;
+    }
+    for (uint32_t fb = f0; fb < f1; fb += U * RF_THREADS) {
+        uint32_t qk[U], pos[U];
+        bool valid[U], live[U];
+        float thr[U];
+        bool one_q = true;
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const uint32_t f = fb + u * RF_THREADS + t;
+            valid[u] = f < f1;
+            if (valid[u])
+                while (pre[q + 1] <= f) q++;
+            qk[u] = q;
+            one_q &= !valid[u] || q == qk[0];
+            const uint64_t k = (uint64_t)q * cap + (cap - 1 - (f - pre[q]));
+            pos[u] = valid[u] ? cand2[k] : 0u;
+            thr[u] = valid[u] ? (float)candq2[k] : 0.f;
+        }
+        // the skip test against the BSF as it stands now (read once per lane)
+        const float lim = bsf_d2(*((volatile const unsigned long long *)&bsf[qk[0]])) * onepd;
+        const float scq = qscale[qk[0]];
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const float l = qk[u] == qk[0] ? lim : bsf_d2(*((volatile const unsigned long long *)&bsf[qk[u]])) * onepd;
+            const float sc = qk[u] == qk[0] ? scq : qscale[qk[u]];
+            live[u] = valid[u] && !(thr[u] > __fmul_ru(l, sc));
+        }
+        const uint32_t q_w = __shfl_sync(FULL, qk[0], 0);  // (every lane shuffles: no short circuit)
+        if (__all_sync(FULL, one_q && qk[0] == q_w)) {
+            uint32_t bl[U], cl = 0, cs = 0;
+#pragma unroll
+            for (int u = 0; u < U; u++) {
+                bl[u] = __ballot_sync(FULL, live[u]);
+                cl += __popc(bl[u]);
+                cs += __popc(__ballot_sync(FULL, valid[u] && !live[u]));
+            }
             uint32_t base = 0;
-            if (lane == leader) base = atomicAdd(live ? &cnt_f[q] : &counters[4 * q + 2], (uint32_t)__popc(peers));
-            base = __shfl_sync(peers, base, leader);
-            if (live) out[(uint64_t)q * cap + base + __popc(peers & lt)] = pos;
+            if (lane == 0 && cl) base = atomicAdd(&cnt_f[q_w], cl);
+            if (lane == 1 && cs) atomicAdd(&counters[4 * q_w + 2], cs);
+            base = __shfl_sync(FULL, base, 0);
+#pragma unroll
+            for (int u = 0; u < U; u++) {
+                if (live[u]) out[(uint64_t)q_w * cap + base + __popc(bl[u] & lt)] = pos[u];
+                base += __popc(bl[u]);
+            }
+        } else {
+#pragma unroll
+            for (int u = 0; u < U; u++) {
+                const uint32_t peers = __match_any_sync(FULL, valid[u] ? 2 * qk[u] + (live[u] ? 1u : 0u) : 0xffffffffu);
+                if (valid[u]) {
+                    const uint32_t leader = __ffs(peers) - 1;
+                    uint32_t base = 0;
+                    if (lane == leader)
+                        base = atomicAdd(live[u] ? &cnt_f[qk[u]] : &counters[4 * qk[u] + 2], (uint32_t)__popc(peers));
+                    base = __shfl_sync(peers, base, leader);
+                    if (live[u]) out[(uint64_t)qk[u] * cap + base + __popc(peers & lt)] = pos[u];
+                }
+            }
         }
     }
 }
