@@ -77,10 +77,10 @@ static cudaError_t dmalloc(T **p, size_t count, size_t *acc) {
 
 static void free_scratch(isax_index *ix) {
     QueryScratch &q = ix->qs;
-    cudaFree(q.qy); cudaFree(q.qpaa); cudaFree(q.qsax); cudaFree(q.lut); cudaFree(q.lut8); cudaFree(q.qconst); cudaFree(q.win); cudaFree(q.pwin); cudaFree(q.bsf);
-    cudaFree(q.cand); cudaFree(q.candq); cudaFree(q.cand2); cudaFree(q.candq2); cudaFree(q.cand_cnt2); cudaFree(q.cnt_hi); cudaFree(q.cnt_f); cudaFree(q.qscale); cudaFree(q.qT); cudaFree(q.cand_cnt); cudaFree(q.near); cudaFree(q.near_cnt); cudaFree(q.qmap); cudaFree(q.qband); cudaFree(q.cand_hist);
-    cudaFree(q.counters); cudaFree(q.counters_leaf); cudaFree(q.scan_bytes_dev); cudaFree(q.task_ctr); cudaFree(q.refine_bytes);
-    cudaFree(q.flag); cudaFree(q.qmap2);
+    cudaFree(q.qy); cudaFree(q.qpaa); cudaFree(q.qsax); cudaFree(q.lut); cudaFree(q.lut8); cudaFree(q.qconst); cudaFree(q.pwin);
+    cudaFree(q.cand); cudaFree(q.candq); cudaFree(q.cand2); cudaFree(q.candq2); cudaFree(q.cnt_f); cudaFree(q.qscale); cudaFree(q.qT);
+    cudaFree(q.near); cudaFree(q.qmap); cudaFree(q.qband); cudaFree(q.cand_hist); cudaFree(q.task_ctr); cudaFree(q.qmap2);
+    cudaFree(q.status);  // bsf, bsf_scan, cand_cnt, cand_cnt2, cnt_hi, near_cnt, flag, counters, win, leaves, byte counters
     if (q.h_mirror) cudaFreeHost(q.h_mirror);
     q = QueryScratch{};
 }
@@ -114,32 +114,41 @@ static int alloc_scratch_cap(isax_index *ix, uint32_t cap) {
     A(lut, (size_t)Q * W * CARD);
     A(lut8, (size_t)Q * W * CARD);
     A(qconst, Q);
-    A(win, (size_t)Q * 2);
     A(pwin, (size_t)Q * (MAX_PROBES - 1));
-    A(bsf, Q);
     A(cand, (size_t)Q * cap);
     A(candq, (size_t)Q * cap);
     A(cand2, (size_t)Q * cap);
     A(candq2, (size_t)Q * cap);
-    A(cand_cnt2, Q);
-    A(cnt_hi, Q);
     A(cnt_f, Q);
     A(qscale, Q);
     A(qT, Q);
-    A(cand_cnt, Q);
     A(near, (size_t)Q * NEAR_K);
-    A(near_cnt, Q);
     A(qmap, Q);
     A(qband, Q);
     A(cand_hist, (size_t)Q * HIST_BINS);
-    A(counters, (size_t)Q * 4);
-    A(counters_leaf, Q);
-    A(scan_bytes_dev, 1);
     A(task_ctr, 1);
-    A(refine_bytes, 1);
-    A(flag, 1);
     A(qmap2, Q);
 #undef A
+    if (e == cudaSuccess) {
+        e = cudaMalloc(&q.status, StatusBlock::bytes(Q));
+        if (e == cudaSuccess) {
+            acc += StatusBlock::bytes(Q);
+            StatusBlock sb;
+            sb.carve(q.status, Q);
+            q.bsf = sb.bsf;
+            q.bsf_scan = sb.bsf_scan;
+            q.scan_bytes_dev = sb.scan_bytes_dev;
+            q.refine_bytes = sb.refine_bytes;
+            q.cand_cnt = sb.cand_cnt;
+            q.cand_cnt2 = sb.cand_cnt2;
+            q.cnt_hi = sb.cnt_hi;
+            q.near_cnt = sb.near_cnt;
+            q.flag = sb.flag;
+            q.counters = sb.counters;
+            q.win = sb.win;
+            q.counters_leaf = sb.leaves;
+        }
+    }
     if (e == cudaSuccess) e = cudaMallocHost(&q.h_mirror, HostMirror::bytes(Q));
     if (e == cudaSuccess) q.hm.carve(q.h_mirror, Q);
     if (e != cudaSuccess) {
@@ -298,20 +307,16 @@ static int nn1_device(isax_index *ix, const float *d_q, uint32_t Q, int64_t *d_i
     ix->st_launches = 0;
     ix->st_scan_bytes = ix->st_scan_bytes_first = 0;
     ix->st_refine_bytes_first = 0;
-    ISAX_CUDA(cudaMemsetAsync(qs.scan_bytes_dev, 0, sizeof(unsigned long long), s));
-    ISAX_CUDA(cudaMemsetAsync(qs.refine_bytes, 0, sizeof(unsigned long long), s));
-    ISAX_CUDA(cudaMemsetAsync(qs.flag, 0, sizeof(uint32_t), s));
+    ISAX_CUDA(cudaMemsetAsync(qs.scan_bytes_dev, 0, StatusBlock::RESET_BYTES, s));  // + refine_bytes, flag
     int result = ISAX_OK;
     for (uint32_t b0 = 0; b0 < Q && result == ISAX_OK; b0 += qs.cap_Q) {
         const uint32_t B = std::min(qs.cap_Q, Q - b0);
         const bool timed = b0 == 0;
         if (timed) cudaEventRecord(ix->ev[0], s);
         launch_qprep(ix, d_q + (uint64_t)b0 * ix->n, B, s, qs.flag);
-        ISAX_CUDA(cudaMemsetAsync(qs.counters_leaf, 0, B * sizeof(uint32_t), s));
         ix->st_launches += 2;
         if (timed) cudaEventRecord(ix->ev[1], s);
         launch_window(ix, B, nullptr, delta, s);
-        ISAX_CUDA(cudaMemcpyAsync(hm.bsf0, qs.bsf, B * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
         if (timed) cudaEventRecord(ix->ev[2], s);
         // Rounds (R10). Round 0 scans the band (-1, +inf) for every query, i.e. everything
         // under the window BSF. If a query's candidate list overflows, its band is shrunk to the
@@ -325,7 +330,7 @@ static int nn1_device(isax_index *ix, const float *d_q, uint32_t Q, int64_t *d_i
         // copies are enqueued before it; they are redone only if another round follows.
         std::vector<float2> band(B, make_float2(-1.0f, INF));
         std::vector<char> pending(B, 1);
-        std::vector<float> bsf_h(B, INF), tused(B, -1.0f);
+        std::vector<float> bsf_h(B, INF), tused(B, -1.0f), bsf0_h(B, INF);
         std::vector<uint32_t> hist((size_t)B * HIST_BINS);
         std::vector<uint32_t> rewin;
         for (uint32_t round = 0;; round++) {
@@ -339,9 +344,9 @@ static int nn1_device(isax_index *ix, const float *d_q, uint32_t Q, int64_t *d_i
                 nact++;
             }
             if (!nact) break;
-            ISAX_CUDA(cudaMemsetAsync(qs.cand_hist, 0, (size_t)B * HIST_BINS * sizeof(uint32_t), s));
+            // (scanprep_kernel zeroes the candidate counts of all B slots and the scanned queries'
+            // histograms)
             if (round > 0) {
-                ISAX_CUDA(cudaMemsetAsync(qs.cand_cnt, 0, B * sizeof(uint32_t), s));
                 if (!rewin.empty()) {
                     for (uint32_t i : rewin) ISAX_CUDA(cudaMemsetAsync(qs.near_cnt + i, 0, sizeof(uint32_t), s));
                     memcpy(hm.rewin, rewin.data(), rewin.size() * sizeof(uint32_t));
@@ -354,7 +359,7 @@ static int nn1_device(isax_index *ix, const float *d_q, uint32_t Q, int64_t *d_i
             }
             ISAX_CUDA(cudaMemcpyAsync(qs.qmap, hm.qmap, nact * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
             ISAX_CUDA(cudaMemcpyAsync(qs.qband, hm.band, nact * sizeof(float2), cudaMemcpyHostToDevice, s));
-            ix->st_scan_bytes += launch_lbscan(ix, nact, qs.qmap, qs.qband, delta, s);
+            ix->st_scan_bytes += launch_lbscan(ix, nact, B, qs.qmap, qs.qband, delta, s);
             if (timed && round == 0) cudaEventRecord(ix->ev[6], s);
             launch_candcheck(ix, B, s);
             if (timed && round == 0) cudaEventRecord(ix->ev[3], s);
@@ -365,17 +370,8 @@ static int nn1_device(isax_index *ix, const float *d_q, uint32_t Q, int64_t *d_i
             ix->st_launches += ((ix->opts.flags & ISAX_FLAG_FLAT_SCAN) ? 1 : 2) + 5;
             if (timed && round == 0) cudaEventRecord(ix->ev[5], s);
             ISAX_CUDA(cudaGetLastError());
-            ISAX_CUDA(cudaMemcpyAsync(hm.cand_cnt, qs.cand_cnt, B * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
-            ISAX_CUDA(cudaMemcpyAsync(hm.cand_cnt2, qs.cand_cnt2, B * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
-            ISAX_CUDA(cudaMemcpyAsync(hm.cnt_hi, qs.cnt_hi, B * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
-            ISAX_CUDA(cudaMemcpyAsync(hm.near_cnt, qs.near_cnt, B * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
-            ISAX_CUDA(cudaMemcpyAsync(hm.flag, qs.flag, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
-            ISAX_CUDA(cudaMemcpyAsync(hm.bsf, qs.bsf, B * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
-            ISAX_CUDA(cudaMemcpyAsync(hm.counters, qs.counters, (size_t)B * 4 * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
-            ISAX_CUDA(cudaMemcpyAsync(hm.win, qs.win, (size_t)B * 2 * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
-            ISAX_CUDA(cudaMemcpyAsync(hm.leaves, qs.counters_leaf, B * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
-            ISAX_CUDA(cudaMemcpyAsync(hm.scan_bytes_dev, qs.scan_bytes_dev, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
-            ISAX_CUDA(cudaMemcpyAsync(hm.refine_bytes, qs.refine_bytes, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+            // the whole status block in one copy (StatusBlock: bsf, counters, flags, byte counts)
+            ISAX_CUDA(cudaMemcpyAsync(hm.status, qs.status, StatusBlock::bytes(qs.cap_Q), cudaMemcpyDeviceToHost, s));
             ISAX_CUDA(cudaStreamSynchronize(s));
             if (*hm.flag) {
                 result = set_error(ISAX_E_NONFINITE, "a query holds NaN or Inf");
@@ -383,7 +379,8 @@ static int nn1_device(isax_index *ix, const float *d_q, uint32_t Q, int64_t *d_i
             }
             if (round == 0) {  // the window BSF: the threshold round 0 used
                 for (uint32_t i = 0; i < B; i++) {
-                    bsf_h[i] = bsf_d2_host(hm.bsf0[i]);
+                    bsf_h[i] = bsf_d2_host(hm.bsf_scan[i]);
+                    bsf0_h[i] = bsf_h[i];
                     tused[i] = bsf_h[i] * onepd;
                 }
                 if (b0 == 0) {
@@ -438,7 +435,7 @@ static int nn1_device(isax_index *ix, const float *d_q, uint32_t Q, int64_t *d_i
             ix->st_skipped[b0 + i] = hm.counters[4 * i + 2];
             ix->st_near[b0 + i] = hm.near_cnt[i];
             ix->st_leaves[b0 + i] = hm.leaves[i];
-            ix->st_bsf0[b0 + i] = bsf_d2_host(hm.bsf0[i]);
+            ix->st_bsf0[b0 + i] = bsf0_h[i];
             ix->st_bsf_final[b0 + i] = bsf_d2_host(hm.bsf[i]);
             ix->st_win[2 * (b0 + i)] = hm.win[2 * i];
             ix->st_win[2 * (b0 + i) + 1] = hm.win[2 * i + 1];

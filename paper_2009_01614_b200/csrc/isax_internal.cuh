@@ -47,28 +47,43 @@ struct NearEntry {  // a completed refinement within (1+delta) of the BSF at tha
     uint32_t pad;
 };
 
-// Pinned host mirror of the per-batch counters (one async copy each per round, one sync).
-struct HostMirror {
-    uint32_t *cand_cnt, *cand_cnt2, *cnt_hi, *near_cnt, *flag, *counters, *win, *leaves, *qmap, *rewin;
-    unsigned long long *bsf, *bsf0, *scan_bytes_dev, *refine_bytes;
-    float2 *band;
-    static size_t bytes(uint32_t Q) { return (size_t)Q * (8 * 4 + 4 * 4 + 2 * 4 + 8 * 2 + 16) + 512; }
+// The per-batch status the host reads after every round: one contiguous block on the device and
+// the same layout in pinned host memory, so a round ends with a single D2H copy.
+struct StatusBlock {
+    static constexpr size_t RESET_BYTES = 48;  // scan_bytes_dev, refine_bytes, flag (16-B slots)
+    unsigned long long *bsf, *bsf_scan, *scan_bytes_dev, *refine_bytes;
+    uint32_t *cand_cnt, *cand_cnt2, *cnt_hi, *near_cnt, *flag, *counters, *win, *leaves;
+    static size_t bytes(uint32_t Q) { return (size_t)Q * (8 + 8 + 4 * 4 + 16 + 8 + 4) + 16 * 16; }
     void carve(void *base, uint32_t Q) {
         unsigned char *p = static_cast<unsigned char *>(base);
         auto take = [&](size_t n) { unsigned char *r = p; p += (n + 15) & ~size_t(15); return r; };
         bsf = reinterpret_cast<unsigned long long *>(take(8ull * Q));
-        bsf0 = reinterpret_cast<unsigned long long *>(take(8ull * Q));
-        scan_bytes_dev = reinterpret_cast<unsigned long long *>(take(8));
-        refine_bytes = reinterpret_cast<unsigned long long *>(take(8));
-        band = reinterpret_cast<float2 *>(take(8ull * Q));
+        bsf_scan = reinterpret_cast<unsigned long long *>(take(8ull * Q));
+        scan_bytes_dev = reinterpret_cast<unsigned long long *>(take(8));  // these three are zeroed
+        refine_bytes = reinterpret_cast<unsigned long long *>(take(8));    // together: RESET_BYTES
+        flag = reinterpret_cast<uint32_t *>(take(4));
         cand_cnt = reinterpret_cast<uint32_t *>(take(4ull * Q));
         cand_cnt2 = reinterpret_cast<uint32_t *>(take(4ull * Q));
         cnt_hi = reinterpret_cast<uint32_t *>(take(4ull * Q));
         near_cnt = reinterpret_cast<uint32_t *>(take(4ull * Q));
-        flag = reinterpret_cast<uint32_t *>(take(4));
         counters = reinterpret_cast<uint32_t *>(take(16ull * Q));
         win = reinterpret_cast<uint32_t *>(take(8ull * Q));
         leaves = reinterpret_cast<uint32_t *>(take(4ull * Q));
+    }
+};
+
+// Pinned host memory: the status mirror plus the per-round inputs the host writes.
+struct HostMirror : StatusBlock {
+    void *status = nullptr;
+    uint32_t *qmap, *rewin;
+    float2 *band;
+    static size_t bytes(uint32_t Q) { return StatusBlock::bytes(Q) + (size_t)Q * (4 + 4 + 8) + 3 * 16; }
+    void carve(void *base, uint32_t Q) {
+        status = base;
+        StatusBlock::carve(base, Q);
+        unsigned char *p = static_cast<unsigned char *>(base) + StatusBlock::bytes(Q);
+        auto take = [&](size_t n) { unsigned char *r = p; p += (n + 15) & ~size_t(15); return r; };
+        band = reinterpret_cast<float2 *>(take(8ull * Q));
         qmap = reinterpret_cast<uint32_t *>(take(4ull * Q));
         rewin = reinterpret_cast<uint32_t *>(take(4ull * Q));
     }
@@ -109,6 +124,8 @@ struct QueryScratch {
     uint32_t *task_ctr = nullptr;              // work counter of the persistent leaf scan
     unsigned long long *refine_bytes = nullptr;  // bytes of rows the refine kernel read (all launches of a call)
     uint32_t *flag = nullptr;       // non-finite query flag
+    void *status = nullptr;         // the device StatusBlock (bsf, bsf_scan, counters, ... point into it)
+    unsigned long long *bsf_scan = nullptr;  // [Q] the BSF each query's last scan used (the window BSF in round 0)
     uint32_t *qmap2 = nullptr;      // [Q] slots whose window is re-refined
     void *h_mirror = nullptr;       // pinned host memory of hm
     HostMirror hm{};
@@ -193,8 +210,8 @@ void launch_leaf_meta(const uint8_t *sax, uint64_t N, uint8_t *lmeta, uint8_t *s
 // Scan all sorted positions for the nq queries qmap[0..nq), keeping band[i].x < LB^2 <= min(band[i].y,
 // bsf^2 (1+delta)) for slot i. Returns the summary bytes it reads that the host can count (node
 // summaries or flat words); the leaf scan adds its leaf-word and leaf-summary bytes to qs.scan_bytes_dev on the device.
-uint64_t launch_lbscan(const isax_index *ix, uint32_t nq, const uint32_t *qmap, const float2 *band, float delta,
-                       cudaStream_t s);
+uint64_t launch_lbscan(const isax_index *ix, uint32_t nq, uint32_t B, const uint32_t *qmap, const float2 *band,
+                       float delta, cudaStream_t s);
 // lbscan.cu: the exact fp32 rule for the candidates the leaf scan kept on their u8 sum alone,
 // and compaction of every list into cand2 / cand_cnt2 (the refine's input)
 void launch_candcheck(const isax_index *ix, uint32_t Q, cudaStream_t s);

@@ -309,8 +309,19 @@ __global__ void __launch_bounds__(256) scanprep_kernel(const float *__restrict__
                                                        const unsigned long long *__restrict__ bsf,
                                                        const uint32_t *__restrict__ win, float onepd,
                                                        uint8_t *__restrict__ lut8, uint4 *__restrict__ qconst,
-                                                       float *__restrict__ qscale, float *__restrict__ qT) {
+                                                       float *__restrict__ qscale, float *__restrict__ qT,
+                                                       unsigned long long *__restrict__ bsf_scan, uint32_t B,
+                                                       uint32_t *__restrict__ cand_cnt, uint32_t *__restrict__ cand_cnt2,
+                                                       uint32_t *__restrict__ cnt_hi, uint32_t *__restrict__ cnt_f,
+                                                       uint32_t *__restrict__ hist, uint32_t *__restrict__ task_ctr) {
     const uint32_t i = blockIdx.x;
+    // the launch's counters: every batch slot's candidate counts (block 0), the scanned query's
+    // histogram (its block), the persistent scan's task counter
+    if (i == 0) {
+        for (uint32_t q = threadIdx.x; q < B; q += blockDim.x) cand_cnt[q] = cand_cnt2[q] = cnt_hi[q] = cnt_f[q] = 0;
+        if (threadIdx.x == 0) *task_ctr = 0;
+    }
+    if (threadIdx.x < HIST_BINS) hist[qmap[i] * HIST_BINS + threadIdx.x] = 0;
     const uint32_t qi = qmap[i];
     const QConst k = load_qconst(qi, true, bsf, band, i, win, onepd);
     if (threadIdx.x == 0) qconst[i] = make_uint4(__float_as_uint(k.lo), __float_as_uint(k.T), k.ws, k.we);
@@ -319,6 +330,7 @@ __global__ void __launch_bounds__(256) scanprep_kernel(const float *__restrict__
     if (threadIdx.x == 0) {
         qscale[qi] = sc;
         qT[qi] = k.T;
+        bsf_scan[qi] = bsf[qi];
     }
     const float4 *L = reinterpret_cast<const float4 *>(lut_all + (uint64_t)qi * W * CARD);
     uint32_t *o = reinterpret_cast<uint32_t *>(lut8 + (uint64_t)i * W * CARD);
@@ -621,19 +633,19 @@ static void launch_leaf(const isax_index *ix, uint32_t nq, const uint32_t *qmap,
     const uint64_t tasks = (uint64_t)groups * ((nleaf + chunk - 1) / chunk);
     const unsigned grid = (unsigned)std::max<uint64_t>(1, umin64(tasks, (uint64_t)sms));
     const QueryScratch &qs = ix->qs;
-    cudaMemsetAsync(qs.task_ctr, 0, sizeof(uint32_t), s);
     leafscan_kernel<G><<<grid, LF_THREADS, smem, s>>>(
         reinterpret_cast<const uint4 *>(ix->sax), ix->lmeta, ix->smeta, ix->hmeta, (uint32_t)ix->N, qs.lut, qs.lut8, qs.qconst,
         qs.qsax, qmap, nq, nleaf, chunk, qs.cand, qs.candq, qs.cand_cnt, qs.cand_cap, qs.cand_hist, qs.counters_leaf,
         qs.scan_bytes_dev, qs.task_ctr);
 }
 
-uint64_t launch_lbscan(const isax_index *ix, uint32_t nq, const uint32_t *qmap, const float2 *band, float delta,
-                       cudaStream_t s) {
+uint64_t launch_lbscan(const isax_index *ix, uint32_t nq, uint32_t B, const uint32_t *qmap, const float2 *band,
+                       float delta, cudaStream_t s) {
     if (!nq) return 0;
     const float onepd = 1.0f + delta;
     const QueryScratch &qs = ix->qs;
-    scanprep_kernel<<<nq, 256, 0, s>>>(qs.lut, qmap, band, qs.bsf, qs.win, onepd, qs.lut8, qs.qconst, qs.qscale, qs.qT);
+    scanprep_kernel<<<nq, 256, 0, s>>>(qs.lut, qmap, band, qs.bsf, qs.win, onepd, qs.lut8, qs.qconst, qs.qscale, qs.qT, qs.bsf_scan,
+                                      B, qs.cand_cnt, qs.cand_cnt2, qs.cnt_hi, qs.cnt_f, qs.cand_hist, qs.task_ctr);
     if (ix->opts.flags & ISAX_FLAG_FLAT_SCAN) {  // ParIS flat scan, kept for A/B measurement
         const uint32_t G = nq >= 4 ? 4 : nq;
         if (G == 4) launch_g<4>(ix, nq, qmap, band, onepd, s);
@@ -808,8 +820,6 @@ void launch_candcheck(const isax_index *ix, uint32_t Q, cudaStream_t s) {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaMemsetAsync(qs.cand_cnt2, 0, Q * sizeof(uint32_t), s);
-    cudaMemsetAsync(qs.cnt_hi, 0, Q * sizeof(uint32_t), s);
     const unsigned grid = (unsigned)sms * 8;  // the total is only known on the device
     candcheck_kernel<<<grid, CK_THREADS, 0, s>>>(qs.cand, qs.candq, qs.cand_cnt, Q, qs.cand_cap,
                                                  reinterpret_cast<const uint4 *>(ix->sax), qs.lut, qs.qT, qs.qscale,

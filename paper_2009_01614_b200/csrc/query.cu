@@ -30,7 +30,8 @@ __global__ void __launch_bounds__(256) qprep_kernel(const float *__restrict__ qu
                                                     uint8_t *__restrict__ qsax, float *__restrict__ lut,
                                                     uint32_t *__restrict__ win, unsigned long long *__restrict__ bsf,
                                                     uint32_t *__restrict__ cand_cnt, uint32_t *__restrict__ near_cnt,
-                                                    uint32_t *__restrict__ counters, uint32_t *__restrict__ bad) {
+                                                    uint32_t *__restrict__ counters, uint32_t *__restrict__ counters_leaf,
+                                                    uint32_t *__restrict__ bad) {
     __shared__ float row[1024];
     __shared__ double beta[ISAX_NBETA];
     __shared__ double m[W];
@@ -60,6 +61,7 @@ __global__ void __launch_bounds__(256) qprep_kernel(const float *__restrict__ qu
         cand_cnt[q] = 0;
         near_cnt[q] = 0;
         counters[4 * q + 0] = counters[4 * q + 1] = counters[4 * q + 2] = counters[4 * q + 3] = 0;
+        counters_leaf[q] = 0;
         bsf[q] = ~0ull;
     }
     __syncthreads();
@@ -166,7 +168,7 @@ void launch_qprep(const isax_index *ix, const float *queries, uint32_t Q, cudaSt
     const QueryScratch &qs = ix->qs;
     qprep_kernel<<<Q, 256, 0, s>>>(queries, ix->n, reinterpret_cast<const uint4 *>(ix->sax), ix->N,
                                    ix->opts.window_L, probe_bits(ix), ix->opts.probe_L, qs.pwin, qs.qy, qs.qpaa, qs.qsax, qs.lut, qs.win, qs.bsf, qs.cand_cnt,
-                                   qs.near_cnt, qs.counters, bad);
+                                   qs.near_cnt, qs.counters, qs.counters_leaf, bad);
 }
 
 // ------------------------------------------------------------------------------------ window

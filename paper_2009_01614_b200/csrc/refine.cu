@@ -391,7 +391,6 @@ void launch_refine(const isax_index *ix, uint32_t Q, float delta, cudaStream_t s
 #undef RF_CASE
     };
     pass(qs.cand2, qs.cand_cnt2);
-    cudaMemsetAsync(qs.cnt_f, 0, Q * sizeof(uint32_t), s);
     filter_kernel<<<sms * 4, RF_THREADS, 0, s>>>(qs.cand2, qs.candq2, qs.cnt_hi, Q, qs.cand_cap, qs.bsf, qs.qscale,
                                                  onepd, qs.cand, qs.cnt_f, qs.counters);
     pass(qs.cand, qs.cnt_f);
