@@ -60,6 +60,11 @@ typedef struct isax_opts {
  * this exists for A/B measurement. */
 #define ISAX_FLAG_FLAT_SCAN 1u
 
+/* opts.flags: refine the first band's candidates inside the leaf scan kernel (MESSI's workers
+ * compute real distances and update the BSF during the traversal), instead of after
+ * it from global candidate lists. The answers are identical; n must be 128 or 256. */
+#define ISAX_FLAG_FUSED_REFINE 2u
+
 typedef struct isax_index isax_index; /* opaque; owns all of its device memory */
 
 /* Fill callback for isax_build_stream. It writes `count` raw series (ids first_id ..

@@ -62,7 +62,7 @@ static int check_geometry(uint64_t N, uint32_t n, uint32_t w, uint32_t card, con
     if (o.window_L == 0 || o.window_L > 4096) return set_error(ISAX_E_INVAL, "window_L must be in [1, 4096]");
     if (o.slack_log2 > -8 || o.slack_log2 < -20) return set_error(ISAX_E_INVAL, "slack_log2 must be in [-20, -8]");
     if (o.batch_Q > 1024) return set_error(ISAX_E_INVAL, "batch_Q must be <= 1024");
-    if (o.flags & ~ISAX_FLAG_FLAT_SCAN) return set_error(ISAX_E_INVAL, "unknown flags");
+    if (o.flags & ~(ISAX_FLAG_FLAT_SCAN | ISAX_FLAG_FUSED_REFINE)) return set_error(ISAX_E_INVAL, "unknown flags");
     if (o.probe_bits != ISAX_PROBES_NONE && o.probe_bits > 5) return set_error(ISAX_E_INVAL, "probe_bits must be <= 5");
     if (o.probe_L == 0 || o.probe_L > 1024) return set_error(ISAX_E_INVAL, "probe_L must be in [1, 1024]");
     return ISAX_OK;
@@ -245,7 +245,11 @@ static int build_impl(const Source &src, uint64_t N, uint32_t n, uint32_t w, uin
     keys = nullptr;
     cudaFree(ids);
     ids = nullptr;
-    TRY(dmalloc(&ix->sax, N * W, &ix->device_bytes));
+    // padded to whole leaves: the leaf scan loads a partial last leaf's words unconditionally
+    // (the padding is never a candidate: positions >= N are rejected before any emit)
+    const uint64_t npad = ((N + LEAF_SIZE - 1) / LEAF_SIZE) * LEAF_SIZE;
+    TRY(dmalloc(&ix->sax, npad * W, &ix->device_bytes));
+    TRY(cudaMemsetAsync(ix->sax + N * W, 0xFF, (npad - N) * W, s));
     launch_gather_sax(sax_by_id, ix->perm, N, ix->sax, s);
     TRY(dmalloc(&ix->lmeta, ((N + LEAF_SIZE - 1) / LEAF_SIZE) * 32, &ix->device_bytes));
     TRY(dmalloc(&ix->smeta, ((N + SUPER_SIZE - 1) / SUPER_SIZE) * 32, &ix->device_bytes));
@@ -309,6 +313,8 @@ static int nn1_device(isax_index *ix, const float *d_q, uint32_t Q, int64_t *d_i
     ix->st_refine_bytes_first = 0;
     ISAX_CUDA(cudaMemsetAsync(qs.scan_bytes_dev, 0, StatusBlock::RESET_BYTES, s));  // + refine_bytes, flag
     int result = ISAX_OK;
+    const bool fused_ok = (ix->opts.flags & ISAX_FLAG_FUSED_REFINE) && !(ix->opts.flags & ISAX_FLAG_FLAT_SCAN) &&
+                          (ix->n == 128 || ix->n == 256);
     for (uint32_t b0 = 0; b0 < Q && result == ISAX_OK; b0 += qs.cap_Q) {
         const uint32_t B = std::min(qs.cap_Q, Q - b0);
         const bool timed = b0 == 0;
@@ -359,15 +365,17 @@ static int nn1_device(isax_index *ix, const float *d_q, uint32_t Q, int64_t *d_i
             }
             ISAX_CUDA(cudaMemcpyAsync(qs.qmap, hm.qmap, nact * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
             ISAX_CUDA(cudaMemcpyAsync(qs.qband, hm.band, nact * sizeof(float2), cudaMemcpyHostToDevice, s));
-            ix->st_scan_bytes += launch_lbscan(ix, nact, B, qs.qmap, qs.qband, delta, s);
+            // round 0 of the leaf scan may refine inside the scan kernel (ISAX_FLAG_FUSED_REFINE)
+            const bool fused = round == 0 && fused_ok;
+            ix->st_scan_bytes += launch_lbscan(ix, nact, B, qs.qmap, qs.qband, delta, fused, s);
             if (timed && round == 0) cudaEventRecord(ix->ev[6], s);
-            launch_candcheck(ix, B, s);
+            if (!fused) launch_candcheck(ix, B, s);
             if (timed && round == 0) cudaEventRecord(ix->ev[3], s);
-            launch_refine(ix, B, delta, s);
+            if (!fused) launch_refine(ix, B, delta, s);
             if (timed && round == 0) cudaEventRecord(ix->ev[4], s);
             launch_finalize(ix, B, delta, d_id + b0, d_dist + b0, s);  // speculative: redone after another round
             // scanprep + scan, candcheck, refine + filter + refine, finalize
-            ix->st_launches += ((ix->opts.flags & ISAX_FLAG_FLAT_SCAN) ? 1 : 2) + 5;
+            ix->st_launches += ((ix->opts.flags & ISAX_FLAG_FLAT_SCAN) ? 1 : 2) + (fused ? 1 : 5);
             if (timed && round == 0) cudaEventRecord(ix->ev[5], s);
             ISAX_CUDA(cudaGetLastError());
             // the whole status block in one copy (StatusBlock: bsf, counters, flags, byte counts)
@@ -399,7 +407,8 @@ static int nn1_device(isax_index *ix, const float *d_q, uint32_t Q, int64_t *d_i
                 const uint32_t i = hm.qmap[k];
                 const uint32_t cnt = hm.cand_cnt[i];
                 bsf_h[i] = bsf_d2_host(hm.bsf[i]);
-                ix->st_cand[b0 + i] += hm.cand_cnt2[i] + hm.cnt_hi[i];  // after the exact rule (candcheck_kernel)
+                // after the exact rule (candcheck_kernel); fused: counted by the refinement warps
+                ix->st_cand[b0 + i] += hm.cand_cnt2[i] + hm.cnt_hi[i] + (round == 0 && fused_ok ? hm.counters[4 * i + 3] : 0);
                 ix->st_rounds[b0 + i] = round + 1;
                 if (hm.near_cnt[i] > (uint32_t)NEAR_K) {  // near overflow: start over, BSF kept
                     band[i] = make_float2(-1.0f, INF);

@@ -13,7 +13,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libisax.so")
+# ISAX_LIB: an alternative build of the same library (A/B measurement of kernel variants)
+LIB_PATH = os.environ.get("ISAX_LIB") or os.path.join(_HERE, "libisax.so")
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is missing. Build it with `python -m paper_2009_01614_b200.build`; "
                       "there is no CPU fallback.")
