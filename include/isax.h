@@ -43,9 +43,10 @@ enum {
 typedef struct isax_opts {
     uint32_t window_L;   /* leaf-sized window of the approximate answer (R5). Default 1024. */
     int32_t slack_log2;  /* prune/abandon slack delta = 2^slack_log2 (R8). Default -12. */
-    uint32_t batch_Q;    /* queries processed per device batch. Default 128. */
-    uint32_t cand_cap;   /* candidate-list capacity per query per round. 0 = default: min(N, 2^23), halved while the
-                            query scratch (about 10 B x batch_Q x cand_cap) does not fit. Overflow runs more rounds. */
+    uint32_t batch_Q;    /* queries processed per device batch (<= 1024). Default 1024. */
+    uint32_t cand_cap;   /* candidate-list capacity per query per round. 0 = default: a pool of 2^30 entries (about
+                            10 B each; halved while it does not fit) split over the queries of each batch, at most
+                            min(N, 2^23) per query. Overflow runs more rounds (R10). */
     uint32_t flags;      /* ISAX_FLAG_* bits; 0 = defaults */
     uint32_t probe_bits; /* multi-probe approximate answer (R5): refine extra windows at the 2^probe_bits - 1 keys
                             obtained by flipping the most fragile plane-0/1 key bits. 0 = default 4; max 5;
@@ -59,11 +60,6 @@ typedef struct isax_opts {
  * of the default leaf-pruned scan (MESSI's node pruning). The answers are identical;
  * this exists for A/B measurement. */
 #define ISAX_FLAG_FLAT_SCAN 1u
-
-/* opts.flags: refine the first band's candidates inside the leaf scan kernel (MESSI's workers
- * compute real distances and update the BSF during the traversal), instead of after
- * it from global candidate lists. The answers are identical; n must be 128 or 256. */
-#define ISAX_FLAG_FUSED_REFINE 2u
 
 typedef struct isax_index isax_index; /* opaque; owns all of its device memory */
 

@@ -38,7 +38,7 @@ static bool is_device_ptr(const void *p) {
 }
 
 static isax_opts default_opts(const isax_opts *o) {
-    isax_opts r{1024, -12, 128, 0, 0, 4, 256};  // cand_cap 0: chosen at the first query (alloc_scratch)
+    isax_opts r{1024, -12, 1024, 0, 0, 4, 256};  // cand_cap 0: chosen per batch (alloc_scratch, nn1_device)
     if (o) {
         if (o->probe_bits) r.probe_bits = o->probe_bits;
         if (o->probe_L) r.probe_L = o->probe_L;
@@ -62,7 +62,7 @@ static int check_geometry(uint64_t N, uint32_t n, uint32_t w, uint32_t card, con
     if (o.window_L == 0 || o.window_L > 4096) return set_error(ISAX_E_INVAL, "window_L must be in [1, 4096]");
     if (o.slack_log2 > -8 || o.slack_log2 < -20) return set_error(ISAX_E_INVAL, "slack_log2 must be in [-20, -8]");
     if (o.batch_Q > 1024) return set_error(ISAX_E_INVAL, "batch_Q must be <= 1024");
-    if (o.flags & ~(ISAX_FLAG_FLAT_SCAN | ISAX_FLAG_FUSED_REFINE)) return set_error(ISAX_E_INVAL, "unknown flags");
+    if (o.flags & ~ISAX_FLAG_FLAT_SCAN) return set_error(ISAX_E_INVAL, "unknown flags");
     if (o.probe_bits != ISAX_PROBES_NONE && o.probe_bits > 5) return set_error(ISAX_E_INVAL, "probe_bits must be <= 5");
     if (o.probe_L == 0 || o.probe_L > 1024) return set_error(ISAX_E_INVAL, "probe_L must be in [1, 1024]");
     return ISAX_OK;
@@ -85,15 +85,21 @@ static void free_scratch(isax_index *ix) {
     q = QueryScratch{};
 }
 
-// Candidate capacity per query: the caller's, or min(N, 2^23) (a query never has more than N
-// candidates), halved while the scratch does not fit in device memory (down to 2^16). A query that
-// overflows it runs more rounds (R10), each a rescan, so the default is generous: at 100 queries
-// over 200M series a few queries keep millions of candidates.
+// Candidate lists. With opts.cand_cap set, every query of a batch gets that capacity. By default
+// the lists share one pool of CAND_POOL entries (about 10 B each), split evenly over the queries of
+// each batch: a batch of B queries gets min(N, 2^23, pool / B) per query (nn1_device). The pool is
+// halved while the scratch does not fit in device memory (down to 2^16 per query slot). A query
+// that overflows its capacity runs more rounds (R10), each a rescan, refining its smallest bounds
+// first. Small batches of random-walk queries (100 over 200M series: a few keep millions of
+// candidates) get the generous 2^23; a batch of 1000 near-duplicate queries gets 2^20, where the
+// smallest-bounds-first rounds skip most of a heavy query's candidates (BASELINE config 5).
+constexpr uint64_t CAND_POOL = 1ull << 30;
 static int alloc_scratch_cap(isax_index *ix, uint32_t cap);
 static int alloc_scratch(isax_index *ix) {
     if (ix->qs.cap_Q) return ISAX_OK;
     if (ix->opts.cand_cap) return alloc_scratch_cap(ix, ix->opts.cand_cap);
-    uint32_t cap = (uint32_t)std::min<uint64_t>(ix->N, 1ull << 23);
+    const uint64_t per_max = std::min<uint64_t>(ix->N, 1ull << 23);
+    uint32_t cap = (uint32_t)std::min<uint64_t>(per_max, std::max<uint64_t>(CAND_POOL / ix->opts.batch_Q, 1));
     for (;;) {
         const int rc = alloc_scratch_cap(ix, cap);
         if (rc != ISAX_E_NOMEM || cap <= (1u << 16)) return rc;
@@ -158,7 +164,7 @@ static int alloc_scratch_cap(isax_index *ix, uint32_t cap) {
         return cuda_error(e, "allocating query scratch");
     }
     q.cap_Q = Q;
-    q.cand_cap = cap;
+    q.cand_cap = q.cand_cap_slot = cap;
     ix->device_bytes += acc;
     return ISAX_OK;
 }
@@ -313,10 +319,13 @@ static int nn1_device(isax_index *ix, const float *d_q, uint32_t Q, int64_t *d_i
     ix->st_refine_bytes_first = 0;
     ISAX_CUDA(cudaMemsetAsync(qs.scan_bytes_dev, 0, StatusBlock::RESET_BYTES, s));  // + refine_bytes, flag
     int result = ISAX_OK;
-    const bool fused_ok = (ix->opts.flags & ISAX_FLAG_FUSED_REFINE) && !(ix->opts.flags & ISAX_FLAG_FLAT_SCAN) &&
-                          (ix->n == 128 || ix->n == 256);
     for (uint32_t b0 = 0; b0 < Q && result == ISAX_OK; b0 += qs.cap_Q) {
         const uint32_t B = std::min(qs.cap_Q, Q - b0);
+        // the batch's share of the candidate pool (a fixed capacity when opts.cand_cap is set)
+        qs.cand_cap = ix->opts.cand_cap
+                          ? qs.cand_cap_slot
+                          : (uint32_t)std::min<uint64_t>(std::min<uint64_t>(ix->N, 1ull << 23),
+                                                         (uint64_t)qs.cand_cap_slot * qs.cap_Q / B);
         const bool timed = b0 == 0;
         if (timed) cudaEventRecord(ix->ev[0], s);
         launch_qprep(ix, d_q + (uint64_t)b0 * ix->n, B, s, qs.flag);
@@ -365,17 +374,15 @@ static int nn1_device(isax_index *ix, const float *d_q, uint32_t Q, int64_t *d_i
             }
             ISAX_CUDA(cudaMemcpyAsync(qs.qmap, hm.qmap, nact * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
             ISAX_CUDA(cudaMemcpyAsync(qs.qband, hm.band, nact * sizeof(float2), cudaMemcpyHostToDevice, s));
-            // round 0 of the leaf scan may refine inside the scan kernel (ISAX_FLAG_FUSED_REFINE)
-            const bool fused = round == 0 && fused_ok;
-            ix->st_scan_bytes += launch_lbscan(ix, nact, B, qs.qmap, qs.qband, delta, fused, s);
+            ix->st_scan_bytes += launch_lbscan(ix, nact, B, qs.qmap, qs.qband, delta, s);
             if (timed && round == 0) cudaEventRecord(ix->ev[6], s);
-            if (!fused) launch_candcheck(ix, B, s);
+            launch_candcheck(ix, B, s);
             if (timed && round == 0) cudaEventRecord(ix->ev[3], s);
-            if (!fused) launch_refine(ix, B, delta, s);
+            launch_refine(ix, B, delta, s);
             if (timed && round == 0) cudaEventRecord(ix->ev[4], s);
             launch_finalize(ix, B, delta, d_id + b0, d_dist + b0, s);  // speculative: redone after another round
             // scanprep + scan, candcheck, refine + filter + refine, finalize
-            ix->st_launches += ((ix->opts.flags & ISAX_FLAG_FLAT_SCAN) ? 1 : 2) + (fused ? 1 : 5);
+            ix->st_launches += ((ix->opts.flags & ISAX_FLAG_FLAT_SCAN) ? 1 : 2) + 5;
             if (timed && round == 0) cudaEventRecord(ix->ev[5], s);
             ISAX_CUDA(cudaGetLastError());
             // the whole status block in one copy (StatusBlock: bsf, counters, flags, byte counts)
@@ -407,8 +414,7 @@ static int nn1_device(isax_index *ix, const float *d_q, uint32_t Q, int64_t *d_i
                 const uint32_t i = hm.qmap[k];
                 const uint32_t cnt = hm.cand_cnt[i];
                 bsf_h[i] = bsf_d2_host(hm.bsf[i]);
-                // after the exact rule (candcheck_kernel); fused: counted by the refinement warps
-                ix->st_cand[b0 + i] += hm.cand_cnt2[i] + hm.cnt_hi[i] + (round == 0 && fused_ok ? hm.counters[4 * i + 3] : 0);
+                ix->st_cand[b0 + i] += hm.cand_cnt2[i] + hm.cnt_hi[i];  // after the exact rule (candcheck_kernel)
                 ix->st_rounds[b0 + i] = round + 1;
                 if (hm.near_cnt[i] > (uint32_t)NEAR_K) {  // near overflow: start over, BSF kept
                     band[i] = make_float2(-1.0f, INF);

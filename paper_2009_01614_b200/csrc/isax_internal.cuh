@@ -92,7 +92,8 @@ struct HostMirror : StatusBlock {
 // Per-batch scratch owned by the index (sized for opts.batch_Q queries).
 struct QueryScratch {
     uint32_t cap_Q = 0;
-    uint32_t cand_cap = 0;
+    uint32_t cand_cap_slot = 0;  // allocated list entries per query slot (cap_Q slots)
+    uint32_t cand_cap = 0;       // the current batch's capacity per query (<= cand_cap_slot * cap_Q / B)
     float *qy = nullptr;            // [Q][n] z-normalised queries
     double *qpaa = nullptr;         // [Q][16]
     uint8_t *qsax = nullptr;        // [Q][16]
@@ -210,9 +211,8 @@ void launch_leaf_meta(const uint8_t *sax, uint64_t N, uint8_t *lmeta, uint8_t *s
 // Scan all sorted positions for the nq queries qmap[0..nq), keeping band[i].x < LB^2 <= min(band[i].y,
 // bsf^2 (1+delta)) for slot i. Returns the summary bytes it reads that the host can count (node
 // summaries or flat words); the leaf scan adds its leaf-word and leaf-summary bytes to qs.scan_bytes_dev on the device.
-// fused: the first band's candidates are refined inside the scan kernel (no candidate lists)
 uint64_t launch_lbscan(const isax_index *ix, uint32_t nq, uint32_t B, const uint32_t *qmap, const float2 *band,
-                       float delta, bool fused, cudaStream_t s);
+                       float delta, cudaStream_t s);
 // lbscan.cu: the exact fp32 rule for the candidates the leaf scan kept on their u8 sum alone,
 // and compaction of every list into cand2 / cand_cnt2 (the refine's input)
 void launch_candcheck(const isax_index *ix, uint32_t Q, cudaStream_t s);

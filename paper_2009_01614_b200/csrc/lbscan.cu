@@ -278,14 +278,7 @@ constexpr uint32_t HYPER = HYPER_SIZE / SUPER_SIZE; // super-nodes per hyper-nod
 static_assert(HYPER == 32, "phase A maps the super-nodes of a hyper-node to the lanes of a warp");
 static_assert(LEAF == 32 && SUPER == 32, "phase A maps a super-node to a warp iteration and a leaf to a lane");
 constexpr int LF_THREADS = 1024;
-#ifndef ISAX_RF_WARPS
-#define ISAX_RF_WARPS 4
-#endif
-constexpr uint32_t LF_RF_WARPS = ISAX_RF_WARPS;             // fused mode: refinement warps per CTA
-constexpr uint32_t LF_SCAN_WARPS = LF_THREADS / 32 - LF_RF_WARPS;  // fused mode: scan warps
-constexpr uint32_t RQ = 2048;                                 // fused mode: shared refine queue entries
 constexpr uint32_t CHUNK = 8192;  // max leaves per phase-A/phase-B round of a CTA
-constexpr uint32_t CHUNK_F = 4096;  // ... in fused mode (its shared memory holds the refinement slots)
 constexpr uint32_t CBUF = 512;    // shared candidate buffer per query slot
 #ifndef ISAX_PD
 #define ISAX_PD 4
@@ -331,282 +324,6 @@ __device__ __forceinline__ void emit(bool keep, uint32_t pos, uint32_t b, uint32
             candq[(uint64_t)q * cap + k] = (uint8_t)b;
         }
     }
-}
-
-// ---- fused refinement (MESSI: the workers that compute lower bounds also compute
-// real distances and update the BSF while the traversal goes on). In fused mode the leaf scan's
-// candidates never reach global memory: the scan warps push them into a bounded queue in shared
-// memory and LF_RF_WARPS warps of the same CTA refine them while the scan continues, so the
-// random row reads of the refinement overlap the scan's shared-memory lookups.
-struct RefineArgs {
-    const float *stored;        // [N][n] rows in sorted order
-    const uint32_t *perm;       // pos -> id
-    const float *qy;            // [B][n] z-normalised queries
-    unsigned long long *bsf;    // [B] packed (d^2, id)
-    const float *qscale, *qT;   // [B] the scan's u8 scale and threshold
-    NearEntry *near;
-    uint32_t *near_cnt, *counters;
-    unsigned long long *refine_bytes;
-    uint32_t n, B;
-    float onepd;
-};
-
-// One candidate into the queue: a bounded multi-producer multi-consumer queue in shared memory
-// (Vyukov's, with the sequence number packed into the entry). Slot i % RQ holds the 64-bit word
-//     pos (32) | q (10) | b (8) | unchecked (1) | seq (13),   seq = ticket mod 2^13,
-// seq == i when the slot is free for ticket i and i + 1 when it holds ticket i's entry. Every
-// transition is one 64-bit shared store, so no fence is needed. A full queue makes the scan
-// warp wait for the refinement warps (back pressure); tickets are handed out in order, so the
-// oldest outstanding ticket always finds its slot freed and there is no deadlock.
-constexpr uint32_t RQ_SEQ_MASK = (1u << 13) - 1;
-__device__ __forceinline__ uint32_t rq_seq_of(unsigned long long e) { return (uint32_t)(e >> 51); }
-__device__ __forceinline__ void rq_push(bool keep, uint32_t pos, uint32_t b, uint32_t unchecked, uint32_t q, uint32_t lane, uint32_t lt,
-                                        unsigned long long *rq, uint32_t *tail) {
-    const uint32_t bal = __ballot_sync(0xffffffffu, keep);
-    if (!bal) return;
-    uint32_t base = 0;
-    if (lane == 0) base = atomicAdd(tail, (uint32_t)__popc(bal));
-    base = __shfl_sync(0xffffffffu, base, 0);
-    if (keep) {
-        const uint32_t i = base + __popc(bal & lt);
-        volatile unsigned long long *slot = reinterpret_cast<volatile unsigned long long *>(rq) + (i % RQ);
-        while (rq_seq_of(*slot) != (i & RQ_SEQ_MASK)) __nanosleep(64);
-        *slot = (unsigned long long)pos | ((unsigned long long)q << 32) | ((unsigned long long)b << 42) |
-                ((unsigned long long)unchecked << 50) | ((unsigned long long)((i + 1) & RQ_SEQ_MASK) << 51);
-    }
-    __syncwarp();
-}
-
-// The refinement warps: TMA bulk copies gather the candidates' half rows into shared memory.
-// Each refinement warp owns RF_SLOTS slots of one half row (n/2 floats) and one mbarrier per
-// slot; lane s keeps slot s's job (query, position, threshold, partial sum, state). The warp
-// takes its slots in round-robin order: it waits for the slot's copy, reduces the half row
-// against the query over all 32 lanes (float4 per lane), and then either abandons (partial >
-// lim, R8), copies the second half into the same slot, or completes the row. A slot that
-// empties is refilled at once from the queue. One lane issues each copy
-// (cp.async.bulk ... mbarrier::complete_tx), so a warp keeps RF_SLOTS half rows in flight
-// without holding registers for them. Per candidate, before its first copy:
-//  - b == B_UNCHECKED (a u8 sum in (E_SURE, 254]): the flat scan's exact fp32 rule LB^2 <= T,
-//    segments left to right; a member that fails it is not a candidate (R11b);
-//  - the skip test of R14 against the BSF: b > lim * sc (rounded up) means LB^2 > lim.
-// Completed rows within (1 + delta) of the BSF update it and join the near list (R9), as in
-// refine_q_kernel. Counters go to shared memory ([B][4]: refined, abandoned, skipped, accepted).
-#ifndef ISAX_RF_SLOTS
-#define ISAX_RF_SLOTS 12
-#endif
-constexpr uint32_t RF_SLOTS = ISAX_RF_SLOTS;
-static_assert(RF_SLOTS <= 32, "one lane per slot");
-
-__device__ __forceinline__ void mbar_init(uint32_t bar) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, uint32_t bytes, uint32_t bar) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
-                 "l"(src), "r"(bytes), "r"(bar)
-                 : "memory");
-}
-// a half row and the same half of the query into one slot, one transaction count
-__device__ __forceinline__ void bulk_pair(uint32_t dst, const float *row, const float *qrow, uint32_t bytes, uint32_t bar) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(2 * bytes) : "memory");
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
-                 "l"(row), "r"(bytes), "r"(bar)
-                 : "memory");
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst + bytes),
-                 "l"(qrow), "r"(bytes), "r"(bar)
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
-    asm volatile(
-        "{\n\t.reg .pred P1;\n\t"
-        "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
-        "@!P1 bra WAIT_%=;\n\t}" ::"r"(bar),
-        "r"(parity)
-        : "memory");
-}
-
-__device__ __forceinline__ void refine_role(const RefineArgs &ra, unsigned long long *rq, uint32_t *head,
-                                            uint32_t *tail, uint32_t *done, uint32_t *rcnt, const float4 *slots,
-                                            uint32_t bars, const float *__restrict__ lut_all,
-                                            const uint4 *__restrict__ sax, uint32_t lane) {
-    constexpr uint32_t FULL = 0xffffffffu;
-    constexpr uint32_t SMASK = RF_SLOTS == 32 ? FULL : (1u << RF_SLOTS) - 1;
-    const uint32_t n = ra.n, hb = n * 2;  // half-row bytes
-    const uint32_t slot0 = (uint32_t)__cvta_generic_to_shared(slots);
-    // lane s: slot s's job. st: 0 empty, 1 first half in flight, 2 second half in flight
-    uint32_t st = 0, jq = 0, jpos = 0, par = 0;
-    float jlim = 0.f, jacc = 0.f;
-    // lane l: pending candidate l of the last batch taken from the queue (bit l of pend)
-    uint32_t pq = 0, ppos = 0, pend = 0;
-    float plim = 0.f;
-    bool closed = false;
-    unsigned long long rows_read = 0;
-    // Take a batch of up to 32 tickets (one per lane) and screen them all at once, so their
-    // global reads (BSF, scale, the exact rule's word and table entries) overlap.
-    auto fetch = [&]() {
-        uint32_t base = 0, cnt = 0;
-        if (lane == 0) {
-            const uint32_t avail = *(volatile uint32_t *)tail - *(volatile uint32_t *)head;
-            cnt = (int32_t)avail <= 0 ? 1u : min(avail, 32u);
-            base = atomicAdd(head, cnt);
-        }
-        base = __shfl_sync(FULL, base, 0);
-        cnt = __shfl_sync(FULL, cnt, 0);
-        uint32_t stt = 0;  // 1 = entry, 2 = closed
-        unsigned long long e = 0;
-        if (lane < cnt) {
-            const uint32_t j = base + lane;
-            volatile unsigned long long *sl = reinterpret_cast<volatile unsigned long long *>(rq) + (j % RQ);
-            for (;;) {
-                e = *sl;
-                if (rq_seq_of(e) == ((j + 1) & RQ_SEQ_MASK)) {
-                    stt = 1;
-                    *sl = (unsigned long long)((j + RQ) & RQ_SEQ_MASK) << 51;  // free for ticket j + RQ
-                    break;
-                }
-                if (*(volatile uint32_t *)done && j >= *(volatile uint32_t *)tail) {
-                    stt = 2;
-                    break;
-                }
-                __nanosleep(64);
-            }
-        }
-        if (__any_sync(FULL, stt == 2)) closed = true;  // a ticket past the end: the queue is drained
-        bool keep = stt == 1;
-        const uint32_t pos = (uint32_t)e, hi32 = (uint32_t)(e >> 32);
-        const uint32_t q = keep ? hi32 & 0x3FFu : 0u;
-        const uint32_t e8 = (hi32 >> 10) & 0xFFu, unchecked = (hi32 >> 18) & 1u;
-        float lim = 0.f;
-        if (keep) {
-            const float sc = __ldg(ra.qscale + q);
-            lim = bsf_d2(*((volatile unsigned long long *)&ra.bsf[q])) * ra.onepd;
-            uint32_t b = e8;  // <= LB^2 * sc for every member (R11b)
-            if (unchecked) {  // the flat scan's exact fp32 rule (R11b)
-                const float lb = word_lb(lut_all + (uint64_t)q * W * CARD, __ldg(sax + pos));
-                keep = lb <= __ldg(ra.qT + q);
-            }
-            if (keep) {
-                atomicAdd(&rcnt[4 * q + 3], 1u);
-                if ((float)b > __fmul_ru(lim, sc)) {  // LB^2 > lim: neither the answer nor a near tie (R14)
-                    atomicAdd(&rcnt[4 * q + 2], 1u);
-                    keep = false;
-                }
-            }
-        }
-        pend = __ballot_sync(FULL, keep);
-        pq = q;
-        ppos = pos;
-        plim = lim;
-    };
-    // start the next pending candidate's first half in slot s (fetching batches as needed)
-    auto refill = [&](uint32_t s) {
-        while (!pend && !closed) fetch();
-        if (!pend) return;
-        const uint32_t p = __ffs(pend) - 1;
-        pend &= pend - 1;
-        const uint32_t q = __shfl_sync(FULL, pq, p), pos = __shfl_sync(FULL, ppos, p);
-        const float lim = __shfl_sync(FULL, plim, p);
-        if (lane == 0) {
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the slot's earlier generic reads
-            bulk_pair(slot0 + s * 2 * hb, ra.stored + (uint64_t)pos * n, ra.qy + (uint64_t)q * n, hb, bars + 8 * s);
-        }
-        if (lane == s) {
-            st = 1;
-            jq = q;
-            jpos = pos;
-            jlim = lim;
-        }
-    };
-#ifdef ISAX_RF_NOP
-    while (!closed) fetch();  // timing experiment only: drain the queue, refine nothing
-    return;
-#endif
-    for (uint32_t s = 0; s < RF_SLOTS; s++) refill(s);
-    const uint32_t ql = lane & 7, quarter = lane >> 3, qb = lane & 24;
-    const uint32_t nf = hb / 16;  // float4 per half row (32 at n = 256)
-    uint32_t r = 0;
-    for (;;) {
-        const uint32_t act = __ballot_sync(FULL, lane < RF_SLOTS && st != 0) & SMASK;
-        if (!act) break;  // every slot is empty and the queue is drained
-        // the (up to) four next active slots in round-robin order, one per quarter warp
-        uint32_t rot = RF_SLOTS == 32 ? __funnelshift_r(act, act, r) : ((act >> r) | (act << (RF_SLOTS - r))) & SMASK;
-        uint32_t pick[4], npick = 0;
-#pragma unroll
-        for (int k = 0; k < 4; k++) {
-            pick[k] = rot ? (r + __ffs(rot) - 1) % RF_SLOTS : 0xffffffffu;
-            if (rot) npick++;
-            rot &= rot - 1;
-        }
-        const uint32_t sk = quarter == 0 ? pick[0] : quarter == 1 ? pick[1] : quarter == 2 ? pick[2] : pick[3];
-        const bool mine = quarter < npick;
-        const uint32_t src = mine ? sk : 0;
-        const uint32_t sst = __shfl_sync(FULL, st, src), q = __shfl_sync(FULL, jq, src);
-        const uint32_t pos = __shfl_sync(FULL, jpos, src), pr = __shfl_sync(FULL, par, src);
-        const float lim = __shfl_sync(FULL, jlim, src), acc0 = __shfl_sync(FULL, jacc, src);
-        if (mine) mbar_wait(bars + 8 * sk, pr);
-        __syncwarp();
-        float a = 0.f;
-        if (mine) {
-            const float4 *row = slots + (size_t)sk * 2 * nf, *qh = row + nf;
-            for (uint32_t m = ql; m < nf; m += 8) {
-                const float4 v = row[m], w = qh[m];
-                float d;
-                d = v.x - w.x; a = fmaf(d, d, a);
-                d = v.y - w.y; a = fmaf(d, d, a);
-                d = v.z - w.z; a = fmaf(d, d, a);
-                d = v.w - w.w; a = fmaf(d, d, a);
-            }
-        }
-        a += __shfl_xor_sync(FULL, a, 1);
-        a += __shfl_xor_sync(FULL, a, 2);
-        a += __shfl_xor_sync(FULL, a, 4);
-        // the quarter's decision: 0 = slot empties, 2 = second half started
-        uint32_t nst = 0;
-        if (mine && ql == 0) {
-            rows_read += 1;
-            if (sst == 1) {
-                if (a > lim) {  // early abandon after half the row (R8)
-                    atomicAdd(&rcnt[4 * q + 1], 1u);
-                } else {
-                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the slot's generic reads above
-                    bulk_pair(slot0 + sk * 2 * hb, ra.stored + (uint64_t)pos * n + n / 2, ra.qy + (uint64_t)q * n + n / 2, hb,
-                              bars + 8 * sk);
-                    nst = 2;
-                }
-            } else {
-                const float d2 = acc0 + a;
-                atomicAdd(&rcnt[4 * q + 0], 1u);
-                if (d2 <= lim) {  // re-read the current BSF before claiming a near slot
-                    const float cur = bsf_d2(*((volatile unsigned long long *)&ra.bsf[q])) * ra.onepd;
-                    if (d2 <= cur) {
-                        const uint32_t id = ra.perm[pos];
-                        atomicMin(&ra.bsf[q], pack_bsf(d2, id));
-                        const uint32_t k = atomicAdd(&ra.near_cnt[q], 1u);
-                        if (k < NEAR_K) ra.near[(uint64_t)q * NEAR_K + k] = NearEntry{id, pos, d2, 0};
-                    }
-                }
-            }
-        }
-        // back to the slots' owner lanes; then refill the slots that emptied
-        uint32_t freed = 0;
-#pragma unroll
-        for (int k = 0; k < 4; k++) {
-            const uint32_t ns = __shfl_sync(FULL, nst, 8 * k);
-            const float ak = __shfl_sync(FULL, a, 8 * k);
-            if (k < (int)npick) {
-                if (lane == pick[k]) {
-                    par ^= 1u;
-                    st = ns;
-                    jacc = ak;
-                }
-                if (ns == 0) freed |= 1u << pick[k];
-            }
-        }
-        for (uint32_t f = freed; f; f &= f - 1) refill(__ffs(f) - 1);
-        r = (pick[npick - 1] + 1) % RF_SLOTS;
-    }
-    if (lane == 0 && rows_read) atomicAdd(ra.refine_bytes, rows_read * (unsigned long long)hb);
 }
 
 // u8 table entry (R11b): floor(v * sc) with sc = 254 / T rounded down, clamped at 255. v = 0 maps
@@ -655,14 +372,14 @@ __global__ void __launch_bounds__(256) scanprep_kernel(const float *__restrict__
     }
 }
 
-template <int G, bool FUSED>
+template <int G>
 __global__ void __launch_bounds__(LF_THREADS, 1) leafscan_kernel(
     const uint4 *__restrict__ sax, const uint8_t *__restrict__ lmeta, const uint8_t *__restrict__ smeta,
     const uint8_t *__restrict__ hmeta, uint32_t N, const float *__restrict__ lut_all, const uint8_t *__restrict__ lut8_all, const uint4 *__restrict__ qconst_all,
     const uint8_t *__restrict__ qsax_all, const uint32_t *__restrict__ qmap, uint32_t nq, uint32_t nleaf,
     uint32_t chunk, uint32_t *__restrict__ cand, uint8_t *__restrict__ candq, uint32_t *__restrict__ cand_cnt, uint32_t cap,
     uint32_t *__restrict__ hist, uint32_t *__restrict__ leaves_alive, unsigned long long *__restrict__ scan_bytes_dev,
-    uint32_t *__restrict__ task_ctr, RefineArgs ra) {
+    uint32_t *__restrict__ task_ctr) {
     // shared: [G][16][256] u8 tables | [G][CBUF] candidates | [CHUNK] worklist | [NW][2][2 LEAF] words
     // (the dynamic region follows the static variables, so the u8 tables are aligned by hand: the
     // PRMT address trick needs a 256-aligned base)
@@ -670,20 +387,11 @@ __global__ void __launch_bounds__(LF_THREADS, 1) leafscan_kernel(
     const uint32_t raw8 = (uint32_t)__cvta_generic_to_shared(smem_dyn);
     const uint32_t lut8_sh = (raw8 + 255u) & ~255u;
     uint8_t *lut8 = smem_dyn + (lut8_sh - raw8);
-    constexpr uint32_t NW = FUSED ? LF_SCAN_WARPS : LF_THREADS / 32;  // scan warps
-    constexpr uint32_t NST = NW * 32;                                  // scan threads
-    // separate refinement: [G][CBUF] candidates | worklist | stage | [G][CBUF] u8 bounds
-    // fused refinement:    [RQ] queue entries | worklist | stage | [B][4] counters
+    constexpr uint32_t NW = LF_THREADS / 32;
     uint32_t *cbuf = reinterpret_cast<uint32_t *>(lut8 + G * W * CARD);
-    unsigned long long *rq = reinterpret_cast<unsigned long long *>(lut8 + G * W * CARD);
-    uint32_t *worklist = FUSED ? reinterpret_cast<uint32_t *>(rq + RQ) : cbuf + G * CBUF;  // (leaf offset in chunk) | (query mask << 16)
-    uint4 *stage = reinterpret_cast<uint4 *>(worklist + (FUSED ? CHUNK_F : CHUNK));
+    uint32_t *worklist = cbuf + G * CBUF;  // (leaf offset in chunk) | (query mask << 16)
+    uint4 *stage = reinterpret_cast<uint4 *>(worklist + CHUNK);
     uint8_t *qbuf = reinterpret_cast<uint8_t *>(stage + NW * PD * LEAF);  // [G][CBUF] u8 bounds
-    uint32_t *rcnt = reinterpret_cast<uint32_t *>(stage + NW * PD * LEAF);  // fused: [B][4] refine counters
-    // fused: [LF_RF_WARPS][RF_SLOTS] half-row slots, then one mbarrier per slot
-    const float4 *rslots = reinterpret_cast<const float4 *>(rcnt + 4 * ra.B);
-    const uint32_t rbars = (uint32_t)__cvta_generic_to_shared(rslots) + LF_RF_WARPS * RF_SLOTS * ra.n * 4;
-    __shared__ uint32_t rq_tail, rq_head, rq_done;
     __shared__ QConst qc[G];
     __shared__ uint4 qsym[G][2];  // the query's 16 symbols as 8 u16x2 pairs
     __shared__ uint32_t qid[G], cb_cnt[G], alive_cnt[G], fbase[G];
@@ -694,11 +402,6 @@ __global__ void __launch_bounds__(LF_THREADS, 1) leafscan_kernel(
     __shared__ uint32_t smask_sh[CHUNK / SUPER];            // query mask of each super-node of the chunk
     const uint32_t t = threadIdx.x, lane = t & 31, warp = t >> 5;
     constexpr uint32_t FULL = 0xffffffffu;
-    // the scan warps' barrier (a named barrier when the refinement warps run beside them)
-    auto scan_bar = [&]() {
-        if constexpr (FUSED) asm volatile("bar.sync 1, %0;" ::"n"(NST) : "memory");
-        else __syncthreads();
-    };
     const uint32_t lt = (1u << lane) - 1u;
     const uint32_t nchunks = (nleaf + chunk - 1) / chunk;
     const uint32_t ngroups = (nq + G - 1) / G;
@@ -713,25 +416,21 @@ __global__ void __launch_bounds__(LF_THREADS, 1) leafscan_kernel(
     auto flush = [&]() {
         if (lane < G && my_alive) atomicAdd(&alive_cnt[lane], my_alive);
         my_alive = 0;
-        scan_bar();
+        __syncthreads();
         if (t < G) {
             const uint32_t c = min(cb_cnt[t], CBUF);
             fbase[t] = (c && g0 + t < nq) ? atomicAdd(&cand_cnt[qid[t]], c) : 0;
             if (alive_cnt[t] && g0 + t < nq) atomicAdd(&leaves_alive[qid[t]], alive_cnt[t]);
         }
-        if constexpr (FUSED) {  // candidates went to the refinement warps; no lists, no histogram
-            scan_bar();
-            return;
-        }
-        for (uint32_t e = t; e < G * HIST_BINS; e += NST) {
+        for (uint32_t e = t; e < G * HIST_BINS; e += LF_THREADS) {
             const uint32_t g = e / HIST_BINS, b = e % HIST_BINS;
             if (g0 + g < nq && shist[g][b]) atomicAdd(&hist[qid[g] * HIST_BINS + b], shist[g][b]);
         }
-        scan_bar();
+        __syncthreads();
         for (uint32_t g = 0; g < G; g++) {
             if (g0 + g >= nq) break;
             const uint32_t c = min(cb_cnt[g], CBUF);
-            for (uint32_t i = t; i < c; i += NST) {
+            for (uint32_t i = t; i < c; i += LF_THREADS) {
                 const uint32_t k = fbase[g] + i;
                 if (k < cap) {
                     cand[(uint64_t)qid[g] * cap + k] = cbuf[g * CBUF + i];
@@ -739,34 +438,19 @@ __global__ void __launch_bounds__(LF_THREADS, 1) leafscan_kernel(
                 }
             }
         }
-        scan_bar();
+        __syncthreads();
     };
-    if (t == 0) {
-        wl_cnt = 0;
-        rq_tail = rq_head = rq_done = 0;
-    }
-    if constexpr (FUSED) {
-        for (uint32_t i = t; i < RQ; i += LF_THREADS) rq[i] = (unsigned long long)i << 51;  // slot i free for ticket i
-        for (uint32_t i = t; i < 4 * ra.B; i += LF_THREADS) rcnt[i] = 0;
-        if (t < LF_RF_WARPS * RF_SLOTS) mbar_init(rbars + 8 * t);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-    if (FUSED && warp >= NW) {
-        const uint32_t rw = warp - NW;
-        refine_role(ra, rq, &rq_head, &rq_tail, &rq_done, rcnt, rslots + rw * RF_SLOTS * (ra.n / 4),
-                    rbars + 8 * RF_SLOTS * rw, lut_all, sax, lane);
-    } else {
+    if (t == 0) wl_cnt = 0;
     for (;;) {
         if (t == 0) s_task = atomicAdd(task_ctr, 1u);
-        scan_bar();
+        __syncthreads();
         const uint32_t task = s_task;
         if (task >= ntasks) break;
         const uint32_t grp = task / nchunks, ch = task % nchunks;
         if (grp * G != g0) {  // new query group: load its tables and constants
             if (g0 != 0xffffffffu) flush();
             g0 = grp * G;
-            for (uint32_t e = t; e < G * HIST_BINS; e += NST) shist[e / HIST_BINS][e % HIST_BINS] = 0;
+            for (uint32_t e = t; e < G * HIST_BINS; e += LF_THREADS) shist[e / HIST_BINS][e % HIST_BINS] = 0;
             if (t < G) {
                 const bool valid = g0 + t < nq;
                 const uint32_t slot = valid ? g0 + t : g0;
@@ -786,19 +470,19 @@ __global__ void __launch_bounds__(LF_THREADS, 1) leafscan_kernel(
                 const uint4 *src = reinterpret_cast<const uint4 *>(lut8_all + (uint64_t)g0 * W * CARD);
                 uint4 *dst = reinterpret_cast<uint4 *>(lut8);
                 constexpr uint32_t PER = W * CARD / 16;
-                for (uint32_t e = t; e < G * PER; e += NST)
+                for (uint32_t e = t; e < G * PER; e += LF_THREADS)
                     dst[e] = g0 + e / PER < nq ? __ldg(src + e) : make_uint4(FULL, FULL, FULL, FULL);
             }
-            scan_bar();
+            __syncthreads();
         }
         const uint32_t c0 = ch * chunk;  // a multiple of SUPER
         const uint32_t c1 = min(c0 + chunk, nleaf);
         // ---- phase A: three node levels, top down.
         const uint32_t s0 = c0 / SUPER, send = (c1 + SUPER - 1) / SUPER;  // the chunk's super-nodes
         const uint32_t h0 = s0 / HYPER, nh = (send - 1) / HYPER - h0 + 1;  // its hyper-nodes (<= 8)
-        for (uint32_t e = t; e < send - s0; e += NST) smask_sh[e] = 0;
+        for (uint32_t e = t; e < send - s0; e += LF_THREADS) smask_sh[e] = 0;
         if (t < nh) hmask[t] = 0;
-        scan_bar();
+        __syncthreads();
         // A0: thread = (hyper-node, query). A hyper-node may extend beyond the chunk (chunk of 512
         // leaves): its bound is over a superset of the chunk's positions, still a lower bound.
         if (t < nh * 16u) {
@@ -809,7 +493,7 @@ __global__ void __launch_bounds__(LF_THREADS, 1) leafscan_kernel(
                 bytes += 32;
             }
         }
-        scan_bar();
+        __syncthreads();
         // A1: for each (hyper-node, query) that survived, lane = one of its 32 super-nodes
         for (uint32_t pr = warp; pr < nh * 16u; pr += NW) {
             const uint32_t h = pr >> 4, g = pr & 15u;
@@ -822,7 +506,7 @@ __global__ void __launch_bounds__(LF_THREADS, 1) leafscan_kernel(
                     atomicOr(&smask_sh[sn - s0], 1u << g);
             }
         }
-        scan_bar();
+        __syncthreads();
         // A2: warp iteration = one super-node (s0 + warp + NW j), lane = one of its 32 leaves, for
         // the queries that kept the super-node. Leaf summaries are read only under surviving
         // super-nodes, one iteration ahead.
@@ -865,7 +549,7 @@ __global__ void __launch_bounds__(LF_THREADS, 1) leafscan_kernel(
                 if (alive) worklist[off + __popc(bal & lt)] = (leaf - c0) | (alive << 16);
             }
         }
-        scan_bar();
+        __syncthreads();
         // ---- phase B: the members of surviving leaves, one worklist entry per warp iteration
         // (lane = member). Each warp takes entries warp, warp + NW, ... and keeps PD of them in
         // flight in its own ring of shared staging slots (cp.async, one commit group per entry).
@@ -928,46 +612,29 @@ __global__ void __launch_bounds__(LF_THREADS, 1) leafscan_kernel(
                     const float y = __fmul_rd(lb, qsc[g]);
                     b = lb > 0.f ? (y >= 254.f ? 254u : (uint32_t)y) : 0u;
                 }
-                if constexpr (FUSED) {  // straight to the refinement warps of this CTA
-                    // the u8 sum itself (a bound for every member) and whether the exact rule is still due
-                    rq_push(keep, pos, check ? b : e8, !check && e8 > E_SURE, qid[g], lane, lt, rq, &rq_tail);
-                } else {
-                    if (keep)
-                        atomicAdd(&shist[g][first ? min(e8 * HIST_BINS / 254u, HIST_BINS - 1) : hist_bin(lb, kq.lo, kq.T)], 1u);
-                    emit(keep, pos, b, g, qid[g], lane, lt, cbuf, qbuf, cb_cnt, cand, candq, cand_cnt, cap);
-                }
+                if (keep)
+                    atomicAdd(&shist[g][first ? min(e8 * HIST_BINS / 254u, HIST_BINS - 1) : hist_bin(lb, kq.lo, kq.T)], 1u);
+                emit(keep, pos, b, g, qid[g], lane, lt, cbuf, qbuf, cb_cnt, cand, candq, cand_cnt, cap);
             }
         }
         cp_async_wait<0>();  // the trailing (empty) groups
-        scan_bar();
+        __syncthreads();
         if (t == 0) wl_cnt = 0;
     }
     if (g0 != 0xffffffffu) flush();
-    if constexpr (FUSED) {  // every push has completed: the queue's tail is final
-        scan_bar();
-        if (t == 0) atomicExch(&rq_done, 1u);
-    }
-    }  // scan role
     bytes = __reduce_add_sync(FULL, bytes);
     if (lane == 0 && bytes) atomicAdd(scan_bytes_dev, (unsigned long long)bytes);
-    if constexpr (FUSED) {
-        __syncthreads();
-        for (uint32_t i = t; i < 4 * ra.B; i += LF_THREADS)
-            if (rcnt[i]) atomicAdd(&ra.counters[i], rcnt[i]);
-    }
 }
 
-template <int G, bool FUSED>
-static void launch_leaf(const isax_index *ix, uint32_t nq, uint32_t B, const uint32_t *qmap, float onepd, cudaStream_t s) {
-    constexpr uint32_t NW = FUSED ? LF_SCAN_WARPS : LF_THREADS / 32;
-    const size_t smem = FUSED ? (size_t)G * W * CARD + 256 + RQ * 8 + CHUNK_F * 4 + (size_t)NW * PD * LEAF * sizeof(uint4) +
-                                    (size_t)B * 16 + (size_t)LF_RF_WARPS * RF_SLOTS * (ix->n * 4 + 8)
-                              : (size_t)G * W * CARD + 256 + (size_t)G * CBUF * sizeof(uint32_t) + CHUNK * 4 +
-                                    (size_t)NW * PD * LEAF * sizeof(uint4) + (size_t)G * CBUF;
-    static size_t configured = 0;
-    if (configured < smem) {
-        cudaFuncSetAttribute(leafscan_kernel<G, FUSED>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        configured = smem;
+template <int G>
+static void launch_leaf(const isax_index *ix, uint32_t nq, const uint32_t *qmap, cudaStream_t s) {
+    constexpr uint32_t NW = LF_THREADS / 32;
+    const size_t smem = (size_t)G * W * CARD + 256 + (size_t)G * CBUF * sizeof(uint32_t) + CHUNK * 4 +
+                        (size_t)NW * PD * LEAF * sizeof(uint4) + (size_t)G * CBUF;
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(leafscan_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        configured = true;
     }
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
@@ -976,28 +643,19 @@ static void launch_leaf(const isax_index *ix, uint32_t nq, uint32_t B, const uin
     const uint32_t nleaf = (uint32_t)((ix->N + LEAF - 1) / LEAF);
     // chunk: as large as possible (fewer phase barriers) while leaving >= 8 tasks per SM for
     // balance; a power of two >= 512, so a multiple of SUPER
-    uint32_t chunk = FUSED ? CHUNK_F : CHUNK;
+    uint32_t chunk = CHUNK;
     while (chunk > 512 && (uint64_t)groups * ((nleaf + chunk - 1) / chunk) < 8ull * sms) chunk >>= 1;
     const uint64_t tasks = (uint64_t)groups * ((nleaf + chunk - 1) / chunk);
     const unsigned grid = (unsigned)std::max<uint64_t>(1, umin64(tasks, (uint64_t)sms));
     const QueryScratch &qs = ix->qs;
-    const RefineArgs ra{ix->stored, ix->perm, qs.qy, qs.bsf, qs.qscale, qs.qT, qs.near, qs.near_cnt, qs.counters,
-                        qs.refine_bytes, ix->n, B, onepd};
-    leafscan_kernel<G, FUSED><<<grid, LF_THREADS, smem, s>>>(
+    leafscan_kernel<G><<<grid, LF_THREADS, smem, s>>>(
         reinterpret_cast<const uint4 *>(ix->sax), ix->lmeta, ix->smeta, ix->hmeta, (uint32_t)ix->N, qs.lut, qs.lut8, qs.qconst,
         qs.qsax, qmap, nq, nleaf, chunk, qs.cand, qs.candq, qs.cand_cnt, qs.cand_cap, qs.cand_hist, qs.counters_leaf,
-        qs.scan_bytes_dev, qs.task_ctr, ra);
-}
-
-template <int G>
-static void launch_leaf_any(const isax_index *ix, uint32_t nq, uint32_t B, const uint32_t *qmap, float onepd, bool fused,
-                            cudaStream_t s) {
-    if (fused) launch_leaf<G, true>(ix, nq, B, qmap, onepd, s);
-    else launch_leaf<G, false>(ix, nq, B, qmap, onepd, s);
+        qs.scan_bytes_dev, qs.task_ctr);
 }
 
 uint64_t launch_lbscan(const isax_index *ix, uint32_t nq, uint32_t B, const uint32_t *qmap, const float2 *band,
-                       float delta, bool fused, cudaStream_t s) {
+                       float delta, cudaStream_t s) {
     if (!nq) return 0;
     const float onepd = 1.0f + delta;
     const QueryScratch &qs = ix->qs;
@@ -1012,11 +670,11 @@ uint64_t launch_lbscan(const isax_index *ix, uint32_t nq, uint32_t B, const uint
         return 16ull * ix->N * ((nq + G - 1) / G);  // words read
     }
     const uint32_t G = nq >= 16 ? 16 : nq >= 8 ? 8 : nq >= 4 ? 4 : nq >= 2 ? 2 : 1;
-    if (G == 16) launch_leaf_any<16>(ix, nq, B, qmap, onepd, fused, s);
-    else if (G == 8) launch_leaf_any<8>(ix, nq, B, qmap, onepd, fused, s);
-    else if (G == 4) launch_leaf_any<4>(ix, nq, B, qmap, onepd, fused, s);
-    else if (G == 2) launch_leaf_any<2>(ix, nq, B, qmap, onepd, fused, s);
-    else launch_leaf_any<1>(ix, nq, B, qmap, onepd, fused, s);
+    if (G == 16) launch_leaf<16>(ix, nq, qmap, s);
+    else if (G == 8) launch_leaf<8>(ix, nq, qmap, s);
+    else if (G == 4) launch_leaf<4>(ix, nq, qmap, s);
+    else if (G == 2) launch_leaf<2>(ix, nq, qmap, s);
+    else launch_leaf<1>(ix, nq, qmap, s);
     return 0;  // the leaf scan counts the node summaries and words it reads on the device
 }
 

@@ -65,19 +65,15 @@ def test_query_summary_lb_and_window(N, n):
         assert tuple(dbg["win"][i]) == ref.window(pos, N, 1024)
 
 
-FUSED = 2  # ISAX_FLAG_FUSED_REFINE
-
-
-@pytest.mark.parametrize("flags", [0, FUSED])
 @pytest.mark.parametrize("N,n,kind,q_noisy", [(100_000, 256, "walk", 0), (100_000, 256, "walk", 8),
                                               (20_000, 256, "sines", 16), (7_777, 128, "walk", 4)])
-def test_nn1_matches_oracle(N, n, kind, q_noisy, flags):
+def test_nn1_matches_oracle(N, n, kind, q_noisy):
     wl = small_workload(N, n, kind, Q=16, q_noisy=q_noisy, sigma=0.1)
     x = datagen.series(wl, 0, N)
     q, src = datagen.queries(wl)
     xh, qh = x.cpu().numpy(), q.cpu().numpy()
     ids_or, dist_or, _ = oracle_nn1(xh, qh)
-    with _build(x, flags=flags) as ix:
+    with _build(x) as ix:
         ids, dist = ix.nn1(q)  # device path (isax_nn1_async)
         st = ix.stats()
         ids_h, dist_h = ix.nn1(qh)  # host path (isax_nn1)
@@ -90,9 +86,8 @@ def test_nn1_matches_oracle(N, n, kind, q_noisy, flags):
         assert st["refined"][j] + st["abandoned"][j] >= (w1 - w0)
 
 
-@pytest.mark.parametrize("flags", [0, FUSED])
 @pytest.mark.parametrize("N,n,kind", [(200_000, 256, "walk"), (50_001, 128, "walk"), (30_000, 256, "sines")])
-def test_candidate_set_is_exactly_the_lb_filter(N, n, kind, flags):
+def test_candidate_set_is_exactly_the_lb_filter(N, n, kind):
     """The leaf-pruned scan keeps exactly {pos outside the window : LB^2(pos) <= bsf0^2 (1 + delta)}.
 
     It is compared with the per-position LB^2 from isax_query_debug (the same fp32 order) and
@@ -102,7 +97,7 @@ def test_candidate_set_is_exactly_the_lb_filter(N, n, kind, flags):
     x = datagen.series(wl, 0, N)
     q, _ = datagen.queries(wl)
     qh = q.cpu().numpy()
-    with _build(x, flags=flags) as ix, _build(x, flags=1) as flat:
+    with _build(x) as ix, _build(x, flags=1) as flat:
         ids, dist = ix.nn1(q)
         st = ix.stats()
         ids_f, dist_f = flat.nn1(q)
@@ -129,8 +124,7 @@ def test_candidate_set_is_exactly_the_lb_filter(N, n, kind, flags):
     assert st_f["leaves_alive"] == [0] * len(qh)
 
 
-@pytest.mark.parametrize("flags", [0, FUSED])
-def test_ties_duplicates_constants_and_exact_copies(flags):
+def test_ties_duplicates_constants_and_exact_copies():
     N, n = 5_000, 256
     wl = small_workload(N, n, Q=8)
     x = datagen.series(wl, 0, N).clone()
@@ -145,7 +139,7 @@ def test_ties_duplicates_constants_and_exact_copies(flags):
     q[2] = x[123]
     xh, qh = x.cpu().numpy(), q.cpu().numpy()
     ids_or, dist_or, _ = oracle_nn1(xh, qh)
-    with _build(x, flags=flags) as ix:
+    with _build(x) as ix:
         ids, dist = ix.nn1(q)
     ids, dist = ids.cpu().numpy(), dist.cpu().numpy()
     assert_nn_parity(ids, dist, ids_or, dist_or)
@@ -156,8 +150,7 @@ def test_ties_duplicates_constants_and_exact_copies(flags):
 
 @pytest.mark.parametrize("opts", [dict(window_L=1), dict(window_L=4096), dict(cand_cap=7), dict(batch_Q=3),
                                   dict(slack_log2=-20), dict(probe_bits=0xFFFFFFFF), dict(probe_bits=5, probe_L=1),
-                                  dict(probe_bits=2, probe_L=1024), dict(flags=FUSED, batch_Q=3),
-                                  dict(flags=FUSED, window_L=1, probe_bits=0xFFFFFFFF), dict(flags=FUSED, cand_cap=7)])
+                                  dict(probe_bits=2, probe_L=1024)])
 def test_options_do_not_change_answers(opts):
     N, n = 30_000, 256
     wl = small_workload(N, n, Q=12, q_noisy=4)
@@ -168,7 +161,7 @@ def test_options_do_not_change_answers(opts):
         ids, dist = ix.nn1(q)
         st = ix.stats()
     assert_nn_parity(ids.cpu().numpy(), dist.cpu().numpy(), ids_or, dist_or)
-    if "cand_cap" in opts and not opts.get("flags", 0) & FUSED:
+    if "cand_cap" in opts:
         assert max(st["rounds"]) >= 2  # overflow rounds were exercised
 
 
