@@ -76,7 +76,10 @@ __device__ __forceinline__ float znorm_value(float x, double mu, double sd, doub
     return __double2float_rn(__ddiv_rn(t, sd));
 }
 
-// exclusive prefix of min(cand_cnt[q], cap) over q < Q into pre[0..Q], by the whole CTA
+// exclusive prefix of the list lengths over q < Q into pre[0..Q], by the whole CTA. A list that
+// overflowed (cand_cnt > cap) counts as empty: it holds an arbitrary subset of its query's
+// candidates, and the query rescans the smallest bounds in its next round anyway (R10), so
+// refining it now would be wasted reads.
 template <int NT>
 __device__ __forceinline__ void cand_prefix(const uint32_t *__restrict__ cand_cnt, uint32_t Q, uint32_t cap,
                                             uint32_t *pre) {
@@ -85,7 +88,7 @@ __device__ __forceinline__ void cand_prefix(const uint32_t *__restrict__ cand_cn
     uint32_t carry = 0;
     for (uint32_t b = 0; b < Q; b += NT) {
         const uint32_t q = b + t;
-        const uint32_t v = q < Q ? min(cand_cnt[q], cap) : 0;
+        const uint32_t v = q < Q && cand_cnt[q] <= cap ? cand_cnt[q] : 0;
         uint32_t inc = v;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {

@@ -38,7 +38,7 @@ __global__ void __launch_bounds__(RF_THREADS) refine_kernel(const float *__restr
         uint32_t run = 0;
         for (uint32_t q = 0; q < Q; q++) {
             pre[q] = run;
-            run += min(cand_cnt[q], cap);
+            run += cand_cnt[q] <= cap ? cand_cnt[q] : 0;  // an overflowed list is redone (cand_prefix)
         }
         pre[Q] = run;
     }
