@@ -290,6 +290,12 @@ constexpr uint32_t E_SURE = 237;
 
 // append `keep` lanes' positions for query slot g: shared buffer first, global list if it is full
 // with its u8 bound b (b / sc <= LB^2, for the refine's skip test)
+// Once this CTA sees the query's global list pass its capacity, it sets CB_OVF in the slot's
+// shared count: the list is dropped for the round anyway (R10: an overflowed list is neither
+// refined nor needed, only the histogram is), so candidates beyond the shared buffer are no
+// longer appended (a query with millions of candidates otherwise serialises every CTA on its
+// global count).
+constexpr uint32_t CB_OVF = 0x80000000u;
 __device__ __forceinline__ void emit(bool keep, uint32_t pos, uint32_t b, uint32_t g, uint32_t q, uint32_t lane,
                                      uint32_t lt, uint32_t *cbuf, uint8_t *qbuf, uint32_t *cb_cnt, uint32_t *cand,
                                      uint8_t *candq, uint32_t *cand_cnt, uint32_t cap) {
@@ -314,8 +320,12 @@ __device__ __forceinline__ void emit(bool keep, uint32_t pos, uint32_t b, uint32
         cbuf[g * CBUF + off + r] = pos;
         qbuf[g * CBUF + off + r] = (uint8_t)b;
     }
+    if (off >= CB_OVF) return;  // the query's list overflowed (see above)
     uint32_t goff = 0;
-    if (lane == 0) goff = atomicAdd(&cand_cnt[q], c - room);
+    if (lane == 0) {
+        goff = atomicAdd(&cand_cnt[q], c - room);
+        if (goff + (c - room) > cap) atomicOr(&cb_cnt[g], CB_OVF);
+    }
     goff = __shfl_sync(0xffffffffu, goff, 0);
     if (keep && r >= room) {
         const uint32_t k = goff + r - room;
