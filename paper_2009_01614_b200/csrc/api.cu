@@ -38,7 +38,7 @@ static bool is_device_ptr(const void *p) {
 }
 
 static isax_opts default_opts(const isax_opts *o) {
-    isax_opts r{1024, -12, 1024, 0, 0, 4, 256};  // cand_cap 0: chosen per batch (alloc_scratch, nn1_device)
+    isax_opts r{3072, -12, 1024, 0, 0, 4, 256};  // cand_cap 0: chosen per batch (alloc_scratch, nn1_device)
     if (o) {
         if (o->probe_bits) r.probe_bits = o->probe_bits;
         if (o->probe_L) r.probe_L = o->probe_L;
@@ -204,6 +204,7 @@ static int build_impl(const Source &src, uint64_t N, uint32_t n, uint32_t w, uin
         cudaFree(sax_by_id); cudaFree(keys); cudaFree(musig); cudaFree(ids); cudaFree(bad); cudaFree(inv);
         cudaFree(stage);
         cudaFree(ix->stored); cudaFree(ix->sax); cudaFree(ix->perm); cudaFree(ix->lmeta); cudaFree(ix->smeta); cudaFree(ix->hmeta);
+        cudaFree(ix->skey); cudaFree(ix->ksplit);
         delete ix;
         cudaStreamDestroy(s);
         return code;
@@ -257,6 +258,10 @@ static int build_impl(const Source &src, uint64_t N, uint32_t n, uint32_t w, uin
     TRY(dmalloc(&ix->sax, npad * W, &ix->device_bytes));
     TRY(cudaMemsetAsync(ix->sax + N * W, 0xFF, (npad - N) * W, s));
     launch_gather_sax(sax_by_id, ix->perm, N, ix->sax, s);
+    // kd order inside each super-node (R6b): before the node summaries and the rows
+    TRY(dmalloc(&ix->skey, (N + SUPER_SIZE - 1) / SUPER_SIZE, &ix->device_bytes));
+    TRY(dmalloc(&ix->ksplit, (N + SUPER_SIZE - 1) / SUPER_SIZE, &ix->device_bytes));
+    launch_superkd(ix->sax, ix->perm, N, ix->skey, ix->ksplit, s);
     TRY(dmalloc(&ix->lmeta, ((N + LEAF_SIZE - 1) / LEAF_SIZE) * 32, &ix->device_bytes));
     TRY(dmalloc(&ix->smeta, ((N + SUPER_SIZE - 1) / SUPER_SIZE) * 32, &ix->device_bytes));
     TRY(dmalloc(&ix->hmeta, ((N + HYPER_SIZE - 1) / HYPER_SIZE) * 32, &ix->device_bytes));
@@ -706,6 +711,8 @@ void isax_free(isax_index *ix) {
         cudaFree(ix->lmeta);
         cudaFree(ix->smeta);
         cudaFree(ix->hmeta);
+        cudaFree(ix->skey);
+        cudaFree(ix->ksplit);
         free_scratch(ix);
         for (auto &ev : ix->ev)
             if (ev) cudaEventDestroy(ev);

@@ -146,6 +146,8 @@ struct isax_index {
     float *stored = nullptr;
     uint8_t *sax = nullptr;
     uint32_t *perm = nullptr;
+    uint4 *skey = nullptr;     // [ceil(N/SUPER_SIZE)] z key of each super-node's first z-order position (R6b)
+    uint2 *ksplit = nullptr;   // [ceil(N/SUPER_SIZE)] first two kd splits of each full super-node (R6b)
     uint8_t *lmeta = nullptr;  // [ceil(N/LEAF_SIZE)][32]: per-leaf min (16 B) and max (16 B) symbols
     uint8_t *smeta = nullptr;  // [ceil(N/SUPER_SIZE)][32]: per-super-node min and max symbols
     uint8_t *hmeta = nullptr;  // [ceil(N/HYPER_SIZE)][32]: per-hyper-node min and max symbols
@@ -208,6 +210,9 @@ void launch_lb_dump(const isax_index *ix, uint32_t Q, uint64_t first_pos, uint64
                     cudaStream_t s);
 // lbscan.cu
 void launch_leaf_meta(const uint8_t *sax, uint64_t N, uint8_t *lmeta, uint8_t *smeta, uint8_t *hmeta, cudaStream_t s);
+// permute.cu: the kd order inside every full super-node (R6b), the super-nodes' smallest keys and
+// their first two kd splits (sax and perm are permuted in place)
+void launch_superkd(uint8_t *sax, uint32_t *perm, uint64_t N, uint4 *skey, uint2 *ksplit, cudaStream_t s);
 // Scan all sorted positions for the nq queries qmap[0..nq), keeping band[i].x < LB^2 <= min(band[i].y,
 // bsf^2 (1+delta)) for slot i. Returns the summary bytes it reads that the host can count (node
 // summaries or flat words); the leaf scan adds its leaf-word and leaf-summary bytes to qs.scan_bytes_dev on the device.

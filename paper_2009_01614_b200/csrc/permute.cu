@@ -104,4 +104,146 @@ void launch_export_sax(const uint8_t *sax, const uint32_t *inv, uint64_t first_i
                                                                count, reinterpret_cast<uint4 *>(out));
 }
 
+
+// ------------------------------------------------------------------------------------ super-node kd order
+// (R6b) The z order groups series by key prefix, but a leaf of 32 consecutive positions often
+// straddles key boundaries, which widens its per-segment [min, max] box. Inside every full
+// super-node (SUPER_SIZE = 1024 consecutive positions of the z order) the positions are reordered
+// by a kd split down to leaves, so the 32 leaves of a super-node have tight boxes:
+//   at each level, every node (a contiguous half of its parent) takes the segment s with the
+//   largest symbol range max_s - min_s over its members (the lowest s on ties) and is sorted by
+//   symbol s, stably (equal symbols keep their order); its halves are its children.
+// Membership of super-nodes and hyper-nodes is unchanged, so their boxes are too. Offline on 4M
+// random walks this cut the members tested under alive leaves by 14%.
+// Per super-node it also records the z key of its first position (the block's smallest key, for
+// the approximate answer's search) and the first two split levels (segment and the smallest
+// symbol of the right half) for locating a 256-row quarter.
+// One CTA per full super-node, 512 threads; each level is a bitonic sort of the 1024 keys
+// (node << 18 | symbol << 10 | position), so the order is exactly the stable one.
+constexpr int KD_THREADS = 512;
+
+__global__ void __launch_bounds__(KD_THREADS) superkd_kernel(uint4 *__restrict__ sax, uint32_t *__restrict__ perm,
+                                                          uint64_t nfull, uint4 *__restrict__ skey,
+                                                          uint2 *__restrict__ ksplit) {
+    constexpr uint32_t S = SUPER_SIZE, LV = 5;  // 1024 -> 32
+    static_assert(SUPER_SIZE == 1024 && LEAF_SIZE == 32, "five kd levels per super-node");
+    __shared__ uint4 wa[S], wb[S];
+    __shared__ uint32_t ia[S], ib[S];
+    __shared__ uint32_t key[S];
+    __shared__ uint32_t mn[16][W], mx[16][W];
+    __shared__ uint32_t segsel[16], lvseg[3];
+    const uint32_t t = threadIdx.x;
+    const uint64_t b = blockIdx.x;
+    if (b >= nfull) return;
+    uint4 *wcur = wa, *wnxt = wb;
+    uint32_t *icur = ia, *inxt = ib;
+    for (uint32_t i = t; i < S; i += KD_THREADS) {
+        wa[i] = sax[b * S + i];
+        ia[i] = perm[b * S + i];
+    }
+    __syncthreads();
+    if (t == 0) skey[b] = word_key(wa[0]);
+    for (uint32_t lv = 0; lv < LV; lv++) {
+        const uint32_t size = S >> lv, nodes = 1u << lv, sh = 10 - lv;
+        for (uint32_t i = t; i < nodes * W; i += KD_THREADS) {
+            mn[i / W][i % W] = 255u;
+            mx[i / W][i % W] = 0u;
+        }
+        __syncthreads();
+        for (uint32_t i = t; i < S; i += KD_THREADS) {
+            const uint4 wv = wcur[i];
+            const uint32_t v[4] = {wv.x, wv.y, wv.z, wv.w};
+            const uint32_t nd = i >> sh;
+#pragma unroll
+            for (int s = 0; s < W; s++) {
+                const uint32_t c = (v[s >> 2] >> (8 * (s & 3))) & 0xFFu;
+                atomicMin(&mn[nd][s], c);
+                atomicMax(&mx[nd][s], c);
+            }
+        }
+        __syncthreads();
+        if (t < nodes) {
+            uint32_t best = 0, br = 0;
+            for (uint32_t s = 0; s < W; s++) {
+                const uint32_t r = mx[t][s] - mn[t][s];
+                if (r > br) {  // strictly larger: the lowest segment wins ties
+                    br = r;
+                    best = s;
+                }
+            }
+            segsel[t] = best;
+            if (lv == 0) lvseg[0] = best;
+            if (lv == 1) lvseg[1 + t] = best;
+        }
+        __syncthreads();
+        for (uint32_t i = t; i < S; i += KD_THREADS) {
+            const uint4 wv = wcur[i];
+            const uint32_t v[4] = {wv.x, wv.y, wv.z, wv.w};
+            const uint32_t nd = i >> sh, s = segsel[nd];
+            const uint32_t c = (v[s >> 2] >> (8 * (s & 3))) & 0xFFu;
+            key[i] = (nd << 18) | (c << 10) | i;
+        }
+        __syncthreads();
+        // bitonic sort of the 1024 keys (all distinct), ascending
+        for (uint32_t k = 2; k <= S; k <<= 1) {
+            for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+                for (uint32_t i = t; i < S; i += KD_THREADS) {
+                    const uint32_t p = i ^ j;
+                    if (p > i) {
+                        const uint32_t a = key[i], c = key[p];
+                        const bool up = (i & k) == 0;
+                        if ((a > c) == up) {
+                            key[i] = c;
+                            key[p] = a;
+                        }
+                    }
+                }
+                __syncthreads();
+            }
+        }
+        for (uint32_t i = t; i < S; i += KD_THREADS) {
+            const uint32_t src = key[i] & 1023u;
+            wnxt[i] = wcur[src];
+            inxt[i] = icur[src];
+        }
+        __syncthreads();
+        uint4 *tw = wcur; wcur = wnxt; wnxt = tw;
+        uint32_t *ti = icur; icur = inxt; inxt = ti;
+    }
+    // the first two levels' splits: segment and smallest symbol of the right half
+    if (t < 3) {
+        const uint32_t s = lvseg[t];
+        const uint32_t r0 = t == 0 ? S / 2 : t == 1 ? S / 4 : 3 * S / 4, r1 = t == 0 ? S : r0 + S / 4;
+        uint32_t m = 255u;
+        for (uint32_t i = r0; i < r1; i++) {
+            const uint4 wv = wcur[i];
+            const uint32_t v[4] = {wv.x, wv.y, wv.z, wv.w};
+            m = min(m, (v[s >> 2] >> (8 * (s & 3))) & 0xFFu);
+        }
+        key[t] = s | (m << 8);
+    }
+    __syncthreads();
+    if (t == 0) ksplit[b] = make_uint2(key[0] | (key[1] << 16), key[2]);
+    for (uint32_t i = t; i < S; i += KD_THREADS) {
+        sax[b * S + i] = wcur[i];
+        perm[b * S + i] = icur[i];
+    }
+}
+
+// the last, partial super-node keeps the z order; it still gets its smallest key
+__global__ void superkey_tail_kernel(const uint4 *__restrict__ sax, uint64_t first, uint4 *__restrict__ skey,
+                                     uint2 *__restrict__ ksplit, uint64_t s) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        skey[s] = word_key(sax[first]);
+        ksplit[s] = make_uint2(0xFFFFFFFFu, 0xFFFFFFFFu);  // no kd splits: quarters are not located
+    }
+}
+
+void launch_superkd(uint8_t *sax, uint32_t *perm, uint64_t N, uint4 *skey, uint2 *ksplit, cudaStream_t s) {
+    const uint64_t nfull = N / SUPER_SIZE;
+    if (nfull) superkd_kernel<<<(unsigned)nfull, KD_THREADS, 0, s>>>(reinterpret_cast<uint4 *>(sax), perm, nfull, skey, ksplit);
+    if (N % SUPER_SIZE)
+        superkey_tail_kernel<<<1, 32, 0, s>>>(reinterpret_cast<const uint4 *>(sax), nfull * SUPER_SIZE, skey, ksplit, nfull);
+}
+
 }  // namespace isax

@@ -7,9 +7,9 @@
 //                LUT[s][c] = (n/w) * max(0, beta_c - m_s, m_s - beta_{c+1})^2 in fp64, rounded
 //                DOWN to fp32 (R7), so an fp32 sum of LUT entries never
 //                overestimates the fp64 bound by more than its own summation error.
-//                locate: the first sorted position whose key is >= the query key. One warp
-//                runs a 32-ary search: each step probes 32 positions, so ~6 dependent loads
-//                at N = 1e8 (R5).
+//                locate: the super-node whose z-order key range holds the query key (the last
+//                one whose smallest key is below it; R5, R6b). One warp runs a 32-ary search
+//                over the super-nodes' smallest keys: ~4 dependent loads at N = 1e8.
 //  window_kernel one CTA per query refines the L sorted rows around that position. P:271-272:
 //                "the real distance between the query and the best candidate series, which is
 //                in the leaf with the smallest lower bound distance"; P:341-345 for MESSI.
@@ -24,7 +24,8 @@ namespace isax {
 __constant__ double c_beta_q[ISAX_NBETA] = ISAX_BETA_INIT;
 
 __global__ void __launch_bounds__(256) qprep_kernel(const float *__restrict__ queries, uint32_t n,
-                                                    const uint4 *__restrict__ sax, uint64_t N, uint32_t L,
+                                                    const uint4 *__restrict__ skey, const uint2 *__restrict__ ksplit,
+                                                    uint64_t N, uint32_t L,
                                                     uint32_t P, uint32_t Lp, uint32_t *__restrict__ pwin,
                                                     float *__restrict__ qy, double *__restrict__ qpaa,
                                                     uint8_t *__restrict__ qsax, float *__restrict__ lut,
@@ -129,11 +130,13 @@ __global__ void __launch_bounds__(256) qprep_kernel(const float *__restrict__ qu
         for (uint32_t b = 0; b < P; b++)
             if ((j >> b) & 1u) sy[sel_s[b]] = sel_c[b];
         const uint4 kq = isax_key(sy);
-        uint64_t lo = 0, hi = N;
+        // super-node of the key (R5, R6b): the last one whose smallest key is below it
+        const uint64_t nsup = (N + SUPER_SIZE - 1) / SUPER_SIZE;
+        uint64_t lo = 0, hi = nsup;
         while (hi - lo > 32) {
             const uint64_t span = hi - lo;
             const uint64_t p = lo + (span * (lane + 1)) / 33;
-            const bool less = key_less(word_key(__ldg(sax + p)), kq);
+            const bool less = key_less(__ldg(skey + p), kq);
             const uint32_t bal = __ballot_sync(0xffffffffu, less);
             const uint32_t c = __popc(bal);  // probes are increasing, so `less` is a prefix
             const uint64_t p_last = __shfl_sync(0xffffffffu, p, (c == 0 ? 0 : c - 1));
@@ -144,10 +147,24 @@ __global__ void __launch_bounds__(256) qprep_kernel(const float *__restrict__ qu
                 if (c < 32) hi = p_next;
             }
         }
-        const bool less = (lo + lane < hi) && key_less(word_key(__ldg(sax + lo + lane)), kq);
-        const uint64_t pos = lo + __popc(__ballot_sync(0xffffffffu, less));
+        const bool less = (lo + lane < hi) && key_less(__ldg(skey + lo + lane), kq);
+        const uint64_t c = lo + __popc(__ballot_sync(0xffffffffu, less));
+        const uint64_t sq = c > 0 ? c - 1 : 0;
         if (lane == 0) {
             const uint32_t len = j == 0 ? L : Lp;
+            // the main window is whole super-nodes around that one: with an odd count (L = 1024,
+            // 3072) it is centred on it, with an even count (2048) it is it and the next. The keys
+            // just below the query's are at its end or in the one before, the keys just above in
+            // it or the next. A probe window sits on the quarter of its super-node that the first
+            // two kd splits send the probe's symbols to.
+            uint64_t pos = sq * SUPER_SIZE + SUPER_SIZE / 2 + (((L / SUPER_SIZE) & 1u) ? 0u : SUPER_SIZE / 2);
+            const uint2 ks = __ldg(ksplit + sq);
+            if (j > 0 && ks.x != 0xFFFFFFFFu) {
+                const uint32_t h = sy[ks.x & 0xFFu] >= ((ks.x >> 8) & 0xFFu);
+                const uint32_t sp = h ? ks.y & 0xFFFFu : ks.x >> 16;
+                const uint32_t qt = 2 * h + (sy[sp & 0xFFu] >= (sp >> 8));
+                pos = sq * SUPER_SIZE + qt * (SUPER_SIZE / 4) + SUPER_SIZE / 8;
+            }
             uint64_t start = 0;
             if (N > len) {
                 const int64_t s0 = (int64_t)pos - (int64_t)(len / 2);
@@ -166,7 +183,7 @@ __global__ void __launch_bounds__(256) qprep_kernel(const float *__restrict__ qu
 
 void launch_qprep(const isax_index *ix, const float *queries, uint32_t Q, cudaStream_t s, uint32_t *bad) {
     const QueryScratch &qs = ix->qs;
-    qprep_kernel<<<Q, 256, 0, s>>>(queries, ix->n, reinterpret_cast<const uint4 *>(ix->sax), ix->N,
+    qprep_kernel<<<Q, 256, 0, s>>>(queries, ix->n, ix->skey, ix->ksplit, ix->N,
                                    ix->opts.window_L, probe_bits(ix), ix->opts.probe_L, qs.pwin, qs.qy, qs.qpaa, qs.qsax, qs.lut, qs.win, qs.bsf, qs.cand_cnt,
                                    qs.near_cnt, qs.counters, qs.counters_leaf, bad);
 }

@@ -35,7 +35,7 @@ def test_summaries_perm_and_rows_bit_exact(N, n, kind):
         ex = ix.export(0, N, sax=True, perm=True, stored=True)
     y, mu, sd, m, word = clib.summarise(xh)
     np.testing.assert_array_equal(ex["sax"], word)  # C4 words, by id
-    perm = ref.canonical_order(word)  # C5
+    perm = ref.sorted_order(word)  # C5 z order, kd order inside each full super-node (R6b)
     np.testing.assert_array_equal(ex["perm"].astype(np.int64), perm)
     np.testing.assert_array_equal(ex["stored"], y[perm])  # C1 rows, in sorted order
 
@@ -53,16 +53,13 @@ def test_query_summary_lb_and_window(N, n):
     np.testing.assert_array_equal(dbg["q_paa"], qm)
     np.testing.assert_array_equal(dbg["q_sax"], qw)
     words_sorted = ex["sax"][ex["perm"]]
-    hi, lo = ref.isax_keys(words_sorted)
-    qhi, qlo = ref.isax_keys(qw)
     for i in range(len(qh)):
         lb_or = ref.lb2(qm[i], words_sorted, n)  # C6, fp64
         lb_gpu = dbg["lb2"][i].astype(np.float64)
         # fp32 sum of 16 rounded-down terms: never above the fp64 bound beyond summation error
         assert np.all(lb_gpu <= lb_or * (1 + 2e-6) + 1e-30)
         assert np.all(lb_gpu >= lb_or * (1 - 1e-5) - 1e-6)
-        pos = ref.lower_bound_pos(hi, lo, qhi[i], qlo[i])
-        assert tuple(dbg["win"][i]) == ref.window(pos, N, 1024)
+        assert tuple(dbg["win"][i]) == ref.super_window(ex["sax"], qw[i], 3072)
 
 
 @pytest.mark.parametrize("N,n,kind,q_noisy", [(100_000, 256, "walk", 0), (100_000, 256, "walk", 8),
