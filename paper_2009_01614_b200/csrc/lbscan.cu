@@ -111,6 +111,11 @@ __device__ __forceinline__ uint32_t node_e8(uint32_t ub, const uint4 &qa, const 
     return es;
 }
 
+__device__ __forceinline__ uint32_t ld_sh_u32(const uint32_t *p) {
+    uint32_t r;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(r) : "r"((uint32_t)__cvta_generic_to_shared(p)));
+    return r;
+}
 __device__ __forceinline__ uint4 ld_sh_v4(const uint4 *p) {
     uint4 r;
     asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
@@ -548,9 +553,12 @@ __global__ void __launch_bounds__(LF_THREADS, 1) leafscan_kernel(
 #pragma unroll
             for (int g = 0; g < G; g++) {
                 if (!((cur_mask >> g) & 1u)) continue;
-                if (node_e8(lut8_sh + g * W * CARD, qsym[g][0], qsym[g][1], mn4, mx4) <= 254u) alive |= 1u << g;
+                const bool ok = leaf < c1 && node_e8(lut8_sh + g * W * CARD, qsym[g][0], qsym[g][1], mn4, mx4) <= 254u;
+                if (ok) alive |= 1u << g;
+                // (leaf, query g) pairs that phase B will test, counted by lane g (stats)
+                const uint32_t np = __popc(__ballot_sync(FULL, ok));
+                if (lane == (uint32_t)g) my_alive += np;
             }
-            if (leaf >= c1) alive = 0;
             const uint32_t bal = __ballot_sync(FULL, alive != 0);
             if (bal) {
                 uint32_t off = 0;
@@ -580,13 +588,10 @@ __global__ void __launch_bounds__(LF_THREADS, 1) leafscan_kernel(
         for (uint32_t e = warp; e < nwl; e += NW) {
             prefetch(e + (PD - 1) * NW, (slot + PD - 1) % PD);
             cp_async_wait<PD - 1>();
-            const uint32_t ent = worklist[e];
-            const uint32_t mask = ent >> 16;
-            const uint32_t pos = (c0 + (ent & 0xFFFFu)) * LEAF + lane;
+            const uint32_t mask = worklist[e] >> 16;
             const uint4 *wp = ring + slot * LEAF;
             const uint4 wv = *wp;
             slot = (slot + 1) % PD;
-            if (lane < G) my_alive += (mask >> lane) & 1u;
             // rolled loop over the queries that kept the leaf: unrolling it over G made the
             // kernel ~120 KB of SASS, and instruction-cache misses became the top stall
 #pragma unroll 1
@@ -607,6 +612,8 @@ __global__ void __launch_bounds__(LF_THREADS, 1) leafscan_kernel(
                 // bands every member gets it here. A first-band member's histogram bin comes from
                 // its u8 sum, never above its exact bin (band shrinking, R10, stays an upper bound
                 // on the count).
+                // the position, from the entry re-read here (volatile): only this rare path needs it
+                const uint32_t pos = (c0 + (ld_sh_u32(worklist + e) & 0xFFFFu)) * LEAF + lane;
                 const bool maybe = pos < N && e8 <= 254u;
                 const QConst kq = qc[g];
                 const bool band0 = kq.lo < 0.f;
