@@ -23,6 +23,13 @@ namespace isax {
 
 __constant__ double c_beta_q[ISAX_NBETA] = ISAX_BETA_INIT;
 
+// The main window covers whole super-nodes around the query key's (R5, R6b). With window_L <
+// 3072 the two neighbouring super-nodes are covered by their kd-descended quarters instead (two
+// extra probe-sized windows), when the probe table has room for them.
+__host__ __device__ __forceinline__ uint32_t neighbour_windows(uint32_t L, uint32_t P) {
+    return (L < 3 * SUPER_SIZE && (1u << P) + 1 <= MAX_PROBES - 1) ? 2u : 0u;
+}
+
 __global__ void __launch_bounds__(256) qprep_kernel(const float *__restrict__ queries, uint32_t n,
                                                     const uint4 *__restrict__ skey, const uint2 *__restrict__ ksplit,
                                                     uint64_t N, uint32_t L,
@@ -122,6 +129,7 @@ __global__ void __launch_bounds__(256) qprep_kernel(const float *__restrict__ qu
     }
     __syncthreads();
     const uint32_t NP = 1u << P;
+    const uint32_t NX = neighbour_windows(L, P);  // 2 extra windows (see neighbour_windows)
     const uint32_t warp = t >> 5, lane = t & 31;
     for (uint32_t j = warp; j < NP; j += blockDim.x / 32) {  // locate each probe key, one warp per probe
         uint32_t sy[W];
@@ -174,6 +182,26 @@ __global__ void __launch_bounds__(256) qprep_kernel(const float *__restrict__ qu
             if (j == 0) {
                 win[2 * q] = (uint32_t)start;
                 win[2 * q + 1] = (uint32_t)(start + (N > len ? len : N));
+                if (NX) {  // the kd-descended quarters of the neighbouring super-nodes (R5, R6b)
+                    for (uint32_t k = 0; k < 2; k++) {
+                        uint64_t sn = k == 0 ? (sq > 0 ? sq - 1 : sq + 1) : (sq + 1 < nsup ? sq + 1 : (sq > 0 ? sq - 1 : sq));
+                        sn = sn < nsup ? sn : nsup - 1;
+                        uint64_t p2 = sn * SUPER_SIZE + SUPER_SIZE / 2;
+                        const uint2 k2 = __ldg(ksplit + sn);
+                        if (k2.x != 0xFFFFFFFFu) {
+                            const uint32_t h = sy[k2.x & 0xFFu] >= ((k2.x >> 8) & 0xFFu);
+                            const uint32_t sp = h ? k2.y & 0xFFFFu : k2.x >> 16;
+                            const uint32_t qt = 2 * h + (sy[sp & 0xFFu] >= (sp >> 8));
+                            p2 = sn * SUPER_SIZE + qt * (SUPER_SIZE / 4) + SUPER_SIZE / 8;
+                        }
+                        uint64_t st2 = 0;
+                        if (N > Lp) {
+                            const int64_t a = (int64_t)p2 - (int64_t)(Lp / 2), smax = (int64_t)(N - Lp);
+                            st2 = (uint64_t)(a < 0 ? 0 : (a > smax ? smax : a));
+                        }
+                        pwin[q * (MAX_PROBES - 1) + NP - 1 + k] = (uint32_t)st2;
+                    }
+                }
             } else {
                 pwin[q * (MAX_PROBES - 1) + j - 1] = (uint32_t)start;
             }
@@ -319,7 +347,7 @@ void launch_window(const isax_index *ix, uint32_t Q, const uint32_t *qmap, float
     const QueryScratch &qs = ix->qs;
     const float onepd = 1.0f + delta;
     const uint32_t ns = (ix->n + 127) / 128;
-    const uint32_t nprobe = (1u << probe_bits(ix)) - 1;
+    const uint32_t nprobe = (1u << probe_bits(ix)) - 1 + neighbour_windows(ix->opts.window_L, probe_bits(ix));
     const uint32_t lp = (uint32_t)(ix->N < ix->opts.probe_L ? ix->N : ix->opts.probe_L);
     const uint32_t L = (uint32_t)(ix->N < ix->opts.window_L ? ix->N : ix->opts.window_L);
     const uint32_t rows = L + nprobe * lp;
