@@ -119,6 +119,10 @@ __global__ void __launch_bounds__(RF_THREADS) refine_kernel(const float *__restr
 // The BSF threshold is refreshed from L2 every RF_REFRESH candidates; a stale value is only
 // looser. Same arithmetic contract as refine_kernel.
 constexpr uint32_t RF_REFRESH = 4;
+#ifndef ISAX_RF_C
+#define ISAX_RF_C 2
+#endif
+constexpr int RF_C = ISAX_RF_C;  // candidates in flight per quarter warp
 
 template <int NH>
 __global__ void __launch_bounds__(RF_THREADS) refine_q_kernel(const float *__restrict__ stored,
@@ -157,25 +161,25 @@ __global__ void __launch_bounds__(RF_THREADS) refine_q_kernel(const float *__res
     const uint32_t per = (total + nquart - 1) / nquart;
     const uint32_t qi = (blockIdx.x * RF_THREADS + t) >> 3;
     const uint32_t fbeg = min(qi * per, total), fend = min(fbeg + per, total);
-    for (uint32_t f0 = fbeg; f0 < fend; f0 += 2) {
-        uint32_t qv[2], pv[2];
-        bool live[2];
+    for (uint32_t f0 = fbeg; f0 < fend; f0 += RF_C) {
+        uint32_t qv[RF_C], pv[RF_C];
+        bool live[RF_C];
 #pragma unroll
-        for (int c = 0; c < 2; c++) {
+        for (int c = 0; c < RF_C; c++) {
             const uint32_t f = f0 + c;
             live[c] = f < fend;
             qv[c] = live[c] ? locate(f) : 0;
             pv[c] = live[c] ? cand[(uint64_t)qv[c] * cap + (f - pre[qv[c]])] : 0;
         }
-        float4 v[2][NH];
+        float4 v[RF_C][NH];
 #pragma unroll
-        for (int c = 0; c < 2; c++)
+        for (int c = 0; c < RF_C; c++)
 #pragma unroll
             for (int k = 0; k < NH; k++)
                 v[c][k] = live[c] ? __ldcs(reinterpret_cast<const float4 *>(stored + (uint64_t)pv[c] * n) + k * 8 + ql)
                                   : make_float4(0, 0, 0, 0);
 #pragma unroll
-        for (int c = 0; c < 2; c++) {
+        for (int c = 0; c < RF_C; c++) {
             if (!live[c]) continue;
             const uint32_t q = qv[c], pos = pv[c];
             if (q != cur_q) {
