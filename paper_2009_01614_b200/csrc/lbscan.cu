@@ -284,7 +284,10 @@ static_assert(HYPER == 32, "phase A maps the super-nodes of a hyper-node to the 
 static_assert(LEAF == 32 && SUPER == 32, "phase A maps a super-node to a warp iteration and a leaf to a lane");
 constexpr int LF_THREADS = 1024;
 constexpr uint32_t CHUNK = 8192;  // max leaves per phase-A/phase-B round of a CTA
-constexpr uint32_t CBUF = 512;    // shared candidate buffer per query slot
+#ifndef ISAX_CBUF
+#define ISAX_CBUF 512
+#endif
+constexpr uint32_t CBUF = ISAX_CBUF;  // shared candidate buffer per query slot
 #ifndef ISAX_PD
 #define ISAX_PD 4
 #endif
