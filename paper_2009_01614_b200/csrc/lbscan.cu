@@ -70,27 +70,6 @@ __device__ __forceinline__ uint32_t word_e8(uint32_t ub, const uint4 &wv) {
     for (int s = 0; s < W; s++) es += ld_sh_u8(__byte_perm(v[s >> 2], ub, 0x7650u | (uint32_t)(s & 3)) + s * CARD);
     return es;
 }
-// the same sum with the additions on the FMA pipe (IMAD with a multiplier the compiler cannot see
-// is 1), leaving the ALU pipe to the PRMT address forms; two chains of 8
-__device__ __forceinline__ uint32_t mad_u32(uint32_t a, uint32_t b, uint32_t c) {
-    uint32_t d;
-    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
-    return d;
-}
-__device__ __forceinline__ uint32_t word_e8_fma(uint32_t ub, const uint4 &wv, uint32_t one) {
-    const uint32_t v[4] = {wv.x, wv.y, wv.z, wv.w};
-    uint32_t l[W];
-#pragma unroll
-    for (int s = 0; s < W; s++) l[s] = ld_sh_u8(__byte_perm(v[s >> 2], ub, 0x7650u | (uint32_t)(s & 3)) + s * CARD);
-    uint32_t a = l[0], b = l[1];
-#pragma unroll
-    for (int s = 2; s < W; s += 2) {
-        a = mad_u32(l[s], one, a);
-        b = mad_u32(l[s + 1], one, b);
-    }
-    return mad_u32(a, one, b);
-}
-
 // u8 node bound (R11, R11b) of a node summary (per-segment min mn, max mx) against one query:
 // q holds the query's symbols as 8 u16x2 pairs; each term is the table entry at the clamped
 // symbol, clamp(q_s, mn_s, mx_s), done two segments at a time with u16x2 min / max.
@@ -577,7 +556,6 @@ __global__ void __launch_bounds__(LF_THREADS, 1) leafscan_kernel(
         // A lane copies and reads only its own word, so no warp barrier is needed. The sorted SAX
         // array is padded to whole leaves (api.cu), so the loads need no bounds test.
         const uint32_t nwl = wl_cnt;
-        const uint32_t one = blockDim.x / LF_THREADS;  // 1, opaque to the compiler (word_e8_fma)
         if (t == 0) bytes += nwl * LEAF * 16u;  // the worklist leaves' words (a partial last leaf is counted whole)
         uint4 *ring = stage + warp * PD * LEAF + lane;  // [PD slots][LEAF] words; this lane's column
         const uint4 *saxc = sax + (uint64_t)c0 * LEAF + lane;
@@ -602,11 +580,7 @@ __global__ void __launch_bounds__(LF_THREADS, 1) leafscan_kernel(
                 const uint32_t g = __ffs(mm) - 1;
                 // integer member filter: 16 lookups of 2.5 instructions (PRMT address, LDS.U8, half
                 // an IADD3)
-#ifdef ISAX_E8_FMA
-                const uint32_t e8 = word_e8_fma(lut8_sh + g * W * CARD, wv, one);
-#else
                 const uint32_t e8 = word_e8(lut8_sh + g * W * CARD, wv);
-#endif
                 if (!__any_sync(FULL, e8 <= 254u)) continue;
                 // The flat scan's rule is lo < LB^2 <= T on the exact fp32 bound. A u8 sum <= E_SURE
                 // already implies LB^2 <= T (R11b), and in the first band (lo < 0) lo < LB^2 always
@@ -706,7 +680,10 @@ uint64_t launch_lbscan(const isax_index *ix, uint32_t nq, uint32_t B, const uint
 // lookups summed left to right). Every list is compacted into cand2 (order is immaterial, R9);
 // the kept ones' u8 bound becomes floor(LB^2 * sc).
 constexpr int CK_THREADS = 256;
-constexpr uint32_t B_SPLIT = 140;     // second refine pass: b > B_SPLIT, i.e. LB^2 above about 0.55 T
+#ifndef ISAX_BSPLIT
+#define ISAX_BSPLIT 140
+#endif
+constexpr uint32_t B_SPLIT = ISAX_BSPLIT;  // second refine pass: b > B_SPLIT, i.e. LB^2 above about 0.55 T
 constexpr uint32_t SPLIT_MIN = 4096;  // ... for queries with more candidates than this
 constexpr uint32_t SPLIT_TARGET = 65536;  // first-pass size a lowered split aims at
 
