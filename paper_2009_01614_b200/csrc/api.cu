@@ -634,10 +634,10 @@ int isax_stats(const isax_index *cix, char *buf, size_t cap) {
     std::string j = "{";
     char tmp[256];
     snprintf(tmp, sizeof tmp,
-             "\"N\":%llu,\"n\":%u,\"window_L\":%u,\"slack_log2\":%d,\"batch_Q\":%u,\"cand_cap\":%u,"
+             "\"N\":%llu,\"n\":%u,\"window_L\":%u,\"probe_windows\":%u,\"probe_L\":%u,\"slack_log2\":%d,\"batch_Q\":%u,\"cand_cap\":%u,"
              "\"ms_first_batch\":{\"qprep\":%.4f,\"window\":%.4f,\"lbscan\":%.4f,\"candcheck\":%.4f,\"refine\":%.4f,\"total\":%.4f},",
-             (unsigned long long)ix->N, ix->n, ix->opts.window_L, ix->opts.slack_log2, ix->opts.batch_Q,
-             ix->qs.cand_cap, ix->st_ms.qprep, ix->st_ms.window, ix->st_ms.lbscan, ix->st_ms.candcheck, ix->st_ms.refine,
+             (unsigned long long)ix->N, ix->n, ix->opts.window_L, window_probes(ix), ix->opts.probe_L, ix->opts.slack_log2,
+             ix->opts.batch_Q, ix->qs.cand_cap, ix->st_ms.qprep, ix->st_ms.window, ix->st_ms.lbscan, ix->st_ms.candcheck, ix->st_ms.refine,
              ix->st_ms.finalize);
     j += tmp;
     auto arr = [&](const char *name, const std::vector<uint32_t> &v, bool last) {

@@ -205,6 +205,7 @@ void launch_export_sax(const uint8_t *sax, const uint32_t *inv, uint64_t first_i
 // query.cu
 void launch_qprep(const isax_index *ix, const float *queries, uint32_t Q, cudaStream_t s, uint32_t *bad);
 uint32_t probe_bits(const isax_index *ix);
+uint32_t window_probes(const isax_index *ix);  // probe-sized windows per query (incl. neighbour quarters)
 void launch_window(const isax_index *ix, uint32_t Q, const uint32_t *qmap, float delta, cudaStream_t s);
 void launch_lb_dump(const isax_index *ix, uint32_t Q, uint64_t first_pos, uint64_t count, float *out,
                     cudaStream_t s);

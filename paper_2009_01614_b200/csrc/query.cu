@@ -343,6 +343,10 @@ uint32_t probe_bits(const isax_index *ix) {
     return ix->opts.probe_bits == ISAX_PROBES_NONE ? 0u : ix->opts.probe_bits;
 }
 
+uint32_t window_probes(const isax_index *ix) {
+    return (1u << probe_bits(ix)) - 1 + neighbour_windows(ix->opts.window_L, probe_bits(ix));
+}
+
 void launch_window(const isax_index *ix, uint32_t Q, const uint32_t *qmap, float delta, cudaStream_t s) {
     const QueryScratch &qs = ix->qs;
     const float onepd = 1.0f + delta;
