@@ -377,8 +377,10 @@ static int nn1_device(isax_index *ix, const float *d_q, uint32_t Q, int64_t *d_i
                     rewin.clear();
                 }
             }
-            ISAX_CUDA(cudaMemcpyAsync(qs.qmap, hm.qmap, nact * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
-            ISAX_CUDA(cudaMemcpyAsync(qs.qband, hm.band, nact * sizeof(float2), cudaMemcpyHostToDevice, s));
+            if (round > 0) {  // (round 0's identity map and open bands are written by qprep_kernel)
+                ISAX_CUDA(cudaMemcpyAsync(qs.qmap, hm.qmap, nact * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+                ISAX_CUDA(cudaMemcpyAsync(qs.qband, hm.band, nact * sizeof(float2), cudaMemcpyHostToDevice, s));
+            }
             ix->st_scan_bytes += launch_lbscan(ix, nact, B, qs.qmap, qs.qband, delta, s);
             if (timed && round == 0) cudaEventRecord(ix->ev[6], s);
             launch_candcheck(ix, B, s);

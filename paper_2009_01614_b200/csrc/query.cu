@@ -39,6 +39,7 @@ __global__ void __launch_bounds__(256) qprep_kernel(const float *__restrict__ qu
                                                     uint32_t *__restrict__ win, unsigned long long *__restrict__ bsf,
                                                     uint32_t *__restrict__ cand_cnt, uint32_t *__restrict__ near_cnt,
                                                     uint32_t *__restrict__ counters, uint32_t *__restrict__ counters_leaf,
+                                                    uint32_t *__restrict__ qmap, float2 *__restrict__ qband,
                                                     uint32_t *__restrict__ bad) {
     __shared__ float row[1024];
     __shared__ double beta[ISAX_NBETA];
@@ -70,6 +71,8 @@ __global__ void __launch_bounds__(256) qprep_kernel(const float *__restrict__ qu
         near_cnt[q] = 0;
         counters[4 * q + 0] = counters[4 * q + 1] = counters[4 * q + 2] = counters[4 * q + 3] = 0;
         counters_leaf[q] = 0;
+        qmap[q] = q;  // round 0 scans every query of the batch over the band (-1, +inf) (R10)
+        qband[q] = make_float2(-1.0f, __int_as_float(0x7f800000));
         bsf[q] = ~0ull;
     }
     __syncthreads();
@@ -213,7 +216,7 @@ void launch_qprep(const isax_index *ix, const float *queries, uint32_t Q, cudaSt
     const QueryScratch &qs = ix->qs;
     qprep_kernel<<<Q, 256, 0, s>>>(queries, ix->n, ix->skey, ix->ksplit, ix->N,
                                    ix->opts.window_L, probe_bits(ix), ix->opts.probe_L, qs.pwin, qs.qy, qs.qpaa, qs.qsax, qs.lut, qs.win, qs.bsf, qs.cand_cnt,
-                                   qs.near_cnt, qs.counters, qs.counters_leaf, bad);
+                                   qs.near_cnt, qs.counters, qs.counters_leaf, qs.qmap, qs.qband, bad);
 }
 
 // ------------------------------------------------------------------------------------ window

@@ -121,6 +121,19 @@ class Index:
         return cls(h.value, keep=ctx)
 
     # -- queries -------------------------------------------------------------------------------
+    def nn1_bound(self, queries, out_id, out_dist, stream):
+        """A zero-argument callable that runs isax_nn1_async on fixed device buffers (the C ABI call
+        itself, with its arguments marshalled once): for tight serving or timing loops."""
+        args = (self._h, _ptr(queries), ctypes.c_uint32(queries.shape[0]), _ptr(out_id), _ptr(out_dist),
+                ctypes.c_void_p(stream))
+        fn = isax_nn1_async
+
+        def call():
+            rc = fn(*args)
+            if rc != ISAX_OK:
+                raise IsaxError(rc, "isax_nn1_async")
+        return call
+
     def nn1(self, queries, out_id=None, out_dist=None, stream=None):
         """Exact 1-NN of raw queries [Q, n].
 
