@@ -216,3 +216,19 @@ def test_errors():
         assert e.value.name == "ISAX_E_NONFINITE"
         ids, dist = ix.nn1(torch.zeros((0, 256), device="cuda"))
         assert ids.numel() == 0
+
+
+def test_heavy_overflow_rounds():
+    """A poor approximate answer (one-row window, no probes) and a small candidate capacity: every
+    CTA's shared buffer fills, the global lists overflow and are dropped for the round (CB_OVF),
+    and the queries finish in several LB bands (R10). Answers stay exact."""
+    N, n = 300_000, 128
+    wl = small_workload(N, n, Q=20, q_noisy=6)
+    x = datagen.series(wl, 0, N)
+    q, _ = datagen.queries(wl)
+    ids_or, dist_or, _ = oracle_nn1(x.cpu().numpy(), q.cpu().numpy())
+    with _build(x, window_L=1, probe_bits=0xFFFFFFFF, cand_cap=1500) as ix:
+        ids, dist = ix.nn1(q)
+        st = ix.stats()
+    assert_nn_parity(ids.cpu().numpy(), dist.cpu().numpy(), ids_or, dist_or)
+    assert max(st["rounds"]) >= 3
