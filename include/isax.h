@@ -78,8 +78,9 @@ typedef int (*isax_fill_fn)(void *ctx, uint64_t first_id, uint64_t count, float 
  *  opts   : NULL for defaults.
  *  out    : receives the index; free it with isax_free.
  * Each series is z-normalised (R2), summarised by PAA then SAX (R3, R4), and keyed by its
- * plane-interleaved iSAX word (R6). The z-normalised rows are stored on the device in
- * ascending (key, id) order: the SAX-sorted, leaf-contiguous layout.
+ * plane-interleaved iSAX word (R6). The z-normalised rows are stored on the device in ascending
+ * (key, id) order, with every full block of 1024 positions (a super-node) reordered by a kd
+ * split down to 32-row leaves (R6b): the SAX-sorted, leaf-contiguous layout.
  * Errors: E_EMPTY if N == 0; E_INVAL; E_UNSUPPORTED; E_NONFINITE; E_NOMEM; E_CUDA. */
 int isax_build(const float *series, uint64_t N, uint32_t n, uint32_t w, uint32_t card,
                const isax_opts *opts, isax_index **out);

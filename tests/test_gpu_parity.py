@@ -232,3 +232,19 @@ def test_heavy_overflow_rounds():
         st = ix.stats()
     assert_nn_parity(ids.cpu().numpy(), dist.cpu().numpy(), ids_or, dist_or)
     assert max(st["rounds"]) >= 3
+
+
+def test_c_abi_from_plain_c(tmp_path):
+    """The boundary from C: examples/nn1_c.c builds, queries through isax_nn1 (host buffers) and
+    checks every answer against its own brute force."""
+    import os
+    import subprocess
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    lib = os.path.join(root, "paper_2009_01614_b200")
+    exe = str(tmp_path / "nn1_c")
+    subprocess.run(["gcc", "-O2", "-std=c99", "-I", os.path.join(root, "include"), os.path.join(root, "examples", "nn1_c.c"),
+                    "-L", lib, "-lisax", f"-Wl,-rpath,{lib}", "-lm", "-o", exe], check=True)
+    r = subprocess.run([exe, "20000", "256", "8"], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert r.stdout.strip().endswith("ok")
