@@ -230,12 +230,13 @@ static void launch_g(const isax_index *ix, uint32_t nq, const uint32_t *qmap, co
 // leaves that survive are examined "by first computing lower bound distances using the
 // iSAX summaries".
 //
-// Two node levels: a leaf is LEAF consecutive sorted positions, a super-node SUPER leaves. A
-// node's summary (leaf_meta_kernel, super_meta_kernel) is the per-segment [min, max] symbol. The
-// node's region on segment s is [beta_min, beta_{max+1}). Its MINDIST term is the minimum of
-// LUT[s][c] over c in [min, max]. LUT[s][.] is V-shaped around the query's own symbol q_s, so that
-// minimum is LUT[s][clamp(q_s, min, max)]. Every node term is <= the term of each member (and of
-// each child node), so a pruned node holds no candidate.
+// Three node levels: a leaf is LEAF consecutive sorted positions, a super-node SUPER leaves, a
+// hyper-node HYPER super-nodes. Inside each super-node the positions follow a kd order (R6b), so
+// its leaves are kd cells. A node's summary (leaf_meta_kernel, parent_meta_kernel) is the
+// per-segment [min, max] symbol. The node's region on segment s is [beta_min, beta_{max+1}). Its
+// MINDIST term is the minimum of LUT[s][c] over c in [min, max]. LUT[s][.] is V-shaped around the
+// query's own symbol q_s, so that minimum is LUT[s][clamp(q_s, min, max)]. Every node term is <=
+// the term of each member (and of each child node), so a pruned node holds no candidate.
 //
 // The tests use the u8 tables of scanprep_kernel (R11b): e = floor(LUT * 254 / T), rounded down at
 // every step and clamped at 255, so sum_s e <= LB^2 * 254 / T and "sum e > 254" implies LB^2 > T.
@@ -246,16 +247,17 @@ static void launch_g(const isax_index *ix, uint32_t nq, const uint32_t *qmap, co
 // Persistent CTAs (one per SM, 1024 threads) pull (query group, chunk of `chunk` leaves) tasks
 // from an atomic counter. The u8 tables of the group's G <= 16 queries sit in shared memory.
 // Per chunk:
-//  A. warp iteration = one super-node, lane = one of its 32 leaves. Lanes (query gq, segment half)
-//     bound the super-node for all G queries; a leaf bound is computed only for the queries whose
-//     super-node survived, and leaf summaries are read only for super-nodes that survived. The next
-//     iteration's super test and leaf-summary loads are issued before this iteration's leaf tests.
-//     Surviving leaves and their query masks go to a shared worklist.
-//  B. each warp takes two worklist entries at a time (lane = member of each leaf) and
-//     double-buffers their words with cp.async. For every query of either mask it runs the u8
-//     member test (two independent chains when both leaves kept the query), one warp vote, and
-//     the exact fp32 test for the rare survivors. Candidates are buffered in shared memory per
-//     query slot and flushed once per group (one global atomic per slot).
+//  A. A0: thread = (hyper-node, query); A1: lane = super-node of a surviving (hyper-node, query);
+//     A2: warp iteration = one super-node, lane = one of its 32 leaves, for the queries that kept
+//     the super-node (leaf summaries are read only under surviving super-nodes, one iteration
+//     ahead). Surviving leaves and their query masks go to a shared worklist; the surviving
+//     (leaf, query) pairs are counted per query.
+//  B. lane = member: each warp takes one worklist entry per iteration and keeps PD entries in
+//     flight in a ring of shared staging slots fed by cp.async (each lane copies and reads only its
+//     own word). For every query of the mask it runs the u8 member test (16 lookups), one warp
+//     vote, and for the rare survivors the exact rule and the candidate append. Candidates are
+//     buffered in shared memory per query slot and flushed once per group (one global atomic per
+//     slot).
 constexpr uint32_t LEAF = LEAF_SIZE;
 constexpr uint32_t SUPER = SUPER_SIZE / LEAF_SIZE;  // leaves per super-node
 constexpr uint32_t HYPER = HYPER_SIZE / SUPER_SIZE; // super-nodes per hyper-node
