@@ -640,7 +640,10 @@ static void launch_leaf(const isax_index *ix, uint32_t nq, const uint32_t *qmap,
     // chunk: as large as possible (fewer phase barriers) while leaving >= 8 tasks per SM for
     // balance; a power of two >= 512, so a multiple of SUPER
     uint32_t chunk = CHUNK;
-    while (chunk > 512 && (uint64_t)groups * ((nleaf + chunk - 1) / chunk) < 8ull * sms) chunk >>= 1;
+#ifndef ISAX_TASKS_PER_SM
+#define ISAX_TASKS_PER_SM 8
+#endif
+    while (chunk > 512 && (uint64_t)groups * ((nleaf + chunk - 1) / chunk) < (uint64_t)ISAX_TASKS_PER_SM * sms) chunk >>= 1;
     const uint64_t tasks = (uint64_t)groups * ((nleaf + chunk - 1) / chunk);
     const unsigned grid = (unsigned)std::max<uint64_t>(1, umin64(tasks, (uint64_t)sms));
     const QueryScratch &qs = ix->qs;
