@@ -50,9 +50,10 @@ typedef struct isax_opts {
                             min(N, 2^23) per query. Overflow runs more rounds (R10). */
     uint32_t flags;      /* ISAX_FLAG_* bits; 0 = defaults */
     uint32_t probe_bits; /* multi-probe approximate answer (R5): refine extra windows at the 2^probe_bits - 1 keys
-                            obtained by flipping the most fragile plane-0/1 key bits. 0 = default 4; max 5;
+                            obtained by flipping the most fragile plane-0/1 key bits. 0 = default 5 (max);
                             ISAX_PROBES_NONE = main window only. */
-    uint32_t probe_L;    /* rows per probe window. 0 = default 256. */
+    uint32_t probe_L;    /* rows per probe window: the kd cell of that many rows in the probe key's super-node
+                            that the probe's symbols descend to (R6b). 0 = default 128. */
 } isax_opts;
 
 #define ISAX_PROBES_NONE 0xFFFFFFFFu

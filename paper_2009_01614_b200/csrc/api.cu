@@ -38,7 +38,7 @@ static bool is_device_ptr(const void *p) {
 }
 
 static isax_opts default_opts(const isax_opts *o) {
-    isax_opts r{3072, -12, 1024, 0, 0, 4, 256};  // cand_cap 0: chosen per batch (alloc_scratch, nn1_device)
+    isax_opts r{3072, -12, 1024, 0, 0, 5, 128};  // cand_cap 0: chosen per batch (alloc_scratch, nn1_device)
     if (o) {
         if (o->probe_bits) r.probe_bits = o->probe_bits;
         if (o->probe_L) r.probe_L = o->probe_L;

@@ -40,6 +40,15 @@ __host__ __device__ inline unsigned long long pack_bsf(float d2, uint32_t id) {
 #endif
 }
 
+// The first four kd levels of a full super-node (R6b), heap order: node k (0..14) splits on
+// segment s[k] & 0xFF, and its right half starts at the smallest symbol s[k] >> 8 of that segment
+// there. s[15] == KD_NONE marks a super-node without kd splits (the partial last one).
+constexpr uint16_t KD_NONE = 0xFFFFu;
+constexpr uint32_t KD_LEVELS = 4;
+struct __align__(16) KdSplits {
+    uint16_t s[16];
+};
+
 struct NearEntry {  // a completed refinement within (1+delta) of the BSF at that moment (R9)
     uint32_t id;
     uint32_t pos;
@@ -147,7 +156,7 @@ struct isax_index {
     uint8_t *sax = nullptr;
     uint32_t *perm = nullptr;
     uint4 *skey = nullptr;     // [ceil(N/SUPER_SIZE)] z key of each super-node's first z-order position (R6b)
-    uint2 *ksplit = nullptr;   // [ceil(N/SUPER_SIZE)] first two kd splits of each full super-node (R6b)
+    isax::KdSplits *ksplit = nullptr;  // [ceil(N/SUPER_SIZE)] first four kd levels of each full super-node (R6b)
     uint8_t *lmeta = nullptr;  // [ceil(N/LEAF_SIZE)][32]: per-leaf min (16 B) and max (16 B) symbols
     uint8_t *smeta = nullptr;  // [ceil(N/SUPER_SIZE)][32]: per-super-node min and max symbols
     uint8_t *hmeta = nullptr;  // [ceil(N/HYPER_SIZE)][32]: per-hyper-node min and max symbols
@@ -213,7 +222,7 @@ void launch_lb_dump(const isax_index *ix, uint32_t Q, uint64_t first_pos, uint64
 void launch_leaf_meta(const uint8_t *sax, uint64_t N, uint8_t *lmeta, uint8_t *smeta, uint8_t *hmeta, cudaStream_t s);
 // permute.cu: the kd order inside every full super-node (R6b), the super-nodes' smallest keys and
 // their first two kd splits (sax and perm are permuted in place)
-void launch_superkd(uint8_t *sax, uint32_t *perm, uint64_t N, uint4 *skey, uint2 *ksplit, cudaStream_t s);
+void launch_superkd(uint8_t *sax, uint32_t *perm, uint64_t N, uint4 *skey, KdSplits *ksplit, cudaStream_t s);
 // Scan all sorted positions for the nq queries qmap[0..nq), keeping band[i].x < LB^2 <= min(band[i].y,
 // bsf^2 (1+delta)) for slot i. Returns the summary bytes it reads that the host can count (node
 // summaries or flat words); the leaf scan adds its leaf-word and leaf-summary bytes to qs.scan_bytes_dev on the device.

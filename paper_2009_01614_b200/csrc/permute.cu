@@ -124,14 +124,14 @@ constexpr int KD_THREADS = 512;
 
 __global__ void __launch_bounds__(KD_THREADS) superkd_kernel(uint4 *__restrict__ sax, uint32_t *__restrict__ perm,
                                                           uint64_t nfull, uint4 *__restrict__ skey,
-                                                          uint2 *__restrict__ ksplit) {
+                                                          KdSplits *__restrict__ ksplit) {
     constexpr uint32_t S = SUPER_SIZE, LV = 5;  // 1024 -> 32
     static_assert(SUPER_SIZE == 1024 && LEAF_SIZE == 32, "five kd levels per super-node");
     __shared__ uint4 wa[S], wb[S];
     __shared__ uint32_t ia[S], ib[S];
     __shared__ uint32_t key[S];
     __shared__ uint32_t mn[16][W], mx[16][W];
-    __shared__ uint32_t segsel[16], lvseg[3];
+    __shared__ uint32_t segsel[16], lvseg[15];  // lvseg: the chosen segment of heap node k (levels 0-3)
     const uint32_t t = threadIdx.x;
     const uint64_t b = blockIdx.x;
     if (b >= nfull) return;
@@ -172,8 +172,7 @@ __global__ void __launch_bounds__(KD_THREADS) superkd_kernel(uint4 *__restrict__
                 }
             }
             segsel[t] = best;
-            if (lv == 0) lvseg[0] = best;
-            if (lv == 1) lvseg[1 + t] = best;
+            if (lv < KD_LEVELS) lvseg[(1u << lv) - 1 + t] = best;
         }
         __syncthreads();
         for (uint32_t i = t; i < S; i += KD_THREADS) {
@@ -210,10 +209,11 @@ __global__ void __launch_bounds__(KD_THREADS) superkd_kernel(uint4 *__restrict__
         uint4 *tw = wcur; wcur = wnxt; wnxt = tw;
         uint32_t *ti = icur; icur = inxt; inxt = ti;
     }
-    // the first two levels' splits: segment and smallest symbol of the right half
-    if (t < 3) {
+    // the first four levels' splits (heap order): segment and smallest symbol of the right half
+    if (t < 15) {
+        const uint32_t lv = 31 - __clz(t + 1), nd = t + 1 - (1u << lv);
+        const uint32_t size = S >> lv, r0 = nd * size + size / 2, r1 = nd * size + size;
         const uint32_t s = lvseg[t];
-        const uint32_t r0 = t == 0 ? S / 2 : t == 1 ? S / 4 : 3 * S / 4, r1 = t == 0 ? S : r0 + S / 4;
         uint32_t m = 255u;
         for (uint32_t i = r0; i < r1; i++) {
             const uint4 wv = wcur[i];
@@ -223,7 +223,7 @@ __global__ void __launch_bounds__(KD_THREADS) superkd_kernel(uint4 *__restrict__
         key[t] = s | (m << 8);
     }
     __syncthreads();
-    if (t == 0) ksplit[b] = make_uint2(key[0] | (key[1] << 16), key[2]);
+    if (t < 16) ksplit[b].s[t] = t < 15 ? (uint16_t)key[t] : (uint16_t)0;
     for (uint32_t i = t; i < S; i += KD_THREADS) {
         sax[b * S + i] = wcur[i];
         perm[b * S + i] = icur[i];
@@ -232,14 +232,14 @@ __global__ void __launch_bounds__(KD_THREADS) superkd_kernel(uint4 *__restrict__
 
 // the last, partial super-node keeps the z order; it still gets its smallest key
 __global__ void superkey_tail_kernel(const uint4 *__restrict__ sax, uint64_t first, uint4 *__restrict__ skey,
-                                     uint2 *__restrict__ ksplit, uint64_t s) {
+                                     KdSplits *__restrict__ ksplit, uint64_t s) {
     if (threadIdx.x == 0 && blockIdx.x == 0) {
         skey[s] = word_key(sax[first]);
-        ksplit[s] = make_uint2(0xFFFFFFFFu, 0xFFFFFFFFu);  // no kd splits: quarters are not located
+        for (int k = 0; k < 16; k++) ksplit[s].s[k] = KD_NONE;  // no kd splits: cells are not located
     }
 }
 
-void launch_superkd(uint8_t *sax, uint32_t *perm, uint64_t N, uint4 *skey, uint2 *ksplit, cudaStream_t s) {
+void launch_superkd(uint8_t *sax, uint32_t *perm, uint64_t N, uint4 *skey, KdSplits *ksplit, cudaStream_t s) {
     const uint64_t nfull = N / SUPER_SIZE;
     if (nfull) superkd_kernel<<<(unsigned)nfull, KD_THREADS, 0, s>>>(reinterpret_cast<uint4 *>(sax), perm, nfull, skey, ksplit);
     if (N % SUPER_SIZE)

@@ -30,8 +30,27 @@ __host__ __device__ __forceinline__ uint32_t neighbour_windows(uint32_t L, uint3
     return (L < 3 * SUPER_SIZE && (1u << P) + 1 <= MAX_PROBES - 1) ? 2u : 0u;
 }
 
+// centre of the kd cell of super-node sb (depth levels down, R6b) that the symbols sy fall in; the
+// super-node's centre when it has no kd splits (the partial last one)
+__device__ __forceinline__ uint64_t kd_cell_centre(const KdSplits *__restrict__ ksplit, uint64_t sb, const uint32_t *sy,
+                                                   uint32_t depth) {
+    KdSplits ks;
+    const uint4 *src = reinterpret_cast<const uint4 *>(ksplit + sb);
+    uint4 *dst = reinterpret_cast<uint4 *>(&ks);
+    dst[0] = __ldg(src);
+    dst[1] = __ldg(src + 1);
+    if (ks.s[15] == KD_NONE || depth == 0) return sb * SUPER_SIZE + SUPER_SIZE / 2;
+    uint32_t node = 0;
+    for (uint32_t lv = 0; lv < depth; lv++) {
+        const uint32_t v = ks.s[node];
+        node = 2 * node + 1 + (sy[v & 0xFFu] >= (v >> 8) ? 1u : 0u);
+    }
+    const uint32_t size = SUPER_SIZE >> depth, cell = node - ((1u << depth) - 1);
+    return sb * SUPER_SIZE + cell * size + size / 2;
+}
+
 __global__ void __launch_bounds__(256) qprep_kernel(const float *__restrict__ queries, uint32_t n,
-                                                    const uint4 *__restrict__ skey, const uint2 *__restrict__ ksplit,
+                                                    const uint4 *__restrict__ skey, const KdSplits *__restrict__ ksplit,
                                                     uint64_t N, uint32_t L,
                                                     uint32_t P, uint32_t Lp, uint32_t *__restrict__ pwin,
                                                     float *__restrict__ qy, double *__restrict__ qpaa,
@@ -132,6 +151,9 @@ __global__ void __launch_bounds__(256) qprep_kernel(const float *__restrict__ qu
     }
     __syncthreads();
     const uint32_t NP = 1u << P;
+    // kd depth of a probe cell: probe_L rows = SUPER_SIZE >> depth (256 -> 2 levels), at most 4
+    uint32_t cell_depth = 0;
+    while (cell_depth < KD_LEVELS && (SUPER_SIZE >> (cell_depth + 1)) >= Lp) cell_depth++;
     const uint32_t NX = neighbour_windows(L, P);  // 2 extra windows (see neighbour_windows)
     const uint32_t warp = t >> 5, lane = t & 31;
     for (uint32_t j = warp; j < NP; j += blockDim.x / 32) {  // locate each probe key, one warp per probe
@@ -166,16 +188,10 @@ __global__ void __launch_bounds__(256) qprep_kernel(const float *__restrict__ qu
             // the main window is whole super-nodes around that one: with an odd count (L = 1024,
             // 3072) it is centred on it, with an even count (2048) it is it and the next. The keys
             // just below the query's are at its end or in the one before, the keys just above in
-            // it or the next. A probe window sits on the quarter of its super-node that the first
-            // two kd splits send the probe's symbols to.
+            // it or the next. A probe window sits on the kd cell of its super-node (probe_L rows)
+            // that the first kd splits send the probe's symbols to.
             uint64_t pos = sq * SUPER_SIZE + SUPER_SIZE / 2 + (((L / SUPER_SIZE) & 1u) ? 0u : SUPER_SIZE / 2);
-            const uint2 ks = __ldg(ksplit + sq);
-            if (j > 0 && ks.x != 0xFFFFFFFFu) {
-                const uint32_t h = sy[ks.x & 0xFFu] >= ((ks.x >> 8) & 0xFFu);
-                const uint32_t sp = h ? ks.y & 0xFFFFu : ks.x >> 16;
-                const uint32_t qt = 2 * h + (sy[sp & 0xFFu] >= (sp >> 8));
-                pos = sq * SUPER_SIZE + qt * (SUPER_SIZE / 4) + SUPER_SIZE / 8;
-            }
+            if (j > 0) pos = kd_cell_centre(ksplit, sq, sy, cell_depth);
             uint64_t start = 0;
             if (N > len) {
                 const int64_t s0 = (int64_t)pos - (int64_t)(len / 2);
@@ -189,14 +205,7 @@ __global__ void __launch_bounds__(256) qprep_kernel(const float *__restrict__ qu
                     for (uint32_t k = 0; k < 2; k++) {
                         uint64_t sn = k == 0 ? (sq > 0 ? sq - 1 : sq + 1) : (sq + 1 < nsup ? sq + 1 : (sq > 0 ? sq - 1 : sq));
                         sn = sn < nsup ? sn : nsup - 1;
-                        uint64_t p2 = sn * SUPER_SIZE + SUPER_SIZE / 2;
-                        const uint2 k2 = __ldg(ksplit + sn);
-                        if (k2.x != 0xFFFFFFFFu) {
-                            const uint32_t h = sy[k2.x & 0xFFu] >= ((k2.x >> 8) & 0xFFu);
-                            const uint32_t sp = h ? k2.y & 0xFFFFu : k2.x >> 16;
-                            const uint32_t qt = 2 * h + (sy[sp & 0xFFu] >= (sp >> 8));
-                            p2 = sn * SUPER_SIZE + qt * (SUPER_SIZE / 4) + SUPER_SIZE / 8;
-                        }
+                        const uint64_t p2 = kd_cell_centre(ksplit, sn, sy, cell_depth);
                         uint64_t st2 = 0;
                         if (N > Lp) {
                             const int64_t a = (int64_t)p2 - (int64_t)(Lp / 2), smax = (int64_t)(N - Lp);
