@@ -30,6 +30,7 @@ __host__ __device__ __forceinline__ uint32_t neighbour_windows(uint32_t L, uint3
     return (L < 3 * SUPER_SIZE && (1u << P) + 1 <= MAX_PROBES - 1) ? 2u : 0u;
 }
 
+
 // centre of the kd cell of super-node sb (depth levels down, R6b) that the symbols sy fall in; the
 // super-node's centre when it has no kd splits (the partial last one)
 __device__ __forceinline__ uint64_t kd_cell_centre(const KdSplits *__restrict__ ksplit, uint64_t sb, const uint32_t *sy,
@@ -49,7 +50,10 @@ __device__ __forceinline__ uint64_t kd_cell_centre(const KdSplits *__restrict__ 
     return sb * SUPER_SIZE + cell * size + size / 2;
 }
 
-__global__ void __launch_bounds__(256) qprep_kernel(const float *__restrict__ queries, uint32_t n,
+// NT threads per query: 1024 (one warp per probe search, a single round of 32) when the batch is
+// one wave of CTAs, 256 for large batches (more queries resident per SM)
+template <int NT>
+__global__ void __launch_bounds__(NT) qprep_kernel(const float *__restrict__ queries, uint32_t n,
                                                     const uint4 *__restrict__ skey, const KdSplits *__restrict__ ksplit,
                                                     uint64_t N, uint32_t L,
                                                     uint32_t P, uint32_t Lp, uint32_t *__restrict__ pwin,
@@ -223,7 +227,11 @@ __global__ void __launch_bounds__(256) qprep_kernel(const float *__restrict__ qu
 
 void launch_qprep(const isax_index *ix, const float *queries, uint32_t Q, cudaStream_t s, uint32_t *bad) {
     const QueryScratch &qs = ix->qs;
-    qprep_kernel<<<Q, 256, 0, s>>>(queries, ix->n, ix->skey, ix->ksplit, ix->N,
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    auto kern = Q <= (uint32_t)(2 * sms) ? qprep_kernel<1024> : qprep_kernel<256>;
+    kern<<<Q, Q <= (uint32_t)(2 * sms) ? 1024 : 256, 0, s>>>(queries, ix->n, ix->skey, ix->ksplit, ix->N,
                                    ix->opts.window_L, probe_bits(ix), ix->opts.probe_L, qs.pwin, qs.qy, qs.qpaa, qs.qsax, qs.lut, qs.win, qs.bsf, qs.cand_cnt,
                                    qs.near_cnt, qs.counters, qs.counters_leaf, qs.qmap, qs.qband, bad);
 }
