@@ -156,8 +156,9 @@ __global__ void __launch_bounds__(NT) qprep_kernel(const float *__restrict__ que
     __syncthreads();
     const uint32_t NP = 1u << P;
     // kd depth of a probe cell: probe_L rows = SUPER_SIZE >> depth (256 -> 2 levels), at most 4
-    uint32_t cell_depth = 0;
+    uint32_t cell_depth = 0, main_depth = 0;
     while (cell_depth < KD_LEVELS && (SUPER_SIZE >> (cell_depth + 1)) >= Lp) cell_depth++;
+    while (main_depth < KD_LEVELS && (SUPER_SIZE >> (main_depth + 1)) >= L) main_depth++;
     const uint32_t NX = neighbour_windows(L, P);  // 2 extra windows (see neighbour_windows)
     const uint32_t warp = t >> 5, lane = t & 31;
     for (uint32_t j = warp; j < NP; j += blockDim.x / 32) {  // locate each probe key, one warp per probe
@@ -196,6 +197,7 @@ __global__ void __launch_bounds__(NT) qprep_kernel(const float *__restrict__ que
             // that the first kd splits send the probe's symbols to.
             uint64_t pos = sq * SUPER_SIZE + SUPER_SIZE / 2 + (((L / SUPER_SIZE) & 1u) ? 0u : SUPER_SIZE / 2);
             if (j > 0) pos = kd_cell_centre(ksplit, sq, sy, cell_depth);
+            else if (L < SUPER_SIZE) pos = kd_cell_centre(ksplit, sq, sy, main_depth);  // a cell of the super-node
             uint64_t start = 0;
             if (N > len) {
                 const int64_t s0 = (int64_t)pos - (int64_t)(len / 2);
