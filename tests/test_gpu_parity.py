@@ -26,7 +26,8 @@ def _build(x, **opts):
     return isax.Index.build(x, **opts)
 
 
-@pytest.mark.parametrize("N,n,kind", [(100_000, 256, "walk"), (12_345, 128, "walk"), (4_099, 64, "sines"), (1, 256, "walk")])
+@pytest.mark.parametrize("N,n,kind", [(100_000, 256, "walk"), (12_345, 128, "walk"), (4_099, 64, "sines"), (1, 256, "walk"),
+                                      (1_024, 256, "walk"), (3_072, 128, "sines"), (1_025, 256, "walk")])
 def test_summaries_perm_and_rows_bit_exact(N, n, kind):
     wl = small_workload(N, n, kind)
     x = datagen.series(wl, 0, N)
@@ -40,7 +41,7 @@ def test_summaries_perm_and_rows_bit_exact(N, n, kind):
     np.testing.assert_array_equal(ex["stored"], y[perm])  # C1 rows, in sorted order
 
 
-@pytest.mark.parametrize("N,n", [(100_000, 256), (9_999, 128)])
+@pytest.mark.parametrize("N,n", [(100_000, 256), (9_999, 128), (3_072, 256), (1_500, 128)])
 def test_query_summary_lb_and_window(N, n):
     wl = small_workload(N, n, Q=16)
     x = datagen.series(wl, 0, N)
