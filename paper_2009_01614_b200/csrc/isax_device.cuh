@@ -61,18 +61,19 @@ __device__ __forceinline__ float bsf_d2(unsigned long long p) { return __uint_as
 
 // y = fp32_rne(fl64((x - mu) / sd)), the stored value of R2/R3, without a full fp64 division per
 // element. q = (x - mu) * rcp, with rcp = fl64(1/sd), is within 2.5 fp64 ulps of the correctly
-// rounded quotient Q. If rounding q +- 8 ulp steps (>= 4 ulps even across a binade) to fp32 gives
-// one value, rounding Q gives it too
-// (Q lies between them and rounding is monotone). Otherwise, about once in 1e8 elements, the true
-// division decides. The result equals the definition bit for bit.
+// rounded quotient Q. Rounding to fp32 drops the low 29 bits of the fp64 significand, and it can
+// only change between q - 8 ulp and q + 8 ulp (>= 4 ulps even across a binade) when those bits lie
+// within 8 of the halfway point 2^28. Outside that window, and with q a normal fp32 magnitude,
+// fp32(q) is what Q rounds to too (Q lies between q - 8 ulp and q + 8 ulp, and rounding is
+// monotone). Otherwise, about once in 1e7 elements, and for q = 0, the true division decides.
+// The result equals the definition bit for bit.
 __device__ __forceinline__ float znorm_value(float x, double mu, double sd, double rcp) {
     const double t = __dsub_rn((double)x, mu);
     const double q = __dmul_rn(t, rcp);
-    if (q == 0.0) return __double2float_rn(__ddiv_rn(t, sd));
-    const long long b = __double_as_longlong(q);
-    const float y1 = __double2float_rn(__longlong_as_double(b + 8));
-    const float y2 = __double2float_rn(__longlong_as_double(b - 8));
-    if (y1 == y2) return y1;
+    const unsigned long long b = (unsigned long long)__double_as_longlong(q);
+    const uint32_t ex = (uint32_t)(b >> 52) & 0x7FFu;          // biased exponent
+    const uint32_t low = (uint32_t)b & ((1u << 29) - 1u);     // the bits fp32 rounding drops
+    if (ex >= 898u && ex <= 1149u && low - ((1u << 28) - 8u) > 16u) return __double2float_rn(q);
     return __double2float_rn(__ddiv_rn(t, sd));
 }
 
