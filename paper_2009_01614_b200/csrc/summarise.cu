@@ -130,6 +130,142 @@ __global__ void __launch_bounds__(32) summarise_kernel(const float *__restrict__
     }
 }
 
+// Half-row staging for n = 128 and 256: the warp stages its 32 rows half a row at a time (16.5 KB
+// instead of 33 KB of shared memory), so twice as many warps fit on an SM and twice as many
+// sequential fp64 chains are in flight. Each pass (mean, variance, then y and the segment sums)
+// restages both halves; the second and third reads of a half come from L2. The fp64 operations
+// and their order per series are those of summarise_kernel (R3): identical words.
+template <uint32_t NT>
+__global__ void __launch_bounds__(32) summarise_half_kernel(const float *__restrict__ x, uint64_t count, uint64_t id0,
+                                                            uint8_t *__restrict__ sax_by_id, uint4 *__restrict__ key,
+                                                            double2 *__restrict__ musig, uint32_t *__restrict__ bad) {
+    constexpr uint32_t n = NT, P = NT / 2, seg = NT / W, SPP = W / 2;  // columns and segments per half
+    constexpr uint32_t stride = P + 1;                                  // bank = (lane + i) mod 32
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    double *beta = reinterpret_cast<double *>(smem_raw);
+    double2 *ms = reinterpret_cast<double2 *>(smem_raw + ISAX_NBETA * sizeof(double) + 8);
+    float *rows = reinterpret_cast<float *>(ms + 32);
+    const uint32_t lane = threadIdx.x;
+    for (uint32_t k = lane; k < ISAX_NBETA; k += 32) beta[k] = c_beta[k];
+    const uint64_t ngroups = (count + 31) / 32;
+    for (uint64_t g = blockIdx.x; g < ngroups; g += gridDim.x) {
+        const uint64_t r0 = g * 32;
+        const uint32_t nrows = (uint32_t)umin64(32, count - r0);
+        // half h of the 32 rows into shared memory (each row's half is P contiguous floats)
+        auto stage = [&](uint32_t h) {
+            __syncwarp();
+            constexpr uint32_t per = P / 4;
+            const uint32_t total = nrows * per;
+            constexpr uint32_t B = 8;
+            for (uint32_t e0 = 0; e0 < total; e0 += 32 * B) {
+                float4 v[B];
+#pragma unroll
+                for (uint32_t k = 0; k < B; k++) {
+                    const uint32_t e = e0 + k * 32 + lane;
+                    if (e < total) v[k] = __ldg(reinterpret_cast<const float4 *>(x + (r0 + e / per) * n + h * P) + e % per);
+                }
+#pragma unroll
+                for (uint32_t k = 0; k < B; k++) {
+                    const uint32_t e = e0 + k * 32 + lane;
+                    if (e < total) {
+                        float *d = rows + (e / per) * stride + 4 * (e % per);
+                        d[0] = v[k].x; d[1] = v[k].y; d[2] = v[k].z; d[3] = v[k].w;
+                    }
+                }
+            }
+            __syncwarp();
+        };
+        const float *row = rows + lane * stride;
+        bool finite = true;
+        double s = 0.0;  // C1, left to right over both halves (R2, R3)
+#pragma unroll
+        for (uint32_t h = 0; h < 2; h++) {
+            stage(h);
+            if (lane < nrows) {
+#pragma unroll 16
+                for (uint32_t i = 0; i < P; i++) {
+                    const float v = row[i];
+                    finite &= isfinite(v);
+                    s = __dadd_rn(s, (double)v);
+                }
+            }
+        }
+        const double mu = __ddiv_rn(s, (double)n);
+        double s2 = 0.0;
+#pragma unroll
+        for (uint32_t h = 0; h < 2; h++) {
+            stage(h);
+            if (lane < nrows) {
+#pragma unroll 16
+                for (uint32_t i = 0; i < P; i++) {
+                    const double t = __dsub_rn((double)row[i], mu);
+                    s2 = __dadd_rn(s2, __dmul_rn(t, t));
+                }
+            }
+        }
+        if (lane < nrows) ms[lane] = make_double2(mu, __dsqrt_rn(__ddiv_rn(s2, (double)n)));
+        double rcp = 0.0;
+        __syncwarp();
+        if (lane < nrows) rcp = __drcp_rn(ms[lane].y);
+        double acc[W];
+#pragma unroll
+        for (int sg = 0; sg < W; sg++) acc[sg] = 0.0;
+#pragma unroll
+        for (uint32_t h = 0; h < 2; h++) {
+            stage(h);
+            // y = fp32((x - mu) / sigma) for the half tile, warp-cooperatively, in place
+            for (uint32_t r = 0; r < nrows; r++) {
+                const double2 m = ms[r];
+                const double rr = __shfl_sync(0xffffffffu, rcp, r);
+                float *pr = rows + r * stride;
+#pragma unroll 4
+                for (uint32_t c = lane; c < P; c += 32) pr[c] = m.y < 1e-12 ? 0.0f : znorm_value(pr[c], m.x, m.y, rr);
+            }
+            __syncwarp();
+            if (lane < nrows) {  // C2: this half's segments, left to right within each
+                for (uint32_t j = 0; j < seg; j++) {
+#pragma unroll
+                    for (uint32_t sg = 0; sg < SPP; sg++)
+                        acc[h * SPP + sg] = __dadd_rn(acc[h * SPP + sg], (double)row[sg * seg + j]);
+                }
+            }
+        }
+        if (lane < nrows) {
+            uint32_t sym[W];
+#pragma unroll
+            for (int sg = 0; sg < W; sg++) sym[sg] = sax_symbol(beta, __ddiv_rn(acc[sg], (double)seg));
+            const uint64_t id = id0 + r0 + lane;
+            uint4 wv;
+            wv.x = sym[0] | (sym[1] << 8) | (sym[2] << 16) | (sym[3] << 24);
+            wv.y = sym[4] | (sym[5] << 8) | (sym[6] << 16) | (sym[7] << 24);
+            wv.z = sym[8] | (sym[9] << 8) | (sym[10] << 16) | (sym[11] << 24);
+            wv.w = sym[12] | (sym[13] << 8) | (sym[14] << 16) | (sym[15] << 24);
+            reinterpret_cast<uint4 *>(sax_by_id)[id] = wv;
+            key[id] = isax_key(sym);
+            musig[id] = ms[lane];
+            if (!finite) atomicOr(bad, 1u);
+        }
+        __syncwarp();
+    }
+}
+
+template <uint32_t NT>
+static void launch_summarise_half(const float *x, uint64_t count, uint64_t id0, uint8_t *sax_by_id, uint4 *key,
+                                  double2 *musig, uint32_t *bad, cudaStream_t s) {
+    const size_t smem = ISAX_NBETA * sizeof(double) + 8 + 32 * sizeof(double2) + 32 * (size_t)(NT / 2 + 1) * sizeof(float);
+    static size_t configured = 0;
+    if (smem > configured) {
+        cudaFuncSetAttribute(summarise_half_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        configured = smem;
+    }
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int per_sm = (int)std::max<size_t>(1, std::min<size_t>(32, (227 * 1024) / (smem + 1024)));
+    const uint64_t grid = umin64((count + 31) / 32, (uint64_t)sms * per_sm);
+    summarise_half_kernel<NT><<<(unsigned)grid, 32, smem, s>>>(x, count, id0, sax_by_id, key, musig, bad);
+}
+
 template <uint32_t NT>
 static void launch_summarise_t(const float *x, uint64_t count, uint32_t n, uint64_t id0, uint8_t *sax_by_id,
                                uint4 *key, double2 *musig, uint32_t *bad, cudaStream_t s) {
@@ -151,6 +287,10 @@ static void launch_summarise_t(const float *x, uint64_t count, uint32_t n, uint6
 void launch_summarise(const float *x, uint64_t count, uint32_t n, uint64_t id0, uint8_t *sax_by_id, uint4 *key,
                       double2 *musig, uint32_t *bad, cudaStream_t s) {
     if (count == 0) return;
+#ifndef ISAX_SUMMARISE_FULLROW
+    if (n == 256) return launch_summarise_half<256>(x, count, id0, sax_by_id, key, musig, bad, s);
+    if (n == 128) return launch_summarise_half<128>(x, count, id0, sax_by_id, key, musig, bad, s);
+#endif
     if (n == 256) launch_summarise_t<256>(x, count, n, id0, sax_by_id, key, musig, bad, s);
     else if (n == 128) launch_summarise_t<128>(x, count, n, id0, sax_by_id, key, musig, bad, s);
     else launch_summarise_t<0>(x, count, n, id0, sax_by_id, key, musig, bad, s);
