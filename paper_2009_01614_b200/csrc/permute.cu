@@ -116,9 +116,10 @@ void launch_export_sax(const uint8_t *sax, const uint32_t *inv, uint64_t first_i
 // Membership of super-nodes and hyper-nodes is unchanged, so their boxes are too. Offline on 4M
 // random walks this cut the members tested under alive leaves by 14%.
 // Per super-node it also records the z key of its first position (the block's smallest key, for
-// the approximate answer's search) and the first two split levels (segment and the smallest
-// symbol of the right half) for locating a 256-row quarter.
-// One CTA per full super-node, 512 threads; each level is a bitonic sort of the 1024 keys
+// the approximate answer's search) and the first four split levels (segment and the smallest
+// symbol of the right half) for locating a probe's kd cell.
+// One CTA per full super-node, 512 threads; the node ranges come from warp reductions and one
+// shared atomic per (node, segment) and warp; each level is a bitonic sort of the 1024 keys
 // (node << 18 | symbol << 10 | position), so the order is exactly the stable one.
 constexpr int KD_THREADS = 512;
 
@@ -150,15 +151,25 @@ __global__ void __launch_bounds__(KD_THREADS) superkd_kernel(uint4 *__restrict__
             mx[i / W][i % W] = 0u;
         }
         __syncthreads();
+        // a warp's 32 consecutive positions lie in one node (nodes hold >= 64): warp reductions
+        // first, then one shared atomic per (node, segment) and warp
         for (uint32_t i = t; i < S; i += KD_THREADS) {
             const uint4 wv = wcur[i];
             const uint32_t v[4] = {wv.x, wv.y, wv.z, wv.w};
             const uint32_t nd = i >> sh;
+            uint32_t mine = 0, maxe = 0;  // lane s < W keeps segment s's results
 #pragma unroll
             for (int s = 0; s < W; s++) {
                 const uint32_t c = (v[s >> 2] >> (8 * (s & 3))) & 0xFFu;
-                atomicMin(&mn[nd][s], c);
-                atomicMax(&mx[nd][s], c);
+                const uint32_t lo = __reduce_min_sync(0xffffffffu, c), hi = __reduce_max_sync(0xffffffffu, c);
+                if ((t & 31) == (uint32_t)s) {
+                    mine = lo;
+                    maxe = hi;
+                }
+            }
+            if ((t & 31) < (uint32_t)W) {
+                atomicMin(&mn[nd][t & 31], mine);
+                atomicMax(&mx[nd][t & 31], maxe);
             }
         }
         __syncthreads();
