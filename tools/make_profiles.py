@@ -19,7 +19,7 @@ with open(os.path.join(out, f"{rnd}_launches_{cfg}.txt"), "w") as f:
     f.write(f"# command: python bench.py --config <{cfg}> --steps 2 --warmup 1 --no-cpu-baseline (build + 3 query batches)\n")
     f.write(ns.launches(os.path.join(go, f"{tag}_launches.csv")) + "\n")
 traffic = {}
-for kre in ("leafscan", "refine_q", "window_kernel", "summarise", "candcheck"):
+for kre in ("leafscan", "refine_q", "window_kernel", "summarise", "candcheck", "superkd"):
     rep = os.path.join(go, f"{tag}_{kre}_prof.ncu-rep")
     if not os.path.exists(rep):
         continue
@@ -48,8 +48,12 @@ for kre in ("leafscan", "refine_q", "window_kernel", "summarise", "candcheck"):
         f.write("\n# hottest source lines (stall samples)\n" + hot)
 path = os.path.join(out, "ncu_traffic.json")
 d = json.load(open(path)) if os.path.exists(path) else {}
-d[{"cfg3": "cfg3_walk_100M_x256", "cfg2": "cfg2_walk_10M_x256"}.get(cfg, cfg)] = {
-    "leafscan_dram_bytes": traffic.get("leafscan"), "refine_dram_bytes": traffic.get("refine_q"),
-    "window_dram_bytes": traffic.get("window_kernel"), "source": f"profiles/{rnd}_*_{cfg}.txt (ncu --set full, first launch)"}
+key = {"cfg3": "cfg3_walk_100M_x256", "cfg2": "cfg2_walk_10M_x256"}.get(cfg, cfg)
+ent = d.get(key, {})
+for name, kre in (("leafscan", "leafscan"), ("refine", "refine_q"), ("window", "window_kernel")):
+    if traffic.get(kre) is not None:  # only kernels captured under this tag
+        ent[f"{name}_dram_bytes"] = traffic[kre]
+ent["source"] = f"profiles/{rnd}_*_{cfg}.txt (ncu --set full, first launch)"
+d[key] = ent
 json.dump(d, open(path, "w"), indent=1)
 print("wrote", sorted(os.listdir(out)))
