@@ -27,7 +27,8 @@ def _build(x, **opts):
 
 
 @pytest.mark.parametrize("N,n,kind", [(100_000, 256, "walk"), (12_345, 128, "walk"), (4_099, 64, "sines"), (1, 256, "walk"),
-                                      (1_024, 256, "walk"), (3_072, 128, "sines"), (1_025, 256, "walk")])
+                                      (1_024, 256, "walk"), (3_072, 128, "sines"), (1_025, 256, "walk"),
+                                      (2_500, 1024, "walk"), (3_333, 512, "sines")])
 def test_summaries_perm_and_rows_bit_exact(N, n, kind):
     wl = small_workload(N, n, kind)
     x = datagen.series(wl, 0, N)
@@ -64,7 +65,8 @@ def test_query_summary_lb_and_window(N, n):
 
 
 @pytest.mark.parametrize("N,n,kind,q_noisy", [(100_000, 256, "walk", 0), (100_000, 256, "walk", 8),
-                                              (20_000, 256, "sines", 16), (7_777, 128, "walk", 4)])
+                                              (20_000, 256, "sines", 16), (7_777, 128, "walk", 4),
+                                              (5_000, 64, "sines", 4), (3_000, 1024, "walk", 4), (6_001, 512, "walk", 3)])
 def test_nn1_matches_oracle(N, n, kind, q_noisy):
     wl = small_workload(N, n, kind, Q=16, q_noisy=q_noisy, sigma=0.1)
     x = datagen.series(wl, 0, N)
@@ -148,7 +150,7 @@ def test_ties_duplicates_constants_and_exact_copies():
 
 @pytest.mark.parametrize("opts", [dict(window_L=1), dict(window_L=4096), dict(cand_cap=7), dict(batch_Q=3),
                                   dict(slack_log2=-20), dict(probe_bits=0xFFFFFFFF), dict(probe_bits=5, probe_L=1),
-                                  dict(probe_bits=2, probe_L=1024)])
+                                  dict(probe_bits=2, probe_L=1024), dict(flags=1)])
 def test_options_do_not_change_answers(opts):
     N, n = 30_000, 256
     wl = small_workload(N, n, Q=12, q_noisy=4)
