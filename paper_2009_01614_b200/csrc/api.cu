@@ -120,7 +120,7 @@ static int alloc_scratch_cap(isax_index *ix, uint32_t cap) {
     A(lut, (size_t)Q * W * CARD);
     A(lut8, (size_t)Q * W * CARD);
     A(qconst, Q);
-    A(pwin, (size_t)Q * (MAX_PROBES - 1));
+    A(pwin, (size_t)Q * MAX_PROBES);
     A(cand, (size_t)Q * cap);
     A(candq, (size_t)Q * cap);
     A(cand2, (size_t)Q * cap);
@@ -313,6 +313,7 @@ static int nn1_device(isax_index *ix, const float *d_q, uint32_t Q, int64_t *d_i
     ix->st_refined.assign(Q, 0);
     ix->st_abandoned.assign(Q, 0);
     ix->st_skipped.assign(Q, 0);
+    ix->st_winrows.assign(Q, 0);
     ix->st_rounds.assign(Q, 0);
     ix->st_near.assign(Q, 0);
     ix->st_leaves.assign(Q, 0);
@@ -455,6 +456,7 @@ static int nn1_device(isax_index *ix, const float *d_q, uint32_t Q, int64_t *d_i
             ix->st_refined[b0 + i] = hm.counters[4 * i];
             ix->st_abandoned[b0 + i] = hm.counters[4 * i + 1];
             ix->st_skipped[b0 + i] = hm.counters[4 * i + 2];
+            ix->st_winrows[b0 + i] = hm.counters[4 * i + 3];
             ix->st_near[b0 + i] = hm.near_cnt[i];
             ix->st_leaves[b0 + i] = hm.leaves[i];
             ix->st_bsf0[b0 + i] = bsf0_h[i];
@@ -657,6 +659,7 @@ int isax_stats(const isax_index *cix, char *buf, size_t cap) {
     arr("refined", ix->st_refined, false);
     arr("abandoned", ix->st_abandoned, false);
     arr("skipped", ix->st_skipped, false);
+    arr("window_rows", ix->st_winrows, false);
     arr("rounds", ix->st_rounds, false);
     arr("near", ix->st_near, false);
     arr("leaves_alive", ix->st_leaves, false);

@@ -110,7 +110,7 @@ struct QueryScratch {
     uint8_t *lut8 = nullptr;        // [Q][16][256] u8 scan table of each active slot (R11b)
     uint4 *qconst = nullptr;        // [Q] scan constants of each active slot (band lo, T, window)
     uint32_t *win = nullptr;        // [Q][2] window [start, end)
-    uint32_t *pwin = nullptr;       // [Q][MAX_PROBES-1] probe window starts (probe_L rows each)
+    uint32_t *pwin = nullptr;       // [Q][MAX_PROBES]: kept probe window starts (probe_L rows each), count last
     unsigned long long *bsf = nullptr;  // [Q] packed
     uint32_t *cand = nullptr;       // [Q][cand_cap] sorted positions
     uint8_t *candq = nullptr;       // [Q][cand_cap] u8 bound b of each candidate: b / qscale <= LB^2,
@@ -164,7 +164,7 @@ struct isax_index {
     isax::QueryScratch qs;
     std::mutex mu;
     // last-call statistics (host copies)
-    std::vector<uint32_t> st_win, st_cand, st_refined, st_abandoned, st_skipped, st_rounds, st_near, st_leaves;
+    std::vector<uint32_t> st_win, st_cand, st_refined, st_abandoned, st_skipped, st_winrows, st_rounds, st_near, st_leaves;
     std::vector<float> st_bsf0, st_bsf_final;
     isax::StageTimes st_ms;
     uint64_t st_launches = 0;  // kernels launched by the last nn1 call

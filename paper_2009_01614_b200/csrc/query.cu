@@ -217,13 +217,28 @@ __global__ void __launch_bounds__(NT) qprep_kernel(const float *__restrict__ que
                             const int64_t a = (int64_t)p2 - (int64_t)(Lp / 2), smax = (int64_t)(N - Lp);
                             st2 = (uint64_t)(a < 0 ? 0 : (a > smax ? smax : a));
                         }
-                        pwin[q * (MAX_PROBES - 1) + NP - 1 + k] = (uint32_t)st2;
+                        pwin[q * MAX_PROBES + NP - 1 + k] = (uint32_t)st2;
                     }
                 }
             } else {
-                pwin[q * (MAX_PROBES - 1) + j - 1] = (uint32_t)start;
+                pwin[q * MAX_PROBES + j - 1] = (uint32_t)start;
             }
         }
+    }
+    __syncthreads();
+    // keep the probe windows that add rows: drop those inside the main window (already refined)
+    // and repeats of an earlier start; their count goes into the last slot. Warp 0, lane = probe.
+    if (warp == 0) {
+        uint32_t *pw = pwin + (uint64_t)q * MAX_PROBES;
+        const uint32_t np = NP - 1 + NX, lp = (uint32_t)(N < Lp ? N : Lp);
+        const uint32_t ws = win[2 * q], we = win[2 * q + 1];
+        const uint32_t a = lane < np ? pw[lane] : 0xFFFFFFFFu;
+        const bool rep = (__match_any_sync(0xffffffffu, a) & ((1u << lane) - 1u)) != 0;
+        const bool keep = lane < np && !rep && !(a >= ws && a + lp <= we);
+        const uint32_t kb = __ballot_sync(0xffffffffu, keep);
+        __syncwarp();
+        if (keep) pw[__popc(kb & ((1u << lane) - 1u))] = a;
+        if (lane == 0) pw[MAX_PROBES - 1] = __popc(kb);
     }
 }
 
@@ -281,14 +296,14 @@ __global__ void __launch_bounds__(256) window_kernel(const float *__restrict__ s
     const uint32_t t = threadIdx.x, lane = t & 31, warp = t >> 5;
     const uint32_t ws = win[2 * q], we = win[2 * q + 1], L = we - ws;
     const uint32_t lp = (uint32_t)(N < Lp ? N : Lp);
-    const uint32_t rows = L + nprobe * lp;
+    const uint32_t rows = L + (nprobe ? pwin[q * MAX_PROBES + MAX_PROBES - 1] : 0u) * lp;  // kept probes (qprep)
     const uint32_t r0 = blockIdx.x * WIN_ROWS;
     if (r0 >= rows) return;
     const uint32_t r1 = min(rows, r0 + WIN_ROWS);
     auto row_pos = [&](uint32_t r) -> uint32_t {
         if (r < L) return ws + r;
         r -= L;
-        return pwin[q * (MAX_PROBES - 1) + r / lp] + r % lp;
+        return pwin[q * MAX_PROBES + r / lp] + r % lp;
     };
     float4 qv[NS];
 #pragma unroll
@@ -349,6 +364,7 @@ __global__ void __launch_bounds__(256) window_kernel(const float *__restrict__ s
         atomicMin(&bsf[q], smin);
         cur = atomicAdd(&bsf[q], 0ull);
         atomicAdd(&counters[4 * q + 0], r1 - r0);
+        atomicAdd(&counters[4 * q + 3], r1 - r0);  // window rows (stats)
     }
     __syncthreads();
     const float lim = bsf_d2(cur) * onepd;

@@ -84,6 +84,11 @@ def test_nn1_matches_oracle(N, n, kind, q_noisy):
         w0, w1 = st["window"][2 * j], st["window"][2 * j + 1]
         assert st["candidates"][j] + (w1 - w0) <= N
         assert st["refined"][j] + st["abandoned"][j] >= (w1 - w0)
+        # window rows refined: the main window plus the kept probe windows (each at most probe_L
+        # rows, none inside the main window, no repeats)
+        lp = min(st["probe_L"], N)
+        assert (w1 - w0) <= st["window_rows"][j] <= (w1 - w0) + st["probe_windows"] * lp
+        assert (st["window_rows"][j] - (w1 - w0)) % lp == 0
 
 
 @pytest.mark.parametrize("N,n,kind", [(200_000, 256, "walk"), (50_001, 128, "walk"), (30_000, 256, "sines")])
