@@ -50,7 +50,8 @@ typedef struct isax_opts {
                             min(N, 2^23) per query. Overflow runs more rounds (R10). */
     uint32_t flags;      /* ISAX_FLAG_* bits; 0 = defaults */
     uint32_t probe_bits; /* multi-probe approximate answer (R5): refine extra windows at the 2^probe_bits - 1 keys
-                            obtained by flipping the most fragile plane-0/1 key bits. 0 = default 5 (max);
+                            obtained by flipping the most fragile plane-0/1 key bits; a probe window inside the main
+                            window, or at the start of an earlier one, is skipped. 0 = default 5 (max);
                             ISAX_PROBES_NONE = main window only. */
     uint32_t probe_L;    /* rows per probe window: the kd cell of that many rows in the probe key's super-node
                             that the probe's symbols descend to (R6b). 0 = default 128. */
@@ -126,8 +127,9 @@ int isax_query_debug(const isax_index *ix, const float *queries, uint32_t Q, dou
                      float *lut, uint64_t first_pos, uint64_t count, float *lb2, uint32_t *win);
 
 /* Counters of the last isax_nn1 / isax_nn1_async call, as a JSON object written to buf.
- * It holds per-query window, candidates, refined, abandoned and rounds, plus per-stage
- * device milliseconds. Returns the length needed (excluding NUL); truncates if cap is too small. */
+ * It holds per-query window, window_rows (rows the approximate answer refined), candidates,
+ * refined, abandoned, skipped, rounds, near, leaves_alive and the BSF before and after the scan,
+ * plus per-stage device milliseconds of the first batch. Returns the length needed (excluding NUL); truncates if cap is too small. */
 int isax_stats(const isax_index *ix, char *buf, size_t cap);
 
 /* Index geometry: any out pointer may be NULL. device_bytes = bytes the index holds on the device. */
