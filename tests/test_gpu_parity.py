@@ -155,7 +155,9 @@ def test_ties_duplicates_constants_and_exact_copies():
 
 @pytest.mark.parametrize("opts", [dict(window_L=1), dict(window_L=4096), dict(cand_cap=7), dict(batch_Q=3),
                                   dict(slack_log2=-20), dict(probe_bits=0xFFFFFFFF), dict(probe_bits=5, probe_L=1),
-                                  dict(probe_bits=2, probe_L=1024), dict(flags=1)])
+                                  dict(probe_bits=2, probe_L=1024), dict(flags=1), dict(window_L=2048),
+                                  dict(window_L=1024), dict(window_L=512, probe_L=64), dict(probe_L=256),
+                                  dict(probe_bits=3, probe_L=512)])
 def test_options_do_not_change_answers(opts):
     N, n = 30_000, 256
     wl = small_workload(N, n, Q=12, q_noisy=4)
@@ -256,3 +258,18 @@ def test_c_abi_from_plain_c(tmp_path):
     r = subprocess.run([exe, "20000", "256", "8"], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout + r.stderr
     assert r.stdout.strip().endswith("ok")
+
+
+def test_many_queries_span_batches():
+    """Q = 1100 with the default batch_Q (1024): a full batch and a ragged one of 76, each with its
+    own share of the candidate pool; answers equal the oracle's."""
+    N, n, Q = 20_000, 128, 1100
+    wl = small_workload(N, n, "sines", Q=Q, q_noisy=600, sigma=0.05)
+    x = datagen.series(wl, 0, N)
+    q, _ = datagen.queries(wl)
+    ids_or, dist_or, _ = oracle_nn1(x.cpu().numpy(), q.cpu().numpy())
+    with _build(x) as ix:
+        ids, dist = ix.nn1(q)
+        st = ix.stats()
+    assert_nn_parity(ids.cpu().numpy(), dist.cpu().numpy(), ids_or, dist_or)
+    assert len(st["rounds"]) == Q and min(st["window_rows"]) >= min(3072, N)
