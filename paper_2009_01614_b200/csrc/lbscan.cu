@@ -692,7 +692,12 @@ constexpr uint32_t B_SPLIT = ISAX_BSPLIT;  // second refine pass: b > B_SPLIT, i
 constexpr uint32_t SPLIT_MIN = 4096;  // ... for queries with more candidates than this
 constexpr uint32_t SPLIT_TARGET = 65536;  // first-pass size a lowered split aims at
 
-__global__ void __launch_bounds__(CK_THREADS) candcheck_kernel(
+// three CTAs per SM (at most 80 registers; 92 allowed only two): the kernel is latency-bound on
+// its word and table loads, so the extra warps pay (cfg3 0.074 -> 0.057 ms)
+#ifndef ISAX_CK_MINB
+#define ISAX_CK_MINB 3
+#endif
+__global__ void __launch_bounds__(CK_THREADS, ISAX_CK_MINB) candcheck_kernel(
     const uint32_t *__restrict__ cand, const uint8_t *__restrict__ candq, const uint32_t *__restrict__ cand_cnt,
     uint32_t Q, uint32_t cap, const uint4 *__restrict__ sax, const float *__restrict__ lut_all,
     const float *__restrict__ qT, const float *__restrict__ qscale, uint32_t *__restrict__ cand2,
