@@ -42,7 +42,8 @@ enum {
 /* Tunables. Pass NULL for the defaults. */
 typedef struct isax_opts {
     uint32_t window_L;   /* rows of the approximate answer's main window (R5, R6b): whole
-                            super-nodes around the query key's. Default 3072: it, the one before and the one after. */
+                            super-nodes around the query key's. Default 3072: it, the one before and the one after.
+                            Range [1, 4096]; below 1024, a kd cell of the key's super-node. */
     int32_t slack_log2;  /* prune/abandon slack delta = 2^slack_log2 (R8). Default -12. */
     uint32_t batch_Q;    /* queries processed per device batch (<= 1024). Default 1024. */
     uint32_t cand_cap;   /* candidate-list capacity per query per round. 0 = default: a pool of 2^30 entries (about

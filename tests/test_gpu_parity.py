@@ -64,6 +64,26 @@ def test_query_summary_lb_and_window(N, n):
         assert tuple(dbg["win"][i]) == ref.super_window(ex["sax"], qw[i], 3072)
 
 
+@pytest.mark.parametrize("L", [1024, 2048, 4096])
+def test_window_of_whole_super_nodes(L):
+    """Main windows of an odd (1024) or even (2048, 4096) count of super-nodes follow the oracle's
+    centre rule (R5, R6b): odd counts centred on the query key's super-node, even counts on its end.
+    window_L above 4096 is rejected (include/isax.h)."""
+    N, n = 60_000, 128
+    wl = small_workload(N, n, Q=16, q_noisy=8)
+    x = datagen.series(wl, 0, N)
+    q, _ = datagen.queries(wl)
+    qh = q.cpu().numpy()
+    with _build(x, window_L=L) as ix:
+        ex = ix.export(0, N, sax=True)
+        dbg = ix.query_debug(qh, 0, 1)
+    _, _, _, _, qw = clib.summarise(qh)
+    for i in range(len(qh)):
+        assert tuple(dbg["win"][i]) == ref.super_window(ex["sax"], qw[i], L)
+    with pytest.raises(isax.IsaxError):
+        _build(x, window_L=4097)
+
+
 @pytest.mark.parametrize("N,n,kind,q_noisy", [(100_000, 256, "walk", 0), (100_000, 256, "walk", 8),
                                               (20_000, 256, "sines", 16), (7_777, 128, "walk", 4),
                                               (5_000, 64, "sines", 4), (3_000, 1024, "walk", 4), (6_001, 512, "walk", 3)])
