@@ -19,7 +19,7 @@ with open(os.path.join(out, f"{rnd}_launches_{cfg}.txt"), "w") as f:
     f.write(f"# command: python bench.py --config <{cfg}> --steps 2 --warmup 1 --no-cpu-baseline (build + 3 query batches)\n")
     f.write(ns.launches(os.path.join(go, f"{tag}_launches.csv")) + "\n")
 traffic = {}
-for kre in ("leafscan", "refine_q", "window_kernel", "summarise", "candcheck", "superkd"):
+for kre in ("leafscan", "refine_q", "window_kernel", "summarise", "candcheck", "superkd", "qprep"):
     rep = os.path.join(go, f"{tag}_{kre}_prof.ncu-rep")
     if not os.path.exists(rep):
         continue
