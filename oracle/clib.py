@@ -91,7 +91,7 @@ class NN1Scan:
         self.cnt = np.zeros(self.Q, np.int32)
         self.ids = np.zeros((self.Q, K), np.int64)
         self.d2 = np.zeros((self.Q, K), np.float64)
-        self.ovf = np.zeros(self.Q, np.int32)
+        self.ovf = np.full(self.Q, np.inf)  # smallest d2 dropped for lack of room (oracle.c)
         self.rows = {}
 
     def feed(self, id0: int, xraw: np.ndarray):
@@ -112,8 +112,9 @@ class NN1Scan:
         self.rows = {i: r for i, r in self.rows.items() if i in live}
 
     def result(self):
-        if self.ovf.any():
-            raise RuntimeError("oracle near-tie list overflow; raise K")
+        lost = self.ovf <= self.best * (1 + ref.NEAR_REL) + 1e-300
+        if lost.any():
+            raise RuntimeError(f"oracle near-tie list overflow at queries {np.nonzero(lost)[0][:8]}; raise K")
         ids, dist, d2 = [], [], []
         for q in range(self.Q):
             cand = {int(i): self.rows[int(i)] for i in self.ids[q, : self.cnt[q]]}

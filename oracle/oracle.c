@@ -85,16 +85,18 @@ int64_t orc_summarise(const float *x, int64_t N, int n, int w, const double *bet
  *
  * Per query it keeps best_d2[q] (running minimum) and a "near" list of up to K (id, d2) entries
  * with d2 <= best * (1 + rel) + 1e-300. Those entries are resolved exactly by the caller
- * (oracle/clib.py) with rationals. If an entry does not fit, overflow[q] is set. State
- * (best_d2, near_cnt, near_id, near_d2, overflow) is carried across chunks; initialise
- * best_d2 to +inf and the counts to 0.
+ * (oracle/clib.py) with rationals. If an entry does not fit, ovf_d2[q] records the smallest
+ * d2 dropped that way: the list is complete iff ovf_d2[q] > best_d2[q] * (1 + rel) + 1e-300 at
+ * the end (a dropped entry outside the final band cannot be the answer). State (best_d2,
+ * near_cnt, near_id, near_d2, ovf_d2) is carried across chunks; initialise best_d2 and ovf_d2
+ * to +inf and the counts to 0.
  *
  * The per-row loop is blocked over queries (qt is the transposed query matrix [n][Q]) so the
  * accumulators for different queries are independent. Each accumulator still sums its own
  * terms left to right.
  */
 static void near_insert(int K, double rel, double *best, int *cnt, int64_t *ids, double *d2s,
-                        int *ovf, int64_t id, double d)
+                        double *ovf, int64_t id, double d)
 {
     if (d < *best) {
         *best = d;
@@ -105,13 +107,13 @@ static void near_insert(int K, double rel, double *best, int *cnt, int64_t *ids,
     }
     if (d <= *best * (1.0 + rel) + 1e-300) {
         if (*cnt < K) { ids[*cnt] = id; d2s[*cnt] = d; (*cnt)++; }
-        else *ovf = 1;
+        else if (d < *ovf) *ovf = d;
     }
 }
 
 int64_t orc_nn1_scan(const float *xraw, int64_t m, int n, int64_t id0, const float *qt, int Q,
                      int K, double rel, double *best_d2, int *near_cnt, int64_t *near_id,
-                     double *near_d2, int *overflow)
+                     double *near_d2, double *ovf_d2)
 {
     int64_t bad = 0;
 #pragma omp parallel reduction(+ : bad)
@@ -122,8 +124,8 @@ int64_t orc_nn1_scan(const float *xraw, int64_t m, int n, int64_t id0, const flo
         int *lc = (int *)calloc((size_t)Q, sizeof(int));
         int64_t *li = (int64_t *)malloc(sizeof(int64_t) * (size_t)Q * K);
         double *ld = (double *)malloc(sizeof(double) * (size_t)Q * K);
-        int *lo = (int *)calloc((size_t)Q, sizeof(int));
-        for (int q = 0; q < Q; q++) lb[q] = INFINITY;
+        double *lo = (double *)malloc(sizeof(double) * (size_t)Q);
+        for (int q = 0; q < Q; q++) lb[q] = INFINITY, lo[q] = INFINITY;
 #pragma omp for schedule(static)
         for (int64_t r = 0; r < m; r++) {
             if (znorm_row(xraw + r * (int64_t)n, n, y, NULL, NULL)) { bad++; continue; }
@@ -143,10 +145,10 @@ int64_t orc_nn1_scan(const float *xraw, int64_t m, int n, int64_t id0, const flo
 #pragma omp critical
         {
             for (int q = 0; q < Q; q++) {
-                if (lo[q]) overflow[q] = 1;
+                if (lo[q] < ovf_d2[q]) ovf_d2[q] = lo[q];
                 for (int i = 0; i < lc[q]; i++)
                     near_insert(K, rel, &best_d2[q], &near_cnt[q], near_id + (int64_t)q * K,
-                                near_d2 + (int64_t)q * K, &overflow[q], li[(int64_t)q * K + i],
+                                near_d2 + (int64_t)q * K, &ovf_d2[q], li[(int64_t)q * K + i],
                                 ld[(int64_t)q * K + i]);
             }
         }

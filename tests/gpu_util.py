@@ -15,21 +15,21 @@ def device_data(wl):
     return datagen.series(wl, 0, wl.N)
 
 
-def oracle_nn1(x_host: np.ndarray, q_host: np.ndarray, chunk: int = 1 << 20):
+def oracle_nn1(x_host: np.ndarray, q_host: np.ndarray, chunk: int = 1 << 20, K: int = 32):
     """Exact 1-NN by the C oracle (brute force over raw rows; z-norm inside), same bytes as the GPU."""
     qy, _, _, _, _ = clib.summarise(q_host, want_paa=False)
-    sc = clib.NN1Scan(qy, K=32)
+    sc = clib.NN1Scan(qy, K=K)
     for s in range(0, x_host.shape[0], chunk):
         sc.feed(s, x_host[s : s + chunk])
     return sc.result()
 
 
-def oracle_nn1_streamed(wl, q_host: np.ndarray, chunk: int = 1 << 21):
+def oracle_nn1_streamed(wl, q_host: np.ndarray, chunk: int = 1 << 21, K: int = 32):
     """Exact 1-NN over a workload too big for host RAM: regenerate chunks on the device, copy each to host."""
     import torch
 
     qy, _, _, _, _ = clib.summarise(q_host, want_paa=False)
-    sc = clib.NN1Scan(qy, K=32)
+    sc = clib.NN1Scan(qy, K=K)
     buf = torch.empty((chunk, wl.n), dtype=torch.float32, device="cuda")
     host = torch.empty((chunk, wl.n), dtype=torch.float32, pin_memory=True)
     for s in range(0, wl.N, chunk):
