@@ -127,6 +127,16 @@ int isax_export(const isax_index *ix, uint64_t first_id, uint64_t count, uint8_t
 int isax_query_debug(const isax_index *ix, const float *queries, uint32_t Q, double *q_paa, uint8_t *q_sax,
                      float *lut, uint64_t first_pos, uint64_t count, float *lb2, uint32_t *win);
 
+/* Debug / parity entry: the candidate list of query q (0-based in the last isax_nn1 /
+ * isax_nn1_async call) after the LB filter (the series "not pruned" by their lower
+ * bound), as sorted positions, in no particular order. These are the positions p outside the
+ * approximate answer's window with LB^2(p) <= bsf0^2 (1 + delta), bsf0 = the window's BSF
+ * (R8, R10). *count receives the list length; out_pos (any pointer kind, or NULL to query the
+ * length) receives it when cap >= *count.
+ * Errors: E_INVAL if the last call spanned more than one batch (Q > batch_Q) or ran more than
+ * one scan round (an overflowed list: the round's candidates are not kept). */
+int isax_debug_candidates(const isax_index *ix, uint32_t q, uint32_t *out_pos, uint64_t cap, uint64_t *count);
+
 /* Counters of the last isax_nn1 / isax_nn1_async call, as a JSON object written to buf.
  * It holds per-query window, window_rows (rows the approximate answer refined), candidates,
  * refined, abandoned, skipped, rounds, near, leaves_alive and the BSF before and after the scan,

@@ -37,6 +37,24 @@ static bool is_device_ptr(const void *p) {
     return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
 }
 
+// Every entry point that touches an index runs on the index's device (a caller may
+// have another device current); the caller's current device is restored on return.
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        if (cudaGetDevice(&prev) != cudaSuccess) {
+            cudaGetLastError();
+            prev = -1;
+            return;
+        }
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+    }
+};
+
 static isax_opts default_opts(const isax_opts *o) {
     isax_opts r{3072, -12, 1024, 0, 0, 5, 128};  // cand_cap 0: chosen per batch (alloc_scratch, nn1_device)
     if (o) {
@@ -79,7 +97,8 @@ static void free_scratch(isax_index *ix) {
     QueryScratch &q = ix->qs;
     cudaFree(q.qy); cudaFree(q.qpaa); cudaFree(q.qsax); cudaFree(q.lut); cudaFree(q.lut8); cudaFree(q.qconst); cudaFree(q.pwin);
     cudaFree(q.cand); cudaFree(q.candq); cudaFree(q.cand2); cudaFree(q.candq2); cudaFree(q.cnt_f); cudaFree(q.qscale); cudaFree(q.qT);
-    cudaFree(q.near); cudaFree(q.qmap); cudaFree(q.qband); cudaFree(q.cand_hist); cudaFree(q.task_ctr); cudaFree(q.qmap2);
+    cudaFree(q.near); cudaFree(q.near_off); cudaFree(q.near_cap);
+    cudaFree(q.qmap); cudaFree(q.qband); cudaFree(q.cand_hist); cudaFree(q.task_ctr); cudaFree(q.qmap2);
     cudaFree(q.status);  // bsf, bsf_scan, cand_cnt, cand_cnt2, cnt_hi, near_cnt, flag, counters, win, leaves, byte counters
     if (q.h_mirror) cudaFreeHost(q.h_mirror);
     q = QueryScratch{};
@@ -119,7 +138,7 @@ static int alloc_scratch_cap(isax_index *ix, uint32_t cap) {
     A(qsax, (size_t)Q * W);
     A(lut, (size_t)Q * W * CARD);
     A(lut8, (size_t)Q * W * CARD);
-    A(qconst, Q);
+    A(qconst, 2 * (size_t)Q);
     A(pwin, (size_t)Q * MAX_PROBES);
     A(cand, (size_t)Q * cap);
     A(candq, (size_t)Q * cap);
@@ -129,6 +148,8 @@ static int alloc_scratch_cap(isax_index *ix, uint32_t cap) {
     A(qscale, Q);
     A(qT, Q);
     A(near, (size_t)Q * NEAR_K);
+    A(near_off, Q);
+    A(near_cap, Q);
     A(qmap, Q);
     A(qband, Q);
     A(cand_hist, (size_t)Q * HIST_BINS);
@@ -164,6 +185,7 @@ static int alloc_scratch_cap(isax_index *ix, uint32_t cap) {
         return cuda_error(e, "allocating query scratch");
     }
     q.cap_Q = Q;
+    q.near_pool = (uint64_t)Q * NEAR_K;
     q.cand_cap = q.cand_cap_slot = cap;
     ix->device_bytes += acc;
     return ISAX_OK;
@@ -300,6 +322,37 @@ static float bsf_d2_host(unsigned long long p) {
     return f;
 }
 
+// Grow query i's near list after it overflowed (R9): a fresh region of the pool with room for
+// twice the appends it saw. Its rescan collects every near tie of its current BSF again: those rows
+// were all appended before (the BSF only falls, and a row within (1 + delta) of it completes and
+// is appended wherever it is refined), so the list keeps growing until it holds them all and the
+// rescan terminates. The pool grows (copying the live lists) when it has no room left.
+static int grow_near(isax_index *ix, uint32_t i, uint32_t seen, cudaStream_t s) {
+    QueryScratch &qs = ix->qs;
+    HostMirror &hm = qs.hm;
+    const uint64_t need = std::max<uint64_t>(2ull * seen, 2ull * hm.near_cap[i]);
+    if (need > 0xffffffffull) return set_error(ISAX_E_UNSUPPORTED, "more than 2^32 near ties for one query");
+    if (qs.near_used + need > qs.near_pool) {
+        const uint64_t pool = std::max<uint64_t>(2 * qs.near_pool, qs.near_used + need);
+        NearEntry *np = nullptr;
+        cudaError_t e = cudaMalloc(&np, pool * sizeof(NearEntry));
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            return cuda_error(e, "growing the near-tie pool");
+        }
+        ISAX_CUDA(cudaMemcpyAsync(np, qs.near, qs.near_used * sizeof(NearEntry), cudaMemcpyDeviceToDevice, s));
+        ISAX_CUDA(cudaStreamSynchronize(s));
+        cudaFree(qs.near);
+        ix->device_bytes += (pool - qs.near_pool) * sizeof(NearEntry);
+        qs.near = np;
+        qs.near_pool = pool;
+    }
+    hm.near_off[i] = qs.near_used;
+    hm.near_cap[i] = (uint32_t)need;
+    qs.near_used += need;
+    return ISAX_OK;
+}
+
 static int nn1_device(isax_index *ix, const float *d_q, uint32_t Q, int64_t *d_id, float *d_dist, cudaStream_t s) {
     int rc = alloc_scratch(ix);
     if (rc) return rc;
@@ -308,6 +361,7 @@ static int nn1_device(isax_index *ix, const float *d_q, uint32_t Q, int64_t *d_i
     const float delta = std::ldexp(1.0f, ix->opts.slack_log2);
     const float onepd = 1.0f + delta;
     const float INF = std::numeric_limits<float>::infinity();
+    const uint32_t NP = (uint32_t)ix->N;
     ix->st_win.assign(2 * (size_t)Q, 0);
     ix->st_cand.assign(Q, 0);
     ix->st_refined.assign(Q, 0);
@@ -332,6 +386,12 @@ static int nn1_device(isax_index *ix, const float *d_q, uint32_t Q, int64_t *d_i
                           ? qs.cand_cap_slot
                           : (uint32_t)std::min<uint64_t>(std::min<uint64_t>(ix->N, 1ull << 23),
                                                          (uint64_t)qs.cand_cap_slot * qs.cap_Q / B);
+        // near lists: q * NEAR_K, NEAR_K entries each (qprep_kernel writes the same on the device)
+        qs.near_used = (uint64_t)B * NEAR_K;
+        for (uint32_t i = 0; i < B; i++) {
+            hm.near_off[i] = (unsigned long long)i * NEAR_K;
+            hm.near_cap[i] = NEAR_K;
+        }
         const bool timed = b0 == 0;
         if (timed) cudaEventRecord(ix->ev[0], s);
         launch_qprep(ix, d_q + (uint64_t)b0 * ix->n, B, s, qs.flag);
@@ -340,20 +400,25 @@ static int nn1_device(isax_index *ix, const float *d_q, uint32_t Q, int64_t *d_i
         launch_window(ix, B, nullptr, delta, s);
         if (timed) cudaEventRecord(ix->ev[2], s);
         // Rounds (R10). Round 0 scans the band (-1, +inf) for every query, i.e. everything
-        // under the window BSF. If a query's candidate list overflows, its band is shrunk to the
-        // largest prefix of its LB histogram that fits, so the smallest bounds are refined first
-        // and the BSF tightens (MESSI's priority-queue order). When a shrunk band
-        // completes, the next band starts where it ended. It is skipped when the BSF has
-        // dropped below it. If a query's near list overflowed, its BSF is kept, the list is
-        // emptied, the window is re-refined and everything is rescanned, so every near tie of
-        // the final BSF is collected.
-        // Every round ends with one host synchronisation. The finalise kernel and all counter
-        // copies are enqueued before it; they are redone only if another round follows.
-        std::vector<float2> band(B, make_float2(-1.0f, INF));
+        // under the window BSF, over all positions. If a query's candidate list overflows, its
+        // band is shrunk to the largest prefix of its LB histogram that fits, so the smallest
+        // bounds are refined first and the BSF tightens (MESSI's priority-queue order,
+        // P:349-361). When a shrunk band completes, the next band starts where it ended; it is
+        // skipped when the BSF has dropped below it. A band the histogram cannot split any
+        // further (its bounds all but equal, e.g. many copies of one series) is scanned over
+        // parts of the sorted positions instead: halved while it overflows, then advanced with
+        // doubling length. If a query's near list overflowed, its BSF is kept, the list grows
+        // (grow_near), the window is re-refined and everything is rescanned, so every near tie of
+        // the final BSF is collected (R9).
+        // Every round ends with one host synchronisation. The finalise kernel (for the queries
+        // scanned in the round) and all counter copies are enqueued before it.
+        std::vector<Band> band(B, Band{-1.0f, INF, 0u, NP});
+        std::vector<uint32_t> plen(B, NP);  // position mode: length of the next range
+        std::vector<uint32_t> nfirst(B, 0);  // consecutive overflows whose first histogram bin alone overflowed
         std::vector<char> pending(B, 1);
         std::vector<float> bsf_h(B, INF), tused(B, -1.0f), bsf0_h(B, INF);
-        std::vector<uint32_t> hist((size_t)B * HIST_BINS);
         std::vector<uint32_t> rewin;
+        bool offs_dirty = false;
         for (uint32_t round = 0;; round++) {
             uint32_t nact = 0;
             for (uint32_t i = 0; i < B; i++) {
@@ -361,13 +426,18 @@ static int nn1_device(isax_index *ix, const float *d_q, uint32_t Q, int64_t *d_i
                 pending[i] = 0;
                 hm.qmap[nact] = i;
                 hm.band[nact] = band[i];
-                tused[i] = std::fmin(bsf_h[i] * onepd, band[i].y);  // round 0: set after the sync
+                tused[i] = std::fmin(bsf_h[i] * onepd, band[i].hi);  // round 0: set after the sync
                 nact++;
             }
             if (!nact) break;
             // (scanprep_kernel zeroes the candidate counts of all B slots and the scanned queries'
             // histograms)
             if (round > 0) {
+                if (offs_dirty) {
+                    ISAX_CUDA(cudaMemcpyAsync(qs.near_off, hm.near_off, B * sizeof(unsigned long long), cudaMemcpyHostToDevice, s));
+                    ISAX_CUDA(cudaMemcpyAsync(qs.near_cap, hm.near_cap, B * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+                    offs_dirty = false;
+                }
                 if (!rewin.empty()) {
                     for (uint32_t i : rewin) ISAX_CUDA(cudaMemsetAsync(qs.near_cnt + i, 0, sizeof(uint32_t), s));
                     memcpy(hm.rewin, rewin.data(), rewin.size() * sizeof(uint32_t));
@@ -377,10 +447,9 @@ static int nn1_device(isax_index *ix, const float *d_q, uint32_t Q, int64_t *d_i
                     ix->st_launches += 1;
                     rewin.clear();
                 }
-            }
-            if (round > 0) {  // (round 0's identity map and open bands are written by qprep_kernel)
+                // (round 0's identity map and open bands are written by qprep_kernel)
                 ISAX_CUDA(cudaMemcpyAsync(qs.qmap, hm.qmap, nact * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
-                ISAX_CUDA(cudaMemcpyAsync(qs.qband, hm.band, nact * sizeof(float2), cudaMemcpyHostToDevice, s));
+                ISAX_CUDA(cudaMemcpyAsync(qs.qband, hm.band, nact * sizeof(Band), cudaMemcpyHostToDevice, s));
             }
             ix->st_scan_bytes += launch_lbscan(ix, nact, B, qs.qmap, qs.qband, delta, s);
             if (timed && round == 0) cudaEventRecord(ix->ev[6], s);
@@ -388,7 +457,8 @@ static int nn1_device(isax_index *ix, const float *d_q, uint32_t Q, int64_t *d_i
             if (timed && round == 0) cudaEventRecord(ix->ev[3], s);
             launch_refine(ix, B, delta, s);
             if (timed && round == 0) cudaEventRecord(ix->ev[4], s);
-            launch_finalize(ix, B, delta, d_id + b0, d_dist + b0, s);  // speculative: redone after another round
+            // speculative: a query scanned again in a later round is finalised again
+            launch_finalize(ix, nact, qs.qmap, delta, d_id + b0, d_dist + b0, s);
             // scanprep + scan, candcheck, refine + filter + refine, finalize
             ix->st_launches += ((ix->opts.flags & ISAX_FLAG_FLAT_SCAN) ? 1 : 2) + 5;
             if (timed && round == 0) cudaEventRecord(ix->ev[5], s);
@@ -416,33 +486,74 @@ static int nn1_device(isax_index *ix, const float *d_q, uint32_t Q, int64_t *d_i
             }
             bool any_ovf = false;
             for (uint32_t k = 0; k < nact; k++) any_ovf |= hm.cand_cnt[hm.qmap[k]] > qs.cand_cap;
-            if (any_ovf)
-                ISAX_CUDA(cudaMemcpy(hist.data(), qs.cand_hist, hist.size() * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+            if (any_ovf) {  // the scanned queries' LB histograms (pinned mirror)
+                ISAX_CUDA(cudaMemcpyAsync(hm.hist, qs.cand_hist, (size_t)B * HIST_BINS * sizeof(uint32_t),
+                                          cudaMemcpyDeviceToHost, s));
+                ISAX_CUDA(cudaStreamSynchronize(s));
+            }
             for (uint32_t k = 0; k < nact; k++) {
                 const uint32_t i = hm.qmap[k];
                 const uint32_t cnt = hm.cand_cnt[i];
                 bsf_h[i] = bsf_d2_host(hm.bsf[i]);
                 ix->st_cand[b0 + i] += hm.cand_cnt2[i] + hm.cnt_hi[i];  // after the exact rule (candcheck_kernel)
                 ix->st_rounds[b0 + i] = round + 1;
-                if (hm.near_cnt[i] > (uint32_t)NEAR_K) {  // near overflow: start over, BSF kept
-                    band[i] = make_float2(-1.0f, INF);
+                Band &bd = band[i];
+                if (cnt <= qs.cand_cap) nfirst[i] = 0;
+                if (hm.near_cnt[i] > hm.near_cap[i]) {  // near overflow: grow the list, start over, BSF kept
+                    if ((rc = grow_near(ix, i, hm.near_cnt[i], s))) return rc;
+                    offs_dirty = true;
+                    bd = Band{-1.0f, INF, 0u, NP};
+                    plen[i] = NP;
                     pending[i] = 1;
                     rewin.push_back(i);
-                } else if (cnt > qs.cand_cap) {  // shrink the band to the histogram prefix that fits
-                    const float lo0 = std::fmax(band[i].x, 0.0f), span = tused[i] - lo0;
+                } else if (cnt > qs.cand_cap) {
+                    // shrink the band to the histogram prefix that fits
+                    const float lo0 = std::fmax(bd.lo, 0.0f), span = tused[i] - lo0;
                     uint64_t cum = 0;
                     int kk = -1;
                     for (uint32_t bb = 0; bb < HIST_BINS; bb++) {
-                        cum += hist[(size_t)i * HIST_BINS + bb];
+                        cum += hm.hist[(size_t)i * HIST_BINS + bb];
                         if (cum > (uint64_t)qs.cand_cap * 9 / 10) break;
                         kk = (int)bb;
                     }
-                    band[i].y = lo0 + span * (float)(kk + 1) / (float)HIST_BINS;
-                    if (kk < 0) band[i].y = lo0 + span / (float)HIST_BINS;
+                    const float hi_new = kk < 0 ? lo0 + span / (float)HIST_BINS : lo0 + span * (float)(kk + 1) / (float)HIST_BINS;
+                    // The histogram cannot split the band when its first bin alone overflows for the
+                    // third time in a row (many bounds at one value: a bin never gets below it), when
+                    // the band is narrower than 2^-16 of its bounds (or empty: all bounds equal), or
+                    // when the shrunk edge rounds onto the lower one. Then this band is scanned over
+                    // parts of the sorted positions instead.
+                    nfirst[i] = kk < 0 ? nfirst[i] + 1 : 0;
+                    const bool stuck = (kk < 0 && (nfirst[i] >= 3 || !(span > std::fmax(lo0, tused[i]) * 1.52587890625e-05f))) ||
+                                       !(hi_new > lo0);
+                    if (stuck || bd.phi - bd.plo < NP) {
+                        const uint32_t len = bd.phi - bd.plo;
+                        if (len <= 1) return set_error(ISAX_E_CUDA, "candidate list overflow at a single position");
+                        bd.phi = bd.plo + len / 2;
+                        plen[i] = len / 2;
+                    } else {
+                        bd.hi = hi_new;
+                    }
                     pending[i] = 1;
-                } else if (tused[i] == band[i].y && bsf_h[i] * onepd > band[i].y) {
+                } else if (bd.phi < NP || bd.plo > 0) {
+                    // a position range of a split band completed: the next one, twice as long
+                    if (bd.phi < NP) {
+                        const uint64_t len = std::min<uint64_t>(2ull * plen[i], NP);
+                        plen[i] = (uint32_t)len;
+                        bd.plo = bd.phi;
+                        bd.phi = (uint32_t)std::min<uint64_t>((uint64_t)bd.plo + len, NP);
+                        pending[i] = 1;
+                    } else {  // the band is complete over all positions: continue with the next band
+                        bd.plo = 0;
+                        bd.phi = NP;
+                        plen[i] = NP;
+                        if (tused[i] == bd.hi && bsf_h[i] * onepd > bd.hi) {
+                            bd = Band{bd.hi, INF, 0u, NP};
+                            pending[i] = 1;
+                        }
+                    }
+                } else if (tused[i] == bd.hi && bsf_h[i] * onepd > bd.hi) {
                     // the band was capped below the BSF: continue with the next band
-                    band[i] = make_float2(band[i].y, INF);
+                    bd = Band{bd.hi, INF, 0u, NP};
                     pending[i] = 1;
                 }
             }
@@ -513,6 +624,8 @@ int isax_nn1_async(const isax_index *cix, const float *d_queries, uint32_t Q, in
     if (!d_queries || !d_out_id || !d_out_dist) return set_error(ISAX_E_INVAL, "NULL pointer");
     isax_index *ix = const_cast<isax_index *>(cix);
     std::lock_guard<std::mutex> lk(ix->mu);
+    DeviceGuard dg(ix->device);
+    ix->st_last_Q = Q;
     return nn1_device(ix, d_queries, Q, d_out_id, d_out_dist, (cudaStream_t)cuda_stream);
 }
 
@@ -522,6 +635,8 @@ int isax_nn1(const isax_index *cix, const float *queries, uint32_t Q, int64_t *o
     if (!queries || !out_id || !out_dist) return set_error(ISAX_E_INVAL, "NULL pointer");
     isax_index *ix = const_cast<isax_index *>(cix);
     std::lock_guard<std::mutex> lk(ix->mu);
+    DeviceGuard dg(ix->device);
+    ix->st_last_Q = Q;
     // the index keeps one stream and staging buffers for host pointers (grown on demand)
     if (!ix->io_stream) ISAX_CUDA(cudaStreamCreateWithFlags(&ix->io_stream, cudaStreamNonBlocking));
     cudaStream_t s = ix->io_stream;
@@ -557,6 +672,7 @@ int isax_export(const isax_index *ix, uint64_t first_id, uint64_t count, uint8_t
                 float *stored) {
     if (!ix) return set_error(ISAX_E_INVAL, "index is NULL");
     if (first_id > ix->N || count > ix->N - first_id) return set_error(ISAX_E_INVAL, "range out of bounds");
+    DeviceGuard dg(ix->device);
     cudaStream_t s;
     ISAX_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
     int rc = ISAX_OK;
@@ -591,6 +707,7 @@ int isax_query_debug(const isax_index *cix, const float *queries, uint32_t Q, do
     if (lb2 && (first_pos > cix->N || count > cix->N - first_pos)) return set_error(ISAX_E_INVAL, "range out of bounds");
     isax_index *ix = const_cast<isax_index *>(cix);
     std::lock_guard<std::mutex> lk(ix->mu);
+    DeviceGuard dg(ix->device);
     int rc = alloc_scratch(ix);
     if (rc) return rc;
     if (Q > ix->qs.cap_Q) return set_error(ISAX_E_INVAL, "Q exceeds batch_Q");
@@ -629,6 +746,26 @@ int isax_query_debug(const isax_index *cix, const float *queries, uint32_t Q, do
     cudaFree(dq); cudaFree(dlb); cudaFree(flag);
     cudaStreamDestroy(s);
     return rc;
+}
+
+int isax_debug_candidates(const isax_index *cix, uint32_t q, uint32_t *out_pos, uint64_t cap, uint64_t *count) {
+    if (!cix || !count) return set_error(ISAX_E_INVAL, "index or count is NULL");
+    isax_index *ix = const_cast<isax_index *>(cix);
+    std::lock_guard<std::mutex> lk(ix->mu);
+    const QueryScratch &qs = ix->qs;
+    if (!qs.cap_Q || ix->st_last_Q == 0 || ix->st_last_Q > qs.cap_Q || q >= ix->st_last_Q)
+        return set_error(ISAX_E_INVAL, "no candidate list: q out of range, or the last call spanned several batches");
+    for (uint32_t i = 0; i < ix->st_last_Q; i++)
+        if (ix->st_rounds[i] != 1) return set_error(ISAX_E_INVAL, "the last call ran more than one round");
+    DeviceGuard dg(ix->device);
+    const uint32_t n1 = qs.hm.cand_cnt2[q], n2 = qs.hm.cnt_hi[q];
+    *count = (uint64_t)n1 + n2;
+    if (!out_pos || cap < *count) return ISAX_OK;
+    cudaError_t e = cudaMemcpy(out_pos, qs.cand2 + (uint64_t)q * qs.cand_cap, n1 * sizeof(uint32_t), cudaMemcpyDefault);
+    if (e == cudaSuccess && n2)
+        e = cudaMemcpy(out_pos + n1, qs.cand2 + (uint64_t)q * qs.cand_cap + (qs.cand_cap - n2), n2 * sizeof(uint32_t),
+                       cudaMemcpyDefault);
+    return e == cudaSuccess ? ISAX_OK : cuda_error(e, "isax_debug_candidates");
 }
 
 int isax_stats(const isax_index *cix, char *buf, size_t cap) {
@@ -710,6 +847,7 @@ void isax_free(isax_index *ix) {
     if (!ix) return;
     {
         std::lock_guard<std::mutex> lk(ix->mu);
+        DeviceGuard dg(ix->device);
         cudaFree(ix->stored);
         cudaFree(ix->sax);
         cudaFree(ix->perm);

@@ -59,6 +59,13 @@ __device__ __forceinline__ double warp_sum_d(double v) {
 
 __device__ __forceinline__ float bsf_d2(unsigned long long p) { return __uint_as_float((uint32_t)(p >> 32)); }
 
+// append a near tie (R9) of query q; the count keeps growing past the capacity, so the host
+// sees an overflow and sizes the query's next list from it (api.cu)
+__device__ __forceinline__ void near_append(const NearList &nl, uint32_t q, uint32_t id, uint32_t pos, float d2) {
+    const uint32_t k = atomicAdd(&nl.cnt[q], 1u);
+    if (k < nl.cap[q]) nl.base[nl.off[q] + k] = NearEntry{id, pos, d2, 0};
+}
+
 // y = fp32_rne(fl64((x - mu) / sd)), the stored value of R2/R3, without a full fp64 division per
 // element. q = (x - mu) * rcp, with rcp = fl64(1/sd), is within 2.5 fp64 ulps of the correctly
 // rounded quotient Q. Rounding to fp32 drops the low 29 bits of the fp64 significand, and it can

@@ -19,7 +19,7 @@ namespace isax {
 
 constexpr int W = 16;        // segments ("w is fixed to 16")
 constexpr int CARD = 256;    // symbols per segment (8 bits)
-constexpr int NEAR_K = 256;  // near-tie list capacity per query (R9)
+constexpr int NEAR_K = 256;  // near-tie list capacity per query, until it overflows (R9; api.cu grows it)
 constexpr uint32_t MAX_PROBES = 32;  // 2^probe_bits windows per query, probe_bits <= 5
 constexpr uint32_t HIST_BINS = 64;   // per-query histogram of kept LB^2 inside its band (R10)
 constexpr uint32_t LEAF_SIZE = 32;    // sorted positions per leaf node (R11)
@@ -56,13 +56,32 @@ struct NearEntry {  // a completed refinement within (1+delta) of the BSF at tha
     uint32_t pad;
 };
 
+// Query q's near list is near[near_off[q] .. near_off[q] + near_cap[q]). A batch starts with
+// near_off[q] = q * NEAR_K and near_cap[q] = NEAR_K; a query whose list overflowed is given a
+// region as large as twice the count it reached before its rescan (api.cu, R9).
+struct NearList {
+    NearEntry *base;
+    const unsigned long long *off;
+    const uint32_t *cap;
+    uint32_t *cnt;
+};
+
+// One scan round of a query (R10): keep a position iff lo < LB^2 <= min(hi, bsf^2 (1 + delta))
+// and plo <= pos < phi. The position range is [0, N) unless the LB band could not be split any
+// further (many equal bounds): then the round covers part of the sorted positions.
+struct __align__(16) Band {
+    float lo, hi;
+    uint32_t plo, phi;
+};
+
 // The per-batch status the host reads after every round: one contiguous block on the device and
 // the same layout in pinned host memory, so a round ends with a single D2H copy.
 struct StatusBlock {
     static constexpr size_t RESET_BYTES = 48;  // scan_bytes_dev, refine_bytes, flag (16-B slots)
     unsigned long long *bsf, *bsf_scan, *scan_bytes_dev, *refine_bytes;
     uint32_t *cand_cnt, *cand_cnt2, *cnt_hi, *near_cnt, *flag, *counters, *win, *leaves;
-    static size_t bytes(uint32_t Q) { return (size_t)Q * (8 + 8 + 4 * 4 + 16 + 8 + 4) + 16 * 16; }
+    // a multiple of 16: the host mirror's own arrays follow it (Band needs 16-byte alignment)
+    static size_t bytes(uint32_t Q) { return ((size_t)Q * (8 + 8 + 4 * 4 + 16 + 8 + 4) + 16 * 16 + 15) & ~size_t(15); }
     void carve(void *base, uint32_t Q) {
         unsigned char *p = static_cast<unsigned char *>(base);
         auto take = [&](size_t n) { unsigned char *r = p; p += (n + 15) & ~size_t(15); return r; };
@@ -84,17 +103,23 @@ struct StatusBlock {
 // Pinned host memory: the status mirror plus the per-round inputs the host writes.
 struct HostMirror : StatusBlock {
     void *status = nullptr;
-    uint32_t *qmap, *rewin;
-    float2 *band;
-    static size_t bytes(uint32_t Q) { return StatusBlock::bytes(Q) + (size_t)Q * (4 + 4 + 8) + 3 * 16; }
+    uint32_t *qmap, *rewin, *hist, *near_cap;
+    unsigned long long *near_off;
+    Band *band;
+    static size_t bytes(uint32_t Q) {
+        return StatusBlock::bytes(Q) + (size_t)Q * (4 + 4 + 16 + 4 * HIST_BINS + 4 + 8) + 6 * 16;
+    }
     void carve(void *base, uint32_t Q) {
         status = base;
         StatusBlock::carve(base, Q);
         unsigned char *p = static_cast<unsigned char *>(base) + StatusBlock::bytes(Q);
         auto take = [&](size_t n) { unsigned char *r = p; p += (n + 15) & ~size_t(15); return r; };
-        band = reinterpret_cast<float2 *>(take(8ull * Q));
+        band = reinterpret_cast<Band *>(take(16ull * Q));
         qmap = reinterpret_cast<uint32_t *>(take(4ull * Q));
         rewin = reinterpret_cast<uint32_t *>(take(4ull * Q));
+        hist = reinterpret_cast<uint32_t *>(take(4ull * Q * HIST_BINS));
+        near_cap = reinterpret_cast<uint32_t *>(take(4ull * Q));
+        near_off = reinterpret_cast<unsigned long long *>(take(8ull * Q));
     }
 };
 
@@ -108,7 +133,7 @@ struct QueryScratch {
     uint8_t *qsax = nullptr;        // [Q][16]
     float *lut = nullptr;           // [Q][16][256] fp32, rounded down
     uint8_t *lut8 = nullptr;        // [Q][16][256] u8 scan table of each active slot (R11b)
-    uint4 *qconst = nullptr;        // [Q] scan constants of each active slot (band lo, T, window)
+    uint4 *qconst = nullptr;        // [Q][2] scan constants of each active slot (band lo, T, window, positions)
     uint32_t *win = nullptr;        // [Q][2] window [start, end)
     uint32_t *pwin = nullptr;       // [Q][MAX_PROBES]: kept probe window starts (probe_L rows each), count last
     unsigned long long *bsf = nullptr;  // [Q] packed
@@ -123,10 +148,14 @@ struct QueryScratch {
     float *qscale = nullptr;        // [Q] 254 / T of the query's last scan, rounded down (R11b)
     float *qT = nullptr;            // [Q] T of the query's last scan
     uint32_t *cand_cnt = nullptr;   // [Q] (may exceed cand_cap: overflow)
-    NearEntry *near = nullptr;      // [Q][NEAR_K]
-    uint32_t *near_cnt = nullptr;   // [Q]
+    NearEntry *near = nullptr;      // near pool: [Q][NEAR_K], then the grown lists of overflowed queries
+    uint64_t near_pool = 0;         // entries allocated in `near`
+    uint64_t near_used = 0;         // entries handed out in the current batch
+    unsigned long long *near_off = nullptr;  // [Q] first entry of query q's near list in the pool
+    uint32_t *near_cap = nullptr;   // [Q] its capacity
+    uint32_t *near_cnt = nullptr;   // [Q] appends so far (may exceed near_cap: overflow)
     uint32_t *qmap = nullptr;       // [Q] active slot -> batch slot, for re-scan rounds
-    float2 *qband = nullptr;        // [Q] LB band (lo, hi] of each active slot (R10)
+    Band *qband = nullptr;          // [Q] LB band (lo, hi] and position range of each active slot (R10)
     uint32_t *cand_hist = nullptr;  // [Q][HIST_BINS] histogram of kept LB^2 in the band
     uint32_t *counters = nullptr;   // [Q][4]: refined, abandoned, skipped by the u8 bound, (unused)
     uint32_t *counters_leaf = nullptr;  // [Q]: (leaf, query) pairs that survived the node bound
@@ -168,6 +197,7 @@ struct isax_index {
     std::vector<float> st_bsf0, st_bsf_final;
     isax::StageTimes st_ms;
     uint64_t st_launches = 0;  // kernels launched by the last nn1 call
+    uint32_t st_last_Q = 0;     // Q of the last nn1 call
     uint64_t st_scan_bytes = 0, st_scan_bytes_first = 0;  // summary bytes the scan read (all / first launch)
     uint64_t st_refine_bytes_first = 0;                    // row bytes the first refine launch read
     uint64_t st_leaf_pairs_first = 0, st_scan_q_first = 0; // (leaf, query) pairs kept / queries of the first scan
@@ -223,17 +253,18 @@ void launch_leaf_meta(const uint8_t *sax, uint64_t N, uint8_t *lmeta, uint8_t *s
 // permute.cu: the kd order inside every full super-node (R6b), the super-nodes' smallest keys and
 // their first two kd splits (sax and perm are permuted in place)
 void launch_superkd(uint8_t *sax, uint32_t *perm, uint64_t N, uint4 *skey, KdSplits *ksplit, cudaStream_t s);
-// Scan all sorted positions for the nq queries qmap[0..nq), keeping band[i].x < LB^2 <= min(band[i].y,
-// bsf^2 (1+delta)) for slot i. Returns the summary bytes it reads that the host can count (node
+// Scan all sorted positions for the nq queries qmap[0..nq), keeping band[i].lo < LB^2 <= min(band[i].hi,
+// bsf^2 (1+delta)) and band[i].plo <= pos < band[i].phi for slot i. Returns the summary bytes it reads that the host can count (node
 // summaries or flat words); the leaf scan adds its leaf-word and leaf-summary bytes to qs.scan_bytes_dev on the device.
-uint64_t launch_lbscan(const isax_index *ix, uint32_t nq, uint32_t B, const uint32_t *qmap, const float2 *band,
+uint64_t launch_lbscan(const isax_index *ix, uint32_t nq, uint32_t B, const uint32_t *qmap, const Band *band,
                        float delta, cudaStream_t s);
 // lbscan.cu: the exact fp32 rule for the candidates the leaf scan kept on their u8 sum alone,
 // and compaction of every list into cand2 / cand_cnt2 (the refine's input)
 void launch_candcheck(const isax_index *ix, uint32_t Q, cudaStream_t s);
 // refine.cu
 void launch_refine(const isax_index *ix, uint32_t Q, float delta, cudaStream_t s);
-void launch_finalize(const isax_index *ix, uint32_t Q, float delta, int64_t *out_id, float *out_dist,
+// finalise the nq queries qmap[0 .. nq) (the ones the round scanned): exact near-tie resolution (R9)
+void launch_finalize(const isax_index *ix, uint32_t nq, const uint32_t *qmap, float delta, int64_t *out_id, float *out_dist,
                      cudaStream_t s);
 
 }  // namespace isax

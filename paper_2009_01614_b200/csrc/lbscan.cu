@@ -120,16 +120,23 @@ __device__ __forceinline__ uint32_t hist_bin(float lb, float lo, float hi) {
     return min((uint32_t)(fmaxf(x, 0.f) * (float)HIST_BINS), HIST_BINS - 1);
 }
 
-struct __align__(16) QConst {  // per query slot, read with one 16-byte shared load
+struct __align__(16) QConst {  // per query slot, two 16-byte words
     float lo, T;               // band (lo, T]: T = min(band_hi, bsf^2 (1 + delta))
     uint32_t ws, we;           // window [ws, we): already refined, never a candidate
+    uint32_t plo, phi;         // the round's position range [plo, phi) (R10; [0, N) unless split)
+    uint32_t pad0, pad1;
 };
 
+// the keep rule's position part: outside the window, inside the round's range
+__device__ __forceinline__ bool pos_ok(const QConst &k, uint32_t pos) {
+    return (pos < k.ws || pos >= k.we) && pos >= k.plo && pos < k.phi;
+}
+
 __device__ __forceinline__ QConst load_qconst(uint32_t qi, bool valid, const unsigned long long *bsf,
-                                              const float2 *band, uint32_t slot, const uint32_t *win, float onepd) {
-    const float2 b = valid ? band[slot] : make_float2(0.f, -1.f);
-    const float tq = valid ? fminf(bsf_d2(bsf[qi]) * onepd, b.y) : -1.0f;  // an invalid slot keeps nothing
-    return QConst{b.x, tq, win[2 * qi], win[2 * qi + 1]};
+                                              const Band *band, uint32_t slot, const uint32_t *win, float onepd) {
+    const Band b = valid ? band[slot] : Band{0.f, -1.f, 0u, 0u};
+    const float tq = valid ? fminf(bsf_d2(bsf[qi]) * onepd, b.hi) : -1.0f;  // an invalid slot keeps nothing
+    return QConst{b.lo, tq, win[2 * qi], win[2 * qi + 1], b.plo, b.phi, 0u, 0u};
 }
 
 // ------------------------------------------------------------------------------------ flat scan
@@ -140,7 +147,7 @@ template <int G>
 __global__ void __launch_bounds__(LB_THREADS) lbscan_kernel(const uint4 *__restrict__ sax, uint32_t N,
                                                             const float *__restrict__ lut_all,
                                                             const uint32_t *__restrict__ qmap,
-                                                            const float2 *__restrict__ band, uint32_t nq,
+                                                            const Band *__restrict__ band, uint32_t nq,
                                                             const unsigned long long *__restrict__ bsf,
                                                             const uint32_t *__restrict__ win, float onepd,
                                                             uint32_t *__restrict__ cand,
@@ -181,7 +188,7 @@ __global__ void __launch_bounds__(LB_THREADS) lbscan_kernel(const uint4 *__restr
             for (int g = 0; g < G; g++) {
                 const QConst k = qc[g];
                 const float lb = word_lb(slut + g * W * CARD, wv[u]);
-                const bool keep = inr && lb > k.lo && lb <= k.T && (pos < k.ws || pos >= k.we);
+                const bool keep = inr && lb > k.lo && lb <= k.T && pos_ok(k, pos);
                 const uint32_t bal = __ballot_sync(0xffffffffu, keep);
                 if (bal) {
                     uint32_t off = 0;
@@ -202,14 +209,11 @@ __global__ void __launch_bounds__(LB_THREADS) lbscan_kernel(const uint4 *__restr
 }
 
 template <int G>
-static void launch_g(const isax_index *ix, uint32_t nq, const uint32_t *qmap, const float2 *band, float onepd,
+static void launch_g(const isax_index *ix, uint32_t nq, const uint32_t *qmap, const Band *band, float onepd,
                      cudaStream_t s) {
     const size_t smem = (size_t)G * W * CARD * sizeof(float);
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(lbscan_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        configured = true;
-    }
+    // per launch (the attribute is per device; a failure surfaces as the launch's error)
+    cudaFuncSetAttribute(lbscan_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -336,7 +340,7 @@ __device__ __forceinline__ uint32_t q8(float v, float sc) {
 // Per active slot of a scan launch: its constants (band lo, T, window) and its u8 table, once,
 // instead of in every CTA that takes one of its tasks. One CTA per slot.
 __global__ void __launch_bounds__(256) scanprep_kernel(const float *__restrict__ lut_all, const uint32_t *__restrict__ qmap,
-                                                       const float2 *__restrict__ band,
+                                                       const Band *__restrict__ band,
                                                        const unsigned long long *__restrict__ bsf,
                                                        const uint32_t *__restrict__ win, float onepd,
                                                        uint8_t *__restrict__ lut8, uint4 *__restrict__ qconst,
@@ -355,7 +359,10 @@ __global__ void __launch_bounds__(256) scanprep_kernel(const float *__restrict__
     if (threadIdx.x < HIST_BINS) hist[qmap[i] * HIST_BINS + threadIdx.x] = 0;
     const uint32_t qi = qmap[i];
     const QConst k = load_qconst(qi, true, bsf, band, i, win, onepd);
-    if (threadIdx.x == 0) qconst[i] = make_uint4(__float_as_uint(k.lo), __float_as_uint(k.T), k.ws, k.we);
+    if (threadIdx.x == 0) {
+        qconst[2 * i] = make_uint4(__float_as_uint(k.lo), __float_as_uint(k.T), k.ws, k.we);
+        qconst[2 * i + 1] = make_uint4(k.plo, k.phi, 0u, 0u);
+    }
     const bool none = !(k.T >= 0.f);  // an empty band keeps nothing
     const float sc = none ? 0.f : __fdiv_rd(254.0f, k.T);  // T = 0 -> +inf
     if (threadIdx.x == 0) {
@@ -460,8 +467,9 @@ __global__ void __launch_bounds__(LF_THREADS, 1) leafscan_kernel(
                 const uint4 w = reinterpret_cast<const uint4 *>(qsax_all)[qi];
                 qsym[t][0] = make_uint4(lo_u16x2(w.x), hi_u16x2(w.x), lo_u16x2(w.y), hi_u16x2(w.y));
                 qsym[t][1] = make_uint4(lo_u16x2(w.z), hi_u16x2(w.z), lo_u16x2(w.w), hi_u16x2(w.w));
-                const uint4 k = qconst_all[slot];
-                qc[t] = valid ? QConst{__uint_as_float(k.x), __uint_as_float(k.y), k.z, k.w} : QConst{0.f, -1.f, 0u, 0u};
+                const uint4 k = qconst_all[2 * slot], k2 = qconst_all[2 * slot + 1];
+                qc[t] = valid ? QConst{__uint_as_float(k.x), __uint_as_float(k.y), k.z, k.w, k2.x, k2.y, 0u, 0u}
+                              : QConst{0.f, -1.f, 0u, 0u, 0u, 0u, 0u, 0u};
                 qsc[t] = valid && __uint_as_float(k.y) >= 0.f ? __fdiv_rd(254.0f, __uint_as_float(k.y)) : 0.f;  // as scanprep
             }
             // the group's u8 tables; a padding slot gets all-255 entries (it prunes everything)
@@ -601,7 +609,7 @@ __global__ void __launch_bounds__(LF_THREADS, 1) leafscan_kernel(
                 // the word is re-read here (volatile), so that the compiler does not hoist the fp32
                 // path's address arithmetic out of the query loop into every entry
                 const float lb = check ? word_lb(lut_all + (uint64_t)qid[g] * W * CARD, ld_sh_v4(wp)) : 0.f;
-                const bool keep = (first || (check && lb > kq.lo && lb <= kq.T)) && (pos < kq.ws || pos >= kq.we);
+                const bool keep = (first || (check && lb > kq.lo && lb <= kq.T)) && pos_ok(kq, pos);
                 // the candidate's u8 bound b <= LB^2 * sc (for the refine), or B_UNCHECKED
                 uint32_t b = e8 <= E_SURE ? e8 : B_UNCHECKED;
                 if (check) {
@@ -627,11 +635,8 @@ static void launch_leaf(const isax_index *ix, uint32_t nq, const uint32_t *qmap,
     constexpr uint32_t NW = LF_THREADS / 32;
     const size_t smem = (size_t)G * W * CARD + 256 + (size_t)G * CBUF * sizeof(uint32_t) + CHUNK * 4 +
                         (size_t)NW * PD * LEAF * sizeof(uint4) + (size_t)G * CBUF;
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(leafscan_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        configured = true;
-    }
+    // per launch (the attribute is per device; a failure surfaces as the launch's error)
+    cudaFuncSetAttribute(leafscan_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -653,7 +658,7 @@ static void launch_leaf(const isax_index *ix, uint32_t nq, const uint32_t *qmap,
         qs.scan_bytes_dev, qs.task_ctr);
 }
 
-uint64_t launch_lbscan(const isax_index *ix, uint32_t nq, uint32_t B, const uint32_t *qmap, const float2 *band,
+uint64_t launch_lbscan(const isax_index *ix, uint32_t nq, uint32_t B, const uint32_t *qmap, const Band *band,
                        float delta, cudaStream_t s) {
     if (!nq) return 0;
     const float onepd = 1.0f + delta;

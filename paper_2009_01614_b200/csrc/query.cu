@@ -61,8 +61,9 @@ __global__ void __launch_bounds__(NT) qprep_kernel(const float *__restrict__ que
                                                     uint8_t *__restrict__ qsax, float *__restrict__ lut,
                                                     uint32_t *__restrict__ win, unsigned long long *__restrict__ bsf,
                                                     uint32_t *__restrict__ cand_cnt, uint32_t *__restrict__ near_cnt,
+                                                    unsigned long long *__restrict__ near_off, uint32_t *__restrict__ near_cap,
                                                     uint32_t *__restrict__ counters, uint32_t *__restrict__ counters_leaf,
-                                                    uint32_t *__restrict__ qmap, float2 *__restrict__ qband,
+                                                    uint32_t *__restrict__ qmap, Band *__restrict__ qband,
                                                     uint32_t *__restrict__ bad) {
     __shared__ float row[1024];
     __shared__ double beta[ISAX_NBETA];
@@ -92,10 +93,12 @@ __global__ void __launch_bounds__(NT) qprep_kernel(const float *__restrict__ que
         // reset the per-query state of this batch slot
         cand_cnt[q] = 0;
         near_cnt[q] = 0;
+        near_off[q] = (unsigned long long)q * NEAR_K;
+        near_cap[q] = NEAR_K;
         counters[4 * q + 0] = counters[4 * q + 1] = counters[4 * q + 2] = counters[4 * q + 3] = 0;
         counters_leaf[q] = 0;
-        qmap[q] = q;  // round 0 scans every query of the batch over the band (-1, +inf) (R10)
-        qband[q] = make_float2(-1.0f, __int_as_float(0x7f800000));
+        qmap[q] = q;  // round 0 scans every query of the batch over the band (-1, +inf), all positions (R10)
+        qband[q] = Band{-1.0f, __int_as_float(0x7f800000), 0u, (uint32_t)N};
         bsf[q] = ~0ull;
     }
     __syncthreads();
@@ -250,7 +253,7 @@ void launch_qprep(const isax_index *ix, const float *queries, uint32_t Q, cudaSt
     auto kern = Q <= (uint32_t)(2 * sms) ? qprep_kernel<1024> : qprep_kernel<256>;
     kern<<<Q, Q <= (uint32_t)(2 * sms) ? 1024 : 256, 0, s>>>(queries, ix->n, ix->skey, ix->ksplit, ix->N,
                                    ix->opts.window_L, probe_bits(ix), ix->opts.probe_L, qs.pwin, qs.qy, qs.qpaa, qs.qsax, qs.lut, qs.win, qs.bsf, qs.cand_cnt,
-                                   qs.near_cnt, qs.counters, qs.counters_leaf, qs.qmap, qs.qband, bad);
+                                   qs.near_cnt, qs.near_off, qs.near_cap, qs.counters, qs.counters_leaf, qs.qmap, qs.qband, bad);
 }
 
 // ------------------------------------------------------------------------------------ window
@@ -290,9 +293,8 @@ __global__ void __launch_bounds__(256) window_kernel(const float *__restrict__ s
                                                      uint32_t n, uint64_t N, const float *__restrict__ qy,
                                                      const uint32_t *__restrict__ win, const uint32_t *__restrict__ pwin,
                                                      uint32_t nprobe, uint32_t Lp, const uint32_t *__restrict__ qmap,
-                                                     unsigned long long *__restrict__ bsf, NearEntry *__restrict__ near,
-                                                     uint32_t *__restrict__ near_cnt, uint32_t *__restrict__ counters,
-                                                     float onepd) {
+                                                     unsigned long long *__restrict__ bsf, NearList nl,
+                                                     uint32_t *__restrict__ counters, float onepd) {
     __shared__ float d2s[WIN_ROWS];
     __shared__ unsigned long long smin;
     __shared__ unsigned long long cur;
@@ -367,16 +369,14 @@ __global__ void __launch_bounds__(256) window_kernel(const float *__restrict__ s
     if (t == 0) {
         atomicMin(&bsf[q], smin);
         cur = atomicAdd(&bsf[q], 0ull);
-        atomicAdd(&counters[4 * q + 0], r1 - r0);
-        atomicAdd(&counters[4 * q + 3], r1 - r0);  // window rows (stats)
+        atomicAdd(&counters[4 * q + 3], r1 - r0);  // window rows (stats; "refined" counts candidates only)
     }
     __syncthreads();
     const float lim = bsf_d2(cur) * onepd;
     for (uint32_t r = r0 + t; r < r1; r += blockDim.x) {
         if (d2s[r - r0] <= lim) {
             const uint32_t pos = row_pos(r);
-            const uint32_t k = atomicAdd(&near_cnt[q], 1u);
-            if (k < NEAR_K) near[(uint64_t)q * NEAR_K + k] = NearEntry{perm[pos], pos, d2s[r - r0], 0};
+            near_append(nl, q, perm[pos], pos, d2s[r - r0]);
         }
     }
 }
@@ -401,7 +401,8 @@ void launch_window(const isax_index *ix, uint32_t Q, const uint32_t *qmap, float
 #define WIN_CASE(K)                                                                                          \
     case K:                                                                                                  \
         window_kernel<K><<<grid, 256, 0, s>>>(ix->stored, ix->perm, ix->n, ix->N, qs.qy, qs.win, qs.pwin,    \
-                                              nprobe, ix->opts.probe_L, qmap, qs.bsf, qs.near, qs.near_cnt,   \
+                                              nprobe, ix->opts.probe_L, qmap, qs.bsf,                         \
+                                              NearList{qs.near, qs.near_off, qs.near_cap, qs.near_cnt},       \
                                               qs.counters, onepd);                                           \
         break;
     switch (ns) {

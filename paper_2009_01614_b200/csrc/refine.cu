@@ -13,9 +13,9 @@
 //   - after each step but the last, it abandons iff the partial sum > bsf * (1 + delta) (R8);
 //   - on completion it does atomicMin on the packed (d^2, id) word, and appends (id, pos, d^2)
 //     to the near list if d^2 <= bsf * (1 + delta) (R9).
-// finalize_kernel: one warp per query. Near-list entries within (1 + delta) of the final BSF
-//   are recomputed in fp64, in one fixed order for every row. The answer is the
-//   lexicographic min of (d^2_fp64, id) (lowest id on ties; north_star). dist = fp32(sqrt(d^2)).
+// finalize_kernel: one CTA per query. Near-list entries within (1 + delta) of the final BSF are
+//   screened in fp64 and the possible answers compared exactly (integer d^2). The answer is the
+//   lexicographic min of (exact d^2, id) (lowest id on ties; north_star). dist = fp32(sqrt(d^2_fp64)).
 #include "isax_device.cuh"
 
 namespace isax {
@@ -29,8 +29,7 @@ __global__ void __launch_bounds__(RF_THREADS) refine_kernel(const float *__restr
                                                            const float *__restrict__ qy, uint32_t Q,
                                                            const uint32_t *__restrict__ cand,
                                                            const uint32_t *__restrict__ cand_cnt, uint32_t cap,
-                                                           unsigned long long *__restrict__ bsf,
-                                                           NearEntry *__restrict__ near, uint32_t *__restrict__ near_cnt,
+                                                           unsigned long long *__restrict__ bsf, NearList nl,
                                                            uint32_t *__restrict__ counters, float onepd) {
     __shared__ uint32_t pre[RF_MAXQ + 1];
     const uint32_t t = threadIdx.x, lane = t & 31;
@@ -101,8 +100,7 @@ __global__ void __launch_bounds__(RF_THREADS) refine_kernel(const float *__restr
         if (lane == 0 && d2 <= lim) {
             const uint32_t id = perm[pos];
             atomicMin(&bsf[q], pack_bsf(d2, id));
-            const uint32_t k = atomicAdd(&near_cnt[q], 1u);
-            if (k < NEAR_K) near[(uint64_t)q * NEAR_K + k] = NearEntry{id, pos, d2, 0};
+            near_append(nl, q, id, pos, d2);
         }
     }
     if (cur_q != 0xffffffffu && lane == 0) {
@@ -132,9 +130,7 @@ __global__ void __launch_bounds__(RF_THREADS) refine_q_kernel(const float *__res
                                                              const uint8_t *__restrict__ candq,
                                                              const float *__restrict__ qscale,
                                                              const uint32_t *__restrict__ cand_cnt, uint32_t cap,
-                                                             unsigned long long *__restrict__ bsf,
-                                                             NearEntry *__restrict__ near,
-                                                             uint32_t *__restrict__ near_cnt,
+                                                             unsigned long long *__restrict__ bsf, NearList nl,
                                                              uint32_t *__restrict__ counters, float onepd,
                                                              unsigned long long *__restrict__ refine_bytes) {
     __shared__ uint32_t pre[RF_MAXQ + 1];
@@ -246,8 +242,7 @@ __global__ void __launch_bounds__(RF_THREADS) refine_q_kernel(const float *__res
                 if (ql == 0 && acc <= cur) {
                     const uint32_t id = perm[pos];
                     atomicMin(&bsf[q], pack_bsf(acc, id));
-                    const uint32_t k = atomicAdd(&near_cnt[q], 1u);
-                    if (k < NEAR_K) near[(uint64_t)q * NEAR_K + k] = NearEntry{id, pos, acc, 0};
+                    near_append(nl, q, id, pos, acc);
                 }
             }
         }
@@ -361,6 +356,7 @@ void launch_refine(const isax_index *ix, uint32_t Q, float delta, cudaStream_t s
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const float onepd = 1.0f + delta;
+    const NearList nl{qs.near, qs.near_off, qs.near_cap, qs.near_cnt};
     // pass 1: cand2[q][0 .. cand_cnt2); then the filtered second band into cand[q][0 .. cnt_f)
     auto pass = [&](const uint32_t *list, const uint32_t *cnt) {
         if (ix->n <= 256) {
@@ -374,7 +370,7 @@ void launch_refine(const isax_index *ix, uint32_t Q, float delta, cudaStream_t s
 #define RQ_CASE(K)                                                                                                  \
     case K:                                                                                                         \
         refine_q_kernel<K><<<grid, RF_THREADS, 0, s>>>(ix->stored, ix->perm, ix->n, qs.qy, Q, list, nullptr, nullptr, \
-                                                       cnt, qs.cand_cap, qs.bsf, qs.near, qs.near_cnt, qs.counters, \
+                                                       cnt, qs.cand_cap, qs.bsf, nl, qs.counters,                   \
                                                        onepd, qs.refine_bytes);                                     \
         break;
                 RQ_CASE(1) RQ_CASE(2) RQ_CASE(3) RQ_CASE(4)
@@ -387,7 +383,7 @@ void launch_refine(const isax_index *ix, uint32_t Q, float delta, cudaStream_t s
 #define RF_CASE(K)                                                                                              \
     case K:                                                                                                     \
         refine_kernel<K><<<grid, RF_THREADS, 0, s>>>(ix->stored, ix->perm, ix->n, qs.qy, Q, list, cnt,            \
-                                                     qs.cand_cap, qs.bsf, qs.near, qs.near_cnt, qs.counters, onepd); \
+                                                     qs.cand_cap, qs.bsf, nl, qs.counters, onepd);                   \
         break;
         switch (ns) {
             RF_CASE(1) RF_CASE(2) RF_CASE(3) RF_CASE(4) RF_CASE(5) RF_CASE(6) RF_CASE(7) RF_CASE(8)
@@ -401,47 +397,250 @@ void launch_refine(const isax_index *ix, uint32_t Q, float delta, cudaStream_t s
 }
 
 // ------------------------------------------------------------------------------------ finalize
-__global__ void __launch_bounds__(32) finalize_kernel(const float *__restrict__ stored, uint32_t n,
-                                                      const float *__restrict__ qy,
-                                                      const unsigned long long *__restrict__ bsf,
-                                                      const NearEntry *__restrict__ near,
-                                                      const uint32_t *__restrict__ near_cnt, float onepd,
-                                                      int64_t *__restrict__ out_id, float *__restrict__ out_dist) {
-    const uint32_t q = blockIdx.x, lane = threadIdx.x;
-    const unsigned long long fin = bsf[q];
-    const float lim = bsf_d2(fin) * onepd;
-    const uint32_t cnt = min(near_cnt[q], (uint32_t)NEAR_K);
-    double best = __longlong_as_double(0x7ff0000000000000ll);  // +inf
-    uint32_t best_id = (uint32_t)(fin & 0xffffffffu);
-    bool have = false;
-    for (uint32_t k = 0; k < cnt; k++) {
-        const NearEntry e = near[(uint64_t)q * NEAR_K + k];
-        if (!(e.d2 <= lim)) continue;
-        const float *row = stored + (uint64_t)e.pos * n;
-        const float *qr = qy + (uint64_t)q * n;
-        double acc = 0.0;
-        for (uint32_t i = lane; i < n; i += 32) {
-            const double d = __dsub_rn((double)qr[i], (double)row[i]);
-            acc = __dadd_rn(acc, __dmul_rn(d, d));
+// R9: the answer is the lexicographic minimum of (exact d^2, id) over the rows whose fp32 d^2 is
+// within (1 + delta) of the final BSF. Every such row is in the query's near list (its partial
+// sums never pass the threshold, so it completes, and it is appended when it completes).
+//
+// One CTA per scanned query. Pass 1 computes d^2 in fp64 for each listed row (differences and
+// squares rounded once each, sum in a fixed lane order) and its minimum m64. Every term is >= 0,
+// so the fp64 sum is within gamma = (n + 3) 2^-53 (< 1.2e-13 at n <= 1024) of the exact d^2,
+// relatively; a row whose exact d^2 is the minimum has fp64 d^2 <= m64 (1 + gamma) / (1 - gamma),
+// so the rows with fp64 d^2 <= m64 (1 + 4e-13) are the only possible answers ("eligible").
+// Pass 2 finds the lowest and highest id among the eligible rows; if they are equal (the usual
+// case: one row, possibly listed twice), that row is the answer. Otherwise pass 3 evaluates d^2
+// of every eligible row exactly, as an integer (below), and takes the lexicographic minimum.
+// The fp64 values of the first 512 entries are kept in shared memory between the passes.
+//
+// Exact d^2. A finite fp32 value v is an integer multiple of 2^-149: v = +-M 2^(sh - 149) with M
+// the 24-bit significand (23 bits for subnormals, sh = 0) and sh = biased exponent - 1. So
+// A = v 2^149 = +-M << sh is an integer, d = A - B is exact, and sum d^2 = 2^298 d^2(v, w) is an
+// exact integer too. The stored rows and the query are z-normalised (sum y^2 = n <= 1024, so
+// |y| <= 32 < 2^18): A < 2^(24 + 167) fits in six 32-bit limbs, d^2 in twelve. Each lane squares
+// its elements' differences into carry-save accumulators (u64 per 32-bit limb position: at most
+// 12 additions of < 2^32 per term, 32 terms per lane, 32 lanes: < 2^46, no overflow), the warp
+// adds them, and one lane propagates the carries. Keys compare from the top limb down.
+constexpr int FZ_THREADS = 256;
+constexpr int XL = 6;        // 32-bit limbs of |A - B|
+constexpr int XK = 2 * XL;   // limbs of the squared sum
+
+__device__ __forceinline__ void fp32_fixed(float v, uint32_t &neg, uint32_t (&a)[XL]) {
+    const uint32_t u = __float_as_uint(v);
+    const uint32_t e = (u >> 23) & 0xFFu, mant = u & 0x7FFFFFu;
+    const uint32_t M = e ? (mant | 0x800000u) : mant;
+    const uint32_t sh = e ? e - 1u : 0u;
+    const unsigned long long w = (unsigned long long)M << (sh & 31u);
+    const uint32_t j = sh >> 5;
+    neg = u >> 31;
+#pragma unroll
+    for (int i = 0; i < XL; i++) a[i] = (uint32_t)i == j ? (uint32_t)w : ((uint32_t)i == j + 1 ? (uint32_t)(w >> 32) : 0u);
+}
+
+// acc += (a - b)^2, exactly (carry-save, base 2^32)
+__device__ __forceinline__ void exact_term(float av, float bv, unsigned long long (&acc)[XK + 1]) {
+    uint32_t na, nb, a[XL], b[XL], x[XL];
+    fp32_fixed(av, na, a);
+    fp32_fixed(bv, nb, b);
+    if (na != nb) {  // |a - b| = |a| + |b|
+        unsigned long long c = 0;
+#pragma unroll
+        for (int i = 0; i < XL; i++) {
+            c += (unsigned long long)a[i] + b[i];
+            x[i] = (uint32_t)c;
+            c >>= 32;
         }
-        acc = warp_sum_d(acc);
-        if (!have || acc < best || (acc == best && e.id < best_id)) {
-            best = acc;
-            best_id = e.id;
-            have = true;
+    } else {  // |a - b| = | |a| - |b| |
+        long long br = 0;
+#pragma unroll
+        for (int i = 0; i < XL; i++) {
+            const long long t = (long long)a[i] - (long long)b[i] + br;
+            x[i] = (uint32_t)t;
+            br = t >> 32;  // 0 or -1
+        }
+        if (br) {  // negative: two's complement
+            unsigned long long c = 1;
+#pragma unroll
+            for (int i = 0; i < XL; i++) {
+                c += (unsigned long long)(~x[i]);
+                x[i] = (uint32_t)c;
+                c >>= 32;
+            }
         }
     }
-    if (lane == 0) {
-        out_id[q] = (int64_t)best_id;
-        out_dist[q] = have ? __double2float_rn(sqrt(best)) : sqrtf(bsf_d2(fin));
+#pragma unroll
+    for (int i = 0; i < XL; i++)
+#pragma unroll
+        for (int j = 0; j < XL; j++) {
+            const unsigned long long p = (unsigned long long)x[i] * x[j];
+            acc[i + j] += (uint32_t)p;
+            acc[i + j + 1] += p >> 32;
+        }
+}
+
+// exact key of one listed row (its XK limbs, most significant last), computed by one warp
+__device__ __forceinline__ void exact_key(const float *__restrict__ row, const float *__restrict__ qr, uint32_t n,
+                                          uint32_t lane, uint32_t (&key)[XK]) {
+    unsigned long long acc[XK + 1];
+#pragma unroll
+    for (int i = 0; i <= XK; i++) acc[i] = 0;
+    for (uint32_t i = lane; i < n; i += 32) exact_term(qr[i], row[i], acc);
+#pragma unroll
+    for (int i = 0; i <= XK; i++)
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) acc[i] += __shfl_xor_sync(0xffffffffu, acc[i], o);
+    unsigned long long c = 0;
+#pragma unroll
+    for (int i = 0; i < XK; i++) {
+        c += acc[i];
+        key[i] = (uint32_t)c;
+        c >>= 32;
     }
 }
 
-void launch_finalize(const isax_index *ix, uint32_t Q, float delta, int64_t *out_id, float *out_dist,
-                     cudaStream_t s) {
+__device__ __forceinline__ bool key_id_less(const uint32_t (&a)[XK], uint32_t ida, const uint32_t (&b)[XK], uint32_t idb) {
+#pragma unroll
+    for (int i = XK - 1; i >= 0; i--)
+        if (a[i] != b[i]) return a[i] < b[i];
+    return ida < idb;
+}
+
+__device__ __forceinline__ double row_d64(const float *__restrict__ row, const float *__restrict__ qr, uint32_t n,
+                                          uint32_t lane) {
+    double acc = 0.0;
+    for (uint32_t i = lane; i < n; i += 32) {
+        const double d = __dsub_rn((double)qr[i], (double)row[i]);
+        acc = __dadd_rn(acc, __dmul_rn(d, d));
+    }
+    return warp_sum_d(acc);
+}
+
+__global__ void __launch_bounds__(FZ_THREADS) finalize_kernel(const float *__restrict__ stored, uint32_t n,
+                                                              const float *__restrict__ qy, const uint32_t *__restrict__ qmap,
+                                                              const unsigned long long *__restrict__ bsf, NearList nl,
+                                                              float onepd, int64_t *__restrict__ out_id,
+                                                              float *__restrict__ out_dist) {
+    constexpr uint32_t NWF = FZ_THREADS / 32;
+    constexpr uint32_t CACHE = 512;  // fp64 d^2 of the first entries, kept between the passes
+    __shared__ double s_dv[CACHE];
+    __shared__ double s_m[NWF];
+    __shared__ uint32_t s_lo[NWF], s_hi[NWF], s_pos[NWF];
+    __shared__ uint32_t s_key[NWF][XK];
+    __shared__ uint32_t s_id[NWF];
+    __shared__ double s_d64[NWF];
+    const uint32_t q = qmap[blockIdx.x];
+    const uint32_t t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const unsigned long long fin = bsf[q];
+    const float lim = bsf_d2(fin) * onepd;
+    const uint32_t cnt = min(nl.cnt[q], nl.cap[q]);
+    const NearEntry *list = nl.base + nl.off[q];
+    const float *qr = qy + (uint64_t)q * n;
+    const double INF64 = __longlong_as_double(0x7ff0000000000000ll);
+    // fp64 d^2 of entry k (+inf if it is not within (1 + delta) of the final BSF)
+    auto d64_of = [&](uint32_t k, const NearEntry &e) -> double {
+        if (k < CACHE) return s_dv[k];
+        return e.d2 <= lim ? row_d64(stored + (uint64_t)e.pos * n, qr, n, lane) : INF64;
+    };
+    // pass 1: fp64 d^2 of every listed row and their minimum
+    double m = INF64;
+    for (uint32_t k = warp; k < cnt; k += NWF) {
+        const NearEntry e = list[k];
+        const double d = e.d2 <= lim ? row_d64(stored + (uint64_t)e.pos * n, qr, n, lane) : INF64;
+        if (k < CACHE && lane == 0) s_dv[k] = d;
+        m = fmin(m, d);
+    }
+    if (lane == 0) s_m[warp] = m;
+    __syncthreads();
+    m = INF64;
+    for (uint32_t w = 0; w < NWF; w++) m = fmin(m, s_m[w]);
+    if (m == INF64) {  // nothing listed (unreachable: the BSF's own row is listed); the BSF word's id
+        if (t == 0) {
+            out_id[q] = (int64_t)(uint32_t)(fin & 0xffffffffu);
+            out_dist[q] = sqrtf(bsf_d2(fin));
+        }
+        return;
+    }
+    const double elig = m * (1.0 + 4e-13);
+    // pass 2: the lowest and highest id among the eligible rows
+    uint32_t lo_id = 0xffffffffu, hi_id = 0, lo_pos = 0;
+    for (uint32_t k = warp; k < cnt; k += NWF) {
+        const NearEntry e = list[k];
+        if (d64_of(k, e) <= elig) {
+            if (e.id < lo_id) {
+                lo_id = e.id;
+                lo_pos = e.pos;
+            }
+            hi_id = max(hi_id, e.id);
+        }
+    }
+    if (lane == 0) {
+        s_lo[warp] = lo_id;
+        s_hi[warp] = hi_id;
+        s_pos[warp] = lo_pos;
+    }
+    __syncthreads();
+    for (uint32_t w = 0; w < NWF; w++) {
+        if (s_lo[w] < lo_id) {
+            lo_id = s_lo[w];
+            lo_pos = s_pos[w];
+        }
+        hi_id = max(hi_id, s_hi[w]);
+    }
+    if (lo_id == hi_id) {  // one eligible row (possibly listed more than once): the answer
+        const double d = row_d64(stored + (uint64_t)lo_pos * n, qr, n, lane);
+        if (t == 0) {
+            out_id[q] = (int64_t)lo_id;
+            out_dist[q] = __double2float_rn(sqrt(d));
+        }
+        return;
+    }
+    // pass 3: exact keys of the eligible rows, lexicographic minimum of (exact d^2, id)
+    uint32_t best[XK], cur[XK];
+    uint32_t best_id = 0xffffffffu;
+    double best_d = INF64;
+#pragma unroll
+    for (int i = 0; i < XK; i++) best[i] = 0xffffffffu;
+    for (uint32_t k = warp; k < cnt; k += NWF) {
+        const NearEntry e = list[k];
+        const double d = d64_of(k, e);
+        if (!(d <= elig)) continue;
+        exact_key(stored + (uint64_t)e.pos * n, qr, n, lane, cur);
+        if (key_id_less(cur, e.id, best, best_id)) {
+#pragma unroll
+            for (int i = 0; i < XK; i++) best[i] = cur[i];
+            best_id = e.id;
+            best_d = d;
+        }
+    }
+    if (lane == 0) {
+#pragma unroll
+        for (int i = 0; i < XK; i++) s_key[warp][i] = best[i];
+        s_id[warp] = best_id;
+        s_d64[warp] = best_d;
+    }
+    __syncthreads();
+    if (t == 0) {
+        uint32_t bw = 0;
+        for (uint32_t w = 1; w < NWF; w++) {
+            bool less = false, decided = false;
+            for (int i = XK - 1; i >= 0 && !decided; i--)
+                if (s_key[w][i] != s_key[bw][i]) {
+                    less = s_key[w][i] < s_key[bw][i];
+                    decided = true;
+                }
+            if (!decided) less = s_id[w] < s_id[bw];
+            if (less) bw = w;
+        }
+        out_id[q] = (int64_t)s_id[bw];
+        out_dist[q] = __double2float_rn(sqrt(s_d64[bw]));
+    }
+}
+
+void launch_finalize(const isax_index *ix, uint32_t nq, const uint32_t *qmap, float delta, int64_t *out_id,
+                     float *out_dist, cudaStream_t s) {
     const QueryScratch &qs = ix->qs;
-    finalize_kernel<<<Q, 32, 0, s>>>(ix->stored, ix->n, qs.qy, qs.bsf, qs.near, qs.near_cnt, 1.0f + delta, out_id,
-                                     out_dist);
+    if (!nq) return;
+    finalize_kernel<<<nq, FZ_THREADS, 0, s>>>(ix->stored, ix->n, qs.qy, qmap, qs.bsf,
+                                              NearList{qs.near, qs.near_off, qs.near_cap, qs.near_cnt}, 1.0f + delta,
+                                              out_id, out_dist);
 }
 
 }  // namespace isax

@@ -46,6 +46,7 @@ isax_nn1 = _sig("isax_nn1", [_P, _P, _U32, _P, _P])
 isax_nn1_async = _sig("isax_nn1_async", [_P, _P, _U32, _P, _P, _P])
 isax_export = _sig("isax_export", [_P, _U64, _U64, _P, _P, _P])
 isax_query_debug = _sig("isax_query_debug", [_P, _P, _U32, _P, _P, _P, _U64, _U64, _P, _P])
+isax_debug_candidates = _sig("isax_debug_candidates", [_P, _U32, _P, _U64, ctypes.POINTER(_U64)])
 isax_stats = _sig("isax_stats", [_P, ctypes.c_char_p, ctypes.c_size_t])
 isax_info = _sig("isax_info", [_P, ctypes.POINTER(_U64), ctypes.POINTER(_U32), ctypes.POINTER(_U32),
                                ctypes.POINTER(_U32), ctypes.POINTER(_U64)])
@@ -104,7 +105,13 @@ class Index:
         if isinstance(series, np.ndarray):
             series = np.ascontiguousarray(series, dtype=np.float32)
         else:
+            import torch
+
+            if series.dtype != torch.float32:
+                raise TypeError(f"series must be float32, got {series.dtype}")
             series = series.contiguous()
+        if series.ndim != 2:
+            raise ValueError(f"series must be [N, n], got shape {tuple(series.shape)}")
         N, n = series.shape
         h = _P()
         o = _opts(**opts)
@@ -196,6 +203,14 @@ class Index:
         if count:
             r["lb2"] = lb
         return r
+
+    def candidates(self, q: int):
+        """Sorted positions of query q's candidate list in the last nn1 call (isax_debug_candidates)."""
+        cnt = _U64()
+        _check(isax_debug_candidates(self._h, q, None, 0, ctypes.byref(cnt)), "isax_debug_candidates")
+        out = np.empty(cnt.value, np.uint32)
+        _check(isax_debug_candidates(self._h, q, _ptr(out), cnt.value, ctypes.byref(cnt)), "isax_debug_candidates")
+        return out
 
     def stats(self) -> dict:
         need = isax_stats(self._h, None, 0)

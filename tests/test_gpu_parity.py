@@ -103,7 +103,9 @@ def test_nn1_matches_oracle(N, n, kind, q_noisy):
     for j in range(len(qh)):
         w0, w1 = st["window"][2 * j], st["window"][2 * j + 1]
         assert st["candidates"][j] + (w1 - w0) <= N
-        assert st["refined"][j] + st["abandoned"][j] >= (w1 - w0)
+        # accounting: every candidate is refined to the end, abandoned, or skipped by the second
+        # band's bound test (R14); window rows are counted apart
+        assert st["refined"][j] + st["abandoned"][j] + st["skipped"][j] == st["candidates"][j]
         # window rows refined: the main window plus the kept probe windows (each at most probe_L
         # rows, none inside the main window, no repeats)
         lp = min(st["probe_L"], N)
@@ -112,12 +114,12 @@ def test_nn1_matches_oracle(N, n, kind, q_noisy):
 
 
 @pytest.mark.parametrize("N,n,kind", [(200_000, 256, "walk"), (50_001, 128, "walk"), (30_000, 256, "sines")])
-def test_candidate_set_is_exactly_the_lb_filter(N, n, kind):
-    """The leaf-pruned scan keeps exactly {pos outside the window : LB^2(pos) <= bsf0^2 (1 + delta)}.
-
-    It is compared with the per-position LB^2 from isax_query_debug (the same fp32 order) and
-    with the flat scan (ISAX_FLAG_FLAT_SCAN). The fp64 oracle LB brackets the count.
-    """
+def test_candidate_set_equals_the_oracle_lb_filter(N, n, kind):
+    """The scan's candidate set, element by element, against the oracle's fp64 LB filter (C6,
+    P:273-276): {pos outside the window : LB^2_fp64(pos) <= T}, with T = bsf0^2 (1 + delta) the
+    threshold of the GPU's window BSF (R8). The only tolerance is the fp32 summation band around
+    T (|LB^2 / T - 1| <= 1e-5): a position there may go either way. The leaf-pruned scan (R11)
+    and the flat ParIS scan keep the same set."""
     wl = small_workload(N, n, kind, Q=12, q_noisy=4 if kind == "walk" else 12, sigma=0.1)
     x = datagen.series(wl, 0, N)
     q, _ = datagen.queries(wl)
@@ -125,27 +127,35 @@ def test_candidate_set_is_exactly_the_lb_filter(N, n, kind):
     with _build(x) as ix, _build(x, flags=1) as flat:
         ids, dist = ix.nn1(q)
         st = ix.stats()
+        cands = [np.sort(ix.candidates(i)) for i in range(len(qh))]
         ids_f, dist_f = flat.nn1(q)
         st_f = flat.stats()
-        dbg = ix.query_debug(qh, 0, N)
+        cands_f = [np.sort(flat.candidates(i)) for i in range(len(qh))]
         ex = ix.export(0, N, sax=True, perm=True)
     np.testing.assert_array_equal(ids.cpu().numpy(), ids_f.cpu().numpy())
     np.testing.assert_array_equal(dist.cpu().numpy(), dist_f.cpu().numpy())
-    assert st["candidates"] == st_f["candidates"]
     onepd = np.float32(1 + 2.0**-12)
     _, _, _, qm, _ = clib.summarise(qh)
     words_sorted = ex["sax"][ex["perm"]]
+    checked = 0
     for i in range(len(qh)):
         assert st["rounds"][i] == 1
-        T = np.float32(st["bsf0_d2"][i]) * onepd
+        np.testing.assert_array_equal(cands[i], cands_f[i])
+        assert len(np.unique(cands[i])) == len(cands[i])
+        T = float(np.float32(st["bsf0_d2"][i]) * onepd)
         w0, w1 = st["window"][2 * i], st["window"][2 * i + 1]
-        keep = dbg["lb2"][i] <= T
-        keep[w0:w1] = False
-        assert st["candidates"][i] == int(keep.sum())
         lb_or = ref.lb2(qm[i], words_sorted, n)
         lb_or[w0:w1] = np.inf
-        assert (lb_or <= T * (1 - 1e-5)).sum() <= st["candidates"][i] <= (lb_or <= T * (1 + 1e-5)).sum()
+        got = np.zeros(N, bool)
+        got[cands[i]] = True
+        sure = lb_or <= T * (1 - 1e-5)
+        maybe = lb_or <= T * (1 + 1e-5)
+        assert got[sure].all(), f"query {i}: {int((sure & ~got).sum())} oracle candidates missing"
+        assert not (got & ~maybe).any(), f"query {i}: {int((got & ~maybe).sum())} extra candidates"
+        assert st["candidates"][i] == len(cands[i])
+        checked += int(sure.sum())
         assert st["leaves_alive"][i] <= (N + st["leaf_size"] - 1) // st["leaf_size"]
+    assert checked > 0
     assert st_f["leaves_alive"] == [0] * len(qh)
 
 
@@ -293,3 +303,134 @@ def test_many_queries_span_batches():
         st = ix.stats()
     assert_nn_parity(ids.cpu().numpy(), dist.cpu().numpy(), ids_or, dist_or)
     assert len(st["rounds"]) == Q and min(st["window_rows"]) >= min(3072, N)
+
+
+def test_config1_at_its_own_seeds():
+    """BASELINE.json configs[0] exactly: 100,000 walks x 256 (data seed 1), 10 walk queries (seed 2)."""
+    wl = datagen.WORKLOADS[1]
+    x = datagen.series(wl, 0, wl.N)
+    q, _ = datagen.queries(wl)
+    ids_or, dist_or, _ = oracle_nn1(x.cpu().numpy(), q.cpu().numpy())
+    with _build(x) as ix:
+        ids, dist = ix.nn1(q)
+    assert_nn_parity(ids.cpu().numpy(), dist.cpu().numpy(), ids_or, dist_or)
+
+
+@pytest.mark.parametrize("opts", [dict(), dict(window_L=1, probe_bits=0xFFFFFFFF), dict(cand_cap=64)])
+def test_many_exact_ties_terminate(opts):
+    """More near ties than a near list holds (ties -> lowest id; R9): 300 copies of
+    series 17 and 300 constant series (all z-normalise to the zero row). The lists overflow, grow
+    and the queries rescan once; the answers are the lowest ids."""
+    N, n = 6_000, 256
+    wl = small_workload(N, n, Q=6)
+    x = datagen.series(wl, 0, N).clone()
+    x[1000:1300] = x[17]
+    x[3000:3300] = 1.5
+    q, _ = datagen.queries(wl)
+    q = q.clone()
+    q[0] = x[17] * 2.0 + 1.0  # the same shape after z-norm
+    q[1] = -4.0  # constant query: d = 0 to every constant row
+    q[2] = x[1150]
+    xh, qh = x.cpu().numpy(), q.cpu().numpy()
+    ids_or, dist_or, _ = oracle_nn1(xh, qh, K=1024)
+    with _build(x, **opts) as ix:
+        ids, dist = ix.nn1(q)
+        st = ix.stats()
+    ids, dist = ids.cpu().numpy(), dist.cpu().numpy()
+    assert_nn_parity(ids, dist, ids_or, dist_or)
+    assert ids[0] == 17 and ids[1] == 3000 and ids[2] == 17
+    assert max(st["near"][:3]) > 256  # the near lists did overflow their first capacity
+
+
+@pytest.mark.parametrize("exact_copy", [True, False])
+def test_tiny_cand_cap_with_equal_bounds(exact_copy):
+    """cand_cap = 7 and 40 identical rows sharing one LB^2 (0 for an exact-copy query): the LB
+    band cannot be split, so the rounds split the sorted positions (R10). Answers exact."""
+    N, n = 20_000, 128
+    wl = small_workload(N, n, Q=4)
+    x = datagen.series(wl, 0, N).clone()
+    x[5000:5040] = x[333]
+    q, _ = datagen.queries(wl)
+    q = q.clone()
+    q[0] = x[333] if exact_copy else x[333] + 0.05 * torch.randn(n, device="cuda", generator=torch.Generator("cuda").manual_seed(5))
+    ids_or, dist_or, _ = oracle_nn1(x.cpu().numpy(), q.cpu().numpy(), K=64)
+    with _build(x, cand_cap=7, window_L=1, probe_bits=0xFFFFFFFF) as ix:
+        ids, dist = ix.nn1(q)
+        st = ix.stats()
+    assert_nn_parity(ids.cpu().numpy(), dist.cpu().numpy(), ids_or, dist_or)
+    if exact_copy:
+        assert ids[0].item() == 333
+    assert max(st["rounds"]) >= 3
+
+
+def _gpu_fp64_d2(q, y):
+    """finalize_kernel's fp64 d^2: lane l sums elements l, l + 32, ... left to right, then the
+    xor butterfly (16, 8, 4, 2, 1) over the lanes."""
+    q64, y64 = q.astype(np.float64), y.astype(np.float64)
+    v = []
+    for lane in range(32):
+        acc = 0.0
+        for i in range(lane, len(q), 32):
+            d = q64[i] - y64[i]
+            acc = acc + d * d
+        v.append(acc)
+    for o in (16, 8, 4, 2, 1):
+        v = [v[l] + v[l ^ o] for l in range(32)]
+    return v[0]
+
+
+def test_finalize_is_exact_when_fp64_ties():
+    """Two rows whose fp64 d^2 (the kernel's summation order) say the lower id is at least as
+    near, while the exact d^2 says the higher id is nearer: the answer must be the higher id
+    (lexicographic (exact d^2, id), north_star / SPEC.md:285). Built from integer raw rows (so
+    z-norm of a permutation is the permutation of the z-norm, bit for bit: every fp64 sum is
+    exact) and a query with two 1-ulp-apart tiny elements; searched over seeds on the host with
+    the oracle's z-norm."""
+    from fractions import Fraction
+
+    n = 256
+    found = None
+    for seed in range(400):
+        rng = np.random.default_rng(seed)
+        xa = np.cumsum(rng.integers(-3, 4, n)).astype(np.float32)
+        i, j = (int(v) for v in rng.choice(n, 2, replace=False))
+        if xa[i] == xa[j]:
+            continue
+        xb = xa.copy()
+        xb[i], xb[j] = xa[j], xa[i]  # d^2(q, b) - d^2(q, a) = 2 (q_i - q_j)(y_i - y_j), exactly
+        ya, _, _ = ref.znorm(xa[None])
+        yb, _, _ = ref.znorm(xb[None])
+        # a query near row a whose normalised elements i, j are tiny and 1 ulp apart: the other
+        # elements are centred (mean ~1e-9), then q_i = fp32(mean), q_j the next fp32 up
+        qr = (ya[0] + rng.standard_normal(n).astype(np.float32) * np.float32(0.01)).astype(np.float32)
+        qr[i] = qr[j] = 0
+        rest = np.ones(n, bool)
+        rest[[i, j]] = False
+        for _ in range(4):
+            qr[rest] = (qr[rest] - np.float32(qr.astype(np.float64).sum() / (n - 2))).astype(np.float32)
+        qr[i] = np.float32(qr.astype(np.float64).sum() / n)
+        qr[j] = np.nextafter(qr[i], np.float32(1))
+        qy, _, _ = ref.znorm(qr[None])
+        ea, eb = ref.ed2_exact(qy[0], ya[0]), ref.ed2_exact(qy[0], yb[0])
+        fa, fb = _gpu_fp64_d2(qy[0], ya[0]), _gpu_fp64_d2(qy[0], yb[0])
+        if ea > eb and fa <= fb:  # the fp64 rule would pick row a (lower id); the exact one b
+            found = (xa, xb, qr, ea, eb)
+            break
+        if eb > ea and fb <= fa:
+            found = (xb, xa, qr, eb, ea)
+            break
+    assert found is not None, "no fp64-tie construction found"
+    xa, xb, qr, ea, eb = found
+    N = 4_000
+    wl = small_workload(N, n, Q=2)
+    x = datagen.series(wl, 0, N).clone()
+    x[100] = torch.from_numpy(xa).cuda()  # the lower id: exactly farther
+    x[2500] = torch.from_numpy(xb).cuda()
+    q, _ = datagen.queries(wl)
+    q = q.clone()
+    q[0] = torch.from_numpy(qr).cuda()
+    ids_or, dist_or, d2_or = oracle_nn1(x.cpu().numpy(), q.cpu().numpy())
+    assert ids_or[0] == 2500 and d2_or[0] == eb and Fraction(ea) > Fraction(eb)
+    with _build(x) as ix:
+        ids, dist = ix.nn1(q)
+    assert_nn_parity(ids.cpu().numpy(), dist.cpu().numpy(), ids_or, dist_or)
