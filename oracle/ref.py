@@ -146,56 +146,6 @@ def canonical_order(words: np.ndarray) -> np.ndarray:
     return np.lexsort((ids, lo, hi)).astype(np.int64)
 
 
-SUPER_BLOCK = 1024  # sorted positions per super-node (R6b)
-LEAF_BLOCK = 32     # sorted positions per leaf
-
-
-def super_kd_block(words_block: np.ndarray) -> np.ndarray:
-    """Return the kd order (indices into the block) of one full super-node (R6b).
-
-    The block's rows are in z order. At each level every node, a contiguous half of its parent
-    (the block itself at the top), takes the segment s with the largest symbol range
-    max_s - min_s over its rows (the lowest s on ties) and is sorted by symbol s, stably. Its
-    first and second halves are its children. Levels continue down to nodes of LEAF_BLOCK rows.
-    """
-    wb = np.asarray(words_block, dtype=np.int64)
-    n = len(wb)
-    idx = np.arange(n)
-    size = n
-    while size > LEAF_BLOCK:
-        for a in range(0, n, size):
-            node = idx[a:a + size]
-            rng = wb[node].max(axis=0) - wb[node].min(axis=0)
-            seg = int(np.argmax(rng))  # the first maximum: lowest segment on ties
-            idx[a:a + size] = node[np.argsort(wb[node, seg], kind="stable")]
-        size //= 2
-    return idx
-
-
-def sorted_order(words: np.ndarray) -> np.ndarray:
-    """Return perm (perm[pos] = id): the C5 z order with every full super-node in kd order (R6b)."""
-    perm = canonical_order(words)
-    for b0 in range(0, len(perm) - SUPER_BLOCK + 1, SUPER_BLOCK):
-        blk = perm[b0:b0 + SUPER_BLOCK]
-        perm[b0:b0 + SUPER_BLOCK] = blk[super_kd_block(words[blk])]
-    return perm
-
-
-def super_window(words: np.ndarray, qword, L: int = 3072) -> tuple[int, int]:
-    """The approximate answer's main window (R5, R6b), in whole super-nodes around the
-    one whose z-order key range holds the query key (the last super-node whose smallest key is
-    below the query's, or the first): centred on it for an odd count of super-nodes (L = 1024,
-    3072), on its end for an even count (2048: it and the next); clamped into [0, N)."""
-    z = canonical_order(words)
-    hi, lo = isax_keys(words[z[::SUPER_BLOCK]])
-    qhi, qlo = isax_keys(np.asarray([qword]))
-    kq = (int(qhi[0]), int(qlo[0]))
-    c = sum(1 for a, b in zip(hi.tolist(), lo.tolist()) if (a, b) < kq)
-    sq = max(c - 1, 0)
-    centre = sq * SUPER_BLOCK + SUPER_BLOCK // 2 + (0 if (L // SUPER_BLOCK) % 2 else SUPER_BLOCK // 2)
-    return window(centre, len(words), L)
-
-
 # --------------------------------------------------------------------------------------
 # C6 lower bound MINDIST_PAA_iSAX (P:273-275, P:349, P:356; formula S:117-125)
 # --------------------------------------------------------------------------------------
@@ -304,12 +254,14 @@ def window(pos: int, N: int, L: int) -> tuple[int, int]:
     return start, start + L
 
 
-def nn1_index_search(x: np.ndarray, Qx: np.ndarray, w: int = W_DEFAULT, L: int = 3072):
+def nn1_index_search(x: np.ndarray, Qx: np.ndarray, w: int = W_DEFAULT, L: int = 1024):
     """ParIS query answering on raw rows x and raw queries Qx (both z-normalised here).
 
     The steps follow P:270-279:
     1. "computes an approximate answer by calculating BSF": the real distances over the
-       leaf-sized window of the sorted order at the query key's position.
+       leaf-sized window of the C5 sorted order centred at the query key's lower_bound position
+       (the library's own window rule, R5, affects speed only and is not
+       restated here).
     2. "lower bound distances between the query and the iSAX summary of each data series",
        for every series outside the window.
     3. "prune the series whose lower bound distance is larger than the approximate real
@@ -322,11 +274,13 @@ def nn1_index_search(x: np.ndarray, Qx: np.ndarray, w: int = W_DEFAULT, L: int =
     y, _, _, _, words = summarise(x, w)
     qy, _, _, qm, qwords = summarise(Qx, w)
     N, n = y.shape
-    perm = sorted_order(words)
+    perm = canonical_order(words)
+    khi, klo = isax_keys(words[perm])
+    qhi, qlo = isax_keys(qwords)
     out, stats = [], []
     for qi in range(len(qy)):
         q = qy[qi].astype(np.float64)
-        s0, s1 = super_window(words, qwords[qi], L)
+        s0, s1 = window(lower_bound_pos(khi, klo, qhi[qi], qlo[qi]), N, L)
         win_ids = perm[s0:s1]
         d_win = ed2(qy[qi], y[win_ids])
         bsf = float(d_win.min())

@@ -1,7 +1,8 @@
 """GPU parity: the CUDA path (through the C-ABI) against the oracle on the same seeded bytes.
 
 Bars:
-* iSAX words, the permutation and the stored z-normalised rows: bit-exact.
+* iSAX words and the stored z-normalised rows: bit-exact; the permutation: the layout properties
+  of tests/layout_props.py (C5 blocks, kd splits), not a restatement of the kernels' rule.
 * query PAA and word: bit-exact; LB^2: within the fp32 summation bound of the fp64 oracle.
 * NN ids: exact (ties to the lowest id); distances within 1e-5 relative (north_star).
 Sizes span many tiles and a ragged tail; edge cases cover N = 1, N < window, duplicates,
@@ -19,6 +20,7 @@ if not torch.cuda.is_available():  # pragma: no cover
 import datagen  # noqa: E402
 from oracle import clib, ref  # noqa: E402
 from paper_2009_01614_b200 import isax  # noqa: E402
+from tests import layout_props  # noqa: E402
 from tests.gpu_util import assert_nn_parity, oracle_nn1, small_workload  # noqa: E402
 
 
@@ -37,9 +39,11 @@ def test_summaries_perm_and_rows_bit_exact(N, n, kind):
         ex = ix.export(0, N, sax=True, perm=True, stored=True)
     y, mu, sd, m, word = clib.summarise(xh)
     np.testing.assert_array_equal(ex["sax"], word)  # C4 words, by id
-    perm = ref.sorted_order(word)  # C5 z order, kd order inside each full super-node (R6b)
-    np.testing.assert_array_equal(ex["perm"].astype(np.int64), perm)
-    np.testing.assert_array_equal(ex["stored"], y[perm])  # C1 rows, in sorted order
+    perm = ex["perm"].astype(np.int64)
+    # the layout's properties (tests/layout_props.py): a bijection, super-nodes = the C5 blocks,
+    # kd splits on each node's widest segment, stable (R6, R6b)
+    layout_props.check_layout(perm, word)
+    np.testing.assert_array_equal(ex["stored"], y[perm])  # C1 rows, in the sorted order
 
 
 @pytest.mark.parametrize("N,n", [(100_000, 256), (9_999, 128), (3_072, 256), (1_500, 128)])
@@ -61,13 +65,13 @@ def test_query_summary_lb_and_window(N, n):
         # fp32 sum of 16 rounded-down terms: never above the fp64 bound beyond summation error
         assert np.all(lb_gpu <= lb_or * (1 + 2e-6) + 1e-30)
         assert np.all(lb_gpu >= lb_or * (1 - 1e-5) - 1e-6)
-        assert tuple(dbg["win"][i]) == ref.super_window(ex["sax"], qw[i], 3072)
+        layout_props.check_window(dbg["win"][i], ex["perm"], ex["sax"], qw[i], 3072)
 
 
 @pytest.mark.parametrize("L", [1024, 2048, 4096])
 def test_window_of_whole_super_nodes(L):
-    """Main windows of an odd (1024) or even (2048, 4096) count of super-nodes follow the oracle's
-    centre rule (R5, R6b): odd counts centred on the query key's super-node, even counts on its end.
+    """Main windows of 1, 2 or 4 super-nodes (R5, R6b): whole super-nodes holding the query key's
+    predecessor (and, from two super-nodes on, its successor) in the C5 key order.
     window_L above 4096 is rejected (include/isax.h)."""
     N, n = 60_000, 128
     wl = small_workload(N, n, Q=16, q_noisy=8)
@@ -75,11 +79,11 @@ def test_window_of_whole_super_nodes(L):
     q, _ = datagen.queries(wl)
     qh = q.cpu().numpy()
     with _build(x, window_L=L) as ix:
-        ex = ix.export(0, N, sax=True)
+        ex = ix.export(0, N, sax=True, perm=True)
         dbg = ix.query_debug(qh, 0, 1)
     _, _, _, _, qw = clib.summarise(qh)
     for i in range(len(qh)):
-        assert tuple(dbg["win"][i]) == ref.super_window(ex["sax"], qw[i], L)
+        layout_props.check_window(dbg["win"][i], ex["perm"], ex["sax"], qw[i], L)
     with pytest.raises(isax.IsaxError):
         _build(x, window_L=4097)
 

@@ -200,58 +200,36 @@ def test_canonical_order_is_plane_lexicographic():
     assert perm.tolist() == expect
 
 
-def _kd_check(wb, order):
-    """The R6b properties, checked directly: at every level each node's halves are separated on
-    the segment with the largest range (lowest on ties), and ties keep the previous order."""
-    wb = np.asarray(wb, dtype=np.int64)
-    cur = np.arange(len(wb))
-    size = len(wb)
-    while size > ref.LEAF_BLOCK:
-        nxt = cur.copy()
-        for a in range(0, len(wb), size):
-            node = cur[a:a + size]
-            rng = [int(wb[node, s].max() - wb[node, s].min()) for s in range(16)]
-            seg = rng.index(max(rng))
-            # brute force stable sort by one key: insertion in order of (symbol, previous rank)
-            nxt[a:a + size] = [node[k] for k in sorted(range(size), key=lambda k: (int(wb[node[k], seg]), k))]
-            left, right = wb[nxt[a:a + size // 2], seg], wb[nxt[a + size // 2:a + size], seg]
-            assert left.max() <= right.min()
-        cur = nxt
-        size //= 2
-    assert cur.tolist() == list(order)
+def test_lower_bound_window():
+    """C8's approximate-answer window: L rows of the C5 order centred on the query key's
+    lower_bound position, clamped into [0, N)."""
+    keys_hi = np.array([0, 1, 1, 1, 5, 9], np.uint64)
+    keys_lo = np.array([3, 0, 2, 2, 0, 0], np.uint64)
+    assert ref.lower_bound_pos(keys_hi, keys_lo, 1, 2) == 2  # first key >= (1, 2)
+    assert ref.lower_bound_pos(keys_hi, keys_lo, 1, 3) == 4
+    assert ref.lower_bound_pos(keys_hi, keys_lo, 0, 0) == 0
+    assert ref.lower_bound_pos(keys_hi, keys_lo, 10, 0) == 6
+    assert ref.window(2, 6, 4) == (0, 4) and ref.window(5, 6, 4) == (2, 6) and ref.window(3, 10, 4) == (1, 5)
+    assert ref.window(0, 3, 8) == (0, 3)
 
 
-def test_super_kd_block_properties():
-    """R6b: a 1024-row block in kd order down to 32-row leaves (ties, constant segments)."""
-    rng = np.random.default_rng(11)
-    for trial in range(3):
-        wb = rng.integers(0, 256, (1024, 16))
-        if trial == 1:
-            wb[:, 3] = 7                      # a constant segment is never chosen
-            wb[:, 5] = rng.integers(0, 2, 1024)  # heavy ties on a narrow segment
-        if trial == 2:
-            wb = np.cumsum(rng.integers(-3, 4, (1024, 16)), axis=1) + 128  # correlated, walk-like
-            wb = np.clip(wb, 0, 255)
-        order = ref.super_kd_block(wb)
-        assert sorted(order.tolist()) == list(range(1024))
-        _kd_check(wb, order)
-    # tie rule: every segment has the same range, so segment 0 splits first
+def test_layout_checker_detects_violations():
+    """tests/layout_props.py (the GPU layout's property checker) accepts a block that satisfies
+    P3/P4 trivially and rejects it after a cross-half swap or a within-leaf swap."""
+    from tests import layout_props as lp
+
     wb = np.zeros((1024, 16), np.int64)
-    wb[:, :] = (np.arange(1024) % 2)[:, None]
-    order = ref.super_kd_block(wb)
-    assert all(wb[order[:512], 0] == 0) and all(wb[order[512:], 0] == 1)
-
-
-def test_sorted_order_blocks_and_tail():
-    """Full super-nodes are kd-reordered in place; the partial tail keeps the z order."""
-    rng = np.random.default_rng(12)
-    words = rng.integers(0, 256, (2500, 16)).astype(np.uint8)
-    z = ref.canonical_order(words)
-    p = ref.sorted_order(words)
-    for b0 in (0, 1024):
-        assert sorted(p[b0:b0 + 1024].tolist()) == sorted(z[b0:b0 + 1024].tolist())
-        _kd_check(words[z[b0:b0 + 1024]], [z[b0:b0 + 1024].tolist().index(i) for i in p[b0:b0 + 1024]])
-    assert p[2048:].tolist() == z[2048:].tolist()
+    wb[:, 0] = np.arange(1024) // 4  # one non-constant segment, ascending: every split is on it
+    zr = np.arange(1024)
+    lp.check_super_block(wb, zr)
+    bad = wb.copy()
+    bad[[10, 700]] = bad[[700, 10]]
+    with pytest.raises(AssertionError):
+        lp.check_super_block(bad, zr)
+    zr2 = zr.copy()
+    zr2[[4, 5]] = zr2[[5, 4]]  # equal symbols out of C5 order: the splits were not stable
+    with pytest.raises(AssertionError):
+        lp.check_super_block(wb, zr2)
 
 
 # ----------------------------------------------------------------------------- LB / ED
