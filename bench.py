@@ -113,13 +113,13 @@ def peaks():
 
 
 # ------------------------------------------------------------------------------------ oracle
-def cpu_baseline(wl, q_dev, budget_s: float, rank: int):
+def cpu_baseline(wl, q_dev, budget_s: float, rank: int, series: int = 0):
     """The oracle (C7 brute force, oracle/oracle.c, OpenMP on all host cores) on a bounded sample.
 
     Sample: the first S dataset series (streamed from the device generator in 1M-series chunks,
-    copied to host; copies excluded from the timing) against the first 4 queries. S grows
-    chunk by chunk until the oracle has spent ~budget_s seconds. queries/s for the whole
-    workload = 4 / (t * N / S).
+    copied to host; copies excluded from the timing) against the first 4 queries. S is `series`
+    if given, else it grows chunk by chunk until the oracle has spent ~budget_s seconds.
+    queries/s for the whole workload = 4 / (t * N / S).
     """
     import torch
 
@@ -133,8 +133,9 @@ def cpu_baseline(wl, q_dev, budget_s: float, rank: int):
     buf = torch.empty((chunk, wl.n), dtype=torch.float32, device="cuda")
     host = torch.empty((chunk, wl.n), dtype=torch.float32, pin_memory=True)
     t_or, S = 0.0, 0
-    while S < wl.N and t_or < budget_s:
-        c = min(chunk, wl.N - S)
+    limit = min(series, wl.N) if series else wl.N
+    while S < limit and (series or t_or < budget_s):
+        c = min(chunk, limit - S)
         datagen.series(wl, S, c, out=buf[:c])
         host[:c].copy_(buf[:c])
         t0 = time.perf_counter()
@@ -142,7 +143,8 @@ def cpu_baseline(wl, q_dev, budget_s: float, rank: int):
         t_or += time.perf_counter() - t0
         S += c
     qps = 4.0 / (t_or * wl.N / S)
-    return {"value": qps, "unit": "queries/s", "cores": clib.num_threads(), "kind": "oracle",
+    return {"value": qps, "unit": "queries/s", "cores": clib.num_threads(), "kind": "oracle", "series": S,
+            "seconds": t_or,
             "sample": f"brute-force exact 1-NN (oracle C7) of 4 queries over the first {S} of {wl.N} series "
                       f"({t_or:.2f} s); scaled to the full collection"}
 
@@ -230,7 +232,7 @@ def main():
     # on the stream its kernels run on.
     keys = ["lbscan", "candcheck", "refine", "window", "qprep"]
     kms = {k: [] for k in keys}
-    cand, refined, skipped, rounds, scan_b, ref_b, pairs, launches = [], [], [], [], [], [], [], 0
+    cand, refined, abandoned, skipped, winrows, rounds, scan_b, ref_b, pairs, launches = [], [], [], [], [], [], [], [], [], 0
     for _ in range(args.steps):
         ids, dist_ = ix.nn1(q)
         st = ix.stats()
@@ -238,7 +240,9 @@ def main():
             kms[k].append(st["ms_first_batch"][k])
         cand.append(sum(st["candidates"]))
         refined.append(sum(st["refined"]))
+        abandoned.append(sum(st["abandoned"]))
         skipped.append(sum(st.get("skipped", [0])))
+        winrows.append(sum(st["window_rows"]))
         rounds.append(max(st["rounds"]))
         launches += st.get("launches", 0)
         scan_b.append(st["scan_bytes_first_launch"])
@@ -346,9 +350,14 @@ def main():
         "clocks": clocks,
         "build": {"seconds": round(build_s, 3), "mode": build_mode, "N": wl.N, "n": wl.n,
                   "input_GBps": round(raw_bytes / build_s / 1e9, 1), "index_device_bytes": ix.device_bytes},
-        "stats": {"candidates_per_query": statistics.mean(cand) / Q, "refined_per_query": statistics.mean(refined) / Q,
+        "stats": {"candidates_per_query": statistics.mean(cand) / Q,
+                  "refined_per_query": statistics.mean(refined) / Q,
+                  "abandoned_per_query": statistics.mean(abandoned) / Q,
                   "skipped_per_query": statistics.mean(skipped) / Q,
-                  "rounds_max": max(rounds)},
+                  "window_rows_per_query": statistics.mean(winrows) / Q,
+                  "rounds_max": max(rounds),
+                  "note": "candidates = refined to the end + abandoned + skipped by the second band's bound; "
+                          "window rows are counted apart"},
     }
     if rank == 0 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(wl, q, args.cpu_seconds, rank)
@@ -364,7 +373,13 @@ def main():
 
 
 def run_reference(args, wl, world, rank, local):
-    """--impl reference: the oracle (no reference implementation exists), timed on host cores."""
+    """--impl reference: the oracle (no reference implementation exists), timed on host cores.
+
+    Every step is the same bounded sample of the workload: the oracle's brute force (C7) of 4
+    queries over the first S series, S fixed by the first warm-up step (about 2 s of oracle work).
+    ms_per_step is that step's measured wall time (oracle only; generating and copying the
+    sample's series is excluded); value is the workload's queries/s the sample implies,
+    4 / (t_step * N / S)."""
     if rank != 0:
         return
     import torch
@@ -373,18 +388,23 @@ def run_reference(args, wl, world, rank, local):
 
     torch.cuda.set_device(local)
     q, _ = datagen.queries(wl, args.queries or wl.Q)
-    per_step = max(2.0, 60.0 / max(1, args.steps + args.warmup))
-    for _ in range(args.warmup):
-        cpu_baseline(wl, q, min(per_step, 2.0), rank)
-    vals, last = [], None
+    per_step = 2.0
+    first = cpu_baseline(wl, q, per_step, rank)  # calibrates S (counted as a warm-up step)
+    S = first["series"]
+    for _ in range(max(0, args.warmup - 1)):
+        cpu_baseline(wl, q, per_step, rank, series=S)
+    vals, secs, last = [], [], None
     for _ in range(args.steps):
-        last = cpu_baseline(wl, q, per_step, rank)
+        last = cpu_baseline(wl, q, per_step, rank, series=S)
         vals.append(last["value"])
-    v = statistics.mean(vals)
+        secs.append(last["seconds"])
+    v = args.steps * 4 / (sum(secs) * wl.N / S)
     out = {"impl": "reference", "metric": METRIC, "value": v, "unit": "queries/s", "n_gpus": world,
-           "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * 4 / v, "higher_is_better": True,
-           "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-           "config": {"workload": wl.name, "N": wl.N, "n": wl.n, "w": 16, "card": 256},
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(secs) / args.steps,
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": {"workload": wl.name, "N": wl.N, "n": wl.n, "w": 16, "card": 256,
+                      "step": f"oracle C7 brute force of 4 queries over the first {S} of {wl.N} series; "
+                              "value = 4 / (ms_per_step * N / S)"},
            "cpu_baseline": {"kind": "oracle", "cores": last["cores"], "sample": last["sample"], "value": v,
                             "unit": "queries/s"},
            "e2e": {"value": v, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
