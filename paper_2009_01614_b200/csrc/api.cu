@@ -56,7 +56,7 @@ struct DeviceGuard {
 };
 
 static isax_opts default_opts(const isax_opts *o) {
-    isax_opts r{3072, -12, 1024, 0, 0, 5, 128};  // cand_cap 0: chosen per batch (alloc_scratch, nn1_device)
+    isax_opts r{3072, -12, 1024, 0, 0, 5, 128, 0.f};  // cand_cap 0: chosen per batch (alloc_scratch, nn1_device)
     if (o) {
         if (o->probe_bits) r.probe_bits = o->probe_bits;
         if (o->probe_L) r.probe_L = o->probe_L;
@@ -64,6 +64,7 @@ static isax_opts default_opts(const isax_opts *o) {
         if (o->slack_log2) r.slack_log2 = o->slack_log2;
         if (o->batch_Q) r.batch_Q = o->batch_Q;
         if (o->cand_cap) r.cand_cap = o->cand_cap;
+        r.first_band = o->first_band;
         r.flags = o->flags;
     }
     return r;
@@ -83,6 +84,7 @@ static int check_geometry(uint64_t N, uint32_t n, uint32_t w, uint32_t card, con
     if (o.flags & ~ISAX_FLAG_FLAT_SCAN) return set_error(ISAX_E_INVAL, "unknown flags");
     if (o.probe_bits != ISAX_PROBES_NONE && o.probe_bits > 5) return set_error(ISAX_E_INVAL, "probe_bits must be <= 5");
     if (o.probe_L == 0 || o.probe_L > 1024) return set_error(ISAX_E_INVAL, "probe_L must be in [1, 1024]");
+    if (!(o.first_band < 1.0f) || o.first_band != o.first_band) return set_error(ISAX_E_INVAL, "first_band must be < 1");
     return ISAX_OK;
 }
 
@@ -113,6 +115,8 @@ static void free_scratch(isax_index *ix) {
 // candidates) get the generous 2^23; a batch of 1000 near-duplicate queries gets 2^20, where the
 // smallest-bounds-first rounds skip most of a heavy query's candidates (BASELINE config 5).
 constexpr uint64_t CAND_POOL = 1ull << 30;
+constexpr float FB_FRAC = 0.02f;      // R15: the adaptive first band's fraction of the window threshold
+constexpr uint32_t FB_REPROBE = 32;   // batches in the preferred mode before the other one is re-timed
 static int alloc_scratch_cap(isax_index *ix, uint32_t cap);
 static int alloc_scratch(isax_index *ix) {
     if (ix->qs.cap_Q) return ISAX_OK;
@@ -392,9 +396,32 @@ static int nn1_device(isax_index *ix, const float *d_q, uint32_t Q, int64_t *d_i
             hm.near_off[i] = (unsigned long long)i * NEAR_K;
             hm.near_cap[i] = NEAR_K;
         }
+        // R15: the first band (best-first order). Adaptive by default: each mode (with
+        // and without the first band) is timed on the device per query; the cheaper one runs, and
+        // the other is re-timed after FB_REPROBE batches. Answers never depend on it, only the work.
+        const float fopt = ix->opts.first_band;
+        float band0 = 0.f;
+        bool adapt = false;
+        if (fopt > 0.f) {
+            band0 = fopt;
+        } else if (fopt == 0.f) {
+            adapt = true;
+            bool on;
+            if (ix->fb_ms_on < 0.f) on = true;
+            else if (ix->fb_ms_off < 0.f) on = false;
+            else {
+                on = ix->fb_ms_on <= ix->fb_ms_off;
+                if (ix->fb_since >= FB_REPROBE) on = !on;
+            }
+            band0 = on ? FB_FRAC : 0.f;
+        }
         const bool timed = b0 == 0;
-        if (timed) cudaEventRecord(ix->ev[0], s);
-        launch_qprep(ix, d_q + (uint64_t)b0 * ix->n, B, s, qs.flag);
+        if (timed) {
+            ix->st_fb_frac = band0;
+            ix->st_fb_improved = 0;
+        }
+        cudaEventRecord(ix->ev[0], s);
+        launch_qprep(ix, d_q + (uint64_t)b0 * ix->n, B, band0, s, qs.flag);
         ix->st_launches += 2;
         if (timed) cudaEventRecord(ix->ev[1], s);
         launch_window(ix, B, nullptr, delta, s);
@@ -412,7 +439,8 @@ static int nn1_device(isax_index *ix, const float *d_q, uint32_t Q, int64_t *d_i
         // the final BSF is collected (R9).
         // Every round ends with one host synchronisation. The finalise kernel (for the queries
         // scanned in the round) and all counter copies are enqueued before it.
-        std::vector<Band> band(B, Band{-1.0f, INF, 0u, NP});
+        // (round 0 covers (-1, band0 * T0] when band0 > 0; qprep_kernel writes it)
+        std::vector<Band> band(B, Band{-1.0f, band0 > 0.f ? -band0 : INF, 0u, NP});
         std::vector<uint32_t> plen(B, NP);  // position mode: length of the next range
         std::vector<uint32_t> nfirst(B, 0);  // consecutive overflows whose first histogram bin alone overflowed
         std::vector<char> pending(B, 1);
@@ -459,6 +487,7 @@ static int nn1_device(isax_index *ix, const float *d_q, uint32_t Q, int64_t *d_i
             if (timed && round == 0) cudaEventRecord(ix->ev[4], s);
             // speculative: a query scanned again in a later round is finalised again
             launch_finalize(ix, nact, qs.qmap, delta, d_id + b0, d_dist + b0, s);
+            cudaEventRecord(ix->ev[7], s);  // the batch's end so far (R15 policy timing)
             // scanprep + scan, candcheck, refine + filter + refine, finalize
             ix->st_launches += ((ix->opts.flags & ISAX_FLAG_FLAT_SCAN) ? 1 : 2) + 5;
             if (timed && round == 0) cudaEventRecord(ix->ev[5], s);
@@ -475,6 +504,15 @@ static int nn1_device(isax_index *ix, const float *d_q, uint32_t Q, int64_t *d_i
                     bsf_h[i] = bsf_d2_host(hm.bsf_scan[i]);
                     bsf0_h[i] = bsf_h[i];
                     tused[i] = bsf_h[i] * onepd;
+                    if (band[i].hi < 0.f) {  // the first band's edge, as scanprep_kernel computed it
+                        tused[i] = tused[i] * -band[i].hi;
+                        band[i].hi = tused[i];
+                    }
+                }
+                if (band0 > 0.f && timed) {  // stats: queries whose BSF the first band at least halved
+                    uint32_t improved = 0;
+                    for (uint32_t i = 0; i < B; i++) improved += bsf_d2_host(hm.bsf[i]) < 0.5f * bsf0_h[i];
+                    ix->st_fb_improved = improved;
                 }
                 if (b0 == 0) {
                     ix->st_scan_bytes_first = ix->st_scan_bytes + *hm.scan_bytes_dev;
@@ -563,6 +601,19 @@ static int nn1_device(isax_index *ix, const float *d_q, uint32_t Q, int64_t *d_i
             }
         }
         if (result) break;
+        if (adapt) {  // R15 policy: device ms per query of this batch, in its mode
+            float ms = 0.f;
+            if (cudaEventElapsedTime(&ms, ix->ev[0], ix->ev[7]) == cudaSuccess) {
+                const float per = ms / (float)B;
+                float &slot = band0 > 0.f ? ix->fb_ms_on : ix->fb_ms_off;
+                const bool preferred = (band0 > 0.f) == (ix->fb_ms_on >= 0.f && ix->fb_ms_off >= 0.f &&
+                                                         ix->fb_ms_on <= ix->fb_ms_off);
+                slot = slot < 0.f ? per : 0.5f * (slot + per);
+                ix->fb_since = preferred ? ix->fb_since + 1 : 0;
+            } else {
+                cudaGetLastError();
+            }
+        }
         for (uint32_t i = 0; i < B; i++) {
             ix->st_refined[b0 + i] = hm.counters[4 * i];
             ix->st_abandoned[b0 + i] = hm.counters[4 * i + 1];
@@ -722,7 +773,7 @@ int isax_query_debug(const isax_index *cix, const float *queries, uint32_t Q, do
     if (e == cudaSuccess) e = cudaMalloc(&flag, sizeof(uint32_t));
     if (e == cudaSuccess) e = cudaMemsetAsync(flag, 0, sizeof(uint32_t), s);
     if (e == cudaSuccess) {
-        launch_qprep(ix, dq, Q, s, flag);
+        launch_qprep(ix, dq, Q, 0.f, s, flag);
         e = cudaGetLastError();
     }
     const QueryScratch &qs = ix->qs;
@@ -814,6 +865,11 @@ int isax_stats(const isax_index *cix, char *buf, size_t cap) {
         j += b;
     }
     j += "],";
+    {
+        char b[96];
+        snprintf(b, sizeof b, "\"first_band\":%.6g,\"first_band_improved\":%u,", ix->st_fb_frac, ix->st_fb_improved);
+        j += b;
+    }
     j += "\"launches\":" + std::to_string(ix->st_launches);
     j += ",\"scan_bytes\":" + std::to_string(ix->st_scan_bytes);
     j += ",\"scan_bytes_first_launch\":" + std::to_string(ix->st_scan_bytes_first);

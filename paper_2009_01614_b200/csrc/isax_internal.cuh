@@ -198,6 +198,13 @@ struct isax_index {
     isax::StageTimes st_ms;
     uint64_t st_launches = 0;  // kernels launched by the last nn1 call
     uint32_t st_last_Q = 0;     // Q of the last nn1 call
+    // R15 first-band policy (adaptive by default): the measured device ms per query of batches run
+    // with and without the first band (-1 = not measured yet); the cheaper mode is used, the other
+    // one re-measured every FB_REPROBE batches
+    float fb_ms_on = -1.f, fb_ms_off = -1.f;
+    uint32_t fb_since = 0;       // batches since the other mode was last measured
+    float st_fb_frac = 0.f;      // first-band fraction of the last call's first batch (0 = none)
+    uint32_t st_fb_improved = 0; // its queries whose BSF the first band at least halved (stats)
     uint64_t st_scan_bytes = 0, st_scan_bytes_first = 0;  // summary bytes the scan read (all / first launch)
     uint64_t st_refine_bytes_first = 0;                    // row bytes the first refine launch read
     uint64_t st_leaf_pairs_first = 0, st_scan_q_first = 0; // (leaf, query) pairs kept / queries of the first scan
@@ -242,7 +249,8 @@ void launch_invert_perm(const uint32_t *perm, uint64_t N, uint32_t *inv, cudaStr
 void launch_export_sax(const uint8_t *sax, const uint32_t *inv, uint64_t first_id, uint64_t count, uint8_t *out,
                        cudaStream_t s);
 // query.cu
-void launch_qprep(const isax_index *ix, const float *queries, uint32_t Q, cudaStream_t s, uint32_t *bad);
+// band0 > 0: round 0 scans only the first band LB^2 <= band0 * bsf0^2 (1 + delta) (R15)
+void launch_qprep(const isax_index *ix, const float *queries, uint32_t Q, float band0, cudaStream_t s, uint32_t *bad);
 uint32_t probe_bits(const isax_index *ix);
 uint32_t window_probes(const isax_index *ix);  // probe-sized windows per query (incl. neighbour quarters)
 void launch_window(const isax_index *ix, uint32_t Q, const uint32_t *qmap, float delta, cudaStream_t s);

@@ -135,7 +135,9 @@ __device__ __forceinline__ bool pos_ok(const QConst &k, uint32_t pos) {
 __device__ __forceinline__ QConst load_qconst(uint32_t qi, bool valid, const unsigned long long *bsf,
                                               const Band *band, uint32_t slot, const uint32_t *win, float onepd) {
     const Band b = valid ? band[slot] : Band{0.f, -1.f, 0u, 0u};
-    const float tq = valid ? fminf(bsf_d2(bsf[qi]) * onepd, b.hi) : -1.0f;  // an invalid slot keeps nothing
+    // hi < 0 encodes a fraction of the BSF threshold (the first band of a query, R15): T = bsf^2 (1 + delta) * -hi
+    const float tb = bsf_d2(bsf[qi]) * onepd;
+    const float tq = valid ? (b.hi < 0.f ? tb * -b.hi : fminf(tb, b.hi)) : -1.0f;  // an invalid slot keeps nothing
     return QConst{b.lo, tq, win[2 * qi], win[2 * qi + 1], b.plo, b.phi, 0u, 0u};
 }
 

@@ -63,7 +63,7 @@ __global__ void __launch_bounds__(NT) qprep_kernel(const float *__restrict__ que
                                                     uint32_t *__restrict__ cand_cnt, uint32_t *__restrict__ near_cnt,
                                                     unsigned long long *__restrict__ near_off, uint32_t *__restrict__ near_cap,
                                                     uint32_t *__restrict__ counters, uint32_t *__restrict__ counters_leaf,
-                                                    uint32_t *__restrict__ qmap, Band *__restrict__ qband,
+                                                    uint32_t *__restrict__ qmap, Band *__restrict__ qband, float band0,
                                                     uint32_t *__restrict__ bad) {
     __shared__ float row[1024];
     __shared__ double beta[ISAX_NBETA];
@@ -98,7 +98,7 @@ __global__ void __launch_bounds__(NT) qprep_kernel(const float *__restrict__ que
         counters[4 * q + 0] = counters[4 * q + 1] = counters[4 * q + 2] = counters[4 * q + 3] = 0;
         counters_leaf[q] = 0;
         qmap[q] = q;  // round 0 scans every query of the batch over the band (-1, +inf), all positions (R10)
-        qband[q] = Band{-1.0f, __int_as_float(0x7f800000), 0u, (uint32_t)N};
+        qband[q] = Band{-1.0f, band0 > 0.f ? -band0 : __int_as_float(0x7f800000), 0u, (uint32_t)N};
         bsf[q] = ~0ull;
     }
     __syncthreads();
@@ -245,7 +245,7 @@ __global__ void __launch_bounds__(NT) qprep_kernel(const float *__restrict__ que
     }
 }
 
-void launch_qprep(const isax_index *ix, const float *queries, uint32_t Q, cudaStream_t s, uint32_t *bad) {
+void launch_qprep(const isax_index *ix, const float *queries, uint32_t Q, float band0, cudaStream_t s, uint32_t *bad) {
     const QueryScratch &qs = ix->qs;
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
@@ -253,7 +253,8 @@ void launch_qprep(const isax_index *ix, const float *queries, uint32_t Q, cudaSt
     auto kern = Q <= (uint32_t)(2 * sms) ? qprep_kernel<1024> : qprep_kernel<256>;
     kern<<<Q, Q <= (uint32_t)(2 * sms) ? 1024 : 256, 0, s>>>(queries, ix->n, ix->skey, ix->ksplit, ix->N,
                                    ix->opts.window_L, probe_bits(ix), ix->opts.probe_L, qs.pwin, qs.qy, qs.qpaa, qs.qsax, qs.lut, qs.win, qs.bsf, qs.cand_cnt,
-                                   qs.near_cnt, qs.near_off, qs.near_cap, qs.counters, qs.counters_leaf, qs.qmap, qs.qband, bad);
+                                   qs.near_cnt, qs.near_off, qs.near_cap, qs.counters, qs.counters_leaf, qs.qmap, qs.qband,
+                                   band0, bad);
 }
 
 // ------------------------------------------------------------------------------------ window

@@ -30,7 +30,7 @@ ERRORS = {-1: "ISAX_E_INVAL", -2: "ISAX_E_EMPTY", -3: "ISAX_E_UNSUPPORTED", -4: 
 class Opts(ctypes.Structure):
     _fields_ = [("window_L", ctypes.c_uint32), ("slack_log2", ctypes.c_int32), ("batch_Q", ctypes.c_uint32),
                 ("cand_cap", ctypes.c_uint32), ("flags", ctypes.c_uint32), ("probe_bits", ctypes.c_uint32),
-                ("probe_L", ctypes.c_uint32)]
+                ("probe_L", ctypes.c_uint32), ("first_band", ctypes.c_float)]
 
 
 def _sig(name, args, res=ctypes.c_int):
@@ -83,8 +83,8 @@ FLAG_FLAT_SCAN = 1  # include/isax.h ISAX_FLAG_FLAT_SCAN
 PROBES_NONE = 0xFFFFFFFF  # include/isax.h ISAX_PROBES_NONE
 
 
-def _opts(window_L=0, slack_log2=0, batch_Q=0, cand_cap=0, flags=0, probe_bits=0, probe_L=0):
-    return Opts(window_L, slack_log2, batch_Q, cand_cap, flags, probe_bits, probe_L)
+def _opts(window_L=0, slack_log2=0, batch_Q=0, cand_cap=0, flags=0, probe_bits=0, probe_L=0, first_band=0.0):
+    return Opts(window_L, slack_log2, batch_Q, cand_cap, flags, probe_bits, probe_L, first_band)
 
 
 class Index:

@@ -128,7 +128,8 @@ def test_candidate_set_equals_the_oracle_lb_filter(N, n, kind):
     x = datagen.series(wl, 0, N)
     q, _ = datagen.queries(wl)
     qh = q.cpu().numpy()
-    with _build(x) as ix, _build(x, flags=1) as flat:
+    # one round per query (no first band, R15): the list is then the whole LB filter of bsf0
+    with _build(x, first_band=-1) as ix, _build(x, flags=1, first_band=-1) as flat:
         ids, dist = ix.nn1(q)
         st = ix.stats()
         cands = [np.sort(ix.candidates(i)) for i in range(len(qh))]
@@ -191,7 +192,8 @@ def test_ties_duplicates_constants_and_exact_copies():
                                   dict(slack_log2=-20), dict(probe_bits=0xFFFFFFFF), dict(probe_bits=5, probe_L=1),
                                   dict(probe_bits=2, probe_L=1024), dict(flags=1), dict(window_L=2048),
                                   dict(window_L=1024), dict(window_L=512, probe_L=64), dict(probe_L=256),
-                                  dict(probe_bits=3, probe_L=512)])
+                                  dict(probe_bits=3, probe_L=512), dict(first_band=-1), dict(first_band=0.3),
+                                  dict(first_band=0.02, cand_cap=7), dict(first_band=0.999)])
 def test_options_do_not_change_answers(opts):
     N, n = 30_000, 256
     wl = small_workload(N, n, Q=12, q_noisy=4)
