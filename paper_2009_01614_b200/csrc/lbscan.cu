@@ -103,6 +103,20 @@ __device__ __forceinline__ uint4 ld_sh_v4(const uint4 *p) {
     return r;
 }
 
+__device__ __forceinline__ uint32_t ld_sh_u32a(uint32_t a) {
+    uint32_t r;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(r) : "r"(a));
+    return r;
+}
+__device__ __forceinline__ uint4 ld_sh_v4a(uint32_t a) {
+    uint4 r;
+    asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "r"(a));
+    return r;
+}
+// 16-byte global -> shared asynchronous copy (LDGSTS) to a shared-window address
+__device__ __forceinline__ void cp_async16_sh(uint32_t dst, const void *src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
 // 16-byte global -> shared asynchronous copy (LDGSTS); zero-fills the destination when !valid
 __device__ __forceinline__ void cp_async16(void *dst_smem, const void *src, bool valid) {
     const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst_smem);
@@ -261,9 +275,8 @@ static void launch_g(const isax_index *ix, uint32_t nq, const uint32_t *qmap, co
 //  B. lane = member: each warp takes one worklist entry per iteration and keeps PD entries in
 //     flight in a ring of shared staging slots fed by cp.async (each lane copies and reads only its
 //     own word). For every query of the mask it runs the u8 member test (16 lookups), one warp
-//     vote, and for the rare survivors the exact rule and the candidate append. Candidates are
-//     buffered in shared memory per query slot and flushed once per group (one global atomic per
-//     slot).
+//     vote, and for the rare survivors the exact rule and the candidate append (one global
+//     atomic per warp and query).
 constexpr uint32_t LEAF = LEAF_SIZE;
 constexpr uint32_t SUPER = SUPER_SIZE / LEAF_SIZE;  // leaves per super-node
 constexpr uint32_t HYPER = HYPER_SIZE / SUPER_SIZE; // super-nodes per hyper-node
@@ -271,64 +284,63 @@ static_assert(HYPER == 32, "phase A maps the super-nodes of a hyper-node to the 
 static_assert(LEAF == 32 && SUPER == 32, "phase A maps a super-node to a warp iteration and a leaf to a lane");
 constexpr int LF_THREADS = 1024;
 constexpr uint32_t CHUNK = 8192;  // max leaves per phase-A/phase-B round of a CTA
-#ifndef ISAX_CBUF
-#define ISAX_CBUF 512
-#endif
-constexpr uint32_t CBUF = ISAX_CBUF;  // shared candidate buffer per query slot
 #ifndef ISAX_PD
 #define ISAX_PD 4
 #endif
-constexpr uint32_t PD = ISAX_PD;  // phase B: worklist entries in flight per warp
+constexpr uint32_t PD = ISAX_PD;  // phase B: worklist entries in flight per warp (a power of two)
+static_assert((PD & (PD - 1)) == 0, "the staging ring wraps with a mask");
 // a u8 member sum <= E_SURE implies LB^2 <= T: sum_s LUT_s * sc < (sum e + 16) / (1 - 2^-23) and
 // sc >= (254 / T)(1 - 2^-23), so LB^2 < (237 + 16) / 254 * T * (1 + 2^-20) < T (R11b)
 constexpr uint32_t E_SURE = 237;
 
-// append `keep` lanes' positions for query slot g: shared buffer first, global list if it is full
-// with its u8 bound b (b / sc <= LB^2, for the refine's skip test)
-// Once this CTA sees the query's global list pass its capacity, it sets CB_OVF in the slot's
-// shared count: the list is dropped for the round anyway (R10: an overflowed list is neither
-// refined nor needed, only the histogram is), so candidates beyond the shared buffer are no
-// longer appended (a query with millions of candidates otherwise serialises every CTA on its
-// global count).
-constexpr uint32_t CB_OVF = 0x80000000u;
-__device__ __forceinline__ void emit(bool keep, uint32_t pos, uint32_t b, uint32_t g, uint32_t q, uint32_t lane,
-                                     uint32_t lt, uint32_t *cbuf, uint8_t *qbuf, uint32_t *cb_cnt, uint32_t *cand,
-                                     uint8_t *candq, uint32_t *cand_cnt, uint32_t cap) {
+// Candidate appends ("the data series that are not pruned are stored in a candidate list").
+// Each warp stages its kept lanes in a private shared buffer of (position, slot, u8 bound) entries
+// (no atomics: the warp's count is a register) and empties it into the global lists itself when it
+// holds WB - 32 or more, and at the end of each task: the entries of one query slot get one global
+// atomic per flush (match_any groups the lanes by slot). The u8 bound b satisfies b / sc <= LB^2
+// (for the refine's skip test). Once a query's list has passed its capacity the slot's flag stops
+// this CTA's appends: the list is dropped for the round anyway (R10: an overflowed list is neither
+// refined nor needed, only the histogram is), and a query with millions of candidates would
+// otherwise serialise every CTA on its count.
+constexpr uint32_t WB = 64;  // staged candidates per warp
+__device__ __forceinline__ void wflush(uint2 *wb, uint32_t &wcnt, uint32_t lane, volatile uint32_t *ovf,
+                                       const uint32_t *qid, uint32_t *cand, uint8_t *candq, uint32_t *cand_cnt,
+                                       uint32_t cap) {
+    __syncwarp();
+    for (uint32_t i0 = 0; i0 < wcnt; i0 += 32) {
+        const bool have = i0 + lane < wcnt;
+        const uint2 en = have ? wb[i0 + lane] : make_uint2(0u, 0u);
+        const uint32_t g = have ? (en.y >> 8) : 0xFFFFu;
+        const uint32_t peers = __match_any_sync(0xffffffffu, g);
+        if (have) {
+            const uint32_t leader = __ffs(peers) - 1;
+            const uint32_t q = qid[g];
+            uint32_t base = 0xffffffffu;
+            if (lane == leader && !ovf[g]) {
+                const uint32_t c = __popc(peers);
+                base = atomicAdd(&cand_cnt[q], c);
+                if (base + c > cap) ovf[g] = 1u;
+            }
+            base = __shfl_sync(peers, base, leader);
+            const uint32_t k = base + __popc(peers & ((1u << lane) - 1u));
+            if (base != 0xffffffffu && k < cap) {
+                cand[(uint64_t)q * cap + k] = en.x;
+                candq[(uint64_t)q * cap + k] = (uint8_t)(en.y & 0xFFu);
+            }
+        }
+    }
+    __syncwarp();
+    wcnt = 0;
+}
+
+__device__ __forceinline__ void emit(bool keep, uint32_t pos, uint32_t b, uint32_t g, uint32_t lane, uint32_t lt,
+                                     uint2 *wb, uint32_t &wcnt, volatile uint32_t *ovf, const uint32_t *qid,
+                                     uint32_t *cand, uint8_t *candq, uint32_t *cand_cnt, uint32_t cap) {
     const uint32_t bal = __ballot_sync(0xffffffffu, keep);
-    if (!bal) return;
-    const uint32_t c = __popc(bal);
-    uint32_t off = 0;
-    if (lane == 0) off = atomicAdd(&cb_cnt[g], c);
-    off = __shfl_sync(0xffffffffu, off, 0);
-    const uint32_t r = __popc(bal & lt);
-    if (off + c <= CBUF) {
-        if (keep) {
-            cbuf[g * CBUF + off + r] = pos;
-            qbuf[g * CBUF + off + r] = (uint8_t)b;
-        }
-        return;
-    }
-    // the buffer fills up: the slots below CBUF are still written (the flush copies exactly
-    // min(count, CBUF) entries), the rest go straight to the global list
-    const uint32_t room = off < CBUF ? CBUF - off : 0;
-    if (keep && r < room) {
-        cbuf[g * CBUF + off + r] = pos;
-        qbuf[g * CBUF + off + r] = (uint8_t)b;
-    }
-    if (off >= CB_OVF) return;  // the query's list overflowed (see above)
-    uint32_t goff = 0;
-    if (lane == 0) {
-        goff = atomicAdd(&cand_cnt[q], c - room);
-        if (goff + (c - room) > cap) atomicOr(&cb_cnt[g], CB_OVF);
-    }
-    goff = __shfl_sync(0xffffffffu, goff, 0);
-    if (keep && r >= room) {
-        const uint32_t k = goff + r - room;
-        if (k < cap) {
-            cand[(uint64_t)q * cap + k] = pos;
-            candq[(uint64_t)q * cap + k] = (uint8_t)b;
-        }
-    }
+    if (!bal || ovf[g]) return;
+    if (keep) wb[wcnt + __popc(bal & lt)] = make_uint2(pos, (g << 8) | b);
+    wcnt += __popc(bal);
+    if (wcnt > WB - 32) wflush(wb, wcnt, lane, ovf, qid, cand, candq, cand_cnt, cap);
 }
 
 // u8 table entry (R11b): floor(v * sc) with sc = 254 / T rounded down, clamped at 255. v = 0 maps
@@ -388,7 +400,7 @@ __global__ void __launch_bounds__(LF_THREADS, 1) leafscan_kernel(
     uint32_t chunk, uint32_t *__restrict__ cand, uint8_t *__restrict__ candq, uint32_t *__restrict__ cand_cnt, uint32_t cap,
     uint32_t *__restrict__ hist, uint32_t *__restrict__ leaves_alive, unsigned long long *__restrict__ scan_bytes_dev,
     uint32_t *__restrict__ task_ctr) {
-    // shared: [G][16][256] u8 tables | [G][CBUF] candidates | [CHUNK] worklist | [NW][2][2 LEAF] words
+    // shared: [G][16][256] u8 tables | [CHUNK] worklist | [NW][PD][LEAF] staged words
     // (the dynamic region follows the static variables, so the u8 tables are aligned by hand: the
     // PRMT address trick needs a 256-aligned base)
     extern __shared__ __align__(16) uint8_t smem_dyn[];
@@ -396,13 +408,14 @@ __global__ void __launch_bounds__(LF_THREADS, 1) leafscan_kernel(
     const uint32_t lut8_sh = (raw8 + 255u) & ~255u;
     uint8_t *lut8 = smem_dyn + (lut8_sh - raw8);
     constexpr uint32_t NW = LF_THREADS / 32;
-    uint32_t *cbuf = reinterpret_cast<uint32_t *>(lut8 + G * W * CARD);
-    uint32_t *worklist = cbuf + G * CBUF;  // (leaf offset in chunk) | (query mask << 16)
-    uint4 *stage = reinterpret_cast<uint4 *>(worklist + CHUNK);
-    uint8_t *qbuf = reinterpret_cast<uint8_t *>(stage + NW * PD * LEAF);  // [G][CBUF] u8 bounds
+    uint32_t *worklist = reinterpret_cast<uint32_t *>(lut8 + G * W * CARD);  // (leaf offset in chunk) | (query mask << 16)
+    const uint32_t wl_sh = lut8_sh + G * W * CARD;
+    const uint32_t stage_sh = wl_sh + CHUNK * 4;  // 16-byte aligned
+    uint2 *wbuf = reinterpret_cast<uint2 *>(worklist + CHUNK + NW * PD * LEAF * 4) + (threadIdx.x >> 5) * WB;  // this warp's staged candidates
+    uint32_t wcnt = 0;
     __shared__ QConst qc[G];
     __shared__ uint4 qsym[G][2];  // the query's 16 symbols as 8 u16x2 pairs
-    __shared__ uint32_t qid[G], cb_cnt[G], alive_cnt[G], fbase[G];
+    __shared__ uint32_t qid[G], alive_cnt[G], s_ovf[G];
     __shared__ float qsc[G];  // 254 / T rounded down (the u8 table scale)
     __shared__ uint32_t shist[G][HIST_BINS];
     __shared__ uint32_t wl_cnt, s_task;
@@ -420,31 +433,15 @@ __global__ void __launch_bounds__(LF_THREADS, 1) leafscan_kernel(
     uint32_t bytes = 0;            // node summaries and words this thread read
     uint32_t my_alive = 0;         // lane g < G: loaded (leaf, query g) pairs of this warp
     uint32_t g0 = 0xffffffffu;     // first query slot of the group whose tables are loaded
-    // empty the shared candidate buffers and histograms of the loaded group into global memory
+    // the loaded group's histograms and surviving-leaf counts into global memory
     auto flush = [&]() {
         if (lane < G && my_alive) atomicAdd(&alive_cnt[lane], my_alive);
         my_alive = 0;
         __syncthreads();
-        if (t < G) {
-            const uint32_t c = min(cb_cnt[t], CBUF);
-            fbase[t] = (c && g0 + t < nq) ? atomicAdd(&cand_cnt[qid[t]], c) : 0;
-            if (alive_cnt[t] && g0 + t < nq) atomicAdd(&leaves_alive[qid[t]], alive_cnt[t]);
-        }
+        if (t < G && alive_cnt[t] && g0 + t < nq) atomicAdd(&leaves_alive[qid[t]], alive_cnt[t]);
         for (uint32_t e = t; e < G * HIST_BINS; e += LF_THREADS) {
             const uint32_t g = e / HIST_BINS, b = e % HIST_BINS;
             if (g0 + g < nq && shist[g][b]) atomicAdd(&hist[qid[g] * HIST_BINS + b], shist[g][b]);
-        }
-        __syncthreads();
-        for (uint32_t g = 0; g < G; g++) {
-            if (g0 + g >= nq) break;
-            const uint32_t c = min(cb_cnt[g], CBUF);
-            for (uint32_t i = t; i < c; i += LF_THREADS) {
-                const uint32_t k = fbase[g] + i;
-                if (k < cap) {
-                    cand[(uint64_t)qid[g] * cap + k] = cbuf[g * CBUF + i];
-                    candq[(uint64_t)qid[g] * cap + k] = qbuf[g * CBUF + i];
-                }
-            }
         }
         __syncthreads();
     };
@@ -464,8 +461,8 @@ __global__ void __launch_bounds__(LF_THREADS, 1) leafscan_kernel(
                 const uint32_t slot = valid ? g0 + t : g0;
                 const uint32_t qi = qmap[slot];
                 qid[t] = qi;
-                cb_cnt[t] = 0;
                 alive_cnt[t] = 0;
+                s_ovf[t] = 0;
                 const uint4 w = reinterpret_cast<const uint4 *>(qsax_all)[qi];
                 qsym[t][0] = make_uint4(lo_u16x2(w.x), hi_u16x2(w.x), lo_u16x2(w.y), hi_u16x2(w.y));
                 qsym[t][1] = make_uint4(lo_u16x2(w.z), hi_u16x2(w.z), lo_u16x2(w.w), hi_u16x2(w.w));
@@ -517,16 +514,18 @@ __global__ void __launch_bounds__(LF_THREADS, 1) leafscan_kernel(
         }
         __syncthreads();
         // A2: warp iteration = one super-node (s0 + warp + NW j), lane = one of its 32 leaves, for
-        // the queries that kept the super-node. Leaf summaries are read only under surviving
-        // super-nodes, one iteration ahead.
+        // the queries that kept the super-node (a rolled loop over the mask's bits). Leaf summaries
+        // are read only under surviving super-nodes, one iteration ahead.
+        const uint4 *meta8 = meta4;
+        constexpr uint32_t MW = 2;
         uint32_t nmask = 0;
         uint4 mn_n = make_uint4(0, 0, 0, 0), mx_n = mn_n;
         if (s0 + warp < send) {
             nmask = smask_sh[warp];
             const uint32_t leaf = (s0 + warp) * SUPER + lane;
             if (nmask && leaf < c1) {
-                mn_n = __ldg(meta4 + 2 * (uint64_t)leaf);
-                mx_n = __ldg(meta4 + 2 * (uint64_t)leaf + 1);
+                mn_n = __ldg(meta8 + MW * (uint64_t)leaf);
+                mx_n = __ldg(meta8 + MW * (uint64_t)leaf + 1);
             }
         }
         for (uint32_t sn = s0 + warp; sn < send; sn += NW) {
@@ -537,18 +536,19 @@ __global__ void __launch_bounds__(LF_THREADS, 1) leafscan_kernel(
                 nmask = smask_sh[sn + NW - s0];
                 const uint32_t l2 = leaf + NW * SUPER;
                 if (nmask && l2 < c1) {
-                    mn_n = __ldg(meta4 + 2 * (uint64_t)l2);
-                    mx_n = __ldg(meta4 + 2 * (uint64_t)l2 + 1);
+                    mn_n = __ldg(meta8 + MW * (uint64_t)l2);
+                    mx_n = __ldg(meta8 + MW * (uint64_t)l2 + 1);
                 }
             }
             if (!cur_mask) continue;  // the whole super-node is pruned for every query
-            if (leaf < c1) bytes += 32;
+            const bool inr = leaf < c1;
+            if (inr) bytes += 32;
             uint32_t alive = 0;
-#pragma unroll
-            for (int g = 0; g < G; g++) {
-                if (!((cur_mask >> g) & 1u)) continue;
-                const bool ok = leaf < c1 && node_e8(lut8_sh + g * W * CARD, qsym[g][0], qsym[g][1], mn4, mx4) <= 254u;
-                if (ok) alive |= 1u << g;
+#pragma unroll 1
+            for (uint32_t mm = cur_mask; mm; mm &= mm - 1) {
+                const uint32_t g = __ffs(mm) - 1;
+                const bool ok = inr && node_e8(lut8_sh + g * W * CARD, qsym[g][0], qsym[g][1], mn4, mx4) <= 254u;
+                alive |= (ok ? 1u : 0u) << g;
                 // (leaf, query g) pairs that phase B will test, counted by lane g (stats)
                 const uint32_t np = __popc(__ballot_sync(FULL, ok));
                 if (lane == (uint32_t)g) my_alive += np;
@@ -566,29 +566,36 @@ __global__ void __launch_bounds__(LF_THREADS, 1) leafscan_kernel(
         // (lane = member). Each warp takes entries warp, warp + NW, ... and keeps PD of them in
         // flight in its own ring of shared staging slots (cp.async, one commit group per entry).
         // A lane copies and reads only its own word, so no warp barrier is needed. The sorted SAX
-        // array is padded to whole leaves (api.cu), so the loads need no bounds test.
+        // array is padded to whole leaves (api.cu), so the loads need no bounds test. Addresses are
+        // shared-window offsets (u32), the ring position a byte offset wrapped with a mask.
         const uint32_t nwl = wl_cnt;
         if (t == 0) bytes += nwl * LEAF * 16u;  // the worklist leaves' words (a partial last leaf is counted whole)
-        uint4 *ring = stage + warp * PD * LEAF + lane;  // [PD slots][LEAF] words; this lane's column
-        const uint4 *saxc = sax + (uint64_t)c0 * LEAF + lane;
-        auto prefetch = [&](uint32_t e, uint32_t slot) {
-            if (e < nwl) cp_async16(ring + slot * LEAF, saxc + (worklist[e] & 0xFFFFu) * LEAF, true);
-            cp_async_commit();
-        };
+        constexpr uint32_t SLOT = LEAF * 16;  // bytes of one staged leaf
+        const uint32_t ring = stage_sh + warp * PD * SLOT + lane * 16;
+        const char *gsrc = reinterpret_cast<const char *>(sax + (uint64_t)c0 * LEAF + lane);
+        uint32_t pf = warp, pfo = 0;  // next entry to prefetch, its ring offset
 #pragma unroll
-        for (uint32_t k = 0; k < PD - 1; k++) prefetch(warp + k * NW, k);
-        uint32_t slot = 0;
+        for (uint32_t k = 0; k < PD - 1; k++) {
+            if (pf < nwl) cp_async16_sh(ring + pfo, gsrc + (size_t)(ld_sh_u32a(wl_sh + 4 * pf) & 0xFFFFu) * SLOT);
+            cp_async_commit();
+            pf += NW;
+            pfo = (pfo + SLOT) & (PD * SLOT - 1);
+        }
+        uint32_t co = 0;  // ring offset of the entry being consumed
         for (uint32_t e = warp; e < nwl; e += NW) {
-            prefetch(e + (PD - 1) * NW, (slot + PD - 1) % PD);
+            if (pf < nwl) cp_async16_sh(ring + pfo, gsrc + (size_t)(ld_sh_u32a(wl_sh + 4 * pf) & 0xFFFFu) * SLOT);
+            cp_async_commit();
+            pf += NW;
+            pfo = (pfo + SLOT) & (PD * SLOT - 1);
             cp_async_wait<PD - 1>();
-            const uint32_t mask = worklist[e] >> 16;
-            const uint4 *wp = ring + slot * LEAF;
-            const uint4 wv = *wp;
-            slot = (slot + 1) % PD;
+            const uint32_t ent = ld_sh_u32a(wl_sh + 4 * e);
+            const uint32_t wp = ring + co;
+            const uint4 wv = ld_sh_v4a(wp);
+            co = (co + SLOT) & (PD * SLOT - 1);
             // rolled loop over the queries that kept the leaf: unrolling it over G made the
             // kernel ~120 KB of SASS, and instruction-cache misses became the top stall
 #pragma unroll 1
-            for (uint32_t mm = mask; mm; mm &= mm - 1) {
+            for (uint32_t mm = ent >> 16; mm; mm &= mm - 1) {
                 const uint32_t g = __ffs(mm) - 1;
                 // integer member filter: 16 lookups of 2.5 instructions (PRMT address, LDS.U8, half
                 // an IADD3)
@@ -601,8 +608,7 @@ __global__ void __launch_bounds__(LF_THREADS, 1) leafscan_kernel(
                 // bands every member gets it here. A first-band member's histogram bin comes from
                 // its u8 sum, never above its exact bin (band shrinking, R10, stays an upper bound
                 // on the count).
-                // the position, from the entry re-read here (volatile): only this rare path needs it
-                const uint32_t pos = (c0 + (ld_sh_u32(worklist + e) & 0xFFFFu)) * LEAF + lane;
+                const uint32_t pos = (c0 + (ent & 0xFFFFu)) * LEAF + lane;
                 const bool maybe = pos < N && e8 <= 254u;
                 const QConst kq = qc[g];
                 const bool band0 = kq.lo < 0.f;
@@ -610,7 +616,7 @@ __global__ void __launch_bounds__(LF_THREADS, 1) leafscan_kernel(
                 const bool check = maybe && !band0;
                 // the word is re-read here (volatile), so that the compiler does not hoist the fp32
                 // path's address arithmetic out of the query loop into every entry
-                const float lb = check ? word_lb(lut_all + (uint64_t)qid[g] * W * CARD, ld_sh_v4(wp)) : 0.f;
+                const float lb = check ? word_lb(lut_all + (uint64_t)qid[g] * W * CARD, ld_sh_v4a(wp)) : 0.f;
                 const bool keep = (first || (check && lb > kq.lo && lb <= kq.T)) && pos_ok(kq, pos);
                 // the candidate's u8 bound b <= LB^2 * sc (for the refine), or B_UNCHECKED
                 uint32_t b = e8 <= E_SURE ? e8 : B_UNCHECKED;
@@ -620,9 +626,10 @@ __global__ void __launch_bounds__(LF_THREADS, 1) leafscan_kernel(
                 }
                 if (keep)
                     atomicAdd(&shist[g][first ? min(e8 * HIST_BINS / 254u, HIST_BINS - 1) : hist_bin(lb, kq.lo, kq.T)], 1u);
-                emit(keep, pos, b, g, qid[g], lane, lt, cbuf, qbuf, cb_cnt, cand, candq, cand_cnt, cap);
+                emit(keep, pos, b, g, lane, lt, wbuf, wcnt, s_ovf, qid, cand, candq, cand_cnt, cap);
             }
         }
+        if (wcnt) wflush(wbuf, wcnt, lane, s_ovf, qid, cand, candq, cand_cnt, cap);  // (warp-uniform)
         cp_async_wait<0>();  // the trailing (empty) groups
         __syncthreads();
         if (t == 0) wl_cnt = 0;
@@ -635,8 +642,8 @@ __global__ void __launch_bounds__(LF_THREADS, 1) leafscan_kernel(
 template <int G>
 static void launch_leaf(const isax_index *ix, uint32_t nq, const uint32_t *qmap, cudaStream_t s) {
     constexpr uint32_t NW = LF_THREADS / 32;
-    const size_t smem = (size_t)G * W * CARD + 256 + (size_t)G * CBUF * sizeof(uint32_t) + CHUNK * 4 +
-                        (size_t)NW * PD * LEAF * sizeof(uint4) + (size_t)G * CBUF;
+    const size_t smem = (size_t)G * W * CARD + 256 + CHUNK * 4 + (size_t)NW * PD * LEAF * sizeof(uint4) +
+                        (size_t)NW * WB * sizeof(uint2);
     // per launch (the attribute is per device; a failure surfaces as the launch's error)
     cudaFuncSetAttribute(leafscan_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int dev = 0, sms = 148;
