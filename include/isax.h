@@ -57,10 +57,12 @@ typedef struct isax_opts {
     uint32_t probe_L;    /* rows per probe window: the kd cell of that many rows in the probe key's super-node
                             that the probe's symbols descend to (R6b). 0 = default 128. */
     float first_band;    /* best-first scan order (R15): round 0 scans only the smallest bounds,
-                            LB^2 <= first_band * bsf0^2 (1 + delta), refines them, and the next round scans the
-                            rest under the improved BSF. 0 = adaptive (default): fraction 1/50 or none, whichever
-                            the index measured to be faster per query (device time), the other re-timed every
-                            32 batches; in (0, 1) = always, that fraction; < 0 = never. Answers do not depend on it. */
+                            LB^2 <= first_band * bsf0^2 (1 + delta), refines them, and the next round scans
+                            the rest under the improved BSF; with window_L = 0 the main window is then one
+                            super-node. 0 = adaptive (default): fraction 1/50 or none, whichever the index
+                            measured to be faster per query (device time); the other mode is re-timed after
+                            8, 16, ... up to 512 batches while the choice holds. In (0, 1) = always, that
+                            fraction; < 0 = never. Answers do not depend on it. */
 } isax_opts;
 
 #define ISAX_PROBES_NONE 0xFFFFFFFFu

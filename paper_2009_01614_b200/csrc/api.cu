@@ -116,7 +116,7 @@ static void free_scratch(isax_index *ix) {
 // smallest-bounds-first rounds skip most of a heavy query's candidates (BASELINE config 5).
 constexpr uint64_t CAND_POOL = 1ull << 30;
 constexpr float FB_FRAC = 0.02f;      // R15: the adaptive first band's fraction of the window threshold
-constexpr uint32_t FB_REPROBE = 32;   // batches in the preferred mode before the other one is re-timed
+constexpr uint32_t FB_REPROBE = 512;  // longest run in the preferred mode before the other one is re-timed
 static int alloc_scratch_cap(isax_index *ix, uint32_t cap);
 static int alloc_scratch(isax_index *ix) {
     if (ix->qs.cap_Q) return ISAX_OK;
@@ -215,6 +215,8 @@ static int build_impl(const Source &src, uint64_t N, uint32_t n, uint32_t w, uin
     ISAX_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
     isax_index *ix = new isax_index();
     ix->N = N; ix->n = n; ix->w = w; ix->card = card; ix->opts = o; ix->device = dev;
+    ix->win_auto = !(opts && opts->window_L);
+    ix->win_L = o.window_L;
     uint8_t *sax_by_id = nullptr;
     uint4 *keys = nullptr;
     double2 *musig = nullptr;
@@ -411,10 +413,14 @@ static int nn1_device(isax_index *ix, const float *d_q, uint32_t Q, int64_t *d_i
             else if (ix->fb_ms_off < 0.f) on = false;
             else {
                 on = ix->fb_ms_on <= ix->fb_ms_off;
-                if (ix->fb_since >= FB_REPROBE) on = !on;
+                if (ix->fb_since >= ix->fb_every) on = !on;
             }
             band0 = on ? FB_FRAC : 0.f;
         }
+        // In best-first mode the approximate answer only seeds the first band's threshold, so the
+        // main window shrinks to the query key's super-node (plus its neighbours' kd quarters)
+        // unless the caller fixed window_L (R5, R15)
+        ix->win_L = (band0 > 0.f && ix->win_auto) ? std::min<uint32_t>(ix->opts.window_L, SUPER_SIZE) : ix->opts.window_L;
         const bool timed = b0 == 0;
         if (timed) {
             ix->st_fb_frac = band0;
@@ -606,10 +612,19 @@ static int nn1_device(isax_index *ix, const float *d_q, uint32_t Q, int64_t *d_i
             if (cudaEventElapsedTime(&ms, ix->ev[0], ix->ev[7]) == cudaSuccess) {
                 const float per = ms / (float)B;
                 float &slot = band0 > 0.f ? ix->fb_ms_on : ix->fb_ms_off;
-                const bool preferred = (band0 > 0.f) == (ix->fb_ms_on >= 0.f && ix->fb_ms_off >= 0.f &&
-                                                         ix->fb_ms_on <= ix->fb_ms_off);
+                const bool known = ix->fb_ms_on >= 0.f && ix->fb_ms_off >= 0.f;
+                const bool pref_on = ix->fb_ms_on <= ix->fb_ms_off;
+                const bool preferred = known && (band0 > 0.f) == pref_on;
                 slot = slot < 0.f ? per : 0.5f * (slot + per);
-                ix->fb_since = preferred ? ix->fb_since + 1 : 0;
+                if (preferred) {
+                    ix->fb_since++;
+                } else {  // a re-timing: back off if the choice holds, start over if it flipped
+                    ix->fb_since = 0;
+                    if (known) {
+                        const bool now_on = ix->fb_ms_on <= ix->fb_ms_off;
+                        ix->fb_every = now_on == pref_on ? std::min<uint32_t>(2 * ix->fb_every, FB_REPROBE) : 8;
+                    }
+                }
             } else {
                 cudaGetLastError();
             }
@@ -773,6 +788,7 @@ int isax_query_debug(const isax_index *cix, const float *queries, uint32_t Q, do
     if (e == cudaSuccess) e = cudaMalloc(&flag, sizeof(uint32_t));
     if (e == cudaSuccess) e = cudaMemsetAsync(flag, 0, sizeof(uint32_t), s);
     if (e == cudaSuccess) {
+        ix->win_L = ix->opts.window_L;  // (the window of a call without the first band)
         launch_qprep(ix, dq, Q, 0.f, s, flag);
         e = cudaGetLastError();
     }
@@ -828,7 +844,7 @@ int isax_stats(const isax_index *cix, char *buf, size_t cap) {
     snprintf(tmp, sizeof tmp,
              "\"N\":%llu,\"n\":%u,\"window_L\":%u,\"probe_windows\":%u,\"probe_L\":%u,\"slack_log2\":%d,\"batch_Q\":%u,\"cand_cap\":%u,"
              "\"ms_first_batch\":{\"qprep\":%.4f,\"window\":%.4f,\"lbscan\":%.4f,\"candcheck\":%.4f,\"refine\":%.4f,\"total\":%.4f},",
-             (unsigned long long)ix->N, ix->n, ix->opts.window_L, window_probes(ix), ix->opts.probe_L, ix->opts.slack_log2,
+             (unsigned long long)ix->N, ix->n, ix->win_L, window_probes(ix), ix->opts.probe_L, ix->opts.slack_log2,
              ix->opts.batch_Q, ix->qs.cand_cap, ix->st_ms.qprep, ix->st_ms.window, ix->st_ms.lbscan, ix->st_ms.candcheck, ix->st_ms.refine,
              ix->st_ms.finalize);
     j += tmp;
