@@ -230,9 +230,10 @@ def main():
     # ---- per-kernel times and counters: a separate pass of the same steps (stats() is host
     # work, kept out of the timed region). The library times its first batch with CUDA events
     # on the stream its kernels run on.
-    keys = ["lbscan", "candcheck", "refine", "window", "qprep"]
+    keys = ["lbscan", "candcheck", "refine", "refine1", "filter", "refine2", "window", "qprep"]
     kms = {k: [] for k in keys}
     cand, refined, abandoned, skipped, winrows, rounds, scan_b, ref_b, pairs, launches = [], [], [], [], [], [], [], [], [], 0
+    ref1_b, ref2_b = [], []
     for _ in range(args.steps):
         ids, dist_ = ix.nn1(q)
         st = ix.stats()
@@ -247,6 +248,8 @@ def main():
         launches += st.get("launches", 0)
         scan_b.append(st["scan_bytes_first_launch"])
         ref_b.append(st["refine_bytes_first_launch"])
+        ref1_b.append(st["refine1_bytes_first_launch"])
+        ref2_b.append(st["refine2_bytes_first_launch"])
         pairs.append(st["leaf_pairs_first_launch"])
     # ---- e2e through isax_nn1 with host (pinned) buffers, copies inside the timed region
     qh = torch.empty((Q, wl.n), dtype=torch.float32, pin_memory=True)
@@ -278,7 +281,7 @@ def main():
     lk_peak = 148 * 32 * sm_mhz * 1e6  # one conflict-free 32-lane LDS wavefront per clock per SM
     lk_rate = lookups / (lb_ms / 1e3)
     scan_bytes = statistics.mean(scan_b) + 4.0 * statistics.mean(cand) * nq1 / Q
-    traffic = None
+    traffic, tr = None, {}
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
             tr = json.load(f).get(wl.name, {})
@@ -295,6 +298,11 @@ def main():
                              "peak": hbm, "unit": "GB/s", "frac": round(scan_bytes / (lb_ms / 1e3) / 1e9 / hbm, 4),
                              "peak_source": peak_src}}
     rbytes = statistics.mean(ref_b)
+    r1b, r2b = statistics.mean(ref1_b), statistics.mean(ref2_b)
+    r1_ms, f_ms, r2_ms = (statistics.mean(kms[k]) for k in ("refine1", "filter", "refine2"))
+
+    def gbs(b, ms_):
+        return round(b / (ms_ / 1e3) / 1e9, 1) if ms_ > 0 else None
     # window: every row of the main window and of the kept probe windows is read once (4n B each);
     # the rows per query are the library's count (probe windows inside the main window or repeated
     # are dropped by qprep)
@@ -307,7 +315,15 @@ def main():
         "refine_q_kernel": {"bound": "hbm", "bytes_per_launch": rbytes, "launch_ms": round(rf_ms, 4),
                             "achieved": round(rbytes / (rf_ms / 1e3) / 1e9, 1), "peak": hbm, "unit": "GB/s",
                             "frac": round(rbytes / (rf_ms / 1e3) / 1e9 / hbm, 4),
-                            "bytes_rule": "2n B per half row read (n float32 per row), counted by the kernel"},
+                            "bytes_rule": "2n B per half row read (n float32 per row), counted by the kernel; "
+                                          "launch_ms spans pass 1, filter_kernel and pass 2 (R14)",
+                            "pass1": {"bytes": r1b, "ms": round(r1_ms, 4), "achieved": gbs(r1b, r1_ms),
+                                      "frac": round(gbs(r1b, r1_ms) / hbm, 4) if r1_ms > 0 else None},
+                            "filter_ms": round(f_ms, 4),
+                            "traffic": {"pass1": tr.get("refine_pass1_dram_bytes"), "pass2": tr.get("refine_pass2_dram_bytes"),
+                                        "source": "profiles/ncu_traffic.json (ncu dram read + write per launch)"},
+                            "pass2": {"bytes": r2b, "ms": round(r2_ms, 4), "achieved": gbs(r2b, r2_ms),
+                                      "frac": round(gbs(r2b, r2_ms) / hbm, 4) if r2_ms > 0 else None}},
         "window_kernel": {"bound": "hbm", "bytes_per_launch": wbytes, "launch_ms": round(wn_ms, 4),
                           "achieved": round(wbytes / (wn_ms / 1e3) / 1e9, 1), "peak": hbm, "unit": "GB/s",
                           "frac": round(wbytes / (wn_ms / 1e3) / 1e9 / hbm, 4),

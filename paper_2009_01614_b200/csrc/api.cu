@@ -382,7 +382,7 @@ static int nn1_device(isax_index *ix, const float *d_q, uint32_t Q, int64_t *d_i
     ix->st_ms = StageTimes{};
     ix->st_launches = 0;
     ix->st_scan_bytes = ix->st_scan_bytes_first = 0;
-    ix->st_refine_bytes_first = 0;
+    ix->st_refine_bytes_first = ix->st_refine1_bytes_first = ix->st_refine2_bytes_first = 0;
     ISAX_CUDA(cudaMemsetAsync(qs.scan_bytes_dev, 0, StatusBlock::RESET_BYTES, s));  // + refine_bytes, flag
     int result = ISAX_OK;
     for (uint32_t b0 = 0; b0 < Q && result == ISAX_OK; b0 += qs.cap_Q) {
@@ -489,7 +489,7 @@ static int nn1_device(isax_index *ix, const float *d_q, uint32_t Q, int64_t *d_i
             if (timed && round == 0) cudaEventRecord(ix->ev[6], s);
             launch_candcheck(ix, B, s);
             if (timed && round == 0) cudaEventRecord(ix->ev[3], s);
-            launch_refine(ix, B, delta, s);
+            launch_refine(ix, B, delta, s, (timed && round == 0) ? &ix->ev[8] : nullptr);
             if (timed && round == 0) cudaEventRecord(ix->ev[4], s);
             // speculative: a query scanned again in a later round is finalised again
             launch_finalize(ix, nact, qs.qmap, delta, d_id + b0, d_dist + b0, s);
@@ -522,7 +522,9 @@ static int nn1_device(isax_index *ix, const float *d_q, uint32_t Q, int64_t *d_i
                 }
                 if (b0 == 0) {
                     ix->st_scan_bytes_first = ix->st_scan_bytes + *hm.scan_bytes_dev;
-                    ix->st_refine_bytes_first = *hm.refine_bytes;
+                    ix->st_refine1_bytes_first = hm.refine_bytes[0];
+                    ix->st_refine2_bytes_first = hm.refine_bytes[1];
+                    ix->st_refine_bytes_first = hm.refine_bytes[0] + hm.refine_bytes[1];
                     ix->st_leaf_pairs_first = 0;
                     for (uint32_t i = 0; i < B; i++) ix->st_leaf_pairs_first += hm.leaves[i];
                     ix->st_scan_q_first = nact;
@@ -647,6 +649,9 @@ static int nn1_device(isax_index *ix, const float *d_q, uint32_t Q, int64_t *d_i
             cudaEventElapsedTime(&ix->st_ms.lbscan, ix->ev[2], ix->ev[6]);
             cudaEventElapsedTime(&ix->st_ms.candcheck, ix->ev[6], ix->ev[3]);
             cudaEventElapsedTime(&ix->st_ms.refine, ix->ev[3], ix->ev[4]);
+            cudaEventElapsedTime(&ix->st_ms.refine1, ix->ev[3], ix->ev[8]);
+            cudaEventElapsedTime(&ix->st_ms.filter, ix->ev[8], ix->ev[9]);
+            cudaEventElapsedTime(&ix->st_ms.refine2, ix->ev[9], ix->ev[4]);
             float tot = 0;
             cudaEventElapsedTime(&tot, ix->ev[0], ix->ev[5]);
             ix->st_ms.finalize = tot;  // whole first round of the first batch
@@ -840,13 +845,14 @@ int isax_stats(const isax_index *cix, char *buf, size_t cap) {
     isax_index *ix = const_cast<isax_index *>(cix);
     std::lock_guard<std::mutex> lk(ix->mu);
     std::string j = "{";
-    char tmp[256];
+    char tmp[640];
     snprintf(tmp, sizeof tmp,
              "\"N\":%llu,\"n\":%u,\"window_L\":%u,\"probe_windows\":%u,\"probe_L\":%u,\"slack_log2\":%d,\"batch_Q\":%u,\"cand_cap\":%u,"
-             "\"ms_first_batch\":{\"qprep\":%.4f,\"window\":%.4f,\"lbscan\":%.4f,\"candcheck\":%.4f,\"refine\":%.4f,\"total\":%.4f},",
+             "\"ms_first_batch\":{\"qprep\":%.4f,\"window\":%.4f,\"lbscan\":%.4f,\"candcheck\":%.4f,\"refine\":%.4f,"
+             "\"refine1\":%.4f,\"filter\":%.4f,\"refine2\":%.4f,\"total\":%.4f},",
              (unsigned long long)ix->N, ix->n, ix->win_L, window_probes(ix), ix->opts.probe_L, ix->opts.slack_log2,
              ix->opts.batch_Q, ix->qs.cand_cap, ix->st_ms.qprep, ix->st_ms.window, ix->st_ms.lbscan, ix->st_ms.candcheck, ix->st_ms.refine,
-             ix->st_ms.finalize);
+             ix->st_ms.refine1, ix->st_ms.filter, ix->st_ms.refine2, ix->st_ms.finalize);
     j += tmp;
     auto arr = [&](const char *name, const std::vector<uint32_t> &v, bool last) {
         j += "\"";
@@ -890,6 +896,8 @@ int isax_stats(const isax_index *cix, char *buf, size_t cap) {
     j += ",\"scan_bytes\":" + std::to_string(ix->st_scan_bytes);
     j += ",\"scan_bytes_first_launch\":" + std::to_string(ix->st_scan_bytes_first);
     j += ",\"refine_bytes_first_launch\":" + std::to_string(ix->st_refine_bytes_first);
+    j += ",\"refine1_bytes_first_launch\":" + std::to_string(ix->st_refine1_bytes_first);
+    j += ",\"refine2_bytes_first_launch\":" + std::to_string(ix->st_refine2_bytes_first);
     j += ",\"leaf_pairs_first_launch\":" + std::to_string(ix->st_leaf_pairs_first);
     j += ",\"scan_queries_first_launch\":" + std::to_string(ix->st_scan_q_first);
     j += ",\"leaves\":" + std::to_string((ix->N + LEAF_SIZE - 1) / LEAF_SIZE);

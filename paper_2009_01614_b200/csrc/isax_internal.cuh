@@ -88,7 +88,7 @@ struct StatusBlock {
         bsf = reinterpret_cast<unsigned long long *>(take(8ull * Q));
         bsf_scan = reinterpret_cast<unsigned long long *>(take(8ull * Q));
         scan_bytes_dev = reinterpret_cast<unsigned long long *>(take(8));  // these three are zeroed
-        refine_bytes = reinterpret_cast<unsigned long long *>(take(8));    // together: RESET_BYTES
+        refine_bytes = reinterpret_cast<unsigned long long *>(take(16));   // together: RESET_BYTES (2 passes)
         flag = reinterpret_cast<uint32_t *>(take(4));
         cand_cnt = reinterpret_cast<uint32_t *>(take(4ull * Q));
         cand_cnt2 = reinterpret_cast<uint32_t *>(take(4ull * Q));
@@ -161,7 +161,7 @@ struct QueryScratch {
     uint32_t *counters_leaf = nullptr;  // [Q]: (leaf, query) pairs that survived the node bound
     unsigned long long *scan_bytes_dev = nullptr;  // leaf words and leaf summaries the leaf scan read, bytes (all launches of a call)
     uint32_t *task_ctr = nullptr;              // work counter of the persistent leaf scan
-    unsigned long long *refine_bytes = nullptr;  // bytes of rows the refine kernel read (all launches of a call)
+    unsigned long long *refine_bytes = nullptr;  // [2] bytes of rows the refine passes 1 and 2 read (all launches of a call)
     uint32_t *flag = nullptr;       // non-finite query flag
     void *status = nullptr;         // the device StatusBlock (bsf, bsf_scan, counters, ... point into it)
     unsigned long long *bsf_scan = nullptr;  // [Q] the BSF each query's last scan used (the window BSF in round 0)
@@ -172,6 +172,7 @@ struct QueryScratch {
 
 struct StageTimes {
     float qprep = 0, window = 0, lbscan = 0, candcheck = 0, refine = 0, finalize = 0;
+    float refine1 = 0, filter = 0, refine2 = 0;  // the refine's two passes and the filter between them (R14)
 };
 
 }  // namespace isax
@@ -209,9 +210,10 @@ struct isax_index {
     float st_fb_frac = 0.f;      // first-band fraction of the last call's first batch (0 = none)
     uint32_t st_fb_improved = 0; // its queries whose BSF the first band at least halved (stats)
     uint64_t st_scan_bytes = 0, st_scan_bytes_first = 0;  // summary bytes the scan read (all / first launch)
-    uint64_t st_refine_bytes_first = 0;                    // row bytes the first refine launch read
+    uint64_t st_refine_bytes_first = 0;                    // row bytes the first round's refine read (both passes)
+    uint64_t st_refine1_bytes_first = 0, st_refine2_bytes_first = 0;  // ... per pass
     uint64_t st_leaf_pairs_first = 0, st_scan_q_first = 0; // (leaf, query) pairs kept / queries of the first scan
-    cudaEvent_t ev[8] = {};
+    cudaEvent_t ev[11] = {};
     // isax_nn1 (host pointers): one stream and device staging, grown on demand
     cudaStream_t io_stream = nullptr;
     float *io_q = nullptr;
@@ -273,7 +275,8 @@ uint64_t launch_lbscan(const isax_index *ix, uint32_t nq, uint32_t B, const uint
 // and compaction of every list into cand2 / cand_cnt2 (the refine's input)
 void launch_candcheck(const isax_index *ix, uint32_t Q, cudaStream_t s);
 // refine.cu
-void launch_refine(const isax_index *ix, uint32_t Q, float delta, cudaStream_t s);
+// evs (NULL or 2 events): recorded after pass 1 and after the filter (stage timing)
+void launch_refine(const isax_index *ix, uint32_t Q, float delta, cudaStream_t s, cudaEvent_t *evs);
 // finalise the nq queries qmap[0 .. nq) (the ones the round scanned): exact near-tie resolution (R9)
 void launch_finalize(const isax_index *ix, uint32_t nq, const uint32_t *qmap, float delta, int64_t *out_id, float *out_dist,
                      cudaStream_t s);

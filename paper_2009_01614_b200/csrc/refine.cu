@@ -350,7 +350,7 @@ __global__ void __launch_bounds__(RF_THREADS) filter_kernel(const uint32_t *__re
     }
 }
 
-void launch_refine(const isax_index *ix, uint32_t Q, float delta, cudaStream_t s) {
+void launch_refine(const isax_index *ix, uint32_t Q, float delta, cudaStream_t s, cudaEvent_t *evs) {
     const QueryScratch &qs = ix->qs;
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
@@ -358,7 +358,7 @@ void launch_refine(const isax_index *ix, uint32_t Q, float delta, cudaStream_t s
     const float onepd = 1.0f + delta;
     const NearList nl{qs.near, qs.near_off, qs.near_cap, qs.near_cnt};
     // pass 1: cand2[q][0 .. cand_cnt2); then the filtered second band into cand[q][0 .. cnt_f)
-    auto pass = [&](const uint32_t *list, const uint32_t *cnt) {
+    auto pass = [&](const uint32_t *list, const uint32_t *cnt, unsigned long long *bytes) {
         if (ix->n <= 256) {
             int per_sm = 1;
             const uint32_t nh = ix->n / 64;
@@ -371,7 +371,7 @@ void launch_refine(const isax_index *ix, uint32_t Q, float delta, cudaStream_t s
     case K:                                                                                                         \
         refine_q_kernel<K><<<grid, RF_THREADS, 0, s>>>(ix->stored, ix->perm, ix->n, qs.qy, Q, list, nullptr, nullptr, \
                                                        cnt, qs.cand_cap, qs.bsf, nl, qs.counters,                   \
-                                                       onepd, qs.refine_bytes);                                     \
+                                                       onepd, bytes);                                               \
         break;
                 RQ_CASE(1) RQ_CASE(2) RQ_CASE(3) RQ_CASE(4)
 #undef RQ_CASE
@@ -390,10 +390,12 @@ void launch_refine(const isax_index *ix, uint32_t Q, float delta, cudaStream_t s
         }
 #undef RF_CASE
     };
-    pass(qs.cand2, qs.cand_cnt2);
+    pass(qs.cand2, qs.cand_cnt2, qs.refine_bytes);
+    if (evs) cudaEventRecord(evs[0], s);
     filter_kernel<<<sms * 4, RF_THREADS, 0, s>>>(qs.cand2, qs.candq2, qs.cnt_hi, Q, qs.cand_cap, qs.bsf, qs.qscale,
                                                  onepd, qs.cand, qs.cnt_f, qs.counters);
-    pass(qs.cand, qs.cnt_f);
+    if (evs) cudaEventRecord(evs[1], s);
+    pass(qs.cand, qs.cnt_f, qs.refine_bytes + 1);
 }
 
 // ------------------------------------------------------------------------------------ finalize
