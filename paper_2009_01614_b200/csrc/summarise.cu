@@ -249,6 +249,150 @@ __global__ void __launch_bounds__(32) summarise_half_kernel(const float *__restr
     }
 }
 
+// Split summarisation for n = 128 and 256: two kernels with no shared-memory staging.
+//  moments_kernel: thread per series (mu, sigma: two sequential fp64 chains over the row, read
+//    with float4 loads through L1; registers only, so many series are in flight per SM).
+//  paa_sax_kernel: a half-warp per series, lane = segment: the lane z-normalises its n/w points
+//    (znorm_value, the exact rounding of R3), sums them left to right in fp64 and takes the symbol;
+//    the key's bit planes are warp ballots. The per-series operation order is that of
+//    summarise_kernel (and of the oracle): identical words.
+template <uint32_t NT>
+__global__ void __launch_bounds__(256) moments_kernel(const float *__restrict__ x, uint64_t count,
+                                                      double2 *__restrict__ ms_out, uint32_t *__restrict__ bad) {
+    constexpr uint32_t C = NT / 4, U = 8;  // float4 per row; per group (two groups in flight)
+    static_assert(C % (2 * U) == 0, "whole groups");
+    for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < count; r += (uint64_t)gridDim.x * blockDim.x) {
+        const float4 *row = reinterpret_cast<const float4 *>(x + r * NT);
+        bool finite = true;
+        // C1, left to right (R2, R3); the next group's loads are issued before this group's adds
+        double s = 0.0;
+        float4 a[U], b[U];
+#pragma unroll
+        for (uint32_t k = 0; k < U; k++) a[k] = __ldg(row + k);
+#pragma unroll 1
+        for (uint32_t c0 = 0; c0 < C; c0 += 2 * U) {
+#pragma unroll
+            for (uint32_t k = 0; k < U; k++) b[k] = __ldg(row + c0 + U + k);
+#pragma unroll
+            for (uint32_t k = 0; k < U; k++) {
+                finite &= isfinite(a[k].x) && isfinite(a[k].y) && isfinite(a[k].z) && isfinite(a[k].w);
+                s = __dadd_rn(s, (double)(a[k].x));
+                s = __dadd_rn(s, (double)(a[k].y));
+                s = __dadd_rn(s, (double)(a[k].z));
+                s = __dadd_rn(s, (double)(a[k].w));
+            }
+            if (c0 + 2 * U < C) {
+#pragma unroll
+                for (uint32_t k = 0; k < U; k++) a[k] = __ldg(row + c0 + 2 * U + k);
+            }
+#pragma unroll
+            for (uint32_t k = 0; k < U; k++) {
+                finite &= isfinite(b[k].x) && isfinite(b[k].y) && isfinite(b[k].z) && isfinite(b[k].w);
+                s = __dadd_rn(s, (double)(b[k].x));
+                s = __dadd_rn(s, (double)(b[k].y));
+                s = __dadd_rn(s, (double)(b[k].z));
+                s = __dadd_rn(s, (double)(b[k].w));
+            }
+        }
+        const double mu = __ddiv_rn(s, (double)NT);
+        double s2 = 0.0;
+#pragma unroll
+        for (uint32_t k = 0; k < U; k++) a[k] = __ldg(row + k);
+#pragma unroll 1
+        for (uint32_t c0 = 0; c0 < C; c0 += 2 * U) {
+#pragma unroll
+            for (uint32_t k = 0; k < U; k++) b[k] = __ldg(row + c0 + U + k);
+#pragma unroll
+            for (uint32_t k = 0; k < U; k++) {
+                double t;
+                t = __dsub_rn((double)(a[k].x), mu); s2 = __dadd_rn(s2, __dmul_rn(t, t));
+                t = __dsub_rn((double)(a[k].y), mu); s2 = __dadd_rn(s2, __dmul_rn(t, t));
+                t = __dsub_rn((double)(a[k].z), mu); s2 = __dadd_rn(s2, __dmul_rn(t, t));
+                t = __dsub_rn((double)(a[k].w), mu); s2 = __dadd_rn(s2, __dmul_rn(t, t));
+            }
+            if (c0 + 2 * U < C) {
+#pragma unroll
+                for (uint32_t k = 0; k < U; k++) a[k] = __ldg(row + c0 + 2 * U + k);
+            }
+#pragma unroll
+            for (uint32_t k = 0; k < U; k++) {
+                double t;
+                t = __dsub_rn((double)(b[k].x), mu); s2 = __dadd_rn(s2, __dmul_rn(t, t));
+                t = __dsub_rn((double)(b[k].y), mu); s2 = __dadd_rn(s2, __dmul_rn(t, t));
+                t = __dsub_rn((double)(b[k].z), mu); s2 = __dadd_rn(s2, __dmul_rn(t, t));
+                t = __dsub_rn((double)(b[k].w), mu); s2 = __dadd_rn(s2, __dmul_rn(t, t));
+            }
+        }
+        ms_out[r] = make_double2(mu, __dsqrt_rn(__ddiv_rn(s2, (double)NT)));
+        if (!finite) atomicOr(bad, 1u);
+    }
+}
+
+template <uint32_t NT>
+__global__ void __launch_bounds__(256) paa_sax_kernel(const float *__restrict__ x, uint64_t count, uint64_t id0,
+                                                      const double2 *__restrict__ musig, uint8_t *__restrict__ sax_by_id,
+                                                      uint4 *__restrict__ key) {
+    constexpr uint32_t seg = NT / W;
+    __shared__ double beta[ISAX_NBETA];
+    for (uint32_t k = threadIdx.x; k < ISAX_NBETA; k += blockDim.x) beta[k] = c_beta[k];
+    __syncthreads();
+    const uint32_t lane = threadIdx.x & 31, sg = lane & 15;
+    const uint64_t hw0 = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 4;  // half-warp = one series
+    const uint64_t nhw = ((uint64_t)gridDim.x * blockDim.x) >> 4;
+    for (uint64_t r0 = hw0 - (hw0 & 1); r0 < count; r0 += nhw) {  // warp-uniform: two series per warp
+        const uint64_t r = r0 + (lane >> 4);
+        const bool live = r < count;
+        uint32_t sym = 0;
+        if (live) {
+            const double2 m = musig[id0 + r];
+            const double rcp = __drcp_rn(m.y);
+            const float4 *src = reinterpret_cast<const float4 *>(x + r * NT + sg * seg);
+            double acc = 0.0;
+#pragma unroll
+            for (uint32_t c = 0; c < seg / 4; c++) {
+                const float4 v = __ldg(src + c);
+                const float y0 = m.y < 1e-12 ? 0.0f : znorm_value(v.x, m.x, m.y, rcp);
+                const float y1 = m.y < 1e-12 ? 0.0f : znorm_value(v.y, m.x, m.y, rcp);
+                const float y2 = m.y < 1e-12 ? 0.0f : znorm_value(v.z, m.x, m.y, rcp);
+                const float y3 = m.y < 1e-12 ? 0.0f : znorm_value(v.w, m.x, m.y, rcp);
+                acc = __dadd_rn(acc, (double)y0);
+                acc = __dadd_rn(acc, (double)y1);
+                acc = __dadd_rn(acc, (double)y2);
+                acc = __dadd_rn(acc, (double)y3);
+            }
+            sym = sax_symbol(beta, __ddiv_rn(acc, (double)seg));
+            sax_by_id[(id0 + r) * W + sg] = (uint8_t)sym;
+        }
+        // key (R6): plane p holds bit (7 - p) of every segment's symbol, segment 0 most significant
+        uint32_t plane[8];
+#pragma unroll
+        for (int p = 0; p < 8; p++) {
+            const uint32_t b = __ballot_sync(0xffffffffu, (sym >> (7 - p)) & 1u);
+            plane[p] = __brev((lane < 16 ? b : (b >> 16)) & 0xFFFFu) >> 16;
+        }
+        if (live && sg == 0)
+            key[id0 + r] = make_uint4((plane[6] << 16) | plane[7], (plane[4] << 16) | plane[5], (plane[2] << 16) | plane[3],
+                                      (plane[0] << 16) | plane[1]);
+    }
+}
+
+template <uint32_t NT>
+static void launch_summarise_split(const float *x, uint64_t count, uint64_t id0, uint8_t *sax_by_id, uint4 *key,
+                                   double2 *musig, uint32_t *bad, cudaStream_t s) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    // few series in flight (ISAX_MOM_CTAS CTAs of 256 per SM): the rows being read (1 KB each at
+    // n = 256) stay in L2 between the mean and the variance passes
+#ifndef ISAX_MOM_CTAS
+#define ISAX_MOM_CTAS 2
+#endif
+    const uint64_t ga = umin64((count + 255) / 256, (uint64_t)sms * ISAX_MOM_CTAS);
+    moments_kernel<NT><<<(unsigned)ga, 256, 0, s>>>(x, count, musig + id0, bad);
+    const uint64_t gb = umin64((count * 16 + 255) / 256, (uint64_t)sms * 8);
+    paa_sax_kernel<NT><<<(unsigned)gb, 256, 0, s>>>(x, count, id0, musig, sax_by_id, key);
+}
+
 template <uint32_t NT>
 static void launch_summarise_half(const float *x, uint64_t count, uint64_t id0, uint8_t *sax_by_id, uint4 *key,
                                   double2 *musig, uint32_t *bad, cudaStream_t s) {
@@ -287,9 +431,12 @@ static void launch_summarise_t(const float *x, uint64_t count, uint32_t n, uint6
 void launch_summarise(const float *x, uint64_t count, uint32_t n, uint64_t id0, uint8_t *sax_by_id, uint4 *key,
                       double2 *musig, uint32_t *bad, cudaStream_t s) {
     if (count == 0) return;
-#ifndef ISAX_SUMMARISE_FULLROW
+#if defined(ISAX_SUMMARISE_HALF)
     if (n == 256) return launch_summarise_half<256>(x, count, id0, sax_by_id, key, musig, bad, s);
     if (n == 128) return launch_summarise_half<128>(x, count, id0, sax_by_id, key, musig, bad, s);
+#elif !defined(ISAX_SUMMARISE_FULLROW)
+    if (n == 256) return launch_summarise_split<256>(x, count, id0, sax_by_id, key, musig, bad, s);
+    if (n == 128) return launch_summarise_split<128>(x, count, id0, sax_by_id, key, musig, bad, s);
 #endif
     if (n == 256) launch_summarise_t<256>(x, count, n, id0, sax_by_id, key, musig, bad, s);
     else if (n == 128) launch_summarise_t<128>(x, count, n, id0, sax_by_id, key, musig, bad, s);
