@@ -61,7 +61,7 @@ typedef struct isax_opts {
                             the rest under the improved BSF; with window_L = 0 the main window is then one
                             super-node. 0 = adaptive (default): fraction 1/50 or none, whichever the index
                             measured to be faster per query (device time); the other mode is re-timed after
-                            8, 16, ... up to 512 batches while the choice holds. In (0, 1) = always, that
+                            32, 64, ... up to 512 batches while the choice holds. In (0, 1) = always, that
                             fraction; < 0 = never. Answers do not depend on it. */
 } isax_opts;
 

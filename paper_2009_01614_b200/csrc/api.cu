@@ -624,7 +624,7 @@ static int nn1_device(isax_index *ix, const float *d_q, uint32_t Q, int64_t *d_i
                     ix->fb_since = 0;
                     if (known) {
                         const bool now_on = ix->fb_ms_on <= ix->fb_ms_off;
-                        ix->fb_every = now_on == pref_on ? std::min<uint32_t>(2 * ix->fb_every, FB_REPROBE) : 8;
+                        ix->fb_every = now_on == pref_on ? std::min<uint32_t>(2 * ix->fb_every, FB_REPROBE) : 32;
                     }
                 }
             } else {

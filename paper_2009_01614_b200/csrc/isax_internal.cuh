@@ -206,7 +206,7 @@ struct isax_index {
     bool win_auto = true;       // window_L left to the library (opts.window_L == 0)
     uint32_t win_L = 3072;      // main window rows of the current batch (R5; 1024 in best-first mode when auto)
     uint32_t fb_since = 0;       // batches since the other mode was last measured
-    uint32_t fb_every = 8;       // re-time the other mode after this many batches (doubles while the choice holds)
+    uint32_t fb_every = 32;      // re-time the other mode after this many batches (doubles while the choice holds)
     float st_fb_frac = 0.f;      // first-band fraction of the last call's first batch (0 = none)
     uint32_t st_fb_improved = 0; // its queries whose BSF the first band at least halved (stats)
     uint64_t st_scan_bytes = 0, st_scan_bytes_first = 0;  // summary bytes the scan read (all / first launch)
