@@ -144,6 +144,17 @@ int isax_query_debug(const isax_index *ix, const float *queries, uint32_t Q, dou
  * one scan round (an overflowed list: the round's candidates are not kept). */
 int isax_debug_candidates(const isax_index *ix, uint32_t q, uint32_t *out_pos, uint64_t cap, uint64_t *count);
 
+/* Debug / test entry (host only, no device): one step of the per-query plan of scan rounds
+ * (R9, R10; csrc/round_plan.h). In/out: band_lo_hi = the band (lo, hi] of LB^2, band_pos = its
+ * sorted-position range [plo, phi), state = {length of the next position range, consecutive
+ * first-bin overflows}. In: the round's candidate count and list capacity, its 64-bin histogram of
+ * kept LB^2 over [max(lo, 0), tused], whether the near list overflowed, tused = the threshold the
+ * round used, bsf_lim = bsf^2 (1 + delta) now, N. Returns 0 = no more rounds, 1 = scan the
+ * updated band again, 2 = near-list overflow (grow the list, start over), -1 = overflow at a
+ * single position. */
+int isax_debug_plan_round(float *band_lo_hi, uint32_t *band_pos, uint32_t *state, uint32_t cand_cnt, uint32_t cap,
+                          const uint32_t *hist, int near_ovf, float tused, float bsf_lim, uint32_t N);
+
 /* Counters of the last isax_nn1 / isax_nn1_async call, as a JSON object written to buf.
  * It holds per-query window, window_rows (rows the approximate answer refined), candidates,
  * refined, abandoned, skipped, rounds, near, leaves_alive and the BSF before and after the scan,

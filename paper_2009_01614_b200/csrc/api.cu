@@ -12,6 +12,7 @@
 #include <string>
 
 #include "isax_internal.cuh"
+#include "round_plan.h"
 
 namespace isax {
 
@@ -543,65 +544,20 @@ static int nn1_device(isax_index *ix, const float *d_q, uint32_t Q, int64_t *d_i
                 bsf_h[i] = bsf_d2_host(hm.bsf[i]);
                 ix->st_cand[b0 + i] += hm.cand_cnt2[i] + hm.cnt_hi[i];  // after the exact rule (candcheck_kernel)
                 ix->st_rounds[b0 + i] = round + 1;
-                Band &bd = band[i];
-                if (cnt <= qs.cand_cap) nfirst[i] = 0;
-                if (hm.near_cnt[i] > hm.near_cap[i]) {  // near overflow: grow the list, start over, BSF kept
+                RoundState st{band[i], plen[i], nfirst[i]};
+                const bool near_ovf = hm.near_cnt[i] > hm.near_cap[i];
+                const int act = plan_next_round(st, cnt, qs.cand_cap, hm.hist + (size_t)i * HIST_BINS, near_ovf, tused[i],
+                                                bsf_h[i] * onepd, NP);
+                band[i] = st.band;
+                plen[i] = st.plen;
+                nfirst[i] = st.nfirst;
+                if (act == PLAN_ERROR) return set_error(ISAX_E_CUDA, "candidate list overflow at a single position");
+                if (act == PLAN_RESCAN) {  // near overflow: grow the list, start over, BSF kept (R9)
                     if ((rc = grow_near(ix, i, hm.near_cnt[i], s))) return rc;
                     offs_dirty = true;
-                    bd = Band{-1.0f, INF, 0u, NP};
-                    plen[i] = NP;
-                    pending[i] = 1;
                     rewin.push_back(i);
-                } else if (cnt > qs.cand_cap) {
-                    // shrink the band to the histogram prefix that fits
-                    const float lo0 = std::fmax(bd.lo, 0.0f), span = tused[i] - lo0;
-                    uint64_t cum = 0;
-                    int kk = -1;
-                    for (uint32_t bb = 0; bb < HIST_BINS; bb++) {
-                        cum += hm.hist[(size_t)i * HIST_BINS + bb];
-                        if (cum > (uint64_t)qs.cand_cap * 9 / 10) break;
-                        kk = (int)bb;
-                    }
-                    const float hi_new = kk < 0 ? lo0 + span / (float)HIST_BINS : lo0 + span * (float)(kk + 1) / (float)HIST_BINS;
-                    // The histogram cannot split the band when its first bin alone overflows for the
-                    // third time in a row (many bounds at one value: a bin never gets below it), when
-                    // the band is narrower than 2^-16 of its bounds (or empty: all bounds equal), or
-                    // when the shrunk edge rounds onto the lower one. Then this band is scanned over
-                    // parts of the sorted positions instead.
-                    nfirst[i] = kk < 0 ? nfirst[i] + 1 : 0;
-                    const bool stuck = (kk < 0 && (nfirst[i] >= 3 || !(span > std::fmax(lo0, tused[i]) * 1.52587890625e-05f))) ||
-                                       !(hi_new > lo0);
-                    if (stuck || bd.phi - bd.plo < NP) {
-                        const uint32_t len = bd.phi - bd.plo;
-                        if (len <= 1) return set_error(ISAX_E_CUDA, "candidate list overflow at a single position");
-                        bd.phi = bd.plo + len / 2;
-                        plen[i] = len / 2;
-                    } else {
-                        bd.hi = hi_new;
-                    }
-                    pending[i] = 1;
-                } else if (bd.phi < NP || bd.plo > 0) {
-                    // a position range of a split band completed: the next one, twice as long
-                    if (bd.phi < NP) {
-                        const uint64_t len = std::min<uint64_t>(2ull * plen[i], NP);
-                        plen[i] = (uint32_t)len;
-                        bd.plo = bd.phi;
-                        bd.phi = (uint32_t)std::min<uint64_t>((uint64_t)bd.plo + len, NP);
-                        pending[i] = 1;
-                    } else {  // the band is complete over all positions: continue with the next band
-                        bd.plo = 0;
-                        bd.phi = NP;
-                        plen[i] = NP;
-                        if (tused[i] == bd.hi && bsf_h[i] * onepd > bd.hi) {
-                            bd = Band{bd.hi, INF, 0u, NP};
-                            pending[i] = 1;
-                        }
-                    }
-                } else if (tused[i] == bd.hi && bsf_h[i] * onepd > bd.hi) {
-                    // the band was capped below the BSF: continue with the next band
-                    bd = Band{bd.hi, INF, 0u, NP};
-                    pending[i] = 1;
                 }
+                pending[i] = act != PLAN_DONE;
             }
             if (round > 100000) {
                 result = set_error(ISAX_E_CUDA, "candidate rounds did not converge");
@@ -838,6 +794,20 @@ int isax_debug_candidates(const isax_index *cix, uint32_t q, uint32_t *out_pos, 
         e = cudaMemcpy(out_pos + n1, qs.cand2 + (uint64_t)q * qs.cand_cap + (qs.cand_cap - n2), n2 * sizeof(uint32_t),
                        cudaMemcpyDefault);
     return e == cudaSuccess ? ISAX_OK : cuda_error(e, "isax_debug_candidates");
+}
+
+int isax_debug_plan_round(float *band_lo_hi, uint32_t *band_pos, uint32_t *state, uint32_t cand_cnt, uint32_t cap,
+                          const uint32_t *hist, int near_ovf, float tused, float bsf_lim, uint32_t N) {
+    if (!band_lo_hi || !band_pos || !state || !hist) return set_error(ISAX_E_INVAL, "NULL pointer");
+    RoundState st{Band{band_lo_hi[0], band_lo_hi[1], band_pos[0], band_pos[1]}, state[0], state[1]};
+    const int act = plan_next_round(st, cand_cnt, cap, hist, near_ovf != 0, tused, bsf_lim, N);
+    band_lo_hi[0] = st.band.lo;
+    band_lo_hi[1] = st.band.hi;
+    band_pos[0] = st.band.plo;
+    band_pos[1] = st.band.phi;
+    state[0] = st.plen;
+    state[1] = st.nfirst;
+    return act;
 }
 
 int isax_stats(const isax_index *cix, char *buf, size_t cap) {

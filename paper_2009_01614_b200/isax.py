@@ -48,6 +48,8 @@ isax_export = _sig("isax_export", [_P, _U64, _U64, _P, _P, _P])
 isax_query_debug = _sig("isax_query_debug", [_P, _P, _U32, _P, _P, _P, _U64, _U64, _P, _P])
 isax_debug_candidates = _sig("isax_debug_candidates", [_P, _U32, _P, _U64, ctypes.POINTER(_U64)])
 isax_stats = _sig("isax_stats", [_P, ctypes.c_char_p, ctypes.c_size_t])
+isax_debug_plan_round = _sig("isax_debug_plan_round", [_P, _P, _P, _U32, _U32, _P, ctypes.c_int, ctypes.c_float,
+                                                       ctypes.c_float, _U32])
 isax_info = _sig("isax_info", [_P, ctypes.POINTER(_U64), ctypes.POINTER(_U32), ctypes.POINTER(_U32),
                                ctypes.POINTER(_U32), ctypes.POINTER(_U64)])
 isax_free = _sig("isax_free", [_P], None)
@@ -236,6 +238,22 @@ class Index:
 
     def __exit__(self, *a):
         self.close()
+
+
+PLAN_DONE, PLAN_AGAIN, PLAN_RESCAN, PLAN_ERROR = 0, 1, 2, -1
+
+
+def plan_round(band, pos, state, cand_cnt: int, cap: int, hist, near_ovf: bool, tused: float, bsf_lim: float, N: int):
+    """One step of the per-query round plan (isax_debug_plan_round; host logic, no device).
+
+    band: float32[2] (lo, hi], pos: uint32[2] [plo, phi), state: uint32[2] (next range length,
+    first-bin overflows), all updated in place; hist: uint32[64]. Returns the action code."""
+    for a, dt in ((band, np.float32), (pos, np.uint32), (state, np.uint32)):
+        assert isinstance(a, np.ndarray) and a.dtype == dt and a.shape == (2,)
+    hist = np.ascontiguousarray(hist, dtype=np.uint32)
+    assert hist.shape == (64,)
+    return isax_debug_plan_round(_ptr(band), _ptr(pos), _ptr(state), cand_cnt, cap, _ptr(hist), int(near_ovf),
+                                 float(tused), float(bsf_lim), N)
 
 
 def version() -> str:
