@@ -264,8 +264,9 @@ static void launch_g(const isax_index *ix, uint32_t nq, const uint32_t *qmap, co
 // u8 test get the exact fp32 rule of the flat scan, so the candidate set is exactly the flat scan's
 // (tests/test_gpu_parity.py).
 //
-// Persistent CTAs (one per SM, 1024 threads) pull (query group, chunk of `chunk` leaves) tasks
-// from an atomic counter. The u8 tables of the group's G <= 16 queries sit in shared memory.
+// Persistent CTAs (two per SM of 512 threads, so one CTA's phase barriers overlap the other's
+// work; one of 1024 measured 1-4% slower) pull (query group, chunk of `chunk` leaves) tasks from
+// an atomic counter. The u8 tables of the group's G <= 16 queries sit in shared memory.
 // Per chunk:
 //  A. A0: thread = (hyper-node, query); A1: lane = super-node of a surviving (hyper-node, query);
 //     A2: warp iteration = one super-node, lane = one of its 32 leaves, for the queries that kept
@@ -282,10 +283,20 @@ constexpr uint32_t SUPER = SUPER_SIZE / LEAF_SIZE;  // leaves per super-node
 constexpr uint32_t HYPER = HYPER_SIZE / SUPER_SIZE; // super-nodes per hyper-node
 static_assert(HYPER == 32, "phase A maps the super-nodes of a hyper-node to the lanes of a warp");
 static_assert(LEAF == 32 && SUPER == 32, "phase A maps a super-node to a warp iteration and a leaf to a lane");
-constexpr int LF_THREADS = 1024;
-constexpr uint32_t CHUNK = 8192;  // max leaves per phase-A/phase-B round of a CTA
+#ifndef ISAX_LF_THREADS
+#define ISAX_LF_THREADS 512
+#endif
+constexpr int LF_THREADS = ISAX_LF_THREADS;
+#ifndef ISAX_CHUNK
+#define ISAX_CHUNK 4096
+#endif
+#ifndef ISAX_LF_CTAS
+#define ISAX_LF_CTAS 2
+#endif
+constexpr uint32_t CHUNK = ISAX_CHUNK;  // max leaves per phase-A/phase-B round of a CTA
+constexpr int LF_CTAS = ISAX_LF_CTAS;   // leaf-scan CTAs per SM
 #ifndef ISAX_PD
-#define ISAX_PD 4
+#define ISAX_PD 2
 #endif
 constexpr uint32_t PD = ISAX_PD;  // phase B: worklist entries in flight per warp (a power of two)
 static_assert((PD & (PD - 1)) == 0, "the staging ring wraps with a mask");
@@ -393,7 +404,7 @@ __global__ void __launch_bounds__(256) scanprep_kernel(const float *__restrict__
 }
 
 template <int G>
-__global__ void __launch_bounds__(LF_THREADS, 1) leafscan_kernel(
+__global__ void __launch_bounds__(LF_THREADS, LF_CTAS) leafscan_kernel(
     const uint4 *__restrict__ sax, const uint8_t *__restrict__ lmeta, const uint8_t *__restrict__ smeta,
     const uint8_t *__restrict__ hmeta, uint32_t N, const float *__restrict__ lut_all, const uint8_t *__restrict__ lut8_all, const uint4 *__restrict__ qconst_all,
     const uint8_t *__restrict__ qsax_all, const uint32_t *__restrict__ qmap, uint32_t nq, uint32_t nleaf,
@@ -651,15 +662,15 @@ static void launch_leaf(const isax_index *ix, uint32_t nq, const uint32_t *qmap,
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const uint32_t groups = (nq + G - 1) / G;
     const uint32_t nleaf = (uint32_t)((ix->N + LEAF - 1) / LEAF);
-    // chunk: as large as possible (fewer phase barriers) while leaving >= 8 tasks per SM for
+    // chunk: as large as possible (fewer phase barriers) while leaving >= 16 tasks per SM for
     // balance; a power of two >= 512, so a multiple of SUPER
     uint32_t chunk = CHUNK;
 #ifndef ISAX_TASKS_PER_SM
-#define ISAX_TASKS_PER_SM 8
+#define ISAX_TASKS_PER_SM 16
 #endif
     while (chunk > 512 && (uint64_t)groups * ((nleaf + chunk - 1) / chunk) < (uint64_t)ISAX_TASKS_PER_SM * sms) chunk >>= 1;
     const uint64_t tasks = (uint64_t)groups * ((nleaf + chunk - 1) / chunk);
-    const unsigned grid = (unsigned)std::max<uint64_t>(1, umin64(tasks, (uint64_t)sms));
+    const unsigned grid = (unsigned)std::max<uint64_t>(1, umin64(tasks, (uint64_t)sms * LF_CTAS));
     const QueryScratch &qs = ix->qs;
     leafscan_kernel<G><<<grid, LF_THREADS, smem, s>>>(
         reinterpret_cast<const uint4 *>(ix->sax), ix->lmeta, ix->smeta, ix->hmeta, (uint32_t)ix->N, qs.lut, qs.lut8, qs.qconst,
