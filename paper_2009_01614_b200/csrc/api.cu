@@ -108,7 +108,7 @@ static void free_scratch(isax_index *ix) {
 }
 
 // Candidate lists. With opts.cand_cap set, every query of a batch gets that capacity. By default
-// the lists share one pool of CAND_POOL entries (about 10 B each), split evenly over the queries of
+// the lists share one pool of CAND_POOL entries (about 12 B each), split evenly over the queries of
 // each batch: a batch of B queries gets min(N, 2^23, pool / B) per query (nn1_device). The pool is
 // halved while the scratch does not fit in device memory (down to 2^16 per query slot). A query
 // that overflows its capacity runs more rounds (R10), each a rescan, refining its smallest bounds

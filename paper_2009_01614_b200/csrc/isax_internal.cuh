@@ -138,10 +138,11 @@ struct QueryScratch {
     uint32_t *pwin = nullptr;       // [Q][MAX_PROBES]: kept probe window starts (probe_L rows each), count last
     unsigned long long *bsf = nullptr;  // [Q] packed
     uint32_t *cand = nullptr;       // [Q][cand_cap] sorted positions
-    uint8_t *candq = nullptr;       // [Q][cand_cap] u8 bound b of each candidate: b / qscale <= LB^2,
-                                    // or B_UNCHECKED: kept on its u8 sum alone, exact rule pending
+    uint16_t *candq = nullptr;      // [Q][cand_cap] u8 bounds of each candidate, b | (b2 << 8): b / qscale <= LB^2
+                                    // (or B_UNCHECKED: kept on its u8 sum alone, exact rule pending), b2 / qscale <=
+                                    // LB^2 of segments 8..15 (R16)
     uint32_t *cand2 = nullptr;      // [Q][cand_cap] the candidates after candcheck_kernel (the refine's list)
-    uint8_t *candq2 = nullptr;      // [Q][cand_cap] their u8 bounds
+    uint16_t *candq2 = nullptr;     // [Q][cand_cap] their bounds (as candq)
     uint32_t *cand_cnt2 = nullptr;  // [Q] first refine pass: cand2[q][0 .. cand_cnt2)
     uint32_t *cnt_hi = nullptr;     // [Q] second pass before filtering: cand2[q][cap - cnt_hi .. cap)
     uint32_t *cnt_f = nullptr;      // [Q] second pass after filtering: cand[q][0 .. cnt_f)

@@ -63,12 +63,15 @@ __device__ __forceinline__ uint32_t ld_sh_u8(uint32_t addr) {
     asm volatile("ld.shared.u8 %0, [%1];" : "=r"(r) : "r"(addr));
     return r;
 }
-__device__ __forceinline__ uint32_t word_e8(uint32_t ub, const uint4 &wv) {
+__device__ __forceinline__ uint32_t word_e8(uint32_t ub, const uint4 &wv, uint32_t &hi) {
     const uint32_t v[4] = {wv.x, wv.y, wv.z, wv.w};
-    uint32_t es = 0;
+    uint32_t lo = 0;
+    hi = 0;
 #pragma unroll
-    for (int s = 0; s < W; s++) es += ld_sh_u8(__byte_perm(v[s >> 2], ub, 0x7650u | (uint32_t)(s & 3)) + s * CARD);
-    return es;
+    for (int s = 0; s < W / 2; s++) lo += ld_sh_u8(__byte_perm(v[s >> 2], ub, 0x7650u | (uint32_t)(s & 3)) + s * CARD);
+#pragma unroll
+    for (int s = W / 2; s < W; s++) hi += ld_sh_u8(__byte_perm(v[s >> 2], ub, 0x7650u | (uint32_t)(s & 3)) + s * CARD);
+    return lo + hi;  // (hi: the u8 bound of the second half's segments 8..15, R16)
 }
 // u8 node bound (R11, R11b) of a node summary (per-segment min mn, max mx) against one query:
 // q holds the query's symbols as 8 u16x2 pairs; each term is the table entry at the clamped
@@ -167,7 +170,7 @@ __global__ void __launch_bounds__(LB_THREADS) lbscan_kernel(const uint4 *__restr
                                                             const unsigned long long *__restrict__ bsf,
                                                             const uint32_t *__restrict__ win, float onepd,
                                                             uint32_t *__restrict__ cand,
-                                                            uint8_t *__restrict__ candq,
+                                                            uint16_t *__restrict__ candq,
                                                             uint32_t *__restrict__ cand_cnt, uint32_t cap,
                                                             uint32_t *__restrict__ hist) {
     extern __shared__ __align__(16) float slut[];  // [G][16][256]
@@ -214,7 +217,7 @@ __global__ void __launch_bounds__(LB_THREADS) lbscan_kernel(const uint4 *__restr
                         const uint32_t kk = off + __popc(bal & lt);
                         if (kk < cap) {
                             cand[(uint64_t)qid[g] * cap + kk] = pos;
-                            candq[(uint64_t)qid[g] * cap + kk] = 0;  // no bound recorded: never skipped
+                            candq[(uint64_t)qid[g] * cap + kk] = 0;  // no bounds recorded: never skipped
                         }
                         atomicAdd(&hist[qid[g] * HIST_BINS + hist_bin(lb, k.lo, k.T)], 1u);
                     }
@@ -315,13 +318,13 @@ constexpr uint32_t E_SURE = 237;
 // otherwise serialise every CTA on its count.
 constexpr uint32_t WB = 64;  // staged candidates per warp
 __device__ __forceinline__ void wflush(uint2 *wb, uint32_t &wcnt, uint32_t lane, volatile uint32_t *ovf,
-                                       const uint32_t *qid, uint32_t *cand, uint8_t *candq, uint32_t *cand_cnt,
+                                       const uint32_t *qid, uint32_t *cand, uint16_t *candq, uint32_t *cand_cnt,
                                        uint32_t cap) {
     __syncwarp();
     for (uint32_t i0 = 0; i0 < wcnt; i0 += 32) {
         const bool have = i0 + lane < wcnt;
         const uint2 en = have ? wb[i0 + lane] : make_uint2(0u, 0u);
-        const uint32_t g = have ? (en.y >> 8) : 0xFFFFu;
+        const uint32_t g = have ? (en.y >> 16) : 0xFFFFu;
         const uint32_t peers = __match_any_sync(0xffffffffu, g);
         if (have) {
             const uint32_t leader = __ffs(peers) - 1;
@@ -336,7 +339,7 @@ __device__ __forceinline__ void wflush(uint2 *wb, uint32_t &wcnt, uint32_t lane,
             const uint32_t k = base + __popc(peers & ((1u << lane) - 1u));
             if (base != 0xffffffffu && k < cap) {
                 cand[(uint64_t)q * cap + k] = en.x;
-                candq[(uint64_t)q * cap + k] = (uint8_t)(en.y & 0xFFu);
+                candq[(uint64_t)q * cap + k] = (uint16_t)(en.y & 0xFFFFu);
             }
         }
     }
@@ -344,12 +347,13 @@ __device__ __forceinline__ void wflush(uint2 *wb, uint32_t &wcnt, uint32_t lane,
     wcnt = 0;
 }
 
-__device__ __forceinline__ void emit(bool keep, uint32_t pos, uint32_t b, uint32_t g, uint32_t lane, uint32_t lt,
+// bq = the candidate's u8 bounds: b | (b2 << 8), b2 that of the second half's segments (R16)
+__device__ __forceinline__ void emit(bool keep, uint32_t pos, uint32_t bq, uint32_t g, uint32_t lane, uint32_t lt,
                                      uint2 *wb, uint32_t &wcnt, volatile uint32_t *ovf, const uint32_t *qid,
-                                     uint32_t *cand, uint8_t *candq, uint32_t *cand_cnt, uint32_t cap) {
+                                     uint32_t *cand, uint16_t *candq, uint32_t *cand_cnt, uint32_t cap) {
     const uint32_t bal = __ballot_sync(0xffffffffu, keep);
     if (!bal || ovf[g]) return;
-    if (keep) wb[wcnt + __popc(bal & lt)] = make_uint2(pos, (g << 8) | b);
+    if (keep) wb[wcnt + __popc(bal & lt)] = make_uint2(pos, (g << 16) | bq);
     wcnt += __popc(bal);
     if (wcnt > WB - 32) wflush(wb, wcnt, lane, ovf, qid, cand, candq, cand_cnt, cap);
 }
@@ -408,7 +412,7 @@ __global__ void __launch_bounds__(LF_THREADS, LF_CTAS) leafscan_kernel(
     const uint4 *__restrict__ sax, const uint8_t *__restrict__ lmeta, const uint8_t *__restrict__ smeta,
     const uint8_t *__restrict__ hmeta, uint32_t N, const float *__restrict__ lut_all, const uint8_t *__restrict__ lut8_all, const uint4 *__restrict__ qconst_all,
     const uint8_t *__restrict__ qsax_all, const uint32_t *__restrict__ qmap, uint32_t nq, uint32_t nleaf,
-    uint32_t chunk, uint32_t *__restrict__ cand, uint8_t *__restrict__ candq, uint32_t *__restrict__ cand_cnt, uint32_t cap,
+    uint32_t chunk, uint32_t *__restrict__ cand, uint16_t *__restrict__ candq, uint32_t *__restrict__ cand_cnt, uint32_t cap,
     uint32_t *__restrict__ hist, uint32_t *__restrict__ leaves_alive, unsigned long long *__restrict__ scan_bytes_dev,
     uint32_t *__restrict__ task_ctr) {
     // shared: [G][16][256] u8 tables | [CHUNK] worklist | [NW][PD][LEAF] staged words
@@ -610,7 +614,8 @@ __global__ void __launch_bounds__(LF_THREADS, LF_CTAS) leafscan_kernel(
                 const uint32_t g = __ffs(mm) - 1;
                 // integer member filter: 16 lookups of 2.5 instructions (PRMT address, LDS.U8, half
                 // an IADD3)
-                const uint32_t e8 = word_e8(lut8_sh + g * W * CARD, wv);
+                uint32_t e8hi;
+                const uint32_t e8 = word_e8(lut8_sh + g * W * CARD, wv, e8hi);
                 if (!__any_sync(FULL, e8 <= 254u)) continue;
                 // The flat scan's rule is lo < LB^2 <= T on the exact fp32 bound. A u8 sum <= E_SURE
                 // already implies LB^2 <= T (R11b), and in the first band (lo < 0) lo < LB^2 always
@@ -637,7 +642,7 @@ __global__ void __launch_bounds__(LF_THREADS, LF_CTAS) leafscan_kernel(
                 }
                 if (keep)
                     atomicAdd(&shist[g][first ? min(e8 * HIST_BINS / 254u, HIST_BINS - 1) : hist_bin(lb, kq.lo, kq.T)], 1u);
-                emit(keep, pos, b, g, lane, lt, wbuf, wcnt, s_ovf, qid, cand, candq, cand_cnt, cap);
+                emit(keep, pos, b | (e8hi << 8), g, lane, lt, wbuf, wcnt, s_ovf, qid, cand, candq, cand_cnt, cap);
             }
         }
         if (wcnt) wflush(wbuf, wcnt, lane, s_ovf, qid, cand, candq, cand_cnt, cap);  // (warp-uniform)
@@ -723,10 +728,10 @@ constexpr uint32_t SPLIT_TARGET = 65536;  // first-pass size a lowered split aim
 #define ISAX_CK_MINB 3
 #endif
 __global__ void __launch_bounds__(CK_THREADS, ISAX_CK_MINB) candcheck_kernel(
-    const uint32_t *__restrict__ cand, const uint8_t *__restrict__ candq, const uint32_t *__restrict__ cand_cnt,
+    const uint32_t *__restrict__ cand, const uint16_t *__restrict__ candq, const uint32_t *__restrict__ cand_cnt,
     uint32_t Q, uint32_t cap, const uint4 *__restrict__ sax, const float *__restrict__ lut_all,
     const float *__restrict__ qT, const float *__restrict__ qscale, uint32_t *__restrict__ cand2,
-    uint8_t *__restrict__ candq2, uint32_t *__restrict__ cand_cnt2, uint32_t *__restrict__ cnt_hi,
+    uint16_t *__restrict__ candq2, uint32_t *__restrict__ cand_cnt2, uint32_t *__restrict__ cnt_hi,
     const uint32_t *__restrict__ hist) {
     constexpr int U = 8;  // candidates per thread per iteration, all loads in flight together
     __shared__ uint32_t pre[1025];
@@ -780,7 +785,7 @@ __global__ void __launch_bounds__(CK_THREADS, ISAX_CK_MINB) candcheck_kernel(
     const uint32_t b1 = s_b1;
     uint32_t q = q0;  // a thread's query only moves forward
     for (uint32_t fb = f0; fb < f1; fb += U * CK_THREADS) {
-        uint32_t qk[U], pos[U], b[U];
+        uint32_t qk[U], pos[U], b[U], b2[U];
         bool valid[U];
 #pragma unroll
         for (int u = 0; u < U; u++) {
@@ -791,7 +796,9 @@ __global__ void __launch_bounds__(CK_THREADS, ISAX_CK_MINB) candcheck_kernel(
             qk[u] = q;
             const uint64_t k = (uint64_t)q * cap + (f - pre[q]);
             pos[u] = valid[u] ? cand[k] : 0u;
-            b[u] = valid[u] ? candq[k] : 0u;
+            const uint32_t bq = valid[u] ? candq[k] : 0u;
+            b[u] = bq & 0xFFu;
+            b2[u] = bq >> 8;  // the second half's bound (R16), passed through
         }
         uint4 wv[U];
 #pragma unroll
@@ -822,7 +829,7 @@ __global__ void __launch_bounds__(CK_THREADS, ISAX_CK_MINB) candcheck_kernel(
         auto put = [&](uint32_t qq, uint32_t idx, bool h, uint32_t p, uint32_t bb) {
             const uint64_t k2 = (uint64_t)qq * cap + (h ? cap - 1 - idx : idx);
             cand2[k2] = p;
-            candq2[k2] = (uint8_t)bb;
+            candq2[k2] = (uint16_t)bb;
         };
         const uint32_t q_lane = qk[0];
         const uint32_t q_w = __shfl_sync(FULL, q_lane, 0);  // (every lane shuffles: no short circuit)
@@ -841,8 +848,8 @@ __global__ void __launch_bounds__(CK_THREADS, ISAX_CK_MINB) candcheck_kernel(
             uint32_t basel = __shfl_sync(FULL, base, 0), baseh = __shfl_sync(FULL, base, 1);
 #pragma unroll
             for (int u = 0; u < U; u++) {
-                if (keep[u] && !hi[u]) put(q_lane, basel + __popc(bl[u] & lt), false, pos[u], b[u]);
-                if (hi[u]) put(q_lane, baseh + __popc(bh[u] & lt), true, pos[u], b[u]);
+                if (keep[u] && !hi[u]) put(q_lane, basel + __popc(bl[u] & lt), false, pos[u], b[u] | (b2[u] << 8));
+                if (hi[u]) put(q_lane, baseh + __popc(bh[u] & lt), true, pos[u], b[u] | (b2[u] << 8));
                 basel += __popc(bl[u]);
                 baseh += __popc(bh[u]);
             }
@@ -855,7 +862,7 @@ __global__ void __launch_bounds__(CK_THREADS, ISAX_CK_MINB) candcheck_kernel(
                     uint32_t base = 0;
                     if (lane == leader) base = atomicAdd(hi[u] ? &cnt_hi[qk[u]] : &cand_cnt2[qk[u]], (uint32_t)__popc(peers));
                     base = __shfl_sync(peers, base, leader);
-                    put(qk[u], base + __popc(peers & lt), hi[u], pos[u], b[u]);
+                    put(qk[u], base + __popc(peers & lt), hi[u], pos[u], b[u] | (b2[u] << 8));
                 }
             }
         }

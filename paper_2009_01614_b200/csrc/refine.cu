@@ -127,7 +127,7 @@ __global__ void __launch_bounds__(RF_THREADS) refine_q_kernel(const float *__res
                                                              const uint32_t *__restrict__ perm, uint32_t n,
                                                              const float *__restrict__ qy, uint32_t Q,
                                                              const uint32_t *__restrict__ cand,
-                                                             const uint8_t *__restrict__ candq,
+                                                             const uint16_t *__restrict__ candq,
                                                              const float *__restrict__ qscale,
                                                              const uint32_t *__restrict__ cand_cnt, uint32_t cap,
                                                              unsigned long long *__restrict__ bsf, NearList nl,
@@ -149,8 +149,8 @@ __global__ void __launch_bounds__(RF_THREADS) refine_q_kernel(const float *__res
         }
         return lo;
     };
-    uint32_t cur_q = 0xffffffffu, done = 0, abandoned = 0, since = 0;
-    float lim_c = 0.f;
+    uint32_t cur_q = 0xffffffffu, done = 0, abandoned = 0, since = 0, q_rc = 0xffffffffu;
+    float lim_c = 0.f, rsc = 0.f;
     // each quarter owns a contiguous range of the flat candidate index: consecutive candidates
     // share a query (its counters are flushed only when the query changes) and sit close together
     // in the sorted order
@@ -158,14 +158,16 @@ __global__ void __launch_bounds__(RF_THREADS) refine_q_kernel(const float *__res
     const uint32_t qi = (blockIdx.x * RF_THREADS + t) >> 3;
     const uint32_t fbeg = min(qi * per, total), fend = min(fbeg + per, total);
     for (uint32_t f0 = fbeg; f0 < fend; f0 += RF_C) {
-        uint32_t qv[RF_C], pv[RF_C];
+        uint32_t qv[RF_C], pv[RF_C], b2v[RF_C];
         bool live[RF_C];
 #pragma unroll
         for (int c = 0; c < RF_C; c++) {
             const uint32_t f = f0 + c;
             live[c] = f < fend;
             qv[c] = live[c] ? locate(f) : 0;
-            pv[c] = live[c] ? cand[(uint64_t)qv[c] * cap + (f - pre[qv[c]])] : 0;
+            const uint64_t k = (uint64_t)qv[c] * cap + (f - pre[qv[c]]);
+            pv[c] = live[c] ? cand[k] : 0;
+            b2v[c] = live[c] && candq ? (uint32_t)(candq[k] >> 8) : 0u;
         }
         float4 v[RF_C][NH];
 #pragma unroll
@@ -196,6 +198,10 @@ __global__ void __launch_bounds__(RF_THREADS) refine_q_kernel(const float *__res
                 lim_c = __shfl_sync(qmask, l, lane & 24);
                 since = 1;
             }
+            if (q != q_rc) {  // 1 / sc of the query's scan, rounded down (R16)
+                q_rc = q;
+                rsc = qscale ? __frcp_rd(__ldg(qscale + q)) : 0.f;
+            }
             const float lim = lim_c;
             const float4 *qr = reinterpret_cast<const float4 *>(qy + (uint64_t)q * n);
             float acc = 0.f;
@@ -212,7 +218,9 @@ __global__ void __launch_bounds__(RF_THREADS) refine_q_kernel(const float *__res
             part += __shfl_xor_sync(qmask, part, 1);
             part += __shfl_xor_sync(qmask, part, 2);
             part += __shfl_xor_sync(qmask, part, 4);
-            if (part > lim) {  // early abandon after half the row (R8)
+            // early abandon after half the row (R8): the partial sum plus a lower bound of
+            // the second half's distance, b2 / sc <= LB^2 of segments 8..15 <= its ED^2 (R16)
+            if (part + __fmul_rd((float)b2v[c], rsc) > lim) {
                 abandoned++;
                 continue;
             }
@@ -262,12 +270,12 @@ __global__ void __launch_bounds__(RF_THREADS) refine_q_kernel(const float *__res
 // means LB^2 > lim = bsf^2 (1 + delta), and the row can hold neither a new answer nor a near tie.
 // The survivors go to the front of the scan's own list (cand, free again) for the second pass.
 __global__ void __launch_bounds__(RF_THREADS) filter_kernel(const uint32_t *__restrict__ cand2,
-                                                           const uint8_t *__restrict__ candq2,
+                                                           const uint16_t *__restrict__ candq2,
                                                            const uint32_t *__restrict__ cnt_hi, uint32_t Q, uint32_t cap,
                                                            const unsigned long long *__restrict__ bsf,
                                                            const float *__restrict__ qscale, float onepd,
-                                                           uint32_t *__restrict__ out, uint32_t *__restrict__ cnt_f,
-                                                           uint32_t *__restrict__ counters) {
+                                                           uint32_t *__restrict__ out, uint16_t *__restrict__ outq,
+                                                           uint32_t *__restrict__ cnt_f, uint32_t *__restrict__ counters) {
     constexpr int U = 8;  // candidates per thread per iteration, loads in flight together
     __shared__ uint32_t pre[RF_MAXQ + 1];
     constexpr uint32_t FULL = 0xffffffffu;
@@ -290,7 +298,7 @@ __global__ void __launch_bounds__(RF_THREADS) filter_kernel(const uint32_t *__re
         q = lo;
     }
     for (uint32_t fb = f0; fb < f1; fb += U * RF_THREADS) {
-        uint32_t qk[U], pos[U];
+        uint32_t qk[U], pos[U], bq[U];
         bool valid[U], live[U];
         float thr[U];
         bool one_q = true;
@@ -304,7 +312,8 @@ __global__ void __launch_bounds__(RF_THREADS) filter_kernel(const uint32_t *__re
             one_q &= !valid[u] || q == qk[0];
             const uint64_t k = (uint64_t)q * cap + (cap - 1 - (f - pre[q]));
             pos[u] = valid[u] ? cand2[k] : 0u;
-            thr[u] = valid[u] ? (float)candq2[k] : 0.f;
+            bq[u] = valid[u] ? candq2[k] : 0u;
+            thr[u] = (float)(bq[u] & 0xFFu);
         }
         // the skip test against the BSF as it stands now (read once per lane)
         const float lim = bsf_d2(*((volatile const unsigned long long *)&bsf[qk[0]])) * onepd;
@@ -330,7 +339,11 @@ __global__ void __launch_bounds__(RF_THREADS) filter_kernel(const uint32_t *__re
             base = __shfl_sync(FULL, base, 0);
 #pragma unroll
             for (int u = 0; u < U; u++) {
-                if (live[u]) out[(uint64_t)q_w * cap + base + __popc(bl[u] & lt)] = pos[u];
+                if (live[u]) {
+                    const uint64_t k = (uint64_t)q_w * cap + base + __popc(bl[u] & lt);
+                    out[k] = pos[u];
+                    outq[k] = (uint16_t)bq[u];
+                }
                 base += __popc(bl[u]);
             }
         } else {
@@ -343,7 +356,11 @@ __global__ void __launch_bounds__(RF_THREADS) filter_kernel(const uint32_t *__re
                     if (lane == leader)
                         base = atomicAdd(live[u] ? &cnt_f[qk[u]] : &counters[4 * qk[u] + 2], (uint32_t)__popc(peers));
                     base = __shfl_sync(peers, base, leader);
-                    if (live[u]) out[(uint64_t)qk[u] * cap + base + __popc(peers & lt)] = pos[u];
+                    if (live[u]) {
+                        const uint64_t k = (uint64_t)qk[u] * cap + base + __popc(peers & lt);
+                        out[k] = pos[u];
+                        outq[k] = (uint16_t)bq[u];
+                    }
                 }
             }
         }
@@ -358,7 +375,7 @@ void launch_refine(const isax_index *ix, uint32_t Q, float delta, cudaStream_t s
     const float onepd = 1.0f + delta;
     const NearList nl{qs.near, qs.near_off, qs.near_cap, qs.near_cnt};
     // pass 1: cand2[q][0 .. cand_cnt2); then the filtered second band into cand[q][0 .. cnt_f)
-    auto pass = [&](const uint32_t *list, const uint32_t *cnt, unsigned long long *bytes) {
+    auto pass = [&](const uint32_t *list, const uint16_t *listq, const uint32_t *cnt, unsigned long long *bytes) {
         if (ix->n <= 256) {
             int per_sm = 1;
             const uint32_t nh = ix->n / 64;
@@ -369,7 +386,7 @@ void launch_refine(const isax_index *ix, uint32_t Q, float delta, cudaStream_t s
             switch (nh) {
 #define RQ_CASE(K)                                                                                                  \
     case K:                                                                                                         \
-        refine_q_kernel<K><<<grid, RF_THREADS, 0, s>>>(ix->stored, ix->perm, ix->n, qs.qy, Q, list, nullptr, nullptr, \
+        refine_q_kernel<K><<<grid, RF_THREADS, 0, s>>>(ix->stored, ix->perm, ix->n, qs.qy, Q, list, listq, qs.qscale, \
                                                        cnt, qs.cand_cap, qs.bsf, nl, qs.counters,                   \
                                                        onepd, bytes);                                               \
         break;
@@ -390,12 +407,12 @@ void launch_refine(const isax_index *ix, uint32_t Q, float delta, cudaStream_t s
         }
 #undef RF_CASE
     };
-    pass(qs.cand2, qs.cand_cnt2, qs.refine_bytes);
+    pass(qs.cand2, qs.candq2, qs.cand_cnt2, qs.refine_bytes);
     if (evs) cudaEventRecord(evs[0], s);
     filter_kernel<<<sms * 4, RF_THREADS, 0, s>>>(qs.cand2, qs.candq2, qs.cnt_hi, Q, qs.cand_cap, qs.bsf, qs.qscale,
-                                                 onepd, qs.cand, qs.cnt_f, qs.counters);
+                                                 onepd, qs.cand, qs.candq, qs.cnt_f, qs.counters);
     if (evs) cudaEventRecord(evs[1], s);
-    pass(qs.cand, qs.cnt_f, qs.refine_bytes + 1);
+    pass(qs.cand, qs.candq, qs.cnt_f, qs.refine_bytes + 1);
 }
 
 // ------------------------------------------------------------------------------------ finalize
