@@ -414,7 +414,7 @@ __global__ void __launch_bounds__(LF_THREADS, LF_CTAS) leafscan_kernel(
     const uint8_t *__restrict__ qsax_all, const uint32_t *__restrict__ qmap, uint32_t nq, uint32_t nleaf,
     uint32_t chunk, uint32_t *__restrict__ cand, uint16_t *__restrict__ candq, uint32_t *__restrict__ cand_cnt, uint32_t cap,
     uint32_t *__restrict__ hist, uint32_t *__restrict__ leaves_alive, unsigned long long *__restrict__ scan_bytes_dev,
-    uint32_t *__restrict__ task_ctr) {
+    uint32_t *__restrict__ task_ctr, uint32_t run) {
     // shared: [G][16][256] u8 tables | [CHUNK] worklist | [NW][PD][LEAF] staged words
     // (the dynamic region follows the static variables, so the u8 tables are aligned by hand: the
     // PRMT address trick needs a 256-aligned base)
@@ -460,9 +460,20 @@ __global__ void __launch_bounds__(LF_THREADS, LF_CTAS) leafscan_kernel(
         }
         __syncthreads();
     };
-    if (t == 0) wl_cnt = 0;
+    // tasks are taken in runs of `run` consecutive ones (launch_leaf: 1)
+    __shared__ uint32_t s_next, s_end;
+    if (t == 0) {
+        wl_cnt = 0;
+        s_next = s_end = 0;
+    }
     for (;;) {
-        if (t == 0) s_task = atomicAdd(task_ctr, 1u);
+        if (t == 0) {
+            if (s_next >= s_end) {
+                s_next = atomicAdd(task_ctr, run);
+                s_end = s_next + run;
+            }
+            s_task = s_next++;
+        }
         __syncthreads();
         const uint32_t task = s_task;
         if (task >= ntasks) break;
@@ -515,6 +526,13 @@ __global__ void __launch_bounds__(LF_THREADS, LF_CTAS) leafscan_kernel(
             }
         }
         __syncthreads();
+#ifndef ISAX_NO_EARLY
+        {  // a chunk whose hyper-nodes are pruned for every query of the group: the next task
+            uint32_t any = 0;
+            for (uint32_t h = 0; h < nh; h++) any |= hmask[h];
+            if (!any) continue;  // (uniform; wl_cnt is still 0)
+        }
+#endif
         // A1: for each (hyper-node, query) that survived, lane = one of its 32 super-nodes
         for (uint32_t pr = warp; pr < nh * 16u; pr += NW) {
             const uint32_t h = pr >> 4, g = pr & 15u;
@@ -676,11 +694,17 @@ static void launch_leaf(const isax_index *ix, uint32_t nq, const uint32_t *qmap,
     while (chunk > 512 && (uint64_t)groups * ((nleaf + chunk - 1) / chunk) < (uint64_t)ISAX_TASKS_PER_SM * sms) chunk >>= 1;
     const uint64_t tasks = (uint64_t)groups * ((nleaf + chunk - 1) / chunk);
     const unsigned grid = (unsigned)std::max<uint64_t>(1, umin64(tasks, (uint64_t)sms * LF_CTAS));
+    // one task per grab: runs of 4-8 consecutive chunks per CTA (fewer table reloads with many
+    // groups) measured 30-100% slower: the CTAs then stream through scattered parts of the arrays
+#ifndef ISAX_TASK_RUN
+#define ISAX_TASK_RUN 1
+#endif
+    const uint32_t run = ISAX_TASK_RUN;
     const QueryScratch &qs = ix->qs;
     leafscan_kernel<G><<<grid, LF_THREADS, smem, s>>>(
         reinterpret_cast<const uint4 *>(ix->sax), ix->lmeta, ix->smeta, ix->hmeta, (uint32_t)ix->N, qs.lut, qs.lut8, qs.qconst,
         qs.qsax, qmap, nq, nleaf, chunk, qs.cand, qs.candq, qs.cand_cnt, qs.cand_cap, qs.cand_hist, qs.counters_leaf,
-        qs.scan_bytes_dev, qs.task_ctr);
+        qs.scan_bytes_dev, qs.task_ctr, run);
 }
 
 uint64_t launch_lbscan(const isax_index *ix, uint32_t nq, uint32_t B, const uint32_t *qmap, const Band *band,
@@ -719,7 +743,10 @@ constexpr int CK_THREADS = 256;
 #define ISAX_BSPLIT 140
 #endif
 constexpr uint32_t B_SPLIT = ISAX_BSPLIT;  // second refine pass: b > B_SPLIT, i.e. LB^2 above about 0.55 T
-constexpr uint32_t SPLIT_MIN = 4096;  // ... for queries with more candidates than this
+#ifndef ISAX_SPLIT_MIN
+#define ISAX_SPLIT_MIN 4096
+#endif
+constexpr uint32_t SPLIT_MIN = ISAX_SPLIT_MIN;  // ... for queries with more candidates than this
 constexpr uint32_t SPLIT_TARGET = 65536;  // first-pass size a lowered split aims at
 
 // three CTAs per SM (at most 80 registers; 92 allowed only two): the kernel is latency-bound on
