@@ -47,7 +47,7 @@ typedef struct isax_opts {
     int32_t slack_log2;  /* prune/abandon slack delta = 2^slack_log2 (R8). Default -12. */
     uint32_t batch_Q;    /* queries processed per device batch (<= 1024). Default 1024. */
     uint32_t cand_cap;   /* candidate-list capacity per query per round. 0 = default: a pool of 2^30 entries (about
-                            10 B each; halved while it does not fit) split over the queries of each batch, at most
+                            12 B each; halved while it does not fit) split over the queries of each batch, at most
                             min(N, 2^23) per query. Overflow runs more rounds (R10). */
     uint32_t flags;      /* ISAX_FLAG_* bits; 0 = defaults */
     uint32_t probe_bits; /* multi-probe approximate answer (R5): refine extra windows at the 2^probe_bits - 1 keys
@@ -55,12 +55,14 @@ typedef struct isax_opts {
                             window, or at the start of an earlier one, is skipped. 0 = default 5 (max);
                             ISAX_PROBES_NONE = main window only. */
     uint32_t probe_L;    /* rows per probe window: the kd cell of that many rows in the probe key's super-node
-                            that the probe's symbols descend to (R6b). 0 = default 128. */
+                            that the probe's symbols descend to (R6b). 0 = default 128, or 64 in a best-first
+                            batch (first_band, R15). */
     float first_band;    /* best-first scan order (R15): round 0 scans only the smallest bounds,
                             LB^2 <= first_band * bsf0^2 (1 + delta), refines them, and the next round scans
                             the rest under the improved BSF; with window_L = 0 the main window is then one
-                            super-node. 0 = adaptive (default): fraction 1/50 or none, whichever the index
-                            measured to be faster per query (device time); the other mode is re-timed after
+                            super-node (and with probe_L = 0 each probe window 64 rows). 0 = adaptive
+                            (default): fraction 1/50 or none, whichever the index measured to be faster per
+                            query (device time); the other mode is re-timed after
                             32, 64, ... up to 512 batches while the choice holds. In (0, 1) = always, that
                             fraction; < 0 = never. Answers do not depend on it. */
 } isax_opts;

@@ -118,6 +118,7 @@ static void free_scratch(isax_index *ix) {
 constexpr uint64_t CAND_POOL = 1ull << 30;
 constexpr float FB_FRAC = 0.02f;      // R15: the adaptive first band's fraction of the window threshold
 constexpr uint32_t FB_REPROBE = 512;  // longest run in the preferred mode before the other one is re-timed
+constexpr uint32_t PROBE_L_BEST = 64; // probe window rows in best-first mode (the probes only seed the band)
 static int alloc_scratch_cap(isax_index *ix, uint32_t cap);
 static int alloc_scratch(isax_index *ix) {
     if (ix->qs.cap_Q) return ISAX_OK;
@@ -218,6 +219,8 @@ static int build_impl(const Source &src, uint64_t N, uint32_t n, uint32_t w, uin
     ix->N = N; ix->n = n; ix->w = w; ix->card = card; ix->opts = o; ix->device = dev;
     ix->win_auto = !(opts && opts->window_L);
     ix->win_L = o.window_L;
+    ix->pr_auto = !(opts && opts->probe_L);
+    ix->pr_L = o.probe_L;
     uint8_t *sax_by_id = nullptr;
     uint4 *keys = nullptr;
     double2 *musig = nullptr;
@@ -422,6 +425,7 @@ static int nn1_device(isax_index *ix, const float *d_q, uint32_t Q, int64_t *d_i
         // main window shrinks to the query key's super-node (plus its neighbours' kd quarters)
         // unless the caller fixed window_L (R5, R15)
         ix->win_L = (band0 > 0.f && ix->win_auto) ? std::min<uint32_t>(ix->opts.window_L, SUPER_SIZE) : ix->opts.window_L;
+        ix->pr_L = (band0 > 0.f && ix->pr_auto) ? std::min<uint32_t>(ix->opts.probe_L, PROBE_L_BEST) : ix->opts.probe_L;
         const bool timed = b0 == 0;
         if (timed) {
             ix->st_fb_frac = band0;
@@ -750,6 +754,7 @@ int isax_query_debug(const isax_index *cix, const float *queries, uint32_t Q, do
     if (e == cudaSuccess) e = cudaMemsetAsync(flag, 0, sizeof(uint32_t), s);
     if (e == cudaSuccess) {
         ix->win_L = ix->opts.window_L;  // (the window of a call without the first band)
+        ix->pr_L = ix->opts.probe_L;
         launch_qprep(ix, dq, Q, 0.f, s, flag);
         e = cudaGetLastError();
     }
@@ -820,7 +825,7 @@ int isax_stats(const isax_index *cix, char *buf, size_t cap) {
              "\"N\":%llu,\"n\":%u,\"window_L\":%u,\"probe_windows\":%u,\"probe_L\":%u,\"slack_log2\":%d,\"batch_Q\":%u,\"cand_cap\":%u,"
              "\"ms_first_batch\":{\"qprep\":%.4f,\"window\":%.4f,\"lbscan\":%.4f,\"candcheck\":%.4f,\"refine\":%.4f,"
              "\"refine1\":%.4f,\"filter\":%.4f,\"refine2\":%.4f,\"total\":%.4f},",
-             (unsigned long long)ix->N, ix->n, ix->win_L, window_probes(ix), ix->opts.probe_L, ix->opts.slack_log2,
+             (unsigned long long)ix->N, ix->n, ix->win_L, window_probes(ix), ix->pr_L, ix->opts.slack_log2,
              ix->opts.batch_Q, ix->qs.cand_cap, ix->st_ms.qprep, ix->st_ms.window, ix->st_ms.lbscan, ix->st_ms.candcheck, ix->st_ms.refine,
              ix->st_ms.refine1, ix->st_ms.filter, ix->st_ms.refine2, ix->st_ms.finalize);
     j += tmp;

@@ -206,6 +206,8 @@ struct isax_index {
     float fb_ms_on = -1.f, fb_ms_off = -1.f;
     bool win_auto = true;       // window_L left to the library (opts.window_L == 0)
     uint32_t win_L = 3072;      // main window rows of the current batch (R5; 1024 in best-first mode when auto)
+    bool pr_auto = true;        // probe_L left to the library (opts.probe_L == 0)
+    uint32_t pr_L = 128;        // probe window rows of the current batch (64 in best-first mode when auto)
     uint32_t fb_since = 0;       // batches since the other mode was last measured
     uint32_t fb_every = 32;      // re-time the other mode after this many batches (doubles while the choice holds)
     float st_fb_frac = 0.f;      // first-band fraction of the last call's first batch (0 = none)

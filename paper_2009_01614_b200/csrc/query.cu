@@ -252,7 +252,7 @@ void launch_qprep(const isax_index *ix, const float *queries, uint32_t Q, float 
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     auto kern = Q <= (uint32_t)(2 * sms) ? qprep_kernel<1024> : qprep_kernel<256>;
     kern<<<Q, Q <= (uint32_t)(2 * sms) ? 1024 : 256, 0, s>>>(queries, ix->n, ix->skey, ix->ksplit, ix->N,
-                                   ix->win_L, probe_bits(ix), ix->opts.probe_L, qs.pwin, qs.qy, qs.qpaa, qs.qsax, qs.lut, qs.win, qs.bsf, qs.cand_cnt,
+                                   ix->win_L, probe_bits(ix), ix->pr_L, qs.pwin, qs.qy, qs.qpaa, qs.qsax, qs.lut, qs.win, qs.bsf, qs.cand_cnt,
                                    qs.near_cnt, qs.near_off, qs.near_cap, qs.counters, qs.counters_leaf, qs.qmap, qs.qband,
                                    band0, bad);
 }
@@ -395,14 +395,14 @@ void launch_window(const isax_index *ix, uint32_t Q, const uint32_t *qmap, float
     const float onepd = 1.0f + delta;
     const uint32_t ns = (ix->n + 127) / 128;
     const uint32_t nprobe = (1u << probe_bits(ix)) - 1 + neighbour_windows(ix->win_L, probe_bits(ix));
-    const uint32_t lp = (uint32_t)(ix->N < ix->opts.probe_L ? ix->N : ix->opts.probe_L);
+    const uint32_t lp = (uint32_t)(ix->N < ix->pr_L ? ix->N : ix->pr_L);
     const uint32_t L = (uint32_t)(ix->N < ix->win_L ? ix->N : ix->win_L);
     const uint32_t rows = L + nprobe * lp;
     const dim3 grid((rows + WIN_ROWS - 1) / WIN_ROWS, Q);
 #define WIN_CASE(K)                                                                                          \
     case K:                                                                                                  \
         window_kernel<K><<<grid, 256, 0, s>>>(ix->stored, ix->perm, ix->n, ix->N, qs.qy, qs.win, qs.pwin,    \
-                                              nprobe, ix->opts.probe_L, qmap, qs.bsf,                         \
+                                              nprobe, ix->pr_L, qmap, qs.bsf,                         \
                                               NearList{qs.near, qs.near_off, qs.near_cap, qs.near_cnt},       \
                                               qs.counters, onepd);                                           \
         break;
