@@ -157,17 +157,34 @@ __global__ void __launch_bounds__(RF_THREADS) refine_q_kernel(const float *__res
     const uint32_t per = (total + nquart - 1) / nquart;
     const uint32_t qi = (blockIdx.x * RF_THREADS + t) >> 3;
     const uint32_t fbeg = min(qi * per, total), fend = min(fbeg + per, total);
+    // The next step's candidates (query, position, second-half bound) are fetched while this
+    // step's rows load, so the list read is off the row loads' dependency chain. The query of
+    // f advances from the previous one (the range is contiguous).
+    uint32_t qh = fbeg < fend ? locate(fbeg) : 0;
+    uint32_t qn[RF_C], pn[RF_C], bn[RF_C];
+    auto fetch = [&](uint32_t f0) {
+#pragma unroll
+        for (int c = 0; c < RF_C; c++) {
+            const uint32_t f = f0 + c;
+            const bool l = f < fend;
+            if (l)
+                while (pre[qh + 1] <= f) qh++;
+            qn[c] = qh;
+            const uint64_t k = (uint64_t)qh * cap + (f - pre[qh]);
+            pn[c] = l ? cand[k] : 0xffffffffu;
+            bn[c] = l && candq ? (uint32_t)(candq[k] >> 8) : 0u;
+        }
+    };
+    fetch(fbeg);
     for (uint32_t f0 = fbeg; f0 < fend; f0 += RF_C) {
         uint32_t qv[RF_C], pv[RF_C], b2v[RF_C];
         bool live[RF_C];
 #pragma unroll
         for (int c = 0; c < RF_C; c++) {
-            const uint32_t f = f0 + c;
-            live[c] = f < fend;
-            qv[c] = live[c] ? locate(f) : 0;
-            const uint64_t k = (uint64_t)qv[c] * cap + (f - pre[qv[c]]);
-            pv[c] = live[c] ? cand[k] : 0;
-            b2v[c] = live[c] && candq ? (uint32_t)(candq[k] >> 8) : 0u;
+            live[c] = f0 + c < fend;
+            qv[c] = qn[c];
+            pv[c] = pn[c];
+            b2v[c] = bn[c];
         }
         float4 v[RF_C][NH];
 #pragma unroll
@@ -176,6 +193,7 @@ __global__ void __launch_bounds__(RF_THREADS) refine_q_kernel(const float *__res
             for (int k = 0; k < NH; k++)
                 v[c][k] = live[c] ? __ldcs(reinterpret_cast<const float4 *>(stored + (uint64_t)pv[c] * n) + k * 8 + ql)
                                   : make_float4(0, 0, 0, 0);
+        if (f0 + RF_C < fend) fetch(f0 + RF_C);
 #pragma unroll
         for (int c = 0; c < RF_C; c++) {
             if (!live[c]) continue;

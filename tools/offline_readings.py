@@ -275,10 +275,57 @@ def part_next3(out):
     print("next3", json.dumps(out["next3"]), flush=True)
 
 
+def part_early(out):
+    """Early exit inside the member test: after k of the 16 lookups, the warp (32 members of one
+    alive leaf, one query) stops if every lane's partial u8 sum already exceeds 254. Fraction of
+    (leaf, query) pairs that stop at k, in segment order 0..15 and in a per-query order (segments
+    by descending mean table entry), and the lookups per pair that implies."""
+    import datagen
+
+    wl = datagen.Workload("early_walk_4M", 4_000_000, 256, 24, "walk", 51, 52, 24, 0)
+    ix = build(wl, first_band=-1)
+    q, T, dbg = queries_and_T(ix, wl, 24)
+    ex = ix.export(0, wl.N, sax=True, perm=True)
+    ix.close()
+    ws = ex["sax"][ex["perm"].astype(np.int64)]
+    n = len(ws) // LEAF * LEAF
+    ws = ws[:n]
+    mn, mx = leaf_boxes(ws)
+    ks = (2, 4, 6, 8, 10, 12, 14)
+    stop = {o: np.zeros(len(ks)) for o in ("fixed", "by_query")}
+    pairs = 0
+    for i in range(len(T)):
+        e8 = lut_u8(dbg["lut"][i], T[i])
+        alive = np.nonzero(leaf_node_e8(mn, mx, dbg["q_sax"][i].astype(np.int64), e8) <= 254)[0]
+        if not len(alive):
+            continue
+        idx = (alive[:, None] * LEAF + np.arange(LEAF)[None]).ravel()
+        w = ws[idx].astype(np.int64)
+        pairs += len(alive)
+        for o, order in (("fixed", np.arange(16)), ("by_query", np.argsort(-e8.mean(axis=1), kind="stable"))):
+            part = np.zeros(len(idx), np.int32)
+            done = 0
+            for j, s in enumerate(order):
+                part += e8[s][w[:, s]]
+                if j + 1 in ks:
+                    stop[o][ks.index(j + 1)] += int((part.reshape(-1, LEAF) > 254).all(axis=1).sum())
+                    done += 1
+    res = {"workload": "4M walks x 256 (seed 51), 24 walk queries (seed 52), T = final BSF (1 + 2^-12)",
+           "pairs": pairs, "k": list(ks)}
+    for o in stop:
+        f = stop[o] / pairs
+        res[o + "_stopped_after_k"] = [round(float(v), 4) for v in f]
+        # one exit test at k: k lookups for every pair, 16 - k more for the pairs that go on
+        res[o + "_lookups_per_pair_one_test"] = {int(k): round(float(k + (16 - k) * (1 - f[j])), 2)
+                                                 for j, k in enumerate(ks)}
+    out["early"] = res
+    print("early", json.dumps(res), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default="gpurun_out/offline_readings.json")
-    ap.add_argument("--parts", nargs="+", default=["r5", "r6b", "r14", "next3"])
+    ap.add_argument("--parts", nargs="+", default=["r5", "r6b", "r14", "next3", "early"])
     a = ap.parse_args()
     import torch
 
@@ -286,7 +333,7 @@ def main():
     out = {"when": time.strftime("%Y-%m-%dT%H:%M:%SZ", time.gmtime())}
     for p in a.parts:
         t0 = time.time()
-        {"r5": part_r5, "r6b": part_r6b, "r14": part_r14, "next3": part_next3}[p](out)
+        {"r5": part_r5, "r6b": part_r6b, "r14": part_r14, "next3": part_next3, "early": part_early}[p](out)
         out.setdefault("seconds", {})[p] = round(time.time() - t0, 1)
         with open(a.out, "w") as f:
             json.dump(out, f, indent=1)
