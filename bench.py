@@ -173,7 +173,7 @@ def main():
     from paper_2009_01614_b200 import dist as pdist
 
     Q = args.queries or wl.Q
-    opts = {k: int(v) for k, v in (o.split("=", 1) for o in args.opt)}
+    opts = {k: (float(v) if "." in v else int(v)) for k, v in (o.split("=", 1) for o in args.opt)}
     wlq = pdist.rank_workload(wl, rank)  # replicas: every rank answers its own queries
     # ---- build (a1-a5), timed on its own
     free, _ = torch.cuda.mem_get_info()

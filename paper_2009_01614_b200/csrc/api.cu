@@ -98,7 +98,7 @@ static cudaError_t dmalloc(T **p, size_t count, size_t *acc) {
 
 static void free_scratch(isax_index *ix) {
     QueryScratch &q = ix->qs;
-    cudaFree(q.qy); cudaFree(q.qpaa); cudaFree(q.qsax); cudaFree(q.lut); cudaFree(q.lut8); cudaFree(q.qconst); cudaFree(q.pwin);
+    cudaFree(q.qy); cudaFree(q.qpaa); cudaFree(q.qsax); cudaFree(q.lut); cudaFree(q.lut8); cudaFree(q.lut8c); cudaFree(q.qconst); cudaFree(q.pwin);
     cudaFree(q.cand); cudaFree(q.candq); cudaFree(q.cand2); cudaFree(q.candq2); cudaFree(q.cnt_f); cudaFree(q.qscale); cudaFree(q.qT);
     cudaFree(q.near); cudaFree(q.near_off); cudaFree(q.near_cap);
     cudaFree(q.qmap); cudaFree(q.qband); cudaFree(q.cand_hist); cudaFree(q.task_ctr); cudaFree(q.qmap2);
@@ -144,6 +144,7 @@ static int alloc_scratch_cap(isax_index *ix, uint32_t cap) {
     A(qsax, (size_t)Q * W);
     A(lut, (size_t)Q * W * CARD);
     A(lut8, (size_t)Q * W * CARD);
+    A(lut8c, (size_t)Q * (W / 2) * CARD);
     A(qconst, 2 * (size_t)Q);
     A(pwin, (size_t)Q * MAX_PROBES);
     A(cand, (size_t)Q * cap);

@@ -133,6 +133,7 @@ struct QueryScratch {
     uint8_t *qsax = nullptr;        // [Q][16]
     float *lut = nullptr;           // [Q][16][256] fp32, rounded down
     uint8_t *lut8 = nullptr;        // [Q][16][256] u8 scan table of each active slot (R11b)
+    uint8_t *lut8c = nullptr;       // [Q][8][256] u8 coarse table of each active slot: segment pairs at 4 bits (R17)
     uint4 *qconst = nullptr;        // [Q][2] scan constants of each active slot (band lo, T, window, positions)
     uint32_t *win = nullptr;        // [Q][2] window [start, end)
     uint32_t *pwin = nullptr;       // [Q][MAX_PROBES]: kept probe window starts (probe_L rows each), count last

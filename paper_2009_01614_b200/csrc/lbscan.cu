@@ -93,6 +93,28 @@ __device__ __forceinline__ uint32_t node_e8(uint32_t ub, const uint4 &qa, const 
     return es;
 }
 
+// coarse member bound (R17): 8 lookups in the query's [8][256] pair table at cb (256-aligned). P0 / P1
+// hold the pair indices of a word: byte k of P0 = hi4(sym_k) | hi4(sym_{k+4}) << 4 (pairs 0..3), byte k
+// of P1 = hi4(sym_{8+k}) | hi4(sym_{12+k}) << 4 (pairs 4..7).
+__device__ __forceinline__ void pair_index(const uint4 &wv, uint32_t &P0, uint32_t &P1) {
+    P0 = ((wv.x >> 4) & 0x0F0F0F0Fu) | (wv.y & 0xF0F0F0F0u);
+    P1 = ((wv.z >> 4) & 0x0F0F0F0Fu) | (wv.w & 0xF0F0F0F0u);
+}
+__device__ __forceinline__ uint32_t coarse_e8(uint32_t cb, uint32_t P0, uint32_t P1) {
+    uint32_t a = 0, b = 0;
+#pragma unroll
+    for (int p = 0; p < 4; p++) a += ld_sh_u8(__byte_perm(P0, cb, 0x7650u | (uint32_t)p) + p * CARD);
+#pragma unroll
+    for (int p = 0; p < 4; p++) b += ld_sh_u8(__byte_perm(P1, cb, 0x7650u | (uint32_t)p) + (4 + p) * CARD);
+    return a + b;
+}
+__device__ __forceinline__ void st_sh_v4a(uint32_t a, const uint4 &v) {
+    asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+}
+__device__ __forceinline__ void st_sh_u32a(uint32_t a, uint32_t v) {
+    asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+
 __device__ __forceinline__ uint32_t ld_sh_u32(const uint32_t *p) {
     uint32_t r;
     asm volatile("ld.shared.u32 %0, [%1];" : "=r"(r) : "r"((uint32_t)__cvta_generic_to_shared(p)));
@@ -286,6 +308,18 @@ constexpr uint32_t SUPER = SUPER_SIZE / LEAF_SIZE;  // leaves per super-node
 constexpr uint32_t HYPER = HYPER_SIZE / SUPER_SIZE; // super-nodes per hyper-node
 static_assert(HYPER == 32, "phase A maps the super-nodes of a hyper-node to the lanes of a warp");
 static_assert(LEAF == 32 && SUPER == 32, "phase A maps a super-node to a warp iteration and a leaf to a lane");
+#ifndef ISAX_COARSE
+#define ISAX_COARSE 0
+#endif
+#if ISAX_COARSE
+// the coarse tables (32 KB for 16 queries) and the survivor rings leave room for one CTA per SM
+#ifndef ISAX_LF_THREADS
+#define ISAX_LF_THREADS 1024
+#endif
+#ifndef ISAX_LF_CTAS
+#define ISAX_LF_CTAS 1
+#endif
+#endif
 #ifndef ISAX_LF_THREADS
 #define ISAX_LF_THREADS 512
 #endif
@@ -317,6 +351,10 @@ constexpr uint32_t E_SURE = 237;
 // refined nor needed, only the histogram is), and a query with millions of candidates would
 // otherwise serialise every CTA on its count.
 constexpr uint32_t WB = 64;  // staged candidates per warp
+// R17: (member, query) pairs that pass the coarse test wait in a per-warp ring of SV words + metas
+// until 32 of them fill one full-test batch (lane = pair)
+constexpr uint32_t SV = ISAX_COARSE ? 64 : 0;
+constexpr uint32_t CW = ISAX_COARSE ? (W / 2) * CARD : 0;  // coarse table bytes per query
 __device__ __forceinline__ void wflush(uint2 *wb, uint32_t &wcnt, uint32_t lane, volatile uint32_t *ovf,
                                        const uint32_t *qid, uint32_t *cand, uint16_t *candq, uint32_t *cand_cnt,
                                        uint32_t cap) {
@@ -372,7 +410,8 @@ __global__ void __launch_bounds__(256) scanprep_kernel(const float *__restrict__
                                                        const Band *__restrict__ band,
                                                        const unsigned long long *__restrict__ bsf,
                                                        const uint32_t *__restrict__ win, float onepd,
-                                                       uint8_t *__restrict__ lut8, uint4 *__restrict__ qconst,
+                                                       uint8_t *__restrict__ lut8, uint8_t *__restrict__ lut8c,
+                                                       uint4 *__restrict__ qconst,
                                                        float *__restrict__ qscale, float *__restrict__ qT,
                                                        unsigned long long *__restrict__ bsf_scan, uint32_t B,
                                                        uint32_t *__restrict__ cand_cnt, uint32_t *__restrict__ cand_cnt2,
@@ -405,12 +444,38 @@ __global__ void __launch_bounds__(256) scanprep_kernel(const float *__restrict__
         const float4 v = __ldg(L + e);
         o[e] = none ? 0xFFFFFFFFu : (q8(v.x, sc) | q8(v.y, sc) << 8 | q8(v.z, sc) << 16 | q8(v.w, sc) << 24);
     }
+    // the coarse table (R17): per segment and high nibble a, the smallest entry of its 16 symbols
+    // (q8 is monotone, so that is the entry of the smallest LUT value); then per segment pair
+    // (s1, s2) = (p, p + 4) for p < 4, (p + 4, p + 8) for p >= 4, entry a | b << 4 =
+    // min(255, mn[s1][a] + mn[s2][b]) <= e[s1][c1] + e[s2][c2] for every c1 >> 4 = a, c2 >> 4 = b.
+    __shared__ uint32_t mn[W][16];
+    {
+        const uint32_t sg = threadIdx.x >> 4, a = threadIdx.x & 15u;  // 256 threads = 16 x 16
+        const float *Ls = lut_all + (uint64_t)qi * W * CARD + sg * CARD + 16 * a;
+        float v = __ldg(Ls);
+#pragma unroll
+        for (int c = 1; c < 16; c++) v = fminf(v, __ldg(Ls + c));
+        mn[sg][a] = none ? 255u : q8(v, sc);
+    }
+    __syncthreads();
+    uint32_t *oc = reinterpret_cast<uint32_t *>(lut8c + (uint64_t)i * (W / 2) * CARD);
+    for (uint32_t e = threadIdx.x; e < (W / 2) * CARD / 4; e += blockDim.x) {
+        const uint32_t p = e >> 6, s1 = p < 4 ? p : p + 4, s2 = s1 + 4;
+        uint32_t word = 0;
+#pragma unroll
+        for (uint32_t k = 0; k < 4; k++) {
+            const uint32_t idx = (e & 63u) * 4 + k, a = idx & 15u, b = idx >> 4;
+            word |= min(255u, mn[s1][a] + mn[s2][b]) << (8 * k);
+        }
+        oc[e] = word;
+    }
 }
 
 template <int G>
 __global__ void __launch_bounds__(LF_THREADS, LF_CTAS) leafscan_kernel(
     const uint4 *__restrict__ sax, const uint8_t *__restrict__ lmeta, const uint8_t *__restrict__ smeta,
-    const uint8_t *__restrict__ hmeta, uint32_t N, const float *__restrict__ lut_all, const uint8_t *__restrict__ lut8_all, const uint4 *__restrict__ qconst_all,
+    const uint8_t *__restrict__ hmeta, uint32_t N, const float *__restrict__ lut_all, const uint8_t *__restrict__ lut8_all,
+    const uint8_t *__restrict__ lut8c_all, const uint4 *__restrict__ qconst_all,
     const uint8_t *__restrict__ qsax_all, const uint32_t *__restrict__ qmap, uint32_t nq, uint32_t nleaf,
     uint32_t chunk, uint32_t *__restrict__ cand, uint16_t *__restrict__ candq, uint32_t *__restrict__ cand_cnt, uint32_t cap,
     uint32_t *__restrict__ hist, uint32_t *__restrict__ leaves_alive, unsigned long long *__restrict__ scan_bytes_dev,
@@ -423,10 +488,13 @@ __global__ void __launch_bounds__(LF_THREADS, LF_CTAS) leafscan_kernel(
     const uint32_t lut8_sh = (raw8 + 255u) & ~255u;
     uint8_t *lut8 = smem_dyn + (lut8_sh - raw8);
     constexpr uint32_t NW = LF_THREADS / 32;
-    uint32_t *worklist = reinterpret_cast<uint32_t *>(lut8 + G * W * CARD);  // (leaf offset in chunk) | (query mask << 16)
-    const uint32_t wl_sh = lut8_sh + G * W * CARD;
+    const uint32_t lut8c_sh = lut8_sh + G * W * CARD;  // [G][8][256] coarse tables (R17; CW = 0 without)
+    uint32_t *worklist = reinterpret_cast<uint32_t *>(lut8 + G * (W * CARD + CW));  // (leaf offset in chunk) | (query mask << 16)
+    const uint32_t wl_sh = lut8_sh + G * (W * CARD + CW);
     const uint32_t stage_sh = wl_sh + CHUNK * 4;  // 16-byte aligned
     uint2 *wbuf = reinterpret_cast<uint2 *>(worklist + CHUNK + NW * PD * LEAF * 4) + (threadIdx.x >> 5) * WB;  // this warp's staged candidates
+    // this warp's survivor ring (R17): SV words, then SV metas (member offset in the chunk | slot << 20)
+    const uint32_t sv_sh = wl_sh + CHUNK * 4 + NW * PD * LEAF * 16 + NW * WB * 8 + (threadIdx.x >> 5) * SV * 20;
     uint32_t wcnt = 0;
     __shared__ QConst qc[G];
     __shared__ uint4 qsym[G][2];  // the query's 16 symbols as 8 u16x2 pairs
@@ -504,6 +572,13 @@ __global__ void __launch_bounds__(LF_THREADS, LF_CTAS) leafscan_kernel(
                 constexpr uint32_t PER = W * CARD / 16;
                 for (uint32_t e = t; e < G * PER; e += LF_THREADS)
                     dst[e] = g0 + e / PER < nq ? __ldg(src + e) : make_uint4(FULL, FULL, FULL, FULL);
+#if ISAX_COARSE
+                const uint4 *srcc = reinterpret_cast<const uint4 *>(lut8c_all + (uint64_t)g0 * CW);
+                uint4 *dstc = reinterpret_cast<uint4 *>(lut8 + G * W * CARD);
+                constexpr uint32_t PERC = CW / 16;
+                for (uint32_t e = t; e < G * PERC; e += LF_THREADS)
+                    dstc[e] = g0 + e / PERC < nq ? __ldg(srcc + e) : make_uint4(FULL, FULL, FULL, FULL);
+#endif
             }
             __syncthreads();
         }
@@ -615,6 +690,46 @@ __global__ void __launch_bounds__(LF_THREADS, LF_CTAS) leafscan_kernel(
             pfo = (pfo + SLOT) & (PD * SLOT - 1);
         }
         uint32_t co = 0;  // ring offset of the entry being consumed
+#if ISAX_COARSE
+        // R17: the full member test (below) runs on batches of 32 (member, query) pairs that passed
+        // the coarse test, one pair per lane; the survivors of a batch get the exact rule and emit.
+        uint32_t sv_head = 0, sv_tail = 0;  // warp-uniform ring positions
+        auto full_batch = [&](uint32_t cnt) {
+            __syncwarp();
+            const bool have = lane < cnt;
+            const uint32_t ri = (sv_head + lane) & (SV - 1u);
+            const uint4 wv = have ? ld_sh_v4a(sv_sh + ri * 16u) : make_uint4(0u, 0u, 0u, 0u);
+            const uint32_t m = have ? ld_sh_u32a(sv_sh + SV * 16u + ri * 4u) : 0u;
+            __syncwarp();
+            sv_head += cnt;
+            const uint32_t g = m >> 20;
+            uint32_t e8hi;
+            const uint32_t e8 = word_e8(lut8_sh + g * W * CARD, wv, e8hi);
+            const bool maybe = have && e8 <= 254u;
+            if (!__any_sync(FULL, maybe)) return;
+            // the keep rule, as in the per-query loop without R17 (see there)
+            const uint32_t pos = c0 * LEAF + (m & 0xFFFFFu);
+            const QConst kq = qc[g];
+            const bool band0 = kq.lo < 0.f;
+            const bool first = maybe && band0;
+            const bool check = maybe && !band0;
+            const float lb = check ? word_lb(lut_all + (uint64_t)qid[g] * W * CARD, wv) : 0.f;
+            const bool keep = (first || (check && lb > kq.lo && lb <= kq.T)) && pos_ok(kq, pos);
+            uint32_t b = e8 <= E_SURE ? e8 : B_UNCHECKED;
+            if (check) {
+                const float y = __fmul_rd(lb, qsc[g]);
+                b = lb > 0.f ? (y >= 254.f ? 254u : (uint32_t)y) : 0u;
+            }
+            if (keep) atomicAdd(&shist[g][first ? min(e8 * HIST_BINS / 254u, HIST_BINS - 1) : hist_bin(lb, kq.lo, kq.T)], 1u);
+            // lanes of several slots: a slot whose list overflowed stops appending (as emit)
+            const bool k2 = keep && !s_ovf[g];
+            const uint32_t bal = __ballot_sync(FULL, k2);
+            if (!bal) return;
+            if (k2) wbuf[wcnt + __popc(bal & lt)] = make_uint2(pos, (g << 16) | b | (e8hi << 8));
+            wcnt += __popc(bal);
+            if (wcnt > WB - 32) wflush(wbuf, wcnt, lane, s_ovf, qid, cand, candq, cand_cnt, cap);
+        };
+#endif
         for (uint32_t e = warp; e < nwl; e += NW) {
             if (pf < nwl) cp_async16_sh(ring + pfo, gsrc + (size_t)(ld_sh_u32a(wl_sh + 4 * pf) & 0xFFFFu) * SLOT);
             cp_async_commit();
@@ -625,6 +740,27 @@ __global__ void __launch_bounds__(LF_THREADS, LF_CTAS) leafscan_kernel(
             const uint32_t wp = ring + co;
             const uint4 wv = ld_sh_v4a(wp);
             co = (co + SLOT) & (PD * SLOT - 1);
+#if ISAX_COARSE
+            // coarse test per query of the mask (8 lookups, R17); passing pairs join the ring
+            const uint32_t memb = (ent & 0xFFFFu) * LEAF + lane;  // member offset in the chunk
+            const bool inN = c0 * LEAF + memb < N;
+            uint32_t P0, P1;
+            pair_index(wv, P0, P1);
+#pragma unroll 1
+            for (uint32_t mm = ent >> 16; mm; mm &= mm - 1) {
+                const uint32_t g = __ffs(mm) - 1;
+                const bool pass = inN && coarse_e8(lut8c_sh + g * CW, P0, P1) <= 254u;
+                const uint32_t bal = __ballot_sync(FULL, pass);
+                if (!bal) continue;
+                if (pass) {
+                    const uint32_t ri = (sv_tail + __popc(bal & lt)) & (SV - 1u);
+                    st_sh_v4a(sv_sh + ri * 16u, wv);
+                    st_sh_u32a(sv_sh + SV * 16u + ri * 4u, memb | (g << 20));
+                }
+                sv_tail += __popc(bal);
+                if (sv_tail - sv_head >= 32u) full_batch(32u);
+            }
+#else
             // rolled loop over the queries that kept the leaf: unrolling it over G made the
             // kernel ~120 KB of SASS, and instruction-cache misses became the top stall
 #pragma unroll 1
@@ -662,7 +798,11 @@ __global__ void __launch_bounds__(LF_THREADS, LF_CTAS) leafscan_kernel(
                     atomicAdd(&shist[g][first ? min(e8 * HIST_BINS / 254u, HIST_BINS - 1) : hist_bin(lb, kq.lo, kq.T)], 1u);
                 emit(keep, pos, b | (e8hi << 8), g, lane, lt, wbuf, wcnt, s_ovf, qid, cand, candq, cand_cnt, cap);
             }
+#endif
         }
+#if ISAX_COARSE
+        if (sv_tail != sv_head) full_batch(sv_tail - sv_head);  // the task's last pairs (warp-uniform)
+#endif
         if (wcnt) wflush(wbuf, wcnt, lane, s_ovf, qid, cand, candq, cand_cnt, cap);  // (warp-uniform)
         cp_async_wait<0>();  // the trailing (empty) groups
         __syncthreads();
@@ -676,8 +816,8 @@ __global__ void __launch_bounds__(LF_THREADS, LF_CTAS) leafscan_kernel(
 template <int G>
 static void launch_leaf(const isax_index *ix, uint32_t nq, const uint32_t *qmap, cudaStream_t s) {
     constexpr uint32_t NW = LF_THREADS / 32;
-    const size_t smem = (size_t)G * W * CARD + 256 + CHUNK * 4 + (size_t)NW * PD * LEAF * sizeof(uint4) +
-                        (size_t)NW * WB * sizeof(uint2);
+    const size_t smem = (size_t)G * (W * CARD + CW) + 256 + CHUNK * 4 + (size_t)NW * PD * LEAF * sizeof(uint4) +
+                        (size_t)NW * WB * sizeof(uint2) + (size_t)NW * SV * 20;
     // per launch (the attribute is per device; a failure surfaces as the launch's error)
     cudaFuncSetAttribute(leafscan_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int dev = 0, sms = 148;
@@ -702,8 +842,8 @@ static void launch_leaf(const isax_index *ix, uint32_t nq, const uint32_t *qmap,
     const uint32_t run = ISAX_TASK_RUN;
     const QueryScratch &qs = ix->qs;
     leafscan_kernel<G><<<grid, LF_THREADS, smem, s>>>(
-        reinterpret_cast<const uint4 *>(ix->sax), ix->lmeta, ix->smeta, ix->hmeta, (uint32_t)ix->N, qs.lut, qs.lut8, qs.qconst,
-        qs.qsax, qmap, nq, nleaf, chunk, qs.cand, qs.candq, qs.cand_cnt, qs.cand_cap, qs.cand_hist, qs.counters_leaf,
+        reinterpret_cast<const uint4 *>(ix->sax), ix->lmeta, ix->smeta, ix->hmeta, (uint32_t)ix->N, qs.lut, qs.lut8, qs.lut8c,
+        qs.qconst, qs.qsax, qmap, nq, nleaf, chunk, qs.cand, qs.candq, qs.cand_cnt, qs.cand_cap, qs.cand_hist, qs.counters_leaf,
         qs.scan_bytes_dev, qs.task_ctr, run);
 }
 
@@ -712,7 +852,7 @@ uint64_t launch_lbscan(const isax_index *ix, uint32_t nq, uint32_t B, const uint
     if (!nq) return 0;
     const float onepd = 1.0f + delta;
     const QueryScratch &qs = ix->qs;
-    scanprep_kernel<<<nq, 256, 0, s>>>(qs.lut, qmap, band, qs.bsf, qs.win, onepd, qs.lut8, qs.qconst, qs.qscale, qs.qT, qs.bsf_scan,
+    scanprep_kernel<<<nq, 256, 0, s>>>(qs.lut, qmap, band, qs.bsf, qs.win, onepd, qs.lut8, qs.lut8c, qs.qconst, qs.qscale, qs.qT, qs.bsf_scan,
                                       B, qs.cand_cnt, qs.cand_cnt2, qs.cnt_hi, qs.cnt_f, qs.cand_hist, qs.task_ctr);
     if (ix->opts.flags & ISAX_FLAG_FLAT_SCAN) {  // ParIS flat scan, kept for A/B measurement
         const uint32_t G = nq >= 4 ? 4 : nq;
