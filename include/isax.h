@@ -157,6 +157,12 @@ int isax_debug_candidates(const isax_index *ix, uint32_t q, uint32_t *out_pos, u
 int isax_debug_plan_round(float *band_lo_hi, uint32_t *band_pos, uint32_t *state, uint32_t cand_cnt, uint32_t cap,
                           const uint32_t *hist, int near_ovf, float tused, float bsf_lim, uint32_t N);
 
+/* Debug / test entry (device): returns 1 if this build has the device-side bounds checks
+ * (libisax_bounds.so, -DISAX_BOUNDS), else 0. With fire != 0 it launches one kernel whose check
+ * fails: the bounds build then returns ISAX_E_CUDA (the trap leaves the CUDA context unusable, so
+ * call it with fire != 0 only in a process of its own); the product build returns 0. */
+int isax_debug_bounds(int fire);
+
 /* Counters of the last isax_nn1 / isax_nn1_async call, as a JSON object written to buf.
  * It holds per-query window, window_rows (rows the approximate answer refined), candidates,
  * refined, abandoned, skipped, rounds, near, leaves_alive and the BSF before and after the scan,

@@ -1,6 +1,7 @@
 """Build the in-tree shared libraries for sm_100a (no torch extension machinery, plain nvcc).
 
   paper_2009_01614_b200/libisax.so   the product: csrc/*.cu behind include/isax.h
+  paper_2009_01614_b200/libisax_bounds.so   the same with device-side bounds checks (-DISAX_BOUNDS; tests only)
   datagen/libisaxgen.so              the seeded input generator (harness; no method arithmetic)
 
 python -m paper_2009_01614_b200.build [--force]
@@ -21,6 +22,9 @@ FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xptxas", "-v
 
 TARGETS = {
     "isax": (os.path.join(PKG, "csrc"), os.path.join(PKG, "libisax.so")),
+    # the same sources with the device-side bounds checks compiled in (ISAX_BOUND, isax_internal.cuh);
+    # tests/test_bounds.py runs the GPU parity suite against it
+    "isax_bounds": (os.path.join(PKG, "csrc"), os.path.join(PKG, "libisax_bounds.so")),
     "isaxgen": (os.path.join(ROOT, "datagen"), os.path.join(ROOT, "datagen", "libisaxgen.so")),
 }
 
@@ -42,7 +46,7 @@ def build_one(name: str, force: bool = False, verbose: bool = False) -> str:
     tmp = out + f".tmp{os.getpid()}"
     objdir = os.path.join(ROOT, "build", name)
     os.makedirs(objdir, exist_ok=True)
-    inc = ["-I", os.path.join(ROOT, "include")]
+    inc = ["-I", os.path.join(ROOT, "include")] + (["-DISAX_BOUNDS"] if name == "isax_bounds" else [])
     objs = [os.path.join(objdir, os.path.basename(s)[:-3] + ".o") for s in srcs]
     cmds = [[NVCC, *ARCH, *FLAGS, *inc, "-c", s, "-o", o] for s, o in zip(srcs, objs)]
     with ThreadPoolExecutor(max_workers=min(8, len(cmds))) as ex:

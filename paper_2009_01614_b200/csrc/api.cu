@@ -621,6 +621,11 @@ static int nn1_device(isax_index *ix, const float *d_q, uint32_t Q, int64_t *d_i
     return result;
 }
 
+#ifdef ISAX_BOUNDS
+// isax_debug_bounds: one check that fails when fire != 0 (shows the mechanism traps)
+__global__ void bounds_probe_kernel(int fire) { ISAX_BOUND(fire == 0); }
+#endif
+
 }  // namespace isax
 
 using namespace isax;
@@ -800,6 +805,18 @@ int isax_debug_candidates(const isax_index *cix, uint32_t q, uint32_t *out_pos, 
         e = cudaMemcpy(out_pos + n1, qs.cand2 + (uint64_t)q * qs.cand_cap + (qs.cand_cap - n2), n2 * sizeof(uint32_t),
                        cudaMemcpyDefault);
     return e == cudaSuccess ? ISAX_OK : cuda_error(e, "isax_debug_candidates");
+}
+
+int isax_debug_bounds(int fire) {
+#ifdef ISAX_BOUNDS
+    if (!fire) return 1;
+    isax::bounds_probe_kernel<<<1, 32>>>(1);
+    const cudaError_t e = cudaDeviceSynchronize();
+    return e == cudaSuccess ? 1 : cuda_error(e, "isax_debug_bounds");
+#else
+    (void)fire;
+    return 0;
+#endif
 }
 
 int isax_debug_plan_round(float *band_lo_hi, uint32_t *band_pos, uint32_t *state, uint32_t cand_cnt, uint32_t cap,

@@ -63,6 +63,7 @@ __device__ __forceinline__ float bsf_d2(unsigned long long p) { return __uint_as
 // sees an overflow and sizes the query's next list from it (api.cu)
 __device__ __forceinline__ void near_append(const NearList &nl, uint32_t q, uint32_t id, uint32_t pos, float d2) {
     const uint32_t k = atomicAdd(&nl.cnt[q], 1u);
+    ISAX_BOUND(id != 0xffffffffu);
     if (k < nl.cap[q]) nl.base[nl.off[q] + k] = NearEntry{id, pos, d2, 0};
 }
 

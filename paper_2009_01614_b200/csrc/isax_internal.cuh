@@ -15,6 +15,24 @@
 
 #include "../../include/isax.h"
 
+// Device-side bounds checks, compiled in only with -DISAX_BOUNDS (libisax_bounds.so, built next to
+// the product library and run by tests/test_bounds.py over the GPU parity suite): a failed check
+// prints the condition and traps, so the call returns ISAX_E_CUDA instead of touching memory
+// outside its arrays. The product build compiles them to nothing.
+#ifdef ISAX_BOUNDS
+#define ISAX_BOUND(cond)                                                                      \
+    do {                                                                                      \
+        if (!(cond)) {                                                                        \
+            printf("isax bounds check failed: %s (%s:%d)\n", #cond, __FILE__, __LINE__);     \
+            __trap();                                                                         \
+        }                                                                                     \
+    } while (0)
+#else
+#define ISAX_BOUND(cond) \
+    do {                 \
+    } while (0)
+#endif
+
 namespace isax {
 
 constexpr int W = 16;        // segments ("w is fixed to 16")

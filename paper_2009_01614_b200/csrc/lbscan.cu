@@ -375,6 +375,7 @@ __device__ __forceinline__ void wflush(uint2 *wb, uint32_t &wcnt, uint32_t lane,
             }
             base = __shfl_sync(peers, base, leader);
             const uint32_t k = base + __popc(peers & ((1u << lane) - 1u));
+            ISAX_BOUND(g < 16u);
             if (base != 0xffffffffu && k < cap) {
                 cand[(uint64_t)q * cap + k] = en.x;
                 candq[(uint64_t)q * cap + k] = (uint16_t)(en.y & 0xFFFFu);
@@ -666,6 +667,7 @@ __global__ void __launch_bounds__(LF_THREADS, LF_CTAS) leafscan_kernel(
                 uint32_t off = 0;
                 if (lane == 0) off = atomicAdd(&wl_cnt, (uint32_t)__popc(bal));
                 off = __shfl_sync(FULL, off, 0);
+                ISAX_BOUND(off + __popc(bal) <= CHUNK && leaf - c0 < 0x10000u);
                 if (alive) worklist[off + __popc(bal & lt)] = (leaf - c0) | (alive << 16);
             }
         }
@@ -722,6 +724,7 @@ __global__ void __launch_bounds__(LF_THREADS, LF_CTAS) leafscan_kernel(
             }
             if (keep) atomicAdd(&shist[g][first ? min(e8 * HIST_BINS / 254u, HIST_BINS - 1) : hist_bin(lb, kq.lo, kq.T)], 1u);
             // lanes of several slots: a slot whose list overflowed stops appending (as emit)
+            ISAX_BOUND(!keep || pos < N);
             const bool k2 = keep && !s_ovf[g];
             const uint32_t bal = __ballot_sync(FULL, k2);
             if (!bal) return;
@@ -752,6 +755,7 @@ __global__ void __launch_bounds__(LF_THREADS, LF_CTAS) leafscan_kernel(
                 const bool pass = inN && coarse_e8(lut8c_sh + g * CW, P0, P1) <= 254u;
                 const uint32_t bal = __ballot_sync(FULL, pass);
                 if (!bal) continue;
+                ISAX_BOUND(sv_tail - sv_head + __popc(bal) <= SV);
                 if (pass) {
                     const uint32_t ri = (sv_tail + __popc(bal & lt)) & (SV - 1u);
                     st_sh_v4a(sv_sh + ri * 16u, wv);
@@ -796,6 +800,7 @@ __global__ void __launch_bounds__(LF_THREADS, LF_CTAS) leafscan_kernel(
                 }
                 if (keep)
                     atomicAdd(&shist[g][first ? min(e8 * HIST_BINS / 254u, HIST_BINS - 1) : hist_bin(lb, kq.lo, kq.T)], 1u);
+                ISAX_BOUND(!keep || pos < N);
                 emit(keep, pos, b | (e8hi << 8), g, lane, lt, wbuf, wcnt, s_ovf, qid, cand, candq, cand_cnt, cap);
             }
 #endif
@@ -994,6 +999,7 @@ __global__ void __launch_bounds__(CK_THREADS, ISAX_CK_MINB) candcheck_kernel(
         for (int u = 0; u < U; u++)
             hi[u] = keep[u] && b[u] > (qk[u] == q0 ? b1 : B_SPLIT) && pre[qk[u] + 1] - pre[qk[u]] > SPLIT_MIN;
         auto put = [&](uint32_t qq, uint32_t idx, bool h, uint32_t p, uint32_t bb) {
+            ISAX_BOUND(idx < cap && qq < Q);
             const uint64_t k2 = (uint64_t)qq * cap + (h ? cap - 1 - idx : idx);
             cand2[k2] = p;
             candq2[k2] = (uint16_t)bb;

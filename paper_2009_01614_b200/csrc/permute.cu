@@ -38,6 +38,7 @@ __global__ void gather_rows_kernel(const float *__restrict__ x, const double2 *_
     const uint64_t wpb = blockDim.x / 32;
     for (uint64_t pos = blockIdx.x * wpb + threadIdx.x / 32; pos < N; pos += (uint64_t)gridDim.x * wpb) {
         const uint32_t id = perm[pos];
+        ISAX_BOUND(id < N);
         norm_row(x + (uint64_t)id * n, stored + pos * n, musig[id], n, lane);
     }
 }
@@ -49,6 +50,7 @@ __global__ void scatter_rows_kernel(const float *__restrict__ x, uint64_t count,
     const uint64_t wpb = blockDim.x / 32;
     for (uint64_t r = blockIdx.x * wpb + threadIdx.x / 32; r < count; r += (uint64_t)gridDim.x * wpb) {
         const uint64_t id = id0 + r;
+        ISAX_BOUND(inv[id] < 0xffffffffu);
         norm_row(x + r * n, stored + (uint64_t)inv[id] * n, musig[id], n, lane);
     }
 }
@@ -56,7 +58,10 @@ __global__ void scatter_rows_kernel(const float *__restrict__ x, uint64_t count,
 __global__ void gather_sax_kernel(const uint4 *__restrict__ sax_by_id, const uint32_t *__restrict__ perm, uint64_t N,
                                   uint4 *__restrict__ sax) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < N; i += (uint64_t)gridDim.x * blockDim.x)
+    {
+        ISAX_BOUND(perm[i] < N);
         sax[i] = sax_by_id[perm[i]];
+    }
 }
 
 __global__ void invert_perm_kernel(const uint32_t *__restrict__ perm, uint64_t N, uint32_t *__restrict__ inv) {

@@ -307,10 +307,13 @@ __global__ void __launch_bounds__(256) window_kernel(const float *__restrict__ s
     const uint32_t r0 = blockIdx.x * WIN_ROWS;
     if (r0 >= rows) return;
     const uint32_t r1 = min(rows, r0 + WIN_ROWS);
+    ISAX_BOUND(ws <= we && we <= N);
     auto row_pos = [&](uint32_t r) -> uint32_t {
         if (r < L) return ws + r;
         r -= L;
-        return pwin[q * MAX_PROBES + r / lp] + r % lp;
+        const uint32_t p = pwin[q * MAX_PROBES + r / lp] + r % lp;
+        ISAX_BOUND(r / lp < MAX_PROBES - 1 && p < N);
+        return p;
     };
     float4 qv[NS];
 #pragma unroll

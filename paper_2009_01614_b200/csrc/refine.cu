@@ -30,7 +30,7 @@ __global__ void __launch_bounds__(RF_THREADS) refine_kernel(const float *__restr
                                                            const uint32_t *__restrict__ cand,
                                                            const uint32_t *__restrict__ cand_cnt, uint32_t cap,
                                                            unsigned long long *__restrict__ bsf, NearList nl,
-                                                           uint32_t *__restrict__ counters, float onepd) {
+                                                           uint32_t *__restrict__ counters, float onepd, uint32_t N) {
     __shared__ uint32_t pre[RF_MAXQ + 1];
     const uint32_t t = threadIdx.x, lane = t & 31;
     if (t == 0) {
@@ -69,6 +69,7 @@ __global__ void __launch_bounds__(RF_THREADS) refine_kernel(const float *__restr
             }
         }
         const uint32_t pos = cand[(uint64_t)q * cap + (f - pre[q])];
+        ISAX_BOUND(pos < N && f - pre[q] < cap);
         const float *row = stored + (uint64_t)pos * n;
         const float lim = bsf_d2(*((volatile unsigned long long *)&bsf[q])) * onepd;
         float acc = 0.f;
@@ -132,7 +133,7 @@ __global__ void __launch_bounds__(RF_THREADS) refine_q_kernel(const float *__res
                                                              const uint32_t *__restrict__ cand_cnt, uint32_t cap,
                                                              unsigned long long *__restrict__ bsf, NearList nl,
                                                              uint32_t *__restrict__ counters, float onepd,
-                                                             unsigned long long *__restrict__ refine_bytes) {
+                                                             unsigned long long *__restrict__ refine_bytes, uint32_t N) {
     __shared__ uint32_t pre[RF_MAXQ + 1];
     const uint32_t t = threadIdx.x, lane = t & 31, ql = lane & 7;
     unsigned long long rows_read = 0;  // half rows read by this quarter
@@ -184,6 +185,7 @@ __global__ void __launch_bounds__(RF_THREADS) refine_q_kernel(const float *__res
             live[c] = f0 + c < fend;
             qv[c] = qn[c];
             pv[c] = pn[c];
+            ISAX_BOUND(!live[c] || (pv[c] < N && qv[c] < Q));
             b2v[c] = bn[c];
         }
         float4 v[RF_C][NH];
@@ -406,7 +408,7 @@ void launch_refine(const isax_index *ix, uint32_t Q, float delta, cudaStream_t s
     case K:                                                                                                         \
         refine_q_kernel<K><<<grid, RF_THREADS, 0, s>>>(ix->stored, ix->perm, ix->n, qs.qy, Q, list, listq, qs.qscale, \
                                                        cnt, qs.cand_cap, qs.bsf, nl, qs.counters,                   \
-                                                       onepd, bytes);                                               \
+                                                       onepd, bytes, (uint32_t)ix->N);                              \
         break;
                 RQ_CASE(1) RQ_CASE(2) RQ_CASE(3) RQ_CASE(4)
 #undef RQ_CASE
@@ -418,7 +420,7 @@ void launch_refine(const isax_index *ix, uint32_t Q, float delta, cudaStream_t s
 #define RF_CASE(K)                                                                                              \
     case K:                                                                                                     \
         refine_kernel<K><<<grid, RF_THREADS, 0, s>>>(ix->stored, ix->perm, ix->n, qs.qy, Q, list, cnt,            \
-                                                     qs.cand_cap, qs.bsf, nl, qs.counters, onepd);                   \
+                                                     qs.cand_cap, qs.bsf, nl, qs.counters, onepd, (uint32_t)ix->N);  \
         break;
         switch (ns) {
             RF_CASE(1) RF_CASE(2) RF_CASE(3) RF_CASE(4) RF_CASE(5) RF_CASE(6) RF_CASE(7) RF_CASE(8)
@@ -569,6 +571,7 @@ __global__ void __launch_bounds__(FZ_THREADS) finalize_kernel(const float *__res
     const float lim = bsf_d2(fin) * onepd;
     const uint32_t cnt = min(nl.cnt[q], nl.cap[q]);
     const NearEntry *list = nl.base + nl.off[q];
+    ISAX_BOUND(cnt <= nl.cap[q]);
     const float *qr = qy + (uint64_t)q * n;
     const double INF64 = __longlong_as_double(0x7ff0000000000000ll);
     // fp64 d^2 of entry k (+inf if it is not within (1 + delta) of the final BSF)

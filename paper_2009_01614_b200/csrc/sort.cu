@@ -137,6 +137,7 @@ __global__ void __launch_bounds__(RS_THREADS) rs_scatter(const uint4 *__restrict
         __syncthreads();
         if (valid) {
             const uint32_t dst = wcnt[warp][d] + rank;
+            ISAX_BOUND(dst < N);
             kout[dst] = k;
             vout[dst] = v;
         }

@@ -52,6 +52,7 @@ isax_debug_plan_round = _sig("isax_debug_plan_round", [_P, _P, _P, _U32, _U32, _
                                                        ctypes.c_float, _U32])
 isax_info = _sig("isax_info", [_P, ctypes.POINTER(_U64), ctypes.POINTER(_U32), ctypes.POINTER(_U32),
                                ctypes.POINTER(_U32), ctypes.POINTER(_U64)])
+isax_debug_bounds = _sig("isax_debug_bounds", [ctypes.c_int])
 isax_free = _sig("isax_free", [_P], None)
 isax_last_error = _sig("isax_last_error", [], ctypes.c_char_p)
 isax_version = _sig("isax_version", [], ctypes.c_char_p)
