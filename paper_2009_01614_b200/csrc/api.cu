@@ -101,7 +101,7 @@ static void free_scratch(isax_index *ix) {
     cudaFree(q.qy); cudaFree(q.qpaa); cudaFree(q.qsax); cudaFree(q.lut); cudaFree(q.lut8); cudaFree(q.lut8c); cudaFree(q.qconst); cudaFree(q.pwin);
     cudaFree(q.cand); cudaFree(q.candq); cudaFree(q.cand2); cudaFree(q.candq2); cudaFree(q.cnt_f); cudaFree(q.qscale); cudaFree(q.qT);
     cudaFree(q.near); cudaFree(q.near_off); cudaFree(q.near_cap);
-    cudaFree(q.qmap); cudaFree(q.qband); cudaFree(q.cand_hist); cudaFree(q.task_ctr); cudaFree(q.qmap2);
+    cudaFree(q.qmap); cudaFree(q.qband); cudaFree(q.cand_hist); cudaFree(q.task_ctr); cudaFree(q.qmap2); cudaFree(q.scan_entries); cudaFree(q.scan_ctl);
     cudaFree(q.status);  // bsf, bsf_scan, cand_cnt, cand_cnt2, cnt_hi, near_cnt, flag, counters, win, leaves, byte counters
     if (q.h_mirror) cudaFreeHost(q.h_mirror);
     q = QueryScratch{};
@@ -161,6 +161,9 @@ static int alloc_scratch_cap(isax_index *ix, uint32_t cap) {
     A(qband, Q);
     A(cand_hist, (size_t)Q * HIST_BINS);
     A(task_ctr, 1);
+    q.scan_groups = (Q + 15) / 16 + 1;  // (a batch of 2-15 queries scans in two groups of 1-8)
+    A(scan_entries, (size_t)q.scan_groups * ((ix->N + SUPER_SIZE - 1) / SUPER_SIZE));
+    A(scan_ctl, 3 * (size_t)q.scan_groups);
     A(qmap2, Q);
 #undef A
     if (e == cudaSuccess) {
@@ -236,7 +239,7 @@ static int build_impl(const Source &src, uint64_t N, uint32_t n, uint32_t w, uin
         cudaStreamSynchronize(s);
         cudaFree(sax_by_id); cudaFree(keys); cudaFree(musig); cudaFree(ids); cudaFree(bad); cudaFree(inv);
         cudaFree(stage);
-        cudaFree(ix->stored); cudaFree(ix->sax); cudaFree(ix->perm); cudaFree(ix->lmeta); cudaFree(ix->smeta); cudaFree(ix->hmeta);
+        cudaFree(ix->stored); cudaFree(ix->sax); cudaFree(ix->perm); cudaFree(ix->lmeta); cudaFree(ix->cmeta); cudaFree(ix->smeta); cudaFree(ix->hmeta);
         cudaFree(ix->skey); cudaFree(ix->ksplit);
         delete ix;
         cudaStreamDestroy(s);
@@ -296,9 +299,10 @@ static int build_impl(const Source &src, uint64_t N, uint32_t n, uint32_t w, uin
     TRY(dmalloc(&ix->ksplit, (N + SUPER_SIZE - 1) / SUPER_SIZE, &ix->device_bytes));
     launch_superkd(ix->sax, ix->perm, N, ix->skey, ix->ksplit, s);
     TRY(dmalloc(&ix->lmeta, ((N + LEAF_SIZE - 1) / LEAF_SIZE) * 32, &ix->device_bytes));
+    TRY(dmalloc(&ix->cmeta, (npad / KD_CELL) * 32, &ix->device_bytes));
     TRY(dmalloc(&ix->smeta, ((N + SUPER_SIZE - 1) / SUPER_SIZE) * 32, &ix->device_bytes));
     TRY(dmalloc(&ix->hmeta, ((N + HYPER_SIZE - 1) / HYPER_SIZE) * 32, &ix->device_bytes));
-    launch_leaf_meta(ix->sax, N, ix->lmeta, ix->smeta, ix->hmeta, s);
+    launch_leaf_meta(ix->sax, N, ix->cmeta, ix->lmeta, ix->smeta, ix->hmeta, s);
     TRY(cudaStreamSynchronize(s));
     cudaFree(sax_by_id);
     sax_by_id = nullptr;
@@ -528,6 +532,7 @@ static int nn1_device(isax_index *ix, const float *d_q, uint32_t Q, int64_t *d_i
                 }
                 if (b0 == 0) {
                     ix->st_scan_bytes_first = ix->st_scan_bytes + *hm.scan_bytes_dev;
+                    ix->st_scan_lookups_first = hm.scan_bytes_dev[1];  // (the second word of the 16-byte slot)
                     ix->st_refine1_bytes_first = hm.refine_bytes[0];
                     ix->st_refine2_bytes_first = hm.refine_bytes[1];
                     ix->st_refine_bytes_first = hm.refine_bytes[0] + hm.refine_bytes[1];
@@ -892,6 +897,8 @@ int isax_stats(const isax_index *cix, char *buf, size_t cap) {
     j += ",\"refine1_bytes_first_launch\":" + std::to_string(ix->st_refine1_bytes_first);
     j += ",\"refine2_bytes_first_launch\":" + std::to_string(ix->st_refine2_bytes_first);
     j += ",\"leaf_pairs_first_launch\":" + std::to_string(ix->st_leaf_pairs_first);
+    j += ",\"scan_lookups_first_launch\":" + std::to_string(ix->st_scan_lookups_first);
+    j += ",\"cell_size\":" + std::to_string(KD_CELL);
     j += ",\"scan_queries_first_launch\":" + std::to_string(ix->st_scan_q_first);
     j += ",\"leaves\":" + std::to_string((ix->N + LEAF_SIZE - 1) / LEAF_SIZE);
     j += ",\"leaf_size\":" + std::to_string(LEAF_SIZE);
@@ -925,6 +932,7 @@ void isax_free(isax_index *ix) {
         cudaFree(ix->sax);
         cudaFree(ix->perm);
         cudaFree(ix->lmeta);
+        cudaFree(ix->cmeta);
         cudaFree(ix->smeta);
         cudaFree(ix->hmeta);
         cudaFree(ix->skey);

@@ -41,6 +41,7 @@ constexpr int NEAR_K = 256;  // near-tie list capacity per query, until it overf
 constexpr uint32_t MAX_PROBES = 32;  // 2^probe_bits windows per query, probe_bits <= 5
 constexpr uint32_t HIST_BINS = 64;   // per-query histogram of kept LB^2 inside its band (R10)
 constexpr uint32_t LEAF_SIZE = 32;    // sorted positions per leaf node (R11)
+constexpr uint32_t KD_CELL = 8;       // sorted positions per sub-leaf box: the kd cells of a leaf (R6b, R11c)
 constexpr uint32_t SUPER_SIZE = 1024; // sorted positions per super-node (R11)
 constexpr uint32_t HYPER_SIZE = 32768; // sorted positions per hyper-node (R11)
 constexpr uint32_t B_UNCHECKED = 255;  // candq marker: the exact fp32 rule is still to be applied
@@ -180,7 +181,10 @@ struct QueryScratch {
     uint32_t *counters = nullptr;   // [Q][4]: refined, abandoned, skipped by the u8 bound, (unused)
     uint32_t *counters_leaf = nullptr;  // [Q]: (leaf, query) pairs that survived the node bound
     unsigned long long *scan_bytes_dev = nullptr;  // leaf words and leaf summaries the leaf scan read, bytes (all launches of a call)
-    uint32_t *task_ctr = nullptr;              // work counter of the persistent leaf scan
+    uint32_t *task_ctr = nullptr;              // work counter of the persistent leaf scan (v1 kernel)
+    uint2 *scan_entries = nullptr;             // [scan_groups][ceil(N/SUPER_SIZE)] (super-node, query mask) kept by the node scan
+    uint32_t *scan_ctl = nullptr;              // [scan_groups][3]: entries, claim cursor, work estimate of each query group
+    uint32_t scan_groups = 0;                  // groups allocated: ceil(cap_Q / 16) + 1
     unsigned long long *refine_bytes = nullptr;  // [2] bytes of rows the refine passes 1 and 2 read (all launches of a call)
     uint32_t *flag = nullptr;       // non-finite query flag
     void *status = nullptr;         // the device StatusBlock (bsf, bsf_scan, counters, ... point into it)
@@ -208,6 +212,7 @@ struct isax_index {
     uint4 *skey = nullptr;     // [ceil(N/SUPER_SIZE)] z key of each super-node's first z-order position (R6b)
     isax::KdSplits *ksplit = nullptr;  // [ceil(N/SUPER_SIZE)] first four kd levels of each full super-node (R6b)
     uint8_t *lmeta = nullptr;  // [ceil(N/LEAF_SIZE)][32]: per-leaf min (16 B) and max (16 B) symbols
+    uint8_t *cmeta = nullptr;  // [ceil(N/LEAF_SIZE) * LEAF_SIZE / KD_CELL][32]: per-cell (sub-leaf box) min and max symbols (R11c)
     uint8_t *smeta = nullptr;  // [ceil(N/SUPER_SIZE)][32]: per-super-node min and max symbols
     uint8_t *hmeta = nullptr;  // [ceil(N/HYPER_SIZE)][32]: per-hyper-node min and max symbols
     size_t device_bytes = 0;
@@ -234,6 +239,7 @@ struct isax_index {
     uint64_t st_scan_bytes = 0, st_scan_bytes_first = 0;  // summary bytes the scan read (all / first launch)
     uint64_t st_refine_bytes_first = 0;                    // row bytes the first round's refine read (both passes)
     uint64_t st_refine1_bytes_first = 0, st_refine2_bytes_first = 0;  // ... per pass
+    uint64_t st_scan_lookups_first = 0;                    // LUT lookups of the first scan launch, counted by the kernel (16 per node or member test)
     uint64_t st_leaf_pairs_first = 0, st_scan_q_first = 0; // (leaf, query) pairs kept / queries of the first scan
     cudaEvent_t ev[11] = {};
     // isax_nn1 (host pointers): one stream and device staging, grown on demand
@@ -284,7 +290,7 @@ void launch_window(const isax_index *ix, uint32_t Q, const uint32_t *qmap, float
 void launch_lb_dump(const isax_index *ix, uint32_t Q, uint64_t first_pos, uint64_t count, float *out,
                     cudaStream_t s);
 // lbscan.cu
-void launch_leaf_meta(const uint8_t *sax, uint64_t N, uint8_t *lmeta, uint8_t *smeta, uint8_t *hmeta, cudaStream_t s);
+void launch_leaf_meta(const uint8_t *sax, uint64_t N, uint8_t *cmeta, uint8_t *lmeta, uint8_t *smeta, uint8_t *hmeta, cudaStream_t s);
 // permute.cu: the kd order inside every full super-node (R6b), the super-nodes' smallest keys and
 // their first two kd splits (sax and perm are permuted in place)
 void launch_superkd(uint8_t *sax, uint32_t *perm, uint64_t N, uint4 *skey, KdSplits *ksplit, cudaStream_t s);

@@ -350,7 +350,10 @@ constexpr uint32_t E_SURE = 237;
 // this CTA's appends: the list is dropped for the round anyway (R10: an overflowed list is neither
 // refined nor needed, only the histogram is), and a query with millions of candidates would
 // otherwise serialise every CTA on its count.
-constexpr uint32_t WB = 64;  // staged candidates per warp
+#ifndef ISAX_WB
+#define ISAX_WB 48
+#endif
+constexpr uint32_t WB = ISAX_WB;  // staged candidates per warp (flushed when more than WB - 32 are staged)
 // R17: (member, query) pairs that pass the coarse test wait in a per-warp ring of SV words + metas
 // until 32 of them fill one full-test batch (lane = pair)
 constexpr uint32_t SV = ISAX_COARSE ? 64 : 0;
@@ -417,13 +420,15 @@ __global__ void __launch_bounds__(256) scanprep_kernel(const float *__restrict__
                                                        unsigned long long *__restrict__ bsf_scan, uint32_t B,
                                                        uint32_t *__restrict__ cand_cnt, uint32_t *__restrict__ cand_cnt2,
                                                        uint32_t *__restrict__ cnt_hi, uint32_t *__restrict__ cnt_f,
-                                                       uint32_t *__restrict__ hist, uint32_t *__restrict__ task_ctr) {
+                                                       uint32_t *__restrict__ hist, uint32_t *__restrict__ task_ctr,
+                                                       uint32_t *__restrict__ ctl, uint32_t nctl) {
     const uint32_t i = blockIdx.x;
     // the launch's counters: every batch slot's candidate counts (block 0), the scanned query's
     // histogram (its block), the persistent scan's task counter
     if (i == 0) {
         for (uint32_t q = threadIdx.x; q < B; q += blockDim.x) cand_cnt[q] = cand_cnt2[q] = cnt_hi[q] = cnt_f[q] = 0;
         if (threadIdx.x == 0) *task_ctr = 0;
+        for (uint32_t k = threadIdx.x; k < nctl; k += blockDim.x) ctl[k] = 0;  // the item scan's per-group words
     }
     if (threadIdx.x < HIST_BINS) hist[qmap[i] * HIST_BINS + threadIdx.x] = 0;
     const uint32_t qi = qmap[i];
@@ -818,38 +823,444 @@ __global__ void __launch_bounds__(LF_THREADS, LF_CTAS) leafscan_kernel(
     if (lane == 0 && bytes) atomicAdd(scan_bytes_dev, (unsigned long long)bytes);
 }
 
+// ------------------------------------------------------------------------------------ node scan + item scan
+// (R11c) The default scan since round 2c, two kernels.
+//
+// Why: under a surviving leaf most members still fail (about 2% pass at config 3), because a
+// 32-row box is loose in 16 dimensions. One more node level, the kd cells of KD_CELL = 8 rows (the
+// last two kd levels of superkd_kernel), removes about half of the member tests
+// (tools/offline_readings.py `sub`: 0.52-0.54 of the members lie under surviving cells). To turn
+// that into fewer instructions the member tests are pair-major: a warp iteration tests four
+// surviving (cell, query) pairs, one per quarter warp, instead of the 32 members of one leaf. And
+// the v1 kernel spent a third of its time in per-task fixed costs (the hyper- and super-node
+// phases and their barriers, once per chunk and query group: halving the group size added 0.28 ms
+// at config 3), so the upper node levels moved to a kernel of their own.
+//
+// nodescan_kernel: warp = hyper-node, for the 16 queries of a group: the hyper-node bound (lane =
+//   query), then for every query that kept it the bounds of its 32 super-nodes (lane = super-node).
+//   Output per group: a list of entries (super-node, mask of the queries that kept it), appended
+//   with one global atomic per warp and hyper-node, and the group's work estimate (kept pairs).
+// itemscan_kernel: persistent CTAs (the group's 16 u8 tables in shared memory); CTAs spread over
+//   the groups in proportion to their work and move on when a group's list runs out. Each warp
+//   claims entries from the group's cursor and runs everything below by itself, in registers and a
+//   few hundred bytes of its own shared memory, with no CTA barrier:
+//     A2  per entry: lane = one of the super-node's 32 leaves (summaries loaded once), one node
+//         bound per query of the mask -> items (super-node, query, alive-leaf mask) in a ring;
+//     A3  per item: lane = one of the 4 cells of an alive leaf, 32 cells per iteration: node bound
+//         -> the item's alive cells (a byte list);
+//     B   per item: quarter warp = one alive cell, lane = one of its 8 members: the u8 member test
+//         (16 lookups), a vote, and the rare path of the pairs that pass (exact rule, histogram,
+//         append).
+//   A3 of the next item runs before B of this one, the next entry is claimed and its leaf
+//   summaries prefetched into L2 an entry ahead, and the cell summaries of alive leaves and the
+//   words of alive cells are prefetched into L2 as soon as they are known.
+constexpr uint32_t CELL = KD_CELL;
+constexpr uint32_t CPL = LEAF / CELL;        // cells per leaf
+constexpr uint32_t CPS = SUPER_SIZE / CELL;  // cells per super-node
+static_assert(CPL == 4 && CPS == 128, "A3 maps four cells of a leaf to four lanes; a cell index is 7 bits");
+constexpr uint32_t CLIST = CPS + 8;          // bytes of an alive-cell list: a cell index each, 4 padding entries
+constexpr uint32_t IQ = 32;                  // item ring slots per warp (a power of two; an entry adds at most 16)
+constexpr uint32_t WSC = 32 + 2 * CLIST + IQ * 8;  // per-warp scratch bytes: alive-leaf list, two alive-cell lists, item ring
+// scan control words in qs.scan_ctl (reset by scanprep_kernel): per group its entry count, its
+// claim cursor and its work estimate
+constexpr uint32_t CTL_CNT = 0, CTL_CUR = 1, CTL_WORK = 2, CTL_WORDS = 3;
+
+__device__ __forceinline__ void prefetch_l2(const void *p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
+__device__ __forceinline__ void st_sh_u8a(uint32_t a, uint32_t v) { asm volatile("st.shared.u8 [%0], %1;" ::"r"(a), "r"(v) : "memory"); }
+__device__ __forceinline__ void st_sh_v2a(uint32_t a, uint32_t x, uint32_t y) {
+    asm volatile("st.shared.v2.u32 [%0], {%1,%2};" ::"r"(a), "r"(x), "r"(y) : "memory");
+}
+__device__ __forceinline__ uint2 ld_sh_v2a(uint32_t a) {
+    uint2 r;
+    asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(r.x), "=r"(r.y) : "r"(a));
+    return r;
+}
+
+// the group's u8 tables, query symbols and constants into shared memory (both kernels)
+template <int G, int THREADS>
+__device__ __forceinline__ void load_group(uint32_t g0, uint32_t nq, const uint32_t *__restrict__ qmap,
+                                           const uint8_t *__restrict__ qsax_all, const uint8_t *__restrict__ lut8_all,
+                                           uint8_t *lut8, uint4 (*qsym)[2], uint32_t *qid) {
+    const uint32_t t = threadIdx.x;
+    if (t < G) {
+        const uint32_t slot = g0 + t < nq ? g0 + t : g0;
+        const uint32_t qi = qmap[slot];
+        qid[t] = qi;
+        const uint4 w = reinterpret_cast<const uint4 *>(qsax_all)[qi];
+        qsym[t][0] = make_uint4(lo_u16x2(w.x), hi_u16x2(w.x), lo_u16x2(w.y), hi_u16x2(w.y));
+        qsym[t][1] = make_uint4(lo_u16x2(w.z), hi_u16x2(w.z), lo_u16x2(w.w), hi_u16x2(w.w));
+    }
+    // a padding slot gets all-255 entries (it prunes everything)
+    const uint4 *src = reinterpret_cast<const uint4 *>(lut8_all + (uint64_t)g0 * W * CARD);
+    uint4 *dst = reinterpret_cast<uint4 *>(lut8);
+    constexpr uint32_t PER = W * CARD / 16;
+    for (uint32_t e = t; e < G * PER; e += THREADS)
+        dst[e] = g0 + e / PER < nq ? __ldg(src + e) : make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu);
+}
+
+constexpr int NS_THREADS = 256;
+template <int G>
+__global__ void __launch_bounds__(NS_THREADS) nodescan_kernel(
+    const uint8_t *__restrict__ smeta, const uint8_t *__restrict__ hmeta, uint32_t nsuper, uint32_t nhyper,
+    const uint8_t *__restrict__ lut8_all, const uint8_t *__restrict__ qsax_all, const uint32_t *__restrict__ qmap, uint32_t nq,
+    uint32_t hyper_per_cta, uint2 *__restrict__ entries, uint32_t *__restrict__ ctl,
+    unsigned long long *__restrict__ scan_bytes_dev) {
+    extern __shared__ __align__(16) uint8_t smem_dyn[];
+    const uint32_t raw8 = (uint32_t)__cvta_generic_to_shared(smem_dyn);
+    const uint32_t lut8_sh = (raw8 + 255u) & ~255u;
+    uint8_t *lut8 = smem_dyn + (lut8_sh - raw8);
+    __shared__ uint4 qsym[G][2];
+    __shared__ uint32_t qid[G];
+    const uint32_t t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    constexpr uint32_t FULL = 0xffffffffu, NW = NS_THREADS / 32;
+    const uint32_t lt = (1u << lane) - 1u;
+    const uint32_t grp = blockIdx.y, g0 = grp * G;
+    load_group<G, NS_THREADS>(g0, nq, qmap, qsax_all, lut8_all, lut8, qsym, qid);
+    __syncthreads();
+    const uint4 *smeta4 = reinterpret_cast<const uint4 *>(smeta);
+    const uint4 *hmeta4 = reinterpret_cast<const uint4 *>(hmeta);
+    uint2 *out = entries + (uint64_t)grp * nsuper;
+    uint32_t nnode = 0, work = 0;
+    const uint32_t hb = blockIdx.x * hyper_per_cta, he = min(hb + hyper_per_cta, nhyper);
+    for (uint32_t h = hb + warp; h < he; h += NW) {
+        // the hyper-node bound, lane = query
+        bool alive = false;
+        if (lane < G) {
+            const uint4 a = __ldg(hmeta4 + 2 * (uint64_t)h), b = __ldg(hmeta4 + 2 * (uint64_t)h + 1);
+            alive = node_e8(lut8_sh + lane * W * CARD, qsym[lane][0], qsym[lane][1], a, b) <= 254u;
+            nnode++;
+        }
+        uint32_t hm = __ballot_sync(FULL, alive);
+        if (!hm) continue;
+        // the super-node bounds, lane = super-node (its summary loaded once for all the queries)
+        const uint32_t sn = h * HYPER + lane;
+        const bool ins = sn < nsuper;
+        uint4 a = make_uint4(0, 0, 0, 0), b = a;
+        if (ins) {
+            a = __ldg(smeta4 + 2 * (uint64_t)sn);
+            b = __ldg(smeta4 + 2 * (uint64_t)sn + 1);
+        }
+        uint32_t m = 0;  // the queries that keep this lane's super-node
+#pragma unroll 1
+        for (; hm; hm &= hm - 1) {
+            const uint32_t g = __ffs(hm) - 1;
+            const bool ok = ins && node_e8(lut8_sh + g * W * CARD, qsym[g][0], qsym[g][1], a, b) <= 254u;
+            nnode += ins ? 1u : 0u;
+            m |= (ok ? 1u : 0u) << g;
+        }
+        const uint32_t bal = __ballot_sync(FULL, m != 0);
+        if (bal) {
+            uint32_t off = 0;
+            if (lane == 0) off = atomicAdd(&ctl[CTL_WORDS * grp + CTL_CNT], (uint32_t)__popc(bal));
+            off = __shfl_sync(FULL, off, 0);
+            ISAX_BOUND(off + __popc(bal) <= nsuper);
+            if (m) out[off + __popc(bal & lt)] = make_uint2(sn, m);
+            work += __popc(m);
+        }
+    }
+    work = __reduce_add_sync(FULL, work);
+    nnode = __reduce_add_sync(FULL, nnode);
+    if (lane == 0) {
+        if (work) atomicAdd(&ctl[CTL_WORDS * grp + CTL_WORK], work);
+        if (nnode) {
+            atomicAdd(scan_bytes_dev, 32ull * nnode);
+            atomicAdd(scan_bytes_dev + 1, 16ull * nnode);
+        }
+    }
+}
+
+template <int G>
+__global__ void __launch_bounds__(LF_THREADS, LF_CTAS) itemscan_kernel(
+    const uint4 *__restrict__ sax, const uint8_t *__restrict__ cmeta, const uint8_t *__restrict__ lmeta, uint32_t N,
+    uint32_t nleaf, uint32_t nsuper, const float *__restrict__ lut_all, const uint8_t *__restrict__ lut8_all,
+    const uint4 *__restrict__ qconst_all, const uint8_t *__restrict__ qsax_all, const uint32_t *__restrict__ qmap,
+    uint32_t nq, const uint2 *__restrict__ entries, uint32_t *__restrict__ ctl, uint32_t *__restrict__ cand,
+    uint16_t *__restrict__ candq, uint32_t *__restrict__ cand_cnt, uint32_t cap, uint32_t *__restrict__ hist,
+    uint32_t *__restrict__ leaves_alive, unsigned long long *__restrict__ scan_bytes_dev) {
+    // shared: [G][16][256] u8 tables (256-aligned by hand) | per-warp scratch | per-warp candidate staging | per-warp word ring
+    extern __shared__ __align__(16) uint8_t smem_dyn[];
+    const uint32_t raw8 = (uint32_t)__cvta_generic_to_shared(smem_dyn);
+    const uint32_t lut8_sh = (raw8 + 255u) & ~255u;
+    uint8_t *lut8 = smem_dyn + (lut8_sh - raw8);
+    constexpr uint32_t NW = LF_THREADS / 32;
+    constexpr uint32_t WSC_ALL = (NW * WSC + 15u) & ~15u;
+    const uint32_t t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const uint32_t wsc_sh = lut8_sh + G * W * CARD + warp * WSC;  // this warp's scratch
+    const uint32_t la_sh = wsc_sh, cl0_sh = wsc_sh + 32, iq_sh = wsc_sh + 32 + 2 * CLIST;
+    uint2 *wbuf = reinterpret_cast<uint2 *>(lut8 + G * W * CARD + WSC_ALL) + warp * WB;
+    const uint32_t ring = lut8_sh + G * W * CARD + WSC_ALL + NW * WB * 8 + warp * 1024 + lane * 16;  // two slots of 32 words
+    uint32_t wcnt = 0;
+    __shared__ QConst qc[G];
+    __shared__ uint4 qsym[G][2];  // the query's 16 symbols as 8 u16x2 pairs
+    __shared__ uint32_t qid[G], alive_cnt[G], s_ovf[G];
+    __shared__ float qsc[G];  // 254 / T rounded down (the u8 table scale)
+    __shared__ uint32_t shist[G][HIST_BINS];
+    __shared__ uint32_t s_grp;
+    constexpr uint32_t FULL = 0xffffffffu;
+    const uint32_t lt = (1u << lane) - 1u;
+    const uint32_t ngroups = (nq + G - 1) / G;
+    const uint4 *meta4 = reinterpret_cast<const uint4 *>(lmeta);
+    const uint4 *cmeta4 = reinterpret_cast<const uint4 *>(cmeta);
+    // stats: leaf tests of this thread (32 B summary, 16 lookups each); cell tests and alive cells of
+    // this warp's items (each lane counts the same)
+    uint32_t nnode = 0, ncellt = 0, nmembt = 0;
+    // the CTA's first group: the groups share the CTAs in proportion to their work estimates
+    if (t == 0) {
+        unsigned long long tot = 0;
+        for (uint32_t g = 0; g < ngroups; g++) tot += ctl[CTL_WORDS * g + CTL_WORK];
+        const unsigned long long mine = tot * blockIdx.x / gridDim.x;
+        unsigned long long acc = 0;
+        uint32_t pick = 0;
+        for (uint32_t g = 0; g < ngroups; g++) {
+            acc += ctl[CTL_WORDS * g + CTL_WORK];
+            pick = g;
+            if (mine < acc) break;
+        }
+        s_grp = pick;
+    }
+    __syncthreads();
+    uint32_t grp = s_grp;
+    for (uint32_t visited = 0; visited < ngroups; visited++, grp = grp + 1 == ngroups ? 0 : grp + 1) {
+        const uint32_t nent = ctl[CTL_WORDS * grp + CTL_CNT];
+        const uint32_t g0 = grp * G;
+        // one thread decides whether the group still has entries (the cursor moves under our feet);
+        // the barrier also ends the previous group's flush before its tables are overwritten
+        __syncthreads();
+        if (t == 0) s_grp = ctl[CTL_WORDS * grp + CTL_CUR] < nent ? 1u : 0u;
+        __syncthreads();
+        if (!s_grp) continue;
+        load_group<G, LF_THREADS>(g0, nq, qmap, qsax_all, lut8_all, lut8, qsym, qid);
+        for (uint32_t e = t; e < G * HIST_BINS; e += LF_THREADS) shist[e / HIST_BINS][e % HIST_BINS] = 0;
+        if (t < G) {
+            const bool valid = g0 + t < nq;
+            const uint32_t slot = valid ? g0 + t : g0;
+            alive_cnt[t] = 0;
+            s_ovf[t] = 0;
+            const uint4 k = qconst_all[2 * slot], k2 = qconst_all[2 * slot + 1];
+            qc[t] = valid ? QConst{__uint_as_float(k.x), __uint_as_float(k.y), k.z, k.w, k2.x, k2.y, 0u, 0u}
+                          : QConst{0.f, -1.f, 0u, 0u, 0u, 0u, 0u, 0u};
+            qsc[t] = valid && __uint_as_float(k.y) >= 0.f ? __fdiv_rd(254.0f, __uint_as_float(k.y)) : 0.f;  // as scanprep
+        }
+        __syncthreads();
+        const uint2 *ent = entries + (uint64_t)grp * nsuper;
+        uint32_t *cursor = &ctl[CTL_WORDS * grp + CTL_CUR];
+        // ---- this warp's entries
+        auto claim = [&]() -> uint2 {  // the next entry of the group (x = 0xffffffff when none is left)
+            uint32_t e = 0;
+            if (lane == 0) e = atomicAdd(cursor, 1u);
+            e = __shfl_sync(FULL, e, 0);
+            if (e >= nent) return make_uint2(0xffffffffu, 0u);
+            const uint2 en = __ldg(ent + e);
+            const uint32_t leaf = en.x * SUPER + 4 * lane;  // its leaf summaries (32 x 32 B = eight lines) into L2
+            if (lane < 8 && leaf < nleaf) prefetch_l2(meta4 + 2 * (uint64_t)leaf);
+            return en;
+        };
+        uint32_t iq_head = 0, iq_tail = 0;  // the item ring (warp-uniform): (super-node << 4 | query, alive-leaf mask)
+        // A2 of an entry: one node bound per query of its mask, lane = leaf
+        auto stage_a2 = [&](uint2 en) {
+            const uint32_t leaf = en.x * SUPER + lane;
+            const bool inr = leaf < nleaf;
+            uint4 mn4 = make_uint4(0, 0, 0, 0), mx4 = mn4;
+            if (inr) {
+                mn4 = __ldg(meta4 + 2 * (uint64_t)leaf);
+                mx4 = __ldg(meta4 + 2 * (uint64_t)leaf + 1);
+            }
+            bool any_ok = false;
+#pragma unroll 1
+            for (uint32_t mm = en.y; mm; mm &= mm - 1) {
+                const uint32_t g = __ffs(mm) - 1;
+                const bool ok = inr && node_e8(lut8_sh + g * W * CARD, qsym[g][0], qsym[g][1], mn4, mx4) <= 254u;
+                nnode += inr ? 1u : 0u;
+                any_ok |= ok;
+                const uint32_t bal = __ballot_sync(FULL, ok);
+                if (bal) {
+                    if (lane == 0) {
+                        st_sh_v2a(iq_sh + (iq_tail & (IQ - 1)) * 8, (en.x << 4) | g, bal);
+                        atomicAdd(&alive_cnt[g], (uint32_t)__popc(bal));  // (leaf, query) pairs that survived (stats)
+                    }
+                    iq_tail++;
+                }
+            }
+            // the four cell summaries of a leaf some query kept: one 128-byte line
+            if (any_ok) prefetch_l2(cmeta4 + 2 * ((uint64_t)leaf * CPL));
+            __syncwarp();
+        };
+        // A3 of the ring's next item: lane = cell (idx & 3) of the (idx >> 2)-th alive leaf, 32 cells
+        // per iteration; the alive cells go to the list at cl_sh (padded with four copies of its
+        // first entry, so that B reads and stages one iteration ahead without a bounds test).
+        // Returns (item, alive cells), alive cells = 0 when none.
+        auto stage_a3 = [&](uint32_t cl_sh) -> uint2 {
+            const uint2 it = ld_sh_v2a(iq_sh + (iq_head & (IQ - 1)) * 8);
+            iq_head++;
+            const uint32_t am = it.y, sn = it.x >> 4, g = it.x & 15u;
+            const uint32_t ub = lut8_sh + g * W * CARD;
+            if ((am >> lane) & 1u) st_sh_u8a(la_sh + __popc(am & lt), lane);
+            __syncwarp();
+            const uint32_t ncell = __popc(am) * CPL;
+            const uint4 qa = qsym[g][0], qb = qsym[g][1];
+            const uint4 *cm0 = cmeta4 + 2 * ((uint64_t)sn * CPS);
+            uint32_t m = 0;
+#pragma unroll 1
+            for (uint32_t j = 0; j < ncell; j += 32) {
+                const uint32_t idx = j + lane;
+                const bool have = idx < ncell;
+                const uint32_t cell = ld_sh_u8(la_sh + (have ? idx >> 2 : 0u)) * CPL + (idx & 3u);  // in the super-node
+                bool ok = false;
+                if (have) {
+                    const uint4 a = __ldg(cm0 + 2 * cell), b = __ldg(cm0 + 2 * cell + 1);
+                    ok = node_e8(ub, qa, qb, a, b) <= 254u;
+                }
+                const uint32_t bal = __ballot_sync(FULL, ok);
+                if (ok) {
+                    st_sh_u8a(cl_sh + m + __popc(bal & lt), cell);
+                    prefetch_l2(sax + (uint64_t)sn * SUPER_SIZE + cell * CELL);  // the cell's 8 words: one line
+                }
+                m += __popc(bal);
+            }
+            ncellt += ncell;
+            __syncwarp();
+            if (m) {
+                if (lane < 4) st_sh_u8a(cl_sh + m + lane, ld_sh_u8(cl_sh));
+                nmembt += m;
+            }
+            return make_uint2(it.x, m);
+        };
+        // B of an item: quarter warp = alive cell, lane = member. Each lane stages its own word of
+        // the next iteration's cell (cp.async into the warp's other slot) before this one's lookups.
+        auto stage_b = [&](uint32_t item, uint32_t m, uint32_t cl_sh) {
+            const uint32_t sn = item >> 4, g = item & 15u;
+            const uint32_t ub = lut8_sh + g * W * CARD;
+            const char *wbase = reinterpret_cast<const char *>(sax + (lane & 7u));
+            const uint32_t cell0 = sn * CPS;
+            const uint32_t clp = cl_sh + (lane >> 3);
+            const int lim = (int)m - (int)(lane >> 3);  // this quarter has a cell while i < lim
+            cp_async16_sh(ring, wbase + (uint64_t)(cell0 + ld_sh_u8(clp)) * (CELL * 16));
+            cp_async_commit();
+            uint32_t slot = 0;
+#pragma unroll 1
+            for (uint32_t i = 0; i < m; i += 4) {
+                cp_async16_sh(ring + (slot ^ 512u), wbase + (uint64_t)(cell0 + ld_sh_u8(clp + i + 4)) * (CELL * 16));
+                cp_async_commit();
+                cp_async_wait<1>();
+                const uint4 wv = ld_sh_v4a(ring + slot);
+                slot ^= 512u;
+                uint32_t e8hi;
+                const uint32_t e8 = word_e8(ub, wv, e8hi);
+                const bool maybe = (int)i < lim && e8 <= 254u;
+                if (!__any_sync(FULL, maybe)) continue;
+                // the keep rule, as in the v1 kernel (see there): first band on the u8 sum, later
+                // bands on the exact fp32 bound
+                const uint32_t pos = (cell0 + ld_sh_u8(clp + i)) * CELL + (lane & 7u);
+                const QConst kq = qc[g];
+                const bool band0 = kq.lo < 0.f;
+                const bool first = maybe && band0;
+                const bool check = maybe && !band0;
+                const float lb = check ? word_lb(lut_all + (uint64_t)qid[g] * W * CARD, wv) : 0.f;
+                const bool keep = (first || (check && lb > kq.lo && lb <= kq.T)) && pos_ok(kq, pos) && pos < N;
+                uint32_t b = e8 <= E_SURE ? e8 : B_UNCHECKED;
+                if (check) {
+                    const float y = __fmul_rd(lb, qsc[g]);
+                    b = lb > 0.f ? (y >= 254.f ? 254u : (uint32_t)y) : 0u;
+                }
+                if (keep)
+                    atomicAdd(&shist[g][first ? min(e8 * HIST_BINS / 254u, HIST_BINS - 1) : hist_bin(lb, kq.lo, kq.T)], 1u);
+                emit(keep, pos, b | (e8hi << 8), g, lane, lt, wbuf, wcnt, s_ovf, qid, cand, candq, cand_cnt, cap);
+            }
+            cp_async_wait<0>();  // the trailing copy (a repeat of the first cell)
+        };
+        uint2 en_n = claim();  // the next entry (claimed an entry ahead)
+        uint2 prev = make_uint2(0u, 0u);  // the item B runs next (y = its alive cells; its list is list `buf`)
+        uint32_t buf = 0;
+        for (;;) {
+            // refill the ring when it holds at most one item
+            while (iq_tail - iq_head <= 1u && en_n.x != 0xffffffffu) {
+                const uint2 en = en_n;
+                en_n = claim();
+                stage_a2(en);
+            }
+            if (iq_tail == iq_head) break;
+            const uint2 it = stage_a3(cl0_sh + (buf ^ 1u) * CLIST);
+            if (prev.y) stage_b(prev.x, prev.y, cl0_sh + buf * CLIST);
+            if (it.y) {
+                prev = it;
+                buf ^= 1u;
+            } else if (prev.y) {
+                prev.y = 0;  // B ran; the list `buf` is free again, and the new one held nothing
+            }
+        }
+        if (prev.y) stage_b(prev.x, prev.y, cl0_sh + buf * CLIST);
+        if (wcnt) wflush(wbuf, wcnt, lane, s_ovf, qid, cand, candq, cand_cnt, cap);  // (warp-uniform)
+        // the group's histograms and surviving-leaf counts into global memory
+        __syncthreads();
+        if (t < G && alive_cnt[t] && g0 + t < nq) atomicAdd(&leaves_alive[qid[t]], alive_cnt[t]);
+        for (uint32_t e = t; e < G * HIST_BINS; e += LF_THREADS) {
+            const uint32_t g = e / HIST_BINS, b = e % HIST_BINS;
+            if (g0 + g < nq && shist[g][b]) atomicAdd(&hist[qid[g] * HIST_BINS + b], shist[g][b]);
+        }
+    }
+    // stats: bytes of summaries and words read, and the lookups made (16 per test; an alive cell is
+    // CELL member tests of 16 B and 16 lookups each)
+    const unsigned long long nodes = (unsigned long long)__reduce_add_sync(FULL, nnode) + ncellt;
+    const unsigned long long membs = (unsigned long long)nmembt * CELL;
+    if (lane == 0 && nodes) {
+        atomicAdd(scan_bytes_dev, nodes * 32ull + membs * 16ull);
+        atomicAdd(scan_bytes_dev + 1, 16ull * (nodes + membs));
+    }
+}
+
+#ifndef ISAX_SCAN_V1
+#define ISAX_SCAN_V1 0  // 1: the round-2b kernel (leaf worklist, lane = member of a whole leaf), for A/B
+#endif
+#ifndef ISAX_TASKS_PER_SM
+#define ISAX_TASKS_PER_SM 16
+#endif
+
 template <int G>
 static void launch_leaf(const isax_index *ix, uint32_t nq, const uint32_t *qmap, cudaStream_t s) {
     constexpr uint32_t NW = LF_THREADS / 32;
-    const size_t smem = (size_t)G * (W * CARD + CW) + 256 + CHUNK * 4 + (size_t)NW * PD * LEAF * sizeof(uint4) +
-                        (size_t)NW * WB * sizeof(uint2) + (size_t)NW * SV * 20;
-    // per launch (the attribute is per device; a failure surfaces as the launch's error)
-    cudaFuncSetAttribute(leafscan_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const uint32_t groups = (nq + G - 1) / G;
     const uint32_t nleaf = (uint32_t)((ix->N + LEAF - 1) / LEAF);
+    const QueryScratch &qs = ix->qs;
+#if ISAX_SCAN_V1
+    const size_t smem = (size_t)G * (W * CARD + CW) + 256 + CHUNK * 4 + (size_t)NW * PD * LEAF * sizeof(uint4) +
+                        (size_t)NW * WB * sizeof(uint2) + (size_t)NW * SV * 20;
+    // per launch (the attribute is per device; a failure surfaces as the launch's error)
+    cudaFuncSetAttribute(leafscan_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     // chunk: as large as possible (fewer phase barriers) while leaving >= 16 tasks per SM for
     // balance; a power of two >= 512, so a multiple of SUPER
     uint32_t chunk = CHUNK;
-#ifndef ISAX_TASKS_PER_SM
-#define ISAX_TASKS_PER_SM 16
-#endif
     while (chunk > 512 && (uint64_t)groups * ((nleaf + chunk - 1) / chunk) < (uint64_t)ISAX_TASKS_PER_SM * sms) chunk >>= 1;
     const uint64_t tasks = (uint64_t)groups * ((nleaf + chunk - 1) / chunk);
     const unsigned grid = (unsigned)std::max<uint64_t>(1, umin64(tasks, (uint64_t)sms * LF_CTAS));
     // one task per grab: runs of 4-8 consecutive chunks per CTA (fewer table reloads with many
     // groups) measured 30-100% slower: the CTAs then stream through scattered parts of the arrays
-#ifndef ISAX_TASK_RUN
-#define ISAX_TASK_RUN 1
-#endif
-    const uint32_t run = ISAX_TASK_RUN;
-    const QueryScratch &qs = ix->qs;
     leafscan_kernel<G><<<grid, LF_THREADS, smem, s>>>(
         reinterpret_cast<const uint4 *>(ix->sax), ix->lmeta, ix->smeta, ix->hmeta, (uint32_t)ix->N, qs.lut, qs.lut8, qs.lut8c,
         qs.qconst, qs.qsax, qmap, nq, nleaf, chunk, qs.cand, qs.candq, qs.cand_cnt, qs.cand_cap, qs.cand_hist, qs.counters_leaf,
-        qs.scan_bytes_dev, qs.task_ctr, run);
+        qs.scan_bytes_dev, qs.task_ctr, 1u);
+#else
+    const uint32_t nsuper = (nleaf + SUPER - 1) / SUPER, nhyper = (nsuper + HYPER - 1) / HYPER;
+    // node scan: a CTA per (block of hyper-nodes, group); blocks sized for about three CTAs per SM in all
+    const size_t smem_n = (size_t)G * W * CARD + 256;
+    cudaFuncSetAttribute(nodescan_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_n);
+    const uint32_t want = std::max(1u, (uint32_t)sms * 3u / groups);
+    const uint32_t hpc = std::max(8u, (nhyper + want - 1) / want);
+    nodescan_kernel<G><<<dim3((nhyper + hpc - 1) / hpc, groups), NS_THREADS, smem_n, s>>>(
+        ix->smeta, ix->hmeta, nsuper, nhyper, qs.lut8, qs.qsax, qmap, nq, hpc, qs.scan_entries, qs.scan_ctl, qs.scan_bytes_dev);
+    // item scan: persistent CTAs, no more than the entries can occupy
+    const size_t smem = (size_t)G * W * CARD + 256 + ((NW * WSC + 15u) & ~15u) + (size_t)NW * WB * sizeof(uint2) +
+                        (size_t)NW * 1024;
+    cudaFuncSetAttribute(itemscan_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const unsigned grid = (unsigned)std::max<uint64_t>(
+        1, umin64(((uint64_t)nsuper * groups + NW - 1) / NW, (uint64_t)sms * LF_CTAS));
+    itemscan_kernel<G><<<grid, LF_THREADS, smem, s>>>(
+        reinterpret_cast<const uint4 *>(ix->sax), ix->cmeta, ix->lmeta, (uint32_t)ix->N, nleaf, nsuper, qs.lut, qs.lut8,
+        qs.qconst, qs.qsax, qmap, nq, qs.scan_entries, qs.scan_ctl, qs.cand, qs.candq, qs.cand_cnt, qs.cand_cap, qs.cand_hist,
+        qs.counters_leaf, qs.scan_bytes_dev);
+#endif
 }
 
 uint64_t launch_lbscan(const isax_index *ix, uint32_t nq, uint32_t B, const uint32_t *qmap, const Band *band,
@@ -858,7 +1269,8 @@ uint64_t launch_lbscan(const isax_index *ix, uint32_t nq, uint32_t B, const uint
     const float onepd = 1.0f + delta;
     const QueryScratch &qs = ix->qs;
     scanprep_kernel<<<nq, 256, 0, s>>>(qs.lut, qmap, band, qs.bsf, qs.win, onepd, qs.lut8, qs.lut8c, qs.qconst, qs.qscale, qs.qT, qs.bsf_scan,
-                                      B, qs.cand_cnt, qs.cand_cnt2, qs.cnt_hi, qs.cnt_f, qs.cand_hist, qs.task_ctr);
+                                      B, qs.cand_cnt, qs.cand_cnt2, qs.cnt_hi, qs.cnt_f, qs.cand_hist, qs.task_ctr, qs.scan_ctl,
+                                      3u * qs.scan_groups);
     if (ix->opts.flags & ISAX_FLAG_FLAT_SCAN) {  // ParIS flat scan, kept for A/B measurement
         const uint32_t G = nq >= 4 ? 4 : nq;
         if (G == 4) launch_g<4>(ix, nq, qmap, band, onepd, s);
@@ -867,7 +1279,10 @@ uint64_t launch_lbscan(const isax_index *ix, uint32_t nq, uint32_t B, const uint
         else launch_g<1>(ix, nq, qmap, band, onepd, s);
         return 16ull * ix->N * ((nq + G - 1) / G);  // words read
     }
-    const uint32_t G = nq >= 16 ? 16 : nq >= 8 ? 8 : nq >= 4 ? 4 : nq >= 2 ? 2 : 1;
+#ifndef ISAX_GMAX
+#define ISAX_GMAX 16  // queries per scan group (their u8 tables share a CTA's shared memory)
+#endif
+    const uint32_t G = nq >= 16 && ISAX_GMAX >= 16 ? 16 : nq >= 8 && ISAX_GMAX >= 8 ? 8 : nq >= 4 ? 4 : nq >= 2 ? 2 : 1;
     if (G == 16) launch_leaf<16>(ix, nq, qmap, s);
     else if (G == 8) launch_leaf<8>(ix, nq, qmap, s);
     else if (G == 4) launch_leaf<4>(ix, nq, qmap, s);
@@ -1054,13 +1469,15 @@ void launch_candcheck(const isax_index *ix, uint32_t Q, cudaStream_t s) {
 }
 
 // ------------------------------------------------------------------------------------ leaf meta
-// Build: per leaf, the per-segment min and max symbol of its (up to) LEAF members, 32 bytes.
-__global__ void leaf_meta_kernel(const uint4 *__restrict__ sax, uint64_t N, uint8_t *__restrict__ lmeta) {
-    const uint64_t nleaf = (N + LEAF - 1) / LEAF;
-    for (uint64_t l = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; l < nleaf; l += (uint64_t)gridDim.x * blockDim.x) {
+// Build: per box of `box` consecutive sorted positions (a leaf of LEAF, or a kd cell of CELL rows),
+// the per-segment min and max symbol of its members below N, 32 bytes. A box with no member gets
+// min 255 / max 0.
+__global__ void box_meta_kernel(const uint4 *__restrict__ sax, uint64_t N, uint32_t box, uint64_t nbox,
+                                uint8_t *__restrict__ meta) {
+    for (uint64_t l = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; l < nbox; l += (uint64_t)gridDim.x * blockDim.x) {
         uint32_t mn[4] = {~0u, ~0u, ~0u, ~0u}, mx[4] = {0, 0, 0, 0};
-        const uint64_t p1 = umin64(N, (l + 1) * LEAF);
-        for (uint64_t p = l * LEAF; p < p1; p++) {
+        const uint64_t p1 = umin64(N, (l + 1) * box);
+        for (uint64_t p = l * box; p < p1; p++) {
             const uint4 w = __ldg(sax + p);
             const uint32_t v[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
@@ -1069,7 +1486,7 @@ __global__ void leaf_meta_kernel(const uint4 *__restrict__ sax, uint64_t N, uint
                 mx[k] = __vmaxu4(mx[k], v[k]);
             }
         }
-        uint4 *o = reinterpret_cast<uint4 *>(lmeta + l * 32);
+        uint4 *o = reinterpret_cast<uint4 *>(meta + l * 32);
         o[0] = make_uint4(mn[0], mn[1], mn[2], mn[3]);
         o[1] = make_uint4(mx[0], mx[1], mx[2], mx[3]);
     }
@@ -1097,16 +1514,19 @@ __global__ void parent_meta_kernel(const uint4 *__restrict__ child, uint64_t nch
     }
 }
 
-void launch_leaf_meta(const uint8_t *sax, uint64_t N, uint8_t *lmeta, uint8_t *smeta, uint8_t *hmeta, cudaStream_t s) {
+void launch_leaf_meta(const uint8_t *sax, uint64_t N, uint8_t *cmeta, uint8_t *lmeta, uint8_t *smeta, uint8_t *hmeta,
+                      cudaStream_t s) {
     const uint64_t nleaf = (N + LEAF - 1) / LEAF;
-    const unsigned grid = (unsigned)std::max<uint64_t>(1, umin64((nleaf + 255) / 256, 148 * 16));
-    leaf_meta_kernel<<<grid, 256, 0, s>>>(reinterpret_cast<const uint4 *>(sax), N, lmeta);
+    const uint64_t ncell = nleaf * (LEAF / KD_CELL);  // whole leaves (the SAX array is padded to them)
+    auto grid = [](uint64_t n) { return (unsigned)std::max<uint64_t>(1, umin64((n + 255) / 256, 148 * 16)); };
+    box_meta_kernel<<<grid(ncell), 256, 0, s>>>(reinterpret_cast<const uint4 *>(sax), N, KD_CELL, ncell, cmeta);
+    box_meta_kernel<<<grid(nleaf), 256, 0, s>>>(reinterpret_cast<const uint4 *>(sax), N, LEAF, nleaf, lmeta);
     const uint64_t ns = (nleaf + SUPER - 1) / SUPER;
-    parent_meta_kernel<<<(unsigned)std::max<uint64_t>(1, umin64((ns + 255) / 256, 148 * 16)), 256, 0, s>>>(
-        reinterpret_cast<const uint4 *>(lmeta), nleaf, SUPER, reinterpret_cast<uint4 *>(smeta));
+    parent_meta_kernel<<<grid(ns), 256, 0, s>>>(reinterpret_cast<const uint4 *>(lmeta), nleaf, SUPER,
+                                                reinterpret_cast<uint4 *>(smeta));
     const uint64_t nh = (ns + HYPER - 1) / HYPER;
-    parent_meta_kernel<<<(unsigned)std::max<uint64_t>(1, umin64((nh + 255) / 256, 148 * 16)), 256, 0, s>>>(
-        reinterpret_cast<const uint4 *>(smeta), ns, HYPER, reinterpret_cast<uint4 *>(hmeta));
+    parent_meta_kernel<<<grid(nh), 256, 0, s>>>(reinterpret_cast<const uint4 *>(smeta), ns, HYPER,
+                                                reinterpret_cast<uint4 *>(hmeta));
 }
 
 }  // namespace isax

@@ -114,7 +114,8 @@ void launch_export_sax(const uint8_t *sax, const uint32_t *inv, uint64_t first_i
 // (R6b) The z order groups series by key prefix, but a leaf of 32 consecutive positions often
 // straddles key boundaries, which widens its per-segment [min, max] box. Inside every full
 // super-node (SUPER_SIZE = 1024 consecutive positions of the z order) the positions are reordered
-// by a kd split down to leaves, so the 32 leaves of a super-node have tight boxes:
+// by a kd split down to cells of KD_CELL = 8 rows, so the 32 leaves of a super-node and the four
+// cells of each leaf (the scan's sub-leaf boxes, R11c) have tight boxes:
 //   at each level, every node (a contiguous half of its parent) takes the segment s with the
 //   largest symbol range max_s - min_s over its members (the lowest s on ties) and is sorted by
 //   symbol s, stably (equal symbols keep their order); its halves are its children.
@@ -123,16 +124,26 @@ void launch_export_sax(const uint8_t *sax, const uint32_t *inv, uint64_t first_i
 // Per super-node it also records the z key of its first position (the block's smallest key, for
 // the approximate answer's search) and the first four split levels (segment and the smallest
 // symbol of the right half) for locating a probe's kd cell.
-// One CTA per full super-node, 512 threads; the node ranges come from warp reductions and one
-// shared atomic per (node, segment) and warp; each level is a bitonic sort of the 1024 keys
-// (node << 18 | symbol << 10 | position), so the order is exactly the stable one.
+// One CTA per full super-node, 512 threads; down to nodes of 64 rows the node ranges come from
+// warp reductions and one shared atomic per (node, segment) and warp, below that from shuffles
+// inside the node's aligned group of lanes; each level is a bitonic sort of the keys
+// (node << 18 | symbol << 10 | position) inside every node, so the order is exactly the stable one.
 constexpr int KD_THREADS = 512;
+
+// min and max of v over the aligned group of `size` lanes (a power of two <= 32) this lane is in
+__device__ __forceinline__ void group_minmax(uint32_t v, uint32_t size, uint32_t &lo, uint32_t &hi) {
+    lo = hi = v;
+    for (uint32_t o = 1; o < size; o <<= 1) {
+        lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+}
 
 __global__ void __launch_bounds__(KD_THREADS) superkd_kernel(uint4 *__restrict__ sax, uint32_t *__restrict__ perm,
                                                           uint64_t nfull, uint4 *__restrict__ skey,
                                                           KdSplits *__restrict__ ksplit) {
-    constexpr uint32_t S = SUPER_SIZE, LV = 5;  // 1024 -> 32
-    static_assert(SUPER_SIZE == 1024 && LEAF_SIZE == 32, "five kd levels per super-node");
+    constexpr uint32_t S = SUPER_SIZE, LV = 7;  // 1024 -> 8 (KD_CELL)
+    static_assert(SUPER_SIZE == 1024 && KD_CELL == 8, "seven kd levels per super-node");
     __shared__ uint4 wa[S], wb[S];
     __shared__ uint32_t ia[S], ib[S];
     __shared__ uint32_t key[S];
@@ -151,62 +162,86 @@ __global__ void __launch_bounds__(KD_THREADS) superkd_kernel(uint4 *__restrict__
     if (t == 0) skey[b] = word_key(wa[0]);
     for (uint32_t lv = 0; lv < LV; lv++) {
         const uint32_t size = S >> lv, nodes = 1u << lv, sh = 10 - lv;
-        for (uint32_t i = t; i < nodes * W; i += KD_THREADS) {
-            mn[i / W][i % W] = 255u;
-            mx[i / W][i % W] = 0u;
-        }
-        __syncthreads();
-        // a warp's 32 consecutive positions lie in one node (nodes hold >= 64): warp reductions
-        // first, then one shared atomic per (node, segment) and warp
-        for (uint32_t i = t; i < S; i += KD_THREADS) {
-            const uint4 wv = wcur[i];
-            const uint32_t v[4] = {wv.x, wv.y, wv.z, wv.w};
-            const uint32_t nd = i >> sh;
-            uint32_t mine = 0, maxe = 0;  // lane s < W keeps segment s's results
+        if (size > 32) {
+            // levels 0-4 (nodes of 64 rows or more): a warp's 32 consecutive positions lie in one
+            // node: warp reductions first, then one shared atomic per (node, segment) and warp
+            for (uint32_t i = t; i < nodes * W; i += KD_THREADS) {
+                mn[i / W][i % W] = 255u;
+                mx[i / W][i % W] = 0u;
+            }
+            __syncthreads();
+            for (uint32_t i = t; i < S; i += KD_THREADS) {
+                const uint4 wv = wcur[i];
+                const uint32_t v[4] = {wv.x, wv.y, wv.z, wv.w};
+                const uint32_t nd = i >> sh;
+                uint32_t mine = 0, maxe = 0;  // lane s < W keeps segment s's results
 #pragma unroll
-            for (int s = 0; s < W; s++) {
+                for (int s = 0; s < W; s++) {
+                    const uint32_t c = (v[s >> 2] >> (8 * (s & 3))) & 0xFFu;
+                    const uint32_t lo = __reduce_min_sync(0xffffffffu, c), hi = __reduce_max_sync(0xffffffffu, c);
+                    if ((t & 31) == (uint32_t)s) {
+                        mine = lo;
+                        maxe = hi;
+                    }
+                }
+                if ((t & 31) < (uint32_t)W) {
+                    atomicMin(&mn[nd][t & 31], mine);
+                    atomicMax(&mx[nd][t & 31], maxe);
+                }
+            }
+            __syncthreads();
+            if (t < nodes) {
+                uint32_t best = 0, br = 0;
+                for (uint32_t s = 0; s < W; s++) {
+                    const uint32_t r = mx[t][s] - mn[t][s];
+                    if (r > br) {  // strictly larger: the lowest segment wins ties
+                        br = r;
+                        best = s;
+                    }
+                }
+                segsel[t] = best;
+                if (lv < KD_LEVELS) lvseg[(1u << lv) - 1 + t] = best;
+            }
+            __syncthreads();
+            for (uint32_t i = t; i < S; i += KD_THREADS) {
+                const uint4 wv = wcur[i];
+                const uint32_t v[4] = {wv.x, wv.y, wv.z, wv.w};
+                const uint32_t nd = i >> sh, s = segsel[nd];
                 const uint32_t c = (v[s >> 2] >> (8 * (s & 3))) & 0xFFu;
-                const uint32_t lo = __reduce_min_sync(0xffffffffu, c), hi = __reduce_max_sync(0xffffffffu, c);
-                if ((t & 31) == (uint32_t)s) {
-                    mine = lo;
-                    maxe = hi;
+                key[i] = (nd << 18) | (c << 10) | i;
+            }
+        } else {
+            // levels 5-6 (nodes of 32 and 16 rows): a node is an aligned group of lanes, so its
+            // ranges and its segment come from shuffles alone
+            for (uint32_t i = t; i < S; i += KD_THREADS) {
+                const uint4 wv = wcur[i];
+                const uint32_t v[4] = {wv.x, wv.y, wv.z, wv.w};
+                uint32_t best_c = 0, br = 0;
+                bool first = true;
+#pragma unroll
+                for (int s = 0; s < W; s++) {
+                    const uint32_t c = (v[s >> 2] >> (8 * (s & 3))) & 0xFFu;
+                    uint32_t lo, hi;
+                    group_minmax(c, size, lo, hi);
+                    if (first || hi - lo > br) {  // strictly larger: the lowest segment wins ties
+                        br = hi - lo;
+                        best_c = c;
+                        first = false;
+                    }
                 }
-            }
-            if ((t & 31) < (uint32_t)W) {
-                atomicMin(&mn[nd][t & 31], mine);
-                atomicMax(&mx[nd][t & 31], maxe);
+                key[i] = ((i >> sh) << 18) | (best_c << 10) | i;
             }
         }
         __syncthreads();
-        if (t < nodes) {
-            uint32_t best = 0, br = 0;
-            for (uint32_t s = 0; s < W; s++) {
-                const uint32_t r = mx[t][s] - mn[t][s];
-                if (r > br) {  // strictly larger: the lowest segment wins ties
-                    br = r;
-                    best = s;
-                }
-            }
-            segsel[t] = best;
-            if (lv < KD_LEVELS) lvseg[(1u << lv) - 1 + t] = best;
-        }
-        __syncthreads();
-        for (uint32_t i = t; i < S; i += KD_THREADS) {
-            const uint4 wv = wcur[i];
-            const uint32_t v[4] = {wv.x, wv.y, wv.z, wv.w};
-            const uint32_t nd = i >> sh, s = segsel[nd];
-            const uint32_t c = (v[s >> 2] >> (8 * (s & 3))) & 0xFFu;
-            key[i] = (nd << 18) | (c << 10) | i;
-        }
-        __syncthreads();
-        // bitonic sort of the 1024 keys (all distinct), ascending
-        for (uint32_t k = 2; k <= S; k <<= 1) {
+        // bitonic sort of the keys (all distinct), ascending inside every node: a node's rows stay
+        // in its own aligned block of `size` positions, so the network stops at k = size
+        for (uint32_t k = 2; k <= size; k <<= 1) {
             for (uint32_t j = k >> 1; j > 0; j >>= 1) {
                 for (uint32_t i = t; i < S; i += KD_THREADS) {
                     const uint32_t p = i ^ j;
                     if (p > i) {
                         const uint32_t a = key[i], c = key[p];
-                        const bool up = (i & k) == 0;
+                        const bool up = (i & (size - 1) & k) == 0;
                         if ((a > c) == up) {
                             key[i] = c;
                             key[p] = a;

@@ -6,16 +6,17 @@ canonical (key, id) order, oracle.ref.canonical_order, pinned in test_oracle_pin
 key definition (ref.isax_keys).
 
 Layout (R6, R6b): the sorted positions are the C5 z order, except that every full block
-of SUPER = 1024 positions (a super-node) is reordered by a kd split down to 32-row leaves:
+of SUPER = 1024 positions (a super-node) is reordered by a kd split down to cells of CELL = 8 rows
+(the 32-row leaves of the scan are four such cells):
   P1  perm is a bijection of the ids;
   P2  every full super-node holds exactly the ids of the same C5 block, and the partial last
       super-node is in C5 order;
-  P3  inside a full super-node, every node of 1024, 512, ..., 64 rows (a contiguous, aligned half
+  P3  inside a full super-node, every node of 1024, 512, ..., 16 rows (a contiguous, aligned half
       of its parent) has its two halves separated on the node's widest segment (the largest
       max - min symbol range over the node's rows, the lowest segment on ties):
       max over the left half <= min over the right half;
-  P4  the splits are stable: inside every 32-row leaf, the rows are in ascending order of
-      (symbol on the split segment of the level-5 node, ..., symbol on the level-0 one, C5 rank),
+  P4  the splits are stable: inside every 8-row cell, the rows are in ascending order of
+      (symbol on the split segment of the level-6 node, ..., symbol on the level-0 one, C5 rank),
       which is what successive stable sorts by those segments produce.
 Window (R5): the main window covers whole super-nodes around the one whose z-order key range
 holds the query key; so it contains the id of the largest key below key_q (the predecessor) and,
@@ -28,7 +29,7 @@ import numpy as np
 from oracle import ref
 
 SUPER = 1024
-LEAF = 32
+LEAF = 8  # the kd cell: the smallest node of the kd order
 
 
 def _widest(wn: np.ndarray) -> int:
@@ -56,7 +57,7 @@ def check_super_block(words_block: np.ndarray, zrank: np.ndarray):
     for a in range(0, SUPER, LEAF):
         path = [segs[(lv, (a // (SUPER >> lv)) * (SUPER >> lv))] for lv in range(nlev)]
         keys = [tuple(int(wb[r, s]) for s in reversed(path)) + (int(zrank[r]),) for r in range(a, a + LEAF)]
-        assert all(keys[k] < keys[k + 1] for k in range(LEAF - 1)), f"leaf at {a}: not in stable split order"
+        assert all(keys[k] < keys[k + 1] for k in range(LEAF - 1)), f"cell at {a}: not in stable split order"
 
 
 def check_layout(perm: np.ndarray, words_by_id: np.ndarray, full_blocks=None):

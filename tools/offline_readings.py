@@ -322,6 +322,69 @@ def part_early(out):
     print("early", json.dumps(res), flush=True)
 
 
+def kd_refine(ws, size):
+    """One more kd level (R6b) inside every block of `size` consecutive rows: stable sort by the
+    segment with the largest symbol range (lowest on ties). The halves are the children."""
+    w = ws.reshape(-1, size, 16)
+    rng = w.max(axis=1).astype(np.int32) - w.min(axis=1)
+    seg = rng.argmax(axis=1)                                    # first maximum: the lowest segment
+    keys = np.take_along_axis(w, seg[:, None, None], axis=2)[:, :, 0]
+    order = np.argsort(keys, axis=1, kind="stable")
+    return np.take_along_axis(w, order[:, :, None], axis=1).reshape(-1, 16)
+
+
+def boxes(ws, size):
+    w = ws.reshape(-1, size, 16)
+    return w.min(axis=1), w.max(axis=1)
+
+
+def part_sub(out):
+    """Sub-leaf boxes: under the (leaf, query) pairs that survive the 32-member leaf bound, the
+    fraction of 16-member halves and 8-member quarters whose own box bound survives, in the
+    library's layout as it is and after one / two more kd levels inside each leaf; and the members
+    that pass the u8 test (the floor any box level can reach). 10M walks (config 2's shape)."""
+    import datagen
+
+    wl = datagen.Workload("sub_walk_10M", 10_000_000, 256, 24, "walk", 61, 62, 24, 0)
+    ix = build(wl, first_band=-1)
+    q, T, dbg = queries_and_T(ix, wl, 24)
+    import torch
+    st = ix.stats()
+    T0 = np.asarray(st["bsf0_d2"], np.float64) * (1 + DELTA)   # the scan's own threshold (window BSF)
+    ex = ix.export(0, wl.N, sax=True, perm=True)
+    ix.close()
+    ws0 = ex["sax"][ex["perm"].astype(np.int64)]
+    n = len(ws0) // 1024 * 1024
+    ws0 = ws0[:n]
+    ws1 = kd_refine(ws0, 32)      # kd down to 16
+    ws2 = kd_refine(ws1, 16)      # kd down to 8
+    res = {}
+    for name, ws in (("layout_now", ws0), ("kd_to_16", ws1), ("kd_to_8", ws2)):
+        mn, mx = boxes(ws, 32)
+        mn16, mx16 = boxes(ws, 16)
+        mn8, mx8 = boxes(ws, 8)
+        pairs = h16 = h8 = h8_under16 = memb = 0
+        for i in range(len(T0)):
+            e8 = lut_u8(dbg["lut"][i], T0[i])
+            qs = dbg["q_sax"][i].astype(np.int64)
+            alive = np.nonzero(leaf_node_e8(mn, mx, qs, e8) <= 254)[0]
+            pairs += len(alive)
+            i16 = (alive[:, None] * 2 + np.arange(2)[None]).ravel()
+            a16 = leaf_node_e8(mn16[i16], mx16[i16], qs, e8) <= 254
+            h16 += int(a16.sum())
+            i8 = (alive[:, None] * 4 + np.arange(4)[None]).ravel()
+            a8 = leaf_node_e8(mn8[i8], mx8[i8], qs, e8) <= 254
+            h8 += int(a8.sum())
+            idx = (alive[:, None] * LEAF + np.arange(LEAF)[None]).ravel()
+            memb += int((member_e8(ws[idx], e8) <= 254).sum())
+        res[name] = {"leaf_pairs": pairs, "members_under_leaves": pairs * 32,
+                     "members_under_alive_16": h16 * 16, "members_under_alive_8": h8 * 8,
+                     "frac_16": h16 * 16 / (pairs * 32), "frac_8": h8 * 8 / (pairs * 32),
+                     "members_passing_u8": memb}
+    out["sub"] = {"workload": "10M walks x 256 (seed 61), 24 walk queries (seed 62), T = window BSF (1 + 2^-12)", **res}
+    print("sub", json.dumps(out["sub"]), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default="gpurun_out/offline_readings.json")
@@ -333,7 +396,7 @@ def main():
     out = {"when": time.strftime("%Y-%m-%dT%H:%M:%SZ", time.gmtime())}
     for p in a.parts:
         t0 = time.time()
-        {"r5": part_r5, "r6b": part_r6b, "r14": part_r14, "next3": part_next3, "early": part_early}[p](out)
+        {"r5": part_r5, "r6b": part_r6b, "r14": part_r14, "next3": part_next3, "early": part_early, "sub": part_sub}[p](out)
         out.setdefault("seconds", {})[p] = round(time.time() - t0, 1)
         with open(a.out, "w") as f:
             json.dump(out, f, indent=1)
