@@ -233,7 +233,7 @@ def main():
     keys = ["lbscan", "candcheck", "refine", "refine1", "filter", "refine2", "window", "qprep"]
     kms = {k: [] for k in keys}
     cand, refined, abandoned, skipped, winrows, rounds, scan_b, ref_b, pairs, launches = [], [], [], [], [], [], [], [], [], 0
-    ref1_b, ref2_b = [], []
+    ref1_b, ref2_b, lookups_dev = [], [], []
     for _ in range(args.steps):
         ids, dist_ = ix.nn1(q)
         st = ix.stats()
@@ -251,6 +251,7 @@ def main():
         ref1_b.append(st["refine1_bytes_first_launch"])
         ref2_b.append(st["refine2_bytes_first_launch"])
         pairs.append(st["leaf_pairs_first_launch"])
+        lookups_dev.append(st.get("scan_lookups_first_launch", 0))
     # ---- e2e through isax_nn1 with host (pinned) buffers, copies inside the timed region
     qh = torch.empty((Q, wl.n), dtype=torch.float32, pin_memory=True)
     qh.copy_(q)
@@ -276,11 +277,12 @@ def main():
     nq1 = min(Q, st.get("batch_Q", 1024))  # queries of the first batch (the timed launches)
     leaf_size, super_size = st.get("leaf_size", 64), st.get("super_size", 1024)
     supers = (wl.N + super_size - 1) // super_size
-    # algorithmic LUT lookups of the first scan launch: 16 per super-node per query (root-level
-    # node bounds) plus 16 per member of every (leaf, query) pair that survived (per-series
-    # bounds). Leaf-level bounds (16 per leaf of a surviving super-node) are not counted, so this
-    # understates the work done.
-    lookups = 16.0 * supers * nq1 + 16.0 * leaf_size * med(pairs)
+    # algorithmic LUT lookups of the first scan launch, counted by the scan kernels themselves: 16
+    # per node bound computed (hyper-node, super-node, leaf, 8-row cell; only under surviving
+    # parents) and 16 per member of every (cell, query) pair that survived its cell bound. (The
+    # round-2b kernel, -DISAX_SCAN_V1, does not count: 16 per super-node per query plus 16 per
+    # member of every surviving (leaf, query) pair is used then.)
+    lookups = float(med(lookups_dev)) or 16.0 * supers * nq1 + 16.0 * leaf_size * med(pairs)
     lk_peak = 148 * 32 * sm_mhz * 1e6  # one conflict-free 32-lane LDS wavefront per clock per SM
     lk_rate = lookups / (lb_ms / 1e3)
     scan_bytes = med(scan_b) + 4.0 * med(cand) * nq1 / Q
@@ -291,7 +293,7 @@ def main():
         traffic = tr.get("leafscan_dram_bytes")
     except Exception:
         pass
-    roofline = {"kernel": "leafscan_kernel<16>", "bound": "alu", "achieved": round(lk_rate / 1e12, 4),
+    roofline = {"kernel": "itemscan_kernel<16> (+ nodescan_kernel<16>, scanprep_kernel: the scan stage)", "bound": "alu", "achieved": round(lk_rate / 1e12, 4),
                 "peak": round(lk_peak / 1e12, 4), "unit": "T LUT lookups/s", "frac": round(lk_rate / lk_peak, 4),
                 "traffic": traffic,
                 "peak_rule": "148 SMs x 32 lanes x SM clock (one conflict-free shared-memory wavefront per clock per SM); "
