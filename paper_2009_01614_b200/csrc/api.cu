@@ -235,8 +235,19 @@ static int build_impl(const Source &src, uint64_t N, uint32_t n, uint32_t w, uin
     if (chunk == 0) chunk = std::max<uint64_t>(1, (1ull << 30) / ((uint64_t)n * 4));  // ~1 GB per chunk
     chunk = std::min(chunk, N);
     cudaError_t e = cudaSuccess;
+    // stage timing (isax_stats "build_ms"): event pairs around the stage's launches, read at the end
+    std::vector<cudaEvent_t> tev[4];  // 0 summarise, 1 sort, 2 kd order + node summaries, 3 permute
+    auto tick = [&](int stage) {
+        cudaEvent_t e = nullptr;
+        if (cudaEventCreate(&e) == cudaSuccess) {
+            cudaEventRecord(e, s);
+            tev[stage].push_back(e);
+        }
+    };
     auto fail = [&](int code) {
         cudaStreamSynchronize(s);
+        for (auto &v : tev)
+            for (cudaEvent_t e : v) cudaEventDestroy(e);
         cudaFree(sax_by_id); cudaFree(keys); cudaFree(musig); cudaFree(ids); cudaFree(bad); cudaFree(inv);
         cudaFree(stage);
         cudaFree(ix->stored); cudaFree(ix->sax); cudaFree(ix->perm); cudaFree(ix->lmeta); cudaFree(ix->cmeta); cudaFree(ix->smeta); cudaFree(ix->hmeta);
@@ -270,12 +281,16 @@ static int build_impl(const Source &src, uint64_t N, uint32_t n, uint32_t w, uin
         return ISAX_OK;
     };
     if (!chunked) {
+        tick(0);
         launch_summarise(src.dev, N, n, 0, sax_by_id, keys, musig, bad, s);
+        tick(0);
     } else {
         for (uint64_t id0 = 0; id0 < N; id0 += chunk) {
             const uint64_t cnt = std::min(chunk, N - id0);
             if ((rc = produce(id0, cnt))) return fail(rc);
+            tick(0);
             launch_summarise(stage, cnt, n, id0, sax_by_id, keys, musig, bad, s);
+            tick(0);
         }
     }
     TRY(cudaGetLastError());
@@ -283,7 +298,9 @@ static int build_impl(const Source &src, uint64_t N, uint32_t n, uint32_t w, uin
     TRY(cudaStreamSynchronize(s));
     if (h_bad) return fail(set_error(ISAX_E_NONFINITE, "a series holds NaN or Inf"));
     // canonical order (R6)
+    tick(1);
     if ((rc = radix_sort_keys(keys, ids, N, ix->perm, s))) return fail(rc);
+    tick(1);
     cudaFree(keys);
     keys = nullptr;
     cudaFree(ids);
@@ -297,31 +314,46 @@ static int build_impl(const Source &src, uint64_t N, uint32_t n, uint32_t w, uin
     // kd order inside each super-node (R6b): before the node summaries and the rows
     TRY(dmalloc(&ix->skey, (N + SUPER_SIZE - 1) / SUPER_SIZE, &ix->device_bytes));
     TRY(dmalloc(&ix->ksplit, (N + SUPER_SIZE - 1) / SUPER_SIZE, &ix->device_bytes));
+    tick(2);
     launch_superkd(ix->sax, ix->perm, N, ix->skey, ix->ksplit, s);
     TRY(dmalloc(&ix->lmeta, ((N + LEAF_SIZE - 1) / LEAF_SIZE) * 32, &ix->device_bytes));
     TRY(dmalloc(&ix->cmeta, (npad / KD_CELL) * 32, &ix->device_bytes));
     TRY(dmalloc(&ix->smeta, ((N + SUPER_SIZE - 1) / SUPER_SIZE) * 32, &ix->device_bytes));
     TRY(dmalloc(&ix->hmeta, ((N + HYPER_SIZE - 1) / HYPER_SIZE) * 32, &ix->device_bytes));
     launch_leaf_meta(ix->sax, N, ix->cmeta, ix->lmeta, ix->smeta, ix->hmeta, s);
+    tick(2);
     TRY(cudaStreamSynchronize(s));
     cudaFree(sax_by_id);
     sax_by_id = nullptr;
     // pass 2: store the z-normalised rows in sorted order
     TRY(dmalloc(&ix->stored, N * n, &ix->device_bytes));
     if (!chunked) {
+        tick(3);
         launch_gather_rows(src.dev, musig, ix->perm, N, n, ix->stored, s);
+        tick(3);
     } else {
         TRY(dmalloc(&inv, N, nullptr));
         launch_invert_perm(ix->perm, N, inv, s);
         for (uint64_t id0 = 0; id0 < N; id0 += chunk) {
             const uint64_t cnt = std::min(chunk, N - id0);
             if ((rc = produce(id0, cnt))) return fail(rc);
+            tick(3);
             launch_scatter_rows(stage, cnt, id0, musig, inv, n, ix->stored, s);
+            tick(3);
         }
     }
     TRY(cudaGetLastError());
     TRY(cudaStreamSynchronize(s));
     cudaFree(musig); cudaFree(inv); cudaFree(stage); cudaFree(bad);
+    for (int k = 0; k < 4; k++) {
+        float tot = 0.f;
+        for (size_t i = 0; i + 1 < tev[k].size(); i += 2) {
+            float ms = 0.f;
+            if (cudaEventElapsedTime(&ms, tev[k][i], tev[k][i + 1]) == cudaSuccess) tot += ms;
+        }
+        ix->st_build_ms[k] = tot;
+        for (cudaEvent_t e : tev[k]) cudaEventDestroy(e);
+    }
     for (auto &ev : ix->ev) TRY(cudaEventCreate(&ev));
 #undef TRY
     cudaStreamDestroy(s);
@@ -900,6 +932,12 @@ int isax_stats(const isax_index *cix, char *buf, size_t cap) {
     j += ",\"scan_lookups_first_launch\":" + std::to_string(ix->st_scan_lookups_first);
     j += ",\"cell_size\":" + std::to_string(KD_CELL);
     j += ",\"scan_queries_first_launch\":" + std::to_string(ix->st_scan_q_first);
+    {
+        char b[160];
+        snprintf(b, sizeof b, ",\"build_ms\":{\"summarise\":%.4f,\"sort\":%.4f,\"kd_and_node_summaries\":%.4f,\"permute\":%.4f}",
+                 ix->st_build_ms[0], ix->st_build_ms[1], ix->st_build_ms[2], ix->st_build_ms[3]);
+        j += b;
+    }
     j += ",\"leaves\":" + std::to_string((ix->N + LEAF_SIZE - 1) / LEAF_SIZE);
     j += ",\"leaf_size\":" + std::to_string(LEAF_SIZE);
     j += ",\"super_size\":" + std::to_string(SUPER_SIZE);

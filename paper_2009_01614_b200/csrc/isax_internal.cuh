@@ -222,6 +222,7 @@ struct isax_index {
     std::vector<uint32_t> st_win, st_cand, st_refined, st_abandoned, st_skipped, st_winrows, st_rounds, st_near, st_leaves;
     std::vector<float> st_bsf0, st_bsf_final;
     isax::StageTimes st_ms;
+    float st_build_ms[4] = {0, 0, 0, 0};  // device ms of the build's stages: summarise, sort, kd order + node summaries, permute
     uint64_t st_launches = 0;  // kernels launched by the last nn1 call
     uint32_t st_last_Q = 0;     // Q of the last nn1 call
     // R15 first-band policy (adaptive by default): the measured device ms per query of batches run

@@ -376,6 +376,197 @@ __global__ void __launch_bounds__(256) paa_sax_kernel(const float *__restrict__ 
     }
 }
 
+// ------------------------------------------------------------------------------------ TMA tiles
+// The default for n = 128 and 256 since round 2c: a CTA of four warps owns a tile of 32 rows. The
+// rows arrive by the TMA engine: lane r of warp 0 issues one bulk copy (cp.async.bulk, 4n bytes)
+// of row r into its padded shared-memory row, all completing on one mbarrier, so the staging
+// costs no registers, no issue slots and no bank-conflicted stores (the round-1 kernel's scalar
+// stores were 4-way conflicted, and the split kernels' per-thread global reads cost 32 L1
+// wavefronts per warp load). Rows are n + 4 floats apart: a thread reads its row with 16-byte
+// loads, and the eight threads of a quarter warp then hit eight different 16-byte bank groups.
+// Every sum is strictly left to right with explicit __d*_rn (R3): warp 0, thread = row, takes the
+// mean and the variance (two sequential chains); then warp w, lane = row, z-normalises the points
+// of segments 4w .. 4w+3 (znorm_value_d: no conversion back and forth) and adds each to its
+// segment's sum, four independent chains; symbols by binary search, the key by bit interleave.
+// One read of the input from HBM (the split kernels read it twice and converted each point five
+// times: here three F2D per point). Six CTAs fit on an SM (36 KB each); a CTA's compute hides the
+// other CTAs' copies. The per-series operation order is that of summarise_kernel (and of the
+// oracle): identical words.
+__device__ __forceinline__ void mbar_init(uint32_t mbar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(mbar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t mbar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mbar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint32_t mbar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(mbar), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+// one-dimensional bulk copy global -> shared (the TMA engine; UBLKCP in SASS), completing on mbar
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, uint32_t bytes, uint32_t mbar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                 "l"(src), "r"(bytes), "r"(mbar)
+                 : "memory");
+}
+
+// fp64 value of y = fp32_rne(fl64((x - mu) / sd)) (znorm_value's result, as a double) without the
+// two conversions: outside znorm_value's window the low 29 bits of q's significand are not within
+// 8 of the halfway point, so rounding to fp32 precision is "add 2^28, clear the low 29 bits" on
+// q's bit pattern (a carry moves into the exponent as it should; the exponent range keeps the
+// result a normal fp32).
+__device__ __forceinline__ double znorm_value_d(float x, double mu, double sd, double rcp) {
+    const double t = __dsub_rn((double)x, mu);
+    const double q = __dmul_rn(t, rcp);
+    const unsigned long long b = (unsigned long long)__double_as_longlong(q);
+    const uint32_t ex = (uint32_t)(b >> 52) & 0x7FFu;
+    const uint32_t low = (uint32_t)b & ((1u << 29) - 1u);
+    if (ex >= 898u && ex <= 1149u && low - ((1u << 28) - 8u) > 16u)
+        return __longlong_as_double((long long)((b + (1ull << 28)) & ~((1ull << 29) - 1ull)));
+    return (double)__double2float_rn(__ddiv_rn(t, sd));
+}
+
+// Four warps per 32-row tile. (One warp per 32-row tile, everything thread = row: 10.2 ms per
+// 10M x 256, too few warps per scheduler; one warp per 16-row tile with half-idle lanes in the
+// moments: 7.3 ms; this shape: 5.3 ms; the split kernels before it: 8.2 ms.)
+#ifndef ISAX_ST_WARPS
+#define ISAX_ST_WARPS 4
+#endif
+constexpr int ST_WARPS = ISAX_ST_WARPS;  // 4 or 8: warp w takes 16 / ST_WARPS segments of every row
+constexpr int ST_THREADS = 32 * ST_WARPS;
+constexpr int ST_SEGS = W / ST_WARPS;
+static_assert(ST_WARPS == 2 || ST_WARPS == 4 || ST_WARPS == 8, "whole segments per warp");
+template <uint32_t NT>
+__global__ void __launch_bounds__(ST_THREADS) summarise_tma_kernel(const float *__restrict__ x, uint64_t count, uint64_t id0,
+                                                                   uint8_t *__restrict__ sax_by_id, uint4 *__restrict__ key,
+                                                                   double2 *__restrict__ musig, uint32_t *__restrict__ bad) {
+    constexpr uint32_t STRIDE = NT + 4;  // floats between rows
+    constexpr uint32_t seg = NT / W;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    // [0, 16): the mbarrier | beta | (mu, sigma) [32] | words [32] | rows [32][STRIDE]
+    double *beta = reinterpret_cast<double *>(smem_raw + 16);
+    constexpr uint32_t MS_OFF = (16 + ISAX_NBETA * 8 + 15) & ~15u;
+    double2 *ms = reinterpret_cast<double2 *>(smem_raw + MS_OFF);
+    uint8_t *words = smem_raw + MS_OFF + 32 * 16;  // [32 rows][16]
+    constexpr uint32_t ROWS_OFF = MS_OFF + 32 * 16 + 32 * 16;
+    const float *rows = reinterpret_cast<const float *>(smem_raw + ROWS_OFF);
+    const uint32_t mbar = (uint32_t)__cvta_generic_to_shared(smem_raw);
+    const uint32_t rows_sh = mbar + ROWS_OFF;
+    const uint32_t t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    for (uint32_t k = t; k < ISAX_NBETA; k += ST_THREADS) beta[k] = c_beta[k];
+    if (t == 0) {
+        mbar_init(mbar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    uint32_t parity = 0;
+    const uint64_t ngroups = (count + 31) / 32;
+    for (uint64_t g = blockIdx.x; g < ngroups; g += gridDim.x) {
+        const uint64_t r0 = g * 32;
+        const uint32_t nrows = (uint32_t)umin64(32, count - r0);
+        if (warp == 0) {
+            if (lane == 0) mbar_expect_tx(mbar, nrows * NT * 4);
+            __syncwarp();
+            if (lane < nrows) bulk_g2s(rows_sh + lane * STRIDE * 4, x + (r0 + lane) * NT, NT * 4, mbar);
+        }
+        const float4 *row4 = reinterpret_cast<const float4 *>(rows + lane * STRIDE);
+        // C1 (warp 0, thread = row): mu and sigma, left to right (R2, R3). Only warp 0 waits for the
+        // tile; the other warps wait at the barrier below without taking issue slots.
+        if (warp == 0) {
+            while (!mbar_try_wait(mbar, parity)) {
+            }
+        }
+        parity ^= 1u;
+        if (warp == 0 && lane < nrows) {
+            bool finite = true;
+            double s = 0.0;
+#pragma unroll 8
+            for (uint32_t c = 0; c < NT / 4; c++) {
+                const float4 v = row4[c];
+                // (x - x is 0 for a finite x, NaN for NaN or Inf)
+                finite &= (v.x - v.x == 0.f) && (v.y - v.y == 0.f) && (v.z - v.z == 0.f) && (v.w - v.w == 0.f);
+                s = __dadd_rn(s, (double)v.x);
+                s = __dadd_rn(s, (double)v.y);
+                s = __dadd_rn(s, (double)v.z);
+                s = __dadd_rn(s, (double)v.w);
+            }
+            const double mu = __ddiv_rn(s, (double)NT);
+            double s2 = 0.0;
+#pragma unroll 8
+            for (uint32_t c = 0; c < NT / 4; c++) {
+                const float4 v = row4[c];
+                double d;
+                d = __dsub_rn((double)v.x, mu); s2 = __dadd_rn(s2, __dmul_rn(d, d));
+                d = __dsub_rn((double)v.y, mu); s2 = __dadd_rn(s2, __dmul_rn(d, d));
+                d = __dsub_rn((double)v.z, mu); s2 = __dadd_rn(s2, __dmul_rn(d, d));
+                d = __dsub_rn((double)v.w, mu); s2 = __dadd_rn(s2, __dmul_rn(d, d));
+            }
+            ms[lane] = make_double2(mu, __dsqrt_rn(__ddiv_rn(s2, (double)NT)));
+            if (!finite) atomicOr(bad, 1u);
+        }
+        __syncthreads();
+        // C2-C4 (warp w, lane = row): segments ST_SEGS w .. ST_SEGS (w + 1) - 1: y = fp32((x - mu) /
+        // sigma) as a double and the segment sums, left to right within each segment; then the symbols
+        if (lane < nrows) {
+            const double2 m = ms[lane];
+            const double rcp = __drcp_rn(m.y);
+            const bool flat = m.y < 1e-12;
+            double acc[ST_SEGS];
+#pragma unroll
+            for (int k = 0; k < ST_SEGS; k++) acc[k] = 0.0;
+#pragma unroll 2
+            for (uint32_t c = 0; c < seg / 4; c++) {
+#pragma unroll
+                for (int k = 0; k < ST_SEGS; k++) {
+                    const float4 v = row4[(ST_SEGS * warp + k) * (seg / 4) + c];
+                    acc[k] = __dadd_rn(acc[k], flat ? 0.0 : znorm_value_d(v.x, m.x, m.y, rcp));
+                    acc[k] = __dadd_rn(acc[k], flat ? 0.0 : znorm_value_d(v.y, m.x, m.y, rcp));
+                    acc[k] = __dadd_rn(acc[k], flat ? 0.0 : znorm_value_d(v.z, m.x, m.y, rcp));
+                    acc[k] = __dadd_rn(acc[k], flat ? 0.0 : znorm_value_d(v.w, m.x, m.y, rcp));
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < ST_SEGS; k++)
+                words[lane * W + ST_SEGS * warp + k] = (uint8_t)sax_symbol(beta, __ddiv_rn(acc[k], (double)seg));
+        }
+        __syncthreads();
+        if (warp == 0 && lane < nrows) {
+            const uint4 wv = reinterpret_cast<const uint4 *>(words)[lane];
+            const uint32_t v[4] = {wv.x, wv.y, wv.z, wv.w};
+            uint32_t sym[W];
+#pragma unroll
+            for (int sg = 0; sg < W; sg++) sym[sg] = (v[sg >> 2] >> (8 * (sg & 3))) & 0xFFu;
+            const uint64_t id = id0 + r0 + lane;
+            reinterpret_cast<uint4 *>(sax_by_id)[id] = wv;
+            key[id] = isax_key(sym);
+            musig[id] = ms[lane];
+        }
+        // the tile's reads (generic proxy) before the next tile's copies (async proxy)
+        __syncthreads();
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+}
+
+template <uint32_t NT>
+static void launch_summarise_tma(const float *x, uint64_t count, uint64_t id0, uint8_t *sax_by_id, uint4 *key,
+                                 double2 *musig, uint32_t *bad, cudaStream_t s) {
+    const size_t smem = ((16 + ISAX_NBETA * 8 + 15) & ~size_t(15)) + 32 * 16 + 32 * 16 + 32 * (size_t)(NT + 4) * sizeof(float);
+    // per launch (the attribute is per device; a failure surfaces as the launch's error)
+    cudaFuncSetAttribute(summarise_tma_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int per_sm = (int)std::max<size_t>(1, std::min<size_t>(16, (227 * 1024) / (smem + 1024)));
+    const uint64_t grid = umin64((count + 31) / 32, (uint64_t)sms * per_sm);
+    summarise_tma_kernel<NT><<<(unsigned)grid, ST_THREADS, smem, s>>>(x, count, id0, sax_by_id, key, musig, bad);
+}
+
 template <uint32_t NT>
 static void launch_summarise_split(const float *x, uint64_t count, uint64_t id0, uint8_t *sax_by_id, uint4 *key,
                                    double2 *musig, uint32_t *bad, cudaStream_t s) {
@@ -434,9 +625,13 @@ void launch_summarise(const float *x, uint64_t count, uint32_t n, uint64_t id0, 
 #if defined(ISAX_SUMMARISE_HALF)
     if (n == 256) return launch_summarise_half<256>(x, count, id0, sax_by_id, key, musig, bad, s);
     if (n == 128) return launch_summarise_half<128>(x, count, id0, sax_by_id, key, musig, bad, s);
-#elif !defined(ISAX_SUMMARISE_FULLROW)
+#elif defined(ISAX_SUMMARISE_SPLIT)
     if (n == 256) return launch_summarise_split<256>(x, count, id0, sax_by_id, key, musig, bad, s);
     if (n == 128) return launch_summarise_split<128>(x, count, id0, sax_by_id, key, musig, bad, s);
+#elif !defined(ISAX_SUMMARISE_FULLROW)
+    // (the bulk copies need 16-byte aligned rows: x from cudaMalloc or a chunk offset of whole rows)
+    if (n == 256 && (reinterpret_cast<uintptr_t>(x) & 15) == 0) return launch_summarise_tma<256>(x, count, id0, sax_by_id, key, musig, bad, s);
+    if (n == 128 && (reinterpret_cast<uintptr_t>(x) & 15) == 0) return launch_summarise_tma<128>(x, count, id0, sax_by_id, key, musig, bad, s);
 #endif
     if (n == 256) launch_summarise_t<256>(x, count, n, id0, sax_by_id, key, musig, bad, s);
     else if (n == 128) launch_summarise_t<128>(x, count, n, id0, sax_by_id, key, musig, bad, s);

@@ -37,6 +37,7 @@ def main():
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1)
         best = ms if best is None else min(best, ms)
+        print("  stages (device ms):", ix.stats().get("build_ms"), flush=True)
         ix.close()
         torch.cuda.empty_cache()
     gb = wl.N * wl.n * 4 / 1e9
