@@ -273,6 +273,7 @@ def main():
     hbm, peak_src = peaks()
     sm_mhz = clocks.get("sm_mhz") or 1965.0
     lb_ms = med(kms["lbscan"])
+    bms = st.get("build_ms") or {}
     rf_ms = med(kms["refine"])
     nq1 = min(Q, st.get("batch_Q", 1024))  # queries of the first batch (the timed launches)
     leaf_size, super_size = st.get("leaf_size", 64), st.get("super_size", 1024)
@@ -370,7 +371,16 @@ def main():
         "gpu_launches": launches,
         "clocks": clocks,
         "build": {"seconds": round(build_s, 3), "mode": build_mode, "N": wl.N, "n": wl.n,
-                  "input_GBps": round(raw_bytes / build_s / 1e9, 1), "index_device_bytes": ix.device_bytes},
+                  "input_GBps": round(raw_bytes / build_s / 1e9, 1), "index_device_bytes": ix.device_bytes,
+                  "stage_ms": bms,
+                  # the summarise kernel reads every row once (4n B per series) and writes 48 B per series
+                  "summarise": ({"ms": round(bms["summarise"], 3), "bytes": raw_bytes + 48 * wl.N,
+                                 "achieved": round((raw_bytes + 48 * wl.N) / (bms["summarise"] / 1e3) / 1e9, 1),
+                                 "peak": hbm, "unit": "GB/s",
+                                 "frac": round((raw_bytes + 48 * wl.N) / (bms["summarise"] / 1e3) / 1e9 / hbm, 4),
+                                 "bound": "hbm (the sequential fp64 chains of R3 and the float-to-double conversions "
+                                          "limit it below the copy rate; DESIGN.md sec. 6)"}
+                                if bms.get("summarise") else None)},
         "stats": {"candidates_per_query": med(cand) / Q,
                   "refined_per_query": med(refined) / Q,
                   "abandoned_per_query": med(abandoned) / Q,

@@ -166,7 +166,11 @@ int isax_debug_bounds(int fire);
 /* Counters of the last isax_nn1 / isax_nn1_async call, as a JSON object written to buf.
  * It holds per-query window, window_rows (rows the approximate answer refined), candidates,
  * refined, abandoned, skipped, rounds, near, leaves_alive and the BSF before and after the scan,
- * plus per-stage device milliseconds of the first batch. Returns the length needed (excluding NUL); truncates if cap is too small. */
+ * plus per-stage device milliseconds of the first batch, the bytes and LUT lookups the first scan
+ * launch counted (scan_bytes_first_launch, scan_lookups_first_launch: 16 per node or member bound
+ * computed), the bytes its refine passes read, and build_ms: the device milliseconds of the
+ * build's stages (summarise, sort, kd order + node summaries, permute; available right after
+ * isax_build). Returns the length needed (excluding NUL); truncates if cap is too small. */
 int isax_stats(const isax_index *ix, char *buf, size_t cap);
 
 /* Index geometry: any out pointer may be NULL. device_bytes = bytes the index holds on the device. */

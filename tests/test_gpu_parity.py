@@ -441,3 +441,25 @@ def test_finalize_is_exact_when_fp64_ties():
     with _build(x) as ix:
         ids, dist = ix.nn1(q)
     assert_nn_parity(ids.cpu().numpy(), dist.cpu().numpy(), ids_or, dist_or)
+
+
+def test_stats_report_build_stages_and_scan_counters():
+    """isax_stats: the build's stage times are there right after the build, and after a call the
+    scan's own counters are consistent: every lookup belongs to a node or member bound (16 each),
+    and every bound read a summary (32 B) or a word (16 B)."""
+    N, n = 60_000, 256
+    wl = small_workload(N, n, Q=20)
+    x = datagen.series(wl, 0, N)
+    q, _ = datagen.queries(wl)
+    with _build(x, first_band=-1) as ix:
+        st0 = ix.stats()
+        assert all(st0["build_ms"][k] > 0 for k in ("summarise", "sort", "kd_and_node_summaries", "permute"))
+        ix.nn1(q)
+        st = ix.stats()
+    lk, by = st["scan_lookups_first_launch"], st["scan_bytes_first_launch"]
+    assert lk > 0 and lk % 16 == 0
+    tests = lk // 16
+    # between all-member (16 B each) and all-node (32 B each) tests, plus 5 B per candidate
+    assert 16 * tests <= by <= 32 * tests + 5 * sum(st["candidates"]) + 64
+    assert st["cell_size"] == 8 and st["leaf_size"] == 32
+    assert st["leaf_pairs_first_launch"] == sum(st["leaves_alive"])
