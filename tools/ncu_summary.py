@@ -46,7 +46,7 @@ def launches(path):
     out = [f"{'kernel':70s} {'launches':>8s} {'total_us':>12s} {'share':>6s}"]
     for k, (c, v) in sorted(agg.items(), key=lambda x: -x[1][1]):
         out.append(f"{k:70s} {c:8d} {v:12.1f} {100 * v / tot:5.1f}%")
-    qk = ("qprep", "window", "scanprep", "leafscan", "lbscan", "candcheck", "filter", "refine", "finalize")
+    qk = ("qprep", "window", "scanprep", "nodescan", "itemscan", "leafscan", "lbscan", "candcheck", "filter", "refine", "finalize")
     qagg = {k: cv for k, cv in agg.items() if any(x in k for x in qk)}
     qtot = sum(v for _, v in qagg.values()) or 1
     out.append("")
