@@ -1125,6 +1125,56 @@ __global__ void __launch_bounds__(LF_THREADS, LF_CTAS) itemscan_kernel(
             }
             return make_uint2(it.x, m);
         };
+        // The staged members of this warp (they passed the u8 test), one per lane: the keep rule, the
+        // histogram and the append to the query's global list. The rule is the flat scan's, lo <
+        // LB^2 <= T on the exact fp32 bound. A u8 sum <= E_SURE already implies LB^2 <= T (R11b), and
+        // in the first band (lo < 0) lo < LB^2 always holds: there, members with a u8 sum in
+        // (E_SURE, 254] are kept marked B_UNCHECKED and get the exact rule in candcheck_kernel; in
+        // later bands every member gets it here (its word is read again: a rare path). A first-band
+        // member's histogram bin comes from its u8 sum, never above its exact bin (band shrinking,
+        // R10, stays an upper bound on the count). The entries of one query get one global atomic
+        // (match_any groups the lanes); once a query's list has passed its capacity its flag stops
+        // this CTA's appends (the list is dropped for the round anyway, R10).
+        auto flush_staged = [&]() {
+            __syncwarp();
+            for (uint32_t i0 = 0; i0 < wcnt; i0 += 32) {
+                const bool have = i0 + lane < wcnt;
+                const uint2 en = have ? wbuf[i0 + lane] : make_uint2(0u, 0u);
+                const uint32_t g = (en.y >> 16) & 15u, e8 = en.y & 0xFFu, e8hi = (en.y >> 8) & 0xFFu, pos = en.x;
+                const QConst kq = qc[g];
+                const bool band0 = kq.lo < 0.f;
+                float lb = 0.f;
+                if (have && !band0) lb = word_lb(lut_all + (uint64_t)qid[g] * W * CARD, __ldg(sax + pos));
+                const bool keep = have && (band0 || (lb > kq.lo && lb <= kq.T)) && pos_ok(kq, pos) && pos < N;
+                // the candidate's u8 bound b <= LB^2 * sc (for the refine), or B_UNCHECKED
+                uint32_t b = e8 <= E_SURE ? e8 : B_UNCHECKED;
+                if (!band0) {
+                    const float y = __fmul_rd(lb, qsc[g]);
+                    b = lb > 0.f ? (y >= 254.f ? 254u : (uint32_t)y) : 0u;
+                }
+                if (keep) atomicAdd(&shist[g][band0 ? min(e8 * HIST_BINS / 254u, HIST_BINS - 1) : hist_bin(lb, kq.lo, kq.T)], 1u);
+                const uint32_t peers = __match_any_sync(FULL, keep ? g : 0xFFFFu);
+                if (keep) {
+                    const uint32_t leader = __ffs(peers) - 1;
+                    const uint32_t q = qid[g];
+                    uint32_t base = 0xffffffffu;
+                    if (lane == leader && !s_ovf[g]) {
+                        const uint32_t c = __popc(peers);
+                        base = atomicAdd(&cand_cnt[q], c);
+                        if (base + c > cap) s_ovf[g] = 1u;
+                    }
+                    base = __shfl_sync(peers, base, leader);
+                    const uint32_t k = base + __popc(peers & lt);
+                    ISAX_BOUND(pos < N);
+                    if (base != 0xffffffffu && k < cap) {
+                        cand[(uint64_t)q * cap + k] = pos;
+                        candq[(uint64_t)q * cap + k] = (uint16_t)(b | (e8hi << 8));
+                    }
+                }
+            }
+            __syncwarp();
+            wcnt = 0;
+        };
         // B of an item: quarter warp = alive cell, lane = member. Each lane stages its own word of
         // the next iteration's cell (cp.async into the warp's other slot) before this one's lookups.
         auto stage_b = [&](uint32_t item, uint32_t m, uint32_t cl_sh) {
@@ -1147,24 +1197,17 @@ __global__ void __launch_bounds__(LF_THREADS, LF_CTAS) itemscan_kernel(
                 uint32_t e8hi;
                 const uint32_t e8 = word_e8(ub, wv, e8hi);
                 const bool maybe = (int)i < lim && e8 <= 254u;
-                if (!__any_sync(FULL, maybe)) continue;
-                // the keep rule, as in the v1 kernel (see there): first band on the u8 sum, later
-                // bands on the exact fp32 bound
-                const uint32_t pos = (cell0 + ld_sh_u8(clp + i)) * CELL + (lane & 7u);
-                const QConst kq = qc[g];
-                const bool band0 = kq.lo < 0.f;
-                const bool first = maybe && band0;
-                const bool check = maybe && !band0;
-                const float lb = check ? word_lb(lut_all + (uint64_t)qid[g] * W * CARD, wv) : 0.f;
-                const bool keep = (first || (check && lb > kq.lo && lb <= kq.T)) && pos_ok(kq, pos) && pos < N;
-                uint32_t b = e8 <= E_SURE ? e8 : B_UNCHECKED;
-                if (check) {
-                    const float y = __fmul_rd(lb, qsc[g]);
-                    b = lb > 0.f ? (y >= 254.f ? 254u : (uint32_t)y) : 0u;
-                }
-                if (keep)
-                    atomicAdd(&shist[g][first ? min(e8 * HIST_BINS / 254u, HIST_BINS - 1) : hist_bin(lb, kq.lo, kq.T)], 1u);
-                emit(keep, pos, b | (e8hi << 8), g, lane, lt, wbuf, wcnt, s_ovf, qid, cand, candq, cand_cnt, cap);
+                // Members that pass the u8 test are only staged here: (position, query | u8 sums) into
+                // the warp's buffer. The keep rule runs when the buffer is emptied, one staged member
+                // per lane (flush_staged), instead of once per passing warp iteration for one or two
+                // live lanes.
+                const uint32_t bal = __ballot_sync(FULL, maybe);
+                if (!bal) continue;
+                if (maybe)
+                    wbuf[wcnt + __popc(bal & lt)] =
+                        make_uint2((cell0 + ld_sh_u8(clp + i)) * CELL + (lane & 7u), (g << 16) | (e8hi << 8) | e8);
+                wcnt += __popc(bal);
+                if (wcnt > WB - 32) flush_staged();
             }
             cp_async_wait<0>();  // the trailing copy (a repeat of the first cell)
         };
@@ -1189,7 +1232,7 @@ __global__ void __launch_bounds__(LF_THREADS, LF_CTAS) itemscan_kernel(
             }
         }
         if (prev.y) stage_b(prev.x, prev.y, cl0_sh + buf * CLIST);
-        if (wcnt) wflush(wbuf, wcnt, lane, s_ovf, qid, cand, candq, cand_cnt, cap);  // (warp-uniform)
+        if (wcnt) flush_staged();  // (warp-uniform)
         // the group's histograms and surviving-leaf counts into global memory
         __syncthreads();
         if (t < G && alive_cnt[t] && g0 + t < nq) atomicAdd(&leaves_alive[qid[t]], alive_cnt[t]);
