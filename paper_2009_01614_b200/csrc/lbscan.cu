@@ -350,8 +350,11 @@ constexpr uint32_t E_SURE = 237;
 // this CTA's appends: the list is dropped for the round anyway (R10: an overflowed list is neither
 // refined nor needed, only the histogram is), and a query with millions of candidates would
 // otherwise serialise every CTA on its count.
+#ifndef ISAX_SCAN_V1
+#define ISAX_SCAN_V1 0  // 1: the round-2b kernel (leaf worklist, lane = member of a whole leaf), for A/B
+#endif
 #ifndef ISAX_WB
-#define ISAX_WB 48
+#define ISAX_WB (ISAX_SCAN_V1 ? 64 : 96)  // (item scan: 0.736 -> 0.728 ms at cfg3 with 96 instead of 48)
 #endif
 constexpr uint32_t WB = ISAX_WB;  // staged candidates per warp (flushed when more than WB - 32 are staged)
 // R17: (member, query) pairs that pass the coarse test wait in a per-warp ring of SV words + metas
@@ -1251,9 +1254,6 @@ __global__ void __launch_bounds__(LF_THREADS, LF_CTAS) itemscan_kernel(
     }
 }
 
-#ifndef ISAX_SCAN_V1
-#define ISAX_SCAN_V1 0  // 1: the round-2b kernel (leaf worklist, lane = member of a whole leaf), for A/B
-#endif
 #ifndef ISAX_TASKS_PER_SM
 #define ISAX_TASKS_PER_SM 16
 #endif
