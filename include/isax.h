@@ -36,7 +36,8 @@ enum {
     ISAX_E_NOMEM = -4,       /* a device or pinned allocation failed */
     ISAX_E_CUDA = -5,        /* a CUDA runtime error; the message names it */
     ISAX_E_NONFINITE = -6,   /* NaN or Inf in a series or a query */
-    ISAX_E_CALLBACK = -7     /* a fill callback returned non-zero */
+    ISAX_E_CALLBACK = -7,    /* a fill callback returned non-zero */
+    ISAX_E_IO = -8           /* isax_save / isax_load: the file cannot be opened, written or read in full */
 };
 
 /* Tunables. Pass NULL for the defaults. */
@@ -162,6 +163,17 @@ int isax_debug_plan_round(float *band_lo_hi, uint32_t *band_pos, uint32_t *state
  * fails: the bounds build then returns ISAX_E_CUDA (the trap leaves the CUDA context unusable, so
  * call it with fire != 0 only in a process of its own); the product build returns 0. */
 int isax_debug_bounds(int fire);
+
+/* Persistence (not in the paper's in-memory path; the on-disk ParIS pipeline, is out of scope: this
+ * only spares a rebuild). isax_save writes the index's geometry and every device array (stored rows, words,
+ * permutation, kd splits and node summaries) to `path` (host file name), chunked through a pinned buffer;
+ * isax_load reads such a file onto the current device and returns an index that holds byte for byte what the
+ * saved one held, so it returns the same answers. opts as for isax_build (NULL = defaults; the file stores
+ * none). Errors: ISAX_E_IO (open / short read or write), ISAX_E_INVAL (not an index file, sizes inconsistent),
+ * ISAX_E_UNSUPPORTED (a file of another layout version), ISAX_E_NOMEM. The file is as large as the index
+ * (about 4n + 29 bytes per series). */
+int isax_save(const isax_index *ix, const char *path);
+int isax_load(const char *path, const isax_opts *opts, isax_index **out);
 
 /* Counters of the last isax_nn1 / isax_nn1_async call, as a JSON object written to buf.
  * It holds per-query window, window_rows (rows the approximate answer refined), candidates,

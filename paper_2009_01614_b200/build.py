@@ -51,7 +51,7 @@ def build_one(name: str, force: bool = False, verbose: bool = False) -> str:
     cmds = [[NVCC, *ARCH, *FLAGS, *inc, "-c", s, "-o", o] for s, o in zip(srcs, objs)]
     with ThreadPoolExecutor(max_workers=min(8, len(cmds))) as ex:
         results = list(ex.map(lambda c: subprocess.run(c, capture_output=True, text=True), cmds))
-    link = [NVCC, *ARCH, "-shared", "-Xcompiler", "-fPIC", *objs, "-o", tmp]
+    link = [NVCC, *ARCH, "-shared", "-Xcompiler", "-fPIC", *objs, "-ldl", "-o", tmp]
     results.append(subprocess.run(link, capture_output=True, text=True) if all(r.returncode == 0 for r in results) else None)
     log = os.path.join(os.path.dirname(out), f"build_{name}.log")
     text = ""

@@ -11,8 +11,19 @@
 #include <limits>
 #include <string>
 
+#include <nvtx3/nvToolsExt.h>  // header-only; ranges show up under nsys / ncu --nvtx, no-ops otherwise
+
 #include "isax_internal.cuh"
 #include "round_plan.h"
+
+namespace {
+struct NvtxRange {  // an NVTX range for the enclosing scope
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange &) = delete;
+    NvtxRange &operator=(const NvtxRange &) = delete;
+};
+}  // namespace
 
 namespace isax {
 
@@ -269,6 +280,7 @@ static int build_impl(const Source &src, uint64_t N, uint32_t n, uint32_t w, uin
     TRY(dmalloc(&bad, 1, nullptr));
     TRY(cudaMemsetAsync(bad, 0, sizeof(uint32_t), s));
     if (chunked) TRY(dmalloc(&stage, chunk * n, nullptr));
+    NvtxRange nvtx_build("isax_build");
     // pass 1: summarise
     auto produce = [&](uint64_t id0, uint64_t cnt) -> int {
         if (src.host) {
@@ -401,6 +413,7 @@ static int grow_near(isax_index *ix, uint32_t i, uint32_t seen, cudaStream_t s) 
 }
 
 static int nn1_device(isax_index *ix, const float *d_q, uint32_t Q, int64_t *d_id, float *d_dist, cudaStream_t s) {
+    NvtxRange nvtx_call("isax_nn1");
     int rc = alloc_scratch(ix);
     if (rc) return rc;
     QueryScratch &qs = ix->qs;
@@ -450,8 +463,9 @@ static int nn1_device(isax_index *ix, const float *d_q, uint32_t Q, int64_t *d_i
         } else if (fopt == 0.f) {
             adapt = true;
             bool on;
-            if (ix->fb_ms_on < 0.f) on = true;
-            else if (ix->fb_ms_off < 0.f) on = false;
+            // each mode is timed twice at first, alternating, and the smaller time kept: an index's
+            // very first batch also pays for loading its kernels
+            if (ix->fb_n_on < 2 || ix->fb_n_off < 2) on = ix->fb_n_on <= ix->fb_n_off;
             else {
                 on = ix->fb_ms_on <= ix->fb_ms_off;
                 if (ix->fb_since >= ix->fb_every) on = !on;
@@ -496,6 +510,7 @@ static int nn1_device(isax_index *ix, const float *d_q, uint32_t Q, int64_t *d_i
         std::vector<uint32_t> rewin;
         bool offs_dirty = false;
         for (uint32_t round = 0;; round++) {
+            NvtxRange nvtx_round(round == 0 ? "isax_nn1: round 0 (scan, candcheck, refine)" : "isax_nn1: overflow or band round");
             uint32_t nact = 0;
             for (uint32_t i = 0; i < B; i++) {
                 if (!pending[i]) continue;
@@ -612,10 +627,12 @@ static int nn1_device(isax_index *ix, const float *d_q, uint32_t Q, int64_t *d_i
             if (cudaEventElapsedTime(&ms, ix->ev[0], ix->ev[7]) == cudaSuccess) {
                 const float per = ms / (float)B;
                 float &slot = band0 > 0.f ? ix->fb_ms_on : ix->fb_ms_off;
-                const bool known = ix->fb_ms_on >= 0.f && ix->fb_ms_off >= 0.f;
+                uint32_t &nmeas = band0 > 0.f ? ix->fb_n_on : ix->fb_n_off;
+                const bool known = ix->fb_n_on >= 2 && ix->fb_n_off >= 2;
                 const bool pref_on = ix->fb_ms_on <= ix->fb_ms_off;
                 const bool preferred = known && (band0 > 0.f) == pref_on;
-                slot = slot < 0.f ? per : 0.5f * (slot + per);
+                slot = slot < 0.f ? per : (nmeas < 2 ? std::min(slot, per) : 0.5f * (slot + per));
+                nmeas++;
                 if (preferred) {
                     ix->fb_since++;
                 } else {  // a re-timing: back off if the choice holds, start over if it flipped
@@ -666,6 +683,152 @@ __global__ void bounds_probe_kernel(int fire) { ISAX_BOUND(fire == 0); }
 }  // namespace isax
 
 using namespace isax;
+
+// ------------------------------------------------------------------------------------ save / load
+// File: a header (magic, version, geometry, the byte count of every array), then the index's
+// device arrays in a fixed order. A loaded index holds byte for byte what the saved one held, so
+// it answers identically. Arrays move through one pinned staging buffer in chunks.
+namespace {
+constexpr char SAVE_MAGIC[8] = {'I', 'S', 'A', 'X', 'B', '2', '0', '0'};
+constexpr uint32_t SAVE_VERSION = 2;  // bumped with the layout (v2: kd order down to 8-row cells, cell summaries)
+constexpr int SAVE_ARRAYS = 9;
+struct SaveHeader {
+    char magic[8];
+    uint32_t version, n, w, card;
+    uint64_t N;
+    uint32_t leaf, cell, super_, hyper;  // node sizes the arrays were built for
+    uint64_t bytes[SAVE_ARRAYS];         // stored, sax, perm, skey, ksplit, lmeta, cmeta, smeta, hmeta
+};
+struct ArrayRef {
+    void **ptr;
+    uint64_t bytes;
+};
+void index_arrays(isax_index *ix, ArrayRef (&a)[SAVE_ARRAYS]) {
+    const uint64_t N = ix->N;
+    const uint64_t nleaf = (N + LEAF_SIZE - 1) / LEAF_SIZE, npad = nleaf * LEAF_SIZE;
+    const uint64_t nsuper = (N + SUPER_SIZE - 1) / SUPER_SIZE, nhyper = (N + HYPER_SIZE - 1) / HYPER_SIZE;
+    a[0] = {(void **)&ix->stored, N * ix->n * sizeof(float)};
+    a[1] = {(void **)&ix->sax, npad * W};
+    a[2] = {(void **)&ix->perm, N * sizeof(uint32_t)};
+    a[3] = {(void **)&ix->skey, nsuper * sizeof(uint4)};
+    a[4] = {(void **)&ix->ksplit, nsuper * sizeof(KdSplits)};
+    a[5] = {(void **)&ix->lmeta, nleaf * 32};
+    a[6] = {(void **)&ix->cmeta, (npad / KD_CELL) * 32};
+    a[7] = {(void **)&ix->smeta, nsuper * 32};
+    a[8] = {(void **)&ix->hmeta, nhyper * 32};
+}
+constexpr size_t IO_CHUNK = 64u << 20;
+}  // namespace
+
+extern "C" {
+
+int isax_save(const isax_index *cix, const char *path) {
+    if (!cix || !path) return set_error(ISAX_E_INVAL, "NULL argument");
+    isax_index *ix = const_cast<isax_index *>(cix);
+    std::lock_guard<std::mutex> lk(ix->mu);
+    DeviceGuard dg(ix->device);
+    ArrayRef arr[SAVE_ARRAYS];
+    index_arrays(ix, arr);
+    SaveHeader h{};
+    memcpy(h.magic, SAVE_MAGIC, 8);
+    h.version = SAVE_VERSION;
+    h.n = ix->n; h.w = ix->w; h.card = ix->card; h.N = ix->N;
+    h.leaf = LEAF_SIZE; h.cell = KD_CELL; h.super_ = SUPER_SIZE; h.hyper = HYPER_SIZE;
+    for (int k = 0; k < SAVE_ARRAYS; k++) h.bytes[k] = arr[k].bytes;
+    FILE *f = fopen(path, "wb");
+    if (!f) return set_error(ISAX_E_IO, std::string("cannot open for writing: ") + path);
+    void *stage = nullptr;
+    if (cudaMallocHost(&stage, IO_CHUNK) != cudaSuccess) {
+        fclose(f);
+        cudaGetLastError();
+        return set_error(ISAX_E_NOMEM, "pinned staging buffer");
+    }
+    int rc = ISAX_OK;
+    if (fwrite(&h, sizeof h, 1, f) != 1) rc = set_error(ISAX_E_IO, "short write (header)");
+    for (int k = 0; k < SAVE_ARRAYS && !rc; k++) {
+        const char *src = static_cast<const char *>(*arr[k].ptr);
+        for (uint64_t off = 0; off < arr[k].bytes && !rc; off += IO_CHUNK) {
+            const size_t nb = (size_t)std::min<uint64_t>(IO_CHUNK, arr[k].bytes - off);
+            const cudaError_t e = cudaMemcpy(stage, src + off, nb, cudaMemcpyDeviceToHost);
+            if (e != cudaSuccess) rc = cuda_error(e, "D2H (save)");
+            else if (fwrite(stage, 1, nb, f) != nb) rc = set_error(ISAX_E_IO, "short write");
+        }
+    }
+    cudaFreeHost(stage);
+    if (fclose(f) != 0 && !rc) rc = set_error(ISAX_E_IO, "close failed");
+    return rc;
+}
+
+int isax_load(const char *path, const isax_opts *opts, isax_index **out) {
+    if (!path || !out) return set_error(ISAX_E_INVAL, "NULL argument");
+    FILE *f = fopen(path, "rb");
+    if (!f) return set_error(ISAX_E_IO, std::string("cannot open: ") + path);
+    SaveHeader h{};
+    if (fread(&h, sizeof h, 1, f) != 1 || memcmp(h.magic, SAVE_MAGIC, 8) != 0) {
+        fclose(f);
+        return set_error(ISAX_E_INVAL, "not an isax index file");
+    }
+    if (h.version != SAVE_VERSION || h.leaf != LEAF_SIZE || h.cell != KD_CELL || h.super_ != SUPER_SIZE || h.hyper != HYPER_SIZE) {
+        fclose(f);
+        return set_error(ISAX_E_UNSUPPORTED, "index file of another layout version");
+    }
+    const isax_opts o = default_opts(opts);
+    int rc = check_geometry(h.N, h.n, h.w, h.card, o);
+    if (rc) {
+        fclose(f);
+        return rc;
+    }
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) {
+        fclose(f);
+        return cuda_error(cudaGetLastError(), "cudaGetDevice");
+    }
+    isax_index *ix = new isax_index();
+    ix->N = h.N; ix->n = h.n; ix->w = h.w; ix->card = h.card; ix->opts = o; ix->device = dev;
+    ix->win_auto = !(opts && opts->window_L);
+    ix->win_L = o.window_L;
+    ix->pr_auto = !(opts && opts->probe_L);
+    ix->pr_L = o.probe_L;
+    ArrayRef arr[SAVE_ARRAYS];
+    index_arrays(ix, arr);
+    void *stage = nullptr;
+    auto fail = [&](int code) {
+        for (int k = 0; k < SAVE_ARRAYS; k++) cudaFree(*arr[k].ptr);
+        if (stage) cudaFreeHost(stage);
+        fclose(f);
+        delete ix;
+        cudaGetLastError();
+        return code;
+    };
+    for (int k = 0; k < SAVE_ARRAYS; k++)
+        if (h.bytes[k] != arr[k].bytes) return fail(set_error(ISAX_E_INVAL, "index file: array sizes do not match its geometry"));
+    if (cudaMallocHost(&stage, IO_CHUNK) != cudaSuccess) return fail(set_error(ISAX_E_NOMEM, "pinned staging buffer"));
+    for (int k = 0; k < SAVE_ARRAYS; k++) {
+        if (cudaMalloc(arr[k].ptr, std::max<uint64_t>(arr[k].bytes, 1)) != cudaSuccess)
+            return fail(set_error(ISAX_E_NOMEM, "device memory for the index"));
+        ix->device_bytes += arr[k].bytes;
+        char *dst = static_cast<char *>(*arr[k].ptr);
+        for (uint64_t off = 0; off < arr[k].bytes; off += IO_CHUNK) {
+            const size_t nb = (size_t)std::min<uint64_t>(IO_CHUNK, arr[k].bytes - off);
+            if (fread(stage, 1, nb, f) != nb) return fail(set_error(ISAX_E_IO, "index file is truncated"));
+            const cudaError_t e = cudaMemcpy(dst + off, stage, nb, cudaMemcpyHostToDevice);
+            if (e != cudaSuccess) return fail(cuda_error(e, "H2D (load)"));
+        }
+    }
+    cudaFreeHost(stage);
+    stage = nullptr;
+    fclose(f);
+    for (auto &ev : ix->ev)
+        if (cudaEventCreate(&ev) != cudaSuccess) {
+            for (int k = 0; k < SAVE_ARRAYS; k++) cudaFree(*arr[k].ptr);
+            delete ix;
+            return cuda_error(cudaGetLastError(), "cudaEventCreate");
+        }
+    *out = ix;
+    return ISAX_OK;
+}
+
+}  // extern "C"
 
 extern "C" {
 

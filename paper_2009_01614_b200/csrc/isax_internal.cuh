@@ -229,6 +229,7 @@ struct isax_index {
     // with and without the first band (-1 = not measured yet); the cheaper mode is used, the other
     // one re-measured after fb_every batches
     float fb_ms_on = -1.f, fb_ms_off = -1.f;
+    uint32_t fb_n_on = 0, fb_n_off = 0;  // measurements taken of each mode
     bool win_auto = true;       // window_L left to the library (opts.window_L == 0)
     uint32_t win_L = 3072;      // main window rows of the current batch (R5; 1024 in best-first mode when auto)
     bool pr_auto = true;        // probe_L left to the library (opts.probe_L == 0)

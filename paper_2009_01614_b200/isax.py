@@ -24,7 +24,7 @@ _P, _U64, _U32 = ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint32
 
 ISAX_OK = 0
 ERRORS = {-1: "ISAX_E_INVAL", -2: "ISAX_E_EMPTY", -3: "ISAX_E_UNSUPPORTED", -4: "ISAX_E_NOMEM", -5: "ISAX_E_CUDA",
-          -6: "ISAX_E_NONFINITE", -7: "ISAX_E_CALLBACK"}
+          -6: "ISAX_E_NONFINITE", -7: "ISAX_E_CALLBACK", -8: "ISAX_E_IO"}
 
 
 class Opts(ctypes.Structure):
@@ -53,6 +53,8 @@ isax_debug_plan_round = _sig("isax_debug_plan_round", [_P, _P, _P, _U32, _U32, _
 isax_info = _sig("isax_info", [_P, ctypes.POINTER(_U64), ctypes.POINTER(_U32), ctypes.POINTER(_U32),
                                ctypes.POINTER(_U32), ctypes.POINTER(_U64)])
 isax_debug_bounds = _sig("isax_debug_bounds", [ctypes.c_int])
+isax_save = _sig("isax_save", [_P, ctypes.c_char_p])
+isax_load = _sig("isax_load", [ctypes.c_char_p, _P, ctypes.POINTER(_P)])
 isax_free = _sig("isax_free", [_P], None)
 isax_last_error = _sig("isax_last_error", [], ctypes.c_char_p)
 isax_version = _sig("isax_version", [], ctypes.c_char_p)
@@ -129,6 +131,18 @@ class Index:
         _check(isax_build_stream(N, n, w, card, fill_ptr, ctypes.cast(ctypes.pointer(ctx), _P), chunk, ctypes.byref(o),
                                  ctypes.byref(h)), "isax_build_stream")
         return cls(h.value, keep=ctx)
+
+    @classmethod
+    def load(cls, path: str, **opts):
+        """isax_load: an index saved by save(), onto the current CUDA device."""
+        h = _P()
+        o = _opts(**opts)
+        _check(isax_load(os.fsencode(path), ctypes.byref(o), ctypes.byref(h)), "isax_load")
+        return cls(h.value)
+
+    def save(self, path: str):
+        """isax_save: the whole index (rows, words, permutation, node summaries) to a file."""
+        _check(isax_save(self._h, os.fsencode(path)), "isax_save")
 
     # -- queries -------------------------------------------------------------------------------
     def nn1_bound(self, queries, out_id, out_dist, stream):

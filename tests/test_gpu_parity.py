@@ -8,6 +8,8 @@ Bars (DESIGN.md "Parity"):
 Sizes span many tiles and a ragged tail; edge cases cover N = 1, N < window, duplicates,
 constant series, exact-copy queries, overflow rounds and batch splitting.
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -463,3 +465,42 @@ def test_stats_report_build_stages_and_scan_counters():
     assert 16 * tests <= by <= 32 * tests + 5 * sum(st["candidates"]) + 64
     assert st["cell_size"] == 8 and st["leaf_size"] == 32
     assert st["leaf_pairs_first_launch"] == sum(st["leaves_alive"])
+
+
+def test_save_load_round_trip(tmp_path):
+    """isax_save / isax_load: the loaded index holds the same words, permutation and rows, and
+    returns the same (oracle-checked) answers; bad files give the documented errors."""
+    N, n = 40_000, 128
+    wl = small_workload(N, n, Q=12, q_noisy=4)
+    x = datagen.series(wl, 0, N)
+    q, _ = datagen.queries(wl)
+    ids_or, dist_or, _ = oracle_nn1(x.cpu().numpy(), q.cpu().numpy())
+    path = str(tmp_path / "ix.isax")
+    with _build(x) as ix:
+        ids0, dist0 = ix.nn1(q)
+        ex0 = ix.export(0, N, sax=True, perm=True, stored=True)
+        ix.save(path)
+    assert os.path.getsize(path) > N * n * 4
+    with isax.Index.load(path) as ix2:
+        assert (ix2.N, ix2.n, ix2.w, ix2.card) == (N, n, 16, 256)
+        ex1 = ix2.export(0, N, sax=True, perm=True, stored=True)
+        ids1, dist1 = ix2.nn1(q)
+    for k in ("sax", "perm", "stored"):
+        np.testing.assert_array_equal(ex0[k], ex1[k])
+    assert_nn_parity(ids1.cpu().numpy(), dist1.cpu().numpy(), ids_or, dist_or)
+    np.testing.assert_array_equal(ids0.cpu().numpy(), ids1.cpu().numpy())
+    np.testing.assert_array_equal(dist0.cpu().numpy(), dist1.cpu().numpy())
+    # a truncated file, a file that is not an index, a missing file
+    blob = open(path, "rb").read()
+    bad = str(tmp_path / "short.isax")
+    open(bad, "wb").write(blob[: len(blob) // 2])
+    with pytest.raises(isax.IsaxError) as e:
+        isax.Index.load(bad)
+    assert e.value.name == "ISAX_E_IO"
+    open(bad, "wb").write(b"not an index" * 20)
+    with pytest.raises(isax.IsaxError) as e:
+        isax.Index.load(bad)
+    assert e.value.name == "ISAX_E_INVAL"
+    with pytest.raises(isax.IsaxError) as e:
+        isax.Index.load(str(tmp_path / "missing.isax"))
+    assert e.value.name == "ISAX_E_IO"

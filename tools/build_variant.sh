@@ -13,6 +13,6 @@ for s in paper_2009_01614_b200/csrc/*.cu; do
   pids+=($!)
 done
 for p in ${pids[@]}; do wait $p || { cat $od/obj/*.log | grep -i error | head; exit 1; }; done
-/usr/local/cuda/bin/nvcc $ARCH -shared -Xcompiler -fPIC $od/obj/*.o -o $od/libisax.so
+/usr/local/cuda/bin/nvcc $ARCH -shared -Xcompiler -fPIC $od/obj/*.o -ldl -o $od/libisax.so
 grep -h "spill stores" $od/obj/*.log | grep -v " 0 bytes spill" | head -3
 echo "$od/libisax.so"
