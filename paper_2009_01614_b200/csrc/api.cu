@@ -463,9 +463,9 @@ static int nn1_device(isax_index *ix, const float *d_q, uint32_t Q, int64_t *d_i
         } else if (fopt == 0.f) {
             adapt = true;
             bool on;
-            // each mode is timed twice at first, alternating, and the smaller time kept: an index's
-            // very first batch also pays for loading its kernels
-            if (ix->fb_n_on < 2 || ix->fb_n_off < 2) on = ix->fb_n_on <= ix->fb_n_off;
+            // the first three batches run on, off, on, and the smaller of the two "on" times is kept:
+            // an index's very first batch also pays for loading its kernels
+            if (ix->fb_n_on < 2 || ix->fb_n_off < 1) on = ix->fb_n_on <= ix->fb_n_off;
             else {
                 on = ix->fb_ms_on <= ix->fb_ms_off;
                 if (ix->fb_since >= ix->fb_every) on = !on;
@@ -628,7 +628,7 @@ static int nn1_device(isax_index *ix, const float *d_q, uint32_t Q, int64_t *d_i
                 const float per = ms / (float)B;
                 float &slot = band0 > 0.f ? ix->fb_ms_on : ix->fb_ms_off;
                 uint32_t &nmeas = band0 > 0.f ? ix->fb_n_on : ix->fb_n_off;
-                const bool known = ix->fb_n_on >= 2 && ix->fb_n_off >= 2;
+                const bool known = ix->fb_n_on >= 2 && ix->fb_n_off >= 1;
                 const bool pref_on = ix->fb_ms_on <= ix->fb_ms_off;
                 const bool preferred = known && (band0 > 0.f) == pref_on;
                 slot = slot < 0.f ? per : (nmeas < 2 ? std::min(slot, per) : 0.5f * (slot + per));
