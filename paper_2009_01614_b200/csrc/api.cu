@@ -551,8 +551,8 @@ static int nn1_device(isax_index *ix, const float *d_q, uint32_t Q, int64_t *d_i
             // speculative: a query scanned again in a later round is finalised again
             launch_finalize(ix, nact, qs.qmap, delta, d_id + b0, d_dist + b0, s);
             cudaEventRecord(ix->ev[7], s);  // the batch's end so far (R15 policy timing)
-            // scanprep + scan, candcheck, refine + filter + refine, finalize
-            ix->st_launches += ((ix->opts.flags & ISAX_FLAG_FLAT_SCAN) ? 1 : 2) + 5;
+            // scanprep + node scan + item scan (or scanprep + flat scan), candcheck, refine + filter + refine, finalize
+            ix->st_launches += ((ix->opts.flags & ISAX_FLAG_FLAT_SCAN) ? 2 : 3) + 5;
             if (timed && round == 0) cudaEventRecord(ix->ev[5], s);
             ISAX_CUDA(cudaGetLastError());
             // the whole status block in one copy (StatusBlock: bsf, counters, flags, byte counts)
