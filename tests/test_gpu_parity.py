@@ -504,3 +504,30 @@ def test_save_load_round_trip(tmp_path):
     with pytest.raises(isax.IsaxError) as e:
         isax.Index.load(str(tmp_path / "missing.isax"))
     assert e.value.name == "ISAX_E_IO"
+
+
+def test_summaries_bit_exact_when_the_row_sum_rounds():
+    """Rows whose fp64 sum rounds (a value next to zero, a denormal, a wide dynamic range) depend on
+    the summation order: the kernel must take the definition's left-to-right order (R3) and give
+    the oracle's words and rows bit for bit; all-zero and nearly-zero rows too."""
+    N, n = 4_096, 256
+    wl = small_workload(N, n, "walk")
+    x = datagen.series(wl, 0, N).clone()
+    x[5, 17] = 1e-12          # 2^-40 of the row's magnitude: the sum rounds
+    x[6, 3] = 1e-40           # a denormal
+    x[7, :] = 0.0
+    x[7, 100] = 3.0           # zeros and one value: exact
+    x[8, 0] = 1e20            # wide dynamic range
+    x[8, 1] = 1e-3
+    x[9, :] = 0.0             # all zeros -> the all-zero row
+    x[10, :] = x[10, :] * 1e-30  # small normal values
+    x[11, ::2] = 1.00000012   # neighbours one ulp apart
+    x[11, 1::2] = 1.0
+    for r in range(40, 60):    # a value next to zero at every quarter boundary and inside
+        x[r, (r - 40) * 13 % n] = 3e-9
+    xh = x.cpu().numpy()
+    with _build(x) as ix:
+        ex = ix.export(0, N, sax=True, perm=True, stored=True)
+    y, mu, sd, m, word = clib.summarise(xh)
+    np.testing.assert_array_equal(ex["sax"], word)
+    np.testing.assert_array_equal(ex["stored"], y[ex["perm"].astype(np.int64)])
