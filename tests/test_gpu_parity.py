@@ -310,8 +310,8 @@ def test_many_queries_span_batches():
         ids, dist = ix.nn1(q)
         st = ix.stats()
     assert_nn_parity(ids.cpu().numpy(), dist.cpu().numpy(), ids_or, dist_or)
-    # main window of every query: 3072 rows, or one super-node in batches run best-first (R15)
-    assert len(st["rounds"]) == Q and min(st["window_rows"]) >= min(1024, N)
+    # main window of every query: 3072 rows, or a 512-row kd cell in batches run best-first (R15)
+    assert len(st["rounds"]) == Q and min(st["window_rows"]) >= min(512, N)
 
 
 def test_config1_at_its_own_seeds():
