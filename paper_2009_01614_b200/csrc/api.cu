@@ -175,7 +175,7 @@ static int alloc_scratch_cap(isax_index *ix, uint32_t cap) {
     A(task_ctr, 1);
     q.scan_groups = (Q + 15) / 16 + 1;  // (a batch of 2-15 queries scans in two groups of 1-8)
     A(scan_entries, (size_t)q.scan_groups * ((ix->N + SUPER_SIZE - 1) / SUPER_SIZE));
-    A(scan_ctl, 3 * (size_t)q.scan_groups);
+    A(scan_ctl, 4 * (size_t)q.scan_groups);
     A(qmap2, Q);
 #undef A
     if (e == cudaSuccess) {

@@ -183,7 +183,7 @@ struct QueryScratch {
     unsigned long long *scan_bytes_dev = nullptr;  // leaf words and leaf summaries the leaf scan read, bytes (all launches of a call)
     uint32_t *task_ctr = nullptr;              // work counter of the persistent leaf scan (v1 kernel)
     uint2 *scan_entries = nullptr;             // [scan_groups][ceil(N/SUPER_SIZE)] (super-node, query mask) kept by the node scan
-    uint32_t *scan_ctl = nullptr;              // [scan_groups][3]: entries, claim cursor, work estimate of each query group
+    uint32_t *scan_ctl = nullptr;              // [scan_groups][4]: entries (heavy), claim cursor, work estimate, light entries of each query group
     uint32_t scan_groups = 0;                  // groups allocated: ceil(cap_Q / 16) + 1
     unsigned long long *refine_bytes = nullptr;  // [2] bytes of rows the refine passes 1 and 2 read (all launches of a call)
     uint32_t *flag = nullptr;       // non-finite query flag

@@ -866,7 +866,14 @@ constexpr uint32_t IQ = 32;                  // item ring slots per warp (a powe
 constexpr uint32_t WSC = 32 + 2 * CLIST + IQ * 8;  // per-warp scratch bytes: alive-leaf list, two alive-cell lists, item ring
 // scan control words in qs.scan_ctl (reset by scanprep_kernel): per group its entry count, its
 // claim cursor and its work estimate
-constexpr uint32_t CTL_CNT = 0, CTL_CUR = 1, CTL_WORK = 2, CTL_WORDS = 3;
+constexpr uint32_t CTL_CNT = 0, CTL_CUR = 1, CTL_WORK = 2, CTL_CNT_L = 3, CTL_WORDS = 4;
+// entries kept by HEAVY or more queries are stored from the front of the group's array and claimed
+// first, the others from the back and last: the entries still in flight when a list runs out are
+// then the short ones (0 = one list in arrival order)
+#ifndef ISAX_HEAVY
+#define ISAX_HEAVY 0
+#endif
+constexpr uint32_t HEAVY = ISAX_HEAVY;
 
 __device__ __forceinline__ void prefetch_l2(const void *p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
 __device__ __forceinline__ void st_sh_u8a(uint32_t a, uint32_t v) { asm volatile("st.shared.u8 [%0], %1;" ::"r"(a), "r"(v) : "memory"); }
@@ -951,13 +958,16 @@ __global__ void __launch_bounds__(NS_THREADS) nodescan_kernel(
             nnode += ins ? 1u : 0u;
             m |= (ok ? 1u : 0u) << g;
         }
-        const uint32_t bal = __ballot_sync(FULL, m != 0);
-        if (bal) {
+        const bool heavy = HEAVY == 0 ? m != 0 : (uint32_t)__popc(m) >= HEAVY;
+        const uint32_t balh = __ballot_sync(FULL, heavy), ball = __ballot_sync(FULL, m != 0 && !heavy);
+        if (balh | ball) {
             uint32_t off = 0;
-            if (lane == 0) off = atomicAdd(&ctl[CTL_WORDS * grp + CTL_CNT], (uint32_t)__popc(bal));
-            off = __shfl_sync(FULL, off, 0);
-            ISAX_BOUND(off + __popc(bal) <= nsuper);
-            if (m) out[off + __popc(bal & lt)] = make_uint2(sn, m);
+            if (lane == 0 && balh) off = atomicAdd(&ctl[CTL_WORDS * grp + CTL_CNT], (uint32_t)__popc(balh));
+            if (lane == 1 && ball) off = atomicAdd(&ctl[CTL_WORDS * grp + CTL_CNT_L], (uint32_t)__popc(ball));
+            const uint32_t offh = __shfl_sync(FULL, off, 0), offl = __shfl_sync(FULL, off, 1);
+            ISAX_BOUND(offh + __popc(balh) + offl + __popc(ball) <= nsuper);
+            if (heavy) out[offh + __popc(balh & lt)] = make_uint2(sn, m);
+            else if (m) out[nsuper - 1 - (offl + __popc(ball & lt))] = make_uint2(sn, m);
             work += __popc(m);
         }
     }
@@ -1024,7 +1034,8 @@ __global__ void __launch_bounds__(LF_THREADS, LF_CTAS) itemscan_kernel(
     __syncthreads();
     uint32_t grp = s_grp;
     for (uint32_t visited = 0; visited < ngroups; visited++, grp = grp + 1 == ngroups ? 0 : grp + 1) {
-        const uint32_t nent = ctl[CTL_WORDS * grp + CTL_CNT];
+        const uint32_t nheavy = ctl[CTL_WORDS * grp + CTL_CNT];
+        const uint32_t nent = nheavy + ctl[CTL_WORDS * grp + CTL_CNT_L];
         const uint32_t g0 = grp * G;
         // one thread decides whether the group still has entries (the cursor moves under our feet);
         // the barrier also ends the previous group's flush before its tables are overwritten
@@ -1053,7 +1064,7 @@ __global__ void __launch_bounds__(LF_THREADS, LF_CTAS) itemscan_kernel(
             if (lane == 0) e = atomicAdd(cursor, 1u);
             e = __shfl_sync(FULL, e, 0);
             if (e >= nent) return make_uint2(0xffffffffu, 0u);
-            const uint2 en = __ldg(ent + e);
+            const uint2 en = __ldg(ent + (e < nheavy ? e : nsuper - 1 - (e - nheavy)));
             const uint32_t leaf = en.x * SUPER + 4 * lane;  // its leaf summaries (32 x 32 B = eight lines) into L2
             if (lane < 8 && leaf < nleaf) prefetch_l2(meta4 + 2 * (uint64_t)leaf);
             return en;
@@ -1313,7 +1324,7 @@ uint64_t launch_lbscan(const isax_index *ix, uint32_t nq, uint32_t B, const uint
     const QueryScratch &qs = ix->qs;
     scanprep_kernel<<<nq, 256, 0, s>>>(qs.lut, qmap, band, qs.bsf, qs.win, onepd, qs.lut8, qs.lut8c, qs.qconst, qs.qscale, qs.qT, qs.bsf_scan,
                                       B, qs.cand_cnt, qs.cand_cnt2, qs.cnt_hi, qs.cnt_f, qs.cand_hist, qs.task_ctr, qs.scan_ctl,
-                                      3u * qs.scan_groups);
+                                      4u * qs.scan_groups);
     if (ix->opts.flags & ISAX_FLAG_FLAT_SCAN) {  // ParIS flat scan, kept for A/B measurement
         const uint32_t G = nq >= 4 ? 4 : nq;
         if (G == 4) launch_g<4>(ix, nq, qmap, band, onepd, s);
