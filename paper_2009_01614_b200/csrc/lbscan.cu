@@ -14,9 +14,11 @@
 // (MESSI's priority-queue order, done in LB bands). The next band then starts
 // where the previous one ended.
 //
-// Two kernels:
-//  - lbscan_kernel (ISAX_FLAG_FLAT_SCAN): the ParIS flat scan of every 16-byte word.
-//  - leafscan_kernel (default): MESSI-style node pruning on the sorted array (R11).
+// The scans:
+//  - nodescan_kernel + itemscan_kernel (default): MESSI-style node pruning on the sorted array over
+//    four node levels (R11, R11c): hyper-node, super-node | leaf, 8-row kd cell, member.
+//  - lbscan_kernel (ISAX_FLAG_FLAT_SCAN): the ParIS flat scan of every 16-byte word (A/B).
+//  - leafscan_kernel (-DISAX_SCAN_V1=1): the round-2b single-kernel node scan over three levels (A/B).
 #include "isax_device.cuh"
 
 namespace isax {
@@ -269,8 +271,9 @@ static void launch_g(const isax_index *ix, uint32_t nq, const uint32_t *qmap, co
         qs.cand, qs.candq, qs.cand_cnt, qs.cand_cap, qs.cand_hist);
 }
 
-// ------------------------------------------------------------------------------------ leaf scan
-// The default scan: MESSI's node pruning on the sorted array (R11). P:346-349: "the index
+// ------------------------------------------------------------------------------------ leaf scan (round 2b, -DISAX_SCAN_V1=1)
+// The default scan until round 2c (now nodescan_kernel + itemscan_kernel below; the node bounds and
+// the candidate staging defined here are shared): MESSI's node pruning on the sorted array (R11). P:346-349: "the index
 // workers traverse the index subtrees ... using BSF to decide which subtrees will be pruned";
 // leaves that survive are examined "by first computing lower bound distances using the
 // iSAX summaries".
