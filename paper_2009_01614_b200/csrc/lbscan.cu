@@ -95,6 +95,25 @@ __device__ __forceinline__ uint32_t node_e8(uint32_t ub, const uint4 &qa, const 
     return es;
 }
 
+// node_e8 on summaries already unpacked to u16x2 pairs (unpack_u16x2): for a caller that tests one
+// summary against several queries
+__device__ __forceinline__ void unpack_u16x2(const uint4 &v, uint32_t (&o)[8]) {
+    o[0] = lo_u16x2(v.x); o[1] = hi_u16x2(v.x); o[2] = lo_u16x2(v.y); o[3] = hi_u16x2(v.y);
+    o[4] = lo_u16x2(v.z); o[5] = hi_u16x2(v.z); o[6] = lo_u16x2(v.w); o[7] = hi_u16x2(v.w);
+}
+__device__ __forceinline__ uint32_t node_e8_unpacked(uint32_t ub, const uint4 &qa, const uint4 &qb, const uint32_t (&mn)[8],
+                                                    const uint32_t (&mx)[8]) {
+    const uint32_t qv[8] = {qa.x, qa.y, qa.z, qa.w, qb.x, qb.y, qb.z, qb.w};
+    uint32_t es = 0;
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+        const uint32_t c2 = min_u16x2(max_u16x2(qv[k], mn[k]), mx[k]);
+        es += ld_sh_u8(__byte_perm(c2, ub, 0x7650u) + (2 * k) * CARD);
+        es += ld_sh_u8(__byte_perm(c2, ub, 0x7652u) + (2 * k + 1) * CARD);
+    }
+    return es;
+}
+
 // coarse member bound (R17): 8 lookups in the query's [8][256] pair table at cb (256-aligned). P0 / P1
 // hold the pair indices of a word: byte k of P0 = hi4(sym_k) | hi4(sym_{k+4}) << 4 (pairs 0..3), byte k
 // of P1 = hi4(sym_{8+k}) | hi4(sym_{12+k}) << 4 (pairs 4..7).
@@ -1083,10 +1102,13 @@ __global__ void __launch_bounds__(LF_THREADS, LF_CTAS) itemscan_kernel(
                 mx4 = __ldg(meta4 + 2 * (uint64_t)leaf + 1);
             }
             bool any_ok = false;
+            uint32_t mnu[8], mxu[8];  // unpacked once for all the queries of the mask
+            unpack_u16x2(mn4, mnu);
+            unpack_u16x2(mx4, mxu);
 #pragma unroll 1
             for (uint32_t mm = en.y; mm; mm &= mm - 1) {
                 const uint32_t g = __ffs(mm) - 1;
-                const bool ok = inr && node_e8(lut8_sh + g * W * CARD, qsym[g][0], qsym[g][1], mn4, mx4) <= 254u;
+                const bool ok = inr && node_e8_unpacked(lut8_sh + g * W * CARD, qsym[g][0], qsym[g][1], mnu, mxu) <= 254u;
                 nnode += inr ? 1u : 0u;
                 any_ok |= ok;
                 const uint32_t bal = __ballot_sync(FULL, ok);
