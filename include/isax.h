@@ -60,8 +60,10 @@ typedef struct isax_opts {
                             batch (first_band, R15). */
     float first_band;    /* best-first scan order (R15): round 0 scans only the smallest bounds,
                             LB^2 <= first_band * bsf0^2 (1 + delta), refines them, and the next round scans
-                            the rest under the improved BSF; with window_L = 0 the main window is then one
-                            super-node (and with probe_L = 0 each probe window 64 rows). 0 = adaptive
+                            the rest under the improved BSF; only the queries whose scan under the whole
+                            threshold would keep more than 1/16 of the super-nodes get the fraction, the
+                            others are scanned completely in round 0; with window_L = 0 the main window is
+                            then a 512-row kd cell (and with probe_L = 0 each probe window 64 rows). 0 = adaptive
                             (default): fraction 1/50 or none, whichever the index measured to be faster per
                             query (device time); the other mode is re-timed after
                             32, 64, ... up to 512 batches while the choice holds. In (0, 1) = always, that

@@ -112,7 +112,7 @@ static void free_scratch(isax_index *ix) {
     cudaFree(q.qy); cudaFree(q.qpaa); cudaFree(q.qsax); cudaFree(q.lut); cudaFree(q.lut8); cudaFree(q.lut8c); cudaFree(q.qconst); cudaFree(q.pwin);
     cudaFree(q.cand); cudaFree(q.candq); cudaFree(q.cand2); cudaFree(q.candq2); cudaFree(q.cnt_f); cudaFree(q.qscale); cudaFree(q.qT);
     cudaFree(q.near); cudaFree(q.near_off); cudaFree(q.near_cap);
-    cudaFree(q.qmap); cudaFree(q.qband); cudaFree(q.cand_hist); cudaFree(q.task_ctr); cudaFree(q.qmap2); cudaFree(q.scan_entries); cudaFree(q.scan_ctl);
+    cudaFree(q.qmap); cudaFree(q.qband); cudaFree(q.cand_hist); cudaFree(q.task_ctr); cudaFree(q.qmap2); cudaFree(q.scan_entries); cudaFree(q.scan_ctl); cudaFree(q.qkept);
     cudaFree(q.status);  // bsf, bsf_scan, cand_cnt, cand_cnt2, cnt_hi, near_cnt, flag, counters, win, leaves, byte counters
     if (q.h_mirror) cudaFreeHost(q.h_mirror);
     q = QueryScratch{};
@@ -176,6 +176,7 @@ static int alloc_scratch_cap(isax_index *ix, uint32_t cap) {
     q.scan_groups = (Q + 15) / 16 + 1;  // (a batch of 2-15 queries scans in two groups of 1-8)
     A(scan_entries, (size_t)q.scan_groups * ((ix->N + SUPER_SIZE - 1) / SUPER_SIZE));
     A(scan_ctl, 4 * (size_t)q.scan_groups);
+    A(qkept, Q);
     A(qmap2, Q);
 #undef A
     if (e == cudaSuccess) {
@@ -544,7 +545,10 @@ static int nn1_device(isax_index *ix, const float *d_q, uint32_t Q, int64_t *d_i
                 ISAX_CUDA(cudaMemcpyAsync(qs.qmap, hm.qmap, nact * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
                 ISAX_CUDA(cudaMemcpyAsync(qs.qband, hm.band, nact * sizeof(Band), cudaMemcpyHostToDevice, s));
             }
-            ix->st_scan_bytes += launch_lbscan(ix, nact, B, qs.qmap, qs.qband, delta, s);
+            // (round 0 of a best-first batch: the scan itself picks the queries that get the first band)
+            const bool select = round == 0 && band0 > 0.f;
+            ix->st_scan_bytes += launch_lbscan(ix, nact, B, qs.qmap, qs.qband, delta, select, s);
+            if (select) ix->st_launches += 2;  // (the node scan's counting pass and fbdecide_kernel)
             if (timed && round == 0) cudaEventRecord(ix->ev[6], s);
             launch_candcheck(ix, B, s);
             if (timed && round == 0) cudaEventRecord(ix->ev[3], s);
@@ -569,9 +573,13 @@ static int nn1_device(isax_index *ix, const float *d_q, uint32_t Q, int64_t *d_i
                     bsf_h[i] = bsf_d2_host(hm.bsf_scan[i]);
                     bsf0_h[i] = bsf_h[i];
                     tused[i] = bsf_h[i] * onepd;
-                    if (band[i].hi < 0.f) {  // the first band's edge, as scanprep_kernel computed it
-                        tused[i] = tused[i] * -band[i].hi;
-                        band[i].hi = tused[i];
+                    if (band[i].hi < 0.f) {
+                        if (hm.bsf_scan[i] & 1ull) {  // the first band's edge, as the scan computed it
+                            tused[i] = tused[i] * -band[i].hi;
+                            band[i].hi = tused[i];
+                        } else {  // the scan gave this query its whole threshold (a cheap scan, R15)
+                            band[i].hi = INF;
+                        }
                     }
                 }
                 if (band0 > 0.f && timed) {  // stats: queries whose BSF the first band at least halved

@@ -184,6 +184,7 @@ struct QueryScratch {
     uint32_t *task_ctr = nullptr;              // work counter of the persistent leaf scan (v1 kernel)
     uint2 *scan_entries = nullptr;             // [scan_groups][ceil(N/SUPER_SIZE)] (super-node, query mask) kept by the node scan
     uint32_t *scan_ctl = nullptr;              // [scan_groups][4]: entries (heavy), claim cursor, work estimate, light entries of each query group
+    uint32_t *qkept = nullptr;                 // [Q] super-nodes the node scan kept for each active slot (R15 per query)
     uint32_t scan_groups = 0;                  // groups allocated: ceil(cap_Q / 16) + 1
     unsigned long long *refine_bytes = nullptr;  // [2] bytes of rows the refine passes 1 and 2 read (all launches of a call)
     uint32_t *flag = nullptr;       // non-finite query flag
@@ -300,7 +301,7 @@ void launch_superkd(uint8_t *sax, uint32_t *perm, uint64_t N, uint4 *skey, KdSpl
 // bsf^2 (1+delta)) and band[i].plo <= pos < band[i].phi for slot i. Returns the summary bytes it reads that the host can count (node
 // summaries or flat words); the leaf scan adds its leaf-word and leaf-summary bytes to qs.scan_bytes_dev on the device.
 uint64_t launch_lbscan(const isax_index *ix, uint32_t nq, uint32_t B, const uint32_t *qmap, const Band *band,
-                       float delta, cudaStream_t s);
+                       float delta, bool select_first_band, cudaStream_t s);
 // lbscan.cu: the exact fp32 rule for the candidates the leaf scan kept on their u8 sum alone,
 // and compaction of every list into cand2 / cand_cnt2 (the refine's input)
 void launch_candcheck(const isax_index *ix, uint32_t Q, cudaStream_t s);

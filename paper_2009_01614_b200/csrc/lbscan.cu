@@ -193,11 +193,13 @@ __device__ __forceinline__ bool pos_ok(const QConst &k, uint32_t pos) {
 }
 
 __device__ __forceinline__ QConst load_qconst(uint32_t qi, bool valid, const unsigned long long *bsf,
-                                              const Band *band, uint32_t slot, const uint32_t *win, float onepd) {
+                                              const Band *band, uint32_t slot, const uint32_t *win, float onepd,
+                                              bool defer = false) {
     const Band b = valid ? band[slot] : Band{0.f, -1.f, 0u, 0u};
     // hi < 0 encodes a fraction of the BSF threshold (the first band of a query, R15): T = bsf^2 (1 + delta) * -hi
+    // (defer: the whole threshold for now; fbdecide_kernel applies the fraction to the costly queries)
     const float tb = bsf_d2(bsf[qi]) * onepd;
-    const float tq = valid ? (b.hi < 0.f ? tb * -b.hi : fminf(tb, b.hi)) : -1.0f;  // an invalid slot keeps nothing
+    const float tq = valid ? (b.hi < 0.f ? (defer ? tb : tb * -b.hi) : fminf(tb, b.hi)) : -1.0f;  // an invalid slot keeps nothing
     return QConst{b.lo, tq, win[2 * qi], win[2 * qi + 1], b.plo, b.phi, 0u, 0u};
 }
 
@@ -446,7 +448,8 @@ __global__ void __launch_bounds__(256) scanprep_kernel(const float *__restrict__
                                                        uint32_t *__restrict__ cand_cnt, uint32_t *__restrict__ cand_cnt2,
                                                        uint32_t *__restrict__ cnt_hi, uint32_t *__restrict__ cnt_f,
                                                        uint32_t *__restrict__ hist, uint32_t *__restrict__ task_ctr,
-                                                       uint32_t *__restrict__ ctl, uint32_t nctl) {
+                                                       uint32_t *__restrict__ ctl, uint32_t nctl, uint32_t *__restrict__ qkept,
+                                                       bool defer) {
     const uint32_t i = blockIdx.x;
     // the launch's counters: every batch slot's candidate counts (block 0), the scanned query's
     // histogram (its block), the persistent scan's task counter
@@ -457,7 +460,8 @@ __global__ void __launch_bounds__(256) scanprep_kernel(const float *__restrict__
     }
     if (threadIdx.x < HIST_BINS) hist[qmap[i] * HIST_BINS + threadIdx.x] = 0;
     const uint32_t qi = qmap[i];
-    const QConst k = load_qconst(qi, true, bsf, band, i, win, onepd);
+    if (threadIdx.x == 0) qkept[i] = 0;  // super-nodes the node scan keeps for this slot
+    const QConst k = load_qconst(qi, true, bsf, band, i, win, onepd, defer);
     if (threadIdx.x == 0) {
         qconst[2 * i] = make_uint4(__float_as_uint(k.lo), __float_as_uint(k.T), k.ws, k.we);
         qconst[2 * i + 1] = make_uint4(k.plo, k.phi, 0u, 0u);
@@ -467,7 +471,9 @@ __global__ void __launch_bounds__(256) scanprep_kernel(const float *__restrict__
     if (threadIdx.x == 0) {
         qscale[qi] = sc;
         qT[qi] = k.T;
-        bsf_scan[qi] = bsf[qi];
+        // the BSF the scan uses; the id's lowest bit tells the host whether a first-band slot really
+        // got the fraction (always, unless fbdecide_kernel decides per query)
+        bsf_scan[qi] = (bsf[qi] & ~1ull) | (defer ? 0ull : 1ull);
     }
     const float4 *L = reinterpret_cast<const float4 *>(lut_all + (uint64_t)qi * W * CARD);
     uint32_t *o = reinterpret_cast<uint32_t *>(lut8 + (uint64_t)i * W * CARD);
@@ -499,6 +505,40 @@ __global__ void __launch_bounds__(256) scanprep_kernel(const float *__restrict__
             word |= min(255u, mn[s1][a] + mn[s2][b]) << (8 * k);
         }
         oc[e] = word;
+    }
+}
+
+// R15, per query: after the node scan ran under the whole window threshold, a first-band slot whose
+// query kept more than `heavy` super-nodes (a costly scan: its window probably missed the near
+// neighbour) gets the first band after all: T = bsf^2 (1 + delta) * -band.hi, with its u8 table
+// and constants rewritten for it. Its entries stay (super-nodes kept under the larger threshold: a
+// superset, tested again at the leaf level). The other first-band slots keep the whole threshold
+// and are done in this round. One CTA per slot.
+__global__ void __launch_bounds__(256) fbdecide_kernel(const float *__restrict__ lut_all, const uint32_t *__restrict__ qmap,
+                                                       const Band *__restrict__ band, const unsigned long long *__restrict__ bsf,
+                                                       float onepd, const uint32_t *__restrict__ qkept, uint32_t heavy,
+                                                       uint8_t *__restrict__ lut8, uint4 *__restrict__ qconst,
+                                                       float *__restrict__ qscale, float *__restrict__ qT,
+                                                       unsigned long long *__restrict__ bsf_scan) {
+    const uint32_t i = blockIdx.x, qi = qmap[i];
+    const Band b = band[i];
+    if (!(b.hi < 0.f) || qkept[i] <= heavy) return;  // (uniform per CTA)
+    const float T = bsf_d2(bsf[qi]) * onepd * -b.hi;
+    const bool none = !(T >= 0.f);
+    const float sc = none ? 0.f : __fdiv_rd(254.0f, T);
+    if (threadIdx.x == 0) {
+        uint4 k = qconst[2 * i];
+        k.y = __float_as_uint(T);
+        qconst[2 * i] = k;
+        qscale[qi] = sc;
+        qT[qi] = T;
+        bsf_scan[qi] |= 1ull;
+    }
+    const float4 *L = reinterpret_cast<const float4 *>(lut_all + (uint64_t)qi * W * CARD);
+    uint32_t *o = reinterpret_cast<uint32_t *>(lut8 + (uint64_t)i * W * CARD);
+    for (uint32_t e = threadIdx.x; e < W * CARD / 4; e += blockDim.x) {
+        const float4 v = __ldg(L + e);
+        o[e] = none ? 0xFFFFFFFFu : (q8(v.x, sc) | q8(v.y, sc) << 8 | q8(v.z, sc) << 16 | q8(v.w, sc) << 24);
     }
 }
 
@@ -936,7 +976,7 @@ __global__ void __launch_bounds__(NS_THREADS) nodescan_kernel(
     const uint8_t *__restrict__ smeta, const uint8_t *__restrict__ hmeta, uint32_t nsuper, uint32_t nhyper,
     const uint8_t *__restrict__ lut8_all, const uint8_t *__restrict__ qsax_all, const uint32_t *__restrict__ qmap, uint32_t nq,
     uint32_t hyper_per_cta, uint2 *__restrict__ entries, uint32_t *__restrict__ ctl,
-    unsigned long long *__restrict__ scan_bytes_dev) {
+    unsigned long long *__restrict__ scan_bytes_dev, uint32_t *__restrict__ qkept, bool count_only) {
     extern __shared__ __align__(16) uint8_t smem_dyn[];
     const uint32_t raw8 = (uint32_t)__cvta_generic_to_shared(smem_dyn);
     const uint32_t lut8_sh = (raw8 + 255u) & ~255u;
@@ -979,7 +1019,12 @@ __global__ void __launch_bounds__(NS_THREADS) nodescan_kernel(
             const bool ok = ins && node_e8(lut8_sh + g * W * CARD, qsym[g][0], qsym[g][1], a, b) <= 254u;
             nnode += ins ? 1u : 0u;
             m |= (ok ? 1u : 0u) << g;
+            if (qkept) {  // (uniform) the slot's kept super-nodes, for fbdecide_kernel
+                const uint32_t balg = __ballot_sync(FULL, ok);
+                if (lane == 0 && balg && g0 + g < nq) atomicAdd(&qkept[g0 + g], (uint32_t)__popc(balg));
+            }
         }
+        if (count_only) continue;  // (uniform: the counting pass of R15's per-query choice writes no entries)
         const bool heavy = HEAVY == 0 ? m != 0 : (uint32_t)__popc(m) >= HEAVY;
         const uint32_t balh = __ballot_sync(FULL, heavy), ball = __ballot_sync(FULL, m != 0 && !heavy);
         if (balh | ball) {
@@ -1295,7 +1340,8 @@ __global__ void __launch_bounds__(LF_THREADS, LF_CTAS) itemscan_kernel(
 #endif
 
 template <int G>
-static void launch_leaf(const isax_index *ix, uint32_t nq, const uint32_t *qmap, cudaStream_t s) {
+static void launch_leaf(const isax_index *ix, uint32_t nq, const uint32_t *qmap, const Band *band, float onepd, bool select,
+                        cudaStream_t s) {
     constexpr uint32_t NW = LF_THREADS / 32;
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
@@ -1327,8 +1373,23 @@ static void launch_leaf(const isax_index *ix, uint32_t nq, const uint32_t *qmap,
     cudaFuncSetAttribute(nodescan_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_n);
     const uint32_t want = std::max(1u, (uint32_t)sms * 3u / groups);
     const uint32_t hpc = std::max(8u, (nhyper + want - 1) / want);
+    // R15 per query: a counting pass of the node scan under the whole window threshold, then only the
+    // queries that kept many super-nodes get the first band (fbdecide_kernel), then the node scan proper
+    if (select) {
+        nodescan_kernel<G><<<dim3((nhyper + hpc - 1) / hpc, groups), NS_THREADS, smem_n, s>>>(
+            ix->smeta, ix->hmeta, nsuper, nhyper, qs.lut8, qs.qsax, qmap, nq, hpc, qs.scan_entries, qs.scan_ctl, qs.scan_bytes_dev,
+            qs.qkept, true);
+// (a query is costly when it keeps more than 1/16 of the super-nodes: config 5 1.03M q/s with 1/256,
+// 1.06M with 1/64, 1.08M with 1/16, 1.03M with 1/4)
+#ifndef ISAX_FB_HEAVY_DIV
+#define ISAX_FB_HEAVY_DIV 16
+#endif
+        fbdecide_kernel<<<nq, 256, 0, s>>>(qs.lut, qmap, band, qs.bsf, onepd, qs.qkept, std::max(32u, nsuper / ISAX_FB_HEAVY_DIV), qs.lut8,
+                                           qs.qconst, qs.qscale, qs.qT, qs.bsf_scan);
+    }
     nodescan_kernel<G><<<dim3((nhyper + hpc - 1) / hpc, groups), NS_THREADS, smem_n, s>>>(
-        ix->smeta, ix->hmeta, nsuper, nhyper, qs.lut8, qs.qsax, qmap, nq, hpc, qs.scan_entries, qs.scan_ctl, qs.scan_bytes_dev);
+        ix->smeta, ix->hmeta, nsuper, nhyper, qs.lut8, qs.qsax, qmap, nq, hpc, qs.scan_entries, qs.scan_ctl, qs.scan_bytes_dev,
+        nullptr, false);
     // item scan: persistent CTAs, no more than the entries can occupy
     const size_t smem = (size_t)G * W * CARD + 256 + ((NW * WSC + 15u) & ~15u) + (size_t)NW * WB * sizeof(uint2) +
                         (size_t)NW * 1024;
@@ -1343,13 +1404,15 @@ static void launch_leaf(const isax_index *ix, uint32_t nq, const uint32_t *qmap,
 }
 
 uint64_t launch_lbscan(const isax_index *ix, uint32_t nq, uint32_t B, const uint32_t *qmap, const Band *band,
-                       float delta, cudaStream_t s) {
+                       float delta, bool select_first_band, cudaStream_t s) {
     if (!nq) return 0;
     const float onepd = 1.0f + delta;
     const QueryScratch &qs = ix->qs;
+    // (the per-query choice needs the node scan's counts: the default scan only)
+    const bool select = select_first_band && !(ix->opts.flags & ISAX_FLAG_FLAT_SCAN) && !ISAX_SCAN_V1;
     scanprep_kernel<<<nq, 256, 0, s>>>(qs.lut, qmap, band, qs.bsf, qs.win, onepd, qs.lut8, qs.lut8c, qs.qconst, qs.qscale, qs.qT, qs.bsf_scan,
                                       B, qs.cand_cnt, qs.cand_cnt2, qs.cnt_hi, qs.cnt_f, qs.cand_hist, qs.task_ctr, qs.scan_ctl,
-                                      4u * qs.scan_groups);
+                                      4u * qs.scan_groups, qs.qkept, select);
     if (ix->opts.flags & ISAX_FLAG_FLAT_SCAN) {  // ParIS flat scan, kept for A/B measurement
         const uint32_t G = nq >= 4 ? 4 : nq;
         if (G == 4) launch_g<4>(ix, nq, qmap, band, onepd, s);
@@ -1362,11 +1425,11 @@ uint64_t launch_lbscan(const isax_index *ix, uint32_t nq, uint32_t B, const uint
 #define ISAX_GMAX 16  // queries per scan group (their u8 tables share a CTA's shared memory)
 #endif
     const uint32_t G = nq >= 16 && ISAX_GMAX >= 16 ? 16 : nq >= 8 && ISAX_GMAX >= 8 ? 8 : nq >= 4 ? 4 : nq >= 2 ? 2 : 1;
-    if (G == 16) launch_leaf<16>(ix, nq, qmap, s);
-    else if (G == 8) launch_leaf<8>(ix, nq, qmap, s);
-    else if (G == 4) launch_leaf<4>(ix, nq, qmap, s);
-    else if (G == 2) launch_leaf<2>(ix, nq, qmap, s);
-    else launch_leaf<1>(ix, nq, qmap, s);
+    if (G == 16) launch_leaf<16>(ix, nq, qmap, band, onepd, select, s);
+    else if (G == 8) launch_leaf<8>(ix, nq, qmap, band, onepd, select, s);
+    else if (G == 4) launch_leaf<4>(ix, nq, qmap, band, onepd, select, s);
+    else if (G == 2) launch_leaf<2>(ix, nq, qmap, band, onepd, select, s);
+    else launch_leaf<1>(ix, nq, qmap, band, onepd, select, s);
     return 0;  // the leaf scan counts the node summaries and words it reads on the device
 }
 
