@@ -923,7 +923,7 @@ constexpr uint32_t CELL = KD_CELL;
 constexpr uint32_t CPL = LEAF / CELL;        // cells per leaf
 constexpr uint32_t CPS = SUPER_SIZE / CELL;  // cells per super-node
 static_assert(CPL == 4 && CPS == 128, "A3 maps four cells of a leaf to four lanes; a cell index is 7 bits");
-constexpr uint32_t CLIST = CPS + 8;          // bytes of an alive-cell list: a cell index each, 4 padding entries
+constexpr uint32_t CLIST = CPS + 8;          // bytes of an alive-cell list: a cell index each, 8 padding entries
 constexpr uint32_t IQ = 32;                  // item ring slots per warp (a power of two; an entry adds at most 16)
 constexpr uint32_t WSC = 32 + 2 * CLIST + IQ * 8;  // per-warp scratch bytes: alive-leaf list, two alive-cell lists, item ring
 // scan control words in qs.scan_ctl (reset by scanprep_kernel): per group its entry count, its
@@ -1170,7 +1170,7 @@ __global__ void __launch_bounds__(LF_THREADS, LF_CTAS) itemscan_kernel(
             __syncwarp();
         };
         // A3 of the ring's next item: lane = cell (idx & 3) of the (idx >> 2)-th alive leaf, 32 cells
-        // per iteration; the alive cells go to the list at cl_sh (padded with four copies of its
+        // per iteration; the alive cells go to the list at cl_sh (padded with eight copies of its
         // first entry, so that B reads and stages one iteration ahead without a bounds test).
         // Returns (item, alive cells), alive cells = 0 when none.
         auto stage_a3 = [&](uint32_t cl_sh) -> uint2 {
@@ -1204,7 +1204,10 @@ __global__ void __launch_bounds__(LF_THREADS, LF_CTAS) itemscan_kernel(
             ncellt += ncell;
             __syncwarp();
             if (m) {
-                if (lane < 4) st_sh_u8a(cl_sh + m + lane, ld_sh_u8(cl_sh));
+                // (B stages the cells of iteration i + 4 for i up to 4 floor((m - 1) / 4): list indices
+                // up to m + 6, so seven copies are needed; a stale byte there would be a cell index
+                // outside the super-node, and for the last super-nodes outside the array)
+                if (lane < 8) st_sh_u8a(cl_sh + m + lane, ld_sh_u8(cl_sh));
                 nmembt += m;
             }
             return make_uint2(it.x, m);

@@ -21,6 +21,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--seconds", type=float, default=120.0)
     ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--only", type=int, default=0, help="draw every trial of the seed but run only this one (to reproduce)")
+    ap.add_argument("--opt", action="append", default=[], help="with --only: override an index option, key=value")
     a = ap.parse_args()
     import numpy as np
     import torch
@@ -31,7 +33,7 @@ def main():
 
     rnd = random.Random(a.seed)
     t0, trial = time.time(), 0
-    while time.time() - t0 < a.seconds:
+    while time.time() - t0 < a.seconds and (not a.only or trial < a.only):
         trial += 1
         n = rnd.choice([64, 128, 128, 256, 256, 256, 512])
         N = rnd.choice([rnd.randint(1, 40), rnd.randint(900, 1100), rnd.randint(2_000, 40_000), rnd.randint(40_000, 400_000)])
@@ -56,6 +58,12 @@ def main():
             opts["probe_L"] = rnd.choice([1, 32, 64, 256, 1024])
         if rnd.random() < 0.1:
             opts["flags"] = 1
+        if a.only and trial != a.only:
+            rnd.random()  # (the duplicate draw below)
+            continue
+        for o in a.opt:
+            k, v = o.split("=", 1)
+            opts[k] = float(v) if "." in v else int(v)
         wl = datagen.Workload(f"fuzz{trial}", N, n, Q, kind, 1000 + trial, 5000 + trial, Q - noisy, noisy, sigma)
         x = datagen.series(wl, 0, N)
         q, _ = datagen.queries(wl)
