@@ -626,7 +626,10 @@ static int nn1_device(isax_index *ix, const float *d_q, uint32_t Q, int64_t *d_i
                 }
                 pending[i] = act != PLAN_DONE;
             }
-            if (round > 100000) {
+            // a safety net, not a budget: a round refines at least a list's worth of a query's
+            // candidates, so N / cand_cap rounds per query can be legitimate (cand_cap 5 over 220K
+            // series took about 10^5); the net sits well above that
+            if (round > 100000ull + 8ull * ix->N / std::max<uint32_t>(qs.cand_cap, 1u)) {
                 result = set_error(ISAX_E_CUDA, "candidate rounds did not converge");
                 break;
             }
