@@ -484,6 +484,7 @@ static int nn1_device(isax_index *ix, const float *d_q, uint32_t Q, int64_t *d_i
         if (timed) {
             ix->st_fb_frac = band0;
             ix->st_fb_improved = 0;
+            ix->st_fb_banded = 0;
         }
         cudaEventRecord(ix->ev[0], s);
         launch_qprep(ix, d_q + (uint64_t)b0 * ix->n, B, band0, s, qs.flag);
@@ -582,10 +583,14 @@ static int nn1_device(isax_index *ix, const float *d_q, uint32_t Q, int64_t *d_i
                         }
                     }
                 }
-                if (band0 > 0.f && timed) {  // stats: queries whose BSF the first band at least halved
-                    uint32_t improved = 0;
-                    for (uint32_t i = 0; i < B; i++) improved += bsf_d2_host(hm.bsf[i]) < 0.5f * bsf0_h[i];
+                if (band0 > 0.f && timed) {  // stats: queries whose BSF the first band at least halved; queries that got it
+                    uint32_t improved = 0, banded = 0;
+                    for (uint32_t i = 0; i < B; i++) {
+                        improved += bsf_d2_host(hm.bsf[i]) < 0.5f * bsf0_h[i];
+                        banded += std::isfinite(band[i].hi) ? 1u : 0u;
+                    }
                     ix->st_fb_improved = improved;
+                    ix->st_fb_banded = banded;
                 }
                 if (b0 == 0) {
                     ix->st_scan_bytes_first = ix->st_scan_bytes + *hm.scan_bytes_dev;
@@ -1094,8 +1099,9 @@ int isax_stats(const isax_index *cix, char *buf, size_t cap) {
     }
     j += "],";
     {
-        char b[96];
-        snprintf(b, sizeof b, "\"first_band\":%.6g,\"first_band_improved\":%u,", ix->st_fb_frac, ix->st_fb_improved);
+        char b[160];
+        snprintf(b, sizeof b, "\"first_band\":%.6g,\"first_band_improved\":%u,\"first_band_queries\":%u,", ix->st_fb_frac,
+                 ix->st_fb_improved, ix->st_fb_banded);
         j += b;
     }
     j += "\"launches\":" + std::to_string(ix->st_launches);

@@ -239,6 +239,7 @@ struct isax_index {
     uint32_t fb_every = 32;      // re-time the other mode after this many batches (doubles while the choice holds)
     float st_fb_frac = 0.f;      // first-band fraction of the last call's first batch (0 = none)
     uint32_t st_fb_improved = 0; // its queries whose BSF the first band at least halved (stats)
+    uint32_t st_fb_banded = 0;   // its queries that got the first band (R15 per query)
     uint64_t st_scan_bytes = 0, st_scan_bytes_first = 0;  // summary bytes the scan read (all / first launch)
     uint64_t st_refine_bytes_first = 0;                    // row bytes the first round's refine read (both passes)
     uint64_t st_refine1_bytes_first = 0, st_refine2_bytes_first = 0;  // ... per pass
