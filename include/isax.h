@@ -51,8 +51,7 @@ typedef struct isax_opts {
                             12 B each; halved while it does not fit) split over the queries of each batch, at most
                             min(N, 2^23) per query. Overflow runs more rounds (R10): about 5 x candidates /
                             cand_cap of them, each a rescan, so a capacity far below a query's candidate
-                            count is slow (and below about 10 over large collections it may hit the
-                            round limit, ISAX_E_CUDA "did not converge"). */
+                            count is slow (5 over 220K series: about 120K rounds). */
     uint32_t flags;      /* ISAX_FLAG_* bits; 0 = defaults */
     uint32_t probe_bits; /* multi-probe approximate answer (R5): refine extra windows at the 2^probe_bits - 1 keys
                             obtained by flipping the most fragile plane-0/1 key bits; a probe window inside the main

@@ -40,6 +40,7 @@ def build_one(name: str, force: bool = False, verbose: bool = False) -> str:
     src_dir, out = TARGETS[name]
     srcs = sorted(glob.glob(os.path.join(src_dir, "*.cu")))
     deps = srcs + glob.glob(os.path.join(src_dir, "*.cuh")) + glob.glob(os.path.join(src_dir, "*.inc"))
+    deps += glob.glob(os.path.join(src_dir, "*.h"))
     deps += glob.glob(os.path.join(ROOT, "include", "*.h"))
     if not force and not _stale(out, deps):
         return out

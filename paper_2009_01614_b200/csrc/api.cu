@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <string>
@@ -513,6 +514,7 @@ static int nn1_device(isax_index *ix, const float *d_q, uint32_t Q, int64_t *d_i
         std::vector<float> bsf_h(B, INF), tused(B, -1.0f), bsf0_h(B, INF);
         std::vector<uint32_t> rewin;
         bool offs_dirty = false;
+        static const uint32_t dbg_rounds = getenv("ISAX_DEBUG_ROUNDS") ? (uint32_t)atoi(getenv("ISAX_DEBUG_ROUNDS")) : 0u;
         for (uint32_t round = 0;; round++) {
             NvtxRange nvtx_round(round == 0 ? "isax_nn1: round 0 (scan, candcheck, refine)" : "isax_nn1: overflow or band round");
             uint32_t nact = 0;
@@ -620,6 +622,10 @@ static int nn1_device(isax_index *ix, const float *d_q, uint32_t Q, int64_t *d_i
                 const bool near_ovf = hm.near_cnt[i] > hm.near_cap[i];
                 const int act = plan_next_round(st, cnt, qs.cand_cap, hm.hist + (size_t)i * HIST_BINS, near_ovf, tused[i],
                                                 bsf_h[i] * onepd, NP);
+                if (dbg_rounds && round % dbg_rounds == 0 && k == 0)  // ISAX_DEBUG_ROUNDS=<every>: the plan's progress
+                    fprintf(stderr, "[isax] round %u: %u active; query %u: band (%.9g, %.9g] pos [%u, %u) cnt %u cap %u tused %.9g bsf %.9g -> act %d band (%.9g, %.9g] pos [%u, %u)\n",
+                            round, nact, i, band[i].lo, band[i].hi, band[i].plo, band[i].phi, cnt, qs.cand_cap, tused[i], bsf_h[i], act,
+                            st.band.lo, st.band.hi, st.band.plo, st.band.phi);
                 band[i] = st.band;
                 plen[i] = st.plen;
                 nfirst[i] = st.nfirst;
@@ -633,7 +639,7 @@ static int nn1_device(isax_index *ix, const float *d_q, uint32_t Q, int64_t *d_i
             }
             // a safety net, not a budget: a round refines at least a list's worth of a query's
             // candidates, so N / cand_cap rounds per query can be legitimate (cand_cap 5 over 220K
-            // series took about 10^5); the net sits well above that
+            // series: 119,781); the net sits well above that
             if (round > 100000ull + 8ull * ix->N / std::max<uint32_t>(qs.cand_cap, 1u)) {
                 result = set_error(ISAX_E_CUDA, "candidate rounds did not converge");
                 break;

@@ -6,7 +6,7 @@
 //  - candidate-list overflow: the band shrinks to the largest prefix of its 64-bin LB histogram
 //    that fits 9/10 of the capacity; when the histogram cannot split it (the first bin alone
 //    overflows three times in a row, the band is narrower than 2^-16 of its bounds, or the shrunk
-//    edge rounds onto the lower one) the positions are halved instead, and a completed position
+//    edge rounds onto either end of the band) the positions are halved instead, and a completed position
 //    range is followed by the next one, twice as long;
 //  - otherwise the band is done; if it was capped below the BSF, the next band (hi, +inf) follows.
 #pragma once
@@ -50,8 +50,10 @@ inline int plan_next_round(RoundState &st, uint32_t cnt, uint32_t cap, const uin
         }
         const float hi_new = kk < 0 ? lo0 + span / (float)HIST_BINS : lo0 + span * (float)(kk + 1) / (float)HIST_BINS;
         st.nfirst = kk < 0 ? st.nfirst + 1 : 0;
+        // (the shrunk edge must lie strictly inside (lo0, tused): in a band a few ulps wide it can
+        // round onto either end, and an edge equal to tused would repeat the same round for ever)
         const bool stuck = (kk < 0 && (st.nfirst >= 3 || !(span > std::fmax(lo0, tused) * 1.52587890625e-05f))) ||
-                           !(hi_new > lo0);
+                           !(hi_new > lo0) || !(hi_new < tused);
         if (stuck || bd.phi - bd.plo < NP) {
             const uint32_t len = bd.phi - bd.plo;
             if (len <= 1) return PLAN_ERROR;

@@ -96,3 +96,18 @@ def test_near_overflow_starts_over():
     act = isax.plan_round(band, rng, state, 3, 10, np.zeros(64, np.uint32), True, 2.0, 2.5, 1000)
     assert act == isax.PLAN_RESCAN
     assert band[0] == -1.0 and np.isinf(band[1]) and rng.tolist() == [0, 1000]
+
+
+def test_band_a_few_ulps_wide_makes_progress():
+    """Six candidates at the top of a band about 30 fp32 ulps wide against a capacity of 5: the
+    histogram's shrunk edge (63/64 of the span) rounds back onto the band's upper end, so the plan
+    must split positions instead of repeating the round (found on the GPU by tools/fuzz_gpu.py:
+    cand_cap 5 over 220K sines)."""
+    lo = np.float32(182.600998)
+    ulp = np.spacing(lo)
+    top = np.float32(lo + 30 * ulp)
+    lb = np.concatenate([np.full(6, top, np.float32), np.float32(lo) - np.arange(1, 40, dtype=np.float32)])
+    pos = np.arange(len(lb)) * 97 + 11
+    N = 10_000
+    refined, rounds = run_plan(lb, pos, N, cap=5, T=np.float32(top), max_rounds=5000)
+    assert np.all(refined == 1) and rounds < 5000
