@@ -49,7 +49,7 @@ def main():
         if rnd.random() < 0.3:
             # (a capacity of 5 or 64 takes about 5 x candidates / capacity rounds, each a rescan: only
             # over small collections here, to keep a run short; 5 over 220K sines is 120K rounds)
-            opts["cand_cap"] = rnd.choice([5, 64, 1000, 50_000]) if N <= 50_000 else rnd.choice([1000, 50_000])
+            opts["cand_cap"] = rnd.choice([5, 7, 64, 1000, 50_000]) if N <= 50_000 else rnd.choice([300, 1000, 50_000])
         if rnd.random() < 0.4:
             opts["first_band"] = rnd.choice([-1.0, 0.02, 0.3, 0.9])
         if rnd.random() < 0.3:
