@@ -37,8 +37,10 @@ def main():
         trial += 1
         n = rnd.choice([64, 128, 128, 256, 256, 256, 512])
         N = rnd.choice([rnd.randint(1, 40), rnd.randint(900, 1100), rnd.randint(2_000, 40_000), rnd.randint(40_000, 400_000)])
-        if N * n > 60_000_000:
-            N = 60_000_000 // n
+        if rnd.random() < 0.06:  # now and then several hyper-nodes and many super-nodes
+            N = rnd.randint(400_000, 3_000_000)
+        if N * n > 400_000_000:
+            N = 400_000_000 // n
         kind = rnd.choice(["walk", "walk", "sines"])
         Q = rnd.choice([1, 2, 3, 5, 8, 15, 16, 17, 31, 33, 64, 100, 257])
         noisy = rnd.choice([0, 0, Q // 2, Q])
