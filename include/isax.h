@@ -15,6 +15,8 @@
  *    untouched and isax_last_error() returns a thread-local message.
  *  - One index may be used by one host thread at a time; calls on the same index are
  *    serialised by an internal mutex. Separate indices are independent.
+ *  - Environment: ISAX_DEBUG_ROUNDS=<k> prints the round plan's state (band, positions, counts) of every
+ *    k-th round of a batch to stderr (diagnosis of slow overflow rounds; read once per process).
  *  - v1 supports w = 16, card = 256, n a multiple of 64 in [64, 1024], N < 2^32 - 1.
  *    Other valid arguments return ISAX_E_UNSUPPORTED.
  */
