@@ -76,7 +76,17 @@ def main():
             q = q.clone()
             x[N // 2] = x[3]
             q[0] = x[N // 2]
-        ids_or, dist_or, _ = oracle_nn1(x.cpu().numpy(), q.cpu().numpy())
+            if N > 2000 and rnd.random() < 0.5:  # many exact ties: copies of one row, constant rows, a constant query
+                g = torch.Generator().manual_seed(trial)
+                k = rnd.choice([5, 40, 300, 700])
+                idx = torch.randperm(N, generator=g)[:k].to(x.device)
+                x[idx] = x[7].clone()
+                cidx = torch.randperm(N, generator=g)[:rnd.choice([3, 60, 400])].to(x.device)
+                x[cidx] = 2.5
+                q[Q - 1] = x[7].clone()
+                if Q > 2:
+                    q[1] = -4.0
+        ids_or, dist_or, _ = oracle_nn1(x.cpu().numpy(), q.cpu().numpy(), K=1200)  # (room for the tie trials' copies)
         desc = f"trial {trial}: N={N} n={n} {kind} Q={Q} noisy={noisy} sigma={sigma} opts={opts}"
         try:
             with isax.Index.build(x, **opts) as ix:
